@@ -1,0 +1,179 @@
+/*
+ * vm_api.h — C ABI of libvoxmesh_sm100.so, the B200 (sm_100a) hot path of the
+ * spatially-partitioned 3D U-Net train step (arXiv 1909.03108; reference package
+ * `voxmesh` 0.1.0 under /root/reference/pkg/src/voxmesh).
+ *
+ * Conventions:
+ *  - plain pointers + explicit sizes, no torch types; the caller (PyTorch) owns
+ *    every device buffer; the library never allocates device memory;
+ *  - every call is asynchronous on the given stream (cudaStream_t passed as
+ *    void*), never host-synchronises, and returns 0 on success, a negative
+ *    VM_E* code on a bad argument (nothing launched), or a positive CUDA error
+ *    code if a launch failed; vm_last_error() gives a human-readable message;
+ *  - dtypes: VM_F32, VM_BF16, VM_F64, VM_U8 (the reference supports f32/f64/u8,
+ *    sharding.py:21; bf16 is the B200 storage type of the hot path).
+ *
+ * Two tensor formats cross this boundary:
+ *  - dense   : row-major [d0][d1][d2][d3][d4] with d4 fastest — the reference's
+ *              [batch, x, y, z, c] block layout (sharding.py:1-11);
+ *  - slab    : the device activation format, "channel-blocked padded":
+ *              [B][CG][D+2m][H+2m][W+2m][8] with CG = ceil(C/8), channels >= C
+ *              zero; `bstride` = elements between consecutive samples (lets a
+ *              channel-group sub-range of a wider slab — the concat skip half —
+ *              be addressed as a slab of its own).
+ */
+#ifndef VM_API_H
+#define VM_API_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum vm_dtype { VM_F32 = 0, VM_BF16 = 1, VM_F64 = 2, VM_U8 = 3 };
+
+enum vm_status {
+  VM_OK = 0,
+  VM_E_ARG = -1,      /* null pointer / bad size                       */
+  VM_E_DTYPE = -2,    /* dtype not supported by this entry point       */
+  VM_E_SHAPE = -3,    /* inconsistent shapes                           */
+  VM_E_ALIGN = -4,    /* pointer or stride misaligned                  */
+  VM_E_HALO = -5,     /* margin exceeds local extent (halo.py:121-126) */
+  VM_E_UNSUPPORTED = -6
+};
+
+/* Conv epilogue flags */
+#define VM_CONV_RELU 1u      /* y = max(acc + bias, 0)                     (unet.py:351-354 fused) */
+#define VM_CONV_MASK 2u      /* y = acc * (mask > 0)   (relu_backward_local, ops.py:186-187 fused) */
+#define VM_CONV_NOBIAS 4u    /* skip the bias add (dgrad)                                          */
+
+int vm_version(void);
+const char* vm_error_string(int code);
+const char* vm_last_error(void);
+int vm_num_sms(int device);
+
+/* ------------------------------------------------------------------ boxes / halo
+ * Generic 5-D box copies on a dense tensor of shape dims[5] (dims[4] contiguous,
+ * `elem_bytes` per element).  These are the pack / unpack kernels of the halo
+ * exchange: `vm_box_pack` replaces np.ascontiguousarray(_slab(...)) of
+ * halo.py:131-134 and :176-179; `vm_box_unpack` the np.concatenate of
+ * halo.py:148; `vm_box_unpack_add` the `view += recv(...)` of halo.py:181-186;
+ * `vm_box_zero` the zero fill at the global boundary (halo.py:139-147).
+ * A slab is the dense tensor [B*CG][D+2m][H+2m][W+2m][8] (elem = dtype) or,
+ * with a batch stride, [B][CG*...] — pass dims of the 5-D view you need. */
+int vm_box_pack(const void* src, const int64_t dims[5], int elem_bytes, const int64_t lo[5],
+                const int64_t ext[5], void* buf, void* stream);
+int vm_box_unpack(void* dst, const int64_t dims[5], int elem_bytes, const int64_t lo[5],
+                  const int64_t ext[5], const void* buf, void* stream);
+int vm_box_unpack_add(void* dst, const int64_t dims[5], int dtype, const int64_t lo[5],
+                      const int64_t ext[5], const void* buf, void* stream);
+int vm_box_zero(void* dst, const int64_t dims[5], int elem_bytes, const int64_t lo[5],
+                const int64_t ext[5], void* stream);
+
+/* ------------------------------------------------------------------ layout
+ * dense [B][D][H][W][C] (src_dtype) <-> slab interior (slab_dtype), with dtype
+ * conversion (f32 -> bf16 is round-to-nearest-even).  Replaces the driver-side
+ * shard copy (sharding.py:189-201) once the block is on its device. */
+int vm_dense_to_slab(const void* src, int src_dtype, void* slab, int slab_dtype, int64_t bstride,
+                     int B, int C, int D, int H, int W, int m, void* stream);
+int vm_slab_to_dense(const void* slab, int slab_dtype, int64_t bstride, void* dst, int dst_dtype,
+                     int B, int C, int D, int H, int W, int m, void* stream);
+/* labels u8 [B][D][H][W] -> one-hot f32 [B][D][H][W][ncls] (training.py:68-69) */
+int vm_onehot_u8(const uint8_t* labels, float* onehot, int64_t nvox, int ncls, void* stream);
+
+/* ------------------------------------------------------------------ conv3d
+ * Weights: master fp32 in the reference layout [k][k][k][Cin][Cout]
+ * (ops.py:33-34).  The tensor-core path consumes packed bf16 operands produced by
+ * vm_pack_weights (forward) / vm_pack_weights_dgrad (flipped + transposed). */
+
+/* SIMT path (fp32 or bf16 storage, fp32 accumulation) — the fp32 parity path
+ * (cfg1) and the on-device cross-check of the tensor-core kernels.
+ * y_interior = epilogue(bias + sum_taps x_shift @ W)   (conv3d_local, ops.py:69-97) */
+int vm_conv3d_fwd_simt(int dtype, const void* x, int64_t x_bstride, const float* w,
+                       const float* bias, void* y, int64_t y_bstride, const void* mask,
+                       int64_t mask_bstride, int B, int Cin, int Cout, int D, int H, int W,
+                       unsigned flags, void* stream);
+/* per-tap weight gradient partials (conv3d_param_grads_local, ops.py:117-138):
+ * gw[t][ci][co] (+)= sum_v x[v+off_t][ci] * gy[v][co];  gb[co] (+)= sum_v gy[v][co].
+ * Deterministic: ws must hold vm_conv3d_wgrad_simt_ws() bytes. */
+size_t vm_conv3d_wgrad_simt_ws(int B, int Cin, int Cout, int D, int H, int W);
+int vm_conv3d_wgrad_simt(int dtype, const void* x, int64_t x_bstride, const void* gy,
+                         int64_t gy_bstride, float* gw, float* gb, void* ws, int B, int Cin,
+                         int Cout, int D, int H, int W, void* stream);
+
+/* fp32 weight transforms */
+int vm_weight_flip_transpose(const float* w, float* wt, int k, int Cin, int Cout, void* stream);
+
+/* ------------------------------------------------------------------ tcgen05 conv3d
+ * Implicit GEMM on 5th-gen tensor cores: M = 128 flat padded anchors, N = Cout,
+ * K = 27 taps x Cin; A = TMA-staged input rows addressed with row-shifted
+ * SWIZZLE_NONE descriptors, B = packed bf16 weights, fp32 accumulator in TMEM,
+ * fused bias / ReLU / relu-mask epilogue into the output slab interior. */
+size_t vm_packed_weights_bytes(int Cin, int Cout);
+int vm_pack_weights(const float* w, void* packed, int Cin, int Cout, int flip_transpose,
+                    void* stream);
+int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wpacked, const float* bias,
+                     void* y, int64_t y_bstride, const void* mask, int64_t mask_bstride, int B,
+                     int Cin, int Cout, int D, int H, int W, unsigned flags, void* stream);
+size_t vm_conv3d_wgrad_tc_ws(int B, int Cin, int Cout, int D, int H, int W);
+int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* gy, int64_t gy_bstride,
+                       float* gw, float* gb, void* ws, int B, int Cin, int Cout, int D, int H,
+                       int W, void* stream);
+
+/* ------------------------------------------------------------------ HBM-bound ops (slabs)
+ * maxpool 2^3, first-in-scan-order ties (ops.py:141-156); out = pooled slab. */
+int vm_maxpool2_fwd(int dtype, const void* x, int64_t x_bstride, void* y, int64_t y_bstride, int B,
+                    int C, int D, int H, int W, void* stream);
+/* g_in = route(g_out to argmax recomputed from x) [+ add] [* (x > 0)]   (ops.py:159-168) */
+int vm_maxpool2_bwd(int dtype, const void* x, int64_t x_bstride, const void* gout,
+                    int64_t gout_bstride, const void* add, int64_t add_bstride, void* gin,
+                    int64_t gin_bstride, int B, int C, int D, int H, int W, int relu_mask,
+                    void* stream);
+/* nearest x2 (ops.py:171-173): y (2D,2H,2W) from x (D,H,W) */
+int vm_upsample2_fwd(int dtype, const void* x, int64_t x_bstride, void* y, int64_t y_bstride, int B,
+                     int C, int D, int H, int W, void* stream);
+/* g_x = sum over each 2^3 cell of g_y [* (mask > 0)]   (ops.py:176-179) */
+int vm_upsample2_bwd(int dtype, const void* gy, int64_t gy_bstride, const void* mask,
+                     int64_t mask_bstride, void* gx, int64_t gx_bstride, int B, int C, int D, int H,
+                     int W, void* stream);
+/* y = x * (mask > 0) on slab interiors (relu_backward_local, ops.py:186-187) */
+int vm_relu_mask(int dtype, const void* g, int64_t g_bstride, const void* mask,
+                 int64_t mask_bstride, void* out, int64_t out_bstride, int B, int C, int D, int H,
+                 int W, void* stream);
+
+/* ------------------------------------------------------------------ head + loss
+ * 1x1x1 head conv (unet.py:223) + channel softmax (ops.py:190-194) + per-block
+ * loss-statistics partials (training.py:77-92): stats[3*ncls+1] over the
+ * block's voxels.  probs (optional, may be NULL) is dense f32 [B][D][H][W][ncls].
+ * partials must hold vm_head_partials_count(...) * (3*ncls+1) floats. */
+int vm_head_partials_count(int B, int D, int H, int W);
+int vm_head_fwd(int dtype, const void* y, int64_t y_bstride, const float* w, const float* b,
+                const float* onehot, float* probs, float* partials, int B, int C, int ncls, int D,
+                int H, int W, float clamp, void* stream);
+/* deterministic fixed-order sum of `rows` partial vectors of length `width` */
+int vm_reduce_rows(const float* partials, int rows, int width, float* out, void* stream);
+/* loss gradient from reduced stats (training.py:110-127) -> softmax backward
+ * (ops.py:197-199) -> head input grad (masked by y>0) into slab g, plus
+ * head-weight-grad partials [rows][C*ncls + ncls]. */
+int vm_head_bwd(int dtype, const void* y, int64_t y_bstride, const float* w, const float* b,
+                const float* onehot, const float* stats, void* g, int64_t g_bstride,
+                float* wpartials, int B, int C, int ncls, int D, int H, int W, float w_dice,
+                float w_ce, float total_voxels, int dice_mask, float clamp, int relu_mask,
+                void* stream);
+
+/* ------------------------------------------------------------------ optimizer
+ * Parameters, moments and gradients of all layers live in three flat fp32
+ * buffers; layer l owns [offsets[l], offsets[l+1]) (kernel then bias).
+ * v = mu*v + g; p -= lr*v per layer, skipping (flags[l] = 1) every layer whose
+ * gradient is not all finite (sgd_momentum_step, training.py:202-219).
+ * `offsets` (nlayers+1 int64) and `flags` (nlayers int32) are DEVICE arrays. */
+int vm_sgd_momentum(float* params, float* moments, const float* grads, const int64_t* offsets,
+                    int nlayers, int64_t max_layer_elems, int* flags, float lr, float momentum,
+                    void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VM_API_H */

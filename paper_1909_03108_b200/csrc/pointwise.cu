@@ -1,0 +1,537 @@
+// pointwise.cu — HBM-bound kernels of the step on channel-blocked slabs:
+// maxpool2 fwd/bwd, nearest upsample x2 fwd/bwd, relu mask, fused head
+// (1x1x1 conv + softmax + Dice/CE statistics and gradient), fixed-order
+// reductions, SGD with momentum.  One 16-byte channel-block vector per thread
+// access; grids are multiples of the SM count (grid-stride loops).
+#include <cfloat>
+
+#include "vm_common.cuh"
+
+namespace vm {
+
+template <typename T> struct V8;
+template <> struct V8<float> {
+  __device__ __forceinline__ static void ld(const float* p, float (&v)[8]) {
+    float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+  __device__ __forceinline__ static void st(float* p, const float (&v)[8]) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+  }
+};
+template <> struct V8<__nv_bfloat16> {
+  __device__ __forceinline__ static void ld(const __nv_bfloat16* p, float (&v)[8]) {
+    int4 raw = *reinterpret_cast<const int4*>(p);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float2 f = __bfloat1622float2(h[j]);
+      v[2 * j] = f.x;
+      v[2 * j + 1] = f.y;
+    }
+  }
+  __device__ __forceinline__ static void st(__nv_bfloat16* p, const float (&v)[8]) {
+    int4 raw;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+    *reinterpret_cast<int4*>(p) = raw;
+  }
+};
+
+__device__ __forceinline__ void decompose(int64_t v, int D, int H, int W, int& b, int& d, int& h,
+                                          int& w) {
+  w = v % W;
+  int64_t r = v / W;
+  h = r % H;
+  r /= H;
+  d = r % D;
+  b = (int)(r / D);
+}
+
+// ------------------------------------------------------------------ maxpool
+// out grid: pooled voxels (D,H,W are the POOLED extents) x channel blocks
+template <typename T>
+__global__ void k_maxpool_fwd(const T* __restrict__ x, Slab gx, T* __restrict__ y, Slab gy, int B) {
+  const int64_t nvox = (int64_t)B * gy.D * gy.H * gy.W;
+  const int64_t total = nvox * gy.CG;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int cg = (int)(i / nvox);
+    int b, d, h, w;
+    decompose(i % nvox, gy.D, gy.H, gy.W, b, d, h, w);
+    float best[8];
+    for (int cell = 0; cell < 8; ++cell) {  // (dz, dy, dx) scan order, ops.py:149-154
+      float v[8];
+      V8<T>::ld(x + gx.at(b, cg, 2 * d + (cell >> 2), 2 * h + ((cell >> 1) & 1), 2 * w + (cell & 1)), v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) best[j] = (cell == 0 || v[j] > best[j]) ? v[j] : best[j];
+    }
+    V8<T>::st(y + gy.at(b, cg, d, h, w), best);
+  }
+}
+
+// gin[cell] = (cell == argmax) ? gout : 0, first max wins (np.argmax), + add, * (x>0)
+template <typename T>
+__global__ void k_maxpool_bwd(const T* __restrict__ x, Slab gx, const T* __restrict__ gout, Slab go,
+                              const T* __restrict__ add, Slab ga, T* __restrict__ gin, Slab gi,
+                              int B, int relu_mask) {
+  const int64_t nvox = (int64_t)B * go.D * go.H * go.W;
+  const int64_t total = nvox * go.CG;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int cg = (int)(i / nvox);
+    int b, d, h, w;
+    decompose(i % nvox, go.D, go.H, go.W, b, d, h, w);
+    float xv[8][8];
+    int arg[8];
+    float best[8];
+#pragma unroll
+    for (int cell = 0; cell < 8; ++cell) {
+      V8<T>::ld(x + gx.at(b, cg, 2 * d + (cell >> 2), 2 * h + ((cell >> 1) & 1), 2 * w + (cell & 1)),
+                xv[cell]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (cell == 0 || xv[cell][j] > best[j]) {
+          best[j] = xv[cell][j];
+          arg[j] = cell;
+        }
+      }
+    }
+    float g[8];
+    V8<T>::ld(gout + go.at(b, cg, d, h, w), g);
+#pragma unroll
+    for (int cell = 0; cell < 8; ++cell) {
+      int pd = 2 * d + (cell >> 2), ph = 2 * h + ((cell >> 1) & 1), pw = 2 * w + (cell & 1);
+      float o[8];
+      if (add) V8<T>::ld(add + ga.at(b, cg, pd, ph, pw), o);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float r = (arg[j] == cell) ? g[j] : 0.f;
+        if (add) r += o[j];
+        if (relu_mask && !(xv[cell][j] > 0.f)) r = 0.f;
+        o[j] = r;
+      }
+      V8<T>::st(gin + gi.at(b, cg, pd, ph, pw), o);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ upsample
+template <typename T>
+__global__ void k_upsample_fwd(const T* __restrict__ x, Slab gx, T* __restrict__ y, Slab gy, int B) {
+  const int64_t nvox = (int64_t)B * gx.D * gx.H * gx.W;
+  const int64_t total = nvox * gx.CG * 8;  // one output vector per thread
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int cell = i % 8;
+    int64_t r = i / 8;
+    int cg = (int)(r / nvox);
+    int b, d, h, w;
+    decompose(r % nvox, gx.D, gx.H, gx.W, b, d, h, w);
+    int4 v = *reinterpret_cast<const int4*>(x + gx.at(b, cg, d, h, w));
+    if (sizeof(T) == 2) {
+      *reinterpret_cast<int4*>(y + gy.at(b, cg, 2 * d + (cell >> 2), 2 * h + ((cell >> 1) & 1), 2 * w + (cell & 1))) = v;
+    } else {
+      const T* src = x + gx.at(b, cg, d, h, w);
+      T* dst = y + gy.at(b, cg, 2 * d + (cell >> 2), 2 * h + ((cell >> 1) & 1), 2 * w + (cell & 1));
+      *reinterpret_cast<int4*>(dst) = *reinterpret_cast<const int4*>(src);
+      *reinterpret_cast<int4*>(dst + 4) = *reinterpret_cast<const int4*>(src + 4);
+    }
+  }
+}
+
+template <typename T>
+__global__ void k_upsample_bwd(const T* __restrict__ gy, Slab sgy, const T* __restrict__ mask,
+                               Slab sm, T* __restrict__ gx, Slab sgx, int B) {
+  const int64_t nvox = (int64_t)B * sgx.D * sgx.H * sgx.W;
+  const int64_t total = nvox * sgx.CG;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int cg = (int)(i / nvox);
+    int b, d, h, w;
+    decompose(i % nvox, sgx.D, sgx.H, sgx.W, b, d, h, w);
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int cell = 0; cell < 8; ++cell) {
+      float v[8];
+      V8<T>::ld(gy + sgy.at(b, cg, 2 * d + (cell >> 2), 2 * h + ((cell >> 1) & 1), 2 * w + (cell & 1)), v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += v[j];
+    }
+    if (mask) {
+      float mv[8];
+      V8<T>::ld(mask + sm.at(b, cg, d, h, w), mv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = mv[j] > 0.f ? acc[j] : 0.f;
+    }
+    V8<T>::st(gx + sgx.at(b, cg, d, h, w), acc);
+  }
+}
+
+template <typename T>
+__global__ void k_relu_mask(const T* __restrict__ g, Slab sg, const T* __restrict__ mask, Slab sm,
+                            T* __restrict__ out, Slab so, int B) {
+  const int64_t nvox = (int64_t)B * sg.D * sg.H * sg.W;
+  const int64_t total = nvox * sg.CG;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int cg = (int)(i / nvox);
+    int b, d, h, w;
+    decompose(i % nvox, sg.D, sg.H, sg.W, b, d, h, w);
+    float v[8], mv[8];
+    V8<T>::ld(g + sg.at(b, cg, d, h, w), v);
+    V8<T>::ld(mask + sm.at(b, cg, d, h, w), mv);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = mv[j] > 0.f ? v[j] : 0.f;
+    V8<T>::st(out + so.at(b, cg, d, h, w), v);
+  }
+}
+
+// ------------------------------------------------------------------ head + loss
+constexpr int kHeadThreads = 256;
+constexpr int kMaxCls = 8;
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = v;
+  __syncthreads();
+  float s = 0.f;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kHeadThreads / 32; ++i) s += red[i];
+  return s;  // valid in thread 0
+}
+
+template <typename T>
+__device__ __forceinline__ void head_logits(const T* __restrict__ y, Slab sy, int b, int d, int h,
+                                            int w, const float* sW, const float* sb, int C,
+                                            int ncls, float* logits) {
+  for (int k = 0; k < ncls; ++k) logits[k] = sb[k];
+  for (int cg = 0; cg < sy.CG; ++cg) {
+    float v[8];
+    V8<T>::ld(y + sy.at(b, cg, d, h, w), v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      int c = cg * 8 + j;
+      if (c < C)
+        for (int k = 0; k < ncls; ++k) logits[k] = fmaf(v[j], sW[c * ncls + k], logits[k]);
+    }
+  }
+}
+
+__device__ __forceinline__ void softmax_n(const float* logits, int ncls, float* p) {
+  float m = logits[0];
+  for (int k = 1; k < ncls; ++k) m = fmaxf(m, logits[k]);
+  float s = 0.f;
+  for (int k = 0; k < ncls; ++k) {
+    p[k] = expf(logits[k] - m);
+    s += p[k];
+  }
+  for (int k = 0; k < ncls; ++k) p[k] = p[k] / s;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kHeadThreads) k_head_fwd(const T* __restrict__ y, Slab sy,
+                                                           const float* __restrict__ W,
+                                                           const float* __restrict__ bias,
+                                                           const float* __restrict__ onehot,
+                                                           float* __restrict__ probs,
+                                                           float* __restrict__ partials, int B,
+                                                           int C, int ncls, float clamp) {
+  extern __shared__ float sh[];
+  float* sW = sh;
+  float* sb = sW + C * ncls;
+  float* red = sb + ncls;
+  for (int i = threadIdx.x; i < C * ncls; i += blockDim.x) sW[i] = W[i];
+  for (int i = threadIdx.x; i < ncls; i += blockDim.x) sb[i] = bias[i];
+  __syncthreads();
+  const int64_t nvox = (int64_t)B * sy.D * sy.H * sy.W;
+  float st[3 * kMaxCls + 1];
+  for (int k = 0; k < 3 * ncls + 1; ++k) st[k] = 0.f;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvox;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int b, d, h, w;
+    decompose(v, sy.D, sy.H, sy.W, b, d, h, w);
+    float lg[kMaxCls], p[kMaxCls];
+    head_logits(y, sy, b, d, h, w, sW, sb, C, ncls, lg);
+    softmax_n(lg, ncls, p);
+    for (int k = 0; k < ncls; ++k) {
+      float g = onehot[v * ncls + k];
+      if (probs) probs[v * ncls + k] = p[k];
+      st[k] += p[k] * g;
+      st[ncls + k] += p[k];
+      st[2 * ncls + k] += g;
+      st[3 * ncls] += -logf(fmaxf(p[k], clamp)) * g;
+    }
+  }
+  for (int k = 0; k < 3 * ncls + 1; ++k) {
+    float s = block_sum(st[k], red);
+    if (threadIdx.x == 0) partials[(int64_t)blockIdx.x * (3 * ncls + 1) + k] = s;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kHeadThreads) k_head_bwd(
+    const T* __restrict__ y, Slab sy, const float* __restrict__ W, const float* __restrict__ bias,
+    const float* __restrict__ onehot, const float* __restrict__ stats, T* __restrict__ g, Slab sg,
+    float* __restrict__ wpart, int B, int C, int ncls, float w_dice, float w_ce, float total,
+    int dice_mask, float clamp, int relu_mask) {
+  extern __shared__ float sh[];
+  float* sW = sh;
+  float* sb = sW + C * ncls;
+  float* red = sb + ncls;
+  float* coef = red + 32;  // per class: a_k (dice slope), r_k (dice ratio), active flag
+  for (int i = threadIdx.x; i < C * ncls; i += blockDim.x) sW[i] = W[i];
+  for (int i = threadIdx.x; i < ncls; i += blockDim.x) sb[i] = bias[i];
+  if (threadIdx.x == 0) {
+    int nfg = __popc(dice_mask);
+    for (int k = 0; k < ncls; ++k) {
+      // training.py:119-124 — grad_k += (-w_d/nfg) * (2 g_k - r_k) / d_k
+      float nk = 2.f * stats[k] + 1e-6f;
+      float dk = stats[ncls + k] + stats[2 * ncls + k] + 1e-6f;
+      bool on = (dice_mask >> k) & 1;
+      coef[3 * k + 0] = on ? (-w_dice / (float)nfg) / dk : 0.f;
+      coef[3 * k + 1] = on ? nk / dk : 0.f;
+      coef[3 * k + 2] = on ? 1.f : 0.f;
+    }
+  }
+  __syncthreads();
+  const int64_t nvox = (int64_t)B * sy.D * sy.H * sy.W;
+  const float ce_scale = -w_ce / total;
+  // per-thread weight-grad partials: sum_v y_c * gl_k (C*ncls) + sum_v gl_k (ncls)
+  // accumulated per channel block to bound registers; C*ncls <= 64*8 handled by loop
+  const int nw = C * ncls + ncls;
+  for (int base = 0; base < nw; base += 64) {
+    float acc[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) acc[i] = 0.f;
+    const bool write_g = (base == 0);
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvox;
+         v += (int64_t)gridDim.x * blockDim.x) {
+      int b, d, h, w;
+      decompose(v, sy.D, sy.H, sy.W, b, d, h, w);
+      float lg[kMaxCls], p[kMaxCls], gp[kMaxCls], gl[kMaxCls];
+      head_logits(y, sy, b, d, h, w, sW, sb, C, ncls, lg);
+      softmax_n(lg, ncls, p);
+      float dot = 0.f;
+      for (int k = 0; k < ncls; ++k) {
+        float gk = onehot[v * ncls + k];
+        float r = coef[3 * k + 2] != 0.f ? coef[3 * k] * (2.f * gk - coef[3 * k + 1]) : 0.f;
+        float pm = fmaxf(p[k], clamp);
+        r += p[k] >= clamp ? ce_scale * (gk / pm) : 0.f;  // training.py:125-126
+        gp[k] = r;
+        dot += r * p[k];
+      }
+      for (int k = 0; k < ncls; ++k) gl[k] = p[k] * (gp[k] - dot);  // ops.py:197-199
+      for (int cg = 0; cg < sy.CG; ++cg) {
+        float yv[8];
+        V8<T>::ld(y + sy.at(b, cg, d, h, w), yv);
+        float o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          int c = cg * 8 + j;
+          float s = 0.f;
+          if (c < C) {
+            for (int k = 0; k < ncls; ++k) {
+              s = fmaf(sW[c * ncls + k], gl[k], s);
+              int idx = c * ncls + k - base;
+              if (idx >= 0 && idx < 64) acc[idx] = fmaf(yv[j], gl[k], acc[idx]);
+            }
+          }
+          o[j] = (relu_mask && !(yv[j] > 0.f)) ? 0.f : s;
+        }
+        if (write_g) V8<T>::st(g + sg.at(b, cg, d, h, w), o);
+      }
+      for (int k = 0; k < ncls; ++k) {
+        int idx = C * ncls + k - base;
+        if (idx >= 0 && idx < 64) acc[idx] += gl[k];
+      }
+    }
+    for (int i = 0; i < 64 && base + i < nw; ++i) {
+      float s = block_sum(acc[i], red);
+      if (threadIdx.x == 0) wpart[(int64_t)blockIdx.x * nw + base + i] = s;
+    }
+  }
+}
+
+__global__ void k_reduce_rows(const float* __restrict__ part, int rows, int width,
+                              float* __restrict__ out) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < width; j += gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int r = 0; r < rows; ++r) s += part[(int64_t)r * width + j];
+    out[j] = s;
+  }
+}
+
+// ------------------------------------------------------------------ SGD (training.py:202-219)
+__global__ void k_sgd_check(const float* __restrict__ g, const int64_t* __restrict__ off,
+                            int* __restrict__ flags) {
+  const int l = blockIdx.y;
+  const int64_t a = off[l], e = off[l + 1];
+  bool bad = false;
+  for (int64_t i = a + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e;
+       i += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(g[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&flags[l], 1);
+}
+
+__global__ void k_sgd_apply(float* __restrict__ p, float* __restrict__ v, const float* __restrict__ g,
+                            const int64_t* __restrict__ off, const int* __restrict__ flags, float lr,
+                            float mu) {
+  const int l = blockIdx.y;
+  if (flags[l]) return;
+  const int64_t a = off[l], e = off[l + 1];
+  for (int64_t i = a + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    // numpy fp32 order: v *= mu; v += g; p -= lr * v   (no FMA contraction)
+    float vv = __fadd_rn(__fmul_rn(v[i], mu), g[i]);
+    v[i] = vv;
+    p[i] = __fsub_rn(p[i], __fmul_rn(lr, vv));
+  }
+}
+
+}  // namespace vm
+
+using namespace vm;
+
+#define SLAB(bs, C, D, H, W) Slab{(bs) ? (bs) : default_bstride((C), (D), (H), (W), 1), ((C) + 7) / 8, (D), (H), (W), 1}
+
+#define DISPATCH_T(dtype, NAME, ...)                                  \
+  do {                                                                \
+    if ((dtype) == VM_BF16) {                                         \
+      using T = __nv_bfloat16;                                        \
+      __VA_ARGS__;                                                    \
+    } else if ((dtype) == VM_F32) {                                   \
+      using T = float;                                                \
+      __VA_ARGS__;                                                    \
+    } else {                                                          \
+      VM_REQUIRE(false, VM_E_DTYPE, "%s: dtype %d", NAME, (dtype));   \
+    }                                                                 \
+  } while (0)
+
+extern "C" int vm_maxpool2_fwd(int dtype, const void* x, int64_t x_bstride, void* y,
+                               int64_t y_bstride, int B, int C, int D, int H, int W, void* stream) {
+  VM_REQUIRE(x && y, VM_E_ARG, "vm_maxpool2_fwd: null pointer");
+  VM_REQUIRE(D % 2 == 0 && H % 2 == 0 && W % 2 == 0, VM_E_SHAPE,
+             "maxpool2 needs even local extents, got (%d, %d, %d)", D, H, W);
+  Slab gx = SLAB(x_bstride, C, D, H, W), gy = SLAB(y_bstride, C, D / 2, H / 2, W / 2);
+  int64_t work = (int64_t)B * (D / 2) * (H / 2) * (W / 2) * gy.CG;
+  DISPATCH_T(dtype, "vm_maxpool2_fwd",
+             k_maxpool_fwd<T><<<grid_for(work, 256), 256, 0, as_stream(stream)>>>(
+                 (const T*)x, gx, (T*)y, gy, B));
+  return launch_status("vm_maxpool2_fwd");
+}
+
+extern "C" int vm_maxpool2_bwd(int dtype, const void* x, int64_t x_bstride, const void* gout,
+                               int64_t gout_bstride, const void* add, int64_t add_bstride,
+                               void* gin, int64_t gin_bstride, int B, int C, int D, int H, int W,
+                               int relu_mask, void* stream) {
+  VM_REQUIRE(x && gout && gin, VM_E_ARG, "vm_maxpool2_bwd: null pointer");
+  VM_REQUIRE(D % 2 == 0 && H % 2 == 0 && W % 2 == 0, VM_E_SHAPE, "maxpool2_bwd: odd extents");
+  Slab gx = SLAB(x_bstride, C, D, H, W), go = SLAB(gout_bstride, C, D / 2, H / 2, W / 2);
+  Slab ga = SLAB(add_bstride, C, D, H, W), gi = SLAB(gin_bstride, C, D, H, W);
+  int64_t work = (int64_t)B * (D / 2) * (H / 2) * (W / 2) * go.CG;
+  DISPATCH_T(dtype, "vm_maxpool2_bwd",
+             k_maxpool_bwd<T><<<grid_for(work, 256), 256, 0, as_stream(stream)>>>(
+                 (const T*)x, gx, (const T*)gout, go, (const T*)add, ga, (T*)gin, gi, B, relu_mask));
+  return launch_status("vm_maxpool2_bwd");
+}
+
+extern "C" int vm_upsample2_fwd(int dtype, const void* x, int64_t x_bstride, void* y,
+                                int64_t y_bstride, int B, int C, int D, int H, int W, void* stream) {
+  VM_REQUIRE(x && y, VM_E_ARG, "vm_upsample2_fwd: null pointer");
+  Slab gx = SLAB(x_bstride, C, D, H, W), gy = SLAB(y_bstride, C, 2 * D, 2 * H, 2 * W);
+  int64_t work = (int64_t)B * D * H * W * gx.CG * 8;
+  DISPATCH_T(dtype, "vm_upsample2_fwd",
+             k_upsample_fwd<T><<<grid_for(work, 256), 256, 0, as_stream(stream)>>>(
+                 (const T*)x, gx, (T*)y, gy, B));
+  return launch_status("vm_upsample2_fwd");
+}
+
+extern "C" int vm_upsample2_bwd(int dtype, const void* gy, int64_t gy_bstride, const void* mask,
+                                int64_t mask_bstride, void* gx, int64_t gx_bstride, int B, int C,
+                                int D, int H, int W, void* stream) {
+  VM_REQUIRE(gy && gx, VM_E_ARG, "vm_upsample2_bwd: null pointer");
+  Slab sgy = SLAB(gy_bstride, C, 2 * D, 2 * H, 2 * W), sgx = SLAB(gx_bstride, C, D, H, W);
+  Slab sm = SLAB(mask_bstride, C, D, H, W);
+  int64_t work = (int64_t)B * D * H * W * sgx.CG;
+  DISPATCH_T(dtype, "vm_upsample2_bwd",
+             k_upsample_bwd<T><<<grid_for(work, 256), 256, 0, as_stream(stream)>>>(
+                 (const T*)gy, sgy, (const T*)mask, sm, (T*)gx, sgx, B));
+  return launch_status("vm_upsample2_bwd");
+}
+
+extern "C" int vm_relu_mask(int dtype, const void* g, int64_t g_bstride, const void* mask,
+                            int64_t mask_bstride, void* out, int64_t out_bstride, int B, int C,
+                            int D, int H, int W, void* stream) {
+  VM_REQUIRE(g && mask && out, VM_E_ARG, "vm_relu_mask: null pointer");
+  Slab sg = SLAB(g_bstride, C, D, H, W), sm = SLAB(mask_bstride, C, D, H, W);
+  Slab so = SLAB(out_bstride, C, D, H, W);
+  int64_t work = (int64_t)B * D * H * W * sg.CG;
+  DISPATCH_T(dtype, "vm_relu_mask",
+             k_relu_mask<T><<<grid_for(work, 256), 256, 0, as_stream(stream)>>>(
+                 (const T*)g, sg, (const T*)mask, sm, (T*)out, so, B));
+  return launch_status("vm_relu_mask");
+}
+
+extern "C" int vm_head_partials_count(int B, int D, int H, int W) {
+  int64_t nvox = (int64_t)B * D * H * W;
+  int64_t blocks = (nvox + kHeadThreads - 1) / kHeadThreads;
+  int cap = 148 * 4;
+  return (int)(blocks < cap ? (blocks < 1 ? 1 : blocks) : cap);
+}
+
+extern "C" int vm_head_fwd(int dtype, const void* y, int64_t y_bstride, const float* w,
+                           const float* b, const float* onehot, float* probs, float* partials,
+                           int B, int C, int ncls, int D, int H, int W, float clamp, void* stream) {
+  VM_REQUIRE(y && w && b && onehot && partials, VM_E_ARG, "vm_head_fwd: null pointer");
+  VM_REQUIRE(ncls > 0 && ncls <= kMaxCls, VM_E_UNSUPPORTED, "vm_head_fwd: ncls %d > %d", ncls, kMaxCls);
+  Slab sy = SLAB(y_bstride, C, D, H, W);
+  int grid = vm_head_partials_count(B, D, H, W);
+  size_t sh = (C * ncls + ncls + 32) * sizeof(float);
+  DISPATCH_T(dtype, "vm_head_fwd",
+             k_head_fwd<T><<<grid, kHeadThreads, sh, as_stream(stream)>>>(
+                 (const T*)y, sy, w, b, onehot, probs, partials, B, C, ncls, clamp));
+  return launch_status("vm_head_fwd");
+}
+
+extern "C" int vm_reduce_rows(const float* partials, int rows, int width, float* out, void* stream) {
+  VM_REQUIRE(partials && out && rows > 0 && width > 0, VM_E_ARG, "vm_reduce_rows: bad argument");
+  k_reduce_rows<<<(width + 127) / 128, 128, 0, as_stream(stream)>>>(partials, rows, width, out);
+  return launch_status("vm_reduce_rows");
+}
+
+extern "C" int vm_head_bwd(int dtype, const void* y, int64_t y_bstride, const float* w,
+                           const float* b, const float* onehot, const float* stats, void* g,
+                           int64_t g_bstride, float* wpartials, int B, int C, int ncls, int D,
+                           int H, int W, float w_dice, float w_ce, float total_voxels,
+                           int dice_mask, float clamp, int relu_mask, void* stream) {
+  VM_REQUIRE(y && w && b && onehot && stats && g && wpartials, VM_E_ARG, "vm_head_bwd: null pointer");
+  VM_REQUIRE(ncls > 0 && ncls <= kMaxCls, VM_E_UNSUPPORTED, "vm_head_bwd: ncls %d", ncls);
+  Slab sy = SLAB(y_bstride, C, D, H, W), sg = SLAB(g_bstride, C, D, H, W);
+  int grid = vm_head_partials_count(B, D, H, W);
+  size_t sh = (C * ncls + ncls + 32 + 3 * kMaxCls) * sizeof(float);
+  DISPATCH_T(dtype, "vm_head_bwd",
+             k_head_bwd<T><<<grid, kHeadThreads, sh, as_stream(stream)>>>(
+                 (const T*)y, sy, w, b, onehot, stats, (T*)g, sg, wpartials, B, C, ncls, w_dice,
+                 w_ce, total_voxels, dice_mask, clamp, relu_mask));
+  return launch_status("vm_head_bwd");
+}
+
+extern "C" int vm_sgd_momentum(float* params, float* moments, const float* grads,
+                               const int64_t* offsets, int nlayers, int64_t max_layer_elems,
+                               int* flags, float lr, float momentum, void* stream) {
+  VM_REQUIRE(params && moments && grads && offsets && flags && nlayers > 0, VM_E_ARG,
+             "vm_sgd_momentum: bad argument");
+  cudaStream_t st = as_stream(stream);
+  cudaMemsetAsync(flags, 0, sizeof(int) * nlayers, st);
+  int64_t bx = (max_layer_elems + 255) / 256;
+  if (bx > 64) bx = 64;
+  if (bx < 1) bx = 1;
+  dim3 grid((unsigned)bx, (unsigned)nlayers);
+  k_sgd_check<<<grid, 256, 0, st>>>(grads, offsets, flags);
+  k_sgd_apply<<<grid, 256, 0, st>>>(params, moments, grads, offsets, flags, lr, momentum);
+  return launch_status("vm_sgd_momentum");
+}

@@ -1,0 +1,75 @@
+// vm_common.cuh — shared helpers of libvoxmesh_sm100: error plumbing, dtype
+// traits, slab geometry.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/vm_api.h"
+
+namespace vm {
+
+void set_error(const char* fmt, ...);
+int grid_for(int64_t work, int threads);  // grid-stride grid, capped at 8 x #SMs
+
+#define VM_REQUIRE(cond, code, ...)  \
+  do {                               \
+    if (!(cond)) {                   \
+      ::vm::set_error(__VA_ARGS__);  \
+      return (code);                 \
+    }                                \
+  } while (0)
+
+inline int launch_status(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return static_cast<int>(e);
+  }
+  return VM_OK;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int dtype_bytes(int dt) {
+  switch (dt) {
+    case VM_F32: return 4;
+    case VM_BF16: return 2;
+    case VM_F64: return 8;
+    case VM_U8: return 1;
+  }
+  return 0;
+}
+
+template <typename T> struct Cvt;
+template <> struct Cvt<float> {
+  __device__ __forceinline__ static float to_f(float v) { return v; }
+  __device__ __forceinline__ static float from_f(float v) { return v; }
+};
+template <> struct Cvt<__nv_bfloat16> {
+  __device__ __forceinline__ static float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+  __device__ __forceinline__ static __nv_bfloat16 from_f(float v) { return __float2bfloat16_rn(v); }
+};
+
+// Geometry of a channel-blocked padded slab [B][CG][Dp][Hp][Wp][8].
+struct Slab {
+  int64_t bstride;  // elements between samples
+  int CG, D, H, W, m;
+  __host__ __device__ int Dp() const { return D + 2 * m; }
+  __host__ __device__ int Hp() const { return H + 2 * m; }
+  __host__ __device__ int Wp() const { return W + 2 * m; }
+  __host__ __device__ int64_t plane() const { return (int64_t)Dp() * Hp() * Wp() * 8; }
+  // element offset of channel-block (b, cg) at interior voxel (d, h, w)
+  __host__ __device__ int64_t at(int b, int cg, int d, int h, int w) const {
+    return b * bstride + cg * plane() + ((((int64_t)(d + m) * Hp()) + (h + m)) * Wp() + (w + m)) * 8;
+  }
+};
+
+inline int64_t default_bstride(int C, int D, int H, int W, int m) {
+  return (int64_t)((C + 7) / 8) * (D + 2 * m) * (H + 2 * m) * (W + 2 * m) * 8;
+}
+
+}  // namespace vm

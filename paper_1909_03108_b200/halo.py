@@ -1,0 +1,357 @@
+"""Halo exchange of block margins before windowed ops, and its exact adjoint.
+
+Protocol (reference ``voxmesh/halo.py:109-229``), restated on device buffers:
+margins are exchanged one spatial dim at a time; the face sent in phase i spans
+the margins already filled by phases < i, so edges/corners arrive over 2-3 hops
+with no diagonal messages; global-boundary margins are zero; the backward is
+the linear adjoint (dims reversed, interior kept, low side added first).
+
+B200 realisation: the padded buffer is allocated once and filled in place
+(no ``np.concatenate``, halo.py:148): the interior is written by the producer,
+each face is packed into a contiguous message by the ``vm_box_pack`` kernel
+(16-byte vectorised), moved by the mesh transport (NCCL send/recv over NVLink in
+spmd mode, stream-ordered device queues in threads mode) and written into the
+margins by ``vm_box_unpack`` (``vm_box_unpack_add`` for the adjoint).  The same
+plan drives the channel-blocked slabs of the U-Net step (:mod:`.step`).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from . import _lib
+from .errors import HaloError
+from .sharding import BATCH_DIM, CHANNEL_DIM, ShardedTensor, local_shape, torch_dtype
+
+_FWD_TAG = "halo"
+_BWD_TAG = "halo-bwd"
+
+
+@dataclass(frozen=True)
+class HaloSpec:
+    """Per-spatial-dim (lo, hi) margins in voxels (halo.py:34-70)."""
+
+    margins: tuple
+
+    def __init__(self, margins):
+        if isinstance(margins, dict):
+            margins = tuple((d, int(v[0]), int(v[1])) for d, v in sorted(margins.items()))
+        else:
+            margins = tuple((str(d), int(lo), int(hi)) for d, lo, hi in margins)
+        for d, lo, hi in margins:
+            if d in (BATCH_DIM, CHANNEL_DIM):
+                raise HaloError(f"halo margins only apply to spatial dims, not {d!r}")
+            if lo < 0 or hi < 0:
+                raise HaloError(f"negative margin on {d!r}: ({lo}, {hi})")
+        object.__setattr__(self, "margins", margins)
+
+    @classmethod
+    def for_kernel(cls, k, dims=("x", "y", "z")):
+        if k % 2 == 0:
+            raise HaloError(
+                f"even kernel extent {k} is unsupported: margins must be (k-1)/2 per side, which requires odd k"
+            )
+        m = (k - 1) // 2
+        return cls(tuple((d, m, m) for d in dims))
+
+    def margin(self, dim):
+        for d, lo, hi in self.margins:
+            if d == dim:
+                return lo, hi
+        return 0, 0
+
+    def total(self, dim):
+        lo, hi = self.margin(dim)
+        return lo + hi
+
+
+@dataclass
+class PaddedBlock:
+    """A block grown by its margins + per-face provenance ("neighbor" | "zero")."""
+
+    data: object
+    halo: HaloSpec
+    dim_names: tuple
+    faces: dict = field(default_factory=dict)
+
+    def interior_slices(self):
+        return tuple(
+            slice(self.halo.margin(d)[0], self.data.shape[i] - self.halo.margin(d)[1])
+            for i, d in enumerate(self.dim_names)
+        )
+
+    @property
+    def interior(self):
+        return self.data[self.interior_slices()]
+
+
+def dim_axes(spec, layout):
+    """((dim, axis or None), ...) in tensor-dim order (halo.py:98-100)."""
+    return tuple((n, layout.axis_for(n)) for n in spec.names)
+
+
+# ---------------------------------------------------------------------------
+# Plan: the boxes of every phase, in padded coordinates of a 5-D view
+# ---------------------------------------------------------------------------
+
+
+def _pad5(shape):
+    """View any rank-<=5 shape as 5-D (leading ones)."""
+    return (1,) * (5 - len(shape)) + tuple(shape)
+
+
+@dataclass
+class Phase:
+    axis_pos: int  # index of the phase dim in the 5-D view
+    lo: int
+    hi: int
+    lo_nbr: object
+    hi_nbr: object
+    send_down: tuple  # (lo5, ext5) of the first `hi` interior rows -> lo neighbour
+    send_up: tuple  # last `lo` interior rows -> hi neighbour
+    recv_lo: tuple  # margin [0, lo) <- lo neighbour (or zero)
+    recv_hi: tuple  # margin [lo+n, lo+n+hi) <- hi neighbour (or zero)
+
+
+def plan_phases(core5, margins5, nbrs):
+    """Phases for a 5-D block of interior shape ``core5`` with per-axis (lo, hi)
+    margins ``margins5`` and ``nbrs[axis] = (lo_rank|None, hi_rank|None)``."""
+    phases = []
+    for i in range(5):
+        lo, hi = margins5[i]
+        if lo == 0 and hi == 0:
+            continue
+        n = core5[i]
+        if lo > n or hi > n:
+            raise HaloError(
+                f"margin ({lo},{hi}) exceeds local extent {n}; use a smaller mesh axis or a larger volume"
+            )
+
+        def box(a, e):
+            lo5, ext5 = [], []
+            for j in range(5):
+                mlo, mhi = margins5[j]
+                if j == i:
+                    lo5.append(a)
+                    ext5.append(e)
+                elif j < i:
+                    lo5.append(0)
+                    ext5.append(core5[j] + mlo + mhi)
+                else:
+                    lo5.append(mlo)
+                    ext5.append(core5[j])
+            return tuple(lo5), tuple(ext5)
+
+        lo_n, hi_n = nbrs.get(i, (None, None))
+        phases.append(
+            Phase(i, lo, hi, lo_n, hi_n, box(lo, hi), box(n, lo), box(0, lo), box(lo + n, hi))
+        )
+    return phases
+
+
+def _padded5(core5, margins5):
+    return tuple(c + lo + hi for c, (lo, hi) in zip(core5, margins5))
+
+
+def run_exchange(ctx, buf5, core5, margins5, nbrs, elem_bytes, tag=_FWD_TAG, dims_names=None):
+    """Fill the margins of the 5-D padded buffer ``buf5`` in place (forward protocol).
+
+    Returns {(phase_index, "lo"|"hi"): "neighbor"|"zero"}.
+    """
+    import torch
+
+    dims = _padded5(core5, margins5)
+    st = _lib.stream_ptr()
+    d64 = _lib.i64arr(dims)
+    faces = {}
+    for k, ph in enumerate(plan_phases(core5, margins5, nbrs)):
+        name = dims_names[ph.axis_pos] if dims_names else ph.axis_pos
+        sends, recvs = [], []
+        if ph.lo_nbr is not None and ph.hi > 0:
+            lo5, ext5 = ph.send_down
+            m = torch.empty(ext5, dtype=buf5.dtype, device=buf5.device)
+            _lib.call("vm_box_pack", _lib.ptr(buf5), d64, elem_bytes, _lib.i64arr(lo5), _lib.i64arr(ext5), _lib.ptr(m), st)
+            sends.append((ph.lo_nbr, m, (tag, name, "down")))
+        if ph.hi_nbr is not None and ph.lo > 0:
+            lo5, ext5 = ph.send_up
+            m = torch.empty(ext5, dtype=buf5.dtype, device=buf5.device)
+            _lib.call("vm_box_pack", _lib.ptr(buf5), d64, elem_bytes, _lib.i64arr(lo5), _lib.i64arr(ext5), _lib.ptr(m), st)
+            sends.append((ph.hi_nbr, m, (tag, name, "up")))
+        want = []
+        if ph.lo_nbr is not None and ph.lo > 0:
+            recvs.append((ph.lo_nbr, torch.empty(ph.recv_lo[1], dtype=buf5.dtype, device=buf5.device), (tag, name, "up")))
+            want.append(ph.recv_lo)
+        if ph.hi_nbr is not None and ph.hi > 0:
+            recvs.append((ph.hi_nbr, torch.empty(ph.recv_hi[1], dtype=buf5.dtype, device=buf5.device), (tag, name, "down")))
+            want.append(ph.recv_hi)
+        got = ctx.exchange(sends, recvs) if (sends or recvs) else []
+        for (lo5, ext5), t in zip(want, got):
+            _lib.call("vm_box_unpack", _lib.ptr(buf5), d64, elem_bytes, _lib.i64arr(lo5), _lib.i64arr(ext5), _lib.ptr(t), st)
+        for side, nbr, (lo5, ext5) in (("lo", ph.lo_nbr, ph.recv_lo), ("hi", ph.hi_nbr, ph.recv_hi)):
+            if nbr is None and ext5[ph.axis_pos] > 0:
+                _lib.call("vm_box_zero", _lib.ptr(buf5), d64, elem_bytes, _lib.i64arr(lo5), _lib.i64arr(ext5), st)
+            faces[(name, side)] = "neighbor" if nbr is not None else "zero"
+    return faces
+
+
+def run_exchange_backward(ctx, buf5, core5, margins5, nbrs, dtype_code, elem_bytes, tag=_BWD_TAG, dims_names=None):
+    """Adjoint (halo.py:158-194): phases reversed; margins are sent back and added
+    to the owner's interior rows (low side first, then high).  Operates in place
+    on ``buf5``; the result is its interior."""
+    import torch
+
+    dims = _padded5(core5, margins5)
+    st = _lib.stream_ptr()
+    d64 = _lib.i64arr(dims)
+    for ph in reversed(plan_phases(core5, margins5, nbrs)):
+        name = dims_names[ph.axis_pos] if dims_names else ph.axis_pos
+        sends, recvs, targets = [], [], []
+        if ph.lo_nbr is not None and ph.lo > 0:  # margin [0,lo) goes back down
+            lo5, ext5 = ph.recv_lo
+            m = torch.empty(ext5, dtype=buf5.dtype, device=buf5.device)
+            _lib.call("vm_box_pack", _lib.ptr(buf5), d64, elem_bytes, _lib.i64arr(lo5), _lib.i64arr(ext5), _lib.ptr(m), st)
+            sends.append((ph.lo_nbr, m, (tag, name, "down")))
+        if ph.hi_nbr is not None and ph.hi > 0:  # margin [lo+n, lo+n+hi) goes back up
+            lo5, ext5 = ph.recv_hi
+            m = torch.empty(ext5, dtype=buf5.dtype, device=buf5.device)
+            _lib.call("vm_box_pack", _lib.ptr(buf5), d64, elem_bytes, _lib.i64arr(lo5), _lib.i64arr(ext5), _lib.ptr(m), st)
+            sends.append((ph.hi_nbr, m, (tag, name, "up")))
+        if ph.lo_nbr is not None and ph.hi > 0:  # first hi interior rows += from lo nbr
+            recvs.append((ph.lo_nbr, torch.empty(ph.send_down[1], dtype=buf5.dtype, device=buf5.device), (tag, name, "up")))
+            targets.append(ph.send_down)
+        if ph.hi_nbr is not None and ph.lo > 0:  # last lo interior rows += from hi nbr
+            recvs.append((ph.hi_nbr, torch.empty(ph.send_up[1], dtype=buf5.dtype, device=buf5.device), (tag, name, "down")))
+            targets.append(ph.send_up)
+        got = ctx.exchange(sends, recvs) if (sends or recvs) else []
+        for (lo5, ext5), t in zip(targets, got):
+            _lib.call("vm_box_unpack_add", _lib.ptr(buf5), d64, dtype_code, _lib.i64arr(lo5), _lib.i64arr(ext5), _lib.ptr(t), st)
+
+
+# ---------------------------------------------------------------------------
+# Worker-side API (exchange_local / exchange_backward_local, halo.py:109-194)
+# ---------------------------------------------------------------------------
+
+
+def _spec5(block_shape, dims, halo, ctx):
+    names = [n for n, _ in dims]
+    if len(names) > 5:
+        raise HaloError("at most 5 tensor dims are supported")
+    pad = 5 - len(names)
+    core5 = _pad5(block_shape)
+    margins5 = [(0, 0)] * pad + [halo.margin(n) for n in names]
+    nbrs = {}
+    for i, (n, axis) in enumerate(dims):
+        if axis is not None:
+            nbrs[pad + i] = (ctx.neighbor(axis, -1), ctx.neighbor(axis, +1))
+    names5 = (None,) * pad + tuple(names)
+    return core5, margins5, nbrs, names5
+
+
+def exchange_local(ctx, dims, halo, tag, phase_barrier, block):
+    """Worker-side forward exchange; returns the PaddedBlock (device tensor)."""
+    import torch
+
+    core5, margins5, nbrs, names5 = _spec5(tuple(block.shape), dims, halo, ctx)
+    for i, (lo, hi) in enumerate(margins5):
+        if lo > core5[i] or hi > core5[i]:
+            raise HaloError(
+                f"margin ({lo},{hi}) on {names5[i]!r} exceeds local extent {core5[i]}; "
+                "use a smaller mesh axis or a larger volume"
+            )
+    padded_shape = tuple(c + lo + hi for c, (lo, hi) in zip(core5, margins5))
+    buf = torch.empty(padded_shape, dtype=block.dtype, device=block.device)
+    eb = block.element_size()
+    st = _lib.stream_ptr()
+    inner_lo = tuple(lo for lo, _ in margins5)
+    _lib.call(
+        "vm_box_unpack", _lib.ptr(buf), _lib.i64arr(padded_shape), eb, _lib.i64arr(inner_lo),
+        _lib.i64arr(core5), _lib.ptr(block.contiguous().reshape(core5)), st,
+    )
+    faces = run_exchange(ctx, buf, core5, margins5, nbrs, eb, tag, names5)
+    if phase_barrier:
+        pass  # stream/queue ordering replaces the per-phase barrier (halo.py:151-152)
+    out_shape = tuple(e + halo.total(n) for e, (n, _) in zip(block.shape, dims))
+    return PaddedBlock(buf.reshape(out_shape), halo, tuple(n for n, _ in dims), faces)
+
+
+def exchange_backward_local(ctx, dims, halo, tag, phase_barrier, grad_padded):
+    """Worker-side adjoint; returns the interior gradient (device tensor)."""
+    import torch
+
+    g = grad_padded.data if isinstance(grad_padded, PaddedBlock) else grad_padded
+    names = [n for n, _ in dims]
+    core = tuple(e - halo.total(n) for e, n in zip(g.shape, names))
+    for e, n in zip(core, names):
+        if e <= 0:
+            lo, hi = halo.margin(n)
+            raise HaloError(f"gradient block extent {e + lo + hi} too small for margins ({lo},{hi}) on {n!r}")
+    core5, margins5, nbrs, names5 = _spec5(core, dims, halo, ctx)
+    buf = g.contiguous().clone().reshape(_padded5(core5, margins5))
+    run_exchange_backward(ctx, buf, core5, margins5, nbrs, _lib.dtype_code(g.dtype), g.element_size(), tag, names5)
+    out = torch.empty(core5, dtype=g.dtype, device=g.device)
+    inner_lo = tuple(lo for lo, _ in margins5)
+    _lib.call(
+        "vm_box_pack", _lib.ptr(buf), _lib.i64arr(buf.shape), g.element_size(), _lib.i64arr(inner_lo),
+        _lib.i64arr(core5), _lib.ptr(out), _lib.stream_ptr(),
+    )
+    return out.reshape(core)
+
+
+def exchange_byte_count(spec, layout, mesh, halo, direction="forward"):
+    """Analytic bytes sent by all workers in one exchange (halo.py:197-229)."""
+    if direction not in ("forward", "backward"):
+        raise ValueError(f"direction must be forward|backward, got {direction!r}")
+    layout.validate(spec, mesh)
+    cur0 = list(local_shape(spec, layout, mesh))
+    total = 0
+    for coord in mesh.coords:
+        cur = list(cur0)
+        for i, name in enumerate(spec.names):
+            lo, hi = halo.margin(name)
+            if lo == 0 and hi == 0:
+                continue
+            axis = layout.axis_for(name)
+            if axis is not None and mesh.axis_size(axis) > 1:
+                area = 1
+                for j, e in enumerate(cur):
+                    if j != i:
+                        area *= e
+                c = coord[mesh.axis_index[axis]]
+                down, up = (hi, lo) if direction == "forward" else (lo, hi)
+                total += down * area if c > 0 else 0
+                total += up * area if c < mesh.axis_size(axis) - 1 else 0
+            cur[i] += lo + hi
+    return total * spec.dtype.itemsize
+
+
+def halo_exchange(x: ShardedTensor, halo, phase_barrier=True):
+    """Collective forward exchange; one PaddedBlock per rank (None for remote ranks)."""
+    dims = dim_axes(x.spec, x.layout)
+    return x.mesh.run(exchange_local, dims, halo, _FWD_TAG, phase_barrier, per_worker=(x.blocks,))
+
+
+def halo_exchange_backward(grad_padded, x_spec, layout, mesh, halo, phase_barrier=True):
+    """Collective adjoint; returns the interior gradient as a ShardedTensor."""
+    import torch
+
+    dims = dim_axes(x_spec, layout)
+    base = local_shape(x_spec, layout, mesh)
+    expected = tuple(e + halo.total(n) for e, n in zip(base, x_spec.names))
+    arrays = []
+    for r, g in enumerate(grad_padded):
+        if g is None:
+            arrays.append(None)
+            continue
+        arr = g.data if isinstance(g, PaddedBlock) else g
+        if not isinstance(arr, torch.Tensor):
+            arr = torch.as_tensor(arr).to(mesh.device_of(r))
+        if tuple(arr.shape) != expected:
+            raise HaloError(
+                f"gradient block shape {tuple(arr.shape)} does not match padded shape {expected} "
+                f"for margins {halo.margins}"
+            )
+        if arr.dtype != torch_dtype(x_spec.dtype):
+            arr = arr.to(torch_dtype(x_spec.dtype))
+        arrays.append(arr)
+    blocks = mesh.run(exchange_backward_local, dims, halo, _BWD_TAG, phase_barrier, per_worker=(arrays,))
+    return ShardedTensor(x_spec, layout, mesh, blocks)

@@ -1,0 +1,487 @@
+"""The per-GPU U-Net train step on channel-blocked padded slabs (the hot path).
+
+Replaces the reference's per-worker graph interpreter (``unet.run_forward_local``
+/ ``run_backward_local``, unet.py:331-442) and ``training._train_step``
+(training.py:330-343) with a static program over pre-allocated device buffers:
+
+* every activation lives in a slab ``[B][ceil(C/8)][D+2][H+2][W+2][8]`` (bf16 or
+  fp32); producers write interiors, the halo exchange writes margins, global
+  boundary margins stay zero (no re-padding, halo.py:148);
+* conv + bias + ReLU is one kernel (the tape keeps the post-ReLU output only:
+  y>0 <=> x>0, ops.py:186-187); decoder concat [up, skip] is zero-copy when the
+  upsampled channel count is a multiple of 8 (the encoder's last conv writes
+  straight into the skip half of the concat slab);
+* backward: wgrad(x, g) -> [halo(g)] -> dgrad = forward conv of g with flipped,
+  transposed taps, whose epilogue applies the previous layer's ReLU mask;
+  maxpool / upsample backward fuse the fan-out add and the mask;
+* head 1x1x1 conv + softmax + Dice/CE statistics in one kernel; statistics and
+  weight gradients are summed over the mesh (ctx.all_reduce_sum -> NCCL
+  all_reduce in spmd mode); SGD with momentum + non-finite skip in one launch.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import GraphBuildError, VoxmeshError
+from .halo import run_exchange
+
+_DT = {torch.bfloat16: _lib.VM_BF16, torch.float32: _lib.VM_F32}
+
+
+class Slab:
+    """Channel-blocked padded buffer; may be a channel-group window of a wider slab."""
+
+    def __init__(self, B, C, D, H, W, dtype, device, parent=None, cg0=0):
+        self.B, self.C, self.D, self.H, self.W = B, C, D, H, W
+        self.CG = (C + 7) // 8
+        self.dtype = dtype
+        self.plane = (D + 2) * (H + 2) * (W + 2) * 8
+        if parent is None:
+            self.storage = torch.zeros(B * self.CG * self.plane, dtype=dtype, device=device)
+            self.bstride = self.CG * self.plane
+            self.offset = 0
+        else:
+            assert parent.plane == self.plane and parent.dtype == dtype
+            self.storage = parent.storage
+            self.bstride = parent.bstride
+            self.offset = parent.offset + cg0 * self.plane
+        self.parent = parent
+
+    @property
+    def ptr(self):
+        return self.storage.data_ptr() + self.offset * self.storage.element_size()
+
+    def p(self):
+        return _lib.ctypes.c_void_p(self.ptr)
+
+    def view5(self, b):
+        """[CG, D+2, H+2, W+2, 8] view of sample b (for halo box kernels)."""
+        return self.storage.as_strided(
+            (self.CG, self.D + 2, self.H + 2, self.W + 2, 8),
+            (self.plane, (self.H + 2) * (self.W + 2) * 8, (self.W + 2) * 8, 8, 1),
+            self.offset + b * self.bstride,
+        )
+
+    def interior(self):
+        """Dense [B, D, H, W, C] fp32 copy of the interior (test/debug helper)."""
+        out = torch.empty((self.B, self.D, self.H, self.W, self.C), dtype=torch.float32, device=self.storage.device)
+        _lib.call(
+            "vm_slab_to_dense", self.p(), _DT[self.dtype], self.bstride, _lib.ptr(out), _lib.VM_F32,
+            self.B, self.C, self.D, self.H, self.W, 1, _lib.stream_ptr(),
+        )
+        return out
+
+
+class ConvLayer:
+    def __init__(self, node, index, D, H, W):
+        self.node, self.index = node, index
+        self.k, self.cin, self.cout = node.k, node.c_in, node.c_out
+        self.D, self.H, self.W = D, H, W
+        self.nk = self.k ** 3 * self.cin * self.cout
+
+
+class UNetStep:
+    """Static train-step program for one rank's block.
+
+    ``params`` is the reference-format dict {conv id: {"kernel": [k,k,k,ci,co], "bias": [co]}}.
+    ``ctx`` (a mesh WorkerContext) supplies neighbours, halo transport and
+    all-reduce; ``None`` means a single unpartitioned rank.
+    """
+
+    def __init__(self, graph, params, batch=1, ctx=None, device=None, dtype=torch.bfloat16,
+                 conv_impl="tc", lr=0.003, momentum=0.9, loss_weights=(0.9, 0.1),
+                 dice_classes=(1, 2), clamp=1e-12, global_batch=None):
+        cfg = graph.config
+        if cfg.kernel != 3:
+            raise GraphBuildError(f"the slab step supports 3x3x3 convolutions, got k={cfg.kernel}")
+        self.graph, self.cfg, self.ctx = graph, cfg, ctx
+        self.device = torch.device(device) if device is not None else (ctx.device if ctx else torch.device("cuda"))
+        if self.device.type != "cuda":
+            raise VoxmeshError("the step program needs a CUDA device (no CPU fallback)")
+        _lib.load()
+        self.dtype, self.dt = dtype, _DT[dtype]
+        self.conv_impl = conv_impl if dtype == torch.bfloat16 else "simt"
+        self.B = batch
+        self.lr, self.mu = float(lr), float(momentum)
+        self.w_dice, self.w_ce = loss_weights
+        self.dice_mask = sum(1 << k for k in dice_classes)
+        self.clamp = clamp
+        self.keep_probs = False
+        self.probs = None
+        self.ncls = cfg.num_classes
+        # local extents per spatial dim (x->D, y->H, z->W)
+        layout, mesh = graph.layout, graph.mesh
+        self.div = [1, 1, 1]
+        self.nbrs = {}
+        for i, d in enumerate(("x", "y", "z")):
+            a = layout.axis_for(d) if layout is not None else None
+            if a is not None and mesh is not None:
+                self.div[i] = mesh.axis_size(a)
+                if ctx is not None:
+                    self.nbrs[1 + i] = (ctx.neighbor(a, -1), ctx.neighbor(a, +1))
+        self.has_halo = any(lo is not None or hi is not None for lo, hi in self.nbrs.values())
+        bdiv = mesh.axis_size(layout.axis_for("batch")) if (layout is not None and layout.axis_for("batch")) else 1
+        self.global_batch = global_batch or batch * bdiv
+        self.total_voxels = float(self.global_batch * cfg.input_extent ** 3)
+        self._build_buffers(params)
+
+    # ------------------------------------------------------------------ setup
+    def _ext(self, nid):
+        e = self.graph.level_extents[nid]
+        return (e // self.div[0], e // self.div[1], e // self.div[2])
+
+    def _slab(self, C, ext, parent=None, cg0=0):
+        return Slab(self.B, C, *ext, self.dtype, self.device, parent, cg0)
+
+    def _build_buffers(self, params):
+        g = self.graph
+        dev = self.device
+        convs = g.conv_nodes
+        self.layers = []
+        offs = [0]
+        for i, n in enumerate(convs):
+            L = ConvLayer(n, i, *self._ext(n.id))
+            self.layers.append(L)
+            offs.append(offs[-1] + L.nk + n.c_out)
+        self.by_id = {L.node.id: L for L in self.layers}
+        total = offs[-1]
+        self.offsets_host = offs
+        self.offsets = torch.tensor(offs, dtype=torch.int64, device=dev)
+        self.max_layer = max(b - a for a, b in zip(offs, offs[1:]))
+        self.params = torch.zeros(total, dtype=torch.float32, device=dev)
+        self.moments = torch.zeros(total, dtype=torch.float32, device=dev)
+        self.grads = torch.zeros(total, dtype=torch.float32, device=dev)
+        self.skip_flags = torch.zeros(len(self.layers), dtype=torch.int32, device=dev)
+        host = np.zeros(total, dtype=np.float32)
+        for L, a in zip(self.layers, offs):
+            p = params[L.node.id]
+            host[a : a + L.nk] = np.asarray(p["kernel"], dtype=np.float32).reshape(-1)
+            host[a + L.nk : a + L.nk + L.cout] = np.asarray(p["bias"], dtype=np.float32)
+        self.params.copy_(torch.from_numpy(host))
+        for L, a in zip(self.layers, offs):
+            L.w = self.params[a : a + L.nk]
+            L.b = self.params[a + L.nk : a + L.nk + L.cout]
+            L.gw = self.grads[a : a + L.nk]
+            L.gb = self.grads[a + L.nk : a + L.nk + L.cout]
+            if L.k == 3:
+                if self.conv_impl == "tc":
+                    nbytes = int(_lib.call_size("vm_packed_weights_bytes", L.cin, L.cout))
+                    L.wp = torch.empty(nbytes // 2, dtype=torch.bfloat16, device=dev)
+                    L.wpt = torch.empty(int(_lib.call_size("vm_packed_weights_bytes", L.cout, L.cin)) // 2,
+                                        dtype=torch.bfloat16, device=dev)
+                else:
+                    L.wt = torch.empty(L.nk, dtype=torch.float32, device=dev)
+                ws_fn = "vm_conv3d_wgrad_tc_ws" if self.conv_impl == "tc" else "vm_conv3d_wgrad_simt_ws"
+                L.ws_bytes = int(_lib.call_size(ws_fn, self.B, L.cin, L.cout, L.D, L.H, L.W))
+        self.wgrad_ws = torch.empty(max([L.ws_bytes for L in self.layers if L.k == 3] + [16]) // 4 + 4,
+                                    dtype=torch.float32, device=dev)
+
+        # activation slabs -------------------------------------------------
+        self.out = {}  # node id -> Slab holding that node's output (relu shares its conv's slab)
+        nodes = g.nodes
+        consumers = {}
+        for n in nodes:
+            for inp in n.inputs:
+                consumers.setdefault(inp, []).append(n)
+        self.consumers = consumers
+        cfg = self.cfg
+        e0 = self._ext(nodes[0].id)
+        self.x_in = self._slab(cfg.in_channels, e0)
+        self.out["input"] = self.x_in
+        self.cat_parts = {}
+        # concat slabs first, so skip producers can write into them
+        for n in nodes:
+            if n.op == "concat":
+                up_id, skip_id = n.inputs
+                c_up = self.graph.node(up_id).c_out
+                cat = self._slab(n.c_out, self._ext(n.id))
+                self.out[n.id] = cat
+                aligned = c_up % 8 == 0
+                self.cat_parts[n.id] = (c_up, aligned)
+                if aligned:
+                    self.out[up_id] = self._slab(c_up, self._ext(n.id), parent=cat, cg0=0)
+                    skip_c = n.c_out - c_up
+                    self.out[skip_id] = self._slab(skip_c, self._ext(n.id), parent=cat, cg0=c_up // 8)
+        for n in nodes:
+            if n.id in self.out:
+                continue
+            if n.op == "conv" and n.k == 3:
+                relu = next(c for c in consumers[n.id] if c.op == "relu")
+                if relu.id in self.out:  # skip source written into the concat slab
+                    self.out[n.id] = self.out[relu.id]
+                else:
+                    self.out[n.id] = self._slab(n.c_out, self._ext(n.id))
+                    self.out[relu.id] = self.out[n.id]
+            elif n.op == "relu":
+                self.out[n.id] = self.out[n.inputs[0]]
+            elif n.op in ("pool", "up"):
+                self.out[n.id] = self._slab(n.c_out, self._ext(n.id))
+        # gradient slabs ---------------------------------------------------
+        self.gpre = {L.node.id: self._slab(L.cout, (L.D, L.H, L.W)) for L in self.layers if L.k == 3}
+        self.gnode = {}
+        for n in nodes:
+            if n.op in ("pool", "concat"):
+                self.gnode[n.id] = self._slab(n.c_out, self._ext(n.id))
+        # head / loss -------------------------------------------------------
+        head = self.by_id["head"]
+        self.head = head
+        self.head_in = head.node.inputs[0]
+        hD, hH, hW = head.D, head.H, head.W
+        self.nvox = self.B * hD * hH * hW
+        self.onehot = torch.zeros(self.nvox * self.ncls, dtype=torch.float32, device=dev)
+        self.n_part = int(_lib.load().vm_head_partials_count(self.B, hD, hH, hW))
+        self.partials = torch.zeros(self.n_part * (3 * self.ncls + 1), dtype=torch.float32, device=dev)
+        self.stats = torch.zeros(3 * self.ncls + 1, dtype=torch.float32, device=dev)
+        self.hw_width = head.cin * self.ncls + self.ncls
+        self.hpartials = torch.zeros(self.n_part * self.hw_width, dtype=torch.float32, device=dev)
+        self.hgrad = torch.zeros(self.hw_width, dtype=torch.float32, device=dev)
+        self.repack()
+
+    # ------------------------------------------------------------------ kernels
+    def _st(self):
+        return _lib.stream_ptr()
+
+    def repack(self):
+        """Refresh the derived conv operands from the fp32 master weights."""
+        st = self._st()
+        for L in self.layers:
+            if L.k != 3:
+                continue
+            if self.conv_impl == "tc":
+                _lib.call("vm_pack_weights", _lib.ptr(L.w), _lib.ptr(L.wp), L.cin, L.cout, 0, st)
+                _lib.call("vm_pack_weights", _lib.ptr(L.w), _lib.ptr(L.wpt), L.cin, L.cout, 1, st)
+            else:
+                _lib.call("vm_weight_flip_transpose", _lib.ptr(L.w), _lib.ptr(L.wt), 3, L.cin, L.cout, st)
+
+    def _conv(self, x, L, y, flags, mask=None, dgrad=False):
+        cin, cout = (L.cout, L.cin) if dgrad else (L.cin, L.cout)
+        st = self._st()
+        mp = mask.p() if mask is not None else None
+        mb = mask.bstride if mask is not None else 0
+        if self.conv_impl == "tc":
+            w = L.wpt if dgrad else L.wp
+            _lib.call("vm_conv3d_fwd_tc", x.p(), x.bstride, _lib.ptr(w), _lib.ptr(L.b), y.p(), y.bstride,
+                      mp, mb, self.B, cin, cout, L.D, L.H, L.W, flags, st)
+        else:
+            w = L.wt if dgrad else L.w
+            _lib.call("vm_conv3d_fwd_simt", self.dt, x.p(), x.bstride, _lib.ptr(w), _lib.ptr(L.b), y.p(),
+                      y.bstride, mp, mb, self.B, cin, cout, L.D, L.H, L.W, flags, st)
+
+    def _wgrad(self, x, L, g):
+        st = self._st()
+        if self.conv_impl == "tc":
+            _lib.call("vm_conv3d_wgrad_tc", x.p(), x.bstride, g.p(), g.bstride, _lib.ptr(L.gw), _lib.ptr(L.gb),
+                      _lib.ptr(self.wgrad_ws), self.B, L.cin, L.cout, L.D, L.H, L.W, st)
+        else:
+            _lib.call("vm_conv3d_wgrad_simt", self.dt, x.p(), x.bstride, g.p(), g.bstride, _lib.ptr(L.gw),
+                      _lib.ptr(L.gb), _lib.ptr(self.wgrad_ws), self.B, L.cin, L.cout, L.D, L.H, L.W, st)
+
+    def _halo(self, s, tag):
+        if not self.has_halo:
+            return
+        margins5 = [(0, 0), (1, 1), (1, 1), (1, 1), (0, 0)]
+        core5 = (s.CG, s.D, s.H, s.W, 8)
+        for b in range(self.B):
+            run_exchange(self.ctx, s.view5(b), core5, margins5, self.nbrs, s.storage.element_size(), tag)
+
+    def _zero_margins(self, s):
+        if not self.has_halo:
+            return
+        st = self._st()
+        for b in range(self.B):
+            v = s.view5(b)
+            dims = _lib.i64arr(v.shape)
+            for ax in (1, 2, 3):
+                n = v.shape[ax] - 2
+                for lo in (0, n + 1):
+                    lo5 = [0, 0, 0, 0, 0]
+                    ext5 = list(v.shape)
+                    lo5[ax], ext5[ax] = lo, 1
+                    _lib.call("vm_box_zero", _lib.ptr(v), dims, v.element_size(), _lib.i64arr(lo5),
+                              _lib.i64arr(ext5), st)
+
+    # ------------------------------------------------------------------ inputs
+    def load_inputs(self, image, onehot):
+        """image: device f32 [B,D,H,W,Cin] (local block); onehot: device f32 [B,D,H,W,ncls]."""
+        st = self._st()
+        x = self.x_in
+        _lib.call("vm_dense_to_slab", _lib.ptr(image.contiguous()), _lib.VM_F32, x.p(), self.dt, x.bstride,
+                  self.B, x.C, x.D, x.H, x.W, 1, st)
+        self.onehot.copy_(onehot.reshape(-1))
+
+    # ------------------------------------------------------------------ passes
+    def forward(self):
+        st = self._st()
+        for n in self.graph.nodes:
+            if n.op == "conv" and n.k == 3:
+                x = self.out[n.inputs[0]]
+                self._halo(x, "halo")
+                self._conv(x, self.by_id[n.id], self.out[n.id], _lib.VM_CONV_RELU)
+            elif n.op == "pool":
+                x, y = self.out[n.inputs[0]], self.out[n.id]
+                _lib.call("vm_maxpool2_fwd", self.dt, x.p(), x.bstride, y.p(), y.bstride, self.B, x.C, x.D,
+                          x.H, x.W, st)
+            elif n.op == "up":
+                x, y = self.out[n.inputs[0]], self.out[n.id]
+                _lib.call("vm_upsample2_fwd", self.dt, x.p(), x.bstride, y.p(), y.bstride, self.B, x.C, x.D,
+                          x.H, x.W, st)
+            elif n.op == "concat":
+                c_up, aligned = self.cat_parts[n.id]
+                if not aligned:
+                    self._concat_copy(n)
+        h = self.head
+        y = self.out[self.head_in]
+        probs = None
+        if self.keep_probs:
+            if getattr(self, "probs", None) is None:
+                self.probs = torch.empty(self.nvox * self.ncls, dtype=torch.float32, device=self.device)
+            probs = _lib.ptr(self.probs)
+        _lib.call("vm_head_fwd", self.dt, y.p(), y.bstride, _lib.ptr(h.w), _lib.ptr(h.b), _lib.ptr(self.onehot),
+                  probs, _lib.ptr(self.partials), self.B, h.cin, self.ncls, h.D, h.H, h.W, self.clamp, st)
+        _lib.call("vm_reduce_rows", _lib.ptr(self.partials), self.n_part, 3 * self.ncls + 1,
+                  _lib.ptr(self.stats), st)
+        if self.ctx is not None and self.ctx.mesh.worker_count > 1:
+            red = self.ctx.all_reduce_sum(self.stats, tag="loss-stats")
+            if red is not self.stats:
+                self.stats.copy_(red)
+
+    def backward(self):
+        st = self._st()
+        h = self.head
+        y = self.out[self.head_in]
+        last = self.graph.node(self.head_in)
+        last_conv = last.inputs[0] if last.op == "relu" else last.id
+        g = self.gpre[last_conv]
+        _lib.call("vm_head_bwd", self.dt, y.p(), y.bstride, _lib.ptr(h.w), _lib.ptr(h.b), _lib.ptr(self.onehot),
+                  _lib.ptr(self.stats), g.p(), g.bstride, _lib.ptr(self.hpartials), self.B, h.cin, self.ncls,
+                  h.D, h.H, h.W, self.w_dice, self.w_ce, self.total_voxels, self.dice_mask, self.clamp, 1, st)
+        _lib.call("vm_reduce_rows", _lib.ptr(self.hpartials), self.n_part, self.hw_width, _lib.ptr(self.hgrad), st)
+        # head grads: [C*ncls] kernel (DHWIO with k=1) then [ncls] bias
+        h.gw.copy_(self.hgrad[: h.nk])
+        h.gb.copy_(self.hgrad[h.nk :])
+        for n in reversed(self.graph.nodes):
+            if n.op == "conv" and n.k == 3:
+                L = self.by_id[n.id]
+                x = self.out[n.inputs[0]]
+                gp = self.gpre[n.id]
+                self._wgrad(x, L, gp)
+                src = n.inputs[0]
+                if src == "input":
+                    continue
+                self._halo(gp, "halo-bwd")
+                sn = self.graph.node(src)
+                if sn.op == "relu":
+                    self._conv(gp, L, self.gpre[sn.inputs[0]], _lib.VM_CONV_MASK | _lib.VM_CONV_NOBIAS,
+                               mask=self.out[src], dgrad=True)
+                else:  # pool or concat output gradient, unmasked
+                    self._conv(gp, L, self.gnode[src], _lib.VM_CONV_NOBIAS, dgrad=True)
+                self._zero_margins(gp)
+            elif n.op == "up":
+                cat = next(c for c in self.consumers[n.id] if c.op == "concat")
+                gcat = self.gnode[cat.id]
+                c_up, aligned = self.cat_parts[cat.id]
+                gup = self._window(gcat, 0, c_up, aligned, copy_from=cat.id, part="up")
+                src = n.inputs[0]
+                sn = self.graph.node(src)
+                x = self.out[src]
+                dst = self.gpre[sn.inputs[0]]
+                _lib.call("vm_upsample2_bwd", self.dt, gup.p(), gup.bstride, x.p(), x.bstride, dst.p(), dst.bstride,
+                          self.B, x.C, x.D, x.H, x.W, st)
+            elif n.op == "pool":
+                src = n.inputs[0]
+                sn = self.graph.node(src)
+                x = self.out[src]
+                dst = self.gpre[sn.inputs[0]]
+                gpool = self.gnode[n.id]
+                cat = next((c for c in self.consumers[src] if c.op == "concat"), None)
+                add = None
+                if cat is not None:
+                    c_up, aligned = self.cat_parts[cat.id]
+                    add = self._window(self.gnode[cat.id], c_up, cat.c_out - c_up, aligned, copy_from=cat.id,
+                                       part="skip")
+                _lib.call("vm_maxpool2_bwd", self.dt, x.p(), x.bstride, gpool.p(), gpool.bstride,
+                          add.p() if add else None, add.bstride if add else 0, dst.p(), dst.bstride,
+                          self.B, x.C, x.D, x.H, x.W, 1, st)
+
+    def all_reduce_grads(self):
+        if self.ctx is not None and self.ctx.mesh.worker_count > 1:
+            red = self.ctx.all_reduce_sum(self.grads, tag="grads")
+            if red is not self.grads:
+                self.grads.copy_(red)
+
+    def sgd(self):
+        _lib.call("vm_sgd_momentum", _lib.ptr(self.params), _lib.ptr(self.moments), _lib.ptr(self.grads),
+                  _lib.ptr(self.offsets), len(self.layers), self.max_layer, _lib.ptr(self.skip_flags),
+                  self.lr, self.mu, self._st())
+        self.repack()
+
+    def step(self):
+        """One train step on the resident inputs (fwd -> stats -> bwd -> grads -> SGD)."""
+        self.forward()
+        self.backward()
+        self.all_reduce_grads()
+        self.sgd()
+
+    # ------------------------------------------------------------------ helpers
+    def _window(self, s, c0, nc, aligned, copy_from=None, part=None):
+        if aligned:
+            return Slab(self.B, nc, s.D, s.H, s.W, self.dtype, self.device, parent=s, cg0=c0 // 8)
+        key = (copy_from, part)
+        if not hasattr(self, "_tmp"):
+            self._tmp = {}
+        if key not in self._tmp:
+            self._tmp[key] = self._slab(nc, (s.D, s.H, s.W))
+        t = self._tmp[key]
+        self._copy_channels(s, c0, t, 0, nc)
+        return t
+
+    def _copy_channels(self, src, c0, dst, d0, nc):
+        dense = src.interior()[..., c0 : c0 + nc].contiguous()
+        if dst.C != nc or d0 != 0:
+            full = dst.interior()
+            full[..., d0 : d0 + nc] = dense
+            dense = full
+        _lib.call("vm_dense_to_slab", _lib.ptr(dense), _lib.VM_F32, dst.p(), self.dt, dst.bstride, self.B,
+                  dst.C, dst.D, dst.H, dst.W, 1, self._st())
+
+    def _concat_copy(self, n):
+        up_id, skip_id = n.inputs
+        cat = self.out[n.id]
+        up, skip = self.out[up_id], self.out[skip_id]
+        dense = torch.cat([up.interior(), skip.interior()], dim=-1).contiguous()
+        _lib.call("vm_dense_to_slab", _lib.ptr(dense), _lib.VM_F32, cat.p(), self.dt, cat.bstride, self.B,
+                  cat.C, cat.D, cat.H, cat.W, 1, self._st())
+
+    # ------------------------------------------------------------------ readout
+    def loss(self):
+        """(combined, dice, ce) from the reduced statistics (training.py:95-107)."""
+        s = self.stats.double().cpu().numpy()
+        c = self.ncls
+        ks = [k for k in range(c) if (self.dice_mask >> k) & 1]
+        ratios = [(2.0 * s[k] + 1e-6) / (s[c + k] + s[2 * c + k] + 1e-6) for k in ks]
+        dice = 1.0 - sum(ratios) / len(ratios)
+        ce = float(s[3 * c]) / self.total_voxels
+        return self.w_dice * dice + self.w_ce * ce, dice, ce
+
+    def param_dict(self):
+        host = self.params.cpu().numpy()
+        out = {}
+        for L, a in zip(self.layers, self.offsets_host):
+            out[L.node.id] = {
+                "kernel": host[a : a + L.nk].reshape(L.k, L.k, L.k, L.cin, L.cout).copy(),
+                "bias": host[a + L.nk : a + L.nk + L.cout].copy(),
+            }
+        return out
+
+    def grad_dict(self):
+        host = self.grads.cpu().numpy()
+        return {
+            L.node.id: (host[a : a + L.nk].reshape(L.k, L.k, L.k, L.cin, L.cout).copy(),
+                        host[a + L.nk : a + L.nk + L.cout].copy())
+            for L, a in zip(self.layers, self.offsets_host)
+        }
