@@ -53,6 +53,8 @@ int vm_version(void);
 const char* vm_error_string(int code);
 const char* vm_last_error(void);
 int vm_num_sms(int device);
+/* number of kernels this library has launched in this process (bench bookkeeping) */
+long long vm_launch_count(void);
 
 /* ------------------------------------------------------------------ boxes / halo
  * Generic 5-D box copies on a dense tensor of shape dims[5] (dims[4] contiguous,

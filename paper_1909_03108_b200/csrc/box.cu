@@ -6,7 +6,7 @@
 // contiguous copies of the face), :139-148 (zero fill + concatenate),
 // :176-186 (adjoint: receive and add); sharding.py:189-209 (block copies).
 #include <cstdarg>
-#include <mutex>
+#include <atomic>
 
 #include "vm_common.cuh"
 
@@ -19,6 +19,9 @@ void set_error(const char* fmt, ...) {
   vsnprintf(g_err, sizeof g_err, fmt, ap);
   va_end(ap);
 }
+
+static std::atomic<long long> g_launches{0};
+void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 static int g_num_sms = -1;
 static int num_sms() {
@@ -155,6 +158,8 @@ extern "C" const char* vm_error_string(int code) {
 }
 
 extern "C" const char* vm_last_error(void) { return g_err; }
+
+extern "C" long long vm_launch_count(void) { return g_launches.load(); }
 
 extern "C" int vm_num_sms(int device) {
   int n = 0;

@@ -330,7 +330,7 @@ extern "C" int vm_conv3d_wgrad_simt(int dtype, const void* x, int64_t x_bstride,
   }
   k_wgrad_finalize<<<grid_for((int64_t)27 * Cin * Cout + Cout, 256), 256, 0, st>>>(
       wsw, wsb, gw, gb, ns, Cin, Cout, CGin, CGout);
-  return launch_status("vm_conv3d_wgrad_simt");
+  return launch_status("vm_conv3d_wgrad_simt", 3);
 }
 
 extern "C" int vm_weight_flip_transpose(const float* w, float* wt, int k, int Cin, int Cout,

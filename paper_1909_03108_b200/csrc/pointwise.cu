@@ -533,5 +533,5 @@ extern "C" int vm_sgd_momentum(float* params, float* moments, const float* grads
   dim3 grid((unsigned)bx, (unsigned)nlayers);
   k_sgd_check<<<grid, 256, 0, st>>>(grads, offsets, flags);
   k_sgd_apply<<<grid, 256, 0, st>>>(params, moments, grads, offsets, flags, lr, momentum);
-  return launch_status("vm_sgd_momentum");
+  return launch_status("vm_sgd_momentum", 2);
 }

@@ -23,7 +23,10 @@ int grid_for(int64_t work, int threads);  // grid-stride grid, capped at 8 x #SM
     }                                \
   } while (0)
 
-inline int launch_status(const char* what) {
+void count_launches(int n);  // bookkeeping for vm_launch_count()
+
+inline int launch_status(const char* what, int nlaunch = 1) {
+  count_launches(nlaunch);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error("%s: %s", what, cudaGetErrorString(e));

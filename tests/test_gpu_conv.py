@@ -1,0 +1,105 @@
+"""tcgen05 conv3d (forward / dgrad operand) vs the CUDA-core kernel and the f64 oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import voxmesh_oracle as O
+from paper_1909_03108_b200 import _lib
+from paper_1909_03108_b200.step import Slab
+from tests.helpers import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [
+    # B, Cin, Cout, D, H, W
+    (1, 16, 16, 16, 16, 16),
+    (1, 1, 16, 16, 16, 16),
+    (1, 48, 16, 12, 16, 16),
+    (2, 32, 64, 8, 12, 16),
+    (1, 64, 128, 8, 8, 8),
+    (1, 128, 64, 8, 8, 8),
+    (1, 16, 48, 16, 20, 24),
+    (1, 24, 8, 6, 6, 6),
+    (1, 16, 16, 32, 32, 128),
+]
+
+
+def _slab_from(x):
+    B, D, H, W, C = x.shape
+    s = Slab(B, C, D, H, W, torch.bfloat16, "cuda")
+    xt = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+    _lib.call("vm_dense_to_slab", _lib.ptr(xt), _lib.VM_F32, s.p(), _lib.VM_BF16, s.bstride, B, C, D, H, W, 1,
+              _lib.stream_ptr())
+    return s
+
+
+def _conv_tc(xs, w, b, cout, flags=_lib.VM_CONV_RELU, mask=None, flip=False):
+    B, D, H, W = xs.B, xs.D, xs.H, xs.W
+    cin_layer, cout_layer = w.shape[3], w.shape[4]
+    cin = xs.C
+    wt = torch.from_numpy(np.ascontiguousarray(w, np.float32)).cuda()
+    nbytes = _lib.call_size("vm_packed_weights_bytes", cin, cout)
+    wp = torch.empty(nbytes // 2, dtype=torch.bfloat16, device="cuda")
+    _lib.call("vm_pack_weights", _lib.ptr(wt), _lib.ptr(wp), cin_layer, cout_layer, int(flip), _lib.stream_ptr())
+    ys = Slab(B, cout, D, H, W, torch.bfloat16, "cuda")
+    bt = torch.from_numpy(np.ascontiguousarray(b, np.float32)).cuda()
+    _lib.call("vm_conv3d_fwd_tc", xs.p(), xs.bstride, _lib.ptr(wp), _lib.ptr(bt), ys.p(), ys.bstride,
+              mask.p() if mask is not None else None, mask.bstride if mask is not None else 0,
+              B, cin, cout, D, H, W, flags, _lib.stream_ptr())
+    return ys
+
+
+def _conv_simt(xs, w, b, cout, flags=_lib.VM_CONV_RELU, mask=None):
+    B, D, H, W = xs.B, xs.D, xs.H, xs.W
+    wt = torch.from_numpy(np.ascontiguousarray(w, np.float32)).cuda()
+    bt = torch.from_numpy(np.ascontiguousarray(b, np.float32)).cuda()
+    ys = Slab(B, cout, D, H, W, torch.bfloat16, "cuda")
+    _lib.call("vm_conv3d_fwd_simt", _lib.VM_BF16, xs.p(), xs.bstride, _lib.ptr(wt), _lib.ptr(bt), ys.p(), ys.bstride,
+              mask.p() if mask is not None else None, mask.bstride if mask is not None else 0,
+              B, xs.C, cout, D, H, W, flags, _lib.stream_ptr())
+    return ys
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_tc_forward_matches_simt_and_oracle(shape):
+    B, cin, cout, D, H, W = shape
+    rng = np.random.default_rng(sum(shape))
+    x = O.bf16_round(rng.standard_normal((B, D, H, W, cin)).astype(np.float32))
+    w = O.bf16_round(rng.uniform(-1, 1, (3, 3, 3, cin, cout)).astype(np.float32) / np.sqrt(27 * cin))
+    b = rng.standard_normal(cout).astype(np.float32) * 0.1
+    xs = _slab_from(x)
+    got = _conv_tc(xs, w, b, cout).interior().cpu().numpy()
+    ref = _conv_simt(xs, w, b, cout).interior().cpu().numpy()
+    assert rel_l2(got, ref) <= 2e-3
+    dense = np.maximum(O.conv3d_dense(x.astype(np.float64), w.astype(np.float64), b.astype(np.float64)), 0)
+    assert rel_l2(got, dense) <= 1e-2
+
+
+def test_tc_forward_keeps_margins_zero():
+    B, cin, cout, D, H, W = 1, 16, 16, 10, 12, 14
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((B, D, H, W, cin)).astype(np.float32)
+    w = rng.uniform(-0.1, 0.1, (3, 3, 3, cin, cout)).astype(np.float32)
+    ys = _conv_tc(_slab_from(x), w, np.ones(cout, np.float32), cout, flags=0)
+    torch.cuda.synchronize()
+    full = ys.storage.float().reshape(B, 2, D + 2, H + 2, W + 2, 8).cpu().numpy()
+    inner = np.zeros_like(full, dtype=bool)
+    inner[:, :, 1:-1, 1:-1, 1:-1] = True
+    assert not full[~inner].any()
+
+
+def test_tc_dgrad_operand_with_relu_mask_matches_oracle_adjoint():
+    # dgrad of conv(x; W) for output gradient g = conv(g_pad; flip(W)^T), masked by y>0
+    B, cin, cout, D, H, W = 1, 32, 16, 8, 10, 12
+    rng = np.random.default_rng(11)
+    g = O.bf16_round(rng.standard_normal((B, D, H, W, cout)).astype(np.float32))
+    w = O.bf16_round(rng.uniform(-1, 1, (3, 3, 3, cin, cout)).astype(np.float32) / 20)
+    m = O.bf16_round(rng.standard_normal((B, D, H, W, cin)).astype(np.float32))
+    gs, ms = _slab_from(g), _slab_from(m)
+    got = _conv_tc(gs, w, np.zeros(cin, np.float32), cin, flags=_lib.VM_CONV_MASK | _lib.VM_CONV_NOBIAS,
+                   mask=ms, flip=True).interior().cpu().numpy()
+    xdummy = np.zeros((B, D, H, W, cin))
+    gx, _, _ = O.conv3d_dense_backward(g.astype(np.float64), xdummy, w.astype(np.float64))
+    ref = np.where(m > 0, gx, 0.0)
+    assert rel_l2(got, ref) <= 1e-2
