@@ -95,7 +95,7 @@ class UNetStep:
 
     def __init__(self, graph, params, batch=1, ctx=None, device=None, dtype=torch.bfloat16,
                  conv_impl="tc", lr=0.003, momentum=0.9, loss_weights=(0.9, 0.1),
-                 dice_classes=(1, 2), clamp=1e-12, global_batch=None):
+                 dice_classes=(1, 2), clamp=1e-12, global_batch=None, global_shape=None, local_shape=None):
         cfg = graph.config
         if cfg.kernel != 3:
             raise GraphBuildError(f"the slab step supports 3x3x3 convolutions, got k={cfg.kernel}")
@@ -127,13 +127,19 @@ class UNetStep:
         self.has_halo = any(lo is not None or hi is not None for lo, hi in self.nbrs.values())
         bdiv = mesh.axis_size(layout.axis_for("batch")) if (layout is not None and layout.axis_for("batch")) else 1
         self.global_batch = global_batch or batch * bdiv
-        self.total_voxels = float(self.global_batch * cfg.input_extent ** 3)
+        E = cfg.input_extent
+        self.global_shape = tuple(global_shape) if global_shape else (E, E, E)
+        # local block of the level-0 volume; deeper levels scale by level_extent / E
+        self.local_shape = tuple(local_shape) if local_shape else tuple(
+            g // d for g, d in zip(self.global_shape, self.div))
+        self.total_voxels = float(self.global_batch * int(np.prod(self.global_shape)))
+        self._rec = None
         self._build_buffers(params)
 
     # ------------------------------------------------------------------ setup
     def _ext(self, nid):
-        e = self.graph.level_extents[nid]
-        return (e // self.div[0], e // self.div[1], e // self.div[2])
+        shrink = self.cfg.input_extent // self.graph.level_extents[nid]
+        return tuple(n // shrink for n in self.local_shape)
 
     def _slab(self, C, ext, parent=None, cg0=0):
         return Slab(self.B, C, *ext, self.dtype, self.device, parent, cg0)
@@ -246,40 +252,55 @@ class UNetStep:
     def _st(self):
         return _lib.stream_ptr()
 
+    def _k(self, kind, label, flops, nbytes, name, *args):
+        """Launch ``name(*args, stream)``; in record mode, log it for per-kernel timing."""
+        if self._rec is not None:
+            self._rec.append((kind, label, flops, nbytes, name, args))
+        _lib.call(name, *args, self._st())
+
     def repack(self):
         """Refresh the derived conv operands from the fp32 master weights."""
-        st = self._st()
         for L in self.layers:
             if L.k != 3:
                 continue
+            nb = 4 * L.nk
             if self.conv_impl == "tc":
-                _lib.call("vm_pack_weights", _lib.ptr(L.w), _lib.ptr(L.wp), L.cin, L.cout, 0, st)
-                _lib.call("vm_pack_weights", _lib.ptr(L.w), _lib.ptr(L.wpt), L.cin, L.cout, 1, st)
+                self._k("pack", L.node.id, 0, nb, "vm_pack_weights", _lib.ptr(L.w), _lib.ptr(L.wp), L.cin, L.cout, 0)
+                self._k("pack", L.node.id, 0, nb, "vm_pack_weights", _lib.ptr(L.w), _lib.ptr(L.wpt), L.cin, L.cout, 1)
             else:
-                _lib.call("vm_weight_flip_transpose", _lib.ptr(L.w), _lib.ptr(L.wt), 3, L.cin, L.cout, st)
+                self._k("pack", L.node.id, 0, nb, "vm_weight_flip_transpose", _lib.ptr(L.w), _lib.ptr(L.wt), 3,
+                        L.cin, L.cout)
+
+    def _conv_flops(self, L):
+        return 2.0 * self.B * L.D * L.H * L.W * 27 * L.cin * L.cout
 
     def _conv(self, x, L, y, flags, mask=None, dgrad=False):
         cin, cout = (L.cout, L.cin) if dgrad else (L.cin, L.cout)
-        st = self._st()
         mp = mask.p() if mask is not None else None
         mb = mask.bstride if mask is not None else 0
+        kind = "conv_dgrad" if dgrad else "conv_fwd"
+        vox = self.B * L.D * L.H * L.W
+        nbytes = 2.0 * vox * (cin + cout + (cout if mask is not None else 0))
         if self.conv_impl == "tc":
             w = L.wpt if dgrad else L.wp
-            _lib.call("vm_conv3d_fwd_tc", x.p(), x.bstride, _lib.ptr(w), _lib.ptr(L.b), y.p(), y.bstride,
-                      mp, mb, self.B, cin, cout, L.D, L.H, L.W, flags, st)
+            self._k(kind, L.node.id, self._conv_flops(L), nbytes, "vm_conv3d_fwd_tc", x.p(), x.bstride,
+                    _lib.ptr(w), _lib.ptr(L.b), y.p(), y.bstride, mp, mb, self.B, cin, cout, L.D, L.H, L.W, flags)
         else:
             w = L.wt if dgrad else L.w
-            _lib.call("vm_conv3d_fwd_simt", self.dt, x.p(), x.bstride, _lib.ptr(w), _lib.ptr(L.b), y.p(),
-                      y.bstride, mp, mb, self.B, cin, cout, L.D, L.H, L.W, flags, st)
+            self._k(kind, L.node.id, self._conv_flops(L), nbytes, "vm_conv3d_fwd_simt", self.dt, x.p(), x.bstride,
+                    _lib.ptr(w), _lib.ptr(L.b), y.p(), y.bstride, mp, mb, self.B, cin, cout, L.D, L.H, L.W, flags)
 
     def _wgrad(self, x, L, g):
-        st = self._st()
+        vox = self.B * L.D * L.H * L.W
+        nbytes = 2.0 * vox * (L.cin + L.cout) + 4.0 * (L.nk + L.cout)
         if self.conv_impl == "tc":
-            _lib.call("vm_conv3d_wgrad_tc", x.p(), x.bstride, g.p(), g.bstride, _lib.ptr(L.gw), _lib.ptr(L.gb),
-                      _lib.ptr(self.wgrad_ws), self.B, L.cin, L.cout, L.D, L.H, L.W, st)
+            self._k("conv_wgrad", L.node.id, self._conv_flops(L), nbytes, "vm_conv3d_wgrad_tc", x.p(), x.bstride,
+                    g.p(), g.bstride, _lib.ptr(L.gw), _lib.ptr(L.gb), _lib.ptr(self.wgrad_ws), self.B, L.cin,
+                    L.cout, L.D, L.H, L.W)
         else:
-            _lib.call("vm_conv3d_wgrad_simt", self.dt, x.p(), x.bstride, g.p(), g.bstride, _lib.ptr(L.gw),
-                      _lib.ptr(L.gb), _lib.ptr(self.wgrad_ws), self.B, L.cin, L.cout, L.D, L.H, L.W, st)
+            self._k("conv_wgrad", L.node.id, self._conv_flops(L), nbytes, "vm_conv3d_wgrad_simt", self.dt, x.p(),
+                    x.bstride, g.p(), g.bstride, _lib.ptr(L.gw), _lib.ptr(L.gb), _lib.ptr(self.wgrad_ws), self.B,
+                    L.cin, L.cout, L.D, L.H, L.W)
 
     def _halo(self, s, tag):
         if not self.has_halo:
@@ -289,10 +310,33 @@ class UNetStep:
         for b in range(self.B):
             run_exchange(self.ctx, s.view5(b), core5, margins5, self.nbrs, s.storage.element_size(), tag)
 
+    def halo_bytes_per_step(self):
+        """Bytes this rank sends per step (3-phase protocol, fwd + bwd, slab channel padding included)."""
+        if not self.has_halo:
+            return 0
+        total = 0
+        for n in self.graph.nodes:
+            if n.op != "conv" or n.k != 3:
+                continue
+            L = self.by_id[n.id]
+            cur = [L.D, L.H, L.W]
+            cg = (L.cin + 7) // 8
+            per = 0
+            for i in range(3):
+                lo, hi = self.nbrs.get(1 + i, (None, None))
+                area = 1
+                for j in range(3):
+                    if j != i:
+                        area *= cur[j]
+                per += area * ((lo is not None) + (hi is not None))
+                cur[i] += 2
+            nbytes = per * cg * 8 * self.B * torch.tensor([], dtype=self.dtype).element_size()
+            total += nbytes * (1 if n.inputs[0] == "input" else 2)
+        return total
+
     def _zero_margins(self, s):
         if not self.has_halo:
             return
-        st = self._st()
         for b in range(self.B):
             v = s.view5(b)
             dims = _lib.i64arr(v.shape)
@@ -302,21 +346,42 @@ class UNetStep:
                     lo5 = [0, 0, 0, 0, 0]
                     ext5 = list(v.shape)
                     lo5[ax], ext5[ax] = lo, 1
-                    _lib.call("vm_box_zero", _lib.ptr(v), dims, v.element_size(), _lib.i64arr(lo5),
-                              _lib.i64arr(ext5), st)
+                    self._k("halo", "zero", 0, 0, "vm_box_zero", _lib.ptr(v), dims, v.element_size(),
+                            _lib.i64arr(lo5), _lib.i64arr(ext5))
 
     # ------------------------------------------------------------------ inputs
     def load_inputs(self, image, onehot):
         """image: device f32 [B,D,H,W,Cin] (local block); onehot: device f32 [B,D,H,W,ncls]."""
-        st = self._st()
         x = self.x_in
-        _lib.call("vm_dense_to_slab", _lib.ptr(image.contiguous()), _lib.VM_F32, x.p(), self.dt, x.bstride,
-                  self.B, x.C, x.D, x.H, x.W, 1, st)
+        self._k("io", "image", 0, 0, "vm_dense_to_slab", _lib.ptr(image.contiguous()), _lib.VM_F32, x.p(), self.dt,
+                x.bstride, self.B, x.C, x.D, x.H, x.W, 1)
         self.onehot.copy_(onehot.reshape(-1))
+
+    def upload(self, image_host, labels_host):
+        """Public-API input path: host f32 image [B,D,H,W,Cin] + u8 labels [B,D,H,W]
+        -> (pinned) H2D -> slab + on-device one-hot (training.py:68-69, :276-279)."""
+        if getattr(self, "_img_dev", None) is None:
+            self._img_dev = torch.empty(tuple(image_host.shape), dtype=torch.float32, device=self.device)
+            self._lab_dev = torch.empty(tuple(labels_host.shape), dtype=torch.uint8, device=self.device)
+        self._img_dev.copy_(image_host, non_blocking=True)
+        self._lab_dev.copy_(labels_host, non_blocking=True)
+        x = self.x_in
+        self._k("io", "image", 0, 0, "vm_dense_to_slab", _lib.ptr(self._img_dev), _lib.VM_F32, x.p(), self.dt,
+                x.bstride, self.B, x.C, x.D, x.H, x.W, 1)
+        self._k("io", "onehot", 0, 0, "vm_onehot_u8", _lib.ptr(self._lab_dev), _lib.ptr(self.onehot), self.nvox,
+                self.ncls)
+
+    def train_step_host(self, image_host, labels_host, replay=None):
+        """One step through the public API: H2D inputs, step (or graph replay), D2H loss."""
+        self.upload(image_host, labels_host)
+        if replay is not None:
+            replay()
+        else:
+            self.step()
+        return self.loss()[0]
 
     # ------------------------------------------------------------------ passes
     def forward(self):
-        st = self._st()
         for n in self.graph.nodes:
             if n.op == "conv" and n.k == 3:
                 x = self.out[n.inputs[0]]
@@ -324,12 +389,14 @@ class UNetStep:
                 self._conv(x, self.by_id[n.id], self.out[n.id], _lib.VM_CONV_RELU)
             elif n.op == "pool":
                 x, y = self.out[n.inputs[0]], self.out[n.id]
-                _lib.call("vm_maxpool2_fwd", self.dt, x.p(), x.bstride, y.p(), y.bstride, self.B, x.C, x.D,
-                          x.H, x.W, st)
+                nb = 2.0 * self.B * x.D * x.H * x.W * x.C * 9 / 8
+                self._k("pool_fwd", n.id, 0, nb, "vm_maxpool2_fwd", self.dt, x.p(), x.bstride, y.p(), y.bstride,
+                        self.B, x.C, x.D, x.H, x.W)
             elif n.op == "up":
                 x, y = self.out[n.inputs[0]], self.out[n.id]
-                _lib.call("vm_upsample2_fwd", self.dt, x.p(), x.bstride, y.p(), y.bstride, self.B, x.C, x.D,
-                          x.H, x.W, st)
+                nb = 2.0 * self.B * x.D * x.H * x.W * x.C * 9
+                self._k("up_fwd", n.id, 0, nb, "vm_upsample2_fwd", self.dt, x.p(), x.bstride, y.p(), y.bstride,
+                        self.B, x.C, x.D, x.H, x.W)
             elif n.op == "concat":
                 c_up, aligned = self.cat_parts[n.id]
                 if not aligned:
@@ -341,27 +408,31 @@ class UNetStep:
             if getattr(self, "probs", None) is None:
                 self.probs = torch.empty(self.nvox * self.ncls, dtype=torch.float32, device=self.device)
             probs = _lib.ptr(self.probs)
-        _lib.call("vm_head_fwd", self.dt, y.p(), y.bstride, _lib.ptr(h.w), _lib.ptr(h.b), _lib.ptr(self.onehot),
-                  probs, _lib.ptr(self.partials), self.B, h.cin, self.ncls, h.D, h.H, h.W, self.clamp, st)
-        _lib.call("vm_reduce_rows", _lib.ptr(self.partials), self.n_part, 3 * self.ncls + 1,
-                  _lib.ptr(self.stats), st)
+        nb = 2.0 * self.nvox * h.cin + 4.0 * self.nvox * self.ncls
+        self._k("head_fwd", "head", 2.0 * self.nvox * h.cin * self.ncls, nb, "vm_head_fwd", self.dt, y.p(), y.bstride,
+                _lib.ptr(h.w), _lib.ptr(h.b), _lib.ptr(self.onehot), probs, _lib.ptr(self.partials), self.B, h.cin,
+                self.ncls, h.D, h.H, h.W, self.clamp)
+        self._k("reduce", "stats", 0, 0, "vm_reduce_rows", _lib.ptr(self.partials), self.n_part, 3 * self.ncls + 1,
+                _lib.ptr(self.stats))
         if self.ctx is not None and self.ctx.mesh.worker_count > 1:
             red = self.ctx.all_reduce_sum(self.stats, tag="loss-stats")
             if red is not self.stats:
                 self.stats.copy_(red)
 
     def backward(self):
-        st = self._st()
         h = self.head
         y = self.out[self.head_in]
         last = self.graph.node(self.head_in)
         last_conv = last.inputs[0] if last.op == "relu" else last.id
         g = self.gpre[last_conv]
-        _lib.call("vm_head_bwd", self.dt, y.p(), y.bstride, _lib.ptr(h.w), _lib.ptr(h.b), _lib.ptr(self.onehot),
-                  _lib.ptr(self.stats), g.p(), g.bstride, _lib.ptr(self.hpartials), self.B, h.cin, self.ncls,
-                  h.D, h.H, h.W, self.w_dice, self.w_ce, self.total_voxels, self.dice_mask, self.clamp, 1, st)
-        _lib.call("vm_reduce_rows", _lib.ptr(self.hpartials), self.n_part, self.hw_width, _lib.ptr(self.hgrad), st)
-        # head grads: [C*ncls] kernel (DHWIO with k=1) then [ncls] bias
+        nb = 4.0 * self.nvox * h.cin + 4.0 * self.nvox * self.ncls
+        self._k("head_bwd", "head", 4.0 * self.nvox * h.cin * self.ncls, nb, "vm_head_bwd", self.dt, y.p(),
+                y.bstride, _lib.ptr(h.w), _lib.ptr(h.b), _lib.ptr(self.onehot), _lib.ptr(self.stats), g.p(), g.bstride,
+                _lib.ptr(self.hpartials), self.B, h.cin, self.ncls, h.D, h.H, h.W, self.w_dice, self.w_ce,
+                self.total_voxels, self.dice_mask, self.clamp, 1)
+        self._k("reduce", "head", 0, 0, "vm_reduce_rows", _lib.ptr(self.hpartials), self.n_part, self.hw_width,
+                _lib.ptr(self.hgrad))
+        # head grads: [C*ncls] kernel (DHWIO with k=1) then [ncls] bias — contiguous in the flat buffer
         h.gw.copy_(self.hgrad[: h.nk])
         h.gb.copy_(self.hgrad[h.nk :])
         for n in reversed(self.graph.nodes):
@@ -390,8 +461,9 @@ class UNetStep:
                 sn = self.graph.node(src)
                 x = self.out[src]
                 dst = self.gpre[sn.inputs[0]]
-                _lib.call("vm_upsample2_bwd", self.dt, gup.p(), gup.bstride, x.p(), x.bstride, dst.p(), dst.bstride,
-                          self.B, x.C, x.D, x.H, x.W, st)
+                nb = 2.0 * self.B * x.D * x.H * x.W * x.C * 10
+                self._k("up_bwd", n.id, 0, nb, "vm_upsample2_bwd", self.dt, gup.p(), gup.bstride, x.p(), x.bstride,
+                        dst.p(), dst.bstride, self.B, x.C, x.D, x.H, x.W)
             elif n.op == "pool":
                 src = n.inputs[0]
                 sn = self.graph.node(src)
@@ -404,9 +476,11 @@ class UNetStep:
                     c_up, aligned = self.cat_parts[cat.id]
                     add = self._window(self.gnode[cat.id], c_up, cat.c_out - c_up, aligned, copy_from=cat.id,
                                        part="skip")
-                _lib.call("vm_maxpool2_bwd", self.dt, x.p(), x.bstride, gpool.p(), gpool.bstride,
-                          add.p() if add else None, add.bstride if add else 0, dst.p(), dst.bstride,
-                          self.B, x.C, x.D, x.H, x.W, 1, st)
+                vin = self.B * x.D * x.H * x.W * x.C
+                nb = 2.0 * vin * (1 + (1 if add else 0) + 1) + 2.0 * vin / 8
+                self._k("pool_bwd", n.id, 0, nb, "vm_maxpool2_bwd", self.dt, x.p(), x.bstride, gpool.p(),
+                        gpool.bstride, add.p() if add else None, add.bstride if add else 0, dst.p(), dst.bstride,
+                        self.B, x.C, x.D, x.H, x.W, 1)
 
     def all_reduce_grads(self):
         if self.ctx is not None and self.ctx.mesh.worker_count > 1:
@@ -415,9 +489,10 @@ class UNetStep:
                 self.grads.copy_(red)
 
     def sgd(self):
-        _lib.call("vm_sgd_momentum", _lib.ptr(self.params), _lib.ptr(self.moments), _lib.ptr(self.grads),
-                  _lib.ptr(self.offsets), len(self.layers), self.max_layer, _lib.ptr(self.skip_flags),
-                  self.lr, self.mu, self._st())
+        n = self.params.numel()
+        self._k("sgd", "all", 0, 20.0 * n, "vm_sgd_momentum", _lib.ptr(self.params), _lib.ptr(self.moments),
+                _lib.ptr(self.grads), _lib.ptr(self.offsets), len(self.layers), self.max_layer,
+                _lib.ptr(self.skip_flags), self.lr, self.mu)
         self.repack()
 
     def step(self):
@@ -426,6 +501,36 @@ class UNetStep:
         self.backward()
         self.all_reduce_grads()
         self.sgd()
+
+    def profile_kernels(self, reps=5):
+        """Per-launch device time of every kernel of one step: each launch is captured
+        alone in a CUDA graph and replayed ``reps`` times between CUDA events."""
+        self._rec = []
+        try:
+            self.step()
+        finally:
+            rec, self._rec = self._rec, None
+        torch.cuda.synchronize()
+        rows = []
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for kind, label, flops, nbytes, name, args in rec:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    for _ in range(reps):
+                        _lib.call(name, *args, self._st())
+                g.replay()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(s)
+                g.replay()
+                e1.record(s)
+                e1.synchronize()
+                rows.append({"kind": kind, "layer": label, "ms": e0.elapsed_time(e1) / reps, "flops": flops,
+                             "bytes": nbytes})
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        return rows
 
     # ------------------------------------------------------------------ helpers
     def _window(self, s, c0, nc, aligned, copy_from=None, part=None):
