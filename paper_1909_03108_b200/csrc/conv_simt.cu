@@ -253,6 +253,35 @@ __global__ void k_flip_transpose(const float* __restrict__ w, float* __restrict_
   }
 }
 
+__global__ void k_bias_finalize(const float* __restrict__ wsb, float* __restrict__ gb, int nsplit,
+                                int Cout, int CGout) {
+  for (int co = blockIdx.x * blockDim.x + threadIdx.x; co < Cout; co += gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int sp = 0; sp < nsplit; ++sp) s += wsb[(int64_t)sp * CGout * 8 + co];
+    gb[co] = s;
+  }
+}
+
+size_t bias_grad_ws_bytes(int64_t nvox, int Cout) {
+  int64_t s = nvox / 16384;
+  if (s < 1) s = 1;
+  if (s > 64) s = 64;
+  return (size_t)s * ((Cout + 7) / 8) * 8 * sizeof(float);
+}
+
+// gb[co] = sum over interior voxels of gy[.., co], deterministic (bf16 slab)
+int bias_grad_bf16(const void* gy, int64_t gy_bstride, float* gb, float* ws, int B, int Cout, int D,
+                   int H, int W, cudaStream_t st) {
+  Slab gg{gy_bstride ? gy_bstride : default_bstride(Cout, D, H, W, 1), (Cout + 7) / 8, D, H, W, 1};
+  int64_t nvox = (int64_t)B * D * H * W;
+  int ns = (int)(bias_grad_ws_bytes(nvox, Cout) / (gg.CG * 8 * sizeof(float)));
+  int64_t chunk = (nvox + ns - 1) / ns;
+  k_bias_grad_partial<__nv_bfloat16><<<dim3(ns, gg.CG), 256, 0, st>>>((const __nv_bfloat16*)gy, gg, ws, B,
+                                                                      gg.CG, chunk);
+  k_bias_finalize<<<1, 128, 0, st>>>(ws, gb, ns, Cout, gg.CG);
+  return launch_status("bias_grad_bf16", 2);
+}
+
 static int wgrad_splits(int64_t nvox, int64_t combos) {
   int64_t s = nvox / 4096;
   if (s < 1) s = 1;

@@ -334,6 +334,187 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc<512>(tbase);
 }
 
+// ------------------------------------------------------------------ weight-gradient kernel
+// Rows of M: 16 channel groups per M-tile, group g = p*CG + cg with p = kd*3 + kh.
+// Each group is staged as its own run of KS+8 rows (the (kd,kh)-shifted input),
+// so consecutive groups sit at a uniform stride (SBO) and the kw shift is a
+// 16-byte start-address offset along K.  B = gy rows (MN-major, co groups).
+constexpr int kWgKS = 64;       // anchors per stage (K of one stage)
+constexpr int kWgRows = kWgKS + 8;
+
+struct WgParams {
+  const bf16* x;
+  int64_t x_bstride;
+  int64_t plane8;   // elements per channel-group plane
+  int B, D, H, W, Hp, Wp, P;
+  int CG, CGo, Cout, Nc;
+  int MT, mt_per_unit, n_mtgroups;
+  int spk;          // stages per unit (K-split chunk)
+  int ksplit;       // K-split chunks per sample
+  int stages_total; // per sample
+  int units;
+  int stages;       // pipeline depth
+  uint32_t a_bytes; // per stage: mt_per_unit*16 groups * kWgRows * 16
+  uint32_t g_bytes; // per stage loaded: CGo * kWgKS * 16 (allocated: Nc/8 groups)
+  uint32_t stage_bytes;
+  uint32_t idesc;
+  float* ws;        // [kidx = b*ksplit + ks][MT][3][Nc][128]
+};
+
+__global__ void __launch_bounds__(192, 1)
+    k_conv_wgrad_tc(const __grid_constant__ CUtensorMap gmap, const WgParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t full[kMaxStages], empty[kMaxStages], tfull, tempty;
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&tfull, 1);
+    mbar_init(&tempty, 128);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tslot;
+  const int ngroups_total = 9 * p.CG;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch(&gmap);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const int mg = u % p.n_mtgroups;
+        const int ks = (u / p.n_mtgroups) % p.ksplit;
+        const int b = u / (p.n_mtgroups * p.ksplit);
+        const int mt0 = mg * p.mt_per_unit;
+        const int nmt = min(p.mt_per_unit, p.MT - mt0);
+        const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
+        for (int s = s0; s < s1; ++s) {
+          const int64_t k0 = (int64_t)s * kWgKS;
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sA = smem + (size_t)stage * p.stage_bytes;
+          uint8_t* sG = sA + p.a_bytes;
+          int nvalid = 0;
+          for (int i = 0; i < nmt * 16; ++i)
+            if ((mt0 * 16 + i) < ngroups_total) ++nvalid;
+          mbar_arrive_expect_tx(&full[stage], (uint32_t)nvalid * kWgRows * 16 + p.g_bytes);
+          for (int i = 0; i < nmt * 16; ++i) {
+            const int g = mt0 * 16 + i;
+            if (g >= ngroups_total) break;
+            const int pp = g / p.CG, cg = g % p.CG;
+            const int kd = pp / 3, kh = pp % 3;
+            const bf16* src = p.x + b * p.x_bstride + cg * p.plane8 + (k0 + (int64_t)kd * p.P + (int64_t)kh * p.Wp) * 8;
+            bulk_load(sA + (size_t)i * kWgRows * 16, src, kWgRows * 16, &full[stage]);
+          }
+          for (int cgo = 0; cgo < p.CGo; ++cgo)
+            tma_load_4d(sG + (size_t)cgo * kWgKS * 16, &gmap, &full[stage], 0,
+                        (int)(k0 + p.P + p.Wp + 1), cgo, b);
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    int stage = 0;
+    uint32_t phase = 0, tph = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const int mg = u % p.n_mtgroups;
+      const int ks = (u / p.n_mtgroups) % p.ksplit;
+      const int mt0 = mg * p.mt_per_unit;
+      const int nmt = min(p.mt_per_unit, p.MT - mt0);
+      const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
+      mbar_wait(&tempty, tph ^ 1);
+      tc_fence_after();
+      for (int s = s0; s < s1; ++s) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes);
+          const uint32_t sG = sA + p.a_bytes;
+#pragma unroll 1
+          for (int kk = 0; kk < kWgKS / 16; ++kk) {
+            const uint64_t bdesc = make_sdesc(sG + kk * 256, 128, kWgKS * 16);
+#pragma unroll 1
+            for (int m = 0; m < nmt; ++m)
+#pragma unroll 1
+              for (int kw = 0; kw < 3; ++kw) {
+                const uint32_t a_addr = sA + (uint32_t)((m * 16) * kWgRows + kk * 16 + kw) * 16;
+                const uint64_t adesc = make_sdesc(a_addr, 128, kWgRows * 16);
+                mma_bf16_ss(tbase + (uint32_t)((m * 3 + kw) * p.Nc), adesc, bdesc, p.idesc,
+                            (s > s0 || kk > 0) ? 1u : 0u);
+              }
+          }
+          mma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == p.stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (elect_one()) mma_commit(&tfull);
+      __syncwarp();
+      tph ^= 1;
+    }
+  } else {
+    const int q = warp & 3;
+    uint32_t tph = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const int mg = u % p.n_mtgroups;
+      const int ks = (u / p.n_mtgroups) % p.ksplit;
+      const int b = u / (p.n_mtgroups * p.ksplit);
+      const int mt0 = mg * p.mt_per_unit;
+      const int nmt = min(p.mt_per_unit, p.MT - mt0);
+      const int kidx = b * p.ksplit + ks;
+      mbar_wait(&tfull, tph);
+      tc_fence_after();
+      const int m_row = q * 32 + lane;
+      for (int m = 0; m < nmt; ++m)
+        for (int kw = 0; kw < 3; ++kw)
+          for (int n0 = 0; n0 < p.Nc; n0 += 8) {
+            uint32_t r[8];
+            tmem_ld8(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)((m * 3 + kw) * p.Nc + n0), r);
+            tmem_ld_wait();
+            float* dst = p.ws + ((((int64_t)kidx * p.MT + mt0 + m) * 3 + kw) * p.Nc + n0) * 128 + m_row;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) dst[e * 128] = __uint_as_float(r[e]);
+          }
+      tc_fence_before();
+      mbar_arrive(&tempty);
+      tph ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tbase);
+}
+
+// gw[t][ci][co] = sum_k ws[k][mt][kw][co][m], t = (kd*3+kh)*3 + kw, g = (kd*3+kh)*CG + ci/8
+__global__ void k_wgrad_tc_finalize(const float* __restrict__ ws, float* __restrict__ gw, int nk, int MT,
+                                    int Nc, int CG, int Cin, int Cout) {
+  const int64_t n = (int64_t)27 * Cin * Cout;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int co = i % Cout;
+    const int ci = (i / Cout) % Cin;
+    const int t = (int)(i / ((int64_t)Cout * Cin));
+    const int pp = t / 3, kw = t % 3;
+    const int g = pp * CG + ci / 8;
+    const int mt = g / 16, m = (g % 16) * 8 + (ci % 8);
+    float s = 0.f;
+    for (int k = 0; k < nk; ++k) s += ws[((((int64_t)k * MT + mt) * 3 + kw) * Nc + co) * 128 + m];
+    gw[i] = s;
+  }
+}
+
 }  // namespace vm
 
 using namespace vm;
@@ -418,15 +599,97 @@ extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wp
   return launch_status("vm_conv3d_fwd_tc");
 }
 
+
+namespace {
+struct WgPlan {
+  WgParams p;
+  size_t ws_main, ws_bias;
+};
+
+int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
+  WgParams& p = pl.p;
+  p = WgParams{};
+  p.B = B;
+  p.D = D;
+  p.H = H;
+  p.W = W;
+  p.Hp = H + 2;
+  p.Wp = W + 2;
+  p.P = p.Hp * p.Wp;
+  p.plane8 = (int64_t)(D + 2) * p.P * 8;
+  p.CG = (Cin + 7) / 8;
+  p.CGo = (Cout + 7) / 8;
+  p.Cout = Cout;
+  p.Nc = (Cout + 15) / 16 * 16;
+  VM_REQUIRE(3 * p.Nc <= 512, VM_E_UNSUPPORTED, "vm_conv3d_wgrad_tc: Cout %d > 160 not supported yet", Cout);
+  p.MT = (9 * p.CG + 15) / 16;
+  p.mt_per_unit = 512 / (3 * p.Nc);
+  if (p.mt_per_unit > p.MT) p.mt_per_unit = p.MT;
+  // stage smem must allow >= 2 stages
+  for (;;) {
+    p.a_bytes = (uint32_t)p.mt_per_unit * 16 * kWgRows * 16;
+    p.g_bytes = (uint32_t)p.CGo * kWgKS * 16;
+    p.stage_bytes = p.a_bytes + (uint32_t)(p.Nc / 8) * kWgKS * 16;
+    p.stages = kSmemBudget / (int)p.stage_bytes;
+    if (p.stages >= 2 || p.mt_per_unit == 1) break;
+    p.mt_per_unit--;
+  }
+  if (p.stages > kMaxStages) p.stages = kMaxStages;
+  VM_REQUIRE(p.stages >= 2, VM_E_UNSUPPORTED, "vm_conv3d_wgrad_tc: stage does not fit");
+  p.n_mtgroups = (p.MT + p.mt_per_unit - 1) / p.mt_per_unit;
+  const int64_t anchors = (int64_t)D * p.P;
+  p.stages_total = (int)((anchors + kWgKS - 1) / kWgKS);
+  int nsm = vm_num_sms(0);
+  if (nsm <= 0) nsm = 148;
+  int want = (2 * nsm + p.n_mtgroups * B - 1) / (p.n_mtgroups * B);  // ~2 units per SM
+  if (want < 1) want = 1;
+  p.spk = (p.stages_total + want - 1) / want;
+  if (p.spk < 4) p.spk = 4;
+  p.ksplit = (p.stages_total + p.spk - 1) / p.spk;
+  p.units = p.n_mtgroups * B * p.ksplit;
+  p.idesc = make_idesc_bf16(128, p.Nc, true, true);
+  pl.ws_main = (size_t)B * p.ksplit * p.MT * 3 * p.Nc * 128 * sizeof(float);
+  pl.ws_bias = bias_grad_ws_bytes((int64_t)B * D * H * W, Cout);
+  return VM_OK;
+}
+}  // namespace
+
 extern "C" size_t vm_conv3d_wgrad_tc_ws(int B, int Cin, int Cout, int D, int H, int W) {
-  return vm_conv3d_wgrad_simt_ws(B, Cin, Cout, D, H, W);
+  WgPlan pl;
+  if (plan_wgrad(B, Cin, Cout, D, H, W, pl) != VM_OK) return 0;
+  return pl.ws_main + pl.ws_bias + 256;
 }
 
 extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* gy,
                                   int64_t gy_bstride, float* gw, float* gb, void* ws, int B, int Cin,
                                   int Cout, int D, int H, int W, void* stream) {
-  // First version: the tensor-core weight-gradient kernel is not written yet; the
-  // bf16 SIMT kernel computes the same quantity on CUDA cores.
-  return vm_conv3d_wgrad_simt(VM_BF16, x, x_bstride, gy, gy_bstride, gw, gb, ws, B, Cin, Cout, D, H,
-                              W, stream);
+  VM_REQUIRE(x && gy && gw && gb && ws, VM_E_ARG, "vm_conv3d_wgrad_tc: null pointer");
+  VM_REQUIRE(B > 0 && Cin > 0 && Cout > 0 && D > 0 && H > 0 && W > 0, VM_E_SHAPE,
+             "vm_conv3d_wgrad_tc: bad shape");
+  WgPlan pl;
+  int rc = plan_wgrad(B, Cin, Cout, D, H, W, pl);
+  if (rc) return rc;
+  WgParams p = pl.p;
+  p.x = static_cast<const bf16*>(x);
+  p.x_bstride = x_bstride ? x_bstride : default_bstride(Cin, D, H, W, 1);
+  p.ws = static_cast<float*>(ws);
+  const int64_t gbs = gy_bstride ? gy_bstride : default_bstride(Cout, D, H, W, 1);
+  const int64_t rows = (int64_t)(D + 2) * p.P;
+  CUtensorMap gmap;
+  rc = make_slab_map(&gmap, gy, gbs, p.CGo, rows, B, kWgKS);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  cudaFuncSetAttribute(k_conv_wgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
+  int nsm = vm_num_sms(0);
+  int grid = p.units < nsm ? p.units : nsm;
+  k_conv_wgrad_tc<<<grid, 192, (size_t)p.stages * p.stage_bytes, st>>>(gmap, p);
+  rc = launch_status("vm_conv3d_wgrad_tc");
+  if (rc) return rc;
+  const int nk = B * p.ksplit;
+  k_wgrad_tc_finalize<<<grid_for((int64_t)27 * Cin * Cout, 256), 256, 0, st>>>(p.ws, gw, nk, p.MT, p.Nc, p.CG,
+                                                                               Cin, Cout);
+  rc = launch_status("vm_conv3d_wgrad_tc finalize");
+  if (rc) return rc;
+  float* wsb = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ((pl.ws_main + 255) / 256) * 256);
+  return bias_grad_bf16(gy, gbs, gb, wsb, B, Cout, D, H, W, st);
 }

@@ -71,6 +71,10 @@ struct Slab {
   }
 };
 
+size_t bias_grad_ws_bytes(int64_t nvox, int Cout);
+int bias_grad_bf16(const void* gy, int64_t gy_bstride, float* gb, float* ws, int B, int Cout, int D,
+                   int H, int W, cudaStream_t st);
+
 inline int64_t default_bstride(int C, int D, int H, int W, int m) {
   return (int64_t)((C + 7) / 8) * (D + 2 * m) * (H + 2 * m) * (W + 2 * m) * 8;
 }

@@ -36,13 +36,17 @@ _DT = {torch.bfloat16: _lib.VM_BF16, torch.float32: _lib.VM_F32}
 class Slab:
     """Channel-blocked padded buffer; may be a channel-group window of a wider slab."""
 
+    TAIL = 64 * 1024  # elements
+
     def __init__(self, B, C, D, H, W, dtype, device, parent=None, cg0=0):
         self.B, self.C, self.D, self.H, self.W = B, C, D, H, W
         self.CG = (C + 7) // 8
         self.dtype = dtype
         self.plane = (D + 2) * (H + 2) * (W + 2) * 8
         if parent is None:
-            self.storage = torch.zeros(B * self.CG * self.plane, dtype=dtype, device=device)
+            # + tail pad: the tensor-core kernels bulk-copy whole row runs and may read
+            # (and discard) up to a few thousand rows past the last plane
+            self.storage = torch.zeros(B * self.CG * self.plane + self.TAIL, dtype=dtype, device=device)
             self.bstride = self.CG * self.plane
             self.offset = 0
         else:

@@ -83,7 +83,7 @@ def test_tc_forward_keeps_margins_zero():
     w = rng.uniform(-0.1, 0.1, (3, 3, 3, cin, cout)).astype(np.float32)
     ys = _conv_tc(_slab_from(x), w, np.ones(cout, np.float32), cout, flags=0)
     torch.cuda.synchronize()
-    full = ys.storage.float().reshape(B, 2, D + 2, H + 2, W + 2, 8).cpu().numpy()
+    full = ys.storage[: B * 2 * ys.plane].float().reshape(B, 2, D + 2, H + 2, W + 2, 8).cpu().numpy()
     inner = np.zeros_like(full, dtype=bool)
     inner[:, :, 1:-1, 1:-1, 1:-1] = True
     assert not full[~inner].any()
@@ -103,3 +103,49 @@ def test_tc_dgrad_operand_with_relu_mask_matches_oracle_adjoint():
     gx, _, _ = O.conv3d_dense_backward(g.astype(np.float64), xdummy, w.astype(np.float64))
     ref = np.where(m > 0, gx, 0.0)
     assert rel_l2(got, ref) <= 1e-2
+
+
+WG_SHAPES = [
+    (1, 16, 16, 16, 16, 16),
+    (1, 1, 16, 16, 16, 16),
+    (1, 48, 16, 12, 16, 16),
+    (2, 32, 64, 8, 12, 16),
+    (1, 64, 128, 8, 8, 8),
+    (1, 128, 64, 8, 8, 8),
+    (1, 16, 48, 16, 20, 24),
+    (1, 24, 8, 6, 6, 6),
+]
+
+
+def _wgrad(fn, xs, gs, cin, cout):
+    B, D, H, W = xs.B, xs.D, xs.H, xs.W
+    gw = torch.zeros(27 * cin * cout, dtype=torch.float32, device="cuda")
+    gb = torch.zeros(cout, dtype=torch.float32, device="cuda")
+    if fn == "vm_conv3d_wgrad_tc":
+        nb = _lib.call_size("vm_conv3d_wgrad_tc_ws", B, cin, cout, D, H, W)
+        ws = torch.empty(nb // 4 + 64, dtype=torch.float32, device="cuda")
+        _lib.call(fn, xs.p(), xs.bstride, gs.p(), gs.bstride, _lib.ptr(gw), _lib.ptr(gb), _lib.ptr(ws),
+                  B, cin, cout, D, H, W, _lib.stream_ptr())
+    else:
+        nb = _lib.call_size("vm_conv3d_wgrad_simt_ws", B, cin, cout, D, H, W)
+        ws = torch.empty(nb // 4 + 64, dtype=torch.float32, device="cuda")
+        _lib.call(fn, _lib.VM_BF16, xs.p(), xs.bstride, gs.p(), gs.bstride, _lib.ptr(gw), _lib.ptr(gb),
+                  _lib.ptr(ws), B, cin, cout, D, H, W, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    return gw.cpu().numpy().reshape(3, 3, 3, cin, cout), gb.cpu().numpy()
+
+
+@pytest.mark.parametrize("shape", WG_SHAPES)
+def test_tc_wgrad_matches_simt_and_oracle(shape):
+    B, cin, cout, D, H, W = shape
+    rng = np.random.default_rng(100 + sum(shape))
+    x = O.bf16_round(rng.standard_normal((B, D, H, W, cin)).astype(np.float32))
+    g = O.bf16_round(rng.standard_normal((B, D, H, W, cout)).astype(np.float32))
+    xs, gs = _slab_from(x), _slab_from(g)
+    gw, gb = _wgrad("vm_conv3d_wgrad_tc", xs, gs, cin, cout)
+    sw, sb = _wgrad("vm_conv3d_wgrad_simt", xs, gs, cin, cout)
+    assert rel_l2(gw, sw) <= 1e-5 and rel_l2(gb, sb) <= 1e-5
+    _, rgk, rgb = O.conv3d_dense_backward(g.astype(np.float64), x.astype(np.float64),
+                                           np.zeros((3, 3, 3, cin, cout)))
+    assert rel_l2(gw, rgk) <= 1e-5
+    assert rel_l2(gb, rgb) <= 1e-5
