@@ -263,9 +263,9 @@ __global__ void k_bias_finalize(const float* __restrict__ wsb, float* __restrict
 }
 
 size_t bias_grad_ws_bytes(int64_t nvox, int Cout) {
-  int64_t s = nvox / 16384;
+  int64_t s = nvox / 4096;  // ~16 voxels per thread per block
   if (s < 1) s = 1;
-  if (s > 64) s = 64;
+  if (s > 512) s = 512;
   return (size_t)s * ((Cout + 7) / 8) * 8 * sizeof(float);
 }
 

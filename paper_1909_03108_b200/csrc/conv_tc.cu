@@ -141,6 +141,9 @@ __global__ void k_pack_weights(const float* __restrict__ w, bf16* __restrict__ o
 
 // ------------------------------------------------------------------ forward kernel
 struct FwdParams {
+  const bf16* x;
+  int64_t x_bstride;
+  int R;             // staged rows per group per stage (MB*128 + 2*Wp + 2)
   const bf16* wpk;
   const float* bias;
   bf16* y;
@@ -164,7 +167,7 @@ struct FwdParams {
 };
 
 __global__ void __launch_bounds__(192, 1)
-    k_conv_fwd_tc(const __grid_constant__ CUtensorMap xmap, const FwdParams p) {
+    k_conv_fwd_tc(const FwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
   __shared__ uint32_t tslot;
@@ -190,7 +193,6 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (elect_one()) {
-      tma_prefetch(&xmap);
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
@@ -204,11 +206,12 @@ __global__ void __launch_bounds__(192, 1)
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* sA = smem + (size_t)stage * p.stage_bytes;
             uint8_t* sB = sA + 2 * p.a_bytes;
-            mbar_arrive_expect_tx(&full[stage], ng * p.a_bytes + p.b_bytes);
+            mbar_arrive_expect_tx(&full[stage], (uint32_t)ng * p.R * 16 + p.b_bytes);
+            // one bulk copy per 8-channel group: the run of R consecutive rows of plane kd
             for (int g = 0; g < ng; ++g)
-              for (int rb = 0; rb < p.Ralloc; rb += kBoxR)
-                tma_load_4d(sA + (size_t)g * p.a_bytes + (size_t)rb * 16, &xmap, &full[stage], 0,
-                            (int)(a0 + (int64_t)kd * p.P + rb), kc * 2 + g, b);
+              bulk_load(sA + (size_t)g * p.a_bytes,
+                        p.x + b * p.x_bstride + (kc * 2 + g) * p.plane8 + (a0 + (int64_t)kd * p.P) * 8,
+                        (uint32_t)p.R * 16, &full[stage]);
             const bf16* src = p.wpk + (((int64_t)nch * p.KC + kc) * 3 + kd) * (p.b_bytes / 2);
             bulk_load(sB, src, p.b_bytes, &full[stage]);
             if (++stage == p.stages) {
@@ -282,41 +285,56 @@ __global__ void __launch_bounds__(192, 1)
         const int hq = (int)((a / p.Wp) % p.Hp);
         const bool valid = a < p.anchors && wq < p.W && hq < p.H;
         const int64_t orow = a + p.P + p.Wp + 1;
-        for (int g = 0; g * 8 < p.Nc; ++g) {
-          uint32_t r[8];
-          tmem_ld8(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * p.MB + i) * p.Nc + g * 8), r);
-          tmem_ld_wait();
-          const int co0 = nch * p.Nc + g * 8;
-          if (valid && co0 < p.Cout) {
-            float v[8];
-  #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              v[e] = __uint_as_float(r[e]);
-              if (!(p.flags & VM_CONV_NOBIAS) && co0 + e < p.Cout) v[e] += p.bias[co0 + e];
+        const int ng_out = p.Nc / 8;
+        for (int g0 = 0; g0 < ng_out; g0 += 8) {
+          const int gn = min(8, ng_out - g0);
+          int4 mk[8];
+          if (p.flags & VM_CONV_MASK) {  // issue all mask loads first (latency overlap)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int co0 = nch * p.Nc + (g0 + j) * 8;
+              mk[j] = make_int4(0, 0, 0, 0);
+              if (j < gn && valid && co0 < p.Cout)
+                mk[j] = *reinterpret_cast<const int4*>(p.mask + b * p.m_bstride + (co0 / 8) * p.plane8 + orow * 8);
             }
-            if (p.flags & VM_CONV_RELU) {
-  #pragma unroll
-              for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
-            }
-            const int cg = co0 / 8;
-            if (p.flags & VM_CONV_MASK) {
-              int4 mraw = *reinterpret_cast<const int4*>(p.mask + b * p.m_bstride + cg * p.plane8 + orow * 8);
-              const __nv_bfloat162* mh = reinterpret_cast<const __nv_bfloat162*>(&mraw);
-  #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                float2 f = __bfloat1622float2(mh[e]);
-                if (!(f.x > 0.f)) v[2 * e] = 0.f;
-                if (!(f.y > 0.f)) v[2 * e + 1] = 0.f;
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (j >= gn) break;
+            const int g = g0 + j;
+            uint32_t r[8];
+            tmem_ld8(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * p.MB + i) * p.Nc + g * 8), r);
+            tmem_ld_wait();
+            const int co0 = nch * p.Nc + g * 8;
+            if (valid && co0 < p.Cout) {
+              float v[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                v[e] = __uint_as_float(r[e]);
+                if (!(p.flags & VM_CONV_NOBIAS) && co0 + e < p.Cout) v[e] += p.bias[co0 + e];
               }
+              if (p.flags & VM_CONV_RELU) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
+              }
+              if (p.flags & VM_CONV_MASK) {
+                const __nv_bfloat162* mh = reinterpret_cast<const __nv_bfloat162*>(&mk[j]);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  float2 f = __bfloat1622float2(mh[e]);
+                  if (!(f.x > 0.f)) v[2 * e] = 0.f;
+                  if (!(f.y > 0.f)) v[2 * e + 1] = 0.f;
+                }
+              }
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                if (co0 + e >= p.Cout) v[e] = 0.f;
+              int4 out;
+              __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&out);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) oh[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+              *reinterpret_cast<int4*>(p.y + b * p.y_bstride + (co0 / 8) * p.plane8 + orow * 8) = out;
             }
-  #pragma unroll
-            for (int e = 0; e < 8; ++e)
-              if (co0 + e >= p.Cout) v[e] = 0.f;
-            int4 out;
-            __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&out);
-  #pragma unroll
-            for (int e = 0; e < 4; ++e) oh[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
-            *reinterpret_cast<int4*>(p.y + b * p.y_bstride + cg * p.plane8 + orow * 8) = out;
           }
         }
       }
@@ -336,26 +354,30 @@ __global__ void __launch_bounds__(192, 1)
 
 // ------------------------------------------------------------------ weight-gradient kernel
 // Rows of M: 16 channel groups per M-tile, group g = p*CG + cg with p = kd*3 + kh.
-// Each group is staged as its own run of KS+8 rows (the (kd,kh)-shifted input),
-// so consecutive groups sit at a uniform stride (SBO) and the kw shift is a
-// 16-byte start-address offset along K.  B = gy rows (MN-major, co groups).
-constexpr int kWgKS = 64;       // anchors per stage (K of one stage)
-constexpr int kWgRows = kWgKS + 8;
-
+// Each group is staged by one bulk copy as its own run of KS+8 rows (the
+// (kd,kh)-shifted input), so consecutive groups sit at a uniform stride (SBO)
+// and the kw shift is a 16-byte start-address offset along K.  B = gy rows
+// (MN-major, co groups) fetched by ONE 128B-inner TMA box per stage.  A spare
+// M slot (when 9*CG is not a multiple of 16) holds a block of ones, so the same
+// MMAs also produce the bias gradient sum_v gy[v][co].
 struct WgParams {
   const bf16* x;
   int64_t x_bstride;
   int64_t plane8;   // elements per channel-group plane
   int B, D, H, W, Hp, Wp, P;
   int CG, CGo, Cout, Nc;
+  int KS, RR;       // anchors per stage, staged rows per group (KS + 8)
+  int gdelta;       // row misalignment of the gy box start (128B-inner mode)
+  int gwide;        // 1: gy map has 128-byte inner boxes
   int MT, mt_per_unit, n_mtgroups;
+  int ones_slot;    // absolute M slot of the ones block, -1 if none
   int spk;          // stages per unit (K-split chunk)
   int ksplit;       // K-split chunks per sample
   int stages_total; // per sample
   int units;
   int stages;       // pipeline depth
-  uint32_t a_bytes; // per stage: mt_per_unit*16 groups * kWgRows * 16
-  uint32_t g_bytes; // per stage loaded: CGo * kWgKS * 16 (allocated: Nc/8 groups)
+  uint32_t a_bytes; // per stage: mt_per_unit*16 slots * RR * 16
+  uint32_t g_bytes; // per stage loaded: CGo * RR * 16 (allocated: Nc/8 groups)
   uint32_t stage_bytes;
   uint32_t idesc;
   float* ws;        // [kidx = b*ksplit + ks][MT][3][Nc][128]
@@ -367,6 +389,19 @@ __global__ void __launch_bounds__(192, 1)
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages], tfull, tempty;
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int mg_cta = blockIdx.x % p.n_mtgroups;  // every unit of this CTA has the same M-tile group
+  const int mt0 = mg_cta * p.mt_per_unit;
+  const int nmt = min(p.mt_per_unit, p.MT - mt0);
+  // ones block for the bias gradient, written once into every stage buffer
+  if (p.ones_slot >= 0 && p.ones_slot / 16 >= mt0 && p.ones_slot / 16 < mt0 + nmt) {
+    const int local = p.ones_slot - mt0 * 16;
+    const uint32_t one2 = 0x3F803F80u;  // two bf16 1.0
+    for (int s = 0; s < p.stages; ++s) {
+      uint32_t* dst = reinterpret_cast<uint32_t*>(smem + (size_t)s * p.stage_bytes + (size_t)local * p.RR * 16);
+      for (int i = threadIdx.x; i < p.RR * 4; i += blockDim.x) dst[i] = one2;
+    }
+  }
+  fence_proxy_async_smem();
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
@@ -388,33 +423,34 @@ __global__ void __launch_bounds__(192, 1)
       tma_prefetch(&gmap);
       int stage = 0;
       uint32_t phase = 0;
+      int nvalid = 0;
+      for (int i = 0; i < nmt * 16; ++i)
+        if (mt0 * 16 + i < ngroups_total) ++nvalid;
+      const uint32_t tx = (uint32_t)nvalid * p.RR * 16 + p.g_bytes;
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        const int mg = u % p.n_mtgroups;
         const int ks = (u / p.n_mtgroups) % p.ksplit;
         const int b = u / (p.n_mtgroups * p.ksplit);
-        const int mt0 = mg * p.mt_per_unit;
-        const int nmt = min(p.mt_per_unit, p.MT - mt0);
         const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
+        const bf16* xb = p.x + b * p.x_bstride;
         for (int s = s0; s < s1; ++s) {
-          const int64_t k0 = (int64_t)s * kWgKS;
+          const int64_t k0 = (int64_t)s * p.KS;
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = smem + (size_t)stage * p.stage_bytes;
           uint8_t* sG = sA + p.a_bytes;
-          int nvalid = 0;
-          for (int i = 0; i < nmt * 16; ++i)
-            if ((mt0 * 16 + i) < ngroups_total) ++nvalid;
-          mbar_arrive_expect_tx(&full[stage], (uint32_t)nvalid * kWgRows * 16 + p.g_bytes);
+          mbar_arrive_expect_tx(&full[stage], tx);
+          const int gr0 = (int)(k0 + p.P + p.Wp + 1);
+          if (p.gwide)
+            tma_load_4d(sG, &gmap, &full[stage], 0, (gr0 - p.gdelta) >> 3, 0, b);
+          else
+            tma_load_4d(sG, &gmap, &full[stage], 0, gr0, 0, b);
           for (int i = 0; i < nmt * 16; ++i) {
             const int g = mt0 * 16 + i;
             if (g >= ngroups_total) break;
             const int pp = g / p.CG, cg = g % p.CG;
             const int kd = pp / 3, kh = pp % 3;
-            const bf16* src = p.x + b * p.x_bstride + cg * p.plane8 + (k0 + (int64_t)kd * p.P + (int64_t)kh * p.Wp) * 8;
-            bulk_load(sA + (size_t)i * kWgRows * 16, src, kWgRows * 16, &full[stage]);
+            const bf16* src = xb + cg * p.plane8 + (k0 + (int64_t)kd * p.P + (int64_t)kh * p.Wp) * 8;
+            bulk_load(sA + (size_t)i * p.RR * 16, src, p.RR * 16, &full[stage]);
           }
-          for (int cgo = 0; cgo < p.CGo; ++cgo)
-            tma_load_4d(sG + (size_t)cgo * kWgKS * 16, &gmap, &full[stage], 0,
-                        (int)(k0 + p.P + p.Wp + 1), cgo, b);
           if (++stage == p.stages) {
             stage = 0;
             phase ^= 1;
@@ -425,11 +461,9 @@ __global__ void __launch_bounds__(192, 1)
   } else if (warp == 1) {
     int stage = 0;
     uint32_t phase = 0, tph = 0;
+    const uint32_t sbo = (uint32_t)p.RR * 16;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      const int mg = u % p.n_mtgroups;
       const int ks = (u / p.n_mtgroups) % p.ksplit;
-      const int mt0 = mg * p.mt_per_unit;
-      const int nmt = min(p.mt_per_unit, p.MT - mt0);
       const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
       mbar_wait(&tempty, tph ^ 1);
       tc_fence_after();
@@ -440,16 +474,15 @@ __global__ void __launch_bounds__(192, 1)
           const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes);
           const uint32_t sG = sA + p.a_bytes;
 #pragma unroll 1
-          for (int kk = 0; kk < kWgKS / 16; ++kk) {
-            const uint64_t bdesc = make_sdesc(sG + kk * 256, 128, kWgKS * 16);
+          for (int kk = 0; kk < p.KS / 16; ++kk) {
+            const uint64_t bdesc = make_sdesc(sG + (uint32_t)(p.gdelta + kk * 16) * 16, 128, sbo);
 #pragma unroll 1
             for (int m = 0; m < nmt; ++m)
-#pragma unroll 1
+#pragma unroll
               for (int kw = 0; kw < 3; ++kw) {
-                const uint32_t a_addr = sA + (uint32_t)((m * 16) * kWgRows + kk * 16 + kw) * 16;
-                const uint64_t adesc = make_sdesc(a_addr, 128, kWgRows * 16);
-                mma_bf16_ss(tbase + (uint32_t)((m * 3 + kw) * p.Nc), adesc, bdesc, p.idesc,
-                            (s > s0 || kk > 0) ? 1u : 0u);
+                const uint32_t a_addr = sA + (uint32_t)((m * 16) * p.RR + kk * 16 + kw) * 16;
+                mma_bf16_ss(tbase + (uint32_t)((m * 3 + kw) * p.Nc), make_sdesc(a_addr, 128, sbo), bdesc,
+                            p.idesc, (s > s0 || kk > 0) ? 1u : 0u);
               }
           }
           mma_commit(&empty[stage]);
@@ -468,11 +501,8 @@ __global__ void __launch_bounds__(192, 1)
     const int q = warp & 3;
     uint32_t tph = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      const int mg = u % p.n_mtgroups;
       const int ks = (u / p.n_mtgroups) % p.ksplit;
       const int b = u / (p.n_mtgroups * p.ksplit);
-      const int mt0 = mg * p.mt_per_unit;
-      const int nmt = min(p.mt_per_unit, p.MT - mt0);
       const int kidx = b * p.ksplit + ks;
       mbar_wait(&tfull, tph);
       tc_fence_after();
@@ -497,21 +527,42 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc<512>(tbase);
 }
 
-// gw[t][ci][co] = sum_k ws[k][mt][kw][co][m], t = (kd*3+kh)*3 + kw, g = (kd*3+kh)*CG + ci/8
-__global__ void k_wgrad_tc_finalize(const float* __restrict__ ws, float* __restrict__ gw, int nk, int MT,
-                                    int Nc, int CG, int Cin, int Cout) {
-  const int64_t n = (int64_t)27 * Cin * Cout;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int co = i % Cout;
-    const int ci = (i / Cout) % Cin;
-    const int t = (int)(i / ((int64_t)Cout * Cin));
-    const int pp = t / 3, kw = t % 3;
-    const int g = pp * CG + ci / 8;
-    const int mt = g / 16, m = (g % 16) * 8 + (ci % 8);
+// gw[t][ci][co] = sum_k ws[k][mt][kw][co][m], t = (kd*3+kh)*3 + kw, g = (kd*3+kh)*CG + ci/8;
+// gb[co] from the ones slot (kw = 0).  One warp per output, lanes split the K partials.
+__global__ void k_wgrad_tc_finalize(const float* __restrict__ ws, float* __restrict__ gw,
+                                    float* __restrict__ gb, int nk, int MT, int Nc, int CG, int Cin,
+                                    int Cout, int ones_slot) {
+  const int64_t n = (int64_t)27 * Cin * Cout + (ones_slot >= 0 ? Cout : 0);
+  const int lane = threadIdx.x % 32;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+  const int64_t nw = (int64_t)gridDim.x * blockDim.x / 32;
+  for (int64_t i = wid; i < n; i += nw) {
+    int mt, m, kw, co;
+    if (i < (int64_t)27 * Cin * Cout) {
+      co = i % Cout;
+      const int ci = (i / Cout) % Cin;
+      const int t = (int)(i / ((int64_t)Cout * Cin));
+      const int pp = t / 3;
+      kw = t % 3;
+      const int g = pp * CG + ci / 8;
+      mt = g / 16;
+      m = (g % 16) * 8 + (ci % 8);
+    } else {
+      co = (int)(i - (int64_t)27 * Cin * Cout);
+      mt = ones_slot / 16;
+      m = (ones_slot % 16) * 8;
+      kw = 0;
+    }
     float s = 0.f;
-    for (int k = 0; k < nk; ++k) s += ws[((((int64_t)k * MT + mt) * 3 + kw) * Nc + co) * 128 + m];
-    gw[i] = s;
+    for (int k = lane; k < nk; k += 32) s += ws[((((int64_t)k * MT + mt) * 3 + kw) * Nc + co) * 128 + m];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      if (i < (int64_t)27 * Cin * Cout)
+        gw[i] = s;
+      else
+        gb[co] = s;
+    }
   }
 }
 
@@ -568,13 +619,16 @@ extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wp
   p.b_bytes = 9 * 2 * p.Nc * 16;
   const int tiles = (int)((p.anchors + 127) / 128);
   // accumulators: 2 buffers x MB x Nc fp32 columns <= 512
+  int nsm = vm_num_sms(0);
+  if (nsm <= 0) nsm = 148;
   int MB = 256 / p.Nc;
   if (MB > 8) MB = 8;
-  if (MB > tiles) MB = tiles;
+  const int mb_fill = (int)((int64_t)tiles * B * p.nchunk / nsm);  // keep >= 1 unit per SM
+  if (MB > mb_fill) MB = mb_fill;
   if (MB < 1) MB = 1;
   for (;;) {
-    const int R = MB * 128 + 2 * p.Wp + 2;
-    p.Ralloc = (R + kBoxR - 1) / kBoxR * kBoxR;
+    p.R = MB * 128 + 2 * p.Wp + 2;
+    p.Ralloc = (p.R + 7) / 8 * 8;
     p.a_bytes = (uint32_t)p.Ralloc * 16;
     p.stage_bytes = 2 * p.a_bytes + p.b_bytes;
     p.stages = kSmemBudget / (int)p.stage_bytes;
@@ -587,15 +641,15 @@ extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wp
   p.mblocks = (tiles + MB - 1) / MB;
   p.units = B * p.mblocks * p.nchunk;
   p.idesc = make_idesc_bf16(128, p.Nc, false, false);
-  CUtensorMap xmap;
-  int64_t xb = x_bstride ? x_bstride : default_bstride(Cin, D, H, W, 1);
-  int rc = make_slab_map(&xmap, x, xb, p.CG, rows, B, kBoxR);
-  if (rc) return rc;
+  p.x = static_cast<const bf16*>(x);
+  p.x_bstride = x_bstride ? x_bstride : default_bstride(Cin, D, H, W, 1);
+  VM_REQUIRE((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (p.x_bstride & 7) == 0, VM_E_ALIGN,
+             "vm_conv3d_fwd_tc: slab must be 16-byte aligned");
+  (void)rows;
   const size_t smem = (size_t)p.stages * p.stage_bytes;
   cudaFuncSetAttribute(k_conv_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
-  int nsm = vm_num_sms(0);
   int grid = p.units < nsm ? p.units : nsm;
-  k_conv_fwd_tc<<<grid, 192, smem, as_stream(stream)>>>(xmap, p);
+  k_conv_fwd_tc<<<grid, 192, smem, as_stream(stream)>>>(p);
   return launch_status("vm_conv3d_fwd_tc");
 }
 
@@ -616,29 +670,40 @@ int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
   p.Hp = H + 2;
   p.Wp = W + 2;
   p.P = p.Hp * p.Wp;
-  p.plane8 = (int64_t)(D + 2) * p.P * 8;
+  const int64_t rows = (int64_t)(D + 2) * p.P;
+  p.plane8 = rows * 8;
   p.CG = (Cin + 7) / 8;
   p.CGo = (Cout + 7) / 8;
   p.Cout = Cout;
   p.Nc = (Cout + 15) / 16 * 16;
   VM_REQUIRE(3 * p.Nc <= 512, VM_E_UNSUPPORTED, "vm_conv3d_wgrad_tc: Cout %d > 160 not supported yet", Cout);
   p.MT = (9 * p.CG + 15) / 16;
+  p.ones_slot = (9 * p.CG) % 16 ? 9 * p.CG : -1;
+  p.gwide = rows % 8 == 0 ? 1 : 0;
+  p.gdelta = p.gwide ? (int)((p.P + p.Wp + 1) & 7) : 0;
   p.mt_per_unit = 512 / (3 * p.Nc);
   if (p.mt_per_unit > p.MT) p.mt_per_unit = p.MT;
-  // stage smem must allow >= 2 stages
-  for (;;) {
-    p.a_bytes = (uint32_t)p.mt_per_unit * 16 * kWgRows * 16;
-    p.g_bytes = (uint32_t)p.CGo * kWgKS * 16;
-    p.stage_bytes = p.a_bytes + (uint32_t)(p.Nc / 8) * kWgKS * 16;
-    p.stages = kSmemBudget / (int)p.stage_bytes;
-    if (p.stages >= 2 || p.mt_per_unit == 1) break;
-    p.mt_per_unit--;
+  // largest K chunk whose double-buffered stage fits; fewer M-tiles per unit if needed
+  const int ks_opts[4] = {256, 192, 128, 64};
+  p.stages = 0;
+  for (; p.mt_per_unit >= 1 && p.stages < 2; --p.mt_per_unit) {
+    for (int ko = 0; ko < 4; ++ko) {
+      p.KS = ks_opts[ko];
+      if (!p.gwide && p.KS + 8 > 256) continue;  // 16B-inner box height limit
+      p.RR = p.KS + 8;
+      p.a_bytes = (uint32_t)p.mt_per_unit * 16 * p.RR * 16;
+      p.g_bytes = (uint32_t)p.CGo * p.RR * 16;
+      p.stage_bytes = p.a_bytes + (uint32_t)(p.Nc / 8) * p.RR * 16;
+      p.stages = kSmemBudget / (int)p.stage_bytes;
+      if (p.stages >= 2) break;
+    }
+    if (p.stages >= 2) break;
   }
   if (p.stages > kMaxStages) p.stages = kMaxStages;
-  VM_REQUIRE(p.stages >= 2, VM_E_UNSUPPORTED, "vm_conv3d_wgrad_tc: stage does not fit");
+  VM_REQUIRE(p.stages >= 2 && p.mt_per_unit >= 1, VM_E_UNSUPPORTED, "vm_conv3d_wgrad_tc: stage does not fit");
   p.n_mtgroups = (p.MT + p.mt_per_unit - 1) / p.mt_per_unit;
   const int64_t anchors = (int64_t)D * p.P;
-  p.stages_total = (int)((anchors + kWgKS - 1) / kWgKS);
+  p.stages_total = (int)((anchors + p.KS - 1) / p.KS);
   int nsm = vm_num_sms(0);
   if (nsm <= 0) nsm = 148;
   int want = (2 * nsm + p.n_mtgroups * B - 1) / (p.n_mtgroups * B);  // ~2 units per SM
@@ -649,7 +714,39 @@ int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
   p.units = p.n_mtgroups * B * p.ksplit;
   p.idesc = make_idesc_bf16(128, p.Nc, true, true);
   pl.ws_main = (size_t)B * p.ksplit * p.MT * 3 * p.Nc * 128 * sizeof(float);
-  pl.ws_bias = bias_grad_ws_bytes((int64_t)B * D * H * W, Cout);
+  pl.ws_bias = p.ones_slot >= 0 ? 0 : bias_grad_ws_bytes((int64_t)B * D * H * W, Cout);
+  return VM_OK;
+}
+
+// 4-D gy map with 128-byte inner boxes: (64 = 8 rows x 8 ch, rows/8, CG, B)
+int make_wide_map(CUtensorMap* m, const void* base, int64_t bstride, int CG, int64_t rows, int B,
+                  int box_blocks, int box_groups) {
+  auto enc = encode_fn();
+  VM_REQUIRE(enc, VM_E_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+  VM_REQUIRE((reinterpret_cast<uintptr_t>(base) & 15) == 0, VM_E_ALIGN, "slab base not 16B aligned");
+  cuuint64_t dims[4] = {64, (cuuint64_t)(rows / 8), (cuuint64_t)CG, (cuuint64_t)B};
+  cuuint64_t strides[3] = {128, (cuuint64_t)rows * 16, (cuuint64_t)bstride * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)box_blocks, (cuuint32_t)box_groups, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
+                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  VM_REQUIRE(r == CUDA_SUCCESS, VM_E_UNSUPPORTED, "cuTensorMapEncodeTiled (wide) failed (%d)", (int)r);
+  return VM_OK;
+}
+
+int make_group_map(CUtensorMap* m, const void* base, int64_t bstride, int CG, int64_t rows, int B,
+                   int box_rows, int box_groups) {
+  auto enc = encode_fn();
+  VM_REQUIRE(enc, VM_E_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[4] = {8, (cuuint64_t)rows, (cuuint64_t)CG, (cuuint64_t)B};
+  cuuint64_t strides[3] = {16, (cuuint64_t)rows * 16, (cuuint64_t)bstride * 2};
+  cuuint32_t box[4] = {8, (cuuint32_t)box_rows, (cuuint32_t)box_groups, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
+                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  VM_REQUIRE(r == CUDA_SUCCESS, VM_E_UNSUPPORTED, "cuTensorMapEncodeTiled (group) failed (%d)", (int)r);
   return VM_OK;
 }
 }  // namespace
@@ -676,20 +773,24 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
   const int64_t gbs = gy_bstride ? gy_bstride : default_bstride(Cout, D, H, W, 1);
   const int64_t rows = (int64_t)(D + 2) * p.P;
   CUtensorMap gmap;
-  rc = make_slab_map(&gmap, gy, gbs, p.CGo, rows, B, kWgKS);
+  rc = p.gwide ? make_wide_map(&gmap, gy, gbs, p.CGo, rows, B, p.RR / 8, p.CGo)
+               : make_group_map(&gmap, gy, gbs, p.CGo, rows, B, p.RR, p.CGo);
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
   cudaFuncSetAttribute(k_conv_wgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
   int nsm = vm_num_sms(0);
-  int grid = p.units < nsm ? p.units : nsm;
+  int grid = p.units;
+  if (grid > nsm) grid = (nsm / p.n_mtgroups) * p.n_mtgroups;  // CTA keeps one M-tile group
+  if (grid < p.n_mtgroups) grid = p.n_mtgroups;
   k_conv_wgrad_tc<<<grid, 192, (size_t)p.stages * p.stage_bytes, st>>>(gmap, p);
   rc = launch_status("vm_conv3d_wgrad_tc");
   if (rc) return rc;
   const int nk = B * p.ksplit;
-  k_wgrad_tc_finalize<<<grid_for((int64_t)27 * Cin * Cout, 256), 256, 0, st>>>(p.ws, gw, nk, p.MT, p.Nc, p.CG,
-                                                                               Cin, Cout);
+  const int64_t nout = (int64_t)27 * Cin * Cout + (p.ones_slot >= 0 ? Cout : 0);
+  k_wgrad_tc_finalize<<<grid_for(nout * 32, 256), 256, 0, st>>>(p.ws, gw, gb, nk, p.MT, p.Nc, p.CG, Cin,
+                                                                 Cout, p.ones_slot);
   rc = launch_status("vm_conv3d_wgrad_tc finalize");
-  if (rc) return rc;
+  if (rc || p.ones_slot >= 0) return rc;
   float* wsb = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ((pl.ws_main + 255) / 256) * 256);
   return bias_grad_bf16(gy, gbs, gb, wsb, B, Cout, D, H, W, st);
 }
