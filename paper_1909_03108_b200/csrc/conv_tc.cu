@@ -240,15 +240,20 @@ __global__ void __launch_bounds__(192, 1)
           const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes);
           const uint32_t sB = sA + 2 * p.a_bytes;
           const uint32_t lbo_a = ng == 2 ? p.a_bytes : 0;
+          // descriptors advance by plain adds on the 16-byte address field
+          const uint64_t a0desc = make_sdesc(sA, lbo_a, 128);
+          const uint64_t b0desc = make_sdesc(sB, p.Nc * 16, 128);
+          const uint32_t d0 = tbase + (uint32_t)(ab * p.MB * p.Nc);
+          const uint32_t bstep = (uint32_t)(2 * p.Nc * 16) >> 4;
 #pragma unroll 1
           for (int j = 0; j < 9; ++j) {
-            const uint64_t bdesc = make_sdesc(sB + j * (2 * p.Nc * 16), p.Nc * 16, 128);
-            const int roff = (j / 3) * p.Wp + (j % 3);
-#pragma unroll 1
-            for (int i = 0; i < p.MB; ++i) {
-              const uint64_t adesc = make_sdesc(sA + (uint32_t)(i * 128 + roff) * 16, lbo_a, 128);
-              mma_bf16_ss(tbase + (uint32_t)((ab * p.MB + i) * p.Nc), adesc, bdesc, p.idesc,
-                          (s > 0 || j > 0) ? 1u : 0u);
+            const uint64_t bdesc = b0desc + (uint64_t)(j * bstep);
+            const uint64_t adesc = a0desc + (uint64_t)((j / 3) * p.Wp + (j % 3));
+            const uint32_t acc = (s > 0 || j > 0) ? 1u : 0u;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (i < p.MB)
+                mma_bf16_ss(d0 + (uint32_t)(i * p.Nc), adesc + (uint64_t)(i * 128), bdesc, p.idesc, acc);
             }
           }
           mma_commit(&empty[stage]);
@@ -473,17 +478,21 @@ __global__ void __launch_bounds__(192, 1)
         if (elect_one()) {
           const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes);
           const uint32_t sG = sA + p.a_bytes;
+          const uint64_t b0desc = make_sdesc(sG + (uint32_t)p.gdelta * 16, 128, sbo);
+          const uint64_t a0desc = make_sdesc(sA, 128, sbo);
+          const uint32_t mstep = (uint32_t)(16 * p.RR);  // 16 groups of RR rows, in 16-byte units
 #pragma unroll 1
           for (int kk = 0; kk < p.KS / 16; ++kk) {
-            const uint64_t bdesc = make_sdesc(sG + (uint32_t)(p.gdelta + kk * 16) * 16, 128, sbo);
+            const uint64_t bdesc = b0desc + (uint64_t)(kk * 16);
+            const uint32_t acc = (s > s0 || kk > 0) ? 1u : 0u;
 #pragma unroll 1
-            for (int m = 0; m < nmt; ++m)
-#pragma unroll
-              for (int kw = 0; kw < 3; ++kw) {
-                const uint32_t a_addr = sA + (uint32_t)((m * 16) * p.RR + kk * 16 + kw) * 16;
-                mma_bf16_ss(tbase + (uint32_t)((m * 3 + kw) * p.Nc), make_sdesc(a_addr, 128, sbo), bdesc,
-                            p.idesc, (s > s0 || kk > 0) ? 1u : 0u);
-              }
+            for (int m = 0; m < nmt; ++m) {
+              const uint64_t adesc = a0desc + (uint64_t)(m * mstep + kk * 16);
+              const uint32_t d = tbase + (uint32_t)(m * 3 * p.Nc);
+              mma_bf16_ss(d, adesc, bdesc, p.idesc, acc);
+              mma_bf16_ss(d + p.Nc, adesc + 1, bdesc, p.idesc, acc);
+              mma_bf16_ss(d + 2 * p.Nc, adesc + 2, bdesc, p.idesc, acc);
+            }
           }
           mma_commit(&empty[stage]);
         }
@@ -527,41 +536,31 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc<512>(tbase);
 }
 
-// gw[t][ci][co] = sum_k ws[k][mt][kw][co][m], t = (kd*3+kh)*3 + kw, g = (kd*3+kh)*CG + ci/8;
-// gb[co] from the ones slot (kw = 0).  One warp per output, lanes split the K partials.
+// Fixed-order reduction of the K-split partials, one thread per partial element
+// (coalesced over m): ws[k][mt][kw][co][m] -> gw[t][ci][co] with t = (kd*3+kh)*3 + kw,
+// g = mt*16 + m/8 = (kd*3+kh)*CG + ci/8; the ones slot (kw = 0, m%8 = 0) gives gb.
 __global__ void k_wgrad_tc_finalize(const float* __restrict__ ws, float* __restrict__ gw,
                                     float* __restrict__ gb, int nk, int MT, int Nc, int CG, int Cin,
                                     int Cout, int ones_slot) {
-  const int64_t n = (int64_t)27 * Cin * Cout + (ones_slot >= 0 ? Cout : 0);
-  const int lane = threadIdx.x % 32;
-  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
-  const int64_t nw = (int64_t)gridDim.x * blockDim.x / 32;
-  for (int64_t i = wid; i < n; i += nw) {
-    int mt, m, kw, co;
-    if (i < (int64_t)27 * Cin * Cout) {
-      co = i % Cout;
-      const int ci = (i / Cout) % Cin;
-      const int t = (int)(i / ((int64_t)Cout * Cin));
-      const int pp = t / 3;
-      kw = t % 3;
-      const int g = pp * CG + ci / 8;
-      mt = g / 16;
-      m = (g % 16) * 8 + (ci % 8);
-    } else {
-      co = (int)(i - (int64_t)27 * Cin * Cout);
-      mt = ones_slot / 16;
-      m = (ones_slot % 16) * 8;
-      kw = 0;
-    }
+  const int64_t E = (int64_t)MT * 3 * Nc * 128;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int m = e % 128;
+    const int co = (e / 128) % Nc;
+    const int kw = (e / (128 * Nc)) % 3;
+    const int mt = (int)(e / (384LL * Nc));
+    const int g = mt * 16 + m / 8;
+    if (co >= Cout) continue;
+    const bool is_w = g < 9 * CG && (g % CG) * 8 + m % 8 < Cin;
+    const bool is_b = g == ones_slot && kw == 0 && m % 8 == 0;
+    if (!is_w && !is_b) continue;
     float s = 0.f;
-    for (int k = lane; k < nk; k += 32) s += ws[((((int64_t)k * MT + mt) * 3 + kw) * Nc + co) * 128 + m];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) {
-      if (i < (int64_t)27 * Cin * Cout)
-        gw[i] = s;
-      else
-        gb[co] = s;
+    for (int k = 0; k < nk; ++k) s += ws[k * E + e];
+    if (is_w) {
+      const int pp = g / CG, ci = (g % CG) * 8 + m % 8;
+      gw[((int64_t)(pp * 3 + kw) * Cin + ci) * Cout + co] = s;
+    } else {
+      gb[co] = s;
     }
   }
 }
@@ -683,22 +682,39 @@ int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
   p.gdelta = p.gwide ? (int)((p.P + p.Wp + 1) & 7) : 0;
   p.mt_per_unit = 512 / (3 * p.Nc);
   if (p.mt_per_unit > p.MT) p.mt_per_unit = p.MT;
-  // largest K chunk whose double-buffered stage fits; fewer M-tiles per unit if needed
+  // pick (M-tiles per unit, K chunk) minimising a per-anchor cost model:
+  // stage = max(MMA cycles, TMA cycles) with SS-MMA cost max(N/2, 32 + N/4) cycles
+  // and ~70 cycles + bytes/100 per TMA request (tools/probes measurements)
   const int ks_opts[4] = {256, 192, 128, 64};
-  p.stages = 0;
-  for (; p.mt_per_unit >= 1 && p.stages < 2; --p.mt_per_unit) {
+  const int mpu_max = p.mt_per_unit;
+  double best = 1e30;
+  int best_mpu = 0, best_ks = 0;
+  for (int mpu = 1; mpu <= mpu_max; ++mpu) {
     for (int ko = 0; ko < 4; ++ko) {
-      p.KS = ks_opts[ko];
-      if (!p.gwide && p.KS + 8 > 256) continue;  // 16B-inner box height limit
-      p.RR = p.KS + 8;
-      p.a_bytes = (uint32_t)p.mt_per_unit * 16 * p.RR * 16;
-      p.g_bytes = (uint32_t)p.CGo * p.RR * 16;
-      p.stage_bytes = p.a_bytes + (uint32_t)(p.Nc / 8) * p.RR * 16;
-      p.stages = kSmemBudget / (int)p.stage_bytes;
-      if (p.stages >= 2) break;
+      const int KS = ks_opts[ko], RR = KS + 8;
+      if (!p.gwide && RR > 256) continue;
+      const uint32_t stage = (uint32_t)mpu * 16 * RR * 16 + (uint32_t)(p.Nc / 8) * RR * 16;
+      if (kSmemBudget / (int)stage < 2) continue;
+      const double mma_cyc = (double)mpu * 3 * (KS / 16) * fmax(p.Nc / 2.0, 32.0 + p.Nc / 4.0);
+      const int groups = min(mpu * 16, 9 * p.CG);
+      const double tma_cyc = groups * (70.0 + RR * 16 / 100.0) + (70.0 + p.CGo * RR * 16 / 100.0);
+      const int ngrp = (p.MT + mpu - 1) / mpu;
+      const double cost = ngrp * fmax(mma_cyc, tma_cyc) / KS;
+      if (cost < best * 0.999) {
+        best = cost;
+        best_mpu = mpu;
+        best_ks = KS;
+      }
     }
-    if (p.stages >= 2) break;
   }
+  VM_REQUIRE(best_mpu > 0, VM_E_UNSUPPORTED, "vm_conv3d_wgrad_tc: no stage configuration fits");
+  p.mt_per_unit = best_mpu;
+  p.KS = best_ks;
+  p.RR = p.KS + 8;
+  p.a_bytes = (uint32_t)p.mt_per_unit * 16 * p.RR * 16;
+  p.g_bytes = (uint32_t)p.CGo * p.RR * 16;
+  p.stage_bytes = p.a_bytes + (uint32_t)(p.Nc / 8) * p.RR * 16;
+  p.stages = kSmemBudget / (int)p.stage_bytes;
   if (p.stages > kMaxStages) p.stages = kMaxStages;
   VM_REQUIRE(p.stages >= 2 && p.mt_per_unit >= 1, VM_E_UNSUPPORTED, "vm_conv3d_wgrad_tc: stage does not fit");
   p.n_mtgroups = (p.MT + p.mt_per_unit - 1) / p.mt_per_unit;
@@ -786,9 +802,9 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
   rc = launch_status("vm_conv3d_wgrad_tc");
   if (rc) return rc;
   const int nk = B * p.ksplit;
-  const int64_t nout = (int64_t)27 * Cin * Cout + (p.ones_slot >= 0 ? Cout : 0);
-  k_wgrad_tc_finalize<<<grid_for(nout * 32, 256), 256, 0, st>>>(p.ws, gw, gb, nk, p.MT, p.Nc, p.CG, Cin,
-                                                                 Cout, p.ones_slot);
+  const int64_t E = (int64_t)p.MT * 3 * p.Nc * 128;
+  k_wgrad_tc_finalize<<<grid_for(E, 256), 256, 0, st>>>(p.ws, gw, gb, nk, p.MT, p.Nc, p.CG, Cin, Cout,
+                                                         p.ones_slot);
   rc = launch_status("vm_conv3d_wgrad_tc finalize");
   if (rc || p.ones_slot >= 0) return rc;
   float* wsb = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ((pl.ws_main + 255) / 256) * 256);
