@@ -164,11 +164,14 @@ struct FwdParams {
   uint32_t stage_bytes;
   uint32_t idesc;
   unsigned flags;
+  long long* dbg;  // optional timing probes [gridDim][4]
+  uint32_t wp_magic, hp_magic;  // floor(2^32 / d) + 1 for the anchor (w, h) split
 };
 
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     k_conv_fwd_tc(const FwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ float sbias[1024];
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -179,7 +182,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 128);
+      mbar_init(&tempty[b], 256);
     }
     fence_barrier_init();
   }
@@ -224,17 +227,22 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
+    long long t_wait_tmem = 0, t_wait_full = 0, t_start = clock64();
     int stage = 0;
     uint32_t phase = 0;
     int ab = 0;
     uint32_t aphase = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      long long tw0 = clock64();
       mbar_wait(&tempty[ab], aphase ^ 1);
+      t_wait_tmem += clock64() - tw0;
       tc_fence_after();
       for (int s = 0; s < nstage_k; ++s) {
         const int kc = s / 3;
         const int ng = (kc * 2 + 1 < p.CG) ? 2 : 1;
+        long long tf0 = clock64();
         mbar_wait(&full[stage], phase);
+        t_wait_full += clock64() - tf0;
         tc_fence_after();
         if (elect_one()) {
           const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes);
@@ -271,59 +279,92 @@ __global__ void __launch_bounds__(192, 1)
         aphase ^= 1;
       }
     }
+    if (p.dbg && lane == 0) {
+      p.dbg[blockIdx.x * 4 + 0] = clock64() - t_start;
+      p.dbg[blockIdx.x * 4 + 1] = t_wait_tmem;
+      p.dbg[blockIdx.x * 4 + 2] = t_wait_full;
+    }
   } else {
-    // ===================== epilogue (warps 2..5) =====================
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    // ===================== epilogue (warps 2..9) =====================
+    // warp w drains TMEM lane quarter (w & 3) of every other tile (parity (w-2)/4)
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int et = threadIdx.x - 64;  // 0..255
+    if (!(p.flags & VM_CONV_NOBIAS))
+      for (int c = et; c < p.Cout; c += 256) sbias[c] = p.bias[c];
+    asm volatile("bar.sync 1, 256;" ::: "memory");
     int ab = 0;
     uint32_t aphase = 0;
-    const int ngroups = min(p.Nc, p.Cout) / 8;  // channel groups stored per chunk (upper bound)
+    long long t_epi_wait = 0;
+    const int ng_out = p.Nc / 8;
+    const bool domask = p.flags & VM_CONV_MASK;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       const int nch = u % p.nchunk;
       const int mb = (u / p.nchunk) % p.mblocks;
       const int b = u / (p.nchunk * p.mblocks);
-      const int64_t a0 = (int64_t)mb * p.MB * 128;
+      const int a0 = mb * p.MB * 128;
+      const bf16* mbase = p.mask + b * p.m_bstride;
+      bf16* ybase = p.y + b * p.y_bstride;
+      long long te0 = clock64();
       mbar_wait(&tfull[ab], aphase);
+      t_epi_wait += clock64() - te0;
       tc_fence_after();
-      for (int i = 0; i < p.MB; ++i) {
-        const int64_t a = a0 + i * 128 + q * 32 + lane;
-        const int wq = (int)(a % p.Wp);
-        const int hq = (int)((a / p.Wp) % p.Hp);
+      for (int i = half; i < p.MB; i += 2) {
+        const int a = a0 + i * 128 + q * 32 + lane;
+        // (w, h) of the anchor via multiply-high division (divisors are small)
+        uint32_t qa = __umulhi((uint32_t)a, p.wp_magic);
+        if (qa * (uint32_t)p.Wp > (uint32_t)a) --qa;
+        if ((qa + 1) * (uint32_t)p.Wp <= (uint32_t)a) ++qa;
+        const int wq = a - (int)qa * p.Wp;
+        uint32_t qh = __umulhi(qa, p.hp_magic);
+        if (qh * (uint32_t)p.Hp > qa) --qh;
+        if ((qh + 1) * (uint32_t)p.Hp <= qa) ++qh;
+        const int hq = (int)qa - (int)qh * p.Hp;
         const bool valid = a < p.anchors && wq < p.W && hq < p.H;
-        const int64_t orow = a + p.P + p.Wp + 1;
-        const int ng_out = p.Nc / 8;
+        const int64_t orow = (int64_t)a + p.P + p.Wp + 1;
+        const uint32_t tcol = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * p.MB + i) * p.Nc);
         for (int g0 = 0; g0 < ng_out; g0 += 8) {
           const int gn = min(8, ng_out - g0);
           int4 mk[8];
-          if (p.flags & VM_CONV_MASK) {  // issue all mask loads first (latency overlap)
+          if (domask) {  // issue the mask loads first (latency overlap)
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const int co0 = nch * p.Nc + (g0 + j) * 8;
               mk[j] = make_int4(0, 0, 0, 0);
               if (j < gn && valid && co0 < p.Cout)
-                mk[j] = *reinterpret_cast<const int4*>(p.mask + b * p.m_bstride + (co0 / 8) * p.plane8 + orow * 8);
+                mk[j] = __ldg(reinterpret_cast<const int4*>(mbase + (co0 / 8) * p.plane8 + orow * 8));
             }
           }
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
+          for (int j = 0; j < 8; j += 2) {
             if (j >= gn) break;
-            const int g = g0 + j;
-            uint32_t r[8];
-            tmem_ld8(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * p.MB + i) * p.Nc + g * 8), r);
+            uint32_t r[16];
+            if (j + 1 < gn) {
+              tmem_ld16(tcol + (uint32_t)((g0 + j) * 8), r);
+            } else {
+              uint32_t r8[8];
+              tmem_ld8(tcol + (uint32_t)((g0 + j) * 8), r8);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) r[e] = r8[e];
+            }
             tmem_ld_wait();
-            const int co0 = nch * p.Nc + g * 8;
-            if (valid && co0 < p.Cout) {
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+              if (j + jj >= gn) break;
+              const int co0 = nch * p.Nc + (g0 + j + jj) * 8;
+              if (!valid || co0 >= p.Cout) continue;
               float v[8];
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
-                v[e] = __uint_as_float(r[e]);
-                if (!(p.flags & VM_CONV_NOBIAS) && co0 + e < p.Cout) v[e] += p.bias[co0 + e];
+                v[e] = __uint_as_float(r[jj * 8 + e]);
+                if (!(p.flags & VM_CONV_NOBIAS)) v[e] += (co0 + e < p.Cout) ? sbias[co0 + e] : 0.f;
               }
               if (p.flags & VM_CONV_RELU) {
 #pragma unroll
                 for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
               }
-              if (p.flags & VM_CONV_MASK) {
-                const __nv_bfloat162* mh = reinterpret_cast<const __nv_bfloat162*>(&mk[j]);
+              if (domask) {
+                const __nv_bfloat162* mh = reinterpret_cast<const __nv_bfloat162*>(&mk[j + jj]);
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                   float2 f = __bfloat1622float2(mh[e]);
@@ -338,7 +379,7 @@ __global__ void __launch_bounds__(192, 1)
               __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&out);
 #pragma unroll
               for (int e = 0; e < 4; ++e) oh[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
-              *reinterpret_cast<int4*>(p.y + b * p.y_bstride + (co0 / 8) * p.plane8 + orow * 8) = out;
+              *reinterpret_cast<int4*>(ybase + (co0 / 8) * p.plane8 + orow * 8) = out;
             }
           }
         }
@@ -350,7 +391,7 @@ __global__ void __launch_bounds__(192, 1)
         aphase ^= 1;
       }
     }
-    (void)ngroups;
+    if (p.dbg && threadIdx.x == 64) p.dbg[blockIdx.x * 4 + 3] = t_epi_wait;
   }
   tc_fence_before();
   __syncthreads();
@@ -582,6 +623,9 @@ extern "C" int vm_pack_weights(const float* w, void* packed, int Cin, int Cout, 
   return launch_status("vm_pack_weights");
 }
 
+static long long* g_fwd_dbg = nullptr;
+extern "C" void vm_debug_set_fwd_probe(long long* buf) { g_fwd_dbg = buf; }
+
 extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wpacked,
                                 const float* bias, void* y, int64_t y_bstride, const void* mask,
                                 int64_t mask_bstride, int B, int Cin, int Cout, int D, int H, int W,
@@ -615,6 +659,10 @@ extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wp
   p.Nc = pg.Nc;
   p.nchunk = pg.nchunk;
   p.flags = flags;
+  p.dbg = g_fwd_dbg;
+  p.wp_magic = (uint32_t)(0x100000000ULL / (uint64_t)(W + 2)) + 1;
+  p.hp_magic = (uint32_t)(0x100000000ULL / (uint64_t)(H + 2)) + 1;
+  VM_REQUIRE(Cout <= 1024, VM_E_UNSUPPORTED, "vm_conv3d_fwd_tc: Cout %d > 1024", Cout);
   p.b_bytes = 9 * 2 * p.Nc * 16;
   const int tiles = (int)((p.anchors + 127) / 128);
   // accumulators: 2 buffers x MB x Nc fp32 columns <= 512
@@ -648,7 +696,7 @@ extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wp
   const size_t smem = (size_t)p.stages * p.stage_bytes;
   cudaFuncSetAttribute(k_conv_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
   int grid = p.units < nsm ? p.units : nsm;
-  k_conv_fwd_tc<<<grid, 192, smem, as_stream(stream)>>>(p);
+  k_conv_fwd_tc<<<grid, 320, smem, as_stream(stream)>>>(p);
   return launch_status("vm_conv3d_fwd_tc");
 }
 
