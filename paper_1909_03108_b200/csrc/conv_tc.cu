@@ -417,6 +417,9 @@ struct WgParams {
   int gwide;        // 1: gy map has 128-byte inner boxes
   int MT, mt_per_unit, n_mtgroups;
   int ones_slot;    // absolute M slot of the ones block, -1 if none
+  int runs;         // 1: stage one run of KS+2Wp+2 rows per (kd, cg) serving all three kh
+                    //    (M slot g' = (kd*CG + cg)*3 + kh, slot stride Wp rows); 0: one copy per slot
+  int runs_alloc;   // run slots per stage buffer (runs mode)
   int spk;          // stages per unit (K-split chunk)
   int ksplit;       // K-split chunks per sample
   int stages_total; // per sample
@@ -439,12 +442,16 @@ __global__ void __launch_bounds__(192, 1)
   const int mt0 = mg_cta * p.mt_per_unit;
   const int nmt = min(p.mt_per_unit, p.MT - mt0);
   // ones block for the bias gradient, written once into every stage buffer
+  // slot geometry: slot i of this CTA's M-tiles sits at (i + slot_shift) * GS bytes
+  const int r0 = p.runs ? (16 * mt0) / 3 : 0;
+  const int slot_shift = p.runs ? 16 * mt0 - 3 * r0 : 0;
+  const uint32_t GS = (uint32_t)(p.runs ? p.Wp : p.RR) * 16;
   if (p.ones_slot >= 0 && p.ones_slot / 16 >= mt0 && p.ones_slot / 16 < mt0 + nmt) {
-    const int local = p.ones_slot - mt0 * 16;
+    const int local = p.ones_slot - mt0 * 16 + slot_shift;
     const uint32_t one2 = 0x3F803F80u;  // two bf16 1.0
     for (int s = 0; s < p.stages; ++s) {
-      uint32_t* dst = reinterpret_cast<uint32_t*>(smem + (size_t)s * p.stage_bytes + (size_t)local * p.RR * 16);
-      for (int i = threadIdx.x; i < p.RR * 4; i += blockDim.x) dst[i] = one2;
+      uint32_t* dst = reinterpret_cast<uint32_t*>(smem + (size_t)s * p.stage_bytes + (size_t)local * GS);
+      for (int i = threadIdx.x; i < (p.KS + 8) * 4; i += blockDim.x) dst[i] = one2;
     }
   }
   fence_proxy_async_smem();
@@ -470,9 +477,15 @@ __global__ void __launch_bounds__(192, 1)
       int stage = 0;
       uint32_t phase = 0;
       int nvalid = 0;
-      for (int i = 0; i < nmt * 16; ++i)
-        if (mt0 * 16 + i < ngroups_total) ++nvalid;
-      const uint32_t tx = (uint32_t)nvalid * p.RR * 16 + p.g_bytes;
+      const int r_end = min(3 * p.CG - 1, (16 * (mt0 + nmt) - 1) / 3);  // last valid run (runs mode)
+      const int Rrun = p.KS + 2 * p.Wp + 2;
+      if (p.runs) {
+        nvalid = r_end >= r0 ? r_end - r0 + 1 : 0;
+      } else {
+        for (int i = 0; i < nmt * 16; ++i)
+          if (mt0 * 16 + i < ngroups_total) ++nvalid;
+      }
+      const uint32_t tx = (uint32_t)nvalid * (p.runs ? Rrun : p.RR) * 16 + p.g_bytes;
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
         const int ks = (u / p.n_mtgroups) % p.ksplit;
         const int b = u / (p.n_mtgroups * p.ksplit);
@@ -489,13 +502,21 @@ __global__ void __launch_bounds__(192, 1)
             tma_load_4d(sG, &gmap, &full[stage], 0, (gr0 - p.gdelta) >> 3, 0, b);
           else
             tma_load_4d(sG, &gmap, &full[stage], 0, gr0, 0, b);
-          for (int i = 0; i < nmt * 16; ++i) {
-            const int g = mt0 * 16 + i;
-            if (g >= ngroups_total) break;
-            const int pp = g / p.CG, cg = g % p.CG;
-            const int kd = pp / 3, kh = pp % 3;
-            const bf16* src = xb + cg * p.plane8 + (k0 + (int64_t)kd * p.P + (int64_t)kh * p.Wp) * 8;
-            bulk_load(sA + (size_t)i * p.RR * 16, src, p.RR * 16, &full[stage]);
+          if (p.runs) {
+            for (int r = r0; r <= r_end; ++r) {
+              const int kd = r / p.CG, cg = r % p.CG;
+              const bf16* src = xb + cg * p.plane8 + (k0 + (int64_t)kd * p.P) * 8;
+              bulk_load(sA + (size_t)(r - r0) * 3 * GS, src, (uint32_t)Rrun * 16, &full[stage]);
+            }
+          } else {
+            for (int i = 0; i < nmt * 16; ++i) {
+              const int g = mt0 * 16 + i;
+              if (g >= ngroups_total) break;
+              const int pp = g / p.CG, cg = g % p.CG;
+              const int kd = pp / 3, kh = pp % 3;
+              const bf16* src = xb + cg * p.plane8 + (k0 + (int64_t)kd * p.P + (int64_t)kh * p.Wp) * 8;
+              bulk_load(sA + (size_t)i * p.RR * 16, src, p.RR * 16, &full[stage]);
+            }
           }
           if (++stage == p.stages) {
             stage = 0;
@@ -507,7 +528,7 @@ __global__ void __launch_bounds__(192, 1)
   } else if (warp == 1) {
     int stage = 0;
     uint32_t phase = 0, tph = 0;
-    const uint32_t sbo = (uint32_t)p.RR * 16;
+    const uint32_t sbo = GS;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       const int ks = (u / p.n_mtgroups) % p.ksplit;
       const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
@@ -519,9 +540,9 @@ __global__ void __launch_bounds__(192, 1)
         if (elect_one()) {
           const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes);
           const uint32_t sG = sA + p.a_bytes;
-          const uint64_t b0desc = make_sdesc(sG + (uint32_t)p.gdelta * 16, 128, sbo);
-          const uint64_t a0desc = make_sdesc(sA, 128, sbo);
-          const uint32_t mstep = (uint32_t)(16 * p.RR);  // 16 groups of RR rows, in 16-byte units
+          const uint64_t b0desc = make_sdesc(sG + (uint32_t)p.gdelta * 16, 128, (uint32_t)p.RR * 16);
+          const uint64_t a0desc = make_sdesc(sA + (uint32_t)slot_shift * GS, 128, sbo);
+          const uint32_t mstep = 16 * (GS >> 4);  // 16 slots, in 16-byte units
 #pragma unroll 1
           for (int kk = 0; kk < p.KS / 16; ++kk) {
             const uint64_t bdesc = b0desc + (uint64_t)(kk * 16);
@@ -582,7 +603,7 @@ __global__ void __launch_bounds__(192, 1)
 // g = mt*16 + m/8 = (kd*3+kh)*CG + ci/8; the ones slot (kw = 0, m%8 = 0) gives gb.
 __global__ void k_wgrad_tc_finalize(const float* __restrict__ ws, float* __restrict__ gw,
                                     float* __restrict__ gb, int nk, int MT, int Nc, int CG, int Cin,
-                                    int Cout, int ones_slot) {
+                                    int Cout, int ones_slot, int runs) {
   const int64_t E = (int64_t)MT * 3 * Nc * 128;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -592,13 +613,16 @@ __global__ void k_wgrad_tc_finalize(const float* __restrict__ ws, float* __restr
     const int mt = (int)(e / (384LL * Nc));
     const int g = mt * 16 + m / 8;
     if (co >= Cout) continue;
-    const bool is_w = g < 9 * CG && (g % CG) * 8 + m % 8 < Cin;
+    // slot -> (kd*3 + kh, channel group)
+    const int pp = runs ? ((g / 3) / CG) * 3 + g % 3 : g / CG;
+    const int cgi = runs ? (g / 3) % CG : g % CG;
+    const bool is_w = g < 9 * CG && cgi * 8 + m % 8 < Cin;
     const bool is_b = g == ones_slot && kw == 0 && m % 8 == 0;
     if (!is_w && !is_b) continue;
     float s = 0.f;
     for (int k = 0; k < nk; ++k) s += ws[k * E + e];
     if (is_w) {
-      const int pp = g / CG, ci = (g % CG) * 8 + m % 8;
+      const int ci = cgi * 8 + m % 8;
       gw[((int64_t)(pp * 3 + kw) * Cin + ci) * Cout + co] = s;
     } else {
       gb[co] = s;
@@ -707,6 +731,8 @@ struct WgPlan {
   size_t ws_main, ws_bias;
 };
 
+int g_force_runs = -1, g_force_ks = 0, g_force_mpu = 0;
+
 int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
   WgParams& p = pl.p;
   p = WgParams{};
@@ -730,38 +756,50 @@ int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
   p.gdelta = p.gwide ? (int)((p.P + p.Wp + 1) & 7) : 0;
   p.mt_per_unit = 512 / (3 * p.Nc);
   if (p.mt_per_unit > p.MT) p.mt_per_unit = p.MT;
-  // pick (M-tiles per unit, K chunk) minimising a per-anchor cost model:
-  // stage = max(MMA cycles, TMA cycles) with SS-MMA cost max(N/2, 32 + N/4) cycles
-  // and ~70 cycles + bytes/100 per TMA request (tools/probes measurements)
+  // Plan rule, tuned on B200 (tools/tune_wgrad.py): the TMA request count dominates, so
+  //  * rows wide enough (KS = 16*floor((Wp-2)/16) >= 32): "runs" staging, as many M-tiles per
+  //    unit as fit in a double-buffered stage;
+  //  * otherwise one copy per slot with the longest K chunk that double-buffers at 1 M-tile.
   const int ks_opts[4] = {256, 192, 128, 64};
   const int mpu_max = p.mt_per_unit;
-  double best = 1e30;
-  int best_mpu = 0, best_ks = 0;
-  for (int mpu = 1; mpu <= mpu_max; ++mpu) {
-    for (int ko = 0; ko < 4; ++ko) {
-      const int KS = ks_opts[ko], RR = KS + 8;
-      if (!p.gwide && RR > 256) continue;
-      const uint32_t stage = (uint32_t)mpu * 16 * RR * 16 + (uint32_t)(p.Nc / 8) * RR * 16;
-      if (kSmemBudget / (int)stage < 2) continue;
-      const double mma_cyc = (double)mpu * 3 * (KS / 16) * fmax(p.Nc / 2.0, 32.0 + p.Nc / 4.0);
-      const int groups = min(mpu * 16, 9 * p.CG);
-      const double tma_cyc = groups * (70.0 + RR * 16 / 100.0) + (70.0 + p.CGo * RR * 16 / 100.0);
-      const int ngrp = (p.MT + mpu - 1) / mpu;
-      const double cost = ngrp * fmax(mma_cyc, tma_cyc) / KS;
-      if (cost < best * 0.999) {
-        best = cost;
+  const int ks_run = min(256, ((p.Wp - 2) / 16) * 16);
+  int best_mpu = 0, best_ks = 0, best_runs = 0;
+  auto fits = [&](int runs, int KS, int mpu) {
+    const int RR = KS + 8;
+    if (!p.gwide && RR > 256) return false;
+    const int ralloc = (16 * mpu + 2) / 3 + 2;
+    const uint32_t a_b = ((runs ? (uint32_t)ralloc * 3 * p.Wp * 16 : (uint32_t)mpu * 16 * RR * 16) + 1023) & ~1023u;
+    const uint32_t stage = (a_b + (uint32_t)(p.Nc / 8) * RR * 16 + 1023) & ~1023u;
+    return kSmemBudget / (int)stage >= 2;
+  };
+  auto forced_ok = [&](int runs, int KS, int mpu) {
+    return !((g_force_runs >= 0 && runs != g_force_runs) || (g_force_ks && KS != g_force_ks) ||
+             (g_force_mpu && mpu != g_force_mpu));
+  };
+  if (ks_run >= 64 && g_force_runs != 0) {
+    for (int mpu = mpu_max; mpu >= 1 && !best_mpu; --mpu)
+      if (fits(1, ks_run, mpu) && forced_ok(1, ks_run, mpu)) {
         best_mpu = mpu;
-        best_ks = KS;
+        best_ks = ks_run;
+        best_runs = 1;
       }
-    }
   }
+  for (int mpu = 1; mpu <= mpu_max && !best_mpu; ++mpu)
+    for (int ko = 0; ko < 4 && !best_mpu; ++ko)
+      if (fits(0, ks_opts[ko], mpu) && forced_ok(0, ks_opts[ko], mpu)) {
+        best_mpu = mpu;
+        best_ks = ks_opts[ko];
+      }
   VM_REQUIRE(best_mpu > 0, VM_E_UNSUPPORTED, "vm_conv3d_wgrad_tc: no stage configuration fits");
   p.mt_per_unit = best_mpu;
   p.KS = best_ks;
+  p.runs = best_runs;
   p.RR = p.KS + 8;
-  p.a_bytes = (uint32_t)p.mt_per_unit * 16 * p.RR * 16;
+  p.runs_alloc = (16 * p.mt_per_unit + 2) / 3 + 2;
+  // TMA tensor destinations (the gy box) must be 128-byte aligned: keep every region 1 KB aligned
+  p.a_bytes = ((p.runs ? (uint32_t)p.runs_alloc * 3 * p.Wp * 16 : (uint32_t)p.mt_per_unit * 16 * p.RR * 16) + 1023) & ~1023u;
   p.g_bytes = (uint32_t)p.CGo * p.RR * 16;
-  p.stage_bytes = p.a_bytes + (uint32_t)(p.Nc / 8) * p.RR * 16;
+  p.stage_bytes = (p.a_bytes + (uint32_t)(p.Nc / 8) * p.RR * 16 + 1023) & ~1023u;
   p.stages = kSmemBudget / (int)p.stage_bytes;
   if (p.stages > kMaxStages) p.stages = kMaxStages;
   VM_REQUIRE(p.stages >= 2 && p.mt_per_unit >= 1, VM_E_UNSUPPORTED, "vm_conv3d_wgrad_tc: stage does not fit");
@@ -815,6 +853,23 @@ int make_group_map(CUtensorMap* m, const void* base, int64_t bstride, int CG, in
 }
 }  // namespace
 
+extern "C" void vm_debug_force_wgrad_plan(int runs, int ks, int mpu) {
+  g_force_runs = runs;
+  g_force_ks = ks;
+  g_force_mpu = mpu;
+}
+
+extern "C" int vm_debug_wgrad_plan(int B, int Cin, int Cout, int D, int H, int W, int* out) {
+  WgPlan pl;
+  int rc = plan_wgrad(B, Cin, Cout, D, H, W, pl);
+  if (rc) return rc;
+  const WgParams& p = pl.p;
+  const int v[12] = {p.runs, p.KS, p.MT, p.mt_per_unit, p.n_mtgroups, p.stages, p.ksplit, p.spk,
+                     p.units, p.ones_slot, (int)p.stage_bytes, p.gdelta};
+  for (int i = 0; i < 12; ++i) out[i] = v[i];
+  return VM_OK;
+}
+
 extern "C" size_t vm_conv3d_wgrad_tc_ws(int B, int Cin, int Cout, int D, int H, int W) {
   WgPlan pl;
   if (plan_wgrad(B, Cin, Cout, D, H, W, pl) != VM_OK) return 0;
@@ -852,7 +907,7 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
   const int nk = B * p.ksplit;
   const int64_t E = (int64_t)p.MT * 3 * p.Nc * 128;
   k_wgrad_tc_finalize<<<grid_for(E, 256), 256, 0, st>>>(p.ws, gw, gb, nk, p.MT, p.Nc, p.CG, Cin, Cout,
-                                                         p.ones_slot);
+                                                         p.ones_slot, p.runs);
   rc = launch_status("vm_conv3d_wgrad_tc finalize");
   if (rc || p.ones_slot >= 0) return rc;
   float* wsb = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ((pl.ws_main + 255) / 256) * 256);

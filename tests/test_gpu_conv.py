@@ -114,6 +114,12 @@ WG_SHAPES = [
     (1, 128, 64, 8, 8, 8),
     (1, 16, 48, 16, 20, 24),
     (1, 24, 8, 6, 6, 6),
+    # wide rows (W >= 32): the "runs" staging mode
+    (1, 16, 16, 4, 8, 128),
+    (1, 48, 16, 4, 6, 64),
+    (1, 32, 32, 6, 8, 64),
+    (2, 16, 32, 4, 4, 40),
+    (1, 1, 16, 4, 6, 126),
 ]
 
 
