@@ -116,6 +116,15 @@ int vm_weight_flip_transpose(const float* w, float* wt, int k, int Cin, int Cout
 size_t vm_packed_weights_bytes(int Cin, int Cout);
 int vm_pack_weights(const float* w, void* packed, int Cin, int Cout, int flip_transpose,
                     void* stream);
+/* Repack many layers in one launch: `jobs` is a DEVICE array; job i covers packed
+ * elements [begin_i, begin_{i+1}) of the concatenation (begin ascending, last ends at total). */
+typedef struct {
+  const float* w;
+  void* packed;
+  int cin, cout, flip, pad;
+  int64_t begin;
+} vm_pack_job;
+int vm_pack_weights_batch(const vm_pack_job* jobs, int njobs, int64_t total_elems, void* stream);
 int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wpacked, const float* bias,
                      void* y, int64_t y_bstride, const void* mask, int64_t mask_bstride, int B,
                      int Cin, int Cout, int D, int H, int W, unsigned flags, void* stream);

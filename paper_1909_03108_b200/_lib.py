@@ -47,6 +47,7 @@ _SIGS = {
     "vm_weight_flip_transpose": (_I, [_P, _P, _I, _I, _I, _P]),
     "vm_packed_weights_bytes": (ctypes.c_size_t, [_I, _I]),
     "vm_pack_weights": (_I, [_P, _P, _I, _I, _I, _P]),
+    "vm_pack_weights_batch": (_I, [_P, _I, _L, _P]),
     "vm_conv3d_fwd_tc": (_I, [_P, _L, _P, _P, _P, _L, _P, _L, _I, _I, _I, _I, _I, _I, _U, _P]),
     "vm_conv3d_wgrad_tc_ws": (ctypes.c_size_t, [_I, _I, _I, _I, _I, _I]),
     "vm_conv3d_wgrad_tc": (_I, [_P, _L, _P, _L, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),

@@ -95,7 +95,7 @@ struct PackGeom {
   int Nc, nchunk;  // N per chunk (multiple of 16, <= 256)
 };
 
-static PackGeom pack_geom(int cin, int cout) {
+__host__ __device__ static PackGeom pack_geom(int cin, int cout) {
   PackGeom g;
   g.cin = cin;
   g.cout = cout;
@@ -637,6 +637,47 @@ using namespace vm;
 extern "C" size_t vm_packed_weights_bytes(int Cin, int Cout) {
   PackGeom g = pack_geom(Cin, Cout);
   return (size_t)g.nchunk * g.KC * 27 * 2 * g.Nc * 8 * sizeof(bf16);
+}
+
+// Batched repack of every layer's operands in one launch (after each SGD step).
+__global__ void k_pack_batch(const vm_pack_job* __restrict__ jobs, int njobs, int64_t total) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = njobs - 1;
+    while (lo < hi) {  // last job with begin <= i
+      const int mid = (lo + hi + 1) >> 1;
+      if (jobs[mid].begin <= i) lo = mid; else hi = mid - 1;
+    }
+    const vm_pack_job& jb = jobs[lo];
+    const PackGeom g = jb.flip ? pack_geom(jb.cout, jb.cin) : pack_geom(jb.cin, jb.cout);
+    int64_t r = i - jb.begin;
+    const int e = r % 8;
+    r /= 8;
+    const int n = r % g.Nc;
+    r /= g.Nc;
+    const int half = r % 2;
+    r /= 2;
+    const int j = r % 9;
+    r /= 9;
+    const int kd = r % 3;
+    r /= 3;
+    const int kc = r % g.KC;
+    const int nch = (int)(r / g.KC);
+    const int t = kd * 9 + j;
+    const int ci = (kc * 2 + half) * 8 + e;
+    const int co = nch * g.Nc + n;
+    float v = 0.f;
+    if (ci < g.cin && co < g.cout)
+      v = !jb.flip ? jb.w[((int64_t)t * jb.cin + ci) * jb.cout + co]
+                   : jb.w[((int64_t)(26 - t) * jb.cin + co) * jb.cout + ci];
+    static_cast<bf16*>(jb.packed)[i - jb.begin] = __float2bfloat16_rn(v);
+  }
+}
+
+extern "C" int vm_pack_weights_batch(const vm_pack_job* jobs, int njobs, int64_t total_elems, void* stream) {
+  VM_REQUIRE(jobs && njobs > 0 && total_elems > 0, VM_E_ARG, "vm_pack_weights_batch: bad argument");
+  k_pack_batch<<<grid_for(total_elems, 256), 256, 0, as_stream(stream)>>>(jobs, njobs, total_elems);
+  return launch_status("vm_pack_weights_batch");
 }
 
 extern "C" int vm_pack_weights(const float* w, void* packed, int Cin, int Cout, int flip, void* stream) {

@@ -119,26 +119,21 @@ __global__ void k_maxpool_bwd(const T* __restrict__ x, Slab gx, const T* __restr
 }
 
 // ------------------------------------------------------------------ upsample
+// one thread per OUTPUT channel-block vector, in output order: stores are coalesced and
+// neighbouring threads re-read the same input vector from L1
 template <typename T>
 __global__ void k_upsample_fwd(const T* __restrict__ x, Slab gx, T* __restrict__ y, Slab gy, int B) {
-  const int64_t nvox = (int64_t)B * gx.D * gx.H * gx.W;
-  const int64_t total = nvox * gx.CG * 8;  // one output vector per thread
+  const int64_t nvox = (int64_t)B * gy.D * gy.H * gy.W;
+  const int64_t total = nvox * gy.CG;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int cell = i % 8;
-    int64_t r = i / 8;
-    int cg = (int)(r / nvox);
+    const int cg = (int)(i / nvox);
     int b, d, h, w;
-    decompose(r % nvox, gx.D, gx.H, gx.W, b, d, h, w);
-    int4 v = *reinterpret_cast<const int4*>(x + gx.at(b, cg, d, h, w));
-    if (sizeof(T) == 2) {
-      *reinterpret_cast<int4*>(y + gy.at(b, cg, 2 * d + (cell >> 2), 2 * h + ((cell >> 1) & 1), 2 * w + (cell & 1))) = v;
-    } else {
-      const T* src = x + gx.at(b, cg, d, h, w);
-      T* dst = y + gy.at(b, cg, 2 * d + (cell >> 2), 2 * h + ((cell >> 1) & 1), 2 * w + (cell & 1));
-      *reinterpret_cast<int4*>(dst) = *reinterpret_cast<const int4*>(src);
-      *reinterpret_cast<int4*>(dst + 4) = *reinterpret_cast<const int4*>(src + 4);
-    }
+    decompose(i % nvox, gy.D, gy.H, gy.W, b, d, h, w);
+    const T* src = x + gx.at(b, cg, d >> 1, h >> 1, w >> 1);
+    T* dst = y + gy.at(b, cg, d, h, w);
+    *reinterpret_cast<int4*>(dst) = __ldg(reinterpret_cast<const int4*>(src));
+    if (sizeof(T) == 4) *reinterpret_cast<int4*>(dst + 4) = __ldg(reinterpret_cast<const int4*>(src + 4));
   }
 }
 
@@ -356,6 +351,161 @@ __global__ void __launch_bounds__(kHeadThreads) k_head_bwd(
   }
 }
 
+// Fixed-shape head kernels (C input channels, NC classes known at compile time): all
+// per-voxel state and the weight-gradient partials live in registers.
+template <typename T, int C, int NC>
+__global__ void __launch_bounds__(kHeadThreads) k_head_fwd_fixed(
+    const T* __restrict__ y, Slab sy, const float* __restrict__ W, const float* __restrict__ bias,
+    const float* __restrict__ onehot, float* __restrict__ probs, float* __restrict__ partials, int B,
+    float clamp) {
+  __shared__ float sW[C * NC], sb[NC], red[kHeadThreads / 32];
+  for (int i = threadIdx.x; i < C * NC; i += blockDim.x) sW[i] = W[i];
+  if (threadIdx.x < NC) sb[threadIdx.x] = bias[threadIdx.x];
+  __syncthreads();
+  const int64_t nvox = (int64_t)B * sy.D * sy.H * sy.W;
+  float st[3 * NC + 1];
+#pragma unroll
+  for (int k = 0; k < 3 * NC + 1; ++k) st[k] = 0.f;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvox;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int b, d, h, w;
+    decompose(v, sy.D, sy.H, sy.W, b, d, h, w);
+    float lg[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) lg[k] = sb[k];
+    const T* base = y + sy.at(b, 0, d, h, w);
+#pragma unroll
+    for (int cg = 0; cg < C / 8; ++cg) {
+      float yv[8];
+      V8<T>::ld(base + cg * sy.plane(), yv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int k = 0; k < NC; ++k) lg[k] = fmaf(yv[j], sW[(cg * 8 + j) * NC + k], lg[k]);
+    }
+    float m = lg[0];
+#pragma unroll
+    for (int k = 1; k < NC; ++k) m = fmaxf(m, lg[k]);
+    float p[NC], ssum = 0.f;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      p[k] = expf(lg[k] - m);
+      ssum += p[k];
+    }
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      p[k] = p[k] / ssum;
+      const float g = onehot[v * NC + k];
+      if (probs) probs[v * NC + k] = p[k];
+      st[k] += p[k] * g;
+      st[NC + k] += p[k];
+      st[2 * NC + k] += g;
+      st[3 * NC] += -logf(fmaxf(p[k], clamp)) * g;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3 * NC + 1; ++k) {
+    float s = block_sum(st[k], red);
+    if (threadIdx.x == 0) partials[(int64_t)blockIdx.x * (3 * NC + 1) + k] = s;
+  }
+}
+
+template <typename T, int C, int NC>
+__global__ void __launch_bounds__(kHeadThreads) k_head_bwd_fixed(
+    const T* __restrict__ y, Slab sy, const float* __restrict__ W, const float* __restrict__ bias,
+    const float* __restrict__ onehot, const float* __restrict__ stats, T* __restrict__ g, Slab sg,
+    float* __restrict__ wpart, int B, float w_dice, float w_ce, float total, int dice_mask, float clamp,
+    int relu_mask) {
+  __shared__ float sW[C * NC], sb[NC], red[kHeadThreads / 32], coef[3 * NC];
+  for (int i = threadIdx.x; i < C * NC; i += blockDim.x) sW[i] = W[i];
+  if (threadIdx.x < NC) sb[threadIdx.x] = bias[threadIdx.x];
+  if (threadIdx.x == 0) {
+    const int nfg = __popc(dice_mask);
+    for (int k = 0; k < NC; ++k) {  // training.py:119-124
+      const float nk = 2.f * stats[k] + 1e-6f;
+      const float dk = stats[NC + k] + stats[2 * NC + k] + 1e-6f;
+      const bool on = (dice_mask >> k) & 1;
+      coef[3 * k + 0] = on ? (-w_dice / (float)nfg) / dk : 0.f;
+      coef[3 * k + 1] = on ? nk / dk : 0.f;
+      coef[3 * k + 2] = on ? 1.f : 0.f;
+    }
+  }
+  __syncthreads();
+  const int64_t nvox = (int64_t)B * sy.D * sy.H * sy.W;
+  const float ce_scale = -w_ce / total;
+  float acc[C * NC + NC];
+#pragma unroll
+  for (int i = 0; i < C * NC + NC; ++i) acc[i] = 0.f;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvox;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int b, d, h, w;
+    decompose(v, sy.D, sy.H, sy.W, b, d, h, w);
+    float yv[C];
+    const T* base = y + sy.at(b, 0, d, h, w);
+#pragma unroll
+    for (int cg = 0; cg < C / 8; ++cg) {
+      float t8[8];
+      V8<T>::ld(base + cg * sy.plane(), t8);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) yv[cg * 8 + j] = t8[j];
+    }
+    float lg[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      lg[k] = sb[k];
+#pragma unroll
+      for (int c = 0; c < C; ++c) lg[k] = fmaf(yv[c], sW[c * NC + k], lg[k]);
+    }
+    float m = lg[0];
+#pragma unroll
+    for (int k = 1; k < NC; ++k) m = fmaxf(m, lg[k]);
+    float p[NC], ssum = 0.f;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      p[k] = expf(lg[k] - m);
+      ssum += p[k];
+    }
+    float gp[NC], dot = 0.f;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      p[k] = p[k] / ssum;
+      const float gk = onehot[v * NC + k];
+      float r = coef[3 * k + 2] != 0.f ? coef[3 * k] * (2.f * gk - coef[3 * k + 1]) : 0.f;
+      r += p[k] >= clamp ? ce_scale * (gk / fmaxf(p[k], clamp)) : 0.f;  // training.py:125-126
+      gp[k] = r;
+      dot += r * p[k];
+    }
+    float gl[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      gl[k] = p[k] * (gp[k] - dot);  // ops.py:197-199
+      acc[C * NC + k] += gl[k];
+    }
+    T* gbase = g + sg.at(b, 0, d, h, w);
+#pragma unroll
+    for (int cg = 0; cg < C / 8; ++cg) {
+      float o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int c = cg * 8 + j;
+        float sacc = 0.f;
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          sacc = fmaf(sW[c * NC + k], gl[k], sacc);
+          acc[c * NC + k] = fmaf(yv[c], gl[k], acc[c * NC + k]);
+        }
+        o[j] = (relu_mask && !(yv[c] > 0.f)) ? 0.f : sacc;
+      }
+      V8<T>::st(gbase + cg * sg.plane(), o);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < C * NC + NC; ++i) {
+    float s = block_sum(acc[i], red);
+    if (threadIdx.x == 0) wpart[(int64_t)blockIdx.x * (C * NC + NC) + i] = s;
+  }
+}
+
 __global__ void k_reduce_rows(const float* __restrict__ part, int rows, int width,
                               float* __restrict__ out) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < width; j += gridDim.x * blockDim.x) {
@@ -443,7 +593,7 @@ extern "C" int vm_upsample2_fwd(int dtype, const void* x, int64_t x_bstride, voi
                                 int64_t y_bstride, int B, int C, int D, int H, int W, void* stream) {
   VM_REQUIRE(x && y, VM_E_ARG, "vm_upsample2_fwd: null pointer");
   Slab gx = SLAB(x_bstride, C, D, H, W), gy = SLAB(y_bstride, C, 2 * D, 2 * H, 2 * W);
-  int64_t work = (int64_t)B * D * H * W * gx.CG * 8;
+  int64_t work = (int64_t)B * D * H * W * gx.CG * 8;  // output vectors
   DISPATCH_T(dtype, "vm_upsample2_fwd",
              k_upsample_fwd<T><<<grid_for(work, 256), 256, 0, as_stream(stream)>>>(
                  (const T*)x, gx, (T*)y, gy, B));
@@ -491,6 +641,17 @@ extern "C" int vm_head_fwd(int dtype, const void* y, int64_t y_bstride, const fl
   Slab sy = SLAB(y_bstride, C, D, H, W);
   int grid = vm_head_partials_count(B, D, H, W);
   size_t sh = (C * ncls + ncls + 32) * sizeof(float);
+  if (dtype == VM_BF16 && ncls == 3 && (C == 16 || C == 32 || C == 8)) {
+    using T = __nv_bfloat16;
+    auto st = as_stream(stream);
+    if (C == 16)
+      k_head_fwd_fixed<T, 16, 3><<<grid, kHeadThreads, 0, st>>>((const T*)y, sy, w, b, onehot, probs, partials, B, clamp);
+    else if (C == 32)
+      k_head_fwd_fixed<T, 32, 3><<<grid, kHeadThreads, 0, st>>>((const T*)y, sy, w, b, onehot, probs, partials, B, clamp);
+    else
+      k_head_fwd_fixed<T, 8, 3><<<grid, kHeadThreads, 0, st>>>((const T*)y, sy, w, b, onehot, probs, partials, B, clamp);
+    return launch_status("vm_head_fwd");
+  }
   DISPATCH_T(dtype, "vm_head_fwd",
              k_head_fwd<T><<<grid, kHeadThreads, sh, as_stream(stream)>>>(
                  (const T*)y, sy, w, b, onehot, probs, partials, B, C, ncls, clamp));
@@ -513,6 +674,22 @@ extern "C" int vm_head_bwd(int dtype, const void* y, int64_t y_bstride, const fl
   Slab sy = SLAB(y_bstride, C, D, H, W), sg = SLAB(g_bstride, C, D, H, W);
   int grid = vm_head_partials_count(B, D, H, W);
   size_t sh = (C * ncls + ncls + 32 + 3 * kMaxCls) * sizeof(float);
+  if (dtype == VM_BF16 && ncls == 3 && (C == 16 || C == 32 || C == 8)) {
+    using T = __nv_bfloat16;
+    auto st = as_stream(stream);
+#define HEAD_BWD_FIXED(CC)                                                                          \
+  k_head_bwd_fixed<T, CC, 3><<<grid, kHeadThreads, 0, st>>>((const T*)y, sy, w, b, onehot, stats, (T*)g, sg, \
+                                                            wpartials, B, w_dice, w_ce, total_voxels,    \
+                                                            dice_mask, clamp, relu_mask)
+    if (C == 16)
+      HEAD_BWD_FIXED(16);
+    else if (C == 32)
+      HEAD_BWD_FIXED(32);
+    else
+      HEAD_BWD_FIXED(8);
+#undef HEAD_BWD_FIXED
+    return launch_status("vm_head_bwd");
+  }
   DISPATCH_T(dtype, "vm_head_bwd",
              k_head_bwd<T><<<grid, kHeadThreads, sh, as_stream(stream)>>>(
                  (const T*)y, sy, w, b, onehot, stats, (T*)g, sg, wpartials, B, C, ncls, w_dice,

@@ -262,8 +262,32 @@ class UNetStep:
             self._rec.append((kind, label, flops, nbytes, name, args))
         _lib.call(name, *args, self._st())
 
+    def _pack_table(self):
+        """Device job table for vm_pack_weights_batch (one launch repacks every layer)."""
+        if getattr(self, "_pack_jobs", None) is not None:
+            return self._pack_jobs, self._pack_n, self._pack_total
+        dt = np.dtype([("w", "<u8"), ("packed", "<u8"), ("cin", "<i4"), ("cout", "<i4"), ("flip", "<i4"),
+                       ("pad", "<i4"), ("begin", "<i8")])
+        rows, begin = [], 0
+        for L in self.layers:
+            if L.k != 3:
+                continue
+            for flip, buf in ((0, L.wp), (1, L.wpt)):
+                ci, co = (L.cout, L.cin) if flip else (L.cin, L.cout)
+                n = int(_lib.call_size("vm_packed_weights_bytes", ci, co)) // 2
+                rows.append((L.w.data_ptr(), buf.data_ptr(), L.cin, L.cout, flip, 0, begin))
+                begin += n
+        arr = np.array(rows, dtype=dt)
+        self._pack_jobs = torch.from_numpy(arr.view(np.uint8).copy()).to(self.device)
+        self._pack_n, self._pack_total = len(rows), begin
+        return self._pack_jobs, self._pack_n, self._pack_total
+
     def repack(self):
         """Refresh the derived conv operands from the fp32 master weights."""
+        if self.conv_impl == "tc":
+            jobs, n, total = self._pack_table()
+            self._k("pack", "all", 0, 0, "vm_pack_weights_batch", _lib.ptr(jobs), n, total)
+            return
         for L in self.layers:
             if L.k != 3:
                 continue
