@@ -88,7 +88,7 @@ int vm_onehot_u8(const uint8_t* labels, float* onehot, int64_t nvox, int ncls, v
 /* ------------------------------------------------------------------ conv3d
  * Weights: master fp32 in the reference layout [k][k][k][Cin][Cout]
  * (ops.py:33-34).  The tensor-core path consumes packed bf16 operands produced by
- * vm_pack_weights (forward) / vm_pack_weights_dgrad (flipped + transposed). */
+ * vm_pack_weights (flip_transpose = 0: forward; 1: the flipped, transposed dgrad operand). */
 
 /* SIMT path (fp32 or bf16 storage, fp32 accumulation) — the fp32 parity path
  * (cfg1) and the on-device cross-check of the tensor-core kernels.

@@ -176,7 +176,7 @@ def halo_exchange_backward_blocks(grads, dims, layout, axes, margins):
             core = cur - lo - hi
             lo_n = neighbor(c, shape, axis_index[axis], -1) if axis else None
             hi_n = neighbor(c, shape, axis_index[axis], +1) if axis else None
-            out = np.ascontiguousarray(_slab(data[r], i, lo, lo + core))  # halo.py:180
+            out = np.array(_slab(data[r], i, lo, lo + core))  # halo.py:180 (owned copy)
             if lo_n is not None and hi > 0:  # halo.py:181-183
                 v = _slab(out, i, 0, hi)
                 v += msgs[(rank_of[lo_n], r, "up")]

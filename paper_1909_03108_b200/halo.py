@@ -153,78 +153,91 @@ def _padded5(core5, margins5):
     return tuple(c + lo + hi for c, (lo, hi) in zip(core5, margins5))
 
 
-def run_exchange(ctx, buf5, core5, margins5, nbrs, elem_bytes, tag=_FWD_TAG, dims_names=None):
-    """Fill the margins of the 5-D padded buffer ``buf5`` in place (forward protocol).
+class CudaPacker:
+    """The product pack/unpack path: 16-byte vectorised box kernels of libvoxmesh_sm100."""
 
-    Returns {(phase_index, "lo"|"hi"): "neighbor"|"zero"}.
-    """
+    def _args(self, buf5, lo5, ext5):
+        return _lib.ptr(buf5), _lib.i64arr(buf5.shape), _lib.i64arr(lo5), _lib.i64arr(ext5)
+
+    def pack(self, buf5, lo5, ext5):
+        import torch
+
+        m = torch.empty(ext5, dtype=buf5.dtype, device=buf5.device)
+        p, d, lo, ext = self._args(buf5, lo5, ext5)
+        _lib.call("vm_box_pack", p, d, buf5.element_size(), lo, ext, _lib.ptr(m), _lib.stream_ptr())
+        return m
+
+    def unpack(self, buf5, lo5, ext5, t):
+        p, d, lo, ext = self._args(buf5, lo5, ext5)
+        _lib.call("vm_box_unpack", p, d, buf5.element_size(), lo, ext, _lib.ptr(t), _lib.stream_ptr())
+
+    def unpack_add(self, buf5, lo5, ext5, t):
+        p, d, lo, ext = self._args(buf5, lo5, ext5)
+        _lib.call("vm_box_unpack_add", p, d, _lib.dtype_code(buf5.dtype), lo, ext, _lib.ptr(t), _lib.stream_ptr())
+
+    def zero(self, buf5, lo5, ext5):
+        p, d, lo, ext = self._args(buf5, lo5, ext5)
+        _lib.call("vm_box_zero", p, d, buf5.element_size(), lo, ext, _lib.stream_ptr())
+
+
+CUDA_PACKER = CudaPacker()
+
+
+def _empty(like5, shape):
     import torch
 
-    dims = _padded5(core5, margins5)
-    st = _lib.stream_ptr()
-    d64 = _lib.i64arr(dims)
+    return torch.empty(shape, dtype=like5.dtype, device=like5.device)
+
+
+def run_exchange(ctx, buf5, core5, margins5, nbrs, elem_bytes=None, tag=_FWD_TAG, dims_names=None, packer=None):
+    """Fill the margins of the 5-D padded buffer ``buf5`` in place (forward protocol,
+    halo.py:109-155).  Returns {(dim, "lo"|"hi"): "neighbor"|"zero"}."""
+    pk = packer or CUDA_PACKER
     faces = {}
-    for k, ph in enumerate(plan_phases(core5, margins5, nbrs)):
+    for ph in plan_phases(core5, margins5, nbrs):
         name = dims_names[ph.axis_pos] if dims_names else ph.axis_pos
-        sends, recvs = [], []
-        if ph.lo_nbr is not None and ph.hi > 0:
-            lo5, ext5 = ph.send_down
-            m = torch.empty(ext5, dtype=buf5.dtype, device=buf5.device)
-            _lib.call("vm_box_pack", _lib.ptr(buf5), d64, elem_bytes, _lib.i64arr(lo5), _lib.i64arr(ext5), _lib.ptr(m), st)
-            sends.append((ph.lo_nbr, m, (tag, name, "down")))
-        if ph.hi_nbr is not None and ph.lo > 0:
-            lo5, ext5 = ph.send_up
-            m = torch.empty(ext5, dtype=buf5.dtype, device=buf5.device)
-            _lib.call("vm_box_pack", _lib.ptr(buf5), d64, elem_bytes, _lib.i64arr(lo5), _lib.i64arr(ext5), _lib.ptr(m), st)
-            sends.append((ph.hi_nbr, m, (tag, name, "up")))
-        want = []
+        sends, recvs, want = [], [], []
+        if ph.lo_nbr is not None and ph.hi > 0:  # first hi interior rows travel "down"
+            sends.append((ph.lo_nbr, pk.pack(buf5, *ph.send_down), (tag, name, "down")))
+        if ph.hi_nbr is not None and ph.lo > 0:  # last lo interior rows travel "up"
+            sends.append((ph.hi_nbr, pk.pack(buf5, *ph.send_up), (tag, name, "up")))
         if ph.lo_nbr is not None and ph.lo > 0:
-            recvs.append((ph.lo_nbr, torch.empty(ph.recv_lo[1], dtype=buf5.dtype, device=buf5.device), (tag, name, "up")))
+            recvs.append((ph.lo_nbr, _empty(buf5, ph.recv_lo[1]), (tag, name, "up")))
             want.append(ph.recv_lo)
         if ph.hi_nbr is not None and ph.hi > 0:
-            recvs.append((ph.hi_nbr, torch.empty(ph.recv_hi[1], dtype=buf5.dtype, device=buf5.device), (tag, name, "down")))
+            recvs.append((ph.hi_nbr, _empty(buf5, ph.recv_hi[1]), (tag, name, "down")))
             want.append(ph.recv_hi)
         got = ctx.exchange(sends, recvs) if (sends or recvs) else []
         for (lo5, ext5), t in zip(want, got):
-            _lib.call("vm_box_unpack", _lib.ptr(buf5), d64, elem_bytes, _lib.i64arr(lo5), _lib.i64arr(ext5), _lib.ptr(t), st)
+            pk.unpack(buf5, lo5, ext5, t)
         for side, nbr, (lo5, ext5) in (("lo", ph.lo_nbr, ph.recv_lo), ("hi", ph.hi_nbr, ph.recv_hi)):
             if nbr is None and ext5[ph.axis_pos] > 0:
-                _lib.call("vm_box_zero", _lib.ptr(buf5), d64, elem_bytes, _lib.i64arr(lo5), _lib.i64arr(ext5), st)
+                pk.zero(buf5, lo5, ext5)
             faces[(name, side)] = "neighbor" if nbr is not None else "zero"
     return faces
 
 
-def run_exchange_backward(ctx, buf5, core5, margins5, nbrs, dtype_code, elem_bytes, tag=_BWD_TAG, dims_names=None):
-    """Adjoint (halo.py:158-194): phases reversed; margins are sent back and added
-    to the owner's interior rows (low side first, then high).  Operates in place
-    on ``buf5``; the result is its interior."""
-    import torch
-
-    dims = _padded5(core5, margins5)
-    st = _lib.stream_ptr()
-    d64 = _lib.i64arr(dims)
+def run_exchange_backward(ctx, buf5, core5, margins5, nbrs, tag=_BWD_TAG, dims_names=None, packer=None):
+    """Adjoint (halo.py:158-194): phases reversed; each margin is sent back to the rank
+    owning those voxels and added to its interior rows, low side first then high.
+    In place on ``buf5``; the result is its interior."""
+    pk = packer or CUDA_PACKER
     for ph in reversed(plan_phases(core5, margins5, nbrs)):
         name = dims_names[ph.axis_pos] if dims_names else ph.axis_pos
         sends, recvs, targets = [], [], []
         if ph.lo_nbr is not None and ph.lo > 0:  # margin [0,lo) goes back down
-            lo5, ext5 = ph.recv_lo
-            m = torch.empty(ext5, dtype=buf5.dtype, device=buf5.device)
-            _lib.call("vm_box_pack", _lib.ptr(buf5), d64, elem_bytes, _lib.i64arr(lo5), _lib.i64arr(ext5), _lib.ptr(m), st)
-            sends.append((ph.lo_nbr, m, (tag, name, "down")))
+            sends.append((ph.lo_nbr, pk.pack(buf5, *ph.recv_lo), (tag, name, "down")))
         if ph.hi_nbr is not None and ph.hi > 0:  # margin [lo+n, lo+n+hi) goes back up
-            lo5, ext5 = ph.recv_hi
-            m = torch.empty(ext5, dtype=buf5.dtype, device=buf5.device)
-            _lib.call("vm_box_pack", _lib.ptr(buf5), d64, elem_bytes, _lib.i64arr(lo5), _lib.i64arr(ext5), _lib.ptr(m), st)
-            sends.append((ph.hi_nbr, m, (tag, name, "up")))
-        if ph.lo_nbr is not None and ph.hi > 0:  # first hi interior rows += from lo nbr
-            recvs.append((ph.lo_nbr, torch.empty(ph.send_down[1], dtype=buf5.dtype, device=buf5.device), (tag, name, "up")))
+            sends.append((ph.hi_nbr, pk.pack(buf5, *ph.recv_hi), (tag, name, "up")))
+        if ph.lo_nbr is not None and ph.hi > 0:  # first hi interior rows += from the lo neighbour
+            recvs.append((ph.lo_nbr, _empty(buf5, ph.send_down[1]), (tag, name, "up")))
             targets.append(ph.send_down)
-        if ph.hi_nbr is not None and ph.lo > 0:  # last lo interior rows += from hi nbr
-            recvs.append((ph.hi_nbr, torch.empty(ph.send_up[1], dtype=buf5.dtype, device=buf5.device), (tag, name, "down")))
+        if ph.hi_nbr is not None and ph.lo > 0:  # last lo interior rows += from the hi neighbour
+            recvs.append((ph.hi_nbr, _empty(buf5, ph.send_up[1]), (tag, name, "down")))
             targets.append(ph.send_up)
         got = ctx.exchange(sends, recvs) if (sends or recvs) else []
         for (lo5, ext5), t in zip(targets, got):
-            _lib.call("vm_box_unpack_add", _lib.ptr(buf5), d64, dtype_code, _lib.i64arr(lo5), _lib.i64arr(ext5), _lib.ptr(t), st)
+            pk.unpack_add(buf5, lo5, ext5, t)
 
 
 # ---------------------------------------------------------------------------
@@ -247,9 +260,11 @@ def _spec5(block_shape, dims, halo, ctx):
     return core5, margins5, nbrs, names5
 
 
-def exchange_local(ctx, dims, halo, tag, phase_barrier, block):
+def exchange_local(ctx, dims, halo, tag, phase_barrier, block, packer=None):
     """Worker-side forward exchange; returns the PaddedBlock (device tensor)."""
     import torch
+
+    pk = packer or CUDA_PACKER
 
     core5, margins5, nbrs, names5 = _spec5(tuple(block.shape), dims, halo, ctx)
     for i, (lo, hi) in enumerate(margins5):
@@ -260,23 +275,18 @@ def exchange_local(ctx, dims, halo, tag, phase_barrier, block):
             )
     padded_shape = tuple(c + lo + hi for c, (lo, hi) in zip(core5, margins5))
     buf = torch.empty(padded_shape, dtype=block.dtype, device=block.device)
-    eb = block.element_size()
-    st = _lib.stream_ptr()
     inner_lo = tuple(lo for lo, _ in margins5)
-    _lib.call(
-        "vm_box_unpack", _lib.ptr(buf), _lib.i64arr(padded_shape), eb, _lib.i64arr(inner_lo),
-        _lib.i64arr(core5), _lib.ptr(block.contiguous().reshape(core5)), st,
-    )
-    faces = run_exchange(ctx, buf, core5, margins5, nbrs, eb, tag, names5)
+    pk.unpack(buf, inner_lo, core5, block.contiguous().reshape(core5))
+    faces = run_exchange(ctx, buf, core5, margins5, nbrs, tag=tag, dims_names=names5, packer=pk)
     if phase_barrier:
         pass  # stream/queue ordering replaces the per-phase barrier (halo.py:151-152)
     out_shape = tuple(e + halo.total(n) for e, (n, _) in zip(block.shape, dims))
     return PaddedBlock(buf.reshape(out_shape), halo, tuple(n for n, _ in dims), faces)
 
 
-def exchange_backward_local(ctx, dims, halo, tag, phase_barrier, grad_padded):
+def exchange_backward_local(ctx, dims, halo, tag, phase_barrier, grad_padded, packer=None):
     """Worker-side adjoint; returns the interior gradient (device tensor)."""
-    import torch
+    pk = packer or CUDA_PACKER
 
     g = grad_padded.data if isinstance(grad_padded, PaddedBlock) else grad_padded
     names = [n for n, _ in dims]
@@ -287,14 +297,9 @@ def exchange_backward_local(ctx, dims, halo, tag, phase_barrier, grad_padded):
             raise HaloError(f"gradient block extent {e + lo + hi} too small for margins ({lo},{hi}) on {n!r}")
     core5, margins5, nbrs, names5 = _spec5(core, dims, halo, ctx)
     buf = g.contiguous().clone().reshape(_padded5(core5, margins5))
-    run_exchange_backward(ctx, buf, core5, margins5, nbrs, _lib.dtype_code(g.dtype), g.element_size(), tag, names5)
-    out = torch.empty(core5, dtype=g.dtype, device=g.device)
+    run_exchange_backward(ctx, buf, core5, margins5, nbrs, tag=tag, dims_names=names5, packer=pk)
     inner_lo = tuple(lo for lo, _ in margins5)
-    _lib.call(
-        "vm_box_pack", _lib.ptr(buf), _lib.i64arr(buf.shape), g.element_size(), _lib.i64arr(inner_lo),
-        _lib.i64arr(core5), _lib.ptr(out), _lib.stream_ptr(),
-    )
-    return out.reshape(core)
+    return pk.pack(buf, inner_lo, core5).reshape(core)
 
 
 def exchange_byte_count(spec, layout, mesh, halo, direction="forward"):

@@ -138,6 +138,7 @@ class UNetStep:
             g // d for g, d in zip(self.global_shape, self.div))
         self.total_voxels = float(self.global_batch * int(np.prod(self.global_shape)))
         self._rec = None
+        self.packer = None  # halo pack/unpack backend (None: the CUDA box kernels)
         self._build_buffers(params)
 
     # ------------------------------------------------------------------ setup
@@ -336,7 +337,7 @@ class UNetStep:
         margins5 = [(0, 0), (1, 1), (1, 1), (1, 1), (0, 0)]
         core5 = (s.CG, s.D, s.H, s.W, 8)
         for b in range(self.B):
-            run_exchange(self.ctx, s.view5(b), core5, margins5, self.nbrs, s.storage.element_size(), tag)
+            run_exchange(self.ctx, s.view5(b), core5, margins5, self.nbrs, tag=tag, packer=self.packer)
 
     def halo_bytes_per_step(self):
         """Bytes this rank sends per step (3-phase protocol, fwd + bwd, slab channel padding included)."""

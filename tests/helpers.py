@@ -25,3 +25,24 @@ def oracle_step(graph, params, x, oh, dtype=np.float64, round_bf16=False):
 
 def rel_l2(a, b):
     return O.rel_l2(a, b)
+
+
+class TorchPacker:
+    """Test-only stand-in for the CUDA box kernels (tensor slicing), so the halo
+    protocol and its transports can be exercised on CPU."""
+
+    @staticmethod
+    def _sl(lo5, ext5):
+        return tuple(slice(int(a), int(a) + int(e)) for a, e in zip(lo5, ext5))
+
+    def pack(self, buf5, lo5, ext5):
+        return buf5[self._sl(lo5, ext5)].clone().contiguous()
+
+    def unpack(self, buf5, lo5, ext5, t):
+        buf5[self._sl(lo5, ext5)] = t.reshape(tuple(int(e) for e in ext5))
+
+    def unpack_add(self, buf5, lo5, ext5, t):
+        buf5[self._sl(lo5, ext5)] += t.reshape(tuple(int(e) for e in ext5))
+
+    def zero(self, buf5, lo5, ext5):
+        buf5[self._sl(lo5, ext5)] = 0
