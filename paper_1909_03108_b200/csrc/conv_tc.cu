@@ -424,6 +424,7 @@ struct WgParams {
   int ksplit;       // K-split chunks per sample
   int stages_total; // per sample
   int units;
+  int grid;         // CTAs (a multiple of n_mtgroups); one K partial per CTA
   int stages;       // pipeline depth
   uint32_t a_bytes; // per stage: mt_per_unit*16 slots * RR * 16
   uint32_t g_bytes; // per stage loaded: CGo * RR * 16 (allocated: Nc/8 groups)
@@ -526,14 +527,15 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else if (warp == 1) {
+    // All units of this CTA share the M-tile group and cover disjoint K ranges: accumulate
+    // them in TMEM and drain once (one partial per CTA instead of one per unit).
     int stage = 0;
-    uint32_t phase = 0, tph = 0;
+    uint32_t phase = 0;
     const uint32_t sbo = GS;
+    bool started = false;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       const int ks = (u / p.n_mtgroups) % p.ksplit;
       const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
-      mbar_wait(&tempty, tph ^ 1);
-      tc_fence_after();
       for (int s = s0; s < s1; ++s) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
@@ -546,7 +548,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll 1
           for (int kk = 0; kk < p.KS / 16; ++kk) {
             const uint64_t bdesc = b0desc + (uint64_t)(kk * 16);
-            const uint32_t acc = (s > s0 || kk > 0) ? 1u : 0u;
+            const uint32_t acc = (started || kk > 0) ? 1u : 0u;
 #pragma unroll 1
             for (int m = 0; m < nmt; ++m) {
               const uint64_t adesc = a0desc + (uint64_t)(m * mstep + kk * 16);
@@ -559,39 +561,32 @@ __global__ void __launch_bounds__(192, 1)
           mma_commit(&empty[stage]);
         }
         __syncwarp();
+        started = true;
         if (++stage == p.stages) {
           stage = 0;
           phase ^= 1;
         }
       }
-      if (elect_one()) mma_commit(&tfull);
-      __syncwarp();
-      tph ^= 1;
     }
+    if (elect_one()) mma_commit(&tfull);
+    __syncwarp();
   } else {
     const int q = warp & 3;
-    uint32_t tph = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      const int ks = (u / p.n_mtgroups) % p.ksplit;
-      const int b = u / (p.n_mtgroups * p.ksplit);
-      const int kidx = b * p.ksplit + ks;
-      mbar_wait(&tfull, tph);
-      tc_fence_after();
-      const int m_row = q * 32 + lane;
-      for (int m = 0; m < nmt; ++m)
-        for (int kw = 0; kw < 3; ++kw)
-          for (int n0 = 0; n0 < p.Nc; n0 += 8) {
-            uint32_t r[8];
-            tmem_ld8(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)((m * 3 + kw) * p.Nc + n0), r);
-            tmem_ld_wait();
-            float* dst = p.ws + ((((int64_t)kidx * p.MT + mt0 + m) * 3 + kw) * p.Nc + n0) * 128 + m_row;
+    const int kidx = blockIdx.x / p.n_mtgroups;
+    mbar_wait(&tfull, 0);
+    tc_fence_after();
+    const int m_row = q * 32 + lane;
+    for (int m = 0; m < nmt; ++m)
+      for (int kw = 0; kw < 3; ++kw)
+        for (int n0 = 0; n0 < p.Nc; n0 += 16) {
+          uint32_t r[16];
+          tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)((m * 3 + kw) * p.Nc + n0), r);
+          tmem_ld_wait();
+          float* dst = p.ws + ((((int64_t)kidx * p.MT + mt0 + m) * 3 + kw) * p.Nc + n0) * 128 + m_row;
 #pragma unroll
-            for (int e = 0; e < 8; ++e) dst[e * 128] = __uint_as_float(r[e]);
-          }
-      tc_fence_before();
-      mbar_arrive(&tempty);
-      tph ^= 1;
-    }
+          for (int e = 0; e < 16; ++e) dst[e * 128] = __uint_as_float(r[e]);
+        }
+    (void)tempty;
   }
   tc_fence_before();
   __syncthreads();
@@ -619,8 +614,16 @@ __global__ void k_wgrad_tc_finalize(const float* __restrict__ ws, float* __restr
     const bool is_w = g < 9 * CG && cgi * 8 + m % 8 < Cin;
     const bool is_b = g == ones_slot && kw == 0 && m % 8 == 0;
     if (!is_w && !is_b) continue;
-    float s = 0.f;
-    for (int k = 0; k < nk; ++k) s += ws[k * E + e];
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;  // 4 independent chains, fixed order
+    int k = 0;
+    for (; k + 4 <= nk; k += 4) {
+      s0 += ws[(k + 0) * E + e];
+      s1 += ws[(k + 1) * E + e];
+      s2 += ws[(k + 2) * E + e];
+      s3 += ws[(k + 3) * E + e];
+    }
+    for (; k < nk; ++k) s0 += ws[k * E + e];
+    const float s = (s0 + s1) + (s2 + s3);
     if (is_w) {
       const int ci = cgi * 8 + m % 8;
       gw[((int64_t)(pp * 3 + kw) * Cin + ci) * Cout + co] = s;
@@ -856,7 +859,10 @@ int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
   p.ksplit = (p.stages_total + p.spk - 1) / p.spk;
   p.units = p.n_mtgroups * B * p.ksplit;
   p.idesc = make_idesc_bf16(128, p.Nc, true, true);
-  pl.ws_main = (size_t)B * p.ksplit * p.MT * 3 * p.Nc * 128 * sizeof(float);
+  p.grid = p.units;
+  if (p.grid > nsm) p.grid = (nsm / p.n_mtgroups) * p.n_mtgroups;  // CTA keeps one M-tile group
+  if (p.grid < p.n_mtgroups) p.grid = p.n_mtgroups;
+  pl.ws_main = (size_t)(p.grid / p.n_mtgroups) * p.MT * 3 * p.Nc * 128 * sizeof(float);
   pl.ws_bias = p.ones_slot >= 0 ? 0 : bias_grad_ws_bytes((int64_t)B * D * H * W, Cout);
   return VM_OK;
 }
@@ -938,14 +944,10 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
   cudaFuncSetAttribute(k_conv_wgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
-  int nsm = vm_num_sms(0);
-  int grid = p.units;
-  if (grid > nsm) grid = (nsm / p.n_mtgroups) * p.n_mtgroups;  // CTA keeps one M-tile group
-  if (grid < p.n_mtgroups) grid = p.n_mtgroups;
-  k_conv_wgrad_tc<<<grid, 192, (size_t)p.stages * p.stage_bytes, st>>>(gmap, p);
+  k_conv_wgrad_tc<<<p.grid, 192, (size_t)p.stages * p.stage_bytes, st>>>(gmap, p);
   rc = launch_status("vm_conv3d_wgrad_tc");
   if (rc) return rc;
-  const int nk = B * p.ksplit;
+  const int nk = p.grid / p.n_mtgroups;
   const int64_t E = (int64_t)p.MT * 3 * p.Nc * 128;
   k_wgrad_tc_finalize<<<grid_for(E, 256), 256, 0, st>>>(p.ws, gw, gb, nk, p.MT, p.Nc, p.CG, Cin, Cout,
                                                          p.ones_slot, p.runs);

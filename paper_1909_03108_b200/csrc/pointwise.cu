@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_head_bwd(
 // Fixed-shape head kernels (C input channels, NC classes known at compile time): all
 // per-voxel state and the weight-gradient partials live in registers.
 template <typename T, int C, int NC>
-__global__ void __launch_bounds__(kHeadThreads) k_head_fwd_fixed(
+__global__ void __launch_bounds__(kHeadThreads, 2) k_head_fwd_fixed(
     const T* __restrict__ y, Slab sy, const float* __restrict__ W, const float* __restrict__ bias,
     const float* __restrict__ onehot, float* __restrict__ probs, float* __restrict__ partials, int B,
     float clamp) {
@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_head_fwd_fixed(
 }
 
 template <typename T, int C, int NC>
-__global__ void __launch_bounds__(kHeadThreads) k_head_bwd_fixed(
+__global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_fixed(
     const T* __restrict__ y, Slab sy, const float* __restrict__ W, const float* __restrict__ bias,
     const float* __restrict__ onehot, const float* __restrict__ stats, T* __restrict__ g, Slab sg,
     float* __restrict__ wpart, int B, float w_dice, float w_ce, float total, int dice_mask, float clamp,
@@ -506,12 +506,16 @@ __global__ void __launch_bounds__(kHeadThreads) k_head_bwd_fixed(
   }
 }
 
+// one warp per column; lanes take strided rows, then a fixed shuffle tree (deterministic)
 __global__ void k_reduce_rows(const float* __restrict__ part, int rows, int width,
                               float* __restrict__ out) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < width; j += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x % 32;
+  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) / 32; j < width; j += gridDim.x * blockDim.x / 32) {
     float s = 0.f;
-    for (int r = 0; r < rows; ++r) s += part[(int64_t)r * width + j];
-    out[j] = s;
+    for (int r = lane; r < rows; r += 32) s += part[(int64_t)r * width + j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[j] = s;
   }
 }
 
@@ -660,7 +664,7 @@ extern "C" int vm_head_fwd(int dtype, const void* y, int64_t y_bstride, const fl
 
 extern "C" int vm_reduce_rows(const float* partials, int rows, int width, float* out, void* stream) {
   VM_REQUIRE(partials && out && rows > 0 && width > 0, VM_E_ARG, "vm_reduce_rows: bad argument");
-  k_reduce_rows<<<(width + 127) / 128, 128, 0, as_stream(stream)>>>(partials, rows, width, out);
+  k_reduce_rows<<<(width + 3) / 4, 128, 0, as_stream(stream)>>>(partials, rows, width, out);
   return launch_status("vm_reduce_rows");
 }
 
