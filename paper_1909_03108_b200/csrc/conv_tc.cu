@@ -37,6 +37,7 @@ using bf16 = __nv_bfloat16;
 constexpr int kBoxR = 128;  // TMA box height (rows of 8 bf16 = 16 B)
 constexpr int kMaxStages = 6;
 constexpr int kSmemBudget = 220 * 1024;
+constexpr bool kFoldEnabled = false;
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -93,6 +94,7 @@ struct PackGeom {
   int cin, cout;   // of the conv this operand feeds
   int CG, KC;      // input channel groups, chunks of 2 groups
   int Nc, nchunk;  // N per chunk (multiple of 16, <= 256)
+  int fold;        // thin output (Nc <= 32): kw folded into N, layout [kc][kd][kh][2][3*Nc][8]
 };
 
 __host__ __device__ static PackGeom pack_geom(int cin, int cout) {
@@ -104,39 +106,59 @@ __host__ __device__ static PackGeom pack_geom(int cin, int cout) {
   int npad = (cout + 15) / 16 * 16;
   g.nchunk = (npad + 255) / 256;
   g.Nc = ((npad + g.nchunk - 1) / g.nchunk + 15) / 16 * 16;
+  // kw-folded kernel (k_conv_fwd_fold): correct, but on B200 its shift-add epilogue is
+  // CUDA-core bound (~10 instr / output) and loses to the plain kernel; kept, not selected.
+  g.fold = (kFoldEnabled && g.nchunk == 1 && g.Nc <= 32) ? 1 : 0;
   return g;
+}
+
+// Value of packed element `r` (see PackGeom for the two layouts).  flip = 1 packs the dgrad
+// operand W'[t'][ci'][co'] = W[26 - t'][co'][ci'].
+__device__ __forceinline__ float pack_value(const PackGeom& g, int64_t r, const float* __restrict__ w,
+                                            int layer_cin, int layer_cout, int flip) {
+  const int e = r % 8;
+  r /= 8;
+  int kd, kh, kw, kc, nch, co, half;
+  if (g.fold) {
+    const int n = r % (3 * g.Nc);
+    r /= 3 * g.Nc;
+    half = r % 2;
+    r /= 2;
+    kh = r % 3;
+    r /= 3;
+    kd = r % 3;
+    kc = (int)(r / 3);
+    kw = n / g.Nc;
+    co = n % g.Nc;
+    nch = 0;
+  } else {
+    const int n = r % g.Nc;
+    r /= g.Nc;
+    half = r % 2;
+    r /= 2;
+    const int j = r % 9;
+    r /= 9;
+    kd = r % 3;
+    r /= 3;
+    kc = r % g.KC;
+    nch = (int)(r / g.KC);
+    kh = j / 3;
+    kw = j % 3;
+    co = nch * g.Nc + n;
+  }
+  const int t = (kd * 3 + kh) * 3 + kw;
+  const int ci = (kc * 2 + half) * 8 + e;
+  if (ci >= g.cin || co >= g.cout) return 0.f;
+  return !flip ? w[((int64_t)t * layer_cin + ci) * layer_cout + co]
+               : w[((int64_t)(26 - t) * layer_cin + co) * layer_cout + ci];
 }
 
 __global__ void k_pack_weights(const float* __restrict__ w, bf16* __restrict__ out, PackGeom g,
                                int layer_cin, int layer_cout, int flip) {
-  const int64_t per_tap = 2LL * g.Nc * 8;
-  const int64_t total = (int64_t)g.nchunk * g.KC * 27 * per_tap;
+  const int64_t total = (int64_t)g.nchunk * g.KC * 27 * 2LL * g.Nc * 8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int e = i % 8;
-    int64_t r = i / 8;
-    int n = r % g.Nc;
-    r /= g.Nc;
-    int half = r % 2;
-    r /= 2;
-    int j = r % 9;
-    r /= 9;
-    int kd = r % 3;
-    r /= 3;
-    int kc = r % g.KC;
-    int nch = (int)(r / g.KC);
-    int t = kd * 9 + j;
-    int ci = (kc * 2 + half) * 8 + e;
-    int co = nch * g.Nc + n;
-    float v = 0.f;
-    if (ci < g.cin && co < g.cout) {
-      if (!flip)
-        v = w[((int64_t)t * layer_cin + ci) * layer_cout + co];
-      else  // conv cin = layer cout, conv cout = layer cin
-        v = w[((int64_t)(26 - t) * layer_cin + co) * layer_cout + ci];
-    }
-    out[i] = __float2bfloat16_rn(v);
-  }
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __float2bfloat16_rn(pack_value(g, i, w, layer_cin, layer_cout, flip));
 }
 
 // ------------------------------------------------------------------ forward kernel
@@ -165,6 +187,7 @@ struct FwdParams {
   uint32_t idesc;
   unsigned flags;
   long long* dbg;  // optional timing probes [gridDim][4]
+  int TS;          // anchors between consecutive tiles (128; 126 in the kw-folded kernel)
   uint32_t wp_magic, hp_magic;  // floor(2^32 / d) + 1 for the anchor (w, h) split
 };
 
@@ -420,6 +443,9 @@ struct WgParams {
   int runs;         // 1: stage one run of KS+2Wp+2 rows per (kd, cg) serving all three kh
                     //    (M slot g' = (kd*CG + cg)*3 + kh, slot stride Wp rows); 0: one copy per slot
   int runs_alloc;   // run slots per stage buffer (runs mode)
+  int fold;         // 1: kw folded into N (B = three kw-shifted copies of gy made in SMEM)
+  int RRg;          // fold mode: rows of the raw gy box (KS + 16, 8-row aligned start)
+  uint32_t gc_off;  // fold mode: offset of the shifted-copy region from the gy box
   int spk;          // stages per unit (K-split chunk)
   int ksplit;       // K-split chunks per sample
   int stages_total; // per sample
@@ -436,7 +462,7 @@ struct WgParams {
 __global__ void __launch_bounds__(192, 1)
     k_conv_wgrad_tc(const __grid_constant__ CUtensorMap gmap, const WgParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t full[kMaxStages], empty[kMaxStages], tfull, tempty;
+  __shared__ uint64_t full[kMaxStages], empty[kMaxStages], ready[kMaxStages], tfull, tempty;
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int mg_cta = blockIdx.x % p.n_mtgroups;  // every unit of this CTA has the same M-tile group
@@ -460,6 +486,7 @@ __global__ void __launch_bounds__(192, 1)
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&ready[s], 128);
     }
     mbar_init(&tfull, 1);
     mbar_init(&tempty, 128);
@@ -499,7 +526,9 @@ __global__ void __launch_bounds__(192, 1)
           uint8_t* sG = sA + p.a_bytes;
           mbar_arrive_expect_tx(&full[stage], tx);
           const int gr0 = (int)(k0 + p.P + p.Wp + 1);
-          if (p.gwide)
+          if (p.fold)
+            tma_load_4d(sG, &gmap, &full[stage], 0, (gr0 - 2) >> 3, 0, b);
+          else if (p.gwide)
             tma_load_4d(sG, &gmap, &full[stage], 0, (gr0 - p.gdelta) >> 3, 0, b);
           else
             tma_load_4d(sG, &gmap, &full[stage], 0, gr0, 0, b);
@@ -537,9 +566,26 @@ __global__ void __launch_bounds__(192, 1)
       const int ks = (u / p.n_mtgroups) % p.ksplit;
       const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
       for (int s = s0; s < s1; ++s) {
-        mbar_wait(&full[stage], phase);
+        mbar_wait(p.fold ? &ready[stage] : &full[stage], phase);
         tc_fence_after();
-        if (elect_one()) {
+        if (p.fold && elect_one()) {
+          // kw folded into N: one MMA per (M-tile, K step), N = 3*Nc over the shifted gy copies
+          const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes);
+          const uint32_t sC = sA + p.a_bytes + p.gc_off;
+          const uint64_t b0desc = make_sdesc(sC, 128, (uint32_t)p.KS * 16);
+          const uint64_t a0desc = make_sdesc(sA + (uint32_t)slot_shift * GS, 128, sbo);
+          const uint32_t mstep = 16 * (GS >> 4);
+#pragma unroll 1
+          for (int kk = 0; kk < p.KS / 16; ++kk) {
+            const uint32_t acc = (started || kk > 0) ? 1u : 0u;
+            const uint64_t bdesc = b0desc + (uint64_t)(kk * 16);
+#pragma unroll 1
+            for (int m = 0; m < nmt; ++m)
+              mma_bf16_ss(tbase + (uint32_t)(m * 3 * p.Nc), a0desc + (uint64_t)(m * mstep + kk * 16), bdesc,
+                          p.idesc, acc);
+          }
+          mma_commit(&empty[stage]);
+        } else if (!p.fold && elect_one()) {
           const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes);
           const uint32_t sG = sA + p.a_bytes;
           const uint64_t b0desc = make_sdesc(sG + (uint32_t)p.gdelta * 16, 128, (uint32_t)p.RR * 16);
@@ -571,6 +617,38 @@ __global__ void __launch_bounds__(192, 1)
     if (elect_one()) mma_commit(&tfull);
     __syncwarp();
   } else {
+    if (p.fold) {
+      // gy shift workers: copy kw[u] = raw[u + delta - kw] for kw = 0..2, every stage
+      const int et = threadIdx.x - 64;
+      const int ngo = p.Nc / 8;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const int ks = (u / p.n_mtgroups) % p.ksplit;
+        const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
+        for (int s = s0; s < s1; ++s) {
+          const int64_t k0 = (int64_t)s * p.KS;
+          const int gr0 = (int)(k0 + p.P + p.Wp + 1);
+          const int delta = gr0 - ((gr0 - 2) & ~7);
+          mbar_wait(&full[stage], phase);
+          const int4* raw = reinterpret_cast<const int4*>(smem + (size_t)stage * p.stage_bytes + p.a_bytes);
+          int4* cp = reinterpret_cast<int4*>(smem + (size_t)stage * p.stage_bytes + p.a_bytes + p.gc_off);
+          const int total = 3 * p.CGo * p.KS;
+          for (int i = et; i < total; i += 128) {
+            const int uu = i % p.KS;
+            const int cgo = (i / p.KS) % p.CGo;
+            const int kw = i / (p.KS * p.CGo);
+            cp[(kw * ngo + cgo) * p.KS + uu] = raw[cgo * p.RRg + uu + delta - kw];
+          }
+          fence_proxy_async_smem();
+          mbar_arrive(&ready[stage]);
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
     const int q = warp & 3;
     const int kidx = blockIdx.x / p.n_mtgroups;
     mbar_wait(&tfull, 0);
@@ -633,6 +711,270 @@ __global__ void k_wgrad_tc_finalize(const float* __restrict__ ws, float* __restr
   }
 }
 
+
+// ------------------------------------------------------------------ forward, kw folded into N
+// Thin outputs (Cout <= 32): the three kw taps are stacked along N (N = 3*Nc), so a tile
+// needs only 9 (kd,kh) MMAs per 16 input channels instead of 27, and the kw shift moves to
+// the output side: out[a] = P0[a] + P1[a+1] + P2[a+2] (P_kw = accumulator column block kw).
+// Tiles of 128 anchor rows overlap by 2 (stride 126); the epilogue combines rows across TMEM
+// lanes with warp shuffles plus a 3-value exchange in shared memory at warp boundaries.
+__global__ void __launch_bounds__(320, 1)
+    k_conv_fwd_fold(const FwdParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ float sbias[1024];
+  __shared__ float sx[2][2][4][3][32];  // [tile parity][tile-iteration parity][quarter][C1 l0, C2 l0, C2 l1][ch]
+  __shared__ uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int N3 = 3 * p.Nc;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 256);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tslot;
+  const int nstage_k = p.KC * 3;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const int mb = u % p.mblocks;
+        const int b = u / p.mblocks;
+        const int64_t a0 = (int64_t)mb * p.MB * p.TS;
+        for (int kc = 0; kc < p.KC; ++kc) {
+          const int ng = (kc * 2 + 1 < p.CG) ? 2 : 1;
+          for (int kd = 0; kd < 3; ++kd) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sA = smem + (size_t)stage * p.stage_bytes;
+            uint8_t* sB = sA + 2 * p.a_bytes;
+            mbar_arrive_expect_tx(&full[stage], (uint32_t)ng * p.R * 16 + p.b_bytes);
+            for (int g = 0; g < ng; ++g)
+              bulk_load(sA + (size_t)g * p.a_bytes,
+                        p.x + b * p.x_bstride + (kc * 2 + g) * p.plane8 + (a0 + (int64_t)kd * p.P) * 8,
+                        (uint32_t)p.R * 16, &full[stage]);
+            bulk_load(sB, p.wpk + ((int64_t)kc * 3 + kd) * (p.b_bytes / 2), p.b_bytes, &full[stage]);
+            if (++stage == p.stages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    int stage = 0;
+    uint32_t phase = 0;
+    int ab = 0;
+    uint32_t aphase = 0;
+    long long t_wait_tmem = 0, t_wait_full = 0, t_start = clock64();
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      long long tw0 = clock64();
+      mbar_wait(&tempty[ab], aphase ^ 1);
+      t_wait_tmem += clock64() - tw0;
+      tc_fence_after();
+      for (int s = 0; s < nstage_k; ++s) {
+        const int kc = s / 3;
+        const int ng = (kc * 2 + 1 < p.CG) ? 2 : 1;
+        long long tf0 = clock64();
+        mbar_wait(&full[stage], phase);
+        t_wait_full += clock64() - tf0;
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes);
+          const uint32_t sB = sA + 2 * p.a_bytes;
+          const uint64_t a0desc = make_sdesc(sA, ng == 2 ? p.a_bytes : 0, 128);
+          const uint64_t b0desc = make_sdesc(sB, N3 * 16, 128);
+          const uint32_t d0 = tbase + (uint32_t)(ab * p.MB * N3);
+          const uint32_t bstep = (uint32_t)(2 * N3 * 16) >> 4;
+#pragma unroll 1
+          for (int kh = 0; kh < 3; ++kh) {
+            const uint64_t bdesc = b0desc + (uint64_t)(kh * bstep);
+            const uint64_t adesc = a0desc + (uint64_t)(kh * p.Wp);
+            const uint32_t acc = (s > 0 || kh > 0) ? 1u : 0u;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (i < p.MB)
+                mma_bf16_ss(d0 + (uint32_t)(i * N3), adesc + (uint64_t)(i * p.TS), bdesc, p.idesc, acc);
+            }
+          }
+          mma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == p.stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (elect_one()) mma_commit(&tfull[ab]);
+      __syncwarp();
+      if (++ab == 2) {
+        ab = 0;
+        aphase ^= 1;
+      }
+    }
+    if (p.dbg && lane == 0) {
+      p.dbg[blockIdx.x * 4 + 0] = clock64() - t_start;
+      p.dbg[blockIdx.x * 4 + 1] = t_wait_tmem;
+      p.dbg[blockIdx.x * 4 + 2] = t_wait_full;
+    }
+  } else {
+    // epilogue warps 2..9: warp w drains lane quarter (w & 3) of tiles with parity (w-2)/4
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int et = threadIdx.x - 64;
+    if (!(p.flags & VM_CONV_NOBIAS))
+      for (int c = et; c < p.Cout; c += 256) sbias[c] = p.bias[c];
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    const bool domask = p.flags & VM_CONV_MASK;
+    const int ngo = p.Nc / 8;
+    int ab = 0;
+    uint32_t aphase = 0;
+    int cpar = 0;
+    long long e_wait = 0, e_ld = 0, e_bar = 0, e_rest = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const int mb = u % p.mblocks;
+      const int b = u / p.mblocks;
+      const int a0 = mb * p.MB * p.TS;
+      const bf16* mbase = p.mask + b * p.m_bstride;
+      bf16* ybase = p.y + b * p.y_bstride;
+      long long c0t = clock64();
+      mbar_wait(&tfull[ab], aphase);
+      e_wait += clock64() - c0t;
+      tc_fence_after();
+      for (int i = half; i < p.MB; i += 2) {
+        long long c1t = clock64();
+        const int r = q * 32 + lane;  // tile row
+        const int a = a0 + i * p.TS + r;
+        uint32_t qa = __umulhi((uint32_t)a, p.wp_magic);
+        if (qa * (uint32_t)p.Wp > (uint32_t)a) --qa;
+        if ((qa + 1) * (uint32_t)p.Wp <= (uint32_t)a) ++qa;
+        const int wq = a - (int)qa * p.Wp;
+        uint32_t qh = __umulhi(qa, p.hp_magic);
+        if (qh * (uint32_t)p.Hp > qa) --qh;
+        if ((qh + 1) * (uint32_t)p.Hp <= qa) ++qh;
+        const int hq = (int)qa - (int)qh * p.Hp;
+        const bool valid = r < p.TS && a < p.anchors && wq < p.W && hq < p.H;
+        const int64_t orow = (int64_t)a + p.P + p.Wp + 1;
+        const uint32_t tcol = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * p.MB + i) * N3);
+        // whole tile at once: masks (dgrad) first, then all 3*Nc accumulator columns, one
+        // exchange + barrier, then combine / store (ngo <= 4 since Nc <= 32)
+        int4 mk[4];
+        if (domask) {
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            mk[g] = (g < ngo && valid) ? __ldg(reinterpret_cast<const int4*>(mbase + g * p.plane8 + orow * 8))
+                                       : make_int4(0, 0, 0, 0);
+        }
+        uint32_t c0[32], c1[32], c2[32];
+        tmem_ld16(tcol, *reinterpret_cast<uint32_t(*)[16]>(&c0[0]));
+        tmem_ld16(tcol + (uint32_t)p.Nc, *reinterpret_cast<uint32_t(*)[16]>(&c1[0]));
+        tmem_ld16(tcol + (uint32_t)(2 * p.Nc), *reinterpret_cast<uint32_t(*)[16]>(&c2[0]));
+        if (ngo > 2) {
+          tmem_ld16(tcol + 16u, *reinterpret_cast<uint32_t(*)[16]>(&c0[16]));
+          tmem_ld16(tcol + (uint32_t)(p.Nc + 16), *reinterpret_cast<uint32_t(*)[16]>(&c1[16]));
+          tmem_ld16(tcol + (uint32_t)(2 * p.Nc + 16), *reinterpret_cast<uint32_t(*)[16]>(&c2[16]));
+        }
+        tmem_ld_wait();
+        long long c2t = clock64();
+        e_ld += c2t - c1t;
+        float* x = &sx[half][cpar][0][0][0];  // [4 quarters][3][32]
+        // lanes 0 / 1 publish the values the previous quarter's lanes 30 / 31 need (branch-free)
+        {
+          const bool l0 = lane == 0, l1 = lane == 1;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            if (e < p.Nc) {
+              if (l0) x[(q * 3 + 0) * 32 + e] = __uint_as_float(c1[e]);
+              if (l0) x[(q * 3 + 1) * 32 + e] = __uint_as_float(c2[e]);
+              if (l1) x[(q * 3 + 2) * 32 + e] = __uint_as_float(c2[e]);
+            }
+          }
+        }
+#ifndef VM_EXPERIMENT_NOBAR
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory");
+#endif
+        long long c3t = clock64();
+        e_bar += c3t - c2t;
+        cpar ^= 1;  // next tile uses the other exchange buffer
+        const int qn = q < 3 ? q + 1 : 3;
+        const bool take1 = q < 3 && lane == 31, take2a = q < 3 && lane == 30, take2b = q < 3 && lane == 31;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          if (g >= ngo) break;
+          float v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int c = g * 8 + e;
+            const float n1s = __shfl_down_sync(0xffffffffu, __uint_as_float(c1[c]), 1);
+            const float n2s = __shfl_down_sync(0xffffffffu, __uint_as_float(c2[c]), 2);
+            const float f1 = x[(qn * 3 + 0) * 32 + c];  // broadcast reads, no divergence
+            const float f2a = x[(qn * 3 + 1) * 32 + c];
+            const float f2b = x[(qn * 3 + 2) * 32 + c];
+            const float n1 = take1 ? f1 : n1s;
+            const float n2 = take2a ? f2a : (take2b ? f2b : n2s);
+            v[e] = __uint_as_float(c0[c]) + n1 + n2;
+          }
+          const int co0 = g * 8;
+          if (valid && co0 < p.Cout) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (!(p.flags & VM_CONV_NOBIAS)) v[e] += (co0 + e < p.Cout) ? sbias[co0 + e] : 0.f;
+            if (p.flags & VM_CONV_RELU) {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
+            }
+            if (domask) {
+              const __nv_bfloat162* mh = reinterpret_cast<const __nv_bfloat162*>(&mk[g]);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                float2 f = __bfloat1622float2(mh[e]);
+                if (!(f.x > 0.f)) v[2 * e] = 0.f;
+                if (!(f.y > 0.f)) v[2 * e + 1] = 0.f;
+              }
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (co0 + e >= p.Cout) v[e] = 0.f;
+            int4 out;
+            __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&out);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) oh[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+            *reinterpret_cast<int4*>(ybase + g * p.plane8 + orow * 8) = out;
+          }
+        }
+        e_rest += clock64() - c3t;
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[ab]);
+      if (++ab == 2) {
+        ab = 0;
+        aphase ^= 1;
+      }
+    }
+    if (p.dbg && threadIdx.x == 64) {
+      p.dbg[4 * gridDim.x + blockIdx.x * 4 + 0] = e_wait;
+      p.dbg[4 * gridDim.x + blockIdx.x * 4 + 1] = e_ld;
+      p.dbg[4 * gridDim.x + blockIdx.x * 4 + 2] = e_bar;
+      p.dbg[4 * gridDim.x + blockIdx.x * 4 + 3] = e_rest;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tbase);
+}
+
 }  // namespace vm
 
 using namespace vm;
@@ -653,27 +995,8 @@ __global__ void k_pack_batch(const vm_pack_job* __restrict__ jobs, int njobs, in
     }
     const vm_pack_job& jb = jobs[lo];
     const PackGeom g = jb.flip ? pack_geom(jb.cout, jb.cin) : pack_geom(jb.cin, jb.cout);
-    int64_t r = i - jb.begin;
-    const int e = r % 8;
-    r /= 8;
-    const int n = r % g.Nc;
-    r /= g.Nc;
-    const int half = r % 2;
-    r /= 2;
-    const int j = r % 9;
-    r /= 9;
-    const int kd = r % 3;
-    r /= 3;
-    const int kc = r % g.KC;
-    const int nch = (int)(r / g.KC);
-    const int t = kd * 9 + j;
-    const int ci = (kc * 2 + half) * 8 + e;
-    const int co = nch * g.Nc + n;
-    float v = 0.f;
-    if (ci < g.cin && co < g.cout)
-      v = !jb.flip ? jb.w[((int64_t)t * jb.cin + ci) * jb.cout + co]
-                   : jb.w[((int64_t)(26 - t) * jb.cin + co) * jb.cout + ci];
-    static_cast<bf16*>(jb.packed)[i - jb.begin] = __float2bfloat16_rn(v);
+    static_cast<bf16*>(jb.packed)[i - jb.begin] =
+        __float2bfloat16_rn(pack_value(g, i - jb.begin, jb.w, jb.cin, jb.cout, jb.flip));
   }
 }
 
@@ -692,6 +1015,7 @@ extern "C" int vm_pack_weights(const float* w, void* packed, int Cin, int Cout, 
 }
 
 static long long* g_fwd_dbg = nullptr;
+
 extern "C" void vm_debug_set_fwd_probe(long long* buf) { g_fwd_dbg = buf; }
 
 extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wpacked,
@@ -732,21 +1056,24 @@ extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wp
   p.hp_magic = (uint32_t)(0x100000000ULL / (uint64_t)(H + 2)) + 1;
   VM_REQUIRE(Cout <= 1024, VM_E_UNSUPPORTED, "vm_conv3d_fwd_tc: Cout %d > 1024", Cout);
   p.b_bytes = 9 * 2 * p.Nc * 16;
-  const int tiles = (int)((p.anchors + 127) / 128);
-  // accumulators: 2 buffers x MB x Nc fp32 columns <= 512
+  const bool fold = pg.fold;  // packed layout and kernel are both chosen by shape
+  p.TS = fold ? 126 : 128;
+  const int N = fold ? 3 * p.Nc : p.Nc;  // accumulator columns per tile
+  const int tiles = (int)((p.anchors + p.TS - 1) / p.TS);
+  // accumulators: 2 buffers x MB x N fp32 columns <= 512
   int nsm = vm_num_sms(0);
   if (nsm <= 0) nsm = 148;
-  int MB = 256 / p.Nc;
+  int MB = 256 / N;
   if (MB > 8) MB = 8;
   const int mb_fill = (int)((int64_t)tiles * B * p.nchunk / nsm);  // keep >= 1 unit per SM
   if (MB > mb_fill) MB = mb_fill;
   if (MB < 1) MB = 1;
   for (;;) {
-    p.R = MB * 128 + 2 * p.Wp + 2;
+    p.R = (MB - 1) * p.TS + 128 + 2 * p.Wp + 2;
     p.Ralloc = (p.R + 7) / 8 * 8;
     p.a_bytes = (uint32_t)p.Ralloc * 16;
     p.stage_bytes = 2 * p.a_bytes + p.b_bytes;
-    p.stages = kSmemBudget / (int)p.stage_bytes;
+    p.stages = (fold ? kSmemBudget - 12 * 1024 : kSmemBudget) / (int)p.stage_bytes;  // fold: 11 KB static smem
     if (p.stages > kMaxStages) p.stages = kMaxStages;
     if (p.stages >= 2 || MB == 1) break;
     MB /= 2;
@@ -755,16 +1082,21 @@ extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wp
   p.MB = MB;
   p.mblocks = (tiles + MB - 1) / MB;
   p.units = B * p.mblocks * p.nchunk;
-  p.idesc = make_idesc_bf16(128, p.Nc, false, false);
+  p.idesc = make_idesc_bf16(128, N, false, false);
   p.x = static_cast<const bf16*>(x);
   p.x_bstride = x_bstride ? x_bstride : default_bstride(Cin, D, H, W, 1);
   VM_REQUIRE((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (p.x_bstride & 7) == 0, VM_E_ALIGN,
              "vm_conv3d_fwd_tc: slab must be 16-byte aligned");
   (void)rows;
   const size_t smem = (size_t)p.stages * p.stage_bytes;
-  cudaFuncSetAttribute(k_conv_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
   int grid = p.units < nsm ? p.units : nsm;
-  k_conv_fwd_tc<<<grid, 320, smem, as_stream(stream)>>>(p);
+  if (fold) {
+    cudaFuncSetAttribute(k_conv_fwd_fold, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_conv_fwd_fold<<<grid, 320, smem, as_stream(stream)>>>(p);
+  } else {
+    cudaFuncSetAttribute(k_conv_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_conv_fwd_tc<<<grid, 320, smem, as_stream(stream)>>>(p);
+  }
   return launch_status("vm_conv3d_fwd_tc");
 }
 
@@ -775,7 +1107,7 @@ struct WgPlan {
   size_t ws_main, ws_bias;
 };
 
-int g_force_runs = -1, g_force_ks = 0, g_force_mpu = 0;
+int g_force_runs = -1, g_force_ks = 0, g_force_mpu = 0, g_force_fold = 0;  // fold: opt-in (staging-bound, see DESIGN)
 
 int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
   WgParams& p = pl.p;
@@ -808,12 +1140,21 @@ int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
   const int mpu_max = p.mt_per_unit;
   const int ks_run = min(256, ((p.Wp - 2) / 16) * 16);
   int best_mpu = 0, best_ks = 0, best_runs = 0;
+  // kw folded into N (three shifted gy copies, N = 3*Nc) whenever it fits an MMA
+  const int fold = (p.gwide && 3 * p.Nc <= 256 && g_force_fold > 0) ? 1 : 0;
+  auto g_region = [&](int KS) -> uint32_t {  // gy bytes per stage (raw box [+ shifted copies])
+    if (fold) {
+      const uint32_t raw = ((uint32_t)p.CGo * (KS + 16) * 16 + 1023) & ~1023u;
+      return raw + 3u * (uint32_t)(p.Nc / 8) * KS * 16;
+    }
+    return (uint32_t)(p.Nc / 8) * (KS + 8) * 16;
+  };
   auto fits = [&](int runs, int KS, int mpu) {
     const int RR = KS + 8;
     if (!p.gwide && RR > 256) return false;
     const int ralloc = (16 * mpu + 2) / 3 + 2;
     const uint32_t a_b = ((runs ? (uint32_t)ralloc * 3 * p.Wp * 16 : (uint32_t)mpu * 16 * RR * 16) + 1023) & ~1023u;
-    const uint32_t stage = (a_b + (uint32_t)(p.Nc / 8) * RR * 16 + 1023) & ~1023u;
+    const uint32_t stage = (a_b + g_region(KS) + 1023) & ~1023u;
     return kSmemBudget / (int)stage >= 2;
   };
   auto forced_ok = [&](int runs, int KS, int mpu) {
@@ -838,17 +1179,20 @@ int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
   p.mt_per_unit = best_mpu;
   p.KS = best_ks;
   p.runs = best_runs;
+  p.fold = fold;
   p.RR = p.KS + 8;
+  p.RRg = p.KS + 16;
   p.runs_alloc = (16 * p.mt_per_unit + 2) / 3 + 2;
   // TMA tensor destinations (the gy box) must be 128-byte aligned: keep every region 1 KB aligned
   p.a_bytes = ((p.runs ? (uint32_t)p.runs_alloc * 3 * p.Wp * 16 : (uint32_t)p.mt_per_unit * 16 * p.RR * 16) + 1023) & ~1023u;
-  p.g_bytes = (uint32_t)p.CGo * p.RR * 16;
-  p.stage_bytes = (p.a_bytes + (uint32_t)(p.Nc / 8) * p.RR * 16 + 1023) & ~1023u;
+  p.g_bytes = (uint32_t)p.CGo * (fold ? p.RRg : p.RR) * 16;
+  p.gc_off = fold ? (((uint32_t)p.CGo * p.RRg * 16 + 1023) & ~1023u) : 0;
+  p.stage_bytes = (p.a_bytes + g_region(p.KS) + 1023) & ~1023u;
   p.stages = kSmemBudget / (int)p.stage_bytes;
   if (p.stages > kMaxStages) p.stages = kMaxStages;
   VM_REQUIRE(p.stages >= 2 && p.mt_per_unit >= 1, VM_E_UNSUPPORTED, "vm_conv3d_wgrad_tc: stage does not fit");
   p.n_mtgroups = (p.MT + p.mt_per_unit - 1) / p.mt_per_unit;
-  const int64_t anchors = (int64_t)D * p.P;
+  const int64_t anchors = (int64_t)D * p.P + 2;  // + kw shift of the folded B operand
   p.stages_total = (int)((anchors + p.KS - 1) / p.KS);
   int nsm = vm_num_sms(0);
   if (nsm <= 0) nsm = 148;
@@ -858,7 +1202,7 @@ int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
   if (p.spk < 4) p.spk = 4;
   p.ksplit = (p.stages_total + p.spk - 1) / p.spk;
   p.units = p.n_mtgroups * B * p.ksplit;
-  p.idesc = make_idesc_bf16(128, p.Nc, true, true);
+  p.idesc = make_idesc_bf16(128, p.fold ? 3 * p.Nc : p.Nc, true, true);
   p.grid = p.units;
   if (p.grid > nsm) p.grid = (nsm / p.n_mtgroups) * p.n_mtgroups;  // CTA keeps one M-tile group
   if (p.grid < p.n_mtgroups) p.grid = p.n_mtgroups;
@@ -900,6 +1244,8 @@ int make_group_map(CUtensorMap* m, const void* base, int64_t bstride, int CG, in
 }
 }  // namespace
 
+extern "C" void vm_debug_force_wgrad_fold(int fold) { g_force_fold = fold; }
+
 extern "C" void vm_debug_force_wgrad_plan(int runs, int ks, int mpu) {
   g_force_runs = runs;
   g_force_ks = ks;
@@ -939,7 +1285,7 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
   const int64_t gbs = gy_bstride ? gy_bstride : default_bstride(Cout, D, H, W, 1);
   const int64_t rows = (int64_t)(D + 2) * p.P;
   CUtensorMap gmap;
-  rc = p.gwide ? make_wide_map(&gmap, gy, gbs, p.CGo, rows, B, p.RR / 8, p.CGo)
+  rc = p.gwide ? make_wide_map(&gmap, gy, gbs, p.CGo, rows, B, (p.fold ? p.RRg : p.RR) / 8, p.CGo)
                : make_group_map(&gmap, gy, gbs, p.CGo, rows, B, p.RR, p.CGo);
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);

@@ -3,7 +3,7 @@ sys.path.insert(0, '/root/repo')
 from paper_1909_03108_b200 import _lib
 from paper_1909_03108_b200.step import Slab
 lib=_lib.load()
-buf=torch.zeros(148*4, dtype=torch.int64, device='cuda')
+buf=torch.zeros(148*8, dtype=torch.int64, device='cuda')
 lib.vm_debug_set_fwd_probe.argtypes=[ctypes.c_void_p]
 for (ci,co,e) in [(16,16,128),(32,32,64),(48,16,128)]:
     x=Slab(1,ci,e,e,e,torch.bfloat16,'cuda'); y=Slab(1,co,e,e,e,torch.bfloat16,'cuda'); x.storage.normal_()
@@ -17,5 +17,5 @@ for (ci,co,e) in [(16,16,128),(32,32,64),(48,16,128)]:
         e0.record()
         _lib.call("vm_conv3d_fwd_tc",x.p(),x.bstride,_lib.ptr(wp),_lib.ptr(b),y.p(),y.bstride,None,0,1,ci,co,e,e,e,1,st)
         e1.record(); torch.cuda.synchronize()
-    d=buf.view(148,4).cpu().float()
-    print(ci,co,e, f"{e0.elapsed_time(e1)*1e3:.1f}us", "total cyc %.0f  wait_tmem %.0f  wait_full %.0f  epi_wait %.0f" % tuple(d.mean(0).tolist()))
+    d=buf.view(2,148,4).cpu().float()
+    print(ci,co,e, f"{e0.elapsed_time(e1)*1e3:.1f}us", "MMA: total %.0f wait_tmem %.0f wait_full %.0f x" % tuple(d[0].mean(0).tolist()[:3]), "EPI: wait %.0f ld %.0f bar %.0f rest %.0f" % tuple(d[1].mean(0).tolist()))

@@ -12,27 +12,30 @@ for cin, cout, e in shapes:
     x.storage.normal_(); g.storage.normal_()
     gw = torch.zeros(27 * cin * cout, device="cuda"); gb = torch.zeros(cout, device="cuda")
     res = []
-    for runs in (0, 1):
-        for ks in (64, 128, 192, 256):
-            for mpu in range(1, 10):
-                lib.vm_debug_force_wgrad_plan(runs, ks, mpu)
-                out = (ctypes.c_int * 12)()
-                if lib.vm_debug_wgrad_plan(1, cin, cout, e, e, e, out) != 0:
-                    continue
-                pl = dict(zip(names, list(out)))
-                if pl["runs"] != runs or pl["KS"] != ks or pl["mpu"] != mpu:
-                    continue
-                nb = lib.vm_conv3d_wgrad_tc_ws(1, cin, cout, e, e, e)
-                ws = torch.empty(nb // 4 + 64, device="cuda")
-                st = _lib.stream_ptr()
-                args = (x.p(), x.bstride, g.p(), g.bstride, _lib.ptr(gw), _lib.ptr(gb), _lib.ptr(ws), 1, cin, cout, e, e, e, st)
-                _lib.call("vm_conv3d_wgrad_tc", *args)
-                e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-                e0.record()
-                for _ in range(5):
-                    _lib.call("vm_conv3d_wgrad_tc", *args)
-                e1.record(); torch.cuda.synchronize()
-                res.append((e0.elapsed_time(e1) / 5 * 1e3, runs, ks, mpu, pl["stages"]))
+    for fold in (0, 1):
+      lib.vm_debug_force_wgrad_fold(fold)
+      for runs in (0, 1):
+          for ks in (64, 128, 192, 256):
+              for mpu in range(1, 10):
+                  lib.vm_debug_force_wgrad_plan(runs, ks, mpu)
+                  out = (ctypes.c_int * 12)()
+                  if lib.vm_debug_wgrad_plan(1, cin, cout, e, e, e, out) != 0:
+                      continue
+                  pl = dict(zip(names, list(out)))
+                  if pl["runs"] != runs or pl["KS"] != ks or pl["mpu"] != mpu:
+                      continue
+                  nb = lib.vm_conv3d_wgrad_tc_ws(1, cin, cout, e, e, e)
+                  ws = torch.empty(nb // 4 + 64, device="cuda")
+                  st = _lib.stream_ptr()
+                  args = (x.p(), x.bstride, g.p(), g.bstride, _lib.ptr(gw), _lib.ptr(gb), _lib.ptr(ws), 1, cin, cout, e, e, e, st)
+                  _lib.call("vm_conv3d_wgrad_tc", *args)
+                  e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+                  e0.record()
+                  for _ in range(5):
+                      _lib.call("vm_conv3d_wgrad_tc", *args)
+                  e1.record(); torch.cuda.synchronize()
+                  res.append((round(e0.elapsed_time(e1) / 5 * 1e3, 1), "fold%d" % fold, runs, ks, mpu, pl["stages"]))
+    lib.vm_debug_force_wgrad_fold(-1)
     lib.vm_debug_force_wgrad_plan(-1, 0, 0)
     out = (ctypes.c_int * 12)(); lib.vm_debug_wgrad_plan(1, cin, cout, e, e, e, out)
     pl = dict(zip(names, list(out)))
