@@ -39,6 +39,41 @@ def load_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback (B200_PROFILING.md)"
 
 
+def load_traffic(kind):
+    """roofline.traffic: DRAM bytes (read+write) per launch of ``kind``, from the newest
+    committed ncu step capture (dram__bytes_read.sum + dram__bytes_write.sum per launch) (profiles/r*/ncu_step_dram.json, written by
+    tools/ncu_summary.py --map); None when no capture is committed."""
+    import glob
+
+    caps = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_step_dram.json")))
+    if not caps:
+        return None, None
+    try:
+        by = json.load(open(caps[-1]))["by_kind"]
+        return by[kind]["dram_bytes_per_call"], os.path.relpath(caps[-1], ROOT)
+    except Exception:
+        return None, os.path.relpath(caps[-1], ROOT)
+
+
+def _capture(torch, fn):
+    """Capture ``fn`` as one CUDA graph on a side stream; None if capture fails (e.g. a
+    collective that cannot be captured), in which case the step runs eagerly."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    try:
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                fn()
+    except Exception as e:  # pragma: no cover - GPU path
+        print(f"[bench] CUDA graph capture failed ({e}); running eagerly", file=sys.stderr)
+        torch.cuda.synchronize()
+        return None
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    return g
+
+
 def args_parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -234,15 +269,11 @@ def run_ours(a):
     torch.cuda.synchronize()
     launches_per_step = _lib.load().vm_launch_count() - l0
     graph_obj = None
+    graph_note = "disabled (--no-graph)" if a.no_graph else "captured"
     if not a.no_graph:
-        s = torch.cuda.Stream()
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
-            graph_obj = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph_obj, stream=s):
-                st.step()
-        torch.cuda.current_stream().wait_stream(s)
-        torch.cuda.synchronize()
+        graph_obj = _capture(torch, st.step)
+        if graph_obj is None:
+            graph_note = "capture failed, eager launches"
 
     def one():
         if graph_obj is not None:
@@ -300,20 +331,15 @@ def run_ours(a):
     if world > 1:
         st.has_halo_saved = st.has_halo
         st.has_halo = False
-        g2 = torch.cuda.CUDAGraph()
-        s = torch.cuda.Stream()
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
-            with torch.cuda.graph(g2, stream=s):
-                st.step()
-        torch.cuda.current_stream().wait_stream(s)
+        g2 = _capture(torch, st.step) if graph_obj is not None else None
+        run2 = g2.replay if g2 is not None else st.step
         for _ in range(a.warmup):
-            g2.replay()
+            run2()
         barrier()
         h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         h0.record()
         for _ in range(a.steps):
-            g2.replay()
+            run2()
         h1.record()
         h1.synchronize()
         ms_nohalo = h0.elapsed_time(h1) / a.steps
@@ -337,16 +363,21 @@ def run_ours(a):
     dom_kind = max(classes, key=lambda k: classes[k]["ms"])
     dom = classes[dom_kind]
     step_kernel_ms = sum(c["ms"] for c in classes.values())
+    traffic, traffic_src = load_traffic(dom_kind)
     if dom["flops"] > 0:
         achieved = dom["flops"] / (dom["ms"] * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / peaks["bf16_tflops"], "traffic": None}
+                "frac": achieved / peaks["bf16_tflops"], "traffic": traffic}
     else:
         achieved = dom["bytes"] / (dom["ms"] * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": None}
+                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic}
     roof.update({"kernel": dom_kind, "launches_per_step": dom["launches"],
-                 "share_of_kernel_time": dom["ms"] / step_kernel_ms, "peak_source": peak_src})
+                 "algorithmic_bytes_per_launch": dom["bytes"] / max(dom["launches"], 1),
+                 "flops_per_launch": dom["flops"] / max(dom["launches"], 1),
+                 "avg_launch_ms": dom["ms"] / max(dom["launches"], 1),
+                 "share_of_kernel_time": dom["ms"] / step_kernel_ms, "peak_source": peak_src,
+                 "traffic_source": traffic_src})
     conv_flops = graph.conv_flops(a.batch) * (world * E ** 3) / (E ** 3) / world  # per rank
     conv_ms = sum(c["ms"] for k, c in classes.items() if k.startswith("conv"))
     if a.layer_csv and rank == 0:
@@ -388,7 +419,7 @@ def run_ours(a):
             "volume": [E * world, E, E],
             "parallelism": f"spatial depth-split x{world}" if world > 1 else "single GPU",
             "conv": a.conv,
-            "cuda_graph": graph_obj is not None,
+            "cuda_graph": graph_note,
             "l2": "working set (activation slabs, ~1.5 GB) >> 126 MB L2; no flush needed",
             "conv_tflop_per_step_rank": conv_flops / 1e12,
         },
