@@ -37,7 +37,6 @@ using bf16 = __nv_bfloat16;
 constexpr int kBoxR = 128;  // TMA box height (rows of 8 bf16 = 16 B)
 constexpr int kMaxStages = 6;
 constexpr int kSmemBudget = 220 * 1024;
-constexpr bool kFoldEnabled = false;
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -87,15 +86,22 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 }
 
 // ------------------------------------------------------------------ weight packing
-// Packed forward operand: [nchunk][kc][kd][9 taps (kh,kw)][2 K-halves][Nc][8] bf16, where
-// ci = (kc*2 + half)*8 + e, co = nchunk*Nc + n.  flip = 1 packs the dgrad operand:
-// W'[t'][ci'][co'] = W[26 - t'][co'][ci'] (conv of the output gradient).
+// Packed forward operand, two layouts chosen by shape (ci = (kc*2 + half)*8 + e):
+//  * plain  (k_conv_fwd_tc):    [nchunk][kc][kd][9 taps (kh,kw)][2 K-halves][Nc][8],
+//                               co = nchunk*Nc + n;
+//  * sweep  (k_conv_fwd_sweep): [kc][9 taps (kh,kw)][2 K-halves][3*Nc][8], row n holds
+//                               kd = 2 - n / Nc, co = n % Nc (thin outputs, Nc <= 32).
+// flip = 1 packs the dgrad operand W'[t'][ci'][co'] = W[26 - t'][co'][ci'] (conv of the
+// output gradient).  Both layouts hold the same number of elements.
 struct PackGeom {
   int cin, cout;   // of the conv this operand feeds
   int CG, KC;      // input channel groups, chunks of 2 groups
   int Nc, nchunk;  // N per chunk (multiple of 16, <= 256)
-  int fold;        // thin output (Nc <= 32): kw folded into N, layout [kc][kd][kh][2][3*Nc][8]
+  int sweep;       // 1: kd stacked along N (k_conv_fwd_sweep)
 };
+
+constexpr int kSweepMaxNc = 32;  // Nc = 48 (N = 144) measured slower than k_conv_fwd_tc
+constexpr uint32_t kSweepMaxWeightBytes = 100 * 1024;
 
 __host__ __device__ static PackGeom pack_geom(int cin, int cout) {
   PackGeom g;
@@ -106,31 +112,28 @@ __host__ __device__ static PackGeom pack_geom(int cin, int cout) {
   int npad = (cout + 15) / 16 * 16;
   g.nchunk = (npad + 255) / 256;
   g.Nc = ((npad + g.nchunk - 1) / g.nchunk + 15) / 16 * 16;
-  // kw-folded kernel (k_conv_fwd_fold): correct, but on B200 its shift-add epilogue is
-  // CUDA-core bound (~10 instr / output) and loses to the plain kernel; kept, not selected.
-  g.fold = (kFoldEnabled && g.nchunk == 1 && g.Nc <= 32) ? 1 : 0;
+  const uint32_t wbytes = (uint32_t)g.KC * 9 * 2 * 3 * g.Nc * 16;
+  g.sweep = (g.nchunk == 1 && g.Nc <= kSweepMaxNc && wbytes <= kSweepMaxWeightBytes) ? 1 : 0;
   return g;
 }
 
-// Value of packed element `r` (see PackGeom for the two layouts).  flip = 1 packs the dgrad
-// operand W'[t'][ci'][co'] = W[26 - t'][co'][ci'].
+// Value of packed element `r` (see PackGeom for the two layouts).
 __device__ __forceinline__ float pack_value(const PackGeom& g, int64_t r, const float* __restrict__ w,
                                             int layer_cin, int layer_cout, int flip) {
   const int e = r % 8;
   r /= 8;
-  int kd, kh, kw, kc, nch, co, half;
-  if (g.fold) {
+  int kd, kh, kw, kc, co, half;
+  if (g.sweep) {
     const int n = r % (3 * g.Nc);
     r /= 3 * g.Nc;
     half = r % 2;
     r /= 2;
-    kh = r % 3;
-    r /= 3;
-    kd = r % 3;
-    kc = (int)(r / 3);
-    kw = n / g.Nc;
+    const int j = r % 9;
+    kc = (int)(r / 9);
+    kh = j / 3;
+    kw = j % 3;
+    kd = 2 - n / g.Nc;
     co = n % g.Nc;
-    nch = 0;
   } else {
     const int n = r % g.Nc;
     r /= g.Nc;
@@ -141,7 +144,7 @@ __device__ __forceinline__ float pack_value(const PackGeom& g, int64_t r, const 
     kd = r % 3;
     r /= 3;
     kc = r % g.KC;
-    nch = (int)(r / g.KC);
+    const int nch = (int)(r / g.KC);
     kh = j / 3;
     kw = j % 3;
     co = nch * g.Nc + n;
@@ -187,7 +190,6 @@ struct FwdParams {
   uint32_t idesc;
   unsigned flags;
   long long* dbg;  // optional timing probes [gridDim][4]
-  int TS;          // anchors between consecutive tiles (128; 126 in the kw-folded kernel)
   uint32_t wp_magic, hp_magic;  // floor(2^32 / d) + 1 for the anchor (w, h) split
 };
 
@@ -712,30 +714,66 @@ __global__ void k_wgrad_tc_finalize(const float* __restrict__ ws, float* __restr
 }
 
 
-// ------------------------------------------------------------------ forward, kw folded into N
-// Thin outputs (Cout <= 32): the three kw taps are stacked along N (N = 3*Nc), so a tile
-// needs only 9 (kd,kh) MMAs per 16 input channels instead of 27, and the kw shift moves to
-// the output side: out[a] = P0[a] + P1[a+1] + P2[a+2] (P_kw = accumulator column block kw).
-// Tiles of 128 anchor rows overlap by 2 (stride 126); the epilogue combines rows across TMEM
-// lanes with warp shuffles plus a 3-value exchange in shared memory at warp boundaries.
+// ------------------------------------------------------------------ forward, kd stacked along N
+// Thin outputs (Nc <= 32): the three kd taps are stacked along N (N = 3*Nc, rows ordered
+// kd = 2, 1, 0) and a CTA sweeps a column of M tiles (MB*128 in-plane anchors) through a
+// segment of depth planes.  Input plane i contributes to output planes i-2, i-1, i, whose
+// accumulators are consecutive blocks of a TMEM ring (block = ring sequence mod ring), so
+// ONE MMA per (tap (kh,kw), K chunk, tile) covers all three kd taps: 9 MMAs of N = 3*Nc per
+// input plane instead of 27 of N = Nc, each input row is staged once per column instead of
+// three times, and the A operand (the expensive shared-memory read, ~32 cycles per MMA)
+// is read a third as often.  The first K step of a plane overwrites the block of output
+// plane i (a separate N = Nc MMA with enable_input_d = 0) and accumulates into the other
+// two; a block whose three contributions are issued is committed, drained (bias, ReLU /
+// mask, bf16) and handed back.  At the ring's end an MMA is split in two.  Weights stay
+// resident in shared memory.  (Pre-filling blocks with the bias by tcgen05.st instead
+// serialises the epilogue against in-flight MMAs: 5x slower on B200.)
+struct SwParams {
+  const bf16* x;
+  int64_t x_bstride;
+  const bf16* wpk;  // [KC][9][2][3*Nc][8], row n: kd = 2 - n / Nc, co = n % Nc
+  const float* bias;
+  bf16* y;
+  int64_t y_bstride;
+  const bf16* mask;
+  int64_t m_bstride;
+  int D, H, W, Hp, Wp, P;
+  int64_t plane8;
+  int CG, KC, Cout, Nc;
+  int MB;          // M tiles per column (independent accumulator chains: >= 3 hide MMA latency)
+  int R;           // staged rows per group per stage = MB*128 + 2*Wp + 2
+  int ncol, S, nseg, units;
+  int ring;        // TMEM blocks (of Nc columns) per tile
+  int stages;
+  uint32_t a_bytes, stage_bytes, w_bytes;
+  uint32_t idesc1, idesc2, idesc3;
+  unsigned flags;
+  long long* dbg;  // optional cycle probes [gridDim][8] (vm_debug_set_fwd_probe)
+  int xmode;       // experiment: 1 = skip the TMEM drain (wrong results)
+};
+constexpr int kSwMaxRing = 32;
+constexpr int kSwMaxStages = 8;
+
+template <int MB>
 __global__ void __launch_bounds__(320, 1)
-    k_conv_fwd_fold(const FwdParams p) {
+    k_conv_fwd_sweep(const SwParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ float sbias[1024];
-  __shared__ float sx[2][2][4][3][32];  // [tile parity][tile-iteration parity][quarter][C1 l0, C2 l0, C2 l1][ch]
-  __shared__ uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
+  __shared__ uint64_t full[kSwMaxStages], empty[kSwMaxStages], tfull[kSwMaxRing], tempty[kSwMaxRing], wbar;
   __shared__ uint32_t tslot;
+  __shared__ float sbias[kSweepMaxNc];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int N3 = 3 * p.Nc;
+  uint8_t* sW = smem;
+  uint8_t* sStage = smem + p.w_bytes;
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 256);
+    for (int r = 0; r < p.ring; ++r) {
+      mbar_init(&tfull[r], 1);
+      mbar_init(&tempty[r], 256);
     }
+    mbar_init(&wbar, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(&tslot);
@@ -743,28 +781,33 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = tslot;
-  const int nstage_k = p.KC * 3;
 
   if (warp == 0) {
+    // ===================== producer: resident weights, then one stage per (plane, K chunk)
     if (elect_one()) {
+      mbar_arrive_expect_tx(&wbar, p.w_bytes);
+      bulk_load(sW, p.wpk, p.w_bytes, &wbar);
       int stage = 0;
       uint32_t phase = 0;
+      long long t_pw = 0;
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        const int mb = u % p.mblocks;
-        const int b = u / p.mblocks;
-        const int64_t a0 = (int64_t)mb * p.MB * p.TS;
-        for (int kc = 0; kc < p.KC; ++kc) {
-          const int ng = (kc * 2 + 1 < p.CG) ? 2 : 1;
-          for (int kd = 0; kd < 3; ++kd) {
+        const int col = u % p.ncol;
+        const int seg = (u / p.ncol) % p.nseg;
+        const int b = u / (p.ncol * p.nseg);
+        const int o0 = seg * p.S, o1 = min(p.D, o0 + p.S);
+        const int64_t c0 = (int64_t)col * p.MB * 128;
+        const bf16* xb = p.x + b * p.x_bstride;
+        for (int i = o0; i < o1 + 2; ++i) {
+          for (int kc = 0; kc < p.KC; ++kc) {
+            const int ng = (kc * 2 + 1 < p.CG) ? 2 : 1;
+            const long long tw = clock64();
             mbar_wait(&empty[stage], phase ^ 1);
-            uint8_t* sA = smem + (size_t)stage * p.stage_bytes;
-            uint8_t* sB = sA + 2 * p.a_bytes;
-            mbar_arrive_expect_tx(&full[stage], (uint32_t)ng * p.R * 16 + p.b_bytes);
+            t_pw += clock64() - tw;
+            uint8_t* sA = sStage + (size_t)stage * p.stage_bytes;
+            mbar_arrive_expect_tx(&full[stage], (uint32_t)ng * p.R * 16);
             for (int g = 0; g < ng; ++g)
-              bulk_load(sA + (size_t)g * p.a_bytes,
-                        p.x + b * p.x_bstride + (kc * 2 + g) * p.plane8 + (a0 + (int64_t)kd * p.P) * 8,
+              bulk_load(sA + (size_t)g * p.a_bytes, xb + (kc * 2 + g) * p.plane8 + ((int64_t)i * p.P + c0) * 8,
                         (uint32_t)p.R * 16, &full[stage]);
-            bulk_load(sB, p.wpk + ((int64_t)kc * 3 + kd) * (p.b_bytes / 2), p.b_bytes, &full[stage]);
             if (++stage == p.stages) {
               stage = 0;
               phase ^= 1;
@@ -772,202 +815,236 @@ __global__ void __launch_bounds__(320, 1)
           }
         }
       }
+      if (p.dbg) p.dbg[blockIdx.x * 8 + 7] = t_pw;
     }
   } else if (warp == 1) {
+    // ===================== MMA issuer
+    const long long t0 = clock64();
+    long long t_te = 0, t_fu = 0, t_is = 0;
+    mbar_wait(&wbar, 0);
     int stage = 0;
     uint32_t phase = 0;
-    int ab = 0;
-    uint32_t aphase = 0;
-    long long t_wait_tmem = 0, t_wait_full = 0, t_start = clock64();
+    uint32_t nstart = 0;    // ring sequence of the unit's first block (plane o0 - 2)
+    uint32_t acquired = 0;  // ring sequences whose block has been re-armed and taken
+    const uint32_t wblk = (uint32_t)(2 * 3 * p.Nc * 16);  // bytes per (kc, tap) weight block
+    const uint32_t sWa = smem_u32(sW);
+    const uint32_t tstride = (uint32_t)(p.ring * p.Nc);   // TMEM columns per tile ring
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      long long tw0 = clock64();
-      mbar_wait(&tempty[ab], aphase ^ 1);
-      t_wait_tmem += clock64() - tw0;
-      tc_fence_after();
-      for (int s = 0; s < nstage_k; ++s) {
-        const int kc = s / 3;
-        const int ng = (kc * 2 + 1 < p.CG) ? 2 : 1;
-        long long tf0 = clock64();
-        mbar_wait(&full[stage], phase);
-        t_wait_full += clock64() - tf0;
+      const int seg = (u / p.ncol) % p.nseg;
+      const int o0 = seg * p.S, o1 = min(p.D, o0 + p.S);
+      const int nin = o1 - o0 + 2;
+      for (int k = 0; k < nin; ++k) {
+        const uint32_t n = nstart + (uint32_t)k;
+        const long long ta = clock64();
+        while (acquired <= n + 2) {
+          const uint32_t r = acquired % (uint32_t)p.ring;
+          mbar_wait(&tempty[r], (acquired / (uint32_t)p.ring) & 1u);
+          ++acquired;
+        }
+        t_te += clock64() - ta;
         tc_fence_after();
-        if (elect_one()) {
-          const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes);
-          const uint32_t sB = sA + 2 * p.a_bytes;
-          const uint64_t a0desc = make_sdesc(sA, ng == 2 ? p.a_bytes : 0, 128);
-          const uint64_t b0desc = make_sdesc(sB, N3 * 16, 128);
-          const uint32_t d0 = tbase + (uint32_t)(ab * p.MB * N3);
-          const uint32_t bstep = (uint32_t)(2 * N3 * 16) >> 4;
-#pragma unroll 1
-          for (int kh = 0; kh < 3; ++kh) {
-            const uint64_t bdesc = b0desc + (uint64_t)(kh * bstep);
-            const uint64_t adesc = a0desc + (uint64_t)(kh * p.Wp);
-            const uint32_t acc = (s > 0 || kh > 0) ? 1u : 0u;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              if (i < p.MB)
-                mma_bf16_ss(d0 + (uint32_t)(i * N3), adesc + (uint64_t)(i * p.TS), bdesc, p.idesc, acc);
-            }
-          }
-          mma_commit(&empty[stage]);
+        const uint32_t pos = n % (uint32_t)p.ring;
+        // Per-plane issue lists, so the issue loop is descriptor adds only (a single thread
+        // feeds the tensor core; per-MMA integer work shows up directly as MMA time).
+        // Normal K step: blocks pos..pos+2 <- B rows [0, 3Nc), split at the ring's end.
+        // First K step: blocks pos..pos+1 accumulate, block pos+2 (plane i) is overwritten.
+        const uint32_t ring = (uint32_t)p.ring, Nc = (uint32_t)p.Nc;
+        uint32_t nd[2], nid[2], nb[2], fd[3], fid[3], fb[3], facc[3];
+        int nn, nf;
+        if (pos + 3 <= ring) {
+          nn = 1;
+          nd[0] = pos * Nc, nid[0] = p.idesc3, nb[0] = 0;
+          nd[1] = 0, nid[1] = 0, nb[1] = 0;
+        } else if (pos + 2 == ring) {
+          nn = 2;
+          nd[0] = pos * Nc, nid[0] = p.idesc2, nb[0] = 0;
+          nd[1] = 0, nid[1] = p.idesc1, nb[1] = 2 * Nc;
+        } else {
+          nn = 2;
+          nd[0] = pos * Nc, nid[0] = p.idesc1, nb[0] = 0;
+          nd[1] = 0, nid[1] = p.idesc2, nb[1] = Nc;
         }
-        __syncwarp();
-        if (++stage == p.stages) {
-          stage = 0;
-          phase ^= 1;
+        if (pos + 2 < ring) {  // (pos, pos+1) contiguous
+          nf = 2;
+          fd[0] = pos * Nc, fid[0] = p.idesc2, fb[0] = 0, facc[0] = 1;
+          fd[1] = (pos + 2) * Nc, fid[1] = p.idesc1, fb[1] = 2 * Nc, facc[1] = 0;
+          fd[2] = 0, fid[2] = 0, fb[2] = 0, facc[2] = 0;
+        } else if (pos + 2 == ring) {
+          nf = 2;
+          fd[0] = pos * Nc, fid[0] = p.idesc2, fb[0] = 0, facc[0] = 1;
+          fd[1] = 0, fid[1] = p.idesc1, fb[1] = 2 * Nc, facc[1] = 0;
+          fd[2] = 0, fid[2] = 0, fb[2] = 0, facc[2] = 0;
+        } else {
+          nf = 3;
+          fd[0] = pos * Nc, fid[0] = p.idesc1, fb[0] = 0, facc[0] = 1;
+          fd[1] = 0, fid[1] = p.idesc1, fb[1] = Nc, facc[1] = 1;
+          fd[2] = Nc, fid[2] = p.idesc1, fb[2] = 2 * Nc, facc[2] = 0;
         }
-      }
-      if (elect_one()) mma_commit(&tfull[ab]);
-      __syncwarp();
-      if (++ab == 2) {
-        ab = 0;
-        aphase ^= 1;
-      }
-    }
-    if (p.dbg && lane == 0) {
-      p.dbg[blockIdx.x * 4 + 0] = clock64() - t_start;
-      p.dbg[blockIdx.x * 4 + 1] = t_wait_tmem;
-      p.dbg[blockIdx.x * 4 + 2] = t_wait_full;
-    }
-  } else {
-    // epilogue warps 2..9: warp w drains lane quarter (w & 3) of tiles with parity (w-2)/4
-    const int q = warp & 3;
-    const int half = (warp - 2) >> 2;
-    const int et = threadIdx.x - 64;
-    if (!(p.flags & VM_CONV_NOBIAS))
-      for (int c = et; c < p.Cout; c += 256) sbias[c] = p.bias[c];
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    const bool domask = p.flags & VM_CONV_MASK;
-    const int ngo = p.Nc / 8;
-    int ab = 0;
-    uint32_t aphase = 0;
-    int cpar = 0;
-    long long e_wait = 0, e_ld = 0, e_bar = 0, e_rest = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      const int mb = u % p.mblocks;
-      const int b = u / p.mblocks;
-      const int a0 = mb * p.MB * p.TS;
-      const bf16* mbase = p.mask + b * p.m_bstride;
-      bf16* ybase = p.y + b * p.y_bstride;
-      long long c0t = clock64();
-      mbar_wait(&tfull[ab], aphase);
-      e_wait += clock64() - c0t;
-      tc_fence_after();
-      for (int i = half; i < p.MB; i += 2) {
-        long long c1t = clock64();
-        const int r = q * 32 + lane;  // tile row
-        const int a = a0 + i * p.TS + r;
-        uint32_t qa = __umulhi((uint32_t)a, p.wp_magic);
-        if (qa * (uint32_t)p.Wp > (uint32_t)a) --qa;
-        if ((qa + 1) * (uint32_t)p.Wp <= (uint32_t)a) ++qa;
-        const int wq = a - (int)qa * p.Wp;
-        uint32_t qh = __umulhi(qa, p.hp_magic);
-        if (qh * (uint32_t)p.Hp > qa) --qh;
-        if ((qh + 1) * (uint32_t)p.Hp <= qa) ++qh;
-        const int hq = (int)qa - (int)qh * p.Hp;
-        const bool valid = r < p.TS && a < p.anchors && wq < p.W && hq < p.H;
-        const int64_t orow = (int64_t)a + p.P + p.Wp + 1;
-        const uint32_t tcol = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * p.MB + i) * N3);
-        // whole tile at once: masks (dgrad) first, then all 3*Nc accumulator columns, one
-        // exchange + barrier, then combine / store (ngo <= 4 since Nc <= 32)
-        int4 mk[4];
-        if (domask) {
+        for (int kc = 0; kc < p.KC; ++kc) {
+          const int ng = (kc * 2 + 1 < p.CG) ? 2 : 1;
+          const long long tf = clock64();
+          mbar_wait(&full[stage], phase);
+          const long long tf1 = clock64();
+          t_fu += tf1 - tf;
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t sA = smem_u32(sStage + (size_t)stage * p.stage_bytes);
+            const uint64_t a0desc = make_sdesc(sA, ng == 2 ? p.a_bytes : 0, 128);
+            const uint64_t b0desc = make_sdesc(sWa + (uint32_t)kc * 9 * wblk, (uint32_t)(3 * p.Nc * 16), 128);
+            const uint32_t wp1 = (uint32_t)p.Wp, wstep = wblk >> 4;
 #pragma unroll
-          for (int g = 0; g < 4; ++g)
-            mk[g] = (g < ngo && valid) ? __ldg(reinterpret_cast<const int4*>(mbase + g * p.plane8 + orow * 8))
-                                       : make_int4(0, 0, 0, 0);
-        }
-        uint32_t c0[32], c1[32], c2[32];
-        tmem_ld16(tcol, *reinterpret_cast<uint32_t(*)[16]>(&c0[0]));
-        tmem_ld16(tcol + (uint32_t)p.Nc, *reinterpret_cast<uint32_t(*)[16]>(&c1[0]));
-        tmem_ld16(tcol + (uint32_t)(2 * p.Nc), *reinterpret_cast<uint32_t(*)[16]>(&c2[0]));
-        if (ngo > 2) {
-          tmem_ld16(tcol + 16u, *reinterpret_cast<uint32_t(*)[16]>(&c0[16]));
-          tmem_ld16(tcol + (uint32_t)(p.Nc + 16), *reinterpret_cast<uint32_t(*)[16]>(&c1[16]));
-          tmem_ld16(tcol + (uint32_t)(2 * p.Nc + 16), *reinterpret_cast<uint32_t(*)[16]>(&c2[16]));
-        }
-        tmem_ld_wait();
-        long long c2t = clock64();
-        e_ld += c2t - c1t;
-        float* x = &sx[half][cpar][0][0][0];  // [4 quarters][3][32]
-        // lanes 0 / 1 publish the values the previous quarter's lanes 30 / 31 need (branch-free)
-        {
-          const bool l0 = lane == 0, l1 = lane == 1;
+            for (int j = 0; j < 9; ++j) {
+              const uint64_t bdesc = b0desc + (uint64_t)(j * wstep);
+              const uint64_t adesc = a0desc + (uint64_t)((j / 3) * wp1 + (j % 3));
+              if (j == 0 && kc == 0) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            if (e < p.Nc) {
-              if (l0) x[(q * 3 + 0) * 32 + e] = __uint_as_float(c1[e]);
-              if (l0) x[(q * 3 + 1) * 32 + e] = __uint_as_float(c2[e]);
-              if (l1) x[(q * 3 + 2) * 32 + e] = __uint_as_float(c2[e]);
-            }
-          }
-        }
-#ifndef VM_EXPERIMENT_NOBAR
-        asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory");
-#endif
-        long long c3t = clock64();
-        e_bar += c3t - c2t;
-        cpar ^= 1;  // next tile uses the other exchange buffer
-        const int qn = q < 3 ? q + 1 : 3;
-        const bool take1 = q < 3 && lane == 31, take2a = q < 3 && lane == 30, take2b = q < 3 && lane == 31;
+                for (int t = 0; t < MB; ++t)
+                  for (int e = 0; e < nf; ++e)
+                    mma_bf16_ss(tbase + t * tstride + fd[e], adesc + (uint64_t)(t * 128), bdesc + fb[e], fid[e],
+                                facc[e]);
+              } else if (nn == 1) {
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          if (g >= ngo) break;
-          float v[8];
+                for (int t = 0; t < MB; ++t)
+                  mma_bf16_ss(tbase + t * tstride + nd[0], adesc + (uint64_t)(t * 128), bdesc, nid[0], 1u);
+              } else {
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int c = g * 8 + e;
-            const float n1s = __shfl_down_sync(0xffffffffu, __uint_as_float(c1[c]), 1);
-            const float n2s = __shfl_down_sync(0xffffffffu, __uint_as_float(c2[c]), 2);
-            const float f1 = x[(qn * 3 + 0) * 32 + c];  // broadcast reads, no divergence
-            const float f2a = x[(qn * 3 + 1) * 32 + c];
-            const float f2b = x[(qn * 3 + 2) * 32 + c];
-            const float n1 = take1 ? f1 : n1s;
-            const float n2 = take2a ? f2a : (take2b ? f2b : n2s);
-            v[e] = __uint_as_float(c0[c]) + n1 + n2;
-          }
-          const int co0 = g * 8;
-          if (valid && co0 < p.Cout) {
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              if (!(p.flags & VM_CONV_NOBIAS)) v[e] += (co0 + e < p.Cout) ? sbias[co0 + e] : 0.f;
-            if (p.flags & VM_CONV_RELU) {
-#pragma unroll
-              for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
-            }
-            if (domask) {
-              const __nv_bfloat162* mh = reinterpret_cast<const __nv_bfloat162*>(&mk[g]);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                float2 f = __bfloat1622float2(mh[e]);
-                if (!(f.x > 0.f)) v[2 * e] = 0.f;
-                if (!(f.y > 0.f)) v[2 * e + 1] = 0.f;
+                for (int t = 0; t < MB; ++t) {
+                  mma_bf16_ss(tbase + t * tstride + nd[0], adesc + (uint64_t)(t * 128), bdesc + nb[0], nid[0], 1u);
+                  mma_bf16_ss(tbase + t * tstride + nd[1], adesc + (uint64_t)(t * 128), bdesc + nb[1], nid[1], 1u);
+                }
               }
             }
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              if (co0 + e >= p.Cout) v[e] = 0.f;
-            int4 out;
-            __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&out);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) oh[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
-            *reinterpret_cast<int4*>(ybase + g * p.plane8 + orow * 8) = out;
+            mma_commit(&empty[stage]);
+          }
+          __syncwarp();
+          t_is += clock64() - tf1;
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1;
           }
         }
-        e_rest += clock64() - c3t;
+        // block n has received all three contributions (planes below o0 are scratch)
+        if (elect_one()) {
+          mma_commit(&tfull[pos]);
+          if (k == nin - 1) {
+            mma_commit(&tfull[(n + 1) % (uint32_t)p.ring]);
+            mma_commit(&tfull[(n + 2) % (uint32_t)p.ring]);
+          }
+        }
+        __syncwarp();
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[ab]);
-      if (++ab == 2) {
-        ab = 0;
-        aphase ^= 1;
+      nstart += (uint32_t)(nin + 2);
+    }
+    if (p.dbg && lane == 0) {
+      p.dbg[blockIdx.x * 8 + 0] = clock64() - t0;
+      p.dbg[blockIdx.x * 8 + 1] = t_te;
+      p.dbg[blockIdx.x * 8 + 2] = t_fu;
+      p.dbg[blockIdx.x * 8 + 3] = t_is;
+    }
+  } else {
+    // ===================== epilogue (warps 2..9): TMEM lane quarter q, half h
+    const int q = warp & 3;
+    const int h = (warp - 2) >> 2;
+    // tiles t = h, h+2, ... of every block (MB = 1: both halves share the tile, split by group)
+    constexpr int TPT = MB == 1 ? 1 : (MB + 1) / 2;  // tiles per thread (max)
+    constexpr int GPT = MB == 1 ? kSweepMaxNc / 16 : kSweepMaxNc / 8;  // channel groups per thread (max)
+    const int ngrp = p.Nc / 8;
+    const int g_lo = MB == 1 ? h : 0, g_step = MB == 1 ? 2 : 1;  // channel groups of this thread
+    const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
+    const bool nobias = p.flags & VM_CONV_NOBIAS;
+    for (int c = threadIdx.x - 64; c < p.Nc; c += 256) sbias[c] = (!nobias && c < p.Cout) ? p.bias[c] : 0.f;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    // blocks start empty: the first MMA into a block overwrites it (enable_input_d = 0)
+    for (int r = 0; r < p.ring; ++r) mbar_arrive(&tempty[r]);
+    uint32_t n = 0;
+    const long long e0 = clock64();
+    long long e_w = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const int col = u % p.ncol;
+      const int seg = (u / p.ncol) % p.nseg;
+      const int b = u / (p.ncol * p.nseg);
+      const int o0 = seg * p.S, o1 = min(p.D, o0 + p.S);
+      const int L = o1 - o0 + 4;
+      bool valid[TPT];
+      int64_t orow0[TPT];
+#pragma unroll
+      for (int k = 0; k < TPT; ++k) {
+        const int t = MB == 1 ? 0 : h + 2 * k;
+        const int ra = col * MB * 128 + t * 128 + q * 32 + lane;  // in-plane anchor
+        const int hq = ra / p.Wp, wq = ra % p.Wp;
+        valid[k] = t < MB && ra < p.P && hq < p.H && wq < p.W;
+        orow0[k] = (int64_t)ra + p.P + p.Wp + 1;
+      }
+      bf16* yb = p.y + b * p.y_bstride;
+      const bf16* mb = p.mask + b * p.m_bstride;
+      for (int rel = 0; rel < L; ++rel, ++n) {
+        const uint32_t r = n % (uint32_t)p.ring;
+        const int o = o0 + rel - 2;
+        const bool live = o >= o0 && o < o1 && !(p.xmode & 1);  // warp-uniform (tcgen05.ld is .aligned)
+        // dgrad: the ReLU mask of this plane is fetched before waiting for the accumulator
+        int4 mk[TPT][GPT];
+        if (p.flags & VM_CONV_MASK) {
+#pragma unroll
+          for (int k = 0; k < TPT; ++k)
+#pragma unroll
+            for (int gi = 0; gi < GPT; ++gi) {
+              const int g = g_lo + gi * g_step;
+              mk[k][gi] = make_int4(0, 0, 0, 0);
+              if (live && valid[k] && g < ngrp && g * 8 < p.Cout)
+                mk[k][gi] = __ldg(reinterpret_cast<const int4*>(mb + g * p.plane8 + orow0[k] * 8 +
+                                                                (int64_t)o * p.P * 8));
+            }
+        }
+        const long long tw = clock64();
+        mbar_wait(&tfull[r], (n / (uint32_t)p.ring) & 1u);
+        e_w += clock64() - tw;
+        tc_fence_after();
+        if (live) {
+#pragma unroll
+          for (int k = 0; k < TPT; ++k) {
+            const int t = MB == 1 ? 0 : h + 2 * k;
+            if (t >= MB) break;
+            const int64_t orow = orow0[k] + (int64_t)o * p.P;
+            const uint32_t tcol = lane_base + (uint32_t)((t * p.ring + (int)r) * p.Nc);
+#pragma unroll
+            for (int gi = 0; gi < GPT; ++gi) {
+              const int g = g_lo + gi * g_step;
+              if (g >= ngrp || g * 8 >= p.Cout) break;
+              uint32_t rr[8];
+              tmem_ld8(tcol + (uint32_t)(g * 8), rr);
+              tmem_ld_wait();
+              float v[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(rr[e]) + sbias[g * 8 + e];
+              if (p.flags & VM_CONV_MASK) {
+                const uint32_t* mw = reinterpret_cast<const uint32_t*>(&mk[k][gi]);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  if (!((int16_t)(mw[e] & 0xFFFFu) > 0)) v[2 * e] = 0.f;
+                  if (!((int16_t)(mw[e] >> 16) > 0)) v[2 * e + 1] = 0.f;
+                }
+              }
+              int4 out;
+              uint32_t* ow = reinterpret_cast<uint32_t*>(&out);
+              if (p.flags & VM_CONV_RELU) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) ow[e] = pack_bf16x2_relu(v[2 * e], v[2 * e + 1]);
+              } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) ow[e] = pack_bf16x2(v[2 * e], v[2 * e + 1]);
+              }
+              if (valid[k]) *reinterpret_cast<int4*>(yb + g * p.plane8 + orow * 8) = out;
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[r]);
       }
     }
     if (p.dbg && threadIdx.x == 64) {
-      p.dbg[4 * gridDim.x + blockIdx.x * 4 + 0] = e_wait;
-      p.dbg[4 * gridDim.x + blockIdx.x * 4 + 1] = e_ld;
-      p.dbg[4 * gridDim.x + blockIdx.x * 4 + 2] = e_bar;
-      p.dbg[4 * gridDim.x + blockIdx.x * 4 + 3] = e_rest;
+      p.dbg[blockIdx.x * 8 + 4] = clock64() - e0;
+      p.dbg[blockIdx.x * 8 + 5] = e_w;
+      p.dbg[blockIdx.x * 8 + 6] = (long long)n;
     }
   }
   tc_fence_before();
@@ -1015,6 +1092,95 @@ extern "C" int vm_pack_weights(const float* w, void* packed, int Cin, int Cout, 
 }
 
 static long long* g_fwd_dbg = nullptr;
+static int g_sweep_xmode = 0;
+extern "C" void vm_debug_set_sweep_mode(int m) { g_sweep_xmode = m; }
+
+// Plan + launch of the kd-stacked sweep kernel (weights packed with PackGeom::sweep).
+// Units = (sample, column of MB*128 in-plane anchors, segment of S output planes); MB and
+// S minimise waves * (S + 2) * MB, the MMA work per SM in tile-planes.
+static int launch_sweep(const FwdParams& f, int nsm, void* stream) {
+  SwParams p{};
+  p.x = f.x;
+  p.x_bstride = f.x_bstride;
+  p.wpk = f.wpk;
+  p.bias = f.bias;
+  p.y = f.y;
+  p.y_bstride = f.y_bstride;
+  p.mask = f.mask;
+  p.m_bstride = f.m_bstride;
+  p.D = f.D;
+  p.H = f.H;
+  p.W = f.W;
+  p.Hp = f.Hp;
+  p.Wp = f.Wp;
+  p.P = f.P;
+  p.plane8 = f.plane8;
+  p.CG = f.CG;
+  p.KC = f.KC;
+  p.Cout = f.Cout;
+  p.Nc = f.Nc;
+  p.flags = f.flags;
+  p.dbg = f.dbg;
+  p.xmode = g_sweep_xmode;
+  p.w_bytes = (uint32_t)p.KC * 9 * 2 * 3 * p.Nc * 16;
+  const int static_smem = 2 * 1024;
+  // measured SS-mode tcgen05.mma cycles (tools/probes/probe_tput5, profiles/r01): one chain of
+  // dependent accumulations costs ~68 cycles per MMA; >= 3 independent chains reach the
+  // operand-bandwidth bound max(N/2, 32 + N/4)
+  auto mma_cycles = [](int N, int chains) -> double {
+    const double bw = N / 2.0 > 32 + N / 4.0 ? N / 2.0 : 32 + N / 4.0;
+    if (chains >= 3) return bw + 1;
+    if (chains == 2) return bw * 1.3 > 49 ? bw * 1.3 : 49;
+    return bw > 68 ? bw : 68;
+  };
+  double best = 1e30;
+  for (int MB = 4; MB >= 1; --MB) {
+    int ring = 512 / (MB * p.Nc);
+    if (ring > kSwMaxRing) ring = kSwMaxRing;
+    if (ring < 4) continue;
+    const int R = MB * 128 + 2 * p.Wp + 2;
+    const uint32_t a_bytes = ((uint32_t)R * 16 + 127) & ~127u;
+    const uint32_t stage_bytes = 2 * a_bytes;
+    int stages = (int)((kSmemBudget - static_smem - (int)p.w_bytes) / (int)stage_bytes);
+    if (stages > kSwMaxStages) stages = kSwMaxStages;
+    if (stages < 3) continue;
+    const int ncol = (p.P + MB * 128 - 1) / (MB * 128);
+    // per input plane: 9*KC MMAs per tile (+1 at the first K step); a short ring (< 6) stalls
+    const double plane = (9.0 * p.KC + 1) * MB * mma_cycles(3 * p.Nc, MB) * (ring < 6 ? 1.15 : 1.0);
+    for (int S = 1; S <= p.D; ++S) {
+      const int nseg = (p.D + S - 1) / S;
+      const int64_t units = (int64_t)f.B * ncol * nseg;
+      const int64_t waves = (units + nsm - 1) / nsm;
+      const double cost = (double)waves * (S + 3) * plane;  // + ~1 plane of pipeline fill
+      if (cost < best) {
+        best = cost;
+        p.MB = MB;
+        p.ring = ring;
+        p.R = R;
+        p.a_bytes = a_bytes;
+        p.stage_bytes = stage_bytes;
+        p.stages = stages;
+        p.ncol = ncol;
+        p.S = S;
+        p.nseg = nseg;
+        p.units = (int)units;
+      }
+    }
+  }
+  VM_REQUIRE(best < 1e30, VM_E_UNSUPPORTED, "vm_conv3d_fwd_tc: no sweep configuration fits (W=%d)", p.W);
+  p.idesc1 = make_idesc_bf16(128, p.Nc, false, false);
+  p.idesc2 = make_idesc_bf16(128, 2 * p.Nc, false, false);
+  p.idesc3 = make_idesc_bf16(128, 3 * p.Nc, false, false);
+  const size_t smem = (size_t)p.w_bytes + (size_t)p.stages * p.stage_bytes;
+  const int grid = p.units < nsm ? p.units : nsm;
+  auto kern = p.MB == 4 ? k_conv_fwd_sweep<4>
+               : p.MB == 3 ? k_conv_fwd_sweep<3>
+               : p.MB == 2 ? k_conv_fwd_sweep<2>
+                           : k_conv_fwd_sweep<1>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<grid, 320, smem, as_stream(stream)>>>(p);
+  return launch_status("vm_conv3d_fwd_tc (sweep)");
+}
 
 extern "C" void vm_debug_set_fwd_probe(long long* buf) { g_fwd_dbg = buf; }
 
@@ -1055,25 +1221,28 @@ extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wp
   p.wp_magic = (uint32_t)(0x100000000ULL / (uint64_t)(W + 2)) + 1;
   p.hp_magic = (uint32_t)(0x100000000ULL / (uint64_t)(H + 2)) + 1;
   VM_REQUIRE(Cout <= 1024, VM_E_UNSUPPORTED, "vm_conv3d_fwd_tc: Cout %d > 1024", Cout);
-  p.b_bytes = 9 * 2 * p.Nc * 16;
-  const bool fold = pg.fold;  // packed layout and kernel are both chosen by shape
-  p.TS = fold ? 126 : 128;
-  const int N = fold ? 3 * p.Nc : p.Nc;  // accumulator columns per tile
-  const int tiles = (int)((p.anchors + p.TS - 1) / p.TS);
-  // accumulators: 2 buffers x MB x N fp32 columns <= 512
+  p.x = static_cast<const bf16*>(x);
+  p.x_bstride = x_bstride ? x_bstride : default_bstride(Cin, D, H, W, 1);
+  VM_REQUIRE((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (p.x_bstride & 7) == 0, VM_E_ALIGN,
+             "vm_conv3d_fwd_tc: slab must be 16-byte aligned");
   int nsm = vm_num_sms(0);
   if (nsm <= 0) nsm = 148;
+  if (pg.sweep) return launch_sweep(p, nsm, stream);
+  p.b_bytes = 9 * 2 * p.Nc * 16;
+  const int N = p.Nc;  // accumulator columns per tile
+  const int tiles = (int)((p.anchors + 127) / 128);
+  // accumulators: 2 buffers x MB x N fp32 columns <= 512
   int MB = 256 / N;
   if (MB > 8) MB = 8;
   const int mb_fill = (int)((int64_t)tiles * B * p.nchunk / nsm);  // keep >= 1 unit per SM
   if (MB > mb_fill) MB = mb_fill;
   if (MB < 1) MB = 1;
   for (;;) {
-    p.R = (MB - 1) * p.TS + 128 + 2 * p.Wp + 2;
+    p.R = MB * 128 + 2 * p.Wp + 2;
     p.Ralloc = (p.R + 7) / 8 * 8;
     p.a_bytes = (uint32_t)p.Ralloc * 16;
     p.stage_bytes = 2 * p.a_bytes + p.b_bytes;
-    p.stages = (fold ? kSmemBudget - 12 * 1024 : kSmemBudget) / (int)p.stage_bytes;  // fold: 11 KB static smem
+    p.stages = kSmemBudget / (int)p.stage_bytes;
     if (p.stages > kMaxStages) p.stages = kMaxStages;
     if (p.stages >= 2 || MB == 1) break;
     MB /= 2;
@@ -1083,20 +1252,11 @@ extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wp
   p.mblocks = (tiles + MB - 1) / MB;
   p.units = B * p.mblocks * p.nchunk;
   p.idesc = make_idesc_bf16(128, N, false, false);
-  p.x = static_cast<const bf16*>(x);
-  p.x_bstride = x_bstride ? x_bstride : default_bstride(Cin, D, H, W, 1);
-  VM_REQUIRE((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (p.x_bstride & 7) == 0, VM_E_ALIGN,
-             "vm_conv3d_fwd_tc: slab must be 16-byte aligned");
   (void)rows;
   const size_t smem = (size_t)p.stages * p.stage_bytes;
   int grid = p.units < nsm ? p.units : nsm;
-  if (fold) {
-    cudaFuncSetAttribute(k_conv_fwd_fold, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_conv_fwd_fold<<<grid, 320, smem, as_stream(stream)>>>(p);
-  } else {
-    cudaFuncSetAttribute(k_conv_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_conv_fwd_tc<<<grid, 320, smem, as_stream(stream)>>>(p);
-  }
+  cudaFuncSetAttribute(k_conv_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_conv_fwd_tc<<<grid, 320, smem, as_stream(stream)>>>(p);
   return launch_status("vm_conv3d_fwd_tc");
 }
 

@@ -22,6 +22,15 @@ SHAPES = [
     (1, 16, 48, 16, 20, 24),
     (1, 24, 8, 6, 6, 6),
     (1, 16, 16, 32, 32, 128),
+    # kd-stacked sweep kernel (Cout <= 48): single planes, segments, ring wrap-around,
+    # several units per CTA, odd channel counts
+    (1, 8, 16, 1, 9, 9),
+    (1, 16, 24, 2, 5, 7),
+    (2, 16, 16, 40, 8, 8),
+    (1, 32, 32, 40, 24, 24),
+    (1, 16, 3, 5, 6, 7),
+    (3, 16, 16, 3, 30, 30),
+    (1, 8, 48, 70, 4, 4),
 ]
 
 
