@@ -1052,6 +1052,203 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 1) tmem_dealloc<512>(tbase);
 }
 
+// ------------------------------------------------------------------ weight gradient, kd along N
+// Thin outputs (3*Nc <= 144): dW[kd,kh,kw][ci][co] = sum_a x[a + kd*P + kh*Wp + kw][ci] *
+// gy[a + P + Wp + 1][co] is computed with kd moved to the B side: B = three gy slices shifted
+// by -kd*P rows (N = 3*Nc, group (kd, cgo), one 16-byte-box TMA per kd with zero fill outside
+// the sample), A = the runs-mode x staging without kd (M slot g = cg*3 + kh, kw = +16 B start).
+// Per K step: 3 MMAs (one per kw, independent accumulators) of N = 3*Nc per M-tile, against
+// 3 x 3 of N = Nc before.  The anchor range is extended to all Dp*P rows so every kd sees its
+// full sum; anchors whose gy row falls in a margin or outside the sample contribute zero.
+// A ones slot (g = 3*CG) yields the bias gradient in the kd = 0, kw = 0 block.
+struct WkParams {
+  const bf16* x;
+  int64_t x_bstride;
+  int64_t plane8;
+  int B, P, Wp, rows;  // rows = Dp*P per sample
+  int CG, CGo, Cout, Nc;
+  int KS;              // anchors per stage (<= Wp - 2, multiple of 16)
+  int MT, mt_per_unit, n_mtgroups;
+  int ones_slot;
+  int spk, ksplit, stages_total, units, grid, stages;
+  uint32_t a_bytes;
+  uint32_t g_bytes;  // per kd slice: Nc/8 group slots of KS rows (CGo of them loaded)
+  uint32_t g_load;   // loaded bytes per kd slice: CGo * KS * 16
+  uint32_t stage_bytes, idesc;
+  float* ws;  // [kidx][MT][3 kw][3*Nc][128]
+};
+
+__global__ void __launch_bounds__(192, 1)
+    k_conv_wgrad_kd(const __grid_constant__ CUtensorMap gmap, const WkParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t full[kMaxStages], empty[kMaxStages], tfull;
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int mg_cta = blockIdx.x % p.n_mtgroups;
+  const int mt0 = mg_cta * p.mt_per_unit;
+  const int nmt = min(p.mt_per_unit, p.MT - mt0);
+  const int N3 = 3 * p.Nc;
+  // slot i of this CTA's M-tiles sits at (i + slot_shift) * GS: runs of 3 slots (kh) per cg
+  const int r0 = (16 * mt0) / 3;
+  const int slot_shift = 16 * mt0 - 3 * r0;
+  const uint32_t GS = (uint32_t)p.Wp * 16;
+  if (p.ones_slot >= 0 && p.ones_slot / 16 >= mt0 && p.ones_slot / 16 < mt0 + nmt) {
+    const int local = p.ones_slot - mt0 * 16 + slot_shift;
+    for (int s = 0; s < p.stages; ++s) {
+      uint32_t* dst = reinterpret_cast<uint32_t*>(smem + (size_t)s * p.stage_bytes + (size_t)local * GS);
+      for (int i = threadIdx.x; i < (p.KS + 8) * 4; i += blockDim.x) dst[i] = 0x3F803F80u;  // bf16 1.0 x2
+    }
+  }
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tslot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch(&gmap);
+      int stage = 0;
+      uint32_t phase = 0;
+      const int r_end = min(p.CG - 1, (16 * (mt0 + nmt) - 1) / 3);  // last run of this CTA
+      const int nrun = r_end >= r0 ? r_end - r0 + 1 : 0;
+      const int Rrun = p.KS + 2 * p.Wp + 2;
+      const uint32_t tx = (uint32_t)nrun * Rrun * 16 + 3 * p.g_load;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const int ks = (u / p.n_mtgroups) % p.ksplit;
+        const int b = u / (p.n_mtgroups * p.ksplit);
+        const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
+        const bf16* xb = p.x + b * p.x_bstride;
+        for (int s = s0; s < s1; ++s) {
+          const int k0 = s * p.KS;
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sA = smem + (size_t)stage * p.stage_bytes;
+          uint8_t* sG = sA + p.a_bytes;
+          mbar_arrive_expect_tx(&full[stage], tx);
+          const int gr0 = k0 + p.P + p.Wp + 1;
+          for (int kd = 0; kd < 3; ++kd)  // rows outside [0, Dp*P) read as zeros
+            tma_load_4d(sG + (size_t)kd * p.g_bytes, &gmap, &full[stage], 0, gr0 - kd * p.P, 0, b);
+          for (int r = r0; r <= r_end; ++r)
+            bulk_load(sA + (size_t)(r - r0) * 3 * GS, xb + r * p.plane8 + (int64_t)k0 * 8, (uint32_t)Rrun * 16,
+                      &full[stage]);
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    int stage = 0;
+    uint32_t phase = 0;
+    bool started = false;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const int ks = (u / p.n_mtgroups) % p.ksplit;
+      const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
+      for (int s = s0; s < s1; ++s) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes);
+          const uint32_t sG = sA + p.a_bytes;
+          // B: MN-major, N groups (kd, cgo) KS rows apart; A: MN-major slots GS apart
+          const uint64_t b0desc = make_sdesc(sG, 128, (uint32_t)p.KS * 16);
+          const uint64_t a0desc = make_sdesc(sA + (uint32_t)slot_shift * GS, 128, GS);
+          const uint32_t mstep = 16 * (GS >> 4);
+#pragma unroll 1
+          for (int kk = 0; kk < p.KS / 16; ++kk) {
+            const uint64_t bdesc = b0desc + (uint64_t)(kk * 16);
+            const uint32_t acc = (started || kk > 0) ? 1u : 0u;
+            for (int m = 0; m < nmt; ++m) {
+              const uint64_t adesc = a0desc + (uint64_t)(m * mstep + kk * 16);
+              const uint32_t d = tbase + (uint32_t)(m * 3 * N3);
+              mma_bf16_ss(d, adesc, bdesc, p.idesc, acc);
+              mma_bf16_ss(d + N3, adesc + 1, bdesc, p.idesc, acc);
+              mma_bf16_ss(d + 2 * N3, adesc + 2, bdesc, p.idesc, acc);
+            }
+          }
+          mma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        started = true;
+        if (++stage == p.stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    if (elect_one()) mma_commit(&tfull);
+    __syncwarp();
+  } else {
+    // drain: warp (2..5) reads TMEM lane quarter warp & 3
+    const int q = warp & 3;
+    const int kidx = blockIdx.x / p.n_mtgroups;
+    mbar_wait(&tfull, 0);
+    tc_fence_after();
+    const int m_row = q * 32 + lane;
+    for (int m = 0; m < nmt; ++m)
+      for (int c0 = 0; c0 < 3 * N3; c0 += 16) {
+        uint32_t r[16];
+        tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(m * 3 * N3 + c0), r);
+        tmem_ld_wait();
+        float* dst = p.ws + (((int64_t)kidx * p.MT + mt0 + m) * 3 * N3 + c0) * 128 + m_row;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) dst[e * 128] = __uint_as_float(r[e]);
+      }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tbase);
+}
+
+// ws[k][mt][kw][n = kd*Nc + co][m] -> gw[t][ci][co], t = (kd*3 + kh)*3 + kw, slot
+// g = mt*16 + m/8 = cg*3 + kh; the ones slot (kd = 0, kw = 0, m%8 = 0) gives gb.
+__global__ void k_wgrad_kd_finalize(const float* __restrict__ ws, float* __restrict__ gw,
+                                    float* __restrict__ gb, int nk, int MT, int Nc, int CG, int Cin,
+                                    int Cout, int ones_slot) {
+  const int N3 = 3 * Nc;
+  const int64_t E = (int64_t)MT * 3 * N3 * 128;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int m = e % 128;
+    const int n = (e / 128) % N3;
+    const int kw = (e / (128 * N3)) % 3;
+    const int mt = (int)(e / (384LL * N3));
+    const int g = mt * 16 + m / 8;
+    const int kd = n / Nc, co = n % Nc;
+    if (co >= Cout) continue;
+    const int cg = g / 3, kh = g % 3;
+    const bool is_w = g < 3 * CG && cg * 8 + m % 8 < Cin;
+    const bool is_b = g == ones_slot && kw == 0 && kd == 0 && m % 8 == 0;
+    if (!is_w && !is_b) continue;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;  // 4 independent chains, fixed order
+    int k = 0;
+    for (; k + 4 <= nk; k += 4) {
+      s0 += ws[(k + 0) * E + e];
+      s1 += ws[(k + 1) * E + e];
+      s2 += ws[(k + 2) * E + e];
+      s3 += ws[(k + 3) * E + e];
+    }
+    for (; k < nk; ++k) s0 += ws[k * E + e];
+    const float s = (s0 + s1) + (s2 + s3);
+    if (is_w) {
+      const int ci = cg * 8 + m % 8;
+      gw[((int64_t)((kd * 3 + kh) * 3 + kw) * Cin + ci) * Cout + co] = s;
+    } else {
+      gb[co] = s;
+    }
+  }
+}
+
 }  // namespace vm
 
 using namespace vm;
@@ -1423,7 +1620,63 @@ extern "C" int vm_debug_wgrad_plan(int B, int Cin, int Cout, int D, int H, int W
   return VM_OK;
 }
 
+// Plan of the kd-along-N weight-gradient kernel; false when the shape is not eligible
+// (3*Nc > 144 or TMEM, rows narrower than 34, or no double-buffered stage fits).
+static bool plan_wgrad_kd(int B, int Cin, int Cout, int D, int H, int W, WkParams& p, size_t& ws) {
+  p = WkParams{};
+  if (g_force_runs == 0 || g_force_fold > 0) return false;  // debug overrides select the old kernel
+  p.B = B;
+  p.Wp = W + 2;
+  p.P = (H + 2) * p.Wp;
+  p.rows = (D + 2) * p.P;
+  p.plane8 = (int64_t)p.rows * 8;
+  p.CG = (Cin + 7) / 8;
+  p.CGo = (Cout + 7) / 8;
+  p.Cout = Cout;
+  p.Nc = (Cout + 15) / 16 * 16;
+  if (3 * p.Nc > 144) return false;
+  p.KS = min(256, ((p.Wp - 2) / 16) * 16);  // a run of KS + 2Wp + 2 rows fits 3 slots of Wp rows
+  if (p.KS < 32) return false;
+  if ((3 * p.CG) % 16 == 0) return false;  // no spare M slot for the bias-gradient ones block
+  p.MT = (3 * p.CG + 1 + 15) / 16;
+  p.ones_slot = 3 * p.CG;
+  p.mt_per_unit = 512 / (9 * p.Nc);
+  if (p.mt_per_unit > p.MT) p.mt_per_unit = p.MT;
+  if (p.mt_per_unit < 1) return false;
+  p.g_bytes = (uint32_t)(p.Nc / 8) * p.KS * 16;
+  p.g_load = (uint32_t)p.CGo * p.KS * 16;
+  for (;;) {
+    const int runs_alloc = (16 * p.mt_per_unit + 2) / 3 + 2;
+    p.a_bytes = ((uint32_t)runs_alloc * 3 * p.Wp * 16 + 1023) & ~1023u;
+    p.stage_bytes = (p.a_bytes + 3 * p.g_bytes + 1023) & ~1023u;
+    p.stages = kSmemBudget / (int)p.stage_bytes;
+    if (p.stages >= 2 || p.mt_per_unit == 1) break;
+    --p.mt_per_unit;
+  }
+  if (p.stages < 2) return false;
+  if (p.stages > kMaxStages) p.stages = kMaxStages;
+  p.n_mtgroups = (p.MT + p.mt_per_unit - 1) / p.mt_per_unit;
+  p.stages_total = (p.rows + p.KS - 1) / p.KS;
+  int nsm = vm_num_sms(0);
+  if (nsm <= 0) nsm = 148;
+  int want = (2 * nsm + p.n_mtgroups * B - 1) / (p.n_mtgroups * B);  // ~2 units per SM
+  if (want < 1) want = 1;
+  p.spk = (p.stages_total + want - 1) / want;
+  if (p.spk < 4) p.spk = 4;
+  p.ksplit = (p.stages_total + p.spk - 1) / p.spk;
+  p.units = p.n_mtgroups * B * p.ksplit;
+  p.idesc = make_idesc_bf16(128, 3 * p.Nc, true, true);
+  p.grid = p.units;
+  if (p.grid > nsm) p.grid = (nsm / p.n_mtgroups) * p.n_mtgroups;
+  if (p.grid < p.n_mtgroups) p.grid = p.n_mtgroups;
+  ws = (size_t)(p.grid / p.n_mtgroups) * p.MT * 9 * p.Nc * 128 * sizeof(float);
+  return true;
+}
+
 extern "C" size_t vm_conv3d_wgrad_tc_ws(int B, int Cin, int Cout, int D, int H, int W) {
+  WkParams pk;
+  size_t wsk = 0;
+  if (plan_wgrad_kd(B, Cin, Cout, D, H, W, pk, wsk)) return wsk + 256;
   WgPlan pl;
   if (plan_wgrad(B, Cin, Cout, D, H, W, pl) != VM_OK) return 0;
   return pl.ws_main + pl.ws_bias + 256;
@@ -1435,6 +1688,29 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
   VM_REQUIRE(x && gy && gw && gb && ws, VM_E_ARG, "vm_conv3d_wgrad_tc: null pointer");
   VM_REQUIRE(B > 0 && Cin > 0 && Cout > 0 && D > 0 && H > 0 && W > 0, VM_E_SHAPE,
              "vm_conv3d_wgrad_tc: bad shape");
+  {
+    WkParams pk;
+    size_t wsk = 0;
+    if (plan_wgrad_kd(B, Cin, Cout, D, H, W, pk, wsk)) {
+      pk.x = static_cast<const bf16*>(x);
+      pk.x_bstride = x_bstride ? x_bstride : default_bstride(Cin, D, H, W, 1);
+      pk.ws = static_cast<float*>(ws);
+      const int64_t gbs = gy_bstride ? gy_bstride : default_bstride(Cout, D, H, W, 1);
+      CUtensorMap gmap;
+      int rc = make_group_map(&gmap, gy, gbs, pk.CGo, pk.rows, B, pk.KS, pk.CGo);
+      if (rc) return rc;
+      cudaStream_t st = as_stream(stream);
+      cudaFuncSetAttribute(k_conv_wgrad_kd, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
+      k_conv_wgrad_kd<<<pk.grid, 192, (size_t)pk.stages * pk.stage_bytes, st>>>(gmap, pk);
+      rc = launch_status("vm_conv3d_wgrad_tc (kd)");
+      if (rc) return rc;
+      const int nk = pk.grid / pk.n_mtgroups;
+      const int64_t E = (int64_t)pk.MT * 9 * pk.Nc * 128;
+      k_wgrad_kd_finalize<<<grid_for(E, 256), 256, 0, st>>>(pk.ws, gw, gb, nk, pk.MT, pk.Nc, pk.CG, Cin, Cout,
+                                                            pk.ones_slot);
+      return launch_status("vm_conv3d_wgrad_tc (kd) finalize");
+    }
+  }
   WgPlan pl;
   int rc = plan_wgrad(B, Cin, Cout, D, H, W, pl);
   if (rc) return rc;

@@ -129,6 +129,12 @@ WG_SHAPES = [
     (1, 32, 32, 6, 8, 64),
     (2, 16, 32, 4, 4, 40),
     (1, 1, 16, 4, 6, 126),
+    # kd-along-N kernel (Cout <= 48, W >= 32): padded co groups, several M-tile groups,
+    # deep volumes (kd slices reaching outside the sample)
+    (1, 16, 48, 5, 6, 40),
+    (2, 24, 8, 3, 5, 34),
+    (1, 96, 32, 4, 4, 64),
+    (1, 8, 16, 40, 4, 32),
 ]
 
 
