@@ -1074,8 +1074,9 @@ struct WkParams {
   uint32_t a_bytes;
   uint32_t g_bytes;  // per kd slice: Nc/8 group slots of KS rows (CGo of them loaded)
   uint32_t g_load;   // loaded bytes per kd slice: CGo * KS * 16
-  uint32_t stage_bytes, idesc;
+  uint32_t stage_bytes, idesc, idesc64;  // M = 64 for M-tiles with <= 8 live slots
   float* ws;  // [kidx][MT][3 kw][3*Nc][128]
+  long long* dbg;  // optional cycle probes [gridDim][8] (vm_debug_set_fwd_probe)
 };
 
 __global__ void __launch_bounds__(192, 1)
@@ -1092,6 +1093,9 @@ __global__ void __launch_bounds__(192, 1)
   const int r0 = (16 * mt0) / 3;
   const int slot_shift = 16 * mt0 - 3 * r0;
   const uint32_t GS = (uint32_t)p.Wp * 16;
+  // the CTA's last M-tile runs as M = 64 when it holds <= 8 live slots (ones slot included):
+  // half the A-operand reads (TMEM rows m -> lanes (m/16)*32 + m%16)
+  const bool last64 = 3 * p.CG + 1 - 16 * (mt0 + nmt - 1) <= 8;
   if (p.ones_slot >= 0 && p.ones_slot / 16 >= mt0 && p.ones_slot / 16 < mt0 + nmt) {
     const int local = p.ones_slot - mt0 * 16 + slot_shift;
     for (int s = 0; s < p.stages; ++s) {
@@ -1123,6 +1127,7 @@ __global__ void __launch_bounds__(192, 1)
       const int nrun = r_end >= r0 ? r_end - r0 + 1 : 0;
       const int Rrun = p.KS + 2 * p.Wp + 2;
       const uint32_t tx = (uint32_t)nrun * Rrun * 16 + 3 * p.g_load;
+      long long t_pe = 0;
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
         const int ks = (u / p.n_mtgroups) % p.ksplit;
         const int b = u / (p.n_mtgroups * p.ksplit);
@@ -1130,7 +1135,9 @@ __global__ void __launch_bounds__(192, 1)
         const bf16* xb = p.x + b * p.x_bstride;
         for (int s = s0; s < s1; ++s) {
           const int k0 = s * p.KS;
+          const long long tw = clock64();
           mbar_wait(&empty[stage], phase ^ 1);
+          t_pe += clock64() - tw;
           uint8_t* sA = smem + (size_t)stage * p.stage_bytes;
           uint8_t* sG = sA + p.a_bytes;
           mbar_arrive_expect_tx(&full[stage], tx);
@@ -1146,16 +1153,23 @@ __global__ void __launch_bounds__(192, 1)
           }
         }
       }
+      if (p.dbg) p.dbg[blockIdx.x * 8 + 7] = t_pe;
     }
   } else if (warp == 1) {
     int stage = 0;
     uint32_t phase = 0;
     bool started = false;
+    const uint32_t id_last = last64 ? p.idesc64 : p.idesc;
+    const long long t0 = clock64();
+    long long t_fu = 0, t_is = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       const int ks = (u / p.n_mtgroups) % p.ksplit;
       const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
       for (int s = s0; s < s1; ++s) {
+        const long long tf = clock64();
         mbar_wait(&full[stage], phase);
+        const long long tf1 = clock64();
+        t_fu += tf1 - tf;
         tc_fence_after();
         if (elect_one()) {
           const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes);
@@ -1171,14 +1185,16 @@ __global__ void __launch_bounds__(192, 1)
             for (int m = 0; m < nmt; ++m) {
               const uint64_t adesc = a0desc + (uint64_t)(m * mstep + kk * 16);
               const uint32_t d = tbase + (uint32_t)(m * 3 * N3);
-              mma_bf16_ss(d, adesc, bdesc, p.idesc, acc);
-              mma_bf16_ss(d + N3, adesc + 1, bdesc, p.idesc, acc);
-              mma_bf16_ss(d + 2 * N3, adesc + 2, bdesc, p.idesc, acc);
+              const uint32_t id = m == nmt - 1 ? id_last : p.idesc;
+              mma_bf16_ss(d, adesc, bdesc, id, acc);
+              mma_bf16_ss(d + N3, adesc + 1, bdesc, id, acc);
+              mma_bf16_ss(d + 2 * N3, adesc + 2, bdesc, id, acc);
             }
           }
           mma_commit(&empty[stage]);
         }
         __syncwarp();
+        t_is += clock64() - tf1;
         started = true;
         if (++stage == p.stages) {
           stage = 0;
@@ -1188,22 +1204,32 @@ __global__ void __launch_bounds__(192, 1)
     }
     if (elect_one()) mma_commit(&tfull);
     __syncwarp();
+    if (p.dbg && lane == 0) {
+      p.dbg[blockIdx.x * 8 + 0] = clock64() - t0;
+      p.dbg[blockIdx.x * 8 + 2] = t_fu;
+      p.dbg[blockIdx.x * 8 + 3] = t_is;
+    }
   } else {
     // drain: warp (2..5) reads TMEM lane quarter warp & 3
     const int q = warp & 3;
     const int kidx = blockIdx.x / p.n_mtgroups;
     mbar_wait(&tfull, 0);
     tc_fence_after();
-    const int m_row = q * 32 + lane;
-    for (int m = 0; m < nmt; ++m)
+    for (int m = 0; m < nmt; ++m) {
+      const bool m64 = last64 && m == nmt - 1;
+      const int m_row = m64 ? q * 16 + lane : q * 32 + lane;
+      const bool live = !m64 || lane < 16;
       for (int c0 = 0; c0 < 3 * N3; c0 += 16) {
         uint32_t r[16];
         tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(m * 3 * N3 + c0), r);
         tmem_ld_wait();
         float* dst = p.ws + (((int64_t)kidx * p.MT + mt0 + m) * 3 * N3 + c0) * 128 + m_row;
+        if (live) {
 #pragma unroll
-        for (int e = 0; e < 16; ++e) dst[e * 128] = __uint_as_float(r[e]);
+          for (int e = 0; e < 16; ++e) dst[e * 128] = __uint_as_float(r[e]);
+        }
       }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -1666,6 +1692,7 @@ static bool plan_wgrad_kd(int B, int Cin, int Cout, int D, int H, int W, WkParam
   p.ksplit = (p.stages_total + p.spk - 1) / p.spk;
   p.units = p.n_mtgroups * B * p.ksplit;
   p.idesc = make_idesc_bf16(128, 3 * p.Nc, true, true);
+  p.idesc64 = make_idesc_bf16(64, 3 * p.Nc, true, true);
   p.grid = p.units;
   if (p.grid > nsm) p.grid = (nsm / p.n_mtgroups) * p.n_mtgroups;
   if (p.grid < p.n_mtgroups) p.grid = p.n_mtgroups;
@@ -1695,6 +1722,7 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
       pk.x = static_cast<const bf16*>(x);
       pk.x_bstride = x_bstride ? x_bstride : default_bstride(Cin, D, H, W, 1);
       pk.ws = static_cast<float*>(ws);
+      pk.dbg = g_fwd_dbg;
       const int64_t gbs = gy_bstride ? gy_bstride : default_bstride(Cout, D, H, W, 1);
       CUtensorMap gmap;
       int rc = make_group_map(&gmap, gy, gbs, pk.CGo, pk.rows, B, pk.KS, pk.CGo);

@@ -6,7 +6,7 @@
 #include <vector>
 #include "../../paper_1909_03108_b200/csrc/sm100.cuh"
 
-template <int N>
+template <int N, bool MN, int M = 128>
 __global__ void k_tput(int iters, int wp, int chains, long long* cycles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
@@ -23,9 +23,10 @@ __global__ void k_tput(int iters, int wp, int chains, long long* cycles) {
   if (threadIdx.x < 32) {
     uint32_t base = vm::smem_u32(smem);
     const int R = 4096;  // rows per K half (64 KB)
-    constexpr uint32_t id = vm::make_idesc_bf16(128, N, false, false);
-    uint64_t bd = vm::make_sdesc(base + 2 * R * 16, N * 16, 128);
-    uint64_t ad0 = vm::make_sdesc(base, R * 16, 128);
+    constexpr uint32_t id = vm::make_idesc_bf16(M, N, MN, MN);
+    // K-major: LBO = K-half distance, SBO = 128; MN-major: LBO = 128 (8-row K groups), SBO = MN-group stride
+    uint64_t bd = MN ? vm::make_sdesc(base + 64 * 1024, 128, 256 * 16) : vm::make_sdesc(base + 2 * R * 16, N * 16, 128);
+    uint64_t ad0 = MN ? vm::make_sdesc(base, 128, (uint32_t)wp * 16 > 0 ? (uint32_t)wp * 16 : 2048) : vm::make_sdesc(base, R * 16, 128);
     long long t0 = clock64();
     if (vm::elect_one()) {
       for (int it = 0; it < iters; it += 9 * chains) {
@@ -48,25 +49,25 @@ __global__ void k_tput(int iters, int wp, int chains, long long* cycles) {
   if (threadIdx.x < 32) vm::tmem_dealloc<512>(tbase);
 }
 
-template <int N>
+template <int N, bool MN = false, int M = 128>
 void run(int wp, int chains) {
   const int grid = 148, iters = 9 * 24 * 100;
   long long* d; cudaMalloc(&d, grid * 8);
-  cudaFuncSetAttribute(k_tput<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  k_tput<N><<<grid, 128, 200 * 1024>>>(9 * chains, wp, chains, d);
-  k_tput<N><<<grid, 128, 200 * 1024>>>(iters, wp, chains, d);
+  cudaFuncSetAttribute(k_tput<N, MN, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  k_tput<N, MN, M><<<grid, 128, 200 * 1024>>>(9 * chains, wp, chains, d);
+  k_tput<N, MN, M><<<grid, 128, 200 * 1024>>>(iters, wp, chains, d);
   cudaError_t err = cudaDeviceSynchronize();
   std::vector<long long> h(grid); cudaMemcpy(h.data(), d, grid * 8, cudaMemcpyDeviceToHost);
   double avg = 0; for (auto x : h) avg += x; avg /= grid;
-  printf("N=%3d wp=%3d (taps %s) chains=%d: %6.2f cyc/mma  %s\n", N, wp,
-         wp == 0 ? "all aligned" : (wp % 8 ? "row-shifted, misaligned" : "kh aligned, kw shifted"), chains,
+  printf("M=%d %s N=%3d wp=%3d chains=%d: %6.2f cyc/mma  %s\n", M, MN ? "MN-major" : "K-major ", N, wp, chains,
          avg / iters, err ? cudaGetErrorString(err) : "");
   cudaFree(d);
 }
 
 int main() {
-  for (int chains : {1, 2, 3, 4, 6, 8}) {
-    run<16>(130, chains); run<32>(130, chains); run<48>(130, chains); run<96>(130, chains); run<144>(130, chains);
+  for (int chains : {1, 3, 4}) {
+    run<48, true, 64>(130, chains); run<96, true, 64>(130, chains); run<48, true, 128>(130, chains);
+    run<16, false, 64>(130, chains); run<48, false, 64>(130, chains); run<96, false, 64>(130, chains);
   }
   return 0;
 }
