@@ -182,6 +182,8 @@ struct FwdParams {
   int CG, KC;        // input groups, chunks
   int Cout, Nc, nchunk;
   int MB, Ralloc, stages;
+  int nacc;          // accumulator sets per tile (kd % nacc): independent MMA chains
+  int nbuf;          // TMEM buffers across units (2: epilogue overlaps the next unit)
   int mblocks;       // per sample
   int units;
   uint32_t a_bytes;  // per group per stage
@@ -265,6 +267,7 @@ __global__ void __launch_bounds__(320, 1)
       for (int s = 0; s < nstage_k; ++s) {
         const int kc = s / 3;
         const int ng = (kc * 2 + 1 < p.CG) ? 2 : 1;
+        const int aset = s % p.nacc;  // consecutive stages feed different accumulators
         long long tf0 = clock64();
         mbar_wait(&full[stage], phase);
         t_wait_full += clock64() - tf0;
@@ -276,17 +279,19 @@ __global__ void __launch_bounds__(320, 1)
           // descriptors advance by plain adds on the 16-byte address field
           const uint64_t a0desc = make_sdesc(sA, lbo_a, 128);
           const uint64_t b0desc = make_sdesc(sB, p.Nc * 16, 128);
-          const uint32_t d0 = tbase + (uint32_t)(ab * p.MB * p.Nc);
+          // TMEM column of (buffer ab, tile i, set a) = ((ab*MB + i)*nacc + a)*Nc
+          const uint32_t d0 = tbase + (uint32_t)((ab * p.MB * p.nacc + aset) * p.Nc);
+          const uint32_t tstep = (uint32_t)(p.nacc * p.Nc);
           const uint32_t bstep = (uint32_t)(2 * p.Nc * 16) >> 4;
 #pragma unroll 1
           for (int j = 0; j < 9; ++j) {
             const uint64_t bdesc = b0desc + (uint64_t)(j * bstep);
             const uint64_t adesc = a0desc + (uint64_t)((j / 3) * p.Wp + (j % 3));
-            const uint32_t acc = (s > 0 || j > 0) ? 1u : 0u;
+            const uint32_t acc = (s >= p.nacc || j > 0) ? 1u : 0u;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               if (i < p.MB)
-                mma_bf16_ss(d0 + (uint32_t)(i * p.Nc), adesc + (uint64_t)(i * 128), bdesc, p.idesc, acc);
+                mma_bf16_ss(d0 + (uint32_t)i * tstep, adesc + (uint64_t)(i * 128), bdesc, p.idesc, acc);
             }
           }
           mma_commit(&empty[stage]);
@@ -299,7 +304,7 @@ __global__ void __launch_bounds__(320, 1)
       }
       if (elect_one()) mma_commit(&tfull[ab]);
       __syncwarp();
-      if (++ab == 2) {
+      if (++ab == p.nbuf) {
         ab = 0;
         aphase ^= 1;
       }
@@ -347,7 +352,7 @@ __global__ void __launch_bounds__(320, 1)
         const int hq = (int)qa - (int)qh * p.Hp;
         const bool valid = a < p.anchors && wq < p.W && hq < p.H;
         const int64_t orow = (int64_t)a + p.P + p.Wp + 1;
-        const uint32_t tcol = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * p.MB + i) * p.Nc);
+        const uint32_t tcol = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * p.MB + i) * p.nacc * p.Nc);
         for (int g0 = 0; g0 < ng_out; g0 += 8) {
           const int gn = min(8, ng_out - g0);
           int4 mk[8];
@@ -364,15 +369,22 @@ __global__ void __launch_bounds__(320, 1)
           for (int j = 0; j < 8; j += 2) {
             if (j >= gn) break;
             uint32_t r[16];
-            if (j + 1 < gn) {
-              tmem_ld16(tcol + (uint32_t)((g0 + j) * 8), r);
-            } else {
-              uint32_t r8[8];
-              tmem_ld8(tcol + (uint32_t)((g0 + j) * 8), r8);
+            for (int a = 0; a < p.nacc; ++a) {  // sum the accumulator sets (fixed order)
+              uint32_t ra[16];
+              const uint32_t ca = tcol + (uint32_t)(a * p.Nc + (g0 + j) * 8);
+              if (j + 1 < gn) {
+                tmem_ld16(ca, ra);
+              } else {
+                uint32_t r8[8];
+                tmem_ld8(ca, r8);
 #pragma unroll
-              for (int e = 0; e < 8; ++e) r[e] = r8[e];
+                for (int e = 0; e < 8; ++e) ra[e] = r8[e];
+              }
+              tmem_ld_wait();
+#pragma unroll
+              for (int e = 0; e < 16; ++e)
+                r[e] = a == 0 ? ra[e] : __float_as_uint(__uint_as_float(r[e]) + __uint_as_float(ra[e]));
             }
-            tmem_ld_wait();
 #pragma unroll
             for (int jj = 0; jj < 2; ++jj) {
               if (j + jj >= gn) break;
@@ -411,7 +423,7 @@ __global__ void __launch_bounds__(320, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty[ab]);
-      if (++ab == 2) {
+      if (++ab == p.nbuf) {
         ab = 0;
         aphase ^= 1;
       }
@@ -1454,25 +1466,54 @@ extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wp
   p.b_bytes = 9 * 2 * p.Nc * 16;
   const int N = p.Nc;  // accumulator columns per tile
   const int tiles = (int)((p.anchors + 127) / 128);
-  // accumulators: 2 buffers x MB x N fp32 columns <= 512
-  int MB = 256 / N;
-  if (MB > 8) MB = 8;
-  const int mb_fill = (int)((int64_t)tiles * B * p.nchunk / nsm);  // keep >= 1 unit per SM
-  if (MB > mb_fill) MB = mb_fill;
-  if (MB < 1) MB = 1;
-  for (;;) {
-    p.R = MB * 128 + 2 * p.Wp + 2;
-    p.Ralloc = (p.R + 7) / 8 * 8;
-    p.a_bytes = (uint32_t)p.Ralloc * 16;
-    p.stage_bytes = 2 * p.a_bytes + p.b_bytes;
-    p.stages = kSmemBudget / (int)p.stage_bytes;
-    if (p.stages > kMaxStages) p.stages = kMaxStages;
-    if (p.stages >= 2 || MB == 1) break;
-    MB /= 2;
+  // Plan (MB tiles per unit, nacc accumulator sets, nbuf TMEM buffers) by a cost model of the
+  // measured B200 behaviour: an MMA waits for the previous one into the same accumulator
+  // (~68+ cycles), >= 3 independent chains reach max(N/2, 32 + N/4) cycles (tools/probes,
+  // profiles/r01/probe_tput5.txt); a stage also pays its shared-memory traffic (TMA writes +
+  // operand reads at ~128 B/clk).  Units = tiles/MB spread over the SMs in waves.
+  auto mma_cycles = [](int n, int chains) -> double {
+    const double bw = n / 2.0 > 32 + n / 4.0 ? n / 2.0 : 32 + n / 4.0;
+    if (chains >= 3) return bw + 1;
+    if (chains == 2) return bw * 1.3 > 49 ? bw * 1.3 : 49;
+    return bw > 68 ? bw * 1.5 : 68;
+  };
+  double best = 1e30;
+  int bMB = 1, bacc = 1, bbuf = 1, bstages = 0;
+  for (int MB = 1; MB <= 8; ++MB) {
+    const int R = MB * 128 + 2 * p.Wp + 2;
+    const uint32_t a_bytes = (uint32_t)((R + 7) / 8 * 8) * 16;
+    const uint32_t stage_bytes = 2 * a_bytes + p.b_bytes;
+    int stages = kSmemBudget / (int)stage_bytes;
+    if (stages > kMaxStages) stages = kMaxStages;
+    if (stages < 2) continue;
+    const int64_t units = (int64_t)B * ((tiles + MB - 1) / MB) * p.nchunk;
+    const int64_t waves = (units + nsm - 1) / nsm;
+    for (int nacc : {1, 3}) {
+      for (int nbuf = 2; nbuf >= 1; --nbuf) {
+        if (nbuf * MB * nacc * N > 512) continue;
+        const double mma = 9.0 * MB * mma_cycles(N, MB * nacc);
+        const double smem = (2.0 * R * 16 + p.b_bytes + 9.0 * MB * (4096 + 32.0 * N)) / 128.0;
+        const double stage = mma > smem ? mma : smem;
+        // single-buffered TMEM: the epilogue drain (~MB*N/8 x 200 cycles) is not overlapped
+        const double drain = nbuf == 1 ? MB * (N / 8.0) * 200.0 / (MB > 1 ? 2 : 1) : 0.0;
+        const double cost = (double)waves * (3.0 * p.KC * stage + drain + 2000.0);
+        if (cost < best * 0.999) {
+          best = cost;
+          bMB = MB, bacc = nacc, bbuf = nbuf, bstages = stages;
+        }
+      }
+    }
   }
-  VM_REQUIRE(p.stages >= 2, VM_E_UNSUPPORTED, "vm_conv3d_fwd_tc: W=%d too wide for the stage budget", W);
-  p.MB = MB;
-  p.mblocks = (tiles + MB - 1) / MB;
+  VM_REQUIRE(bstages >= 2, VM_E_UNSUPPORTED, "vm_conv3d_fwd_tc: W=%d too wide for the stage budget", W);
+  p.MB = bMB;
+  p.nacc = bacc;
+  p.nbuf = bbuf;
+  p.R = p.MB * 128 + 2 * p.Wp + 2;
+  p.Ralloc = (p.R + 7) / 8 * 8;
+  p.a_bytes = (uint32_t)p.Ralloc * 16;
+  p.stage_bytes = 2 * p.a_bytes + p.b_bytes;
+  p.stages = bstages;
+  p.mblocks = (tiles + p.MB - 1) / p.MB;
   p.units = B * p.mblocks * p.nchunk;
   p.idesc = make_idesc_bf16(128, N, false, false);
   (void)rows;

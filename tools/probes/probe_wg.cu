@@ -8,12 +8,20 @@
 #include "../../paper_1909_03108_b200/csrc/sm100.cuh"
 
 template <int M, int N>
-__global__ void k_wg(int stages, int badv, int aadv, long long* cycles) {
+__global__ void k_wg(int stages, int badv, int aadv, int rnd, long long* cycles, const uint8_t* gsrc, int tma_kb,
+                     int fence) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
-  for (int i = threadIdx.x * 16; i < 200 * 1024; i += blockDim.x * 16)
-    *reinterpret_cast<int4*>(smem + i) = make_int4(0, 0, 0, 0);
+  for (int i = threadIdx.x * 4; i < 200 * 1024; i += blockDim.x * 4) {
+    uint32_t h = (uint32_t)i * 2654435761u + 12345u;
+    h ^= h >> 13;
+    h *= 0x5bd1e995u;
+    // two bf16 in [-1, 1): sign/exponent 0x3F (1.x) or 0xBF, random mantissa
+    const uint32_t lo = ((h & 1u) ? 0xBF00u : 0x3F00u) | ((h >> 1) & 0x7Fu);
+    const uint32_t hi = ((h & 256u) ? 0xBF00u : 0x3F00u) | ((h >> 9) & 0x7Fu);
+    *reinterpret_cast<uint32_t*>(smem + i) = rnd ? (hi << 16 | lo) : 0u;
+  }
   vm::fence_proxy_async_smem();
   if (threadIdx.x == 0) { vm::mbar_init(&bar, 1); vm::fence_barrier_init(); }
   if (threadIdx.x < 32) vm::tmem_alloc<512>(&tslot);
@@ -21,6 +29,25 @@ __global__ void k_wg(int stages, int badv, int aadv, long long* cycles) {
   __syncthreads();
   vm::tc_fence_after();
   uint32_t tbase = tslot;
+  __shared__ uint64_t tbar, cbar[2];
+  __shared__ volatile int done;
+  if (threadIdx.x == 0) { vm::mbar_init(&tbar, 1); vm::mbar_init(&cbar[0], 1); vm::mbar_init(&cbar[1], 1); done = 0; vm::fence_barrier_init(); }
+  __syncthreads();
+  if (threadIdx.x >= 32 && threadIdx.x < 64 && tma_kb > 0) {
+    // concurrent TMA traffic: bulk copies of tma_kb KB into smem[192 KB ..) in a loop
+    uint32_t ph = 0;
+    while (!done) {
+      if (threadIdx.x == 32) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(vm::smem_u32(&tbar)), "r"(tma_kb * 1024) : "memory");
+        for (int c = 0; c < tma_kb; c += 8)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(vm::smem_u32(smem + 150 * 1024)),
+                       "l"(gsrc + (size_t)blockIdx.x * 65536 + c * 1024), "r"(8192), "r"(vm::smem_u32(&tbar)) : "memory");
+      }
+      __syncwarp();
+      vm::mbar_wait(&tbar, ph);
+      ph ^= 1;
+    }
+  }
   if (threadIdx.x < 32) {
     const uint32_t base = vm::smem_u32(smem);
     const uint32_t GS = 130 * 16, KS = 128;
@@ -28,8 +55,10 @@ __global__ void k_wg(int stages, int badv, int aadv, long long* cycles) {
     long long t0 = clock64();
     if (vm::elect_one()) {
       for (int s = 0; s < stages; ++s) {
-        const uint32_t sb = base + (uint32_t)(s & 1) * 96 * 1024;
-        const uint64_t b0 = vm::make_sdesc(sb + 64 * 1024, 128, KS * 16);
+        if (fence & 1) vm::tc_fence_after();
+        if (fence & 2) vm::mma_commit(&cbar[s & 1]);
+        const uint32_t sb = base + (uint32_t)(s & 1) * 64 * 1024;
+        const uint64_t b0 = vm::make_sdesc(sb + 40 * 1024, 128, KS * 16);
         const uint64_t a0 = vm::make_sdesc(sb, 128, GS);
 #pragma unroll 1
         for (int kk = 0; kk < (int)KS / 16; ++kk) {
@@ -46,6 +75,7 @@ __global__ void k_wg(int stages, int badv, int aadv, long long* cycles) {
     vm::mbar_wait(&bar, 0);
     long long t1 = clock64();
     if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+    if (threadIdx.x == 0) done = 1;
   }
   vm::tc_fence_before();
   __syncthreads();
@@ -53,22 +83,24 @@ __global__ void k_wg(int stages, int badv, int aadv, long long* cycles) {
 }
 
 template <int M, int N>
-void run(int badv, int aadv) {
+void run(int badv, int aadv, int rnd = 0, int tma_kb = 0, int fence = 0) {
+  static uint8_t* gsrc = nullptr;
+  if (!gsrc) { cudaMalloc(&gsrc, 148 * 65536 + 65536); cudaMemset(gsrc, 0, 148 * 65536 + 65536); }
   const int grid = 148, stages = 400;
   long long* d; cudaMalloc(&d, grid * 8);
   cudaFuncSetAttribute(k_wg<M, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  k_wg<M, N><<<grid, 128, 200 * 1024>>>(4, badv, aadv, d);
-  k_wg<M, N><<<grid, 128, 200 * 1024>>>(stages, badv, aadv, d);
+  k_wg<M, N><<<grid, 128, 200 * 1024>>>(4, badv, aadv, rnd, d, gsrc, tma_kb, fence);
+  k_wg<M, N><<<grid, 128, 200 * 1024>>>(stages, badv, aadv, rnd, d, gsrc, tma_kb, fence);
   cudaError_t err = cudaDeviceSynchronize();
   std::vector<long long> h(grid); cudaMemcpy(h.data(), d, grid * 8, cudaMemcpyDeviceToHost);
   double avg = 0; for (auto x : h) avg += x; avg /= grid;
-  printf("M=%3d N=%3d B %s A %s: %6.2f cyc/mma %s\n", M, N, badv ? "advancing" : "fixed    ",
+  printf("fence %d tma %2d KB/round ", fence, tma_kb);
+  printf("%s M=%3d N=%3d B %s A %s: %6.2f cyc/mma %s\n", rnd ? "random" : "zeros ", M, N, badv ? "advancing" : "fixed    ",
          aadv ? "advancing" : "fixed    ", avg / (stages * 24.0), err ? cudaGetErrorString(err) : "");
   cudaFree(d);
 }
 
 int main() {
-  for (int badv : {0, 1})
-    for (int aadv : {0, 1}) { run<128, 48>(badv, aadv); run<64, 48>(badv, aadv); run<128, 16>(badv, aadv); }
+  for (int f : {0, 1, 2, 3}) { run<128, 48>(1, 1, 1, 0, f); run<64, 48>(1, 1, 1, 0, f); run<128, 128>(1, 1, 1, 0, f); }
   return 0;
 }
