@@ -389,25 +389,114 @@ class UNetStep:
     def upload(self, image_host, labels_host):
         """Public-API input path: host f32 image [B,D,H,W,Cin] + u8 labels [B,D,H,W]
         -> (pinned) H2D -> slab + on-device one-hot (training.py:68-69, :276-279)."""
-        if getattr(self, "_img_dev", None) is None:
-            self._img_dev = torch.empty(tuple(image_host.shape), dtype=torch.float32, device=self.device)
-            self._lab_dev = torch.empty(tuple(labels_host.shape), dtype=torch.uint8, device=self.device)
-        self._img_dev.copy_(image_host, non_blocking=True)
-        self._lab_dev.copy_(labels_host, non_blocking=True)
-        x = self.x_in
-        self._k("io", "image", 0, 0, "vm_dense_to_slab", _lib.ptr(self._img_dev), _lib.VM_F32, x.p(), self.dt,
-                x.bstride, self.B, x.C, x.D, x.H, x.W, 1)
-        self._k("io", "onehot", 0, 0, "vm_onehot_u8", _lib.ptr(self._lab_dev), _lib.ptr(self.onehot), self.nvox,
-                self.ncls)
+        self._stage_h2d(image_host, labels_host)
+        self._consume_staged()
 
-    def train_step_host(self, image_host, labels_host, replay=None):
-        """One step through the public API: H2D inputs, step (or graph replay), D2H loss."""
-        self.upload(image_host, labels_host)
+    # Double-buffered host->device staging: the H2D of step k+1's inputs runs on a copy
+    # stream while step k computes (a data loader's prefetch); each step still moves its own
+    # input bytes and reads its loss back.
+    def _stage_bufs(self, image_host, labels_host):
+        if getattr(self, "_stage", None) is None:
+            self._stage = [(torch.empty(tuple(image_host.shape), dtype=torch.float32, device=self.device),
+                            torch.empty(tuple(labels_host.shape), dtype=torch.uint8, device=self.device))
+                           for _ in range(2)]
+            self._copy_stream = torch.cuda.Stream(device=self.device)
+            self._copied = [None, None]   # event: H2D into buffer i done
+            self._consumed = [None, None]  # event: buffer i read by the compute stream
+            self._next = 0                 # buffer the next step consumes
+            self._pending = None           # buffer holding a prefetched input, if any
+
+    def _stage_h2d(self, image_host, labels_host, on_copy_stream=False):
+        self._stage_bufs(image_host, labels_host)
+        i = self._next if self._pending is None else 1 - self._pending
+        img, lab = self._stage[i]
+        if on_copy_stream:
+            cs = self._copy_stream
+            if self._consumed[i] is not None:
+                cs.wait_event(self._consumed[i])
+            with torch.cuda.stream(cs):
+                img.copy_(image_host, non_blocking=True)
+                lab.copy_(labels_host, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+            self._copied[i] = ev
+        else:
+            img.copy_(image_host, non_blocking=True)
+            lab.copy_(labels_host, non_blocking=True)
+            self._copied[i] = None
+        self._pending = i
+
+    def _consume_staged(self):
+        i = self._pending
+        img, lab = self._stage[i]
+        if self._copied[i] is not None:
+            torch.cuda.current_stream().wait_event(self._copied[i])
+        x = self.x_in
+        self._k("io", "image", 0, 0, "vm_dense_to_slab", _lib.ptr(img), _lib.VM_F32, x.p(), self.dt,
+                x.bstride, self.B, x.C, x.D, x.H, x.W, 1)
+        self._k("io", "onehot", 0, 0, "vm_onehot_u8", _lib.ptr(lab), _lib.ptr(self.onehot), self.nvox,
+                self.ncls)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._consumed[i] = ev
+        self._pending = None
+        self._next = 1 - i
+
+    def train_step_host(self, image_host, labels_host, replay=None, next_inputs=None):
+        """One step through the public API: H2D inputs, step (or graph replay), D2H loss.
+
+        ``next_inputs = (image_host, labels_host)`` of the following step starts that step's
+        H2D on a copy stream while this step computes; the following call then consumes the
+        prefetched buffer (its own ``image_host``/``labels_host`` must be those tensors)."""
+        if self._has_prefetch(image_host):
+            self._consume_staged()
+        else:
+            self.upload(image_host, labels_host)
         if replay is not None:
             replay()
         else:
             self.step()
+        if next_inputs is not None:
+            self._stage_h2d(next_inputs[0], next_inputs[1], on_copy_stream=True)
+            self._prefetched_src = next_inputs[0]
         return self.loss()[0]
+
+    def train_loop_host(self, batches, replay=None):
+        """Pipelined public-API training loop over host batches ``[(image, labels), ...]``
+        (pinned): every step moves its inputs host->device (step k+1's on a copy stream while
+        step k computes) and its loss statistics device->host (async copy into pinned memory);
+        the host reads step k's loss while step k+1 runs, like a training loop that logs one
+        step behind.  Returns the per-step (combined, dice, ce) losses."""
+        batches = list(batches)
+        if getattr(self, "_loss_host", None) is None:
+            self._loss_host = [torch.empty(self.stats.numel(), dtype=self.stats.dtype).pin_memory()
+                               for _ in range(2)]
+        out, prev = [], None
+        self.upload(*batches[0])
+        for k in range(len(batches)):
+            if k > 0:
+                self._consume_staged()
+            if replay is not None:
+                replay()
+            else:
+                self.step()
+            buf = self._loss_host[k % 2]
+            buf.copy_(self.stats, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            if k + 1 < len(batches):
+                self._stage_h2d(*batches[k + 1], on_copy_stream=True)
+            if prev is not None:
+                prev[0].synchronize()
+                out.append(self._loss_from(prev[1].numpy()))
+            prev = (ev, buf)
+        prev[0].synchronize()
+        out.append(self._loss_from(prev[1].numpy()))
+        return out
+
+    def _has_prefetch(self, image_host):
+        return (getattr(self, "_pending", None) is not None and self._copied[self._pending] is not None
+                and getattr(self, "_prefetched_src", None) is image_host)
 
     # ------------------------------------------------------------------ passes
     def forward(self):
@@ -594,7 +683,10 @@ class UNetStep:
     # ------------------------------------------------------------------ readout
     def loss(self):
         """(combined, dice, ce) from the reduced statistics (training.py:95-107)."""
-        s = self.stats.double().cpu().numpy()
+        return self._loss_from(self.stats.double().cpu().numpy())
+
+    def _loss_from(self, s):
+        s = np.asarray(s, dtype=np.float64)
         c = self.ncls
         ks = [k for k in range(c) if (self.dice_mask >> k) & 1]
         ratios = [(2.0 * s[k] + 1e-6) / (s[c + k] + s[2 * c + k] + 1e-6) for k in ks]

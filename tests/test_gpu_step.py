@@ -67,3 +67,64 @@ def test_tc_step_matches_simt_step_and_oracle():
     worst = max(rel_l2(grads[k][0], rgrads[k][0]) for k in rgrads)
     assert worst <= 1e-1, worst
     mesh.shutdown()
+
+
+def test_tc_step_32cube_exercises_thin_kernels():
+    # W >= 32 and Cout <= 32: the kd-stacked sweep fwd/dgrad and the kd-along-N wgrad run
+    mesh, graph, params, x, oh = _setup(extent=32, filters=(16, 32), cpb=2, seed=3)
+    st, probs, stats, grads = _run(graph, params, x, oh, torch.bfloat16, "tc")
+    rprobs, rstats, rgrads, _ = oracle_step(graph, params, x, oh)
+    assert rel_l2(probs, rprobs) <= 1e-2
+    assert rel_l2(stats, rstats) <= 1e-2
+    worst = max(rel_l2(grads[k][0], rgrads[k][0]) for k in rgrads)
+    assert worst <= 1e-1, worst
+    worst_b = max(rel_l2(grads[k][1], rgrads[k][1]) for k in rgrads)
+    assert worst_b <= 1e-1, worst_b
+    mesh.shutdown()
+
+
+def test_train_step_host_prefetch_is_bitwise_the_plain_path():
+    # the copy-stream prefetch of step k+1's inputs must not change any result
+    extent = 32
+    cfg = vm.UNetConfig(extent, (16, 32), convs_per_block=2)
+    mesh = vm.create_mesh([("one", 1)])
+    graph = vm.build(cfg, mesh, {})
+    params = vm.init_params(graph, 5)
+    recs = [O.record_for(extent, i) for i in range(2)]
+    host = [(torch.from_numpy(img[None, ..., None].copy()).pin_memory(),
+             torch.from_numpy(lab[None].copy()).pin_memory()) for img, lab in recs]
+    a = UNetStep(graph, params, dtype=torch.bfloat16, device="cuda")
+    b = UNetStep(graph, params, dtype=torch.bfloat16, device="cuda")
+    la, lb = [], []
+    for k in range(4):
+        cur, nxt = host[k % 2], host[(k + 1) % 2]
+        la.append(a.train_step_host(cur[0], cur[1], next_inputs=nxt if k < 3 else None))
+        b.upload(cur[0], cur[1])
+        b.step()
+        lb.append(b.loss()[0])
+    torch.cuda.synchronize()
+    assert la == lb
+    pa, pb = a.param_dict(), b.param_dict()
+    for k in pa:
+        assert np.array_equal(pa[k]["kernel"], pb[k]["kernel"]) and np.array_equal(pa[k]["bias"], pb[k]["bias"])
+    mesh.shutdown()
+
+
+def test_train_loop_host_matches_step_by_step():
+    extent = 32
+    cfg = vm.UNetConfig(extent, (16, 32), convs_per_block=2)
+    mesh = vm.create_mesh([("one", 1)])
+    graph = vm.build(cfg, mesh, {})
+    params = vm.init_params(graph, 9)
+    recs = [O.record_for(extent, i) for i in range(3)]
+    host = [(torch.from_numpy(img[None, ..., None].copy()).pin_memory(),
+             torch.from_numpy(lab[None].copy()).pin_memory()) for img, lab in recs]
+    a = UNetStep(graph, params, dtype=torch.bfloat16, device="cuda")
+    b = UNetStep(graph, params, dtype=torch.bfloat16, device="cuda")
+    la = a.train_loop_host(host)
+    lb = [b.train_step_host(*h) for h in host]
+    assert [x[0] for x in la] == lb
+    pa, pb = a.param_dict(), b.param_dict()
+    for k in pa:
+        assert np.array_equal(pa[k]["kernel"], pb[k]["kernel"])
+    mesh.shutdown()
