@@ -1296,25 +1296,77 @@ extern "C" size_t vm_packed_weights_bytes(int Cin, int Cout) {
   return (size_t)g.nchunk * g.KC * 27 * 2 * g.Nc * 8 * sizeof(bf16);
 }
 
-// Batched repack of every layer's operands in one launch (after each SGD step).
+// Batched repack of every layer's operands in one launch (after each SGD step): grid.y = job,
+// one thread per 16-byte output vector (8 input channels of one (tap, output channel)), so
+// the decode runs once per vector and the fp32 reads are coalesced (plain: consecutive
+// threads read consecutive co; flip: each thread reads 8 consecutive floats).
 __global__ void k_pack_batch(const vm_pack_job* __restrict__ jobs, int njobs, int64_t total) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int lo = 0, hi = njobs - 1;
-    while (lo < hi) {  // last job with begin <= i
-      const int mid = (lo + hi + 1) >> 1;
-      if (jobs[mid].begin <= i) lo = mid; else hi = mid - 1;
+  const int jb_i = blockIdx.y;
+  const vm_pack_job& jb = jobs[jb_i];
+  const int64_t nvec = ((jb_i + 1 < njobs ? jobs[jb_i + 1].begin : total) - jb.begin) / 8;
+  const PackGeom g = jb.flip ? pack_geom(jb.cout, jb.cin) : pack_geom(jb.cin, jb.cout);
+  const float* __restrict__ w = jb.w;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = v;
+    int kd, kh, kw, kc, co, half;
+    if (g.sweep) {
+      const int n = r % (3 * g.Nc);
+      r /= 3 * g.Nc;
+      half = r % 2;
+      r /= 2;
+      const int j = r % 9;
+      kc = (int)(r / 9);
+      kh = j / 3;
+      kw = j % 3;
+      kd = 2 - n / g.Nc;
+      co = n % g.Nc;
+    } else {
+      const int n = r % g.Nc;
+      r /= g.Nc;
+      half = r % 2;
+      r /= 2;
+      const int j = r % 9;
+      r /= 9;
+      kd = r % 3;
+      r /= 3;
+      kc = r % g.KC;
+      co = (int)(r / g.KC) * g.Nc + n;
+      kh = j / 3;
+      kw = j % 3;
     }
-    const vm_pack_job& jb = jobs[lo];
-    const PackGeom g = jb.flip ? pack_geom(jb.cout, jb.cin) : pack_geom(jb.cin, jb.cout);
-    static_cast<bf16*>(jb.packed)[i - jb.begin] =
-        __float2bfloat16_rn(pack_value(g, i - jb.begin, jb.w, jb.cin, jb.cout, jb.flip));
+    const int t = (kd * 3 + kh) * 3 + kw;
+    const int ci0 = (kc * 2 + half) * 8;
+    float f[8];
+    if (!jb.flip) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        f[e] = (ci0 + e < g.cin && co < g.cout) ? w[((int64_t)t * jb.cin + ci0 + e) * jb.cout + co] : 0.f;
+    } else {  // W'[t][ci'][co'] = W[26 - t][co'][ci']: 8 consecutive floats of row co'
+      const float* src = w + ((int64_t)(26 - t) * jb.cin + co) * jb.cout + ci0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) f[e] = (ci0 + e < g.cin && co < g.cout) ? src[e] : 0.f;
+    }
+    uint4 o;
+    o.x = pack_bf16x2(f[0], f[1]);
+    o.y = pack_bf16x2(f[2], f[3]);
+    o.z = pack_bf16x2(f[4], f[5]);
+    o.w = pack_bf16x2(f[6], f[7]);
+    reinterpret_cast<uint4*>(jb.packed)[v] = o;
   }
 }
 
 extern "C" int vm_pack_weights_batch(const vm_pack_job* jobs, int njobs, int64_t total_elems, void* stream) {
   VM_REQUIRE(jobs && njobs > 0 && total_elems > 0, VM_E_ARG, "vm_pack_weights_batch: bad argument");
-  k_pack_batch<<<grid_for(total_elems, 256), 256, 0, as_stream(stream)>>>(jobs, njobs, total_elems);
+  VM_REQUIRE(njobs <= 65535, VM_E_ARG, "vm_pack_weights_batch: too many jobs");
+  // ~4 waves of 256-thread blocks over all jobs
+  int nsm = vm_num_sms(0);
+  if (nsm <= 0) nsm = 148;
+  const int64_t per_job = total_elems / 8 / njobs + 1;
+  int gx = (int)((per_job + 255) / 256);
+  const int cap = (4 * nsm * 8 + njobs - 1) / njobs;
+  if (gx > cap) gx = cap;
+  if (gx < 1) gx = 1;
+  k_pack_batch<<<dim3(gx, njobs), 256, 0, as_stream(stream)>>>(jobs, njobs, total_elems);
   return launch_status("vm_pack_weights_batch");
 }
 

@@ -170,3 +170,30 @@ def test_tc_wgrad_matches_simt_and_oracle(shape):
                                            np.zeros((3, 3, 3, cin, cout)))
     assert rel_l2(gw, rgk) <= 1e-5
     assert rel_l2(gb, rgb) <= 1e-5
+
+
+def test_batched_repack_equals_single_packs():
+    # vm_pack_weights_batch (one launch, every layer, both operands) == vm_pack_weights per job
+    shapes = [(1, 16), (16, 16), (48, 16), (16, 32), (96, 32), (64, 128), (128, 64), (24, 8), (16, 48)]
+    rng = np.random.default_rng(5)
+    ws, bufs, refs, rows, begin = [], [], [], [], 0
+    for cin, cout in shapes:
+        w = torch.from_numpy(rng.standard_normal(27 * cin * cout).astype(np.float32)).cuda()
+        ws.append(w)
+        for flip in (0, 1):
+            ci, co = (cout, cin) if flip else (cin, cout)
+            n = _lib.call_size("vm_packed_weights_bytes", ci, co) // 2
+            ref = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+            _lib.call("vm_pack_weights", _lib.ptr(w), _lib.ptr(ref), cin, cout, flip, _lib.stream_ptr())
+            buf = torch.full((n,), float("nan"), dtype=torch.bfloat16, device="cuda")
+            refs.append(ref)
+            bufs.append(buf)
+            rows.append((w.data_ptr(), buf.data_ptr(), cin, cout, flip, 0, begin))
+            begin += n
+    dt = np.dtype([("w", "<u8"), ("packed", "<u8"), ("cin", "<i4"), ("cout", "<i4"), ("flip", "<i4"),
+                   ("pad", "<i4"), ("begin", "<i8")])
+    jobs = torch.from_numpy(np.array(rows, dtype=dt).view(np.uint8).copy()).cuda()
+    _lib.call("vm_pack_weights_batch", _lib.ptr(jobs), len(rows), begin, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    for ref, buf in zip(refs, bufs):
+        assert torch.equal(ref.view(torch.int16), buf.view(torch.int16))
