@@ -40,14 +40,22 @@ template <> struct V8<__nv_bfloat16> {
   }
 };
 
-__device__ __forceinline__ void decompose(int64_t v, int D, int H, int W, int& b, int& d, int& h,
+// 32-bit index math: every launch checks that its index space fits (vm_fits32); 64-bit
+// division costs ~4x the instructions and these kernels are issue-bound at HBM speed
+__device__ __forceinline__ void decompose(uint32_t v, int D, int H, int W, int& b, int& d, int& h,
                                           int& w) {
-  w = v % W;
-  int64_t r = v / W;
-  h = r % H;
-  r /= H;
-  d = r % D;
-  b = (int)(r / D);
+  w = (int)(v % (uint32_t)W);
+  uint32_t r = v / (uint32_t)W;
+  h = (int)(r % (uint32_t)H);
+  r /= (uint32_t)H;
+  d = (int)(r % (uint32_t)D);
+  b = (int)(r / (uint32_t)D);
+}
+__device__ __forceinline__ int split_cg(int64_t i, int64_t nvox, uint32_t& v) {
+  const uint32_t i32 = (uint32_t)i, n32 = (uint32_t)nvox;
+  const uint32_t cg = i32 / n32;
+  v = i32 - cg * n32;
+  return (int)cg;
 }
 
 // ------------------------------------------------------------------ maxpool
@@ -58,9 +66,10 @@ __global__ void k_maxpool_fwd(const T* __restrict__ x, Slab gx, T* __restrict__ 
   const int64_t total = nvox * gy.CG;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int cg = (int)(i / nvox);
+    uint32_t v32;
+    int cg = split_cg(i, nvox, v32);
     int b, d, h, w;
-    decompose(i % nvox, gy.D, gy.H, gy.W, b, d, h, w);
+    decompose(v32, gy.D, gy.H, gy.W, b, d, h, w);
     float best[8];
     for (int cell = 0; cell < 8; ++cell) {  // (dz, dy, dx) scan order, ops.py:149-154
       float v[8];
@@ -81,36 +90,39 @@ __global__ void k_maxpool_bwd(const T* __restrict__ x, Slab gx, const T* __restr
   const int64_t total = nvox * go.CG;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int cg = (int)(i / nvox);
+    uint32_t v32;
+    int cg = split_cg(i, nvox, v32);
     int b, d, h, w;
-    decompose(i % nvox, go.D, go.H, go.W, b, d, h, w);
-    float xv[8][8];
+    decompose(v32, go.D, go.H, go.W, b, d, h, w);
+    // pass 1: argmax per channel (first max wins); pass 2 re-reads the 2x2x2 cell (L1/L2
+    // hits) for the ReLU mask instead of holding 64 values in registers
     int arg[8];
     float best[8];
 #pragma unroll
     for (int cell = 0; cell < 8; ++cell) {
-      V8<T>::ld(x + gx.at(b, cg, 2 * d + (cell >> 2), 2 * h + ((cell >> 1) & 1), 2 * w + (cell & 1)),
-                xv[cell]);
+      float xv[8];
+      V8<T>::ld(x + gx.at(b, cg, 2 * d + (cell >> 2), 2 * h + ((cell >> 1) & 1), 2 * w + (cell & 1)), xv);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        if (cell == 0 || xv[cell][j] > best[j]) {
-          best[j] = xv[cell][j];
+        if (cell == 0 || xv[j] > best[j]) {
+          best[j] = xv[j];
           arg[j] = cell;
         }
       }
     }
     float g[8];
     V8<T>::ld(gout + go.at(b, cg, d, h, w), g);
-#pragma unroll
+#pragma unroll 2
     for (int cell = 0; cell < 8; ++cell) {
       int pd = 2 * d + (cell >> 2), ph = 2 * h + ((cell >> 1) & 1), pw = 2 * w + (cell & 1);
-      float o[8];
+      float o[8], xv[8];
       if (add) V8<T>::ld(add + ga.at(b, cg, pd, ph, pw), o);
+      if (relu_mask) V8<T>::ld(x + gx.at(b, cg, pd, ph, pw), xv);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         float r = (arg[j] == cell) ? g[j] : 0.f;
         if (add) r += o[j];
-        if (relu_mask && !(xv[cell][j] > 0.f)) r = 0.f;
+        if (relu_mask && !(xv[j] > 0.f)) r = 0.f;
         o[j] = r;
       }
       V8<T>::st(gin + gi.at(b, cg, pd, ph, pw), o);
@@ -127,9 +139,10 @@ __global__ void k_upsample_fwd(const T* __restrict__ x, Slab gx, T* __restrict__
   const int64_t total = nvox * gy.CG;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int cg = (int)(i / nvox);
+    uint32_t v32;
+    int cg = split_cg(i, nvox, v32);
     int b, d, h, w;
-    decompose(i % nvox, gy.D, gy.H, gy.W, b, d, h, w);
+    decompose(v32, gy.D, gy.H, gy.W, b, d, h, w);
     const T* src = x + gx.at(b, cg, d >> 1, h >> 1, w >> 1);
     T* dst = y + gy.at(b, cg, d, h, w);
     *reinterpret_cast<int4*>(dst) = __ldg(reinterpret_cast<const int4*>(src));
@@ -144,9 +157,10 @@ __global__ void k_upsample_bwd(const T* __restrict__ gy, Slab sgy, const T* __re
   const int64_t total = nvox * sgx.CG;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int cg = (int)(i / nvox);
+    uint32_t v32;
+    int cg = split_cg(i, nvox, v32);
     int b, d, h, w;
-    decompose(i % nvox, sgx.D, sgx.H, sgx.W, b, d, h, w);
+    decompose(v32, sgx.D, sgx.H, sgx.W, b, d, h, w);
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int cell = 0; cell < 8; ++cell) {
@@ -172,9 +186,10 @@ __global__ void k_relu_mask(const T* __restrict__ g, Slab sg, const T* __restric
   const int64_t total = nvox * sg.CG;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int cg = (int)(i / nvox);
+    uint32_t v32;
+    int cg = split_cg(i, nvox, v32);
     int b, d, h, w;
-    decompose(i % nvox, sg.D, sg.H, sg.W, b, d, h, w);
+    decompose(v32, sg.D, sg.H, sg.W, b, d, h, w);
     float v[8], mv[8];
     V8<T>::ld(g + sg.at(b, cg, d, h, w), v);
     V8<T>::ld(mask + sm.at(b, cg, d, h, w), mv);
@@ -248,7 +263,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_head_fwd(const T* __restrict__
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvox;
        v += (int64_t)gridDim.x * blockDim.x) {
     int b, d, h, w;
-    decompose(v, sy.D, sy.H, sy.W, b, d, h, w);
+    decompose((uint32_t)v, sy.D, sy.H, sy.W, b, d, h, w);
     float lg[kMaxCls], p[kMaxCls];
     head_logits(y, sy, b, d, h, w, sW, sb, C, ncls, lg);
     softmax_n(lg, ncls, p);
@@ -306,7 +321,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_head_bwd(
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvox;
          v += (int64_t)gridDim.x * blockDim.x) {
       int b, d, h, w;
-      decompose(v, sy.D, sy.H, sy.W, b, d, h, w);
+      decompose((uint32_t)v, sy.D, sy.H, sy.W, b, d, h, w);
       float lg[kMaxCls], p[kMaxCls], gp[kMaxCls], gl[kMaxCls];
       head_logits(y, sy, b, d, h, w, sW, sb, C, ncls, lg);
       softmax_n(lg, ncls, p);
@@ -369,7 +384,7 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_fwd_fixed(
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvox;
        v += (int64_t)gridDim.x * blockDim.x) {
     int b, d, h, w;
-    decompose(v, sy.D, sy.H, sy.W, b, d, h, w);
+    decompose((uint32_t)v, sy.D, sy.H, sy.W, b, d, h, w);
     float lg[NC];
 #pragma unroll
     for (int k = 0; k < NC; ++k) lg[k] = sb[k];
@@ -439,7 +454,7 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_fixed(
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvox;
        v += (int64_t)gridDim.x * blockDim.x) {
     int b, d, h, w;
-    decompose(v, sy.D, sy.H, sy.W, b, d, h, w);
+    decompose((uint32_t)v, sy.D, sy.H, sy.W, b, d, h, w);
     float yv[C];
     const T* base = y + sy.at(b, 0, d, h, w);
 #pragma unroll
@@ -572,6 +587,7 @@ extern "C" int vm_maxpool2_fwd(int dtype, const void* x, int64_t x_bstride, void
              "maxpool2 needs even local extents, got (%d, %d, %d)", D, H, W);
   Slab gx = SLAB(x_bstride, C, D, H, W), gy = SLAB(y_bstride, C, D / 2, H / 2, W / 2);
   int64_t work = (int64_t)B * (D / 2) * (H / 2) * (W / 2) * gy.CG;
+  VM_REQUIRE(work < (1LL << 32), VM_E_SHAPE, "index space %lld exceeds 2^32", (long long)work);
   DISPATCH_T(dtype, "vm_maxpool2_fwd",
              k_maxpool_fwd<T><<<grid_for(work, 256), 256, 0, as_stream(stream)>>>(
                  (const T*)x, gx, (T*)y, gy, B));
@@ -587,6 +603,7 @@ extern "C" int vm_maxpool2_bwd(int dtype, const void* x, int64_t x_bstride, cons
   Slab gx = SLAB(x_bstride, C, D, H, W), go = SLAB(gout_bstride, C, D / 2, H / 2, W / 2);
   Slab ga = SLAB(add_bstride, C, D, H, W), gi = SLAB(gin_bstride, C, D, H, W);
   int64_t work = (int64_t)B * (D / 2) * (H / 2) * (W / 2) * go.CG;
+  VM_REQUIRE(work < (1LL << 32), VM_E_SHAPE, "index space %lld exceeds 2^32", (long long)work);
   DISPATCH_T(dtype, "vm_maxpool2_bwd",
              k_maxpool_bwd<T><<<grid_for(work, 256), 256, 0, as_stream(stream)>>>(
                  (const T*)x, gx, (const T*)gout, go, (const T*)add, ga, (T*)gin, gi, B, relu_mask));
@@ -598,6 +615,7 @@ extern "C" int vm_upsample2_fwd(int dtype, const void* x, int64_t x_bstride, voi
   VM_REQUIRE(x && y, VM_E_ARG, "vm_upsample2_fwd: null pointer");
   Slab gx = SLAB(x_bstride, C, D, H, W), gy = SLAB(y_bstride, C, 2 * D, 2 * H, 2 * W);
   int64_t work = (int64_t)B * D * H * W * gx.CG * 8;  // output vectors
+  VM_REQUIRE(work < (1LL << 32), VM_E_SHAPE, "index space %lld exceeds 2^32", (long long)work);
   DISPATCH_T(dtype, "vm_upsample2_fwd",
              k_upsample_fwd<T><<<grid_for(work, 256), 256, 0, as_stream(stream)>>>(
                  (const T*)x, gx, (T*)y, gy, B));
@@ -611,6 +629,7 @@ extern "C" int vm_upsample2_bwd(int dtype, const void* gy, int64_t gy_bstride, c
   Slab sgy = SLAB(gy_bstride, C, 2 * D, 2 * H, 2 * W), sgx = SLAB(gx_bstride, C, D, H, W);
   Slab sm = SLAB(mask_bstride, C, D, H, W);
   int64_t work = (int64_t)B * D * H * W * sgx.CG;
+  VM_REQUIRE(work < (1LL << 32), VM_E_SHAPE, "index space %lld exceeds 2^32", (long long)work);
   DISPATCH_T(dtype, "vm_upsample2_bwd",
              k_upsample_bwd<T><<<grid_for(work, 256), 256, 0, as_stream(stream)>>>(
                  (const T*)gy, sgy, (const T*)mask, sm, (T*)gx, sgx, B));
@@ -624,6 +643,7 @@ extern "C" int vm_relu_mask(int dtype, const void* g, int64_t g_bstride, const v
   Slab sg = SLAB(g_bstride, C, D, H, W), sm = SLAB(mask_bstride, C, D, H, W);
   Slab so = SLAB(out_bstride, C, D, H, W);
   int64_t work = (int64_t)B * D * H * W * sg.CG;
+  VM_REQUIRE(work < (1LL << 32), VM_E_SHAPE, "index space %lld exceeds 2^32", (long long)work);
   DISPATCH_T(dtype, "vm_relu_mask",
              k_relu_mask<T><<<grid_for(work, 256), 256, 0, as_stream(stream)>>>(
                  (const T*)g, sg, (const T*)mask, sm, (T*)out, so, B));
@@ -642,6 +662,7 @@ extern "C" int vm_head_fwd(int dtype, const void* y, int64_t y_bstride, const fl
                            int B, int C, int ncls, int D, int H, int W, float clamp, void* stream) {
   VM_REQUIRE(y && w && b && onehot && partials, VM_E_ARG, "vm_head_fwd: null pointer");
   VM_REQUIRE(ncls > 0 && ncls <= kMaxCls, VM_E_UNSUPPORTED, "vm_head_fwd: ncls %d > %d", ncls, kMaxCls);
+  VM_REQUIRE((int64_t)B * D * H * W < (1LL << 32), VM_E_SHAPE, "vm_head_fwd: voxel count exceeds 2^32");
   Slab sy = SLAB(y_bstride, C, D, H, W);
   int grid = vm_head_partials_count(B, D, H, W);
   size_t sh = (C * ncls + ncls + 32) * sizeof(float);
@@ -675,6 +696,7 @@ extern "C" int vm_head_bwd(int dtype, const void* y, int64_t y_bstride, const fl
                            int dice_mask, float clamp, int relu_mask, void* stream) {
   VM_REQUIRE(y && w && b && onehot && stats && g && wpartials, VM_E_ARG, "vm_head_bwd: null pointer");
   VM_REQUIRE(ncls > 0 && ncls <= kMaxCls, VM_E_UNSUPPORTED, "vm_head_bwd: ncls %d", ncls);
+  VM_REQUIRE((int64_t)B * D * H * W < (1LL << 32), VM_E_SHAPE, "vm_head_bwd: voxel count exceeds 2^32");
   Slab sy = SLAB(y_bstride, C, D, H, W), sg = SLAB(g_bstride, C, D, H, W);
   int grid = vm_head_partials_count(B, D, H, W);
   size_t sh = (C * ncls + ncls + 32 + 3 * kMaxCls) * sizeof(float);
