@@ -766,9 +766,12 @@ struct SwParams {
 constexpr int kSwMaxRing = 32;
 constexpr int kSwMaxStages = 8;
 
+// Warps: 0 producer, 1 and 10 MMA issuers (tiles t = 0, 2, .. and 1, 3, ..: a single issuing
+// thread's per-plane bookkeeping otherwise leaves the tensor core idle), 2..9 epilogue.
 template <int MB>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(352, 1)
     k_conv_fwd_sweep(const SwParams p) {
+  constexpr int NW = MB >= 2 ? 2 : 1;  // MMA-issuing warps
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t full[kSwMaxStages], empty[kSwMaxStages], tfull[kSwMaxRing], tempty[kSwMaxRing], wbar;
   __shared__ uint32_t tslot;
@@ -779,10 +782,10 @@ __global__ void __launch_bounds__(320, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], NW);
     }
     for (int r = 0; r < p.ring; ++r) {
-      mbar_init(&tfull[r], 1);
+      mbar_init(&tfull[r], NW);
       mbar_init(&tempty[r], 256);
     }
     mbar_init(&wbar, 1);
@@ -829,8 +832,10 @@ __global__ void __launch_bounds__(320, 1)
       }
       if (p.dbg) p.dbg[blockIdx.x * 8 + 7] = t_pw;
     }
-  } else if (warp == 1) {
-    // ===================== MMA issuer
+  } else if (warp == 1 || warp == 10) {
+    // ===================== MMA issuers
+    const int mw = warp == 1 ? 0 : 1;
+    if (mw < NW) {  // (MB = 1: warp 10 idles)
     const long long t0 = clock64();
     long long t_te = 0, t_fu = 0, t_is = 0;
     mbar_wait(&wbar, 0);
@@ -910,17 +915,25 @@ __global__ void __launch_bounds__(320, 1)
               const uint64_t adesc = a0desc + (uint64_t)((j / 3) * wp1 + (j % 3));
               if (j == 0 && kc == 0) {
 #pragma unroll
-                for (int t = 0; t < MB; ++t)
+                for (int tt = 0; tt < (MB + NW - 1) / NW; ++tt) {
+                  const int t = mw + tt * NW;
+                  if (t >= MB) break;
                   for (int e = 0; e < nf; ++e)
                     mma_bf16_ss(tbase + t * tstride + fd[e], adesc + (uint64_t)(t * 128), bdesc + fb[e], fid[e],
                                 facc[e]);
+                }
               } else if (nn == 1) {
 #pragma unroll
-                for (int t = 0; t < MB; ++t)
+                for (int tt = 0; tt < (MB + NW - 1) / NW; ++tt) {
+                  const int t = mw + tt * NW;
+                  if (t >= MB) break;
                   mma_bf16_ss(tbase + t * tstride + nd[0], adesc + (uint64_t)(t * 128), bdesc, nid[0], 1u);
+                }
               } else {
 #pragma unroll
-                for (int t = 0; t < MB; ++t) {
+                for (int tt = 0; tt < (MB + NW - 1) / NW; ++tt) {
+                  const int t = mw + tt * NW;
+                  if (t >= MB) break;
                   mma_bf16_ss(tbase + t * tstride + nd[0], adesc + (uint64_t)(t * 128), bdesc + nb[0], nid[0], 1u);
                   mma_bf16_ss(tbase + t * tstride + nd[1], adesc + (uint64_t)(t * 128), bdesc + nb[1], nid[1], 1u);
                 }
@@ -947,11 +960,12 @@ __global__ void __launch_bounds__(320, 1)
       }
       nstart += (uint32_t)(nin + 2);
     }
-    if (p.dbg && lane == 0) {
+    if (p.dbg && lane == 0 && mw == 0) {
       p.dbg[blockIdx.x * 8 + 0] = clock64() - t0;
       p.dbg[blockIdx.x * 8 + 1] = t_te;
       p.dbg[blockIdx.x * 8 + 2] = t_fu;
       p.dbg[blockIdx.x * 8 + 3] = t_is;
+    }
     }
   } else {
     // ===================== epilogue (warps 2..9): TMEM lane quarter q, half h
@@ -1465,7 +1479,7 @@ static int launch_sweep(const FwdParams& f, int nsm, void* stream) {
                : p.MB == 2 ? k_conv_fwd_sweep<2>
                            : k_conv_fwd_sweep<1>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<grid, 320, smem, as_stream(stream)>>>(p);
+  kern<<<grid, 352, smem, as_stream(stream)>>>(p);
   return launch_status("vm_conv3d_fwd_tc (sweep)");
 }
 
