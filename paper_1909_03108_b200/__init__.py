@@ -17,6 +17,20 @@ from .mesh import DeviceMesh, WorkerContext, create_mesh
 from .sharding import Layout, ShardedTensor, TensorSpec, gather, shard
 from .halo import HaloSpec, PaddedBlock, exchange_byte_count, halo_exchange, halo_exchange_backward
 from .unet import LayerGraph, UNetConfig, build, init_params, recipe_for_resolution
+from .training import (
+    BatchSource,
+    LossWeights,
+    TrainConfig,
+    TrainState,
+    dice_global,
+    dice_per_case,
+    evaluate,
+    hard_dice,
+    install_params,
+    load_checkpoint,
+    save_checkpoint,
+    train_loop,
+)
 
 __version__ = "0.1.0"
 
@@ -44,4 +58,16 @@ __all__ = [
     "init_params",
     "recipe_for_resolution",
     "shard",
+    "BatchSource",
+    "LossWeights",
+    "TrainConfig",
+    "TrainState",
+    "dice_global",
+    "dice_per_case",
+    "evaluate",
+    "hard_dice",
+    "install_params",
+    "load_checkpoint",
+    "save_checkpoint",
+    "train_loop",
 ]

@@ -704,6 +704,35 @@ class UNetStep:
             }
         return out
 
+    def skipped_layers(self):
+        """Conv ids whose gradients were non-finite in the last SGD step (training.py:202-219)."""
+        flags = self.skip_flags.cpu().numpy()
+        return [L.node.id for L, f in zip(self.layers, flags) if f]
+
+    def moment_dict(self):
+        """SGD momentum buffers in the reference layout {id: {"kernel", "bias"}}."""
+        host = self.moments.cpu().numpy()
+        return {
+            L.node.id: {"kernel": host[a : a + L.nk].reshape(L.k, L.k, L.k, L.cin, L.cout).copy(),
+                        "bias": host[a + L.nk : a + L.nk + L.cout].copy()}
+            for L, a in zip(self.layers, self.offsets_host)
+        }
+
+    def load_state(self, params=None, moments=None):
+        """Install reference-layout parameters and/or momentum buffers (checkpoint resume,
+        ``training.install_params``); the conv operands are repacked."""
+        for store, buf in ((params, self.params), (moments, self.moments)):
+            if store is None:
+                continue
+            host = buf.cpu().numpy()
+            for L, a in zip(self.layers, self.offsets_host):
+                blob = store[L.node.id]
+                host[a : a + L.nk] = np.asarray(blob["kernel"], dtype=np.float32).reshape(-1)
+                host[a + L.nk : a + L.nk + L.cout] = np.asarray(blob["bias"], dtype=np.float32)
+            buf.copy_(torch.from_numpy(host))
+        if params is not None:
+            self.repack()
+
     def grad_dict(self):
         host = self.grads.cpu().numpy()
         return {

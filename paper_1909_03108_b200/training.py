@@ -1,0 +1,362 @@
+"""Training loop, checkpoints and evaluation around the GPU train step (SURVEY §8(f) rows 1
+and 3: the caller of the hot path and the step after it).
+
+Mirrors ``voxmesh.training`` (training.py) for a user switching over:
+
+* ``TrainConfig`` / ``TrainState`` / ``LossWeights`` (training.py:43-50, :364-387);
+* ``save_checkpoint`` / ``load_checkpoint`` write and read the reference's on-disk format,
+  one directory per checkpoint with ``{param,moment}__{node}__{kernel,bias}.npy`` blobs and
+  a ``manifest.json`` (training.py:414-439), so either implementation resumes from the
+  other's checkpoints;
+* ``BatchSource`` draws the same batches from (seed, step): per-epoch permutations seeded
+  ``SeedSequence([seed, 7919, epoch])`` (training.py:241-279), which is what makes resume
+  bitwise;
+* ``train_loop`` (training.py:442-533) runs ``UNetStep`` on every rank of the graph's mesh
+  (threads: one worker thread + CUDA stream per rank; spmd: this process's rank), streams
+  ``metrics.csv`` and ``run.json`` in the reference's formats and checkpoints every
+  ``checkpoint_every`` steps;
+* ``evaluate`` (training.py:543-602) runs the forward pass on the GPU and reports hard
+  tumour Dice per case and pooled (``hard_dice`` / ``dice_per_case`` / ``dice_global``,
+  training.py:166-194) plus the mean loss.
+
+The arithmetic is the GPU step's (bf16 storage, fp32 accumulation; ``compute_dtype="f32"``
+selects the fp32 CUDA-core kernels).  Augmentation (``augment.py``) is out of scope (§8(f)
+row 4) and rejected explicitly.
+"""
+
+from __future__ import annotations
+
+import json
+import time
+import warnings
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+
+from .errors import VoxmeshError
+
+DICE_EPS = 1e-6
+
+
+@dataclass(frozen=True)
+class LossWeights:
+    dice: float = 0.9
+    ce: float = 0.1
+
+    def __post_init__(self):
+        if self.dice < 0 or self.ce < 0:
+            raise VoxmeshError(f"loss weights must be non-negative: {self}")
+
+
+@dataclass
+class TrainConfig:
+    """Same fields and defaults as the reference (training.py:364-379), plus
+    ``compute_dtype`` ("bf16": tensor-core path, "f32": CUDA-core fp32 path)."""
+
+    steps: int = 200
+    batch_size: int = 1
+    lr: float = 0.003
+    momentum: float = 0.9
+    seed: int = 0
+    dice_classes: tuple = (1, 2)
+    loss_weights: LossWeights = field(default_factory=LossWeights)
+    prob_clamp: float = 1e-12
+    dtype: str = "f32"
+    augment: object = None
+    checkpoint_every: int = 0
+    log_every: int = 1
+    out_dir: str = None
+    phase_barrier: bool = True
+    compute_dtype: str = "bf16"
+
+
+@dataclass
+class TrainState:
+    step: int
+    params: dict
+    moments: dict
+    history: list = field(default_factory=list)
+
+
+# ---------------------------------------------------------------------------- metrics
+def hard_dice(pred_mask, gt_mask):
+    """2|A∩B| / (|A|+|B|); 1 when both are empty, 0 when only one is (training.py:166-175)."""
+    a, b = int(np.count_nonzero(pred_mask)), int(np.count_nonzero(gt_mask))
+    if a + b == 0:
+        return 1.0
+    if a == 0 or b == 0:
+        return 0.0
+    return 2.0 * int(np.count_nonzero(np.logical_and(pred_mask, gt_mask))) / (a + b)
+
+
+def _check_pairs(preds, gts):
+    if len(preds) != len(gts):
+        raise VoxmeshError(f"{len(preds)} predictions vs {len(gts)} ground truths")
+
+
+def dice_per_case(preds, gts, cls=2):
+    """Mean over cases of the hard Dice of class ``cls`` (training.py:178-183)."""
+    _check_pairs(preds, gts)
+    return float(np.mean([hard_dice(p == cls, g == cls) for p, g in zip(preds, gts)]))
+
+
+def dice_global(preds, gts, cls=2):
+    """Hard Dice of class ``cls`` with all cases pooled (training.py:186-194)."""
+    _check_pairs(preds, gts)
+    inter = tot = 0
+    for p, g in zip(preds, gts):
+        pm, gm = p == cls, g == cls
+        inter += int(np.count_nonzero(pm & gm))
+        tot += int(np.count_nonzero(pm)) + int(np.count_nonzero(gm))
+    return 1.0 if tot == 0 else 2.0 * inter / tot
+
+
+# ---------------------------------------------------------------------------- checkpoints
+def save_checkpoint(path, step, params, moments, extra=None):
+    """Reference checkpoint layout (training.py:414-428)."""
+    path = Path(path)
+    path.mkdir(parents=True, exist_ok=True)
+    names = []
+    for kind, store in (("param", params), ("moment", moments)):
+        for nid, blobs in store.items():
+            for key, arr in blobs.items():
+                name = f"{kind}__{nid}__{key}.npy"
+                np.save(path / name, np.asarray(arr))
+                names.append(name)
+    manifest = {"step": int(step), "blobs": names}
+    manifest.update(extra or {})
+    (path / "manifest.json").write_text(json.dumps(manifest, indent=2, default=str))
+
+
+def load_checkpoint(path):
+    """(step, params, moments) from a reference-format checkpoint (training.py:431-439)."""
+    path = Path(path)
+    manifest = json.loads((path / "manifest.json").read_text())
+    stores = {"param": {}, "moment": {}}
+    for name in manifest["blobs"]:
+        kind, nid, key = name[: -len(".npy")].split("__")
+        if kind not in stores:
+            raise VoxmeshError(f"checkpoint {path}: unknown blob kind in {name!r}")
+        stores[kind].setdefault(nid, {})[key] = np.load(path / name)
+    return manifest["step"], stores["param"], stores["moment"]
+
+
+# ---------------------------------------------------------------------------- batches
+def _image_labels(rec):
+    if hasattr(rec, "image"):
+        return rec.image, rec.labels
+    return rec[0], rec[1]
+
+
+class BatchSource:
+    """Deterministic batches from (seed, step) (training.py:241-279): epoch e visits the
+    records in ``default_rng(SeedSequence([seed, 7919, e])).permutation(n)`` order.
+    Returns the host image ``[B, E, E, E, 1]`` (f32) and labels ``[B, E, E, E]`` (u8); the
+    one-hot expansion happens on the GPU."""
+
+    def __init__(self, records, batch_size, seed):
+        if not records:
+            raise VoxmeshError("empty training set")
+        self.records = list(records)
+        self.batch_size = int(batch_size)
+        self.seed = int(seed)
+        self._perms = {}
+
+    def perm(self, epoch):
+        if epoch not in self._perms:
+            rng = np.random.default_rng(np.random.SeedSequence([self.seed, 7919, int(epoch)]))
+            self._perms[epoch] = rng.permutation(len(self.records))
+        return self._perms[epoch]
+
+    def record_index(self, global_idx):
+        n = len(self.records)
+        return int(self.perm(global_idx // n)[global_idx % n])
+
+    def batch(self, step):
+        idx = [self.record_index(step * self.batch_size + j) for j in range(self.batch_size)]
+        pairs = [_image_labels(self.records[i]) for i in idx]
+        img = np.stack([np.asarray(p[0], dtype=np.float32) for p in pairs])[..., None]
+        lab = np.stack([np.asarray(p[1], dtype=np.uint8) for p in pairs])
+        return img, lab
+
+
+# ---------------------------------------------------------------------------- placement
+def _blocks(graph, arr, spatial_from=1):
+    """Per-rank local blocks of a host array whose spatial dims start at ``spatial_from``
+    (the layout's x/y/z → mesh axes, sharding.py:123-143); batch sharding is not used by
+    the slab step, so every rank sees the whole batch of its spatial block."""
+    mesh, layout = graph.mesh, graph.layout
+    out = []
+    for coord in mesh.coords:
+        sl = [slice(None)] * arr.ndim
+        for i, d in enumerate(("x", "y", "z")):
+            ax = layout.axis_for(d) if layout is not None else None
+            if ax is None:
+                continue
+            n = arr.shape[spatial_from + i] // mesh.axis_size(ax)
+            c = coord[mesh.axis_index[ax]]
+            sl[spatial_from + i] = slice(c * n, (c + 1) * n)
+        out.append(np.ascontiguousarray(arr[tuple(sl)]))
+    return out
+
+
+def _make_steps(graph, params, cfg, batch):
+    import torch
+
+    from .step import UNetStep
+
+    if graph.layout is not None and graph.layout.axis_for("batch") is not None:
+        raise VoxmeshError("train_loop: batch-sharded layouts are not supported by the slab step")
+    dtype = torch.bfloat16 if cfg.compute_dtype == "bf16" else torch.float32
+    E = graph.config.input_extent
+    multi = graph.mesh.worker_count > 1
+
+    def make(ctx):
+        st = UNetStep(graph, params, batch=batch, ctx=ctx if multi else None, device=ctx.device, dtype=dtype,
+                      lr=cfg.lr, momentum=cfg.momentum,
+                      loss_weights=(cfg.loss_weights.dice, cfg.loss_weights.ce),
+                      dice_classes=tuple(cfg.dice_classes), clamp=cfg.prob_clamp, global_shape=(E, E, E))
+        ctx.store["vm_step"] = st
+        return None
+
+    graph.mesh.run(make)
+
+
+def _pinned(a):
+    import torch
+
+    return torch.from_numpy(a).pin_memory()
+
+
+def _host_step(ctx, img, lab):
+    st = ctx.store["vm_step"]
+    st.train_step_host(img, lab)
+    return st.loss(), st.skipped_layers()
+
+
+def install_params(graph, params, moments=None):
+    """Put an externally built parameter store on every rank's step (training.py:536-540)."""
+    graph.mesh.run(lambda ctx: ctx.store["vm_step"].load_state(params, moments))
+
+
+def _export_state(graph):
+    return graph.mesh.run(lambda ctx: (ctx.store["vm_step"].param_dict(), ctx.store["vm_step"].moment_dict())
+                          if ctx.rank == 0 else None)[0]
+
+
+def train_loop(graph, dataset, cfg, resume_from=None, run_echo=None):
+    """Train on the graph's mesh; returns the final TrainState (training.py:442-533)."""
+    from . import unet as _unet
+
+    if cfg.augment:
+        raise VoxmeshError("train_loop: augmentation is not part of the GPU path (SURVEY §8(f) row 4)")
+    records = dataset.load_split("train") if hasattr(dataset, "load_split") else list(dataset)
+    mesh = graph.mesh
+    if resume_from is not None:
+        start, params, moments = load_checkpoint(resume_from)
+    else:
+        start = 0
+        params = _unet.init_params(graph, cfg.seed)
+        moments = None
+    _make_steps(graph, params, cfg, cfg.batch_size)
+    if moments is not None:
+        install_params(graph, None, moments)
+
+    out_dir = Path(cfg.out_dir) if cfg.out_dir else None
+    csv_f = None
+    if out_dir:
+        out_dir.mkdir(parents=True, exist_ok=True)
+        echo = {
+            "mesh": mesh.describe(), "layout": graph.layout.as_dict() if graph.layout is not None else {},
+            "seed": cfg.seed, "steps": cfg.steps, "batch_size": cfg.batch_size, "lr": cfg.lr,
+            "momentum": cfg.momentum, "dtype": cfg.dtype, "compute_dtype": cfg.compute_dtype,
+            "dice_classes": list(cfg.dice_classes), "loss_weights": [cfg.loss_weights.dice, cfg.loss_weights.ce],
+            "augment": False, "config_kv": graph.config.to_kv(),
+            "resume_from": str(resume_from) if resume_from else None,
+        }
+        echo.update(run_echo or {})
+        (out_dir / "run.json").write_text(json.dumps(echo, indent=2, default=str))
+        fresh = resume_from is None or not (out_dir / "metrics.csv").exists()
+        csv_f = open(out_dir / "metrics.csv", "w" if fresh else "a")
+        if fresh:
+            csv_f.write("step,loss,dice_loss,ce_loss,lr,wall_ms\n")
+
+    source = BatchSource(records, cfg.batch_size, cfg.seed)
+    state = TrainState(start, params, moments or {})
+    try:
+        for step in range(start, start + cfg.steps):
+            img, lab = source.batch(step)
+            t0 = time.perf_counter()
+            bi = [_pinned(b) for b in _blocks(graph, img)]
+            bl = [_pinned(b) for b in _blocks(graph, lab)]
+            res = mesh.run(_host_step, per_worker=(bi, bl))
+            (loss, dice, ce), skipped = res[0]
+            wall_ms = (time.perf_counter() - t0) * 1e3
+            if skipped:
+                warnings.warn(f"step {step}: non-finite gradients, skipped layers {skipped}")
+            state.step = step + 1
+            state.history.append((step, loss, dice, ce, wall_ms))
+            if csv_f:
+                csv_f.write(f"{step},{loss:.8f},{dice:.8f},{ce:.8f},{cfg.lr},{wall_ms:.2f}\n")
+            if cfg.log_every and step % cfg.log_every == 0:
+                print(f"step {step:5d}  loss {loss:.6f}  dice {dice:.6f}  ce {ce:.6f}  ({wall_ms:.0f} ms)")
+            if cfg.checkpoint_every and out_dir and (step + 1) % cfg.checkpoint_every == 0:
+                p, m = _export_state(graph)
+                save_checkpoint(out_dir / "checkpoints" / f"step_{step + 1:06d}", step + 1, p, m,
+                                extra={"config_kv": graph.config.to_kv(), "seed": cfg.seed})
+    finally:
+        if csv_f:
+            csv_f.close()
+    state.params, state.moments = _export_state(graph)
+    if out_dir:
+        save_checkpoint(out_dir / "checkpoints" / f"step_{state.step:06d}", state.step, state.params,
+                        state.moments, extra={"config_kv": graph.config.to_kv(), "seed": cfg.seed})
+    return state
+
+
+def evaluate(graph, dataset, cfg, params=None):
+    """Forward-only pass over records on the GPU; hard Dice per case / pooled and the mean
+    per-sample loss (training.py:543-602).  ``params`` defaults to the weights installed by
+    the last ``train_loop``/``install_params`` on this graph."""
+    import torch
+
+    records = dataset.load_split("val") if hasattr(dataset, "load_split") else list(dataset)
+    if not records:
+        raise VoxmeshError("empty evaluation set")
+    mesh = graph.mesh
+    have = mesh.run(lambda ctx: "vm_step" in ctx.store)[0]
+    if not have or params is not None:
+        if params is None:
+            raise VoxmeshError("evaluate: no parameters installed on this graph")
+        _make_steps(graph, params, cfg, 1)
+    preds, gts, losses = [], [], []
+    for rec in records:
+        img, lab = _image_labels(rec)
+        img = np.asarray(img, dtype=np.float32)[None, ..., None]
+        lab = np.asarray(lab, dtype=np.uint8)[None]
+        bi = [_pinned(b) for b in _blocks(graph, img)]
+        bl = [_pinned(b) for b in _blocks(graph, lab)]
+
+        def fwd(ctx, i, l):
+            st = ctx.store["vm_step"]
+            st.keep_probs = True
+            st.upload(i, l)
+            st.forward()
+            p = st.probs.reshape(i.shape[1], i.shape[2], i.shape[3], -1)
+            pred = torch.argmax(p, dim=-1).to(torch.uint8).cpu().numpy()
+            return pred, st.loss()[0]
+
+        res = mesh.run(fwd, per_worker=(bi, bl))
+        full = np.zeros(lab.shape[1:], dtype=np.uint8)
+        for (pred, _), blk in zip(res, _blocks(graph, np.arange(full.size).reshape(full.shape)[None])):
+            full.reshape(-1)[blk[0].reshape(-1)] = pred.reshape(-1)
+        preds.append(full)
+        gts.append(lab[0])
+        losses.append(res[0][1])
+    return {
+        "dice_per_case": dice_per_case(preds, gts),
+        "dice_global": dice_global(preds, gts),
+        "mean_loss": float(sum(losses) / len(losses)),
+        "n_cases": len(preds),
+    }
