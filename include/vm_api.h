@@ -184,6 +184,39 @@ int vm_sgd_momentum(float* params, float* moments, const float* grads, const int
                     int nlayers, int64_t max_layer_elems, int* flags, float lr, float momentum,
                     void* stream);
 
+/* ------------------------------------------------------------------ SURVEY §8(b) names
+ * Thin wrappers (csrc/abi.cu) carrying the entry-point names of the SURVEY's ABI sketch.
+ * Transport (vm_init / vm_comm_split / vm_allreduce_f32, the NCCL half of vm_halo_fwd/bwd)
+ * is torch.distributed on the Python side (mesh.py); the halo's device half is
+ * vm_box_pack / vm_box_unpack / vm_box_unpack_add above. */
+/* conv3d_local (ops.py:69-97) */
+int vm_conv3d_fwd(const void* x, int64_t x_bstride, const void* wpacked, const float* bias, void* y,
+                  int64_t y_bstride, int B, int Cin, int Cout, int D, int H, int W, unsigned flags,
+                  void* stream);
+/* conv3d_input_grad_local (ops.py:100-114) [* relu mask]; Cin/Cout of the forward conv */
+int vm_conv3d_dgrad(const void* gy, int64_t gy_bstride, const void* wpacked_t, const void* mask,
+                    int64_t mask_bstride, void* gx, int64_t gx_bstride, int B, int Cin, int Cout,
+                    int D, int H, int W, void* stream);
+/* conv3d_param_grads_local (ops.py:117-138) */
+size_t vm_conv3d_wgrad_ws(int B, int Cin, int Cout, int D, int H, int W);
+int vm_conv3d_wgrad(const void* x, int64_t x_bstride, const void* gy, int64_t gy_bstride, float* gw,
+                    float* gb, void* ws, int B, int Cin, int Cout, int D, int H, int W, void* stream);
+/* relu_backward_local (ops.py:186-187) */
+int vm_relu_bwd(int dtype, const void* g, int64_t g_bstride, const void* mask, int64_t mask_bstride,
+                void* out, int64_t out_bstride, int B, int C, int D, int H, int W, void* stream);
+/* upsample2_local (ops.py:171-173) into the concat slab's up half (unet.py:215) */
+int vm_upsample2_concat_fwd(int dtype, const void* x, int64_t x_bstride, void* y_concat,
+                            int64_t y_bstride, int B, int C, int D, int H, int W, void* stream);
+/* head + softmax + loss statistics; loss gradient + head backward (== vm_head_fwd / _bwd) */
+int vm_head_softmax_stats(int dtype, const void* y, int64_t y_bstride, const float* w,
+                          const float* b, const float* onehot, float* probs, float* partials, int B,
+                          int C, int ncls, int D, int H, int W, float clamp, void* stream);
+int vm_loss_grad_head_bwd(int dtype, const void* y, int64_t y_bstride, const float* w,
+                          const float* b, const float* onehot, const float* stats, void* g,
+                          int64_t g_bstride, float* wpartials, int B, int C, int ncls, int D, int H,
+                          int W, float w_dice, float w_ce, float total_voxels, int dice_mask,
+                          float clamp, int relu_mask, void* stream);
+
 #ifdef __cplusplus
 }
 #endif
