@@ -195,6 +195,10 @@ struct FwdParams {
   uint32_t wp_magic, hp_magic;  // floor(2^32 / d) + 1 for the anchor (w, h) split
 };
 
+// MB (tiles per unit) is a template parameter so that the MMA issue loop is straight-line
+// code: measured on B200, a runtime-bounded issue loop costs 1.5x in MMA throughput for
+// N = 128 (tools/probes/probe_pipe.cu).
+template <int MB>
 __global__ void __launch_bounds__(320, 1)
     k_conv_fwd_tc(const FwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -283,16 +287,16 @@ __global__ void __launch_bounds__(320, 1)
           const uint32_t d0 = tbase + (uint32_t)((ab * p.MB * p.nacc + aset) * p.Nc);
           const uint32_t tstep = (uint32_t)(p.nacc * p.Nc);
           const uint32_t bstep = (uint32_t)(2 * p.Nc * 16) >> 4;
-#pragma unroll 1
+          const uint32_t acc0 = s >= p.nacc ? 1u : 0u;
+          const uint32_t wp1 = (uint32_t)p.Wp;
+#pragma unroll
           for (int j = 0; j < 9; ++j) {
             const uint64_t bdesc = b0desc + (uint64_t)(j * bstep);
-            const uint64_t adesc = a0desc + (uint64_t)((j / 3) * p.Wp + (j % 3));
-            const uint32_t acc = (s >= p.nacc || j > 0) ? 1u : 0u;
+            const uint64_t adesc = a0desc + (uint64_t)((j / 3) * wp1 + (j % 3));
+            const uint32_t acc = j > 0 ? 1u : acc0;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              if (i < p.MB)
-                mma_bf16_ss(d0 + (uint32_t)i * tstep, adesc + (uint64_t)(i * 128), bdesc, p.idesc, acc);
-            }
+            for (int i = 0; i < MB; ++i)
+              mma_bf16_ss(d0 + (uint32_t)i * tstep, adesc + (uint64_t)(i * 128), bdesc, p.idesc, acc);
           }
           mma_commit(&empty[stage]);
         }
@@ -1585,8 +1589,19 @@ extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wp
   (void)rows;
   const size_t smem = (size_t)p.stages * p.stage_bytes;
   int grid = p.units < nsm ? p.units : nsm;
-  cudaFuncSetAttribute(k_conv_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_conv_fwd_tc<<<grid, 320, smem, as_stream(stream)>>>(p);
+  void (*kern)(const FwdParams) = nullptr;
+  switch (p.MB) {
+    case 1: kern = k_conv_fwd_tc<1>; break;
+    case 2: kern = k_conv_fwd_tc<2>; break;
+    case 3: kern = k_conv_fwd_tc<3>; break;
+    case 4: kern = k_conv_fwd_tc<4>; break;
+    case 5: kern = k_conv_fwd_tc<5>; break;
+    case 6: kern = k_conv_fwd_tc<6>; break;
+    case 7: kern = k_conv_fwd_tc<7>; break;
+    default: kern = k_conv_fwd_tc<8>; break;
+  }
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<grid, 320, smem, as_stream(stream)>>>(p);
   return launch_status("vm_conv3d_fwd_tc");
 }
 

@@ -16,7 +16,7 @@ __device__ __forceinline__ void bulk(void* dst, const void* src, uint32_t bytes,
 
 template <int N, int MB>
 __global__ void __launch_bounds__(320, 1) k_pipe(const uint8_t* gA, const uint8_t* gW, int nst, int shared_w,
-                                                 int nstages, long long* out, int spin, int Wp, int nacc) {
+                                                 int nstages, long long* out, int spin, int Wp, int nacc, int notma) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t full[8], empty[8], fin;
   __shared__ uint32_t tslot;
@@ -42,6 +42,11 @@ __global__ void __launch_bounds__(320, 1) k_pipe(const uint8_t* gA, const uint8_
       for (int s = 0; s < nst; ++s) {
         vm::mbar_wait(&empty[stage], ph ^ 1);
         uint8_t* sA = smem + stage * stage_bytes;
+        if (notma) {
+          vm::mbar_arrive(&full[stage]);
+          if (++stage == nstages) { stage = 0; ph ^= 1; }
+          continue;
+        }
         vm::mbar_arrive_expect_tx(&full[stage], 2 * R * 16 + b_bytes);
         const uint8_t* ga = gA + ((size_t)blockIdx.x * 64 + (s % 64)) * 8192;
         bulk(sA, ga, R * 16, &full[stage]);
@@ -55,13 +60,13 @@ __global__ void __launch_bounds__(320, 1) k_pipe(const uint8_t* gA, const uint8_
     int stage = 0; uint32_t ph = 0;
     constexpr uint32_t id = vm::make_idesc_bf16(128, N, false, false);
     for (int s = 0; s < nst; ++s) {
-      vm::mbar_wait(&full[stage], ph);
-      vm::tc_fence_after();
+      if (!(notma & 4)) vm::mbar_wait(&full[stage], ph);
+      if (!(notma & 2)) vm::tc_fence_after();
       if (vm::elect_one()) {
         const uint32_t sA = vm::smem_u32(smem + stage * stage_bytes);
         const uint64_t a0 = vm::make_sdesc(sA, a_bytes, 128);
         const uint64_t b0 = vm::make_sdesc(sA + 2 * a_bytes, N * 16, 128);
-#pragma unroll 1
+#pragma unroll
         for (int j = 0; j < 9; ++j) {
           const uint64_t bd = b0 + (uint64_t)(j * (2 * N * 16 / 16));
           const uint64_t ad = a0 + (uint64_t)((j / 3) * Wp + (j % 3));
@@ -89,7 +94,7 @@ __global__ void __launch_bounds__(320, 1) k_pipe(const uint8_t* gA, const uint8_
 }
 
 template <int N, int MB>
-void run(int grid, int shared_w, int nstages, int spin = 0, int Wp = 34, int nacc = 1) {
+void run(int grid, int shared_w, int nstages, int spin = 0, int Wp = 34, int nacc = 1, int notma = 0) {
   static uint8_t *gA = nullptr, *gW = nullptr;
   if (!gA) {
     cudaMalloc(&gA, (size_t)148 * 64 * 8192 + 65536);
@@ -103,20 +108,18 @@ void run(int grid, int shared_w, int nstages, int spin = 0, int Wp = 34, int nac
   if (smem > 220 * 1024) { printf("N=%d MB=%d stages=%d: smem too big\n", N, MB, nstages); return; }
   cudaFuncSetAttribute(k_pipe<N, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int nst = 240;
-  k_pipe<N, MB><<<grid, 320, smem>>>(gA, gW, 24, shared_w, nstages, d, spin, Wp, nacc);
-  k_pipe<N, MB><<<grid, 320, smem>>>(gA, gW, nst, shared_w, nstages, d, spin, Wp, nacc);
+  k_pipe<N, MB><<<grid, 320, smem>>>(gA, gW, 24, shared_w, nstages, d, spin, Wp, nacc, notma);
+  k_pipe<N, MB><<<grid, 320, smem>>>(gA, gW, nst, shared_w, nstages, d, spin, Wp, nacc, notma);
   cudaError_t err = cudaDeviceSynchronize();
   std::vector<long long> h(grid); cudaMemcpy(h.data(), d, grid * 8, cudaMemcpyDeviceToHost);
   double avg = 0; for (auto x : h) avg += x; avg /= grid;
-  printf("Wp=%d nacc=%d ", Wp, nacc);
+  printf("notma=%d Wp=%d nacc=%d ", notma, Wp, nacc);
   printf("N=%3d MB=%d grid=%3d stages=%d weights %s: %7.1f cyc/mma (%7.0f cyc/stage) %s\n", N, MB, grid, nstages,
          shared_w ? "shared " : "private", avg / (nst * 9.0 * MB), avg / nst, err ? cudaGetErrorString(err) : "");
   cudaFree(d);
 }
 
 int main() {
-  run<128, 1>(41, 1, 4, 1, 34, 1); run<128, 1>(41, 1, 4, 1, 18, 1); run<128, 1>(41, 1, 4, 1, 18, 3);
-  run<128, 1>(41, 1, 5, 1, 18, 3);
-  run<64, 2>(145, 1, 6, 1, 34, 1); run<64, 2>(145, 1, 6, 1, 34, 3);
+  for (int m : {1, 7}) { run<48, 3>(148, 1, 4, 1, 130, 1, m); run<128, 1>(41, 1, 4, 1, 18, 3, m); run<64, 2>(145, 1, 6, 1, 34, 1, m); }
   return 0;
 }
