@@ -477,6 +477,7 @@ struct WgParams {
   float* ws;        // [kidx = b*ksplit + ks][MT][3][Nc][128]
 };
 
+template <int NMT>  // > 0: M-tiles per CTA known at compile time (straight-line MMA issue); 0: runtime
 __global__ void __launch_bounds__(192, 1)
     k_conv_wgrad_tc(const __grid_constant__ CUtensorMap gmap, const WgParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -609,17 +610,35 @@ __global__ void __launch_bounds__(192, 1)
           const uint64_t b0desc = make_sdesc(sG + (uint32_t)p.gdelta * 16, 128, (uint32_t)p.RR * 16);
           const uint64_t a0desc = make_sdesc(sA + (uint32_t)slot_shift * GS, 128, sbo);
           const uint32_t mstep = 16 * (GS >> 4);  // 16 slots, in 16-byte units
+          const int nkk = p.KS / 16;
+          const uint32_t acc0 = started ? 1u : 0u;
+          if (NMT > 0) {
+#pragma unroll 4
+            for (int kk = 0; kk < nkk; ++kk) {
+              const uint64_t bdesc = b0desc + (uint64_t)(kk * 16);
+              const uint32_t acc = kk > 0 ? 1u : acc0;
+#pragma unroll
+              for (int m = 0; m < (NMT > 0 ? NMT : 1); ++m) {
+                const uint64_t adesc = a0desc + (uint64_t)(m * mstep + kk * 16);
+                const uint32_t d = tbase + (uint32_t)(m * 3 * p.Nc);
+                mma_bf16_ss(d, adesc, bdesc, p.idesc, acc);
+                mma_bf16_ss(d + p.Nc, adesc + 1, bdesc, p.idesc, acc);
+                mma_bf16_ss(d + 2 * p.Nc, adesc + 2, bdesc, p.idesc, acc);
+              }
+            }
+          } else {
 #pragma unroll 1
-          for (int kk = 0; kk < p.KS / 16; ++kk) {
-            const uint64_t bdesc = b0desc + (uint64_t)(kk * 16);
-            const uint32_t acc = (started || kk > 0) ? 1u : 0u;
+            for (int kk = 0; kk < nkk; ++kk) {
+              const uint64_t bdesc = b0desc + (uint64_t)(kk * 16);
+              const uint32_t acc = kk > 0 ? 1u : acc0;
 #pragma unroll 1
-            for (int m = 0; m < nmt; ++m) {
-              const uint64_t adesc = a0desc + (uint64_t)(m * mstep + kk * 16);
-              const uint32_t d = tbase + (uint32_t)(m * 3 * p.Nc);
-              mma_bf16_ss(d, adesc, bdesc, p.idesc, acc);
-              mma_bf16_ss(d + p.Nc, adesc + 1, bdesc, p.idesc, acc);
-              mma_bf16_ss(d + 2 * p.Nc, adesc + 2, bdesc, p.idesc, acc);
+              for (int m = 0; m < nmt; ++m) {
+                const uint64_t adesc = a0desc + (uint64_t)(m * mstep + kk * 16);
+                const uint32_t d = tbase + (uint32_t)(m * 3 * p.Nc);
+                mma_bf16_ss(d, adesc, bdesc, p.idesc, acc);
+                mma_bf16_ss(d + p.Nc, adesc + 1, bdesc, p.idesc, acc);
+                mma_bf16_ss(d + 2 * p.Nc, adesc + 2, bdesc, p.idesc, acc);
+              }
             }
           }
           mma_commit(&empty[stage]);
@@ -1109,6 +1128,7 @@ struct WkParams {
   long long* dbg;  // optional cycle probes [gridDim][8] (vm_debug_set_fwd_probe)
 };
 
+template <int NMT>  // M-tiles of this CTA (compile-time: straight-line MMA issue)
 __global__ void __launch_bounds__(192, 1)
     k_conv_wgrad_kd(const __grid_constant__ CUtensorMap gmap, const WkParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -1208,14 +1228,17 @@ __global__ void __launch_bounds__(192, 1)
           const uint64_t b0desc = make_sdesc(sG, 128, (uint32_t)p.KS * 16);
           const uint64_t a0desc = make_sdesc(sA + (uint32_t)slot_shift * GS, 128, GS);
           const uint32_t mstep = 16 * (GS >> 4);
-#pragma unroll 1
-          for (int kk = 0; kk < p.KS / 16; ++kk) {
+          const int nkk = p.KS / 16;
+          const uint32_t acc0 = started ? 1u : 0u;
+#pragma unroll 4
+          for (int kk = 0; kk < nkk; ++kk) {
             const uint64_t bdesc = b0desc + (uint64_t)(kk * 16);
-            const uint32_t acc = (started || kk > 0) ? 1u : 0u;
-            for (int m = 0; m < nmt; ++m) {
+            const uint32_t acc = kk > 0 ? 1u : acc0;
+#pragma unroll
+            for (int m = 0; m < NMT; ++m) {
               const uint64_t adesc = a0desc + (uint64_t)(m * mstep + kk * 16);
               const uint32_t d = tbase + (uint32_t)(m * 3 * N3);
-              const uint32_t id = m == nmt - 1 ? id_last : p.idesc;
+              const uint32_t id = m == NMT - 1 ? id_last : p.idesc;
               mma_bf16_ss(d, adesc, bdesc, id, acc);
               mma_bf16_ss(d + N3, adesc + 1, bdesc, id, acc);
               mma_bf16_ss(d + 2 * N3, adesc + 2, bdesc, id, acc);
@@ -1790,6 +1813,7 @@ static bool plan_wgrad_kd(int B, int Cin, int Cout, int D, int H, int W, WkParam
   p.ones_slot = 3 * p.CG;
   p.mt_per_unit = 512 / (9 * p.Nc);
   if (p.mt_per_unit > p.MT) p.mt_per_unit = p.MT;
+  while (p.mt_per_unit > 1 && p.MT % p.mt_per_unit) --p.mt_per_unit;  // equal groups (kernel template)
   if (p.mt_per_unit < 1) return false;
   p.g_bytes = (uint32_t)(p.Nc / 8) * p.KS * 16;
   p.g_load = (uint32_t)p.CGo * p.KS * 16;
@@ -1799,7 +1823,7 @@ static bool plan_wgrad_kd(int B, int Cin, int Cout, int D, int H, int W, WkParam
     p.stage_bytes = (p.a_bytes + 3 * p.g_bytes + 1023) & ~1023u;
     p.stages = kSmemBudget / (int)p.stage_bytes;
     if (p.stages >= 2 || p.mt_per_unit == 1) break;
-    --p.mt_per_unit;
+    do --p.mt_per_unit; while (p.mt_per_unit > 1 && p.MT % p.mt_per_unit);
   }
   if (p.stages < 2) return false;
   if (p.stages > kMaxStages) p.stages = kMaxStages;
@@ -1850,8 +1874,9 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
       int rc = make_group_map(&gmap, gy, gbs, pk.CGo, pk.rows, B, pk.KS, pk.CGo);
       if (rc) return rc;
       cudaStream_t st = as_stream(stream);
-      cudaFuncSetAttribute(k_conv_wgrad_kd, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
-      k_conv_wgrad_kd<<<pk.grid, 192, (size_t)pk.stages * pk.stage_bytes, st>>>(gmap, pk);
+      auto kern = pk.mt_per_unit == 3 ? k_conv_wgrad_kd<3> : pk.mt_per_unit == 2 ? k_conv_wgrad_kd<2> : k_conv_wgrad_kd<1>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
+      kern<<<pk.grid, 192, (size_t)pk.stages * pk.stage_bytes, st>>>(gmap, pk);
       rc = launch_status("vm_conv3d_wgrad_tc (kd)");
       if (rc) return rc;
       const int nk = pk.grid / pk.n_mtgroups;
@@ -1875,8 +1900,16 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
                : make_group_map(&gmap, gy, gbs, p.CGo, rows, B, p.RR, p.CGo);
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
-  cudaFuncSetAttribute(k_conv_wgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
-  k_conv_wgrad_tc<<<p.grid, 192, (size_t)p.stages * p.stage_bytes, st>>>(gmap, p);
+  // compile-time M-tile count when every CTA holds the same number of tiles
+  const bool even = p.MT % p.mt_per_unit == 0 && !p.fold;
+  auto kern = !even ? k_conv_wgrad_tc<0>
+            : p.mt_per_unit == 1 ? k_conv_wgrad_tc<1>
+            : p.mt_per_unit == 2 ? k_conv_wgrad_tc<2>
+            : p.mt_per_unit == 3 ? k_conv_wgrad_tc<3>
+            : p.mt_per_unit == 4 ? k_conv_wgrad_tc<4>
+                                 : k_conv_wgrad_tc<0>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
+  kern<<<p.grid, 192, (size_t)p.stages * p.stage_bytes, st>>>(gmap, p);
   rc = launch_status("vm_conv3d_wgrad_tc");
   if (rc) return rc;
   const int nk = p.grid / p.n_mtgroups;
