@@ -932,7 +932,35 @@ __global__ void __launch_bounds__(352, 1)
             const uint64_t a0desc = make_sdesc(sA, ng == 2 ? p.a_bytes : 0, 128);
             const uint64_t b0desc = make_sdesc(sWa + (uint32_t)kc * 9 * wblk, (uint32_t)(3 * p.Nc * 16), 128);
             const uint32_t wp1 = (uint32_t)p.Wp, wstep = wblk >> 4;
+            if (pos + 3 <= ring) {
+              // common case, straight-line: blocks pos..pos+2 contiguous
+              const uint32_t dpos = tbase + pos * Nc;
+              const uint32_t id1 = p.idesc1, id2 = p.idesc2, id3 = p.idesc3;
 #pragma unroll
+              for (int j = 0; j < 9; ++j) {
+                const uint64_t bdesc = b0desc + (uint64_t)(j * wstep);
+                const uint64_t adesc = a0desc + (uint64_t)((j / 3) * wp1 + (j % 3));
+                if (j == 0 && kc == 0) {  // block pos+2 (output plane i) starts here
+#pragma unroll
+                  for (int tt = 0; tt < (MB + NW - 1) / NW; ++tt) {
+                    const int t = mw + tt * NW;
+                    if (t >= MB) break;
+                    const uint32_t dt = dpos + t * tstride;
+                    const uint64_t at = adesc + (uint64_t)(t * 128);
+                    mma_bf16_ss(dt, at, bdesc, id2, 1u);
+                    mma_bf16_ss(dt + 2 * Nc, at, bdesc + (uint64_t)(2 * Nc), id1, 0u);
+                  }
+                } else {
+#pragma unroll
+                  for (int tt = 0; tt < (MB + NW - 1) / NW; ++tt) {
+                    const int t = mw + tt * NW;
+                    if (t >= MB) break;
+                    mma_bf16_ss(dpos + t * tstride, adesc + (uint64_t)(t * 128), bdesc, id3, 1u);
+                  }
+                }
+              }
+            } else {
+#pragma unroll 1
             for (int j = 0; j < 9; ++j) {
               const uint64_t bdesc = b0desc + (uint64_t)(j * wstep);
               const uint64_t adesc = a0desc + (uint64_t)((j / 3) * wp1 + (j % 3));
@@ -962,6 +990,7 @@ __global__ void __launch_bounds__(352, 1)
                 }
               }
             }
+            }  // ring-end planes
             mma_commit(&empty[stage]);
           }
           __syncwarp();
