@@ -102,6 +102,7 @@ struct PackGeom {
 
 constexpr int kSweepMaxNc = 32;  // Nc = 48 (N = 144) measured slower than k_conv_fwd_tc
 constexpr uint32_t kSweepMaxWeightBytes = 100 * 1024;
+constexpr bool kSweepEnabled = true;
 
 __host__ __device__ static PackGeom pack_geom(int cin, int cout) {
   PackGeom g;
@@ -113,7 +114,7 @@ __host__ __device__ static PackGeom pack_geom(int cin, int cout) {
   g.nchunk = (npad + 255) / 256;
   g.Nc = ((npad + g.nchunk - 1) / g.nchunk + 15) / 16 * 16;
   const uint32_t wbytes = (uint32_t)g.KC * 9 * 2 * 3 * g.Nc * 16;
-  g.sweep = (g.nchunk == 1 && g.Nc <= kSweepMaxNc && wbytes <= kSweepMaxWeightBytes) ? 1 : 0;
+  g.sweep = (kSweepEnabled && g.nchunk == 1 && g.Nc <= kSweepMaxNc && wbytes <= kSweepMaxWeightBytes) ? 1 : 0;
   return g;
 }
 
@@ -866,6 +867,8 @@ __global__ void __launch_bounds__(352, 1)
     uint32_t phase = 0;
     uint32_t nstart = 0;    // ring sequence of the unit's first block (plane o0 - 2)
     uint32_t acquired = 0;  // ring sequences whose block has been re-armed and taken
+    uint32_t acq_slot = 0, acq_phase = 0;  // acquired % ring, (acquired / ring) & 1
+    uint32_t pos = 0;                      // n % ring (incremental: no divisions per plane)
     const uint32_t wblk = (uint32_t)(2 * 3 * p.Nc * 16);  // bytes per (kc, tap) weight block
     const uint32_t sWa = smem_u32(sW);
     const uint32_t tstride = (uint32_t)(p.ring * p.Nc);   // TMEM columns per tile ring
@@ -877,13 +880,15 @@ __global__ void __launch_bounds__(352, 1)
         const uint32_t n = nstart + (uint32_t)k;
         const long long ta = clock64();
         while (acquired <= n + 2) {
-          const uint32_t r = acquired % (uint32_t)p.ring;
-          mbar_wait(&tempty[r], (acquired / (uint32_t)p.ring) & 1u);
+          mbar_wait(&tempty[acq_slot], acq_phase);
           ++acquired;
+          if (++acq_slot == (uint32_t)p.ring) {
+            acq_slot = 0;
+            acq_phase ^= 1u;
+          }
         }
         t_te += clock64() - ta;
         tc_fence_after();
-        const uint32_t pos = n % (uint32_t)p.ring;
         // Per-plane issue lists, so the issue loop is descriptor adds only (a single thread
         // feeds the tensor core; per-MMA integer work shows up directly as MMA time).
         // Normal K step: blocks pos..pos+2 <- B rows [0, 3Nc), split at the ring's end.
@@ -1001,16 +1006,20 @@ __global__ void __launch_bounds__(352, 1)
           }
         }
         // block n has received all three contributions (planes below o0 are scratch)
+        const uint32_t p1 = pos + 1 == (uint32_t)p.ring ? 0u : pos + 1;
         if (elect_one()) {
           mma_commit(&tfull[pos]);
           if (k == nin - 1) {
-            mma_commit(&tfull[(n + 1) % (uint32_t)p.ring]);
-            mma_commit(&tfull[(n + 2) % (uint32_t)p.ring]);
+            mma_commit(&tfull[p1]);
+            mma_commit(&tfull[p1 + 1 == (uint32_t)p.ring ? 0u : p1 + 1]);
           }
         }
         __syncwarp();
+        pos = p1;
       }
       nstart += (uint32_t)(nin + 2);
+      pos += 2;  // the unit's two trailing blocks
+      if (pos >= (uint32_t)p.ring) pos -= (uint32_t)p.ring;
     }
     if (p.dbg && lane == 0 && mw == 0) {
       p.dbg[blockIdx.x * 8 + 0] = clock64() - t0;
@@ -1030,11 +1039,12 @@ __global__ void __launch_bounds__(352, 1)
     const int g_lo = MB == 1 ? h : 0, g_step = MB == 1 ? 2 : 1;  // channel groups of this thread
     const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
     const bool nobias = p.flags & VM_CONV_NOBIAS;
-    for (int c = threadIdx.x - 64; c < p.Nc; c += 256) sbias[c] = (!nobias && c < p.Cout) ? p.bias[c] : 0.f;
-    asm volatile("bar.sync 1, 256;" ::: "memory");
     // blocks start empty: the first MMA into a block overwrites it (enable_input_d = 0)
     for (int r = 0; r < p.ring; ++r) mbar_arrive(&tempty[r]);
+    for (int c = threadIdx.x - 64; c < p.Nc; c += 256) sbias[c] = (!nobias && c < p.Cout) ? p.bias[c] : 0.f;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
     uint32_t n = 0;
+    uint32_t r = 0, rphase = 0;  // n % ring, (n / ring) & 1
     const long long e0 = clock64();
     long long e_w = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
@@ -1056,7 +1066,6 @@ __global__ void __launch_bounds__(352, 1)
       bf16* yb = p.y + b * p.y_bstride;
       const bf16* mb = p.mask + b * p.m_bstride;
       for (int rel = 0; rel < L; ++rel, ++n) {
-        const uint32_t r = n % (uint32_t)p.ring;
         const int o = o0 + rel - 2;
         const bool live = o >= o0 && o < o1 && !(p.xmode & 1);  // warp-uniform (tcgen05.ld is .aligned)
         // dgrad: the ReLU mask of this plane is fetched before waiting for the accumulator
@@ -1074,7 +1083,7 @@ __global__ void __launch_bounds__(352, 1)
             }
         }
         const long long tw = clock64();
-        mbar_wait(&tfull[r], (n / (uint32_t)p.ring) & 1u);
+        mbar_wait(&tfull[r], rphase);
         e_w += clock64() - tw;
         tc_fence_after();
         if (live) {
@@ -1117,6 +1126,10 @@ __global__ void __launch_bounds__(352, 1)
         }
         tc_fence_before();
         mbar_arrive(&tempty[r]);
+        if (++r == (uint32_t)p.ring) {
+          r = 0;
+          rphase ^= 1u;
+        }
       }
     }
     if (p.dbg && threadIdx.x == 64) {
