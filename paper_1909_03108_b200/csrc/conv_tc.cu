@@ -792,9 +792,10 @@ constexpr int kSwMaxStages = 8;
 
 // Warps: 0 producer, 1 and 10 MMA issuers (tiles t = 0, 2, .. and 1, 3, ..: a single issuing
 // thread's per-plane bookkeeping otherwise leaves the tensor core idle), 2..9 epilogue.
-template <int MB>
+template <int MB, bool DBG>  // DBG: cycle probes (tools/dbg_sweep_probe.py); off in production
 __global__ void __launch_bounds__(352, 1)
     k_conv_fwd_sweep(const SwParams p) {
+  auto clk = []() -> long long { return DBG ? (long long)clock64() : 0LL; };
   constexpr int NW = MB >= 2 ? 2 : 1;  // MMA-issuing warps
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t full[kSwMaxStages], empty[kSwMaxStages], tfull[kSwMaxRing], tempty[kSwMaxRing], wbar;
@@ -839,9 +840,9 @@ __global__ void __launch_bounds__(352, 1)
         for (int i = o0; i < o1 + 2; ++i) {
           for (int kc = 0; kc < p.KC; ++kc) {
             const int ng = (kc * 2 + 1 < p.CG) ? 2 : 1;
-            const long long tw = clock64();
+            const long long tw = clk();
             mbar_wait(&empty[stage], phase ^ 1);
-            t_pw += clock64() - tw;
+            t_pw += clk() - tw;
             uint8_t* sA = sStage + (size_t)stage * p.stage_bytes;
             mbar_arrive_expect_tx(&full[stage], (uint32_t)ng * p.R * 16);
             for (int g = 0; g < ng; ++g)
@@ -860,7 +861,7 @@ __global__ void __launch_bounds__(352, 1)
     // ===================== MMA issuers
     const int mw = warp == 1 ? 0 : 1;
     if (mw < NW) {  // (MB = 1: warp 10 idles)
-    const long long t0 = clock64();
+    const long long t0 = clk();
     long long t_te = 0, t_fu = 0, t_is = 0;
     mbar_wait(&wbar, 0);
     int stage = 0;
@@ -878,7 +879,7 @@ __global__ void __launch_bounds__(352, 1)
       const int nin = o1 - o0 + 2;
       for (int k = 0; k < nin; ++k) {
         const uint32_t n = nstart + (uint32_t)k;
-        const long long ta = clock64();
+        const long long ta = clk();
         while (acquired <= n + 2) {
           mbar_wait(&tempty[acq_slot], acq_phase);
           ++acquired;
@@ -887,7 +888,7 @@ __global__ void __launch_bounds__(352, 1)
             acq_phase ^= 1u;
           }
         }
-        t_te += clock64() - ta;
+        t_te += clk() - ta;
         tc_fence_after();
         // Per-plane issue lists, so the issue loop is descriptor adds only (a single thread
         // feeds the tensor core; per-MMA integer work shows up directly as MMA time).
@@ -927,9 +928,9 @@ __global__ void __launch_bounds__(352, 1)
         }
         for (int kc = 0; kc < p.KC; ++kc) {
           const int ng = (kc * 2 + 1 < p.CG) ? 2 : 1;
-          const long long tf = clock64();
+          const long long tf = clk();
           mbar_wait(&full[stage], phase);
-          const long long tf1 = clock64();
+          const long long tf1 = clk();
           t_fu += tf1 - tf;
           tc_fence_after();
           if (elect_one()) {
@@ -999,7 +1000,7 @@ __global__ void __launch_bounds__(352, 1)
             mma_commit(&empty[stage]);
           }
           __syncwarp();
-          t_is += clock64() - tf1;
+          t_is += clk() - tf1;
           if (++stage == p.stages) {
             stage = 0;
             phase ^= 1;
@@ -1022,7 +1023,7 @@ __global__ void __launch_bounds__(352, 1)
       if (pos >= (uint32_t)p.ring) pos -= (uint32_t)p.ring;
     }
     if (p.dbg && lane == 0 && mw == 0) {
-      p.dbg[blockIdx.x * 8 + 0] = clock64() - t0;
+      p.dbg[blockIdx.x * 8 + 0] = clk() - t0;
       p.dbg[blockIdx.x * 8 + 1] = t_te;
       p.dbg[blockIdx.x * 8 + 2] = t_fu;
       p.dbg[blockIdx.x * 8 + 3] = t_is;
@@ -1045,7 +1046,7 @@ __global__ void __launch_bounds__(352, 1)
     asm volatile("bar.sync 1, 256;" ::: "memory");
     uint32_t n = 0;
     uint32_t r = 0, rphase = 0;  // n % ring, (n / ring) & 1
-    const long long e0 = clock64();
+    const long long e0 = clk();
     long long e_w = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       const int col = u % p.ncol;
@@ -1082,9 +1083,9 @@ __global__ void __launch_bounds__(352, 1)
                                                                 (int64_t)o * p.P * 8));
             }
         }
-        const long long tw = clock64();
+        const long long tw = clk();
         mbar_wait(&tfull[r], rphase);
-        e_w += clock64() - tw;
+        e_w += clk() - tw;
         tc_fence_after();
         if (live) {
 #pragma unroll
@@ -1133,7 +1134,7 @@ __global__ void __launch_bounds__(352, 1)
       }
     }
     if (p.dbg && threadIdx.x == 64) {
-      p.dbg[blockIdx.x * 8 + 4] = clock64() - e0;
+      p.dbg[blockIdx.x * 8 + 4] = clk() - e0;
       p.dbg[blockIdx.x * 8 + 5] = e_w;
       p.dbg[blockIdx.x * 8 + 6] = (long long)n;
     }
@@ -1543,10 +1544,11 @@ static int launch_sweep(const FwdParams& f, int nsm, void* stream) {
   p.idesc3 = make_idesc_bf16(128, 3 * p.Nc, false, false);
   const size_t smem = (size_t)p.w_bytes + (size_t)p.stages * p.stage_bytes;
   const int grid = p.units < nsm ? p.units : nsm;
-  auto kern = p.MB == 4 ? k_conv_fwd_sweep<4>
-               : p.MB == 3 ? k_conv_fwd_sweep<3>
-               : p.MB == 2 ? k_conv_fwd_sweep<2>
-                           : k_conv_fwd_sweep<1>;
+  const bool dbg = p.dbg != nullptr;
+  auto kern = p.MB == 4 ? (dbg ? k_conv_fwd_sweep<4, true> : k_conv_fwd_sweep<4, false>)
+            : p.MB == 3 ? (dbg ? k_conv_fwd_sweep<3, true> : k_conv_fwd_sweep<3, false>)
+            : p.MB == 2 ? (dbg ? k_conv_fwd_sweep<2, true> : k_conv_fwd_sweep<2, false>)
+                        : (dbg ? k_conv_fwd_sweep<1, true> : k_conv_fwd_sweep<1, false>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<grid, 352, smem, as_stream(stream)>>>(p);
   return launch_status("vm_conv3d_fwd_tc (sweep)");
