@@ -521,6 +521,121 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_fixed(
   }
 }
 
+// Head backward with C/8 threads per voxel (one 8-channel group each): logits are summed
+// across the group with shuffles, so a thread holds 8*NC (+NC) weight-gradient accumulators
+// instead of C*NC + NC (no spills, full occupancy).  Per-block partials are reduced over lanes
+// of the same group and then over warps in a fixed order (deterministic), into the layout
+// of k_head_bwd_fixed: wpart[block][c*NC + k], bias at [C*NC + k].
+template <typename T, int C, int NC>
+__global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_grp(
+    const T* __restrict__ y, Slab sy, const float* __restrict__ W, const float* __restrict__ bias,
+    const float* __restrict__ onehot, const float* __restrict__ stats, T* __restrict__ g, Slab sg,
+    float* __restrict__ wpart, int B, float w_dice, float w_ce, float total, int dice_mask, float clamp,
+    int relu_mask) {
+  constexpr int TPV = C / 8;
+  constexpr int NACC = 8 * NC + NC;  // group's weight grads + bias grads (used by cg == 0)
+  constexpr int NWARP = kHeadThreads / 32;
+  __shared__ float sW[C * NC], sb[NC], coef[3 * NC];
+  __shared__ float red[NWARP][TPV][NACC];
+  for (int i = threadIdx.x; i < C * NC; i += blockDim.x) sW[i] = W[i];
+  if (threadIdx.x < NC) sb[threadIdx.x] = bias[threadIdx.x];
+  if (threadIdx.x == 0) {
+    const int nfg = __popc(dice_mask);
+    for (int k = 0; k < NC; ++k) {  // training.py:119-124
+      const float nk = 2.f * stats[k] + 1e-6f;
+      const float dk = stats[NC + k] + stats[2 * NC + k] + 1e-6f;
+      const bool on = (dice_mask >> k) & 1;
+      coef[3 * k + 0] = on ? (-w_dice / (float)nfg) / dk : 0.f;
+      coef[3 * k + 1] = on ? nk / dk : 0.f;
+      coef[3 * k + 2] = on ? 1.f : 0.f;
+    }
+  }
+  __syncthreads();
+  const int cg = threadIdx.x % TPV;
+  float wr[8 * NC];  // this thread's 8 channels of the head weights, in registers
+#pragma unroll
+  for (int i = 0; i < 8 * NC; ++i) wr[i] = sW[cg * 8 * NC + i];
+  const uint32_t nvox = (uint32_t)B * sy.D * sy.H * sy.W;
+  const float ce_scale = -w_ce / total;
+  float acc[NACC];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) acc[i] = 0.f;
+  for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < nvox * TPV; gi += gridDim.x * blockDim.x) {
+    const uint32_t v = gi / TPV;
+    int b, d, h, w;
+    decompose(v, sy.D, sy.H, sy.W, b, d, h, w);
+    float yv[8];
+    V8<T>::ld(y + sy.at(b, cg, d, h, w), yv);
+    float lg[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      float t = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) t = fmaf(yv[j], wr[j * NC + k], t);
+#pragma unroll
+      for (int o = 1; o < TPV; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      lg[k] = t + sb[k];
+    }
+    float m = lg[0];
+#pragma unroll
+    for (int k = 1; k < NC; ++k) m = fmaxf(m, lg[k]);
+    float p[NC], ssum = 0.f;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      p[k] = __expf(lg[k] - m);
+      ssum += p[k];
+    }
+    float gp[NC], dot = 0.f;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      p[k] = __fdividef(p[k], ssum);
+      const float gk = onehot[(size_t)v * NC + k];
+      float r = coef[3 * k + 2] != 0.f ? coef[3 * k] * (2.f * gk - coef[3 * k + 1]) : 0.f;
+      r += p[k] >= clamp ? ce_scale * (gk / fmaxf(p[k], clamp)) : 0.f;  // training.py:125-126
+      gp[k] = r;
+      dot += r * p[k];
+    }
+    float gl[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      gl[k] = p[k] * (gp[k] - dot);  // ops.py:197-199
+      if (cg == 0) acc[8 * NC + k] += gl[k];
+    }
+    float o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float sacc = 0.f;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        sacc = fmaf(wr[j * NC + k], gl[k], sacc);
+        acc[j * NC + k] = fmaf(yv[j], gl[k], acc[j * NC + k]);
+      }
+      o[j] = (relu_mask && !(yv[j] > 0.f)) ? 0.f : sacc;
+    }
+    V8<T>::st(g + sg.at(b, cg, d, h, w), o);
+  }
+  // reduce over the lanes of this warp holding the same group, then over warps (fixed order)
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) {
+    float t = acc[i];
+#pragma unroll
+    for (int o = TPV; o < 32; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane < TPV) red[warp][lane][i] = t;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < C * NC + NC; i += blockDim.x) {
+    float t = 0.f;
+    if (i < C * NC) {
+      const int c = i / NC, k = i % NC;
+      for (int wq = 0; wq < NWARP; ++wq) t += red[wq][c / 8][(c % 8) * NC + k];
+    } else {
+      for (int wq = 0; wq < NWARP; ++wq) t += red[wq][0][8 * NC + (i - C * NC)];
+    }
+    wpart[(int64_t)blockIdx.x * (C * NC + NC) + i] = t;
+  }
+}
+
 // one warp per column; lanes take strided rows, then a fixed shuffle tree (deterministic)
 __global__ void k_reduce_rows(const float* __restrict__ part, int rows, int width,
                               float* __restrict__ out) {
@@ -704,7 +819,7 @@ extern "C" int vm_head_bwd(int dtype, const void* y, int64_t y_bstride, const fl
     using T = __nv_bfloat16;
     auto st = as_stream(stream);
 #define HEAD_BWD_FIXED(CC)                                                                          \
-  k_head_bwd_fixed<T, CC, 3><<<grid, kHeadThreads, 0, st>>>((const T*)y, sy, w, b, onehot, stats, (T*)g, sg, \
+  k_head_bwd_grp<T, CC, 3><<<grid, kHeadThreads, 0, st>>>((const T*)y, sy, w, b, onehot, stats, (T*)g, sg, \
                                                             wpartials, B, w_dice, w_ce, total_voxels,    \
                                                             dice_mask, clamp, relu_mask)
     if (C == 16)
