@@ -1862,8 +1862,10 @@ static bool plan_wgrad_kd(int B, int Cin, int Cout, int D, int H, int W, WkParam
   p.g_bytes = (uint32_t)(p.Nc / 8) * p.KS * 16;
   p.g_load = (uint32_t)p.CGo * p.KS * 16;
   for (;;) {
-    const int runs_alloc = (16 * p.mt_per_unit + 2) / 3 + 2;
-    p.a_bytes = ((uint32_t)runs_alloc * 3 * p.Wp * 16 + 1023) & ~1023u;
+    // slot positions a CTA touches: its 16*mt_per_unit M slots (+ up to 2 of run alignment),
+    // never more than the 3*CG run slots + the ones slot; + 1 slot of slack for the last run
+    const int slots = min(16 * p.mt_per_unit + 2, 3 * p.CG + 1) + 1;
+    p.a_bytes = ((uint32_t)slots * p.Wp * 16 + 1023) & ~1023u;
     p.stage_bytes = (p.a_bytes + 3 * p.g_bytes + 1023) & ~1023u;
     p.stages = kSmemBudget / (int)p.stage_bytes;
     if (p.stages >= 2 || p.mt_per_unit == 1) break;
