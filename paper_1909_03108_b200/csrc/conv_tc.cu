@@ -709,45 +709,63 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc<512>(tbase);
 }
 
+// Fixed-order reduction of nk K-split partials for 32 consecutive elements e per block:
+// warp w sums k = w, w+8, ... (two interleaved chains), then warp 0 adds the 8 warp sums in
+// order.  Deterministic, coalesced (a warp reads 128 contiguous bytes per k), and 8 warps per
+// 32 elements keep enough loads in flight (one thread per element with a 148-deep serial loop
+// ran at ~0.6 TB/s).
+__device__ __forceinline__ float ksplit_sum(const float* __restrict__ ws, int64_t E, int nk, int64_t e,
+                                            float (*red)[32]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float s0 = 0.f, s1 = 0.f;
+  if (e < E) {
+    int k = w;
+    for (; k + 8 < nk; k += 16) {
+      s0 += ws[(int64_t)k * E + e];
+      s1 += ws[(int64_t)(k + 8) * E + e];
+    }
+    if (k < nk) s0 += ws[(int64_t)k * E + e];
+  }
+  red[w][lane] = s0 + s1;
+  __syncthreads();
+  float t = 0.f;
+  if (w == 0) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += red[i][lane];
+  }
+  return t;  // valid in warp 0
+}
+
 // Fixed-order reduction of the K-split partials, one thread per partial element
 // (coalesced over m): ws[k][mt][kw][co][m] -> gw[t][ci][co] with t = (kd*3+kh)*3 + kw,
 // g = mt*16 + m/8 = (kd*3+kh)*CG + ci/8; the ones slot (kw = 0, m%8 = 0) gives gb.
-__global__ void k_wgrad_tc_finalize(const float* __restrict__ ws, float* __restrict__ gw,
-                                    float* __restrict__ gb, int nk, int MT, int Nc, int CG, int Cin,
-                                    int Cout, int ones_slot, int runs) {
+__global__ void __launch_bounds__(256) k_wgrad_tc_finalize(const float* __restrict__ ws, float* __restrict__ gw,
+                                                          float* __restrict__ gb, int nk, int MT, int Nc, int CG,
+                                                          int Cin, int Cout, int ones_slot, int runs) {
+  __shared__ float red[8][32];
   const int64_t E = (int64_t)MT * 3 * Nc * 128;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int m = e % 128;
-    const int co = (e / 128) % Nc;
-    const int kw = (e / (128 * Nc)) % 3;
-    const int mt = (int)(e / (384LL * Nc));
-    const int g = mt * 16 + m / 8;
-    if (co >= Cout) continue;
-    // slot -> (kd*3 + kh, channel group)
-    const int pp = runs ? ((g / 3) / CG) * 3 + g % 3 : g / CG;
-    const int cgi = runs ? (g / 3) % CG : g % CG;
-    const bool is_w = g < 9 * CG && cgi * 8 + m % 8 < Cin;
-    const bool is_b = g == ones_slot && kw == 0 && m % 8 == 0;
-    if (!is_w && !is_b) continue;
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;  // 4 independent chains, fixed order
-    int k = 0;
-    for (; k + 4 <= nk; k += 4) {
-      s0 += ws[(k + 0) * E + e];
-      s1 += ws[(k + 1) * E + e];
-      s2 += ws[(k + 2) * E + e];
-      s3 += ws[(k + 3) * E + e];
-    }
-    for (; k < nk; ++k) s0 += ws[k * E + e];
-    const float s = (s0 + s1) + (s2 + s3);
-    if (is_w) {
-      const int ci = cgi * 8 + m % 8;
-      gw[((int64_t)(pp * 3 + kw) * Cin + ci) * Cout + co] = s;
-    } else {
-      gb[co] = s;
-    }
+  const int64_t e = blockIdx.x * 32LL + (threadIdx.x & 31);
+  const float s = ksplit_sum(ws, E, nk, e, red);
+  if (threadIdx.x >= 32 || e >= E) return;
+  const int m = e % 128;
+  const int co = (e / 128) % Nc;
+  const int kw = (e / (128 * Nc)) % 3;
+  const int mt = (int)(e / (384LL * Nc));
+  const int g = mt * 16 + m / 8;
+  if (co >= Cout) return;
+  // slot -> (kd*3 + kh, channel group)
+  const int pp = runs ? ((g / 3) / CG) * 3 + g % 3 : g / CG;
+  const int cgi = runs ? (g / 3) % CG : g % CG;
+  const bool is_w = g < 9 * CG && cgi * 8 + m % 8 < Cin;
+  const bool is_b = g == ones_slot && kw == 0 && m % 8 == 0;
+  if (is_w) {
+    const int ci = cgi * 8 + m % 8;
+    gw[((int64_t)(pp * 3 + kw) * Cin + ci) * Cout + co] = s;
+  } else if (is_b) {
+    gb[co] = s;
   }
 }
+
 
 
 // ------------------------------------------------------------------ forward, kd stacked along N
@@ -1334,42 +1352,33 @@ __global__ void __launch_bounds__(192, 1)
 
 // ws[k][mt][kw][n = kd*Nc + co][m] -> gw[t][ci][co], t = (kd*3 + kh)*3 + kw, slot
 // g = mt*16 + m/8 = cg*3 + kh; the ones slot (kd = 0, kw = 0, m%8 = 0) gives gb.
-__global__ void k_wgrad_kd_finalize(const float* __restrict__ ws, float* __restrict__ gw,
-                                    float* __restrict__ gb, int nk, int MT, int Nc, int CG, int Cin,
-                                    int Cout, int ones_slot) {
+__global__ void __launch_bounds__(256) k_wgrad_kd_finalize(const float* __restrict__ ws, float* __restrict__ gw,
+                                                          float* __restrict__ gb, int nk, int MT, int Nc, int CG,
+                                                          int Cin, int Cout, int ones_slot) {
+  __shared__ float red[8][32];
   const int N3 = 3 * Nc;
   const int64_t E = (int64_t)MT * 3 * N3 * 128;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int m = e % 128;
-    const int n = (e / 128) % N3;
-    const int kw = (e / (128 * N3)) % 3;
-    const int mt = (int)(e / (384LL * N3));
-    const int g = mt * 16 + m / 8;
-    const int kd = n / Nc, co = n % Nc;
-    if (co >= Cout) continue;
-    const int cg = g / 3, kh = g % 3;
-    const bool is_w = g < 3 * CG && cg * 8 + m % 8 < Cin;
-    const bool is_b = g == ones_slot && kw == 0 && kd == 0 && m % 8 == 0;
-    if (!is_w && !is_b) continue;
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;  // 4 independent chains, fixed order
-    int k = 0;
-    for (; k + 4 <= nk; k += 4) {
-      s0 += ws[(k + 0) * E + e];
-      s1 += ws[(k + 1) * E + e];
-      s2 += ws[(k + 2) * E + e];
-      s3 += ws[(k + 3) * E + e];
-    }
-    for (; k < nk; ++k) s0 += ws[k * E + e];
-    const float s = (s0 + s1) + (s2 + s3);
-    if (is_w) {
-      const int ci = cg * 8 + m % 8;
-      gw[((int64_t)((kd * 3 + kh) * 3 + kw) * Cin + ci) * Cout + co] = s;
-    } else {
-      gb[co] = s;
-    }
+  const int64_t e = blockIdx.x * 32LL + (threadIdx.x & 31);
+  const float s = ksplit_sum(ws, E, nk, e, red);
+  if (threadIdx.x >= 32 || e >= E) return;
+  const int m = e % 128;
+  const int n = (e / 128) % N3;
+  const int kw = (e / (128 * N3)) % 3;
+  const int mt = (int)(e / (384LL * N3));
+  const int g = mt * 16 + m / 8;
+  const int kd = n / Nc, co = n % Nc;
+  if (co >= Cout) return;
+  const int cg = g / 3, kh = g % 3;
+  const bool is_w = g < 3 * CG && cg * 8 + m % 8 < Cin;
+  const bool is_b = g == ones_slot && kw == 0 && kd == 0 && m % 8 == 0;
+  if (is_w) {
+    const int ci = cg * 8 + m % 8;
+    gw[((int64_t)((kd * 3 + kh) * 3 + kw) * Cin + ci) * Cout + co] = s;
+  } else if (is_b) {
+    gb[co] = s;
   }
 }
+
 
 }  // namespace vm
 
@@ -1927,8 +1936,8 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
       if (rc) return rc;
       const int nk = pk.grid / pk.n_mtgroups;
       const int64_t E = (int64_t)pk.MT * 9 * pk.Nc * 128;
-      k_wgrad_kd_finalize<<<grid_for(E, 256), 256, 0, st>>>(pk.ws, gw, gb, nk, pk.MT, pk.Nc, pk.CG, Cin, Cout,
-                                                            pk.ones_slot);
+      k_wgrad_kd_finalize<<<(unsigned)((E + 31) / 32), 256, 0, st>>>(pk.ws, gw, gb, nk, pk.MT, pk.Nc, pk.CG, Cin,
+                                                                    Cout, pk.ones_slot);
       return launch_status("vm_conv3d_wgrad_tc (kd) finalize");
     }
   }
@@ -1960,8 +1969,8 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
   if (rc) return rc;
   const int nk = p.grid / p.n_mtgroups;
   const int64_t E = (int64_t)p.MT * 3 * p.Nc * 128;
-  k_wgrad_tc_finalize<<<grid_for(E, 256), 256, 0, st>>>(p.ws, gw, gb, nk, p.MT, p.Nc, p.CG, Cin, Cout,
-                                                         p.ones_slot, p.runs);
+  k_wgrad_tc_finalize<<<(unsigned)((E + 31) / 32), 256, 0, st>>>(p.ws, gw, gb, nk, p.MT, p.Nc, p.CG, Cin, Cout,
+                                                                 p.ones_slot, p.runs);
   rc = launch_status("vm_conv3d_wgrad_tc finalize");
   if (rc || p.ones_slot >= 0) return rc;
   float* wsb = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ((pl.ws_main + 255) / 256) * 256);
