@@ -1526,7 +1526,8 @@ static int launch_sweep(const FwdParams& f, int nsm, void* stream) {
     if (stages < 3) continue;
     const int ncol = (p.P + MB * 128 - 1) / (MB * 128);
     // per input plane: 9*KC MMAs per tile (+1 at the first K step); a short ring (< 6) stalls
-    const double plane = (9.0 * p.KC + 1) * MB * mma_cycles(3 * p.Nc, MB) * (ring < 6 ? 1.15 : 1.0);
+    // + ~900 cycles of per-plane MMA-warp bookkeeping (measured with tools/dbg_sweep_probe.py)
+    const double plane = (9.0 * p.KC + 1) * MB * mma_cycles(3 * p.Nc, MB) * (ring < 6 ? 1.15 : 1.0) + 900.0;
     for (int S = 1; S <= p.D; ++S) {
       const int nseg = (p.D + S - 1) / S;
       const int64_t units = (int64_t)f.B * ncol * nseg;
