@@ -90,7 +90,7 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 //  * plain  (k_conv_fwd_tc):    [nchunk][kc][kd][9 taps (kh,kw)][2 K-halves][Nc][8],
 //                               co = nchunk*Nc + n;
 //  * sweep  (k_conv_fwd_sweep): [kc][9 taps (kh,kw)][2 K-halves][3*Nc][8], row n holds
-//                               kd = 2 - n / Nc, co = n % Nc (thin outputs, Nc <= 32).
+//                               kd = 2 - n / Nc, co = n % Nc (thin outputs, Nc <= 48).
 // flip = 1 packs the dgrad operand W'[t'][ci'][co'] = W[26 - t'][co'][ci'] (conv of the
 // output gradient).  Both layouts hold the same number of elements.
 struct PackGeom {
@@ -100,7 +100,7 @@ struct PackGeom {
   int sweep;       // 1: kd stacked along N (k_conv_fwd_sweep)
 };
 
-constexpr int kSweepMaxNc = 32;  // Nc = 48 (N = 144) measured slower than k_conv_fwd_tc
+constexpr int kSweepMaxNc = 48;  // Nc = 48 (16->48 dgrad): 141 -> 91 us vs k_conv_fwd_tc
 constexpr uint32_t kSweepMaxWeightBytes = 100 * 1024;
 constexpr bool kSweepEnabled = true;
 
@@ -769,7 +769,7 @@ __global__ void __launch_bounds__(256) k_wgrad_tc_finalize(const float* __restri
 
 
 // ------------------------------------------------------------------ forward, kd stacked along N
-// Thin outputs (Nc <= 32): the three kd taps are stacked along N (N = 3*Nc, rows ordered
+// Thin outputs (Nc <= 48): the three kd taps are stacked along N (N = 3*Nc, rows ordered
 // kd = 2, 1, 0) and a CTA sweeps a column of M tiles (MB*128 in-plane anchors) through a
 // segment of depth planes.  Input plane i contributes to output planes i-2, i-1, i, whose
 // accumulators are consecutive blocks of a TMEM ring (block = ring sequence mod ring), so
