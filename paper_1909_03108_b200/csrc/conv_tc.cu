@@ -1184,6 +1184,8 @@ struct WkParams {
   uint32_t a_bytes;
   uint32_t g_bytes;  // per kd slice: Nc/8 group slots of KS rows (CGo of them loaded)
   uint32_t g_load;   // loaded bytes per kd slice: CGo * KS * 16
+  int ksub;              // K chunks of KS anchors per pipeline stage
+  uint32_t sub_bytes;    // bytes per K chunk (A runs + 3 gy slices)
   uint32_t stage_bytes, idesc, idesc64;  // M = 64 for M-tiles with <= 8 live slots
   float* ws;  // [kidx][MT][3 kw][3*Nc][128]
   long long* dbg;  // optional cycle probes [gridDim][8] (vm_debug_set_fwd_probe)
@@ -1237,7 +1239,7 @@ __global__ void __launch_bounds__(192, 1)
       const int r_end = min(p.CG - 1, (16 * (mt0 + nmt) - 1) / 3);  // last run of this CTA
       const int nrun = r_end >= r0 ? r_end - r0 + 1 : 0;
       const int Rrun = p.KS + 2 * p.Wp + 2;
-      const uint32_t tx = (uint32_t)nrun * Rrun * 16 + 3 * p.g_load;
+      const uint32_t tx = p.ksub * ((uint32_t)nrun * Rrun * 16 + 3 * p.g_load);
       long long t_pe = 0;
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
         const int ks = (u / p.n_mtgroups) % p.ksplit;
@@ -1245,19 +1247,21 @@ __global__ void __launch_bounds__(192, 1)
         const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
         const bf16* xb = p.x + b * p.x_bstride;
         for (int s = s0; s < s1; ++s) {
-          const int k0 = s * p.KS;
           const long long tw = clock64();
           mbar_wait(&empty[stage], phase ^ 1);
           t_pe += clock64() - tw;
-          uint8_t* sA = smem + (size_t)stage * p.stage_bytes;
-          uint8_t* sG = sA + p.a_bytes;
           mbar_arrive_expect_tx(&full[stage], tx);
-          const int gr0 = k0 + p.P + p.Wp + 1;
-          for (int kd = 0; kd < 3; ++kd)  // rows outside [0, Dp*P) read as zeros
-            tma_load_4d(sG + (size_t)kd * p.g_bytes, &gmap, &full[stage], 0, gr0 - kd * p.P, 0, b);
-          for (int r = r0; r <= r_end; ++r)
-            bulk_load(sA + (size_t)(r - r0) * 3 * GS, xb + r * p.plane8 + (int64_t)k0 * 8, (uint32_t)Rrun * 16,
-                      &full[stage]);
+          for (int j = 0; j < p.ksub; ++j) {  // ksub consecutive K chunks per stage
+            const int k0 = (s * p.ksub + j) * p.KS;
+            uint8_t* sA = smem + (size_t)stage * p.stage_bytes + (size_t)j * p.sub_bytes;
+            uint8_t* sG = sA + p.a_bytes;
+            const int gr0 = k0 + p.P + p.Wp + 1;
+            for (int kd = 0; kd < 3; ++kd)  // rows outside [0, Dp*P) read as zeros
+              tma_load_4d(sG + (size_t)kd * p.g_bytes, &gmap, &full[stage], 0, gr0 - kd * p.P, 0, b);
+            for (int r = r0; r <= r_end; ++r)
+              bulk_load(sA + (size_t)(r - r0) * 3 * GS, xb + r * p.plane8 + (int64_t)k0 * 8, (uint32_t)Rrun * 16,
+                        &full[stage]);
+          }
           if (++stage == p.stages) {
             stage = 0;
             phase ^= 1;
@@ -1283,14 +1287,15 @@ __global__ void __launch_bounds__(192, 1)
         t_fu += tf1 - tf;
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes);
+         for (int j = 0; j < p.ksub; ++j) {
+          const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes + (size_t)j * p.sub_bytes);
           const uint32_t sG = sA + p.a_bytes;
           // B: MN-major, N groups (kd, cgo) KS rows apart; A: MN-major slots GS apart
           const uint64_t b0desc = make_sdesc(sG, 128, (uint32_t)p.KS * 16);
           const uint64_t a0desc = make_sdesc(sA + (uint32_t)slot_shift * GS, 128, GS);
           const uint32_t mstep = 16 * (GS >> 4);
           const int nkk = p.KS / 16;
-          const uint32_t acc0 = started ? 1u : 0u;
+          const uint32_t acc0 = (started || j > 0) ? 1u : 0u;
 #pragma unroll 4
           for (int kk = 0; kk < nkk; ++kk) {
             const uint64_t bdesc = b0desc + (uint64_t)(kk * 16);
@@ -1305,6 +1310,7 @@ __global__ void __launch_bounds__(192, 1)
               mma_bf16_ss(d + 2 * N3, adesc + 2, bdesc, id, acc);
             }
           }
+         }
           mma_commit(&empty[stage]);
         }
         __syncwarp();
@@ -1876,7 +1882,10 @@ static bool plan_wgrad_kd(int B, int Cin, int Cout, int D, int H, int W, WkParam
     // never more than the 3*CG run slots + the ones slot; + 1 slot of slack for the last run
     const int slots = min(16 * p.mt_per_unit + 2, 3 * p.CG + 1) + 1;
     p.a_bytes = ((uint32_t)slots * p.Wp * 16 + 1023) & ~1023u;
-    p.stage_bytes = (p.a_bytes + 3 * p.g_bytes + 1023) & ~1023u;
+    p.sub_bytes = (p.a_bytes + 3 * p.g_bytes + 1023) & ~1023u;
+    // two K chunks per stage halve the per-stage MMA-warp bookkeeping when 4 stages still fit
+    p.ksub = kSmemBudget / (int)(2 * p.sub_bytes) >= 4 ? 2 : 1;
+    p.stage_bytes = p.ksub * p.sub_bytes;
     p.stages = kSmemBudget / (int)p.stage_bytes;
     if (p.stages >= 2 || p.mt_per_unit == 1) break;
     do --p.mt_per_unit; while (p.mt_per_unit > 1 && p.MT % p.mt_per_unit);
@@ -1884,13 +1893,13 @@ static bool plan_wgrad_kd(int B, int Cin, int Cout, int D, int H, int W, WkParam
   if (p.stages < 2) return false;
   if (p.stages > kMaxStages) p.stages = kMaxStages;
   p.n_mtgroups = (p.MT + p.mt_per_unit - 1) / p.mt_per_unit;
-  p.stages_total = (p.rows + p.KS - 1) / p.KS;
+  p.stages_total = (p.rows + p.KS * p.ksub - 1) / (p.KS * p.ksub);
   int nsm = vm_num_sms(0);
   if (nsm <= 0) nsm = 148;
   int want = (2 * nsm + p.n_mtgroups * B - 1) / (p.n_mtgroups * B);  // ~2 units per SM
   if (want < 1) want = 1;
   p.spk = (p.stages_total + want - 1) / want;
-  if (p.spk < 4) p.spk = 4;
+  if (p.spk < 2) p.spk = 2;
   p.ksplit = (p.stages_total + p.spk - 1) / p.spk;
   p.units = p.n_mtgroups * B * p.ksplit;
   p.idesc = make_idesc_bf16(128, 3 * p.Nc, true, true);
