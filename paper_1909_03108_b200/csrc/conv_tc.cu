@@ -1179,6 +1179,8 @@ struct WkParams {
   int CG, CGo, Cout, Nc;
   int KS;              // anchors per stage (<= Wp - 2, multiple of 16)
   int MT, mt_per_unit, n_mtgroups;
+  int nkw;             // kw taps per CTA (3, or 1 when 3 accumulators of N = 3*Nc exceed TMEM)
+  int ngroups;         // CTA groups = n_mtgroups * (3 / nkw): (M-tile group, kw group)
   int ones_slot;
   int spk, ksplit, stages_total, units, grid, stages;
   uint32_t a_bytes;
@@ -1198,7 +1200,9 @@ __global__ void __launch_bounds__(192, 1)
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages], tfull;
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int mg_cta = blockIdx.x % p.n_mtgroups;
+  const int grp = blockIdx.x % p.ngroups;      // (M-tile group, kw group) of this CTA
+  const int mg_cta = grp % p.n_mtgroups;
+  const int kw0 = (grp / p.n_mtgroups) * p.nkw;  // first kw tap of this CTA
   const int mt0 = mg_cta * p.mt_per_unit;
   const int nmt = min(p.mt_per_unit, p.MT - mt0);
   const int N3 = 3 * p.Nc;
@@ -1211,8 +1215,9 @@ __global__ void __launch_bounds__(192, 1)
   const bool last64 = 3 * p.CG + 1 - 16 * (mt0 + nmt - 1) <= 8;
   if (p.ones_slot >= 0 && p.ones_slot / 16 >= mt0 && p.ones_slot / 16 < mt0 + nmt) {
     const int local = p.ones_slot - mt0 * 16 + slot_shift;
-    for (int s = 0; s < p.stages; ++s) {
-      uint32_t* dst = reinterpret_cast<uint32_t*>(smem + (size_t)s * p.stage_bytes + (size_t)local * GS);
+    for (int s = 0; s < p.stages * p.ksub; ++s) {  // every K chunk of every stage
+      uint32_t* dst = reinterpret_cast<uint32_t*>(smem + (size_t)(s / p.ksub) * p.stage_bytes +
+                                                  (size_t)(s % p.ksub) * p.sub_bytes + (size_t)local * GS);
       for (int i = threadIdx.x; i < (p.KS + 8) * 4; i += blockDim.x) dst[i] = 0x3F803F80u;  // bf16 1.0 x2
     }
   }
@@ -1242,8 +1247,8 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t tx = p.ksub * ((uint32_t)nrun * Rrun * 16 + 3 * p.g_load);
       long long t_pe = 0;
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        const int ks = (u / p.n_mtgroups) % p.ksplit;
-        const int b = u / (p.n_mtgroups * p.ksplit);
+        const int ks = (u / p.ngroups) % p.ksplit;
+        const int b = u / (p.ngroups * p.ksplit);
         const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
         const bf16* xb = p.x + b * p.x_bstride;
         for (int s = s0; s < s1; ++s) {
@@ -1278,7 +1283,7 @@ __global__ void __launch_bounds__(192, 1)
     const long long t0 = clock64();
     long long t_fu = 0, t_is = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      const int ks = (u / p.n_mtgroups) % p.ksplit;
+      const int ks = (u / p.ngroups) % p.ksplit;
       const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
       for (int s = s0; s < s1; ++s) {
         const long long tf = clock64();
@@ -1302,12 +1307,14 @@ __global__ void __launch_bounds__(192, 1)
             const uint32_t acc = kk > 0 ? 1u : acc0;
 #pragma unroll
             for (int m = 0; m < NMT; ++m) {
-              const uint64_t adesc = a0desc + (uint64_t)(m * mstep + kk * 16);
-              const uint32_t d = tbase + (uint32_t)(m * 3 * N3);
+              const uint64_t adesc = a0desc + (uint64_t)(m * mstep + kk * 16 + kw0);
+              const uint32_t d = tbase + (uint32_t)(m * p.nkw * N3);
               const uint32_t id = m == NMT - 1 ? id_last : p.idesc;
               mma_bf16_ss(d, adesc, bdesc, id, acc);
-              mma_bf16_ss(d + N3, adesc + 1, bdesc, id, acc);
-              mma_bf16_ss(d + 2 * N3, adesc + 2, bdesc, id, acc);
+              if (p.nkw == 3) {
+                mma_bf16_ss(d + N3, adesc + 1, bdesc, id, acc);
+                mma_bf16_ss(d + 2 * N3, adesc + 2, bdesc, id, acc);
+              }
             }
           }
          }
@@ -1332,18 +1339,18 @@ __global__ void __launch_bounds__(192, 1)
   } else {
     // drain: warp (2..5) reads TMEM lane quarter warp & 3
     const int q = warp & 3;
-    const int kidx = blockIdx.x / p.n_mtgroups;
+    const int kidx = blockIdx.x / p.ngroups;
     mbar_wait(&tfull, 0);
     tc_fence_after();
     for (int m = 0; m < nmt; ++m) {
       const bool m64 = last64 && m == nmt - 1;
       const int m_row = m64 ? q * 16 + lane : q * 32 + lane;
       const bool live = !m64 || lane < 16;
-      for (int c0 = 0; c0 < 3 * N3; c0 += 16) {
+      for (int c0 = 0; c0 < p.nkw * N3; c0 += 16) {
         uint32_t r[16];
-        tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(m * 3 * N3 + c0), r);
+        tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(m * p.nkw * N3 + c0), r);
         tmem_ld_wait();
-        float* dst = p.ws + (((int64_t)kidx * p.MT + mt0 + m) * 3 * N3 + c0) * 128 + m_row;
+        float* dst = p.ws + (((int64_t)kidx * p.MT + mt0 + m) * 3 * N3 + kw0 * N3 + c0) * 128 + m_row;
         if (live) {
 #pragma unroll
           for (int e = 0; e < 16; ++e) dst[e * 128] = __uint_as_float(r[e]);
@@ -1865,13 +1872,18 @@ static bool plan_wgrad_kd(int B, int Cin, int Cout, int D, int H, int W, WkParam
   p.CGo = (Cout + 7) / 8;
   p.Cout = Cout;
   p.Nc = (Cout + 15) / 16 * 16;
-  if (3 * p.Nc > 144) return false;
+  if (3 * p.Nc > 256) return false;  // N = 3*Nc per MMA
   p.KS = min(256, ((p.Wp - 2) / 16) * 16);  // a run of KS + 2Wp + 2 rows fits 3 slots of Wp rows
   if (p.KS < 32) return false;
+  // one kw tap per CTA (Nc > 48) triples the A traffic per output: only with long K chunks
+  // (measured: 64->64 at 32^3, KS = 32, is slower than k_conv_wgrad_tc)
+  if (p.Nc > 48 && p.KS < 64) return false;
   if ((3 * p.CG) % 16 == 0) return false;  // no spare M slot for the bias-gradient ones block
   p.MT = (3 * p.CG + 1 + 15) / 16;
   p.ones_slot = 3 * p.CG;
-  p.mt_per_unit = 512 / (9 * p.Nc);
+  // TMEM: mt_per_unit tiles x nkw kw accumulators x 3*Nc columns <= 512
+  p.nkw = 9 * p.Nc <= 512 ? 3 : 1;
+  p.mt_per_unit = 512 / (p.nkw * 3 * p.Nc);
   if (p.mt_per_unit > p.MT) p.mt_per_unit = p.MT;
   while (p.mt_per_unit > 1 && p.MT % p.mt_per_unit) --p.mt_per_unit;  // equal groups (kernel template)
   if (p.mt_per_unit < 1) return false;
@@ -1893,21 +1905,22 @@ static bool plan_wgrad_kd(int B, int Cin, int Cout, int D, int H, int W, WkParam
   if (p.stages < 2) return false;
   if (p.stages > kMaxStages) p.stages = kMaxStages;
   p.n_mtgroups = (p.MT + p.mt_per_unit - 1) / p.mt_per_unit;
+  p.ngroups = p.n_mtgroups * (3 / p.nkw);
   p.stages_total = (p.rows + p.KS * p.ksub - 1) / (p.KS * p.ksub);
   int nsm = vm_num_sms(0);
   if (nsm <= 0) nsm = 148;
-  int want = (2 * nsm + p.n_mtgroups * B - 1) / (p.n_mtgroups * B);  // ~2 units per SM
+  int want = (2 * nsm + p.ngroups * B - 1) / (p.ngroups * B);  // ~2 units per SM
   if (want < 1) want = 1;
   p.spk = (p.stages_total + want - 1) / want;
   if (p.spk < 2) p.spk = 2;
   p.ksplit = (p.stages_total + p.spk - 1) / p.spk;
-  p.units = p.n_mtgroups * B * p.ksplit;
+  p.units = p.ngroups * B * p.ksplit;
   p.idesc = make_idesc_bf16(128, 3 * p.Nc, true, true);
   p.idesc64 = make_idesc_bf16(64, 3 * p.Nc, true, true);
   p.grid = p.units;
-  if (p.grid > nsm) p.grid = (nsm / p.n_mtgroups) * p.n_mtgroups;
-  if (p.grid < p.n_mtgroups) p.grid = p.n_mtgroups;
-  ws = (size_t)(p.grid / p.n_mtgroups) * p.MT * 9 * p.Nc * 128 * sizeof(float);
+  if (p.grid > nsm) p.grid = (nsm / p.ngroups) * p.ngroups;
+  if (p.grid < p.ngroups) p.grid = p.ngroups;
+  ws = (size_t)(p.grid / p.ngroups) * p.MT * 9 * p.Nc * 128 * sizeof(float);
   return true;
 }
 
@@ -1944,7 +1957,7 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
       kern<<<pk.grid, 192, (size_t)pk.stages * pk.stage_bytes, st>>>(gmap, pk);
       rc = launch_status("vm_conv3d_wgrad_tc (kd)");
       if (rc) return rc;
-      const int nk = pk.grid / pk.n_mtgroups;
+      const int nk = pk.grid / pk.ngroups;
       const int64_t E = (int64_t)pk.MT * 9 * pk.Nc * 128;
       k_wgrad_kd_finalize<<<(unsigned)((E + 31) / 32), 256, 0, st>>>(pk.ws, gw, gb, nk, pk.MT, pk.Nc, pk.CG, Cin,
                                                                     Cout, pk.ones_slot);

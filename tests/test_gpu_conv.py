@@ -135,6 +135,10 @@ WG_SHAPES = [
     (2, 24, 8, 3, 5, 34),
     (1, 96, 32, 4, 4, 64),
     (1, 8, 16, 40, 4, 32),
+    # Cout 64..80: one kw tap per CTA (three accumulators of N = 3*Nc exceed TMEM)
+    (1, 64, 64, 6, 6, 34),
+    (1, 32, 64, 4, 8, 40),
+    (2, 16, 80, 3, 4, 48),
 ]
 
 
