@@ -462,9 +462,6 @@ struct WgParams {
   int runs;         // 1: stage one run of KS+2Wp+2 rows per (kd, cg) serving all three kh
                     //    (M slot g' = (kd*CG + cg)*3 + kh, slot stride Wp rows); 0: one copy per slot
   int runs_alloc;   // run slots per stage buffer (runs mode)
-  int fold;         // 1: kw folded into N (B = three kw-shifted copies of gy made in SMEM)
-  int RRg;          // fold mode: rows of the raw gy box (KS + 16, 8-row aligned start)
-  uint32_t gc_off;  // fold mode: offset of the shifted-copy region from the gy box
   int spk;          // stages per unit (K-split chunk)
   int ksplit;       // K-split chunks per sample
   int stages_total; // per sample
@@ -482,7 +479,7 @@ template <int NMT>  // > 0: M-tiles per CTA known at compile time (straight-line
 __global__ void __launch_bounds__(192, 1)
     k_conv_wgrad_tc(const __grid_constant__ CUtensorMap gmap, const WgParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t full[kMaxStages], empty[kMaxStages], ready[kMaxStages], tfull, tempty;
+  __shared__ uint64_t full[kMaxStages], empty[kMaxStages], tfull, tempty;
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int mg_cta = blockIdx.x % p.n_mtgroups;  // every unit of this CTA has the same M-tile group
@@ -506,7 +503,6 @@ __global__ void __launch_bounds__(192, 1)
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&ready[s], 128);
     }
     mbar_init(&tfull, 1);
     mbar_init(&tempty, 128);
@@ -546,9 +542,7 @@ __global__ void __launch_bounds__(192, 1)
           uint8_t* sG = sA + p.a_bytes;
           mbar_arrive_expect_tx(&full[stage], tx);
           const int gr0 = (int)(k0 + p.P + p.Wp + 1);
-          if (p.fold)
-            tma_load_4d(sG, &gmap, &full[stage], 0, (gr0 - 2) >> 3, 0, b);
-          else if (p.gwide)
+          if (p.gwide)
             tma_load_4d(sG, &gmap, &full[stage], 0, (gr0 - p.gdelta) >> 3, 0, b);
           else
             tma_load_4d(sG, &gmap, &full[stage], 0, gr0, 0, b);
@@ -586,26 +580,9 @@ __global__ void __launch_bounds__(192, 1)
       const int ks = (u / p.n_mtgroups) % p.ksplit;
       const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
       for (int s = s0; s < s1; ++s) {
-        mbar_wait(p.fold ? &ready[stage] : &full[stage], phase);
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        if (p.fold && elect_one()) {
-          // kw folded into N: one MMA per (M-tile, K step), N = 3*Nc over the shifted gy copies
-          const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes);
-          const uint32_t sC = sA + p.a_bytes + p.gc_off;
-          const uint64_t b0desc = make_sdesc(sC, 128, (uint32_t)p.KS * 16);
-          const uint64_t a0desc = make_sdesc(sA + (uint32_t)slot_shift * GS, 128, sbo);
-          const uint32_t mstep = 16 * (GS >> 4);
-#pragma unroll 1
-          for (int kk = 0; kk < p.KS / 16; ++kk) {
-            const uint32_t acc = (started || kk > 0) ? 1u : 0u;
-            const uint64_t bdesc = b0desc + (uint64_t)(kk * 16);
-#pragma unroll 1
-            for (int m = 0; m < nmt; ++m)
-              mma_bf16_ss(tbase + (uint32_t)(m * 3 * p.Nc), a0desc + (uint64_t)(m * mstep + kk * 16), bdesc,
-                          p.idesc, acc);
-          }
-          mma_commit(&empty[stage]);
-        } else if (!p.fold && elect_one()) {
+        if (elect_one()) {
           const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes);
           const uint32_t sG = sA + p.a_bytes;
           const uint64_t b0desc = make_sdesc(sG + (uint32_t)p.gdelta * 16, 128, (uint32_t)p.RR * 16);
@@ -655,38 +632,6 @@ __global__ void __launch_bounds__(192, 1)
     if (elect_one()) mma_commit(&tfull);
     __syncwarp();
   } else {
-    if (p.fold) {
-      // gy shift workers: copy kw[u] = raw[u + delta - kw] for kw = 0..2, every stage
-      const int et = threadIdx.x - 64;
-      const int ngo = p.Nc / 8;
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        const int ks = (u / p.n_mtgroups) % p.ksplit;
-        const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
-        for (int s = s0; s < s1; ++s) {
-          const int64_t k0 = (int64_t)s * p.KS;
-          const int gr0 = (int)(k0 + p.P + p.Wp + 1);
-          const int delta = gr0 - ((gr0 - 2) & ~7);
-          mbar_wait(&full[stage], phase);
-          const int4* raw = reinterpret_cast<const int4*>(smem + (size_t)stage * p.stage_bytes + p.a_bytes);
-          int4* cp = reinterpret_cast<int4*>(smem + (size_t)stage * p.stage_bytes + p.a_bytes + p.gc_off);
-          const int total = 3 * p.CGo * p.KS;
-          for (int i = et; i < total; i += 128) {
-            const int uu = i % p.KS;
-            const int cgo = (i / p.KS) % p.CGo;
-            const int kw = i / (p.KS * p.CGo);
-            cp[(kw * ngo + cgo) * p.KS + uu] = raw[cgo * p.RRg + uu + delta - kw];
-          }
-          fence_proxy_async_smem();
-          mbar_arrive(&ready[stage]);
-          if (++stage == p.stages) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
     const int q = warp & 3;
     const int kidx = blockIdx.x / p.n_mtgroups;
     mbar_wait(&tfull, 0);
@@ -1702,7 +1647,7 @@ struct WgPlan {
   size_t ws_main, ws_bias;
 };
 
-int g_force_runs = -1, g_force_ks = 0, g_force_mpu = 0, g_force_fold = 0;  // fold: opt-in (staging-bound, see DESIGN)
+int g_force_runs = -1, g_force_ks = 0, g_force_mpu = 0;  // tools/tune_wgrad.py overrides
 
 int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
   WgParams& p = pl.p;
@@ -1735,13 +1680,7 @@ int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
   const int mpu_max = p.mt_per_unit;
   const int ks_run = min(256, ((p.Wp - 2) / 16) * 16);
   int best_mpu = 0, best_ks = 0, best_runs = 0;
-  // kw folded into N (three shifted gy copies, N = 3*Nc) whenever it fits an MMA
-  const int fold = (p.gwide && 3 * p.Nc <= 256 && g_force_fold > 0) ? 1 : 0;
-  auto g_region = [&](int KS) -> uint32_t {  // gy bytes per stage (raw box [+ shifted copies])
-    if (fold) {
-      const uint32_t raw = ((uint32_t)p.CGo * (KS + 16) * 16 + 1023) & ~1023u;
-      return raw + 3u * (uint32_t)(p.Nc / 8) * KS * 16;
-    }
+  auto g_region = [&](int KS) -> uint32_t {  // gy bytes per stage (Nc/8 group slots)
     return (uint32_t)(p.Nc / 8) * (KS + 8) * 16;
   };
   auto fits = [&](int runs, int KS, int mpu) {
@@ -1774,20 +1713,17 @@ int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
   p.mt_per_unit = best_mpu;
   p.KS = best_ks;
   p.runs = best_runs;
-  p.fold = fold;
   p.RR = p.KS + 8;
-  p.RRg = p.KS + 16;
   p.runs_alloc = (16 * p.mt_per_unit + 2) / 3 + 2;
   // TMA tensor destinations (the gy box) must be 128-byte aligned: keep every region 1 KB aligned
   p.a_bytes = ((p.runs ? (uint32_t)p.runs_alloc * 3 * p.Wp * 16 : (uint32_t)p.mt_per_unit * 16 * p.RR * 16) + 1023) & ~1023u;
-  p.g_bytes = (uint32_t)p.CGo * (fold ? p.RRg : p.RR) * 16;
-  p.gc_off = fold ? (((uint32_t)p.CGo * p.RRg * 16 + 1023) & ~1023u) : 0;
+  p.g_bytes = (uint32_t)p.CGo * p.RR * 16;
   p.stage_bytes = (p.a_bytes + g_region(p.KS) + 1023) & ~1023u;
   p.stages = kSmemBudget / (int)p.stage_bytes;
   if (p.stages > kMaxStages) p.stages = kMaxStages;
   VM_REQUIRE(p.stages >= 2 && p.mt_per_unit >= 1, VM_E_UNSUPPORTED, "vm_conv3d_wgrad_tc: stage does not fit");
   p.n_mtgroups = (p.MT + p.mt_per_unit - 1) / p.mt_per_unit;
-  const int64_t anchors = (int64_t)D * p.P + 2;  // + kw shift of the folded B operand
+  const int64_t anchors = (int64_t)D * p.P;
   p.stages_total = (int)((anchors + p.KS - 1) / p.KS);
   int nsm = vm_num_sms(0);
   if (nsm <= 0) nsm = 148;
@@ -1797,7 +1733,7 @@ int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
   if (p.spk < 4) p.spk = 4;
   p.ksplit = (p.stages_total + p.spk - 1) / p.spk;
   p.units = p.n_mtgroups * B * p.ksplit;
-  p.idesc = make_idesc_bf16(128, p.fold ? 3 * p.Nc : p.Nc, true, true);
+  p.idesc = make_idesc_bf16(128, p.Nc, true, true);
   p.grid = p.units;
   if (p.grid > nsm) p.grid = (nsm / p.n_mtgroups) * p.n_mtgroups;  // CTA keeps one M-tile group
   if (p.grid < p.n_mtgroups) p.grid = p.n_mtgroups;
@@ -1839,7 +1775,6 @@ int make_group_map(CUtensorMap* m, const void* base, int64_t bstride, int CG, in
 }
 }  // namespace
 
-extern "C" void vm_debug_force_wgrad_fold(int fold) { g_force_fold = fold; }
 
 extern "C" void vm_debug_force_wgrad_plan(int runs, int ks, int mpu) {
   g_force_runs = runs;
@@ -1862,7 +1797,7 @@ extern "C" int vm_debug_wgrad_plan(int B, int Cin, int Cout, int D, int H, int W
 // (3*Nc > 144 or TMEM, rows narrower than 34, or no double-buffered stage fits).
 static bool plan_wgrad_kd(int B, int Cin, int Cout, int D, int H, int W, WkParams& p, size_t& ws) {
   p = WkParams{};
-  if (g_force_runs == 0 || g_force_fold > 0) return false;  // debug overrides select the old kernel
+  if (g_force_runs == 0) return false;  // debug override selects the general kernel
   p.B = B;
   p.Wp = W + 2;
   p.P = (H + 2) * p.Wp;
@@ -1974,12 +1909,12 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
   const int64_t gbs = gy_bstride ? gy_bstride : default_bstride(Cout, D, H, W, 1);
   const int64_t rows = (int64_t)(D + 2) * p.P;
   CUtensorMap gmap;
-  rc = p.gwide ? make_wide_map(&gmap, gy, gbs, p.CGo, rows, B, (p.fold ? p.RRg : p.RR) / 8, p.CGo)
+  rc = p.gwide ? make_wide_map(&gmap, gy, gbs, p.CGo, rows, B, p.RR / 8, p.CGo)
                : make_group_map(&gmap, gy, gbs, p.CGo, rows, B, p.RR, p.CGo);
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
   // compile-time M-tile count when every CTA holds the same number of tiles
-  const bool even = p.MT % p.mt_per_unit == 0 && !p.fold;
+  const bool even = p.MT % p.mt_per_unit == 0;
   auto kern = !even ? k_conv_wgrad_tc<0>
             : p.mt_per_unit == 1 ? k_conv_wgrad_tc<1>
             : p.mt_per_unit == 2 ? k_conv_wgrad_tc<2>

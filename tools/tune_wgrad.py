@@ -12,8 +12,7 @@ for cin, cout, e in shapes:
     x.storage.normal_(); g.storage.normal_()
     gw = torch.zeros(27 * cin * cout, device="cuda"); gb = torch.zeros(cout, device="cuda")
     res = []
-    for fold in (0, 1):
-      lib.vm_debug_force_wgrad_fold(fold)
+    for fold in (0,):  # (the kw-folded variant was removed; kept as a 1-element loop)
       for runs in (0, 1):
           for ks in (64, 128, 192, 256):
               for mpu in range(1, 10):
@@ -35,7 +34,6 @@ for cin, cout, e in shapes:
                       _lib.call("vm_conv3d_wgrad_tc", *args)
                   e1.record(); torch.cuda.synchronize()
                   res.append((round(e0.elapsed_time(e1) / 5 * 1e3, 1), "fold%d" % fold, runs, ks, mpu, pl["stages"]))
-    lib.vm_debug_force_wgrad_fold(-1)
     lib.vm_debug_force_wgrad_plan(-1, 0, 0)
     out = (ctypes.c_int * 12)(); lib.vm_debug_wgrad_plan(1, cin, cout, e, e, e, out)
     pl = dict(zip(names, list(out)))
