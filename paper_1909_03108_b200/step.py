@@ -139,6 +139,7 @@ class UNetStep:
         self.total_voxels = float(self.global_batch * int(np.prod(self.global_shape)))
         self._rec = None
         self.packer = None  # halo pack/unpack backend (None: the CUDA box kernels)
+        self.overlap_wgrad = True  # weight gradients on a side stream, concurrent with dgrad
         self._build_buffers(params)
 
     # ------------------------------------------------------------------ setup
@@ -553,12 +554,25 @@ class UNetStep:
         # head grads: [C*ncls] kernel (DHWIO with k=1) then [ncls] bias — contiguous in the flat buffer
         h.gw.copy_(self.hgrad[: h.nk])
         h.gb.copy_(self.hgrad[h.nk :])
+        # wgrad(x, g) and dgrad(g) of a conv are independent: the weight gradients run on a
+        # side stream (joined before the gradient all-reduce), which fills the SMs the small
+        # deep-level kernels leave idle.  With a halo, the exchange writes g's margins, which
+        # wgrad reads as zeros, so it waits for that layer's wgrad.
+        main = torch.cuda.current_stream()
+        side = self._side_stream() if self.overlap_wgrad else None
         for n in reversed(self.graph.nodes):
             if n.op == "conv" and n.k == 3:
                 L = self.by_id[n.id]
                 x = self.out[n.inputs[0]]
                 gp = self.gpre[n.id]
-                self._wgrad(x, L, gp)
+                if side is not None:
+                    side.wait_stream(main)
+                    with torch.cuda.stream(side):
+                        self._wgrad(x, L, gp)
+                    if self.has_halo:
+                        main.wait_stream(side)
+                else:
+                    self._wgrad(x, L, gp)
                 src = n.inputs[0]
                 if src == "input":
                     continue
@@ -599,6 +613,14 @@ class UNetStep:
                 self._k("pool_bwd", n.id, 0, nb, "vm_maxpool2_bwd", self.dt, x.p(), x.bstride, gpool.p(),
                         gpool.bstride, add.p() if add else None, add.bstride if add else 0, dst.p(), dst.bstride,
                         self.B, x.C, x.D, x.H, x.W, 1)
+
+        if side is not None:
+            main.wait_stream(side)
+
+    def _side_stream(self):
+        if getattr(self, "_wg_stream", None) is None:
+            self._wg_stream = torch.cuda.Stream(device=self.device)
+        return self._wg_stream
 
     def all_reduce_grads(self):
         if self.ctx is not None and self.ctx.mesh.worker_count > 1:
