@@ -13,8 +13,9 @@ buf = torch.zeros(148 * 8, dtype=torch.int64, device='cuda')
 lib.vm_debug_set_fwd_probe.argtypes = [ctypes.c_void_p]
 lib.vm_debug_set_sweep_mode.argtypes = [ctypes.c_int]
 MODES = [int(v) for v in sys.argv[1:]] or [0]
-for (ci, co, e, mode) in [(ci, co, e, m) for m in MODES for (ci, co, e) in [(16, 16, 128), (48, 16, 128)]]:
-    lib.vm_debug_set_sweep_mode(mode)
+for (ci, co, e, mode) in [(ci, co, e, m) for m in MODES for (ci, co, e) in [(16, 16, 128), (48, 16, 128)]] + [(16, 16, 128, 'dgrad')]:
+    dgrad = mode == 'dgrad'
+    lib.vm_debug_set_sweep_mode(0 if dgrad else mode)
     x = Slab(1, ci, e, e, e, torch.bfloat16, 'cuda')
     y = Slab(1, co, e, e, e, torch.bfloat16, 'cuda')
     x.storage.normal_()
@@ -29,8 +30,12 @@ for (ci, co, e, mode) in [(ci, co, e, m) for m in MODES for (ci, co, e) in [(16,
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        _lib.call("vm_conv3d_fwd_tc", x.p(), x.bstride, _lib.ptr(wp), _lib.ptr(b), y.p(), y.bstride, None, 0, 1, ci,
-                  co, e, e, e, 1, st)
+        if dgrad:  # masked, no bias (the dgrad epilogue)
+            _lib.call("vm_conv3d_fwd_tc", x.p(), x.bstride, _lib.ptr(wp), _lib.ptr(b), y.p(), y.bstride, y.p(),
+                      y.bstride, 1, ci, co, e, e, e, 2 | 4, st)
+        else:
+            _lib.call("vm_conv3d_fwd_tc", x.p(), x.bstride, _lib.ptr(wp), _lib.ptr(b), y.p(), y.bstride, None, 0, 1,
+                      ci, co, e, e, e, 1, st)
         e1.record()
         torch.cuda.synchronize()
     lib.vm_debug_set_fwd_probe(None)
