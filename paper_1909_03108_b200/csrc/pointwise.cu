@@ -42,14 +42,14 @@ template <> struct V8<__nv_bfloat16> {
 
 // 32-bit index math: every launch checks that its index space fits (vm_fits32); 64-bit
 // division costs ~4x the instructions and these kernels are issue-bound at HBM speed
-__device__ __forceinline__ void decompose(uint32_t v, int D, int H, int W, int& b, int& d, int& h,
-                                          int& w) {
-  w = (int)(v % (uint32_t)W);
-  uint32_t r = v / (uint32_t)W;
-  h = (int)(r % (uint32_t)H);
-  r /= (uint32_t)H;
-  d = (int)(r % (uint32_t)D);
-  b = (int)(r / (uint32_t)D);
+__device__ __forceinline__ void decompose(uint32_t v, const Slab& s, int& b, int& d, int& h, int& w) {
+  const uint32_t q1 = fastdiv(v, (uint32_t)s.W, s.mW);
+  w = (int)(v - q1 * (uint32_t)s.W);
+  const uint32_t q2 = fastdiv(q1, (uint32_t)s.H, s.mH);
+  h = (int)(q1 - q2 * (uint32_t)s.H);
+  const uint32_t q3 = fastdiv(q2, (uint32_t)s.D, s.mD);
+  d = (int)(q2 - q3 * (uint32_t)s.D);
+  b = (int)q3;
 }
 __device__ __forceinline__ int split_cg(int64_t i, int64_t nvox, uint32_t& v) {
   const uint32_t i32 = (uint32_t)i, n32 = (uint32_t)nvox;
@@ -69,7 +69,7 @@ __global__ void k_maxpool_fwd(const T* __restrict__ x, Slab gx, T* __restrict__ 
     uint32_t v32;
     int cg = split_cg(i, nvox, v32);
     int b, d, h, w;
-    decompose(v32, gy.D, gy.H, gy.W, b, d, h, w);
+    decompose(v32, gy, b, d, h, w);
     float best[8];
     for (int cell = 0; cell < 8; ++cell) {  // (dz, dy, dx) scan order, ops.py:149-154
       float v[8];
@@ -93,7 +93,7 @@ __global__ void k_maxpool_bwd(const T* __restrict__ x, Slab gx, const T* __restr
     uint32_t v32;
     int cg = split_cg(i, nvox, v32);
     int b, d, h, w;
-    decompose(v32, go.D, go.H, go.W, b, d, h, w);
+    decompose(v32, go, b, d, h, w);
     // pass 1: argmax per channel (first max wins); pass 2 re-reads the 2x2x2 cell (L1/L2
     // hits) for the ReLU mask instead of holding 64 values in registers
     int arg[8];
@@ -142,7 +142,7 @@ __global__ void k_upsample_fwd(const T* __restrict__ x, Slab gx, T* __restrict__
     uint32_t v32;
     int cg = split_cg(i, nvox, v32);
     int b, d, h, w;
-    decompose(v32, gy.D, gy.H, gy.W, b, d, h, w);
+    decompose(v32, gy, b, d, h, w);
     const T* src = x + gx.at(b, cg, d >> 1, h >> 1, w >> 1);
     T* dst = y + gy.at(b, cg, d, h, w);
     *reinterpret_cast<int4*>(dst) = __ldg(reinterpret_cast<const int4*>(src));
@@ -160,7 +160,7 @@ __global__ void k_upsample_bwd(const T* __restrict__ gy, Slab sgy, const T* __re
     uint32_t v32;
     int cg = split_cg(i, nvox, v32);
     int b, d, h, w;
-    decompose(v32, sgx.D, sgx.H, sgx.W, b, d, h, w);
+    decompose(v32, sgx, b, d, h, w);
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int cell = 0; cell < 8; ++cell) {
@@ -189,7 +189,7 @@ __global__ void k_relu_mask(const T* __restrict__ g, Slab sg, const T* __restric
     uint32_t v32;
     int cg = split_cg(i, nvox, v32);
     int b, d, h, w;
-    decompose(v32, sg.D, sg.H, sg.W, b, d, h, w);
+    decompose(v32, sg, b, d, h, w);
     float v[8], mv[8];
     V8<T>::ld(g + sg.at(b, cg, d, h, w), v);
     V8<T>::ld(mask + sm.at(b, cg, d, h, w), mv);
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_head_fwd(const T* __restrict__
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvox;
        v += (int64_t)gridDim.x * blockDim.x) {
     int b, d, h, w;
-    decompose((uint32_t)v, sy.D, sy.H, sy.W, b, d, h, w);
+    decompose((uint32_t)v, sy, b, d, h, w);
     float lg[kMaxCls], p[kMaxCls];
     head_logits(y, sy, b, d, h, w, sW, sb, C, ncls, lg);
     softmax_n(lg, ncls, p);
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_head_bwd(
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvox;
          v += (int64_t)gridDim.x * blockDim.x) {
       int b, d, h, w;
-      decompose((uint32_t)v, sy.D, sy.H, sy.W, b, d, h, w);
+      decompose((uint32_t)v, sy, b, d, h, w);
       float lg[kMaxCls], p[kMaxCls], gp[kMaxCls], gl[kMaxCls];
       head_logits(y, sy, b, d, h, w, sW, sb, C, ncls, lg);
       softmax_n(lg, ncls, p);
@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_fwd_fixed(
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvox;
        v += (int64_t)gridDim.x * blockDim.x) {
     int b, d, h, w;
-    decompose((uint32_t)v, sy.D, sy.H, sy.W, b, d, h, w);
+    decompose((uint32_t)v, sy, b, d, h, w);
     float lg[NC];
 #pragma unroll
     for (int k = 0; k < NC; ++k) lg[k] = sb[k];
@@ -404,18 +404,18 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_fwd_fixed(
     float p[NC], ssum = 0.f;
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
-      p[k] = expf(lg[k] - m);
+      p[k] = __expf(lg[k] - m);
       ssum += p[k];
     }
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
-      p[k] = p[k] / ssum;
+      p[k] = __fdividef(p[k], ssum);
       const float g = onehot[v * NC + k];
       if (probs) probs[v * NC + k] = p[k];
       st[k] += p[k] * g;
       st[NC + k] += p[k];
       st[2 * NC + k] += g;
-      st[3 * NC] += -logf(fmaxf(p[k], clamp)) * g;
+      st[3 * NC] += -__logf(fmaxf(p[k], clamp)) * g;
     }
   }
 #pragma unroll
@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_fixed(
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvox;
        v += (int64_t)gridDim.x * blockDim.x) {
     int b, d, h, w;
-    decompose((uint32_t)v, sy.D, sy.H, sy.W, b, d, h, w);
+    decompose((uint32_t)v, sy, b, d, h, w);
     float yv[C];
     const T* base = y + sy.at(b, 0, d, h, w);
 #pragma unroll
@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_grp(
   for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < nvox * TPV; gi += gridDim.x * blockDim.x) {
     const uint32_t v = gi / TPV;
     int b, d, h, w;
-    decompose(v, sy.D, sy.H, sy.W, b, d, h, w);
+    decompose(v, sy, b, d, h, w);
     float yv[8];
     V8<T>::ld(y + sy.at(b, cg, d, h, w), yv);
     float lg[NC];
@@ -680,7 +680,7 @@ __global__ void k_sgd_apply(float* __restrict__ p, float* __restrict__ v, const 
 
 using namespace vm;
 
-#define SLAB(bs, C, D, H, W) Slab{(bs) ? (bs) : default_bstride((C), (D), (H), (W), 1), ((C) + 7) / 8, (D), (H), (W), 1}
+#define SLAB(bs, C, D, H, W) make_slab((bs) ? (bs) : default_bstride((C), (D), (H), (W), 1), ((C) + 7) / 8, (D), (H), (W), 1)
 
 #define DISPATCH_T(dtype, NAME, ...)                                  \
   do {                                                                \

@@ -61,6 +61,9 @@ template <> struct Cvt<__nv_bfloat16> {
 struct Slab {
   int64_t bstride;  // elements between samples
   int CG, D, H, W, m;
+  // floor(2^32 / d) + 1 for W, H, D: voxel-index decomposition by multiply-high instead of
+  // runtime division (the HBM-bound kernels are issue-bound otherwise); set by make_slab()
+  uint32_t mW = 0, mH = 0, mD = 0;
   __host__ __device__ int Dp() const { return D + 2 * m; }
   __host__ __device__ int Hp() const { return H + 2 * m; }
   __host__ __device__ int Wp() const { return W + 2 * m; }
@@ -70,6 +73,21 @@ struct Slab {
     return b * bstride + cg * plane() + ((((int64_t)(d + m) * Hp()) + (h + m)) * Wp() + (w + m)) * 8;
   }
 };
+
+inline uint32_t fastdiv_magic(uint32_t d) { return (uint32_t)(0x100000000ULL / d) + 1u; }
+// q = n / d for n < 2^31, d < 2^16: multiply-high estimate plus one correction step
+__device__ __forceinline__ uint32_t fastdiv(uint32_t n, uint32_t d, uint32_t magic) {
+  uint32_t q = __umulhi(n, magic);
+  if (q * d > n) --q;
+  return q;
+}
+inline Slab make_slab(int64_t bstride, int CG, int D, int H, int W, int m) {
+  Slab s{bstride, CG, D, H, W, m};
+  s.mW = fastdiv_magic((uint32_t)W);
+  s.mH = fastdiv_magic((uint32_t)H);
+  s.mD = fastdiv_magic((uint32_t)D);
+  return s;
+}
 
 size_t bias_grad_ws_bytes(int64_t nvox, int Cout);
 int bias_grad_bf16(const void* gy, int64_t gy_bstride, float* gb, float* ws, int B, int Cout, int D,
