@@ -199,9 +199,10 @@ struct FwdParams {
 // MB (tiles per unit) is a template parameter so that the MMA issue loop is straight-line
 // code: measured on B200, a runtime-bounded issue loop costs 1.5x in MMA throughput for
 // N = 128 (tools/probes/probe_pipe.cu).
-template <int MB>
+template <int MB, bool DBG>  // DBG: cycle probes (tools/dbg_fwd_probe.py)
 __global__ void __launch_bounds__(320, 1)
     k_conv_fwd_tc(const FwdParams p) {
+  auto clk = []() -> long long { return DBG ? (long long)clock64() : 0LL; };
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ float sbias[1024];
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
@@ -259,23 +260,23 @@ __global__ void __launch_bounds__(320, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    long long t_wait_tmem = 0, t_wait_full = 0, t_start = clock64();
+    long long t_wait_tmem = 0, t_wait_full = 0, t_start = clk();
     int stage = 0;
     uint32_t phase = 0;
     int ab = 0;
     uint32_t aphase = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      long long tw0 = clock64();
+      long long tw0 = clk();
       mbar_wait(&tempty[ab], aphase ^ 1);
-      t_wait_tmem += clock64() - tw0;
+      t_wait_tmem += clk() - tw0;
       tc_fence_after();
       for (int s = 0; s < nstage_k; ++s) {
         const int kc = s / 3;
         const int ng = (kc * 2 + 1 < p.CG) ? 2 : 1;
         const int aset = s % p.nacc;  // consecutive stages feed different accumulators
-        long long tf0 = clock64();
+        long long tf0 = clk();
         mbar_wait(&full[stage], phase);
-        t_wait_full += clock64() - tf0;
+        t_wait_full += clk() - tf0;
         tc_fence_after();
         if (elect_one()) {
           const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes);
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
     if (p.dbg && lane == 0) {
-      p.dbg[blockIdx.x * 4 + 0] = clock64() - t_start;
+      p.dbg[blockIdx.x * 4 + 0] = clk() - t_start;
       p.dbg[blockIdx.x * 4 + 1] = t_wait_tmem;
       p.dbg[blockIdx.x * 4 + 2] = t_wait_full;
     }
@@ -340,9 +341,9 @@ __global__ void __launch_bounds__(320, 1)
       const int a0 = mb * p.MB * 128;
       const bf16* mbase = p.mask + b * p.m_bstride;
       bf16* ybase = p.y + b * p.y_bstride;
-      long long te0 = clock64();
+      long long te0 = clk();
       mbar_wait(&tfull[ab], aphase);
-      t_epi_wait += clock64() - te0;
+      t_epi_wait += clk() - te0;
       tc_fence_after();
       for (int i = half; i < p.MB; i += 2) {
         const int a = a0 + i * 128 + q * 32 + lane;
@@ -1138,9 +1139,10 @@ struct WkParams {
   long long* dbg;  // optional cycle probes [gridDim][8] (vm_debug_set_fwd_probe)
 };
 
-template <int NMT>  // M-tiles of this CTA (compile-time: straight-line MMA issue)
+template <int NMT, bool DBG>  // M-tiles of this CTA (straight-line MMA issue); DBG: cycle probes
 __global__ void __launch_bounds__(192, 1)
     k_conv_wgrad_kd(const __grid_constant__ CUtensorMap gmap, const WkParams p) {
+  auto clk = []() -> long long { return DBG ? (long long)clock64() : 0LL; };
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages], tfull;
   __shared__ uint32_t tslot;
@@ -1197,9 +1199,9 @@ __global__ void __launch_bounds__(192, 1)
         const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
         const bf16* xb = p.x + b * p.x_bstride;
         for (int s = s0; s < s1; ++s) {
-          const long long tw = clock64();
+          const long long tw = clk();
           mbar_wait(&empty[stage], phase ^ 1);
-          t_pe += clock64() - tw;
+          t_pe += clk() - tw;
           mbar_arrive_expect_tx(&full[stage], tx);
           for (int j = 0; j < p.ksub; ++j) {  // ksub consecutive K chunks per stage
             const int k0 = (s * p.ksub + j) * p.KS;
@@ -1225,15 +1227,15 @@ __global__ void __launch_bounds__(192, 1)
     uint32_t phase = 0;
     bool started = false;
     const uint32_t id_last = last64 ? p.idesc64 : p.idesc;
-    const long long t0 = clock64();
+    const long long t0 = clk();
     long long t_fu = 0, t_is = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       const int ks = (u / p.ngroups) % p.ksplit;
       const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
       for (int s = s0; s < s1; ++s) {
-        const long long tf = clock64();
+        const long long tf = clk();
         mbar_wait(&full[stage], phase);
-        const long long tf1 = clock64();
+        const long long tf1 = clk();
         t_fu += tf1 - tf;
         tc_fence_after();
         if (elect_one()) {
@@ -1266,7 +1268,7 @@ __global__ void __launch_bounds__(192, 1)
           mma_commit(&empty[stage]);
         }
         __syncwarp();
-        t_is += clock64() - tf1;
+        t_is += clk() - tf1;
         started = true;
         if (++stage == p.stages) {
           stage = 0;
@@ -1277,7 +1279,7 @@ __global__ void __launch_bounds__(192, 1)
     if (elect_one()) mma_commit(&tfull);
     __syncwarp();
     if (p.dbg && lane == 0) {
-      p.dbg[blockIdx.x * 8 + 0] = clock64() - t0;
+      p.dbg[blockIdx.x * 8 + 0] = clk() - t0;
       p.dbg[blockIdx.x * 8 + 2] = t_fu;
       p.dbg[blockIdx.x * 8 + 3] = t_is;
     }
@@ -1625,15 +1627,16 @@ extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wp
   const size_t smem = (size_t)p.stages * p.stage_bytes;
   int grid = p.units < nsm ? p.units : nsm;
   void (*kern)(const FwdParams) = nullptr;
+  const bool dbg = p.dbg != nullptr;
   switch (p.MB) {
-    case 1: kern = k_conv_fwd_tc<1>; break;
-    case 2: kern = k_conv_fwd_tc<2>; break;
-    case 3: kern = k_conv_fwd_tc<3>; break;
-    case 4: kern = k_conv_fwd_tc<4>; break;
-    case 5: kern = k_conv_fwd_tc<5>; break;
-    case 6: kern = k_conv_fwd_tc<6>; break;
-    case 7: kern = k_conv_fwd_tc<7>; break;
-    default: kern = k_conv_fwd_tc<8>; break;
+    case 1: kern = dbg ? k_conv_fwd_tc<1, true> : k_conv_fwd_tc<1, false>; break;
+    case 2: kern = dbg ? k_conv_fwd_tc<2, true> : k_conv_fwd_tc<2, false>; break;
+    case 3: kern = dbg ? k_conv_fwd_tc<3, true> : k_conv_fwd_tc<3, false>; break;
+    case 4: kern = dbg ? k_conv_fwd_tc<4, true> : k_conv_fwd_tc<4, false>; break;
+    case 5: kern = dbg ? k_conv_fwd_tc<5, true> : k_conv_fwd_tc<5, false>; break;
+    case 6: kern = dbg ? k_conv_fwd_tc<6, true> : k_conv_fwd_tc<6, false>; break;
+    case 7: kern = dbg ? k_conv_fwd_tc<7, true> : k_conv_fwd_tc<7, false>; break;
+    default: kern = dbg ? k_conv_fwd_tc<8, true> : k_conv_fwd_tc<8, false>; break;
   }
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<grid, 320, smem, as_stream(stream)>>>(p);
@@ -1887,7 +1890,10 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
       int rc = make_group_map(&gmap, gy, gbs, pk.CGo, pk.rows, B, pk.KS, pk.CGo);
       if (rc) return rc;
       cudaStream_t st = as_stream(stream);
-      auto kern = pk.mt_per_unit == 3 ? k_conv_wgrad_kd<3> : pk.mt_per_unit == 2 ? k_conv_wgrad_kd<2> : k_conv_wgrad_kd<1>;
+      const bool dbg = pk.dbg != nullptr;
+      auto kern = pk.mt_per_unit == 3 ? (dbg ? k_conv_wgrad_kd<3, true> : k_conv_wgrad_kd<3, false>)
+                : pk.mt_per_unit == 2 ? (dbg ? k_conv_wgrad_kd<2, true> : k_conv_wgrad_kd<2, false>)
+                                      : (dbg ? k_conv_wgrad_kd<1, true> : k_conv_wgrad_kd<1, false>);
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
       kern<<<pk.grid, 192, (size_t)pk.stages * pk.stage_bytes, st>>>(gmap, pk);
       rc = launch_status("vm_conv3d_wgrad_tc (kd)");
