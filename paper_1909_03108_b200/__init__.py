@@ -17,6 +17,20 @@ from .mesh import DeviceMesh, WorkerContext, create_mesh
 from .sharding import Layout, ShardedTensor, TensorSpec, gather, shard
 from .halo import HaloSpec, PaddedBlock, exchange_byte_count, halo_exchange, halo_exchange_backward
 from .unet import LayerGraph, UNetConfig, build, init_params, recipe_for_resolution
+from .ops import (
+    ConvParams,
+    ConvTape,
+    concat_channels,
+    conv3d_backward,
+    conv3d_forward,
+    maxpool2_backward,
+    maxpool2_forward,
+    relu,
+    relu_backward,
+    softmax_channels,
+    upsample2_backward,
+    upsample2_forward,
+)
 from .training import (
     BatchSource,
     LossWeights,
@@ -70,4 +84,16 @@ __all__ = [
     "load_checkpoint",
     "save_checkpoint",
     "train_loop",
+    "ConvParams",
+    "ConvTape",
+    "concat_channels",
+    "conv3d_backward",
+    "conv3d_forward",
+    "maxpool2_backward",
+    "maxpool2_forward",
+    "relu",
+    "relu_backward",
+    "softmax_channels",
+    "upsample2_backward",
+    "upsample2_forward",
 ]

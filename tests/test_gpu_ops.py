@@ -1,0 +1,79 @@
+"""The reference's per-op API on ShardedTensors (ops.py:221-333), GPU kernels vs the f64
+oracle, on a 2x2 threads mesh on one GPU (halo exchange included)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1909_03108_b200 as vm
+from oracle import voxmesh_oracle as O
+from tests.helpers import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+AXES = [("mx", 2), ("my", 2)]
+LAYOUT = {"x": "mx", "y": "my"}
+
+
+def _mesh():
+    return vm.create_mesh(AXES, backend="threads")
+
+
+@pytest.mark.parametrize("dtype,tol", [("f32", 1e-5), ("bf16", 1e-2)])
+def test_conv3d_forward_backward(dtype, tol):
+    rng = np.random.default_rng(7)
+    B, D, H, W, ci, co = 1, 8, 8, 12, 16, 24
+    x = rng.standard_normal((B, D, H, W, ci)).astype(np.float32)
+    k = (rng.uniform(-1, 1, (3, 3, 3, ci, co)) / np.sqrt(27 * ci)).astype(np.float32)
+    b = (0.1 * rng.standard_normal(co)).astype(np.float32)
+    g = rng.standard_normal((B, D, H, W, co)).astype(np.float32)
+    if dtype == "bf16":
+        x, k, g = O.bf16_round(x), O.bf16_round(k), O.bf16_round(g)
+    with _mesh() as mesh:
+        spec = vm.TensorSpec((("batch", B), ("x", D), ("y", H), ("z", W), ("c", ci)), dtype)
+        gspec = vm.TensorSpec((("batch", B), ("x", D), ("y", H), ("z", W), ("c", co)), dtype)
+        xs = vm.shard(x, spec, vm.Layout(LAYOUT), mesh)
+        params = vm.ConvParams(k, b)
+        y, tape = vm.conv3d_forward(xs, params)
+        gx, gk, gb = vm.conv3d_backward(vm.shard(g, gspec, vm.Layout(LAYOUT), mesh), tape)
+        yg = vm.gather(y).astype(np.float64)
+        gxg = vm.gather(gx).astype(np.float64)
+        with pytest.raises(vm.VoxmeshError):
+            vm.conv3d_backward(vm.shard(g, gspec, vm.Layout(LAYOUT), mesh), tape)
+    ry = O.conv3d_dense(x.astype(np.float64), k.astype(np.float64), b.astype(np.float64))
+    rgx, rgk, rgb = O.conv3d_dense_backward(g.astype(np.float64), x.astype(np.float64), k.astype(np.float64))
+    assert rel_l2(yg, ry) <= tol
+    assert rel_l2(gxg, rgx) <= tol
+    assert rel_l2(gk, rgk) <= tol and rel_l2(gb, rgb) <= tol
+    assert gk.shape == k.shape and gb.shape == b.shape
+
+
+def test_shard_local_ops_match_oracle():
+    rng = np.random.default_rng(3)
+    B, D, H, W, C = 1, 8, 8, 8, 8
+    x = rng.standard_normal((B, D, H, W, C)).astype(np.float32)
+    with _mesh() as mesh:
+        lay = vm.Layout(LAYOUT)
+        spec = vm.TensorSpec((("batch", B), ("x", D), ("y", H), ("z", W), ("c", C)), "f32")
+        xs = vm.shard(x, spec, lay, mesh)
+        p, ptape = vm.maxpool2_forward(xs)
+        pg = rng.standard_normal(p.spec.shape).astype(np.float32)
+        gin = vm.maxpool2_backward(vm.shard(pg, p.spec, lay, mesh), ptape)
+        up = vm.upsample2_forward(p)
+        upb = vm.upsample2_backward(vm.shard(x, spec, lay, mesh))
+        r = vm.relu(xs)
+        rb = vm.relu_backward(vm.shard(pg.repeat(2, 1).repeat(2, 2).repeat(2, 3), spec, lay, mesh), xs)
+        cat = vm.concat_channels(xs, r)
+        sm = vm.softmax_channels(xs)
+        got = {n: vm.gather(t) for n, t in (("p", p), ("gin", gin), ("up", up), ("upb", upb), ("r", r),
+                                              ("rb", rb), ("cat", cat), ("sm", sm))}
+    rp, idx = O.maxpool2_dense(x)
+    assert np.array_equal(got["p"], rp)
+    assert np.array_equal(got["gin"], O.maxpool2_dense_backward(pg, idx, x.shape))
+    assert np.array_equal(got["up"], O.upsample2_dense(rp))
+    assert rel_l2(got["upb"], O.upsample2_dense_backward(x.astype(np.float64))) <= 1e-6
+    assert np.array_equal(got["r"], np.maximum(x, 0))
+    gfull = pg.repeat(2, 1).repeat(2, 2).repeat(2, 3)
+    assert np.array_equal(got["rb"], np.where(x > 0, gfull, 0))
+    assert np.array_equal(got["cat"], np.concatenate([x, np.maximum(x, 0)], axis=-1))
+    assert rel_l2(got["sm"], O.softmax_dense(x.astype(np.float64))) <= 1e-6

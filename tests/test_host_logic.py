@@ -232,3 +232,14 @@ def test_no_cpu_fallback_without_cuda():
         pytest.skip("CUDA present")
     with pytest.raises(vm.VoxmeshError, match="no CPU fallback"):
         _lib.stream_ptr()
+
+
+def test_conv_params_validation():
+    k = np.zeros((3, 3, 3, 2, 4), np.float32)
+    vm.ConvParams(k, np.zeros(4, np.float32))
+    with pytest.raises(vm.HaloError):
+        vm.ConvParams(np.zeros((2, 2, 2, 2, 4), np.float32), np.zeros(4, np.float32))
+    with pytest.raises(vm.VoxmeshError):
+        vm.ConvParams(k, np.zeros(3, np.float32))
+    with pytest.raises(vm.VoxmeshError):
+        vm.ConvParams(np.full((3, 3, 3, 2, 4), np.nan, np.float32), np.zeros(4, np.float32))
