@@ -33,6 +33,10 @@ from .ops import (
 )
 from .training import (
     BatchSource,
+    combined_loss,
+    cross_entropy_loss,
+    one_hot,
+    soft_dice_loss,
     LossWeights,
     TrainConfig,
     TrainState,
@@ -84,6 +88,10 @@ __all__ = [
     "load_checkpoint",
     "save_checkpoint",
     "train_loop",
+    "combined_loss",
+    "cross_entropy_loss",
+    "one_hot",
+    "soft_dice_loss",
     "ConvParams",
     "ConvTape",
     "concat_channels",

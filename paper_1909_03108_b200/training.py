@@ -79,6 +79,60 @@ class TrainState:
     history: list = field(default_factory=list)
 
 
+# ---------------------------------------------------------------------------- losses
+def one_hot(labels, num_classes, dtype=np.float32):
+    """training.py:68-69."""
+    return np.eye(num_classes, dtype=dtype)[labels]
+
+
+def _loss_stats_block(p, g, clamp):
+    """Per-class [sum p*g, sum p, sum g] plus the summed NLL of one device block, accumulated
+    in float64 on the GPU (training.py:77-92)."""
+    import torch
+
+    c = p.shape[-1]
+    pd = p.reshape(-1, c).double()
+    gd = g.reshape(-1, c).double()
+    nll = -(torch.log(torch.clamp_min(pd, clamp)) * gd).sum()
+    return torch.cat([(pd * gd).sum(0), pd.sum(0), gd.sum(0), nll[None]]).cpu().numpy()
+
+
+def soft_dice_from_stats(stats, num_classes, dice_classes, eps=DICE_EPS):
+    """1 - mean over ``dice_classes`` of (2*sum(p*g)+eps)/(sum(p)+sum(g)+eps) (training.py:95-100)."""
+    c = num_classes
+    pg, ps, gs = stats[0:c], stats[c : 2 * c], stats[2 * c : 3 * c]
+    ratios = [(2.0 * float(pg[k]) + eps) / (float(ps[k]) + float(gs[k]) + eps) for k in dice_classes]
+    return 1.0 - sum(ratios) / len(ratios)
+
+
+def _reduced_stats(probs, labels_onehot, clamp, tag):
+    def fn(ctx, p, g):
+        return ctx.all_reduce_sum(_loss_stats_block(p, g, clamp), tag=tag)
+
+    return next(r for r in probs.mesh.run(fn, per_worker=(probs.blocks, labels_onehot.blocks)) if r is not None)
+
+
+def soft_dice_loss(probs, labels_onehot, dice_classes=(1, 2)):
+    """Distributed soft-Dice loss over sharded probabilities and one-hot labels (training.py:130-139)."""
+    stats = _reduced_stats(probs, labels_onehot, 1e-12, "dice-stats")
+    return soft_dice_from_stats(stats, probs.spec.extent("c"), dice_classes)
+
+
+def cross_entropy_loss(probs, labels_onehot, clamp=1e-12):
+    """Distributed mean per-voxel negative log-likelihood (training.py:142-152)."""
+    c = probs.spec.extent("c")
+    stats = _reduced_stats(probs, labels_onehot, clamp, "ce-stats")
+    voxels = int(np.prod([e for n, e in probs.spec.dims if n != "c"]))
+    return float(stats[3 * c]) / voxels
+
+
+def combined_loss(weights, probs, labels_onehot, dice_classes=(1, 2)):
+    """training.py:155-158."""
+    return weights.dice * soft_dice_loss(probs, labels_onehot, dice_classes) + weights.ce * cross_entropy_loss(
+        probs, labels_onehot
+    )
+
+
 # ---------------------------------------------------------------------------- metrics
 def hard_dice(pred_mask, gt_mask):
     """2|A∩B| / (|A|+|B|); 1 when both are empty, 0 when only one is (training.py:166-175)."""

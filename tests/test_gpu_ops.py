@@ -77,3 +77,22 @@ def test_shard_local_ops_match_oracle():
     assert np.array_equal(got["rb"], np.where(x > 0, gfull, 0))
     assert np.array_equal(got["cat"], np.concatenate([x, np.maximum(x, 0)], axis=-1))
     assert rel_l2(got["sm"], O.softmax_dense(x.astype(np.float64))) <= 1e-6
+
+
+def test_distributed_losses_match_oracle():
+    rng = np.random.default_rng(11)
+    B, D, H, W, C = 1, 8, 8, 8, 3
+    logits = rng.standard_normal((B, D, H, W, C))
+    probs = (np.exp(logits) / np.exp(logits).sum(-1, keepdims=True)).astype(np.float32)
+    lab = rng.integers(0, 3, (B, D, H, W))
+    oh = vm.one_hot(lab, 3)
+    with _mesh() as mesh:
+        lay = vm.Layout(LAYOUT)
+        spec = vm.TensorSpec((("batch", B), ("x", D), ("y", H), ("z", W), ("c", C)), "f32")
+        ps, gs = vm.shard(probs, spec, lay, mesh), vm.shard(oh, spec, lay, mesh)
+        dice = vm.soft_dice_loss(ps, gs)
+        ce = vm.cross_entropy_loss(ps, gs)
+        comb = vm.combined_loss(vm.LossWeights(), ps, gs)
+    st = O.loss_stats(probs.astype(np.float64), oh.astype(np.float64))
+    rcomb, rdice, rce = O.losses_from_stats(st, 3, D * H * W)
+    assert abs(dice - rdice) <= 1e-9 and abs(ce - rce) <= 1e-9 and abs(comb - rcomb) <= 1e-9
