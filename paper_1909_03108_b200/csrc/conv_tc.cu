@@ -1030,21 +1030,29 @@ __global__ void __launch_bounds__(352, 1)
       }
       bf16* yb = p.y + b * p.y_bstride;
       const bf16* mb = p.mask + b * p.m_bstride;
+      int4 mkn[TPT][GPT];
+#pragma unroll
+      for (int k = 0; k < TPT; ++k)
+#pragma unroll
+        for (int gi = 0; gi < GPT; ++gi) mkn[k][gi] = make_int4(0, 0, 0, 0);
       for (int rel = 0; rel < L; ++rel, ++n) {
         const int o = o0 + rel - 2;
         const bool live = o >= o0 && o < o1 && !(p.xmode & 1);  // warp-uniform (tcgen05.ld is .aligned)
-        // dgrad: the ReLU mask of this plane is fetched before waiting for the accumulator
+        // dgrad: the ReLU mask of the NEXT plane is fetched one plane ahead (mkn), so its HBM
+        // latency overlaps this plane's TMEM drain instead of sitting in front of it
         int4 mk[TPT][GPT];
         if (p.flags & VM_CONV_MASK) {
 #pragma unroll
           for (int k = 0; k < TPT; ++k)
 #pragma unroll
             for (int gi = 0; gi < GPT; ++gi) {
+              mk[k][gi] = mkn[k][gi];
               const int g = g_lo + gi * g_step;
-              mk[k][gi] = make_int4(0, 0, 0, 0);
-              if (live && valid[k] && g < ngrp && g * 8 < p.Cout)
-                mk[k][gi] = __ldg(reinterpret_cast<const int4*>(mb + g * p.plane8 + orow0[k] * 8 +
-                                                                (int64_t)o * p.P * 8));
+              const int on = o + 1;
+              mkn[k][gi] = make_int4(0, 0, 0, 0);
+              if (on >= o0 && on < o1 && valid[k] && g < ngrp && g * 8 < p.Cout)
+                mkn[k][gi] = __ldg(reinterpret_cast<const int4*>(mb + g * p.plane8 + orow0[k] * 8 +
+                                                                 (int64_t)on * p.P * 8));
             }
         }
         const long long tw = clk();
