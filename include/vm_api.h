@@ -55,6 +55,9 @@ const char* vm_last_error(void);
 int vm_num_sms(int device);
 /* number of kernels this library has launched in this process (bench bookkeeping) */
 long long vm_launch_count(void);
+/* programmatic dependent launch between this library's kernels (default from $VM_PDL);
+ * returns the previous setting */
+int vm_set_pdl(int on);
 
 /* ------------------------------------------------------------------ boxes / halo
  * Generic 5-D box copies on a dense tensor of shape dims[5] (dims[4] contiguous,

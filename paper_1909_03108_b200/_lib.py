@@ -34,6 +34,7 @@ _SIGS = {
     "vm_last_error": (ctypes.c_char_p, []),
     "vm_num_sms": (_I, [_I]),
     "vm_launch_count": (ctypes.c_longlong, []),
+    "vm_set_pdl": (ctypes.c_int, [ctypes.c_int]),
     "vm_box_pack": (_I, [_P, _c_i64p, _I, _c_i64p, _c_i64p, _P, _P]),
     "vm_box_unpack": (_I, [_P, _c_i64p, _I, _c_i64p, _c_i64p, _P, _P]),
     "vm_box_unpack_add": (_I, [_P, _c_i64p, _I, _c_i64p, _c_i64p, _P, _P]),

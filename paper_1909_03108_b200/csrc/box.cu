@@ -7,6 +7,7 @@
 // :176-186 (adjoint: receive and add); sharding.py:189-209 (block copies).
 #include <cstdarg>
 #include <atomic>
+#include <cstdlib>
 
 #include "vm_common.cuh"
 
@@ -22,6 +23,15 @@ void set_error(const char* fmt, ...) {
 
 static std::atomic<long long> g_launches{0};
 void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+static int g_pdl = -1;  // -1: from $VM_PDL (default on)
+bool pdl_enabled() {
+  if (g_pdl < 0) {
+    const char* e = getenv("VM_PDL");
+    g_pdl = (e && e[0] == '1') ? 1 : 0;
+  }
+  return g_pdl != 0;
+}
 
 static int g_num_sms = -1;
 static int num_sms() {
@@ -160,6 +170,11 @@ extern "C" const char* vm_error_string(int code) {
 extern "C" const char* vm_last_error(void) { return g_err; }
 
 extern "C" long long vm_launch_count(void) { return g_launches.load(); }
+extern "C" int vm_set_pdl(int on) {
+  const int prev = vm::pdl_enabled() ? 1 : 0;
+  vm::g_pdl = on ? 1 : 0;
+  return prev;
+}
 
 extern "C" int vm_num_sms(int device) {
   int n = 0;

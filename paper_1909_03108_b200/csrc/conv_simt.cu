@@ -263,10 +263,24 @@ __global__ void k_bias_finalize(const float* __restrict__ wsb, float* __restrict
 }
 
 size_t bias_grad_ws_bytes(int64_t nvox, int Cout) {
-  int64_t s = nvox / 4096;  // ~16 voxels per thread per block
+  int64_t s = nvox / 1024;  // ~4 voxels per thread per block
   if (s < 1) s = 1;
   if (s > 512) s = 512;
   return (size_t)s * ((Cout + 7) / 8) * 8 * sizeof(float);
+}
+
+// Per-split partial sums of gy over interior voxels: ws[ns][CGo*8] (bf16 slab); the caller
+// reduces the ns splits in order.
+int bias_grad_partial_bf16(const void* gy, int64_t gy_bstride, float* ws, int B, int Cout, int D, int H, int W,
+                           cudaStream_t st, int* nsplit) {
+  Slab gg{gy_bstride ? gy_bstride : default_bstride(Cout, D, H, W, 1), (Cout + 7) / 8, D, H, W, 1};
+  int64_t nvox = (int64_t)B * D * H * W;
+  int ns = (int)(bias_grad_ws_bytes(nvox, Cout) / (gg.CG * 8 * sizeof(float)));
+  int64_t chunk = (nvox + ns - 1) / ns;
+  k_bias_grad_partial<__nv_bfloat16><<<dim3(ns, gg.CG), 256, 0, st>>>((const __nv_bfloat16*)gy, gg, ws, B,
+                                                                      gg.CG, chunk);
+  *nsplit = ns;
+  return launch_status("bias_grad_partial_bf16");
 }
 
 // gb[co] = sum over interior voxels of gy[.., co], deterministic (bf16 slab)

@@ -224,6 +224,8 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = tslot;
+  pdl_wait();
+  pdl_trigger();
   const int nstage_k = p.KC * 3;
 
   if (warp == 0) {
@@ -655,64 +657,89 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc<512>(tbase);
 }
 
-// Fixed-order reduction of nk K-split partials for 32 consecutive elements e per block:
-// warp w sums k = w, w+8, ... (two interleaved chains), then warp 0 adds the 8 warp sums in
-// order.  Deterministic, coalesced (a warp reads 128 contiguous bytes per k), and 8 warps per
-// 32 elements keep enough loads in flight (one thread per element with a 148-deep serial loop
-// ran at ~0.6 TB/s).
-__device__ __forceinline__ float ksplit_sum(const float* __restrict__ ws, int64_t E, int nk, int64_t e,
-                                            float (*red)[32]) {
+// Fixed-order reduction of the nk K-split partials ws[k][mt][kw][n][m] (E floats per split)
+// and scatter into gw[t][ci][co] (+ gb from the ones slot or from bias partials).
+//   KD = false (k_conv_wgrad_tc): n = co, slot g = mt*16 + m/8 -> (kd*3 + kh, cg);
+//   KD = true  (k_conv_wgrad_kd): n = kd*Nc + co, slot g = cg*3 + kh.
+// A block owns a 32 (m) x 8 (n) tile.  Warp w sums splits k = w, w+8, ... for all 8 n
+// (8 independent coalesced 128-byte loads per k), the 8 warp sums are added in warp order
+// through shared memory (deterministic), and the tile is written transposed so that 8
+// consecutive co (32 bytes) go out together; the old one-warp-per-32-elements version wrote
+// 4-byte scattered stores with a Cout stride.  Blocks past the tiles reduce the separate
+// bias partials wsb[nsb][CGo*8] when the ones slot does not exist.
+template <bool KD>
+__global__ void __launch_bounds__(256) k_wgrad_finalize_tiles(const float* __restrict__ ws, float* __restrict__ gw,
+                                                             float* __restrict__ gb, int nk, int MT, int Nc, int CG,
+                                                             int Cin, int Cout, int ones_slot, int runs,
+                                                             const float* __restrict__ wsb, int nsb, int CGo) {
+  __shared__ float part[8][8][33];
+  const int N = KD ? 3 * Nc : Nc;
+  const int n8 = N / 8;
+  const int64_t E = (int64_t)MT * 3 * N * 128;
+  const int ntiles = MT * 3 * n8 * 4;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float s0 = 0.f, s1 = 0.f;
-  if (e < E) {
-    int k = w;
-    for (; k + 8 < nk; k += 16) {
-      s0 += ws[(int64_t)k * E + e];
-      s1 += ws[(int64_t)(k + 8) * E + e];
+  if ((int)blockIdx.x >= ntiles) {
+    const int co = ((int)blockIdx.x - ntiles) * 256 + threadIdx.x;
+    if (co < Cout) {
+      float sb = 0.f;
+      for (int sp = 0; sp < nsb; ++sp) sb += wsb[(int64_t)sp * CGo * 8 + co];
+      gb[co] = sb;
     }
-    if (k < nk) s0 += ws[(int64_t)k * E + e];
+    return;
   }
-  red[w][lane] = s0 + s1;
-  __syncthreads();
-  float t = 0.f;
-  if (w == 0) {
+  int r = blockIdx.x;
+  const int mq = r % 4;
+  r /= 4;
+  const int nb = r % n8;
+  r /= n8;
+  const int kw = r % 3;
+  const int mt = r / 3;
+  const int64_t e0 = (((int64_t)(mt * 3 + kw) * N + nb * 8) * 128) + mq * 32 + lane;
+  float acc[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) t += red[i][lane];
+  for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+  for (int k = w; k < nk; k += 8) {
+    const float* src = ws + (int64_t)k * E + e0;
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = src[j * 128];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] += v[j];
   }
-  return t;  // valid in warp 0
-}
-
-// Fixed-order reduction of the K-split partials, one thread per partial element
-// (coalesced over m): ws[k][mt][kw][co][m] -> gw[t][ci][co] with t = (kd*3+kh)*3 + kw,
-// g = mt*16 + m/8 = (kd*3+kh)*CG + ci/8; the ones slot (kw = 0, m%8 = 0) gives gb.
-__global__ void __launch_bounds__(256) k_wgrad_tc_finalize(const float* __restrict__ ws, float* __restrict__ gw,
-                                                          float* __restrict__ gb, int nk, int MT, int Nc, int CG,
-                                                          int Cin, int Cout, int ones_slot, int runs) {
-  __shared__ float red[8][32];
-  const int64_t E = (int64_t)MT * 3 * Nc * 128;
-  const int64_t e = blockIdx.x * 32LL + (threadIdx.x & 31);
-  const float s = ksplit_sum(ws, E, nk, e, red);
-  if (threadIdx.x >= 32 || e >= E) return;
-  const int m = e % 128;
-  const int co = (e / 128) % Nc;
-  const int kw = (e / (128 * Nc)) % 3;
-  const int mt = (int)(e / (384LL * Nc));
+#pragma unroll
+  for (int j = 0; j < 8; ++j) part[w][j][lane] = acc[j];
+  __syncthreads();
+  // thread -> (m = mq*32 + mm, n = nb*8 + j): 8 consecutive n per m
+  const int j = threadIdx.x & 7, mm = threadIdx.x >> 3;
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += part[i][j][mm];
+  const int m = mq * 32 + mm;
+  const int n = nb * 8 + j;
   const int g = mt * 16 + m / 8;
+  int kd, co, pp, cgi;
+  bool is_w, is_b;
+  if (KD) {
+    kd = n / Nc;
+    co = n % Nc;
+    cgi = g / 3;
+    pp = kd * 3 + g % 3;
+    is_w = g < 3 * CG && cgi * 8 + m % 8 < Cin;
+    is_b = g == ones_slot && kw == 0 && kd == 0 && m % 8 == 0;
+  } else {
+    co = n;
+    pp = runs ? ((g / 3) / CG) * 3 + g % 3 : g / CG;
+    cgi = runs ? (g / 3) % CG : g % CG;
+    is_w = g < 9 * CG && cgi * 8 + m % 8 < Cin;
+    is_b = g == ones_slot && kw == 0 && m % 8 == 0;
+  }
   if (co >= Cout) return;
-  // slot -> (kd*3 + kh, channel group)
-  const int pp = runs ? ((g / 3) / CG) * 3 + g % 3 : g / CG;
-  const int cgi = runs ? (g / 3) % CG : g % CG;
-  const bool is_w = g < 9 * CG && cgi * 8 + m % 8 < Cin;
-  const bool is_b = g == ones_slot && kw == 0 && m % 8 == 0;
   if (is_w) {
-    const int ci = cgi * 8 + m % 8;
-    gw[((int64_t)(pp * 3 + kw) * Cin + ci) * Cout + co] = s;
+    gw[((int64_t)(pp * 3 + kw) * Cin + cgi * 8 + m % 8) * Cout + co] = s;
   } else if (is_b) {
     gb[co] = s;
   }
 }
-
-
 
 // ------------------------------------------------------------------ forward, kd stacked along N
 // Thin outputs (Nc <= 48): the three kd taps are stacked along N (N = 3*Nc, rows ordered
@@ -785,6 +812,8 @@ __global__ void __launch_bounds__(352, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = tslot;
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 0) {
     // ===================== producer: resident weights, then one stage per (plane, K chunk)
@@ -1318,36 +1347,6 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc<512>(tbase);
 }
 
-// ws[k][mt][kw][n = kd*Nc + co][m] -> gw[t][ci][co], t = (kd*3 + kh)*3 + kw, slot
-// g = mt*16 + m/8 = cg*3 + kh; the ones slot (kd = 0, kw = 0, m%8 = 0) gives gb.
-__global__ void __launch_bounds__(256) k_wgrad_kd_finalize(const float* __restrict__ ws, float* __restrict__ gw,
-                                                          float* __restrict__ gb, int nk, int MT, int Nc, int CG,
-                                                          int Cin, int Cout, int ones_slot) {
-  __shared__ float red[8][32];
-  const int N3 = 3 * Nc;
-  const int64_t E = (int64_t)MT * 3 * N3 * 128;
-  const int64_t e = blockIdx.x * 32LL + (threadIdx.x & 31);
-  const float s = ksplit_sum(ws, E, nk, e, red);
-  if (threadIdx.x >= 32 || e >= E) return;
-  const int m = e % 128;
-  const int n = (e / 128) % N3;
-  const int kw = (e / (128 * N3)) % 3;
-  const int mt = (int)(e / (384LL * N3));
-  const int g = mt * 16 + m / 8;
-  const int kd = n / Nc, co = n % Nc;
-  if (co >= Cout) return;
-  const int cg = g / 3, kh = g % 3;
-  const bool is_w = g < 3 * CG && cg * 8 + m % 8 < Cin;
-  const bool is_b = g == ones_slot && kw == 0 && kd == 0 && m % 8 == 0;
-  if (is_w) {
-    const int ci = cg * 8 + m % 8;
-    gw[((int64_t)((kd * 3 + kh) * 3 + kw) * Cin + ci) * Cout + co] = s;
-  } else if (is_b) {
-    gb[co] = s;
-  }
-}
-
-
 }  // namespace vm
 
 using namespace vm;
@@ -1528,7 +1527,7 @@ static int launch_sweep(const FwdParams& f, int nsm, void* stream) {
             : p.MB == 2 ? (dbg ? k_conv_fwd_sweep<2, true> : k_conv_fwd_sweep<2, false>)
                         : (dbg ? k_conv_fwd_sweep<1, true> : k_conv_fwd_sweep<1, false>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<grid, 352, smem, as_stream(stream)>>>(p);
+  launch_pdl(kern, grid, 352, smem, as_stream(stream), p);
   return launch_status("vm_conv3d_fwd_tc (sweep)");
 }
 
@@ -1647,7 +1646,7 @@ extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wp
     default: kern = dbg ? k_conv_fwd_tc<8, true> : k_conv_fwd_tc<8, false>; break;
   }
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<grid, 320, smem, as_stream(stream)>>>(p);
+  launch_pdl(kern, grid, 320, smem, as_stream(stream), p);
   return launch_status("vm_conv3d_fwd_tc");
 }
 
@@ -1907,9 +1906,9 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
       rc = launch_status("vm_conv3d_wgrad_tc (kd)");
       if (rc) return rc;
       const int nk = pk.grid / pk.ngroups;
-      const int64_t E = (int64_t)pk.MT * 9 * pk.Nc * 128;
-      k_wgrad_kd_finalize<<<(unsigned)((E + 31) / 32), 256, 0, st>>>(pk.ws, gw, gb, nk, pk.MT, pk.Nc, pk.CG, Cin,
-                                                                    Cout, pk.ones_slot);
+      const int ntiles = pk.MT * 3 * (3 * pk.Nc / 8) * 4;
+      k_wgrad_finalize_tiles<true><<<ntiles, 256, 0, st>>>(pk.ws, gw, gb, nk, pk.MT, pk.Nc, pk.CG, Cin, Cout,
+                                                          pk.ones_slot, 0, nullptr, 0, 0);
       return launch_status("vm_conv3d_wgrad_tc (kd) finalize");
     }
   }
@@ -1940,11 +1939,17 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
   rc = launch_status("vm_conv3d_wgrad_tc");
   if (rc) return rc;
   const int nk = p.grid / p.n_mtgroups;
-  const int64_t E = (int64_t)p.MT * 3 * p.Nc * 128;
-  k_wgrad_tc_finalize<<<(unsigned)((E + 31) / 32), 256, 0, st>>>(p.ws, gw, gb, nk, p.MT, p.Nc, p.CG, Cin, Cout,
-                                                                 p.ones_slot, p.runs);
-  rc = launch_status("vm_conv3d_wgrad_tc finalize");
-  if (rc || p.ones_slot >= 0) return rc;
+  // without a ones slot the bias gradient comes from separate partials, reduced by the
+  // finalize's extra blocks
+  int nsb = 0;
   float* wsb = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ((pl.ws_main + 255) / 256) * 256);
-  return bias_grad_bf16(gy, gbs, gb, wsb, B, Cout, D, H, W, st);
+  if (p.ones_slot < 0) {
+    rc = bias_grad_partial_bf16(gy, gbs, wsb, B, Cout, D, H, W, st, &nsb);
+    if (rc) return rc;
+  }
+  const int ntiles = p.MT * 3 * (p.Nc / 8) * 4;
+  const int nbias = p.ones_slot < 0 ? (Cout + 255) / 256 : 0;
+  k_wgrad_finalize_tiles<false><<<ntiles + nbias, 256, 0, st>>>(p.ws, gw, gb, nk, p.MT, p.Nc, p.CG, Cin, Cout,
+                                                               p.ones_slot, p.runs, wsb, nsb, (Cout + 7) / 8);
+  return launch_status("vm_conv3d_wgrad_tc finalize");
 }

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <utility>
 
 #include "../../include/vm_api.h"
 
@@ -36,6 +37,35 @@ inline int launch_status(const char* what, int nlaunch = 1) {
 }
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Programmatic dependent launch (PDL).  A kernel launched by launch_pdl may start while the
+// previous kernel on its stream is still running: it must call pdl_wait() before its first
+// global-memory access (read or write), and calls pdl_trigger() to let the NEXT kernel's
+// CTAs be scheduled (prologue: barrier init, TMEM alloc) before this one finishes.  Both are
+// no-ops when the kernel was launched without the attribute.  vm_set_pdl(0) turns it off.
+bool pdl_enabled();
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  if (!pdl_enabled()) {
+    kern<<<grid, block, smem, st>>>(std::forward<Args>(args)...);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 inline int dtype_bytes(int dt) {
   switch (dt) {
@@ -92,6 +122,8 @@ inline Slab make_slab(int64_t bstride, int CG, int D, int H, int W, int m) {
 size_t bias_grad_ws_bytes(int64_t nvox, int Cout);
 int bias_grad_bf16(const void* gy, int64_t gy_bstride, float* gb, float* ws, int B, int Cout, int D,
                    int H, int W, cudaStream_t st);
+int bias_grad_partial_bf16(const void* gy, int64_t gy_bstride, float* ws, int B, int Cout, int D, int H, int W,
+                           cudaStream_t st, int* nsplit);
 
 inline int64_t default_bstride(int C, int D, int H, int W, int m) {
   return (int64_t)((C + 7) / 8) * (D + 2 * m) * (H + 2 * m) * (W + 2 * m) * 8;

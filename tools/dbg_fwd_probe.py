@@ -5,7 +5,8 @@ from paper_1909_03108_b200.step import Slab
 lib=_lib.load()
 buf=torch.zeros(148*8, dtype=torch.int64, device='cuda')
 lib.vm_debug_set_fwd_probe.argtypes=[ctypes.c_void_p]
-for (ci,co,e,fl) in [(ci,co,e,fl) for fl in (1, 1|(1<<16), 1|(1<<17)) for (ci,co,e) in [(64,64,32),(128,128,16)]]:
+SHAPES=[(64,64,32),(128,128,16),(64,128,16),(192,64,32),(96,32,64)]
+for (ci,co,e,fl) in [(ci,co,e,1) for (ci,co,e) in SHAPES]:
     x=Slab(1,ci,e,e,e,torch.bfloat16,'cuda'); y=Slab(1,co,e,e,e,torch.bfloat16,'cuda'); x.storage.normal_()
     w=torch.randn(27*ci*co,device='cuda')*0.05; b=torch.zeros(co,device='cuda')
     wp=torch.empty(_lib.call_size("vm_packed_weights_bytes",ci,co)//2,dtype=torch.bfloat16,device='cuda')
