@@ -476,12 +476,17 @@ struct WgParams {
   uint32_t stage_bytes;
   uint32_t idesc;
   float* ws;        // [kidx = b*ksplit + ks][MT][3][Nc][128]
+  long long* dbg;   // optional cycle probes [gridDim][8] (vm_debug_set_fwd_probe)
 };
 
-template <int NMT>  // > 0: M-tiles per CTA known at compile time (straight-line MMA issue); 0: runtime
+// NMT > 0: M-tiles per CTA, NKK > 0: K steps per stage (KS/16), known at compile time so the
+// MMA issue is straight-line code (a runtime-bounded issue loop costs 1.5-2x on B200); 0: runtime.
+template <int NMT, int NKK>
 __global__ void __launch_bounds__(192, 1)
     k_conv_wgrad_tc(const __grid_constant__ CUtensorMap gmap, const WgParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  const bool dbg = p.dbg != nullptr;
+  const long long t_entry = dbg ? (long long)clock64() : 0;
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages], tfull, tempty;
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -521,6 +526,7 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) {
     if (elect_one()) {
       tma_prefetch(&gmap);
+      long long t_pe = 0;
       int stage = 0;
       uint32_t phase = 0;
       int nvalid = 0;
@@ -540,7 +546,9 @@ __global__ void __launch_bounds__(192, 1)
         const bf16* xb = p.x + b * p.x_bstride;
         for (int s = s0; s < s1; ++s) {
           const int64_t k0 = (int64_t)s * p.KS;
+          const long long tw = dbg ? (long long)clock64() : 0;
           mbar_wait(&empty[stage], phase ^ 1);
+          if (dbg) t_pe += clock64() - tw;
           uint8_t* sA = smem + (size_t)stage * p.stage_bytes;
           uint8_t* sG = sA + p.a_bytes;
           mbar_arrive_expect_tx(&full[stage], tx);
@@ -571,6 +579,7 @@ __global__ void __launch_bounds__(192, 1)
           }
         }
       }
+      if (dbg) p.dbg[blockIdx.x * 8 + 5] = t_pe;
     }
   } else if (warp == 1) {
     // All units of this CTA share the M-tile group and cover disjoint K ranges: accumulate
@@ -579,11 +588,18 @@ __global__ void __launch_bounds__(192, 1)
     uint32_t phase = 0;
     const uint32_t sbo = GS;
     bool started = false;
+    const long long t_m0 = dbg ? (long long)clock64() : 0;
+    long long t_wf = 0, t_first = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       const int ks = (u / p.n_mtgroups) % p.ksplit;
       const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
       for (int s = s0; s < s1; ++s) {
+        const long long tw = dbg ? (long long)clock64() : 0;
         mbar_wait(&full[stage], phase);
+        if (dbg) {
+          const long long dt = clock64() - tw;
+          if (!started) t_first = dt; else t_wf += dt;
+        }
         tc_fence_after();
         if (elect_one()) {
           const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes);
@@ -591,11 +607,11 @@ __global__ void __launch_bounds__(192, 1)
           const uint64_t b0desc = make_sdesc(sG + (uint32_t)p.gdelta * 16, 128, (uint32_t)p.RR * 16);
           const uint64_t a0desc = make_sdesc(sA + (uint32_t)slot_shift * GS, 128, sbo);
           const uint32_t mstep = 16 * (GS >> 4);  // 16 slots, in 16-byte units
-          const int nkk = p.KS / 16;
+          const int nkk = NKK > 0 ? NKK : p.KS / 16;
           const uint32_t acc0 = started ? 1u : 0u;
-          if (NMT > 0) {
-#pragma unroll 4
-            for (int kk = 0; kk < nkk; ++kk) {
+          if (NMT > 0 && NKK > 0) {
+#pragma unroll
+            for (int kk = 0; kk < (NKK > 0 ? NKK : 1); ++kk) {
               const uint64_t bdesc = b0desc + (uint64_t)(kk * 16);
               const uint32_t acc = kk > 0 ? 1u : acc0;
 #pragma unroll
@@ -607,6 +623,7 @@ __global__ void __launch_bounds__(192, 1)
                 mma_bf16_ss(d + 2 * p.Nc, adesc + 2, bdesc, p.idesc, acc);
               }
             }
+          } else if (NMT > 0) {
           } else {
 #pragma unroll 1
             for (int kk = 0; kk < nkk; ++kk) {
@@ -634,6 +651,12 @@ __global__ void __launch_bounds__(192, 1)
     }
     if (elect_one()) mma_commit(&tfull);
     __syncwarp();
+    if (dbg && lane == 0) {
+      p.dbg[blockIdx.x * 8 + 0] = t_m0 - t_entry;
+      p.dbg[blockIdx.x * 8 + 1] = clock64() - t_m0;
+      p.dbg[blockIdx.x * 8 + 2] = t_first;
+      p.dbg[blockIdx.x * 8 + 3] = t_wf;
+    }
   } else {
     const int q = warp & 3;
     const int kidx = blockIdx.x / p.n_mtgroups;
@@ -651,6 +674,7 @@ __global__ void __launch_bounds__(192, 1)
           for (int e = 0; e < 16; ++e) dst[e * 128] = __uint_as_float(r[e]);
         }
     (void)tempty;
+    if (dbg && threadIdx.x == 64) p.dbg[blockIdx.x * 8 + 4] = clock64() - t_entry;
   }
   tc_fence_before();
   __syncthreads();
@@ -1176,10 +1200,15 @@ struct WkParams {
   long long* dbg;  // optional cycle probes [gridDim][8] (vm_debug_set_fwd_probe)
 };
 
-template <int NMT, bool DBG>  // M-tiles of this CTA (straight-line MMA issue); DBG: cycle probes
+// NMT: M-tiles of this CTA.  NKK > 0: K steps per chunk (KS/16), KSUB chunks per stage and
+// all three kw taps, known at compile time so the MMA issue is straight-line code (measured:
+// the runtime-bounded issue loop ran at ~39 cycles per M = 64, N = 48 MMA against 28);
+// NKK = 0: runtime bounds.  Cycle probes when p.dbg is set.
+template <int NMT, int NKK, int KSUB>
 __global__ void __launch_bounds__(192, 1)
     k_conv_wgrad_kd(const __grid_constant__ CUtensorMap gmap, const WkParams p) {
-  auto clk = []() -> long long { return DBG ? (long long)clock64() : 0LL; };
+  const bool DBG = p.dbg != nullptr;
+  auto clk = [DBG]() -> long long { return DBG ? (long long)clock64() : 0LL; };
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages], tfull;
   __shared__ uint32_t tslot;
@@ -1276,32 +1305,36 @@ __global__ void __launch_bounds__(192, 1)
         t_fu += tf1 - tf;
         tc_fence_after();
         if (elect_one()) {
-         for (int j = 0; j < p.ksub; ++j) {
-          const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes + (size_t)j * p.sub_bytes);
-          const uint32_t sG = sA + p.a_bytes;
-          // B: MN-major, N groups (kd, cgo) KS rows apart; A: MN-major slots GS apart
-          const uint64_t b0desc = make_sdesc(sG, 128, (uint32_t)p.KS * 16);
-          const uint64_t a0desc = make_sdesc(sA + (uint32_t)slot_shift * GS, 128, GS);
+          const int ksub = NKK > 0 ? KSUB : p.ksub;
+          const int nkk = NKK > 0 ? NKK : p.KS / 16;
+          const int nkw = NKK > 0 ? 3 : p.nkw;
+          const uint32_t sA0 = smem_u32(smem + (size_t)stage * p.stage_bytes);
           const uint32_t mstep = 16 * (GS >> 4);
-          const int nkk = p.KS / 16;
-          const uint32_t acc0 = (started || j > 0) ? 1u : 0u;
-#pragma unroll 4
-          for (int kk = 0; kk < nkk; ++kk) {
-            const uint64_t bdesc = b0desc + (uint64_t)(kk * 16);
-            const uint32_t acc = kk > 0 ? 1u : acc0;
 #pragma unroll
-            for (int m = 0; m < NMT; ++m) {
-              const uint64_t adesc = a0desc + (uint64_t)(m * mstep + kk * 16 + kw0);
-              const uint32_t d = tbase + (uint32_t)(m * p.nkw * N3);
-              const uint32_t id = m == NMT - 1 ? id_last : p.idesc;
-              mma_bf16_ss(d, adesc, bdesc, id, acc);
-              if (p.nkw == 3) {
-                mma_bf16_ss(d + N3, adesc + 1, bdesc, id, acc);
-                mma_bf16_ss(d + 2 * N3, adesc + 2, bdesc, id, acc);
+          for (int j = 0; j < ksub; ++j) {
+            const uint32_t sA = sA0 + (uint32_t)j * p.sub_bytes;
+            const uint32_t sG = sA + p.a_bytes;
+            // B: MN-major, N groups (kd, cgo) KS rows apart; A: MN-major slots GS apart
+            const uint64_t b0desc = make_sdesc(sG, 128, (uint32_t)p.KS * 16);
+            const uint64_t a0desc = make_sdesc(sA + (uint32_t)slot_shift * GS, 128, GS) + (uint64_t)kw0;
+            const uint32_t acc0 = (started || j > 0) ? 1u : 0u;
+#pragma unroll
+            for (int kk = 0; kk < nkk; ++kk) {
+              const uint64_t bdesc = b0desc + (uint64_t)(kk * 16);
+              const uint32_t acc = kk > 0 ? 1u : acc0;
+#pragma unroll
+              for (int m = 0; m < NMT; ++m) {
+                const uint64_t adesc = a0desc + (uint64_t)(m * mstep + kk * 16);
+                const uint32_t d = tbase + (uint32_t)(m * nkw * N3);
+                const uint32_t id = m == NMT - 1 ? id_last : p.idesc;
+                mma_bf16_ss(d, adesc, bdesc, id, acc);
+                if (nkw == 3) {
+                  mma_bf16_ss(d + N3, adesc + 1, bdesc, id, acc);
+                  mma_bf16_ss(d + 2 * N3, adesc + 2, bdesc, id, acc);
+                }
               }
             }
           }
-         }
           mma_commit(&empty[stage]);
         }
         __syncwarp();
@@ -1658,6 +1691,8 @@ struct WgPlan {
 };
 
 int g_force_runs = -1, g_force_ks = 0, g_force_mpu = 0;  // tools/tune_wgrad.py overrides
+int g_wg_min_spk = 2;  // minimum stages per K-split unit (vm_debug_set_wgrad_min_spk)
+int g_wk_runtime = 0;  // 1: force the runtime-bounded kd wgrad issue loop (A/B probe)
 
 int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
   WgParams& p = pl.p;
@@ -1737,10 +1772,12 @@ int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
   p.stages_total = (int)((anchors + p.KS - 1) / p.KS);
   int nsm = vm_num_sms(0);
   if (nsm <= 0) nsm = 148;
-  int want = (2 * nsm + p.n_mtgroups * B - 1) / (p.n_mtgroups * B);  // ~2 units per SM
+  // one unit per CTA (a second wave of units would double the slowest CTA's time): as many
+  // K splits as fit in one wave, at least g_wg_min_spk stages per unit (pipeline fill)
+  int want = nsm / (p.n_mtgroups * B);
   if (want < 1) want = 1;
   p.spk = (p.stages_total + want - 1) / want;
-  if (p.spk < 4) p.spk = 4;
+  if (p.spk < g_wg_min_spk) p.spk = g_wg_min_spk;
   p.ksplit = (p.stages_total + p.spk - 1) / p.spk;
   p.units = p.n_mtgroups * B * p.ksplit;
   p.idesc = make_idesc_bf16(128, p.Nc, true, true);
@@ -1785,6 +1822,10 @@ int make_group_map(CUtensorMap* m, const void* base, int64_t bstride, int CG, in
 }
 }  // namespace
 
+
+extern "C" void vm_debug_set_wgrad_kd_runtime(int v) { g_wk_runtime = v; }
+
+extern "C" void vm_debug_set_wgrad_min_spk(int v) { g_wg_min_spk = v > 0 ? v : 2; }
 
 extern "C" void vm_debug_force_wgrad_plan(int runs, int ks, int mpu) {
   g_force_runs = runs;
@@ -1898,9 +1939,22 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
       if (rc) return rc;
       cudaStream_t st = as_stream(stream);
       const bool dbg = pk.dbg != nullptr;
-      auto kern = pk.mt_per_unit == 3 ? (dbg ? k_conv_wgrad_kd<3, true> : k_conv_wgrad_kd<3, false>)
-                : pk.mt_per_unit == 2 ? (dbg ? k_conv_wgrad_kd<2, true> : k_conv_wgrad_kd<2, false>)
-                                      : (dbg ? k_conv_wgrad_kd<1, true> : k_conv_wgrad_kd<1, false>);
+      using WkKern = void (*)(const CUtensorMap, const WkParams);
+      // [NMT-1][variant]: 0 runtime, then (NKK, KSUB) = (2,1) (2,2) (4,1) (4,2) (8,1) (8,2)
+      static const WkKern table[3][7] = {
+          {k_conv_wgrad_kd<1, 0, 0>, k_conv_wgrad_kd<1, 2, 1>, k_conv_wgrad_kd<1, 2, 2>, k_conv_wgrad_kd<1, 4, 1>,
+           k_conv_wgrad_kd<1, 4, 2>, k_conv_wgrad_kd<1, 8, 1>, k_conv_wgrad_kd<1, 8, 2>},
+          {k_conv_wgrad_kd<2, 0, 0>, k_conv_wgrad_kd<2, 2, 1>, k_conv_wgrad_kd<2, 2, 2>, k_conv_wgrad_kd<2, 4, 1>,
+           k_conv_wgrad_kd<2, 4, 2>, k_conv_wgrad_kd<2, 8, 1>, k_conv_wgrad_kd<2, 8, 2>},
+          {k_conv_wgrad_kd<3, 0, 0>, k_conv_wgrad_kd<3, 2, 1>, k_conv_wgrad_kd<3, 2, 2>, k_conv_wgrad_kd<3, 4, 1>,
+           k_conv_wgrad_kd<3, 4, 2>, k_conv_wgrad_kd<3, 8, 1>, k_conv_wgrad_kd<3, 8, 2>},
+      };
+      const int nkk = pk.KS / 16;
+      int var = 0;
+      if (pk.nkw == 3 && (pk.ksub == 1 || pk.ksub == 2) && (nkk == 2 || nkk == 4 || nkk == 8) && !g_wk_runtime)
+        var = (nkk == 2 ? 1 : nkk == 4 ? 3 : 5) + (pk.ksub - 1);
+      auto kern = table[pk.mt_per_unit - 1][var];
+      (void)dbg;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
       kern<<<pk.grid, 192, (size_t)pk.stages * pk.stage_bytes, st>>>(gmap, pk);
       rc = launch_status("vm_conv3d_wgrad_tc (kd)");
@@ -1919,6 +1973,7 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
   p.x = static_cast<const bf16*>(x);
   p.x_bstride = x_bstride ? x_bstride : default_bstride(Cin, D, H, W, 1);
   p.ws = static_cast<float*>(ws);
+  p.dbg = g_fwd_dbg;
   const int64_t gbs = gy_bstride ? gy_bstride : default_bstride(Cout, D, H, W, 1);
   const int64_t rows = (int64_t)(D + 2) * p.P;
   CUtensorMap gmap;
@@ -1926,14 +1981,19 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
                : make_group_map(&gmap, gy, gbs, p.CGo, rows, B, p.RR, p.CGo);
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
-  // compile-time M-tile count when every CTA holds the same number of tiles
+  // compile-time M-tile count (when every CTA holds the same number of tiles) and K steps
   const bool even = p.MT % p.mt_per_unit == 0;
-  auto kern = !even ? k_conv_wgrad_tc<0>
-            : p.mt_per_unit == 1 ? k_conv_wgrad_tc<1>
-            : p.mt_per_unit == 2 ? k_conv_wgrad_tc<2>
-            : p.mt_per_unit == 3 ? k_conv_wgrad_tc<3>
-            : p.mt_per_unit == 4 ? k_conv_wgrad_tc<4>
-                                 : k_conv_wgrad_tc<0>;
+  const int nmt_t = even && p.mt_per_unit <= 4 ? p.mt_per_unit : 0;
+  const int nkk_t = (p.KS == 64 || p.KS == 128 || p.KS == 192 || p.KS == 256) ? p.KS / 16 : 0;
+  using WgKern = void (*)(const CUtensorMap, const WgParams);
+  static const WgKern table[5][5] = {
+      {k_conv_wgrad_tc<0, 0>, k_conv_wgrad_tc<0, 4>, k_conv_wgrad_tc<0, 8>, k_conv_wgrad_tc<0, 12>, k_conv_wgrad_tc<0, 16>},
+      {k_conv_wgrad_tc<1, 0>, k_conv_wgrad_tc<1, 4>, k_conv_wgrad_tc<1, 8>, k_conv_wgrad_tc<1, 12>, k_conv_wgrad_tc<1, 16>},
+      {k_conv_wgrad_tc<2, 0>, k_conv_wgrad_tc<2, 4>, k_conv_wgrad_tc<2, 8>, k_conv_wgrad_tc<2, 12>, k_conv_wgrad_tc<2, 16>},
+      {k_conv_wgrad_tc<3, 0>, k_conv_wgrad_tc<3, 4>, k_conv_wgrad_tc<3, 8>, k_conv_wgrad_tc<3, 12>, k_conv_wgrad_tc<3, 16>},
+      {k_conv_wgrad_tc<4, 0>, k_conv_wgrad_tc<4, 4>, k_conv_wgrad_tc<4, 8>, k_conv_wgrad_tc<4, 12>, k_conv_wgrad_tc<4, 16>},
+  };
+  auto kern = table[nmt_t][nkk_t / 4];
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
   kern<<<p.grid, 192, (size_t)p.stages * p.stage_bytes, st>>>(gmap, p);
   rc = launch_status("vm_conv3d_wgrad_tc");
