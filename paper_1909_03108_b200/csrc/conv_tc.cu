@@ -204,7 +204,6 @@ __global__ void __launch_bounds__(320, 1)
     k_conv_fwd_tc(const FwdParams p) {
   auto clk = []() -> long long { return DBG ? (long long)clock64() : 0LL; };
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ float sbias[1024];
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -327,10 +326,6 @@ __global__ void __launch_bounds__(320, 1)
     // warp w drains TMEM lane quarter (w & 3) of every other tile (parity (w-2)/4)
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
-    const int et = threadIdx.x - 64;  // 0..255
-    if (!(p.flags & VM_CONV_NOBIAS))
-      for (int c = et; c < p.Cout; c += 256) sbias[c] = p.bias[c];
-    asm volatile("bar.sync 1, 256;" ::: "memory");
     int ab = 0;
     uint32_t aphase = 0;
     long long t_epi_wait = 0;
@@ -402,7 +397,7 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
                 v[e] = __uint_as_float(r[jj * 8 + e]);
-                if (!(p.flags & VM_CONV_NOBIAS)) v[e] += (co0 + e < p.Cout) ? sbias[co0 + e] : 0.f;
+                if (!(p.flags & VM_CONV_NOBIAS)) v[e] += (co0 + e < p.Cout) ? __ldg(p.bias + co0 + e) : 0.f;
               }
               if (p.flags & VM_CONV_RELU) {
 #pragma unroll
@@ -690,12 +685,14 @@ __global__ void __launch_bounds__(192, 1)
 // through shared memory (deterministic), and the tile is written transposed so that 8
 // consecutive co (32 bytes) go out together; the old one-warp-per-32-elements version wrote
 // 4-byte scattered stores with a Cout stride.  Blocks past the tiles reduce the separate
-// bias partials wsb[nsb][CGo*8] when the ones slot does not exist.
+// bias partials wsb[nsb][CGo*8] when the ones slot does not exist.  ldo: row stride of gw
+// (the full Cout when this call covers a chunk of the output channels).
 template <bool KD>
 __global__ void __launch_bounds__(256) k_wgrad_finalize_tiles(const float* __restrict__ ws, float* __restrict__ gw,
                                                              float* __restrict__ gb, int nk, int MT, int Nc, int CG,
                                                              int Cin, int Cout, int ones_slot, int runs,
-                                                             const float* __restrict__ wsb, int nsb, int CGo) {
+                                                             const float* __restrict__ wsb, int nsb, int CGo,
+                                                             int ldo) {
   __shared__ float part[8][8][33];
   const int N = KD ? 3 * Nc : Nc;
   const int n8 = N / 8;
@@ -759,7 +756,7 @@ __global__ void __launch_bounds__(256) k_wgrad_finalize_tiles(const float* __res
   }
   if (co >= Cout) return;
   if (is_w) {
-    gw[((int64_t)(pp * 3 + kw) * Cin + cgi * 8 + m % 8) * Cout + co] = s;
+    gw[((int64_t)(pp * 3 + kw) * Cin + cgi * 8 + m % 8) * ldo + co] = s;
   } else if (is_b) {
     gb[co] = s;
   }
@@ -1602,7 +1599,6 @@ extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wp
   p.dbg = g_fwd_dbg;
   p.wp_magic = (uint32_t)(0x100000000ULL / (uint64_t)(W + 2)) + 1;
   p.hp_magic = (uint32_t)(0x100000000ULL / (uint64_t)(H + 2)) + 1;
-  VM_REQUIRE(Cout <= 1024, VM_E_UNSUPPORTED, "vm_conv3d_fwd_tc: Cout %d > 1024", Cout);
   p.x = static_cast<const bf16*>(x);
   p.x_bstride = x_bstride ? x_bstride : default_bstride(Cin, D, H, W, 1);
   VM_REQUIRE((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (p.x_bstride & 7) == 0, VM_E_ALIGN,
@@ -1910,7 +1906,13 @@ static bool plan_wgrad_kd(int B, int Cin, int Cout, int D, int H, int W, WkParam
   return true;
 }
 
+// Output channels per weight-gradient call: the accumulators of one M-tile are 3 kw x Nc
+// TMEM columns (<= 512), so wider layers (cfg3/cfg4: up to 512 -> 1024 channels) run as
+// chunks of 128 output channels; each chunk reads its own channel-group planes of gy.
+constexpr int kWgradMaxCout = 160, kWgradChunk = 128;
+
 extern "C" size_t vm_conv3d_wgrad_tc_ws(int B, int Cin, int Cout, int D, int H, int W) {
+  if (Cout > kWgradMaxCout) Cout = kWgradChunk;  // chunked (vm_conv3d_wgrad_tc): the widest chunk
   WkParams pk;
   size_t wsk = 0;
   if (plan_wgrad_kd(B, Cin, Cout, D, H, W, pk, wsk)) return wsk + 256;
@@ -1919,12 +1921,10 @@ extern "C" size_t vm_conv3d_wgrad_tc_ws(int B, int Cin, int Cout, int D, int H, 
   return pl.ws_main + pl.ws_bias + 256;
 }
 
-extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* gy,
-                                  int64_t gy_bstride, float* gw, float* gb, void* ws, int B, int Cin,
-                                  int Cout, int D, int H, int W, void* stream) {
-  VM_REQUIRE(x && gy && gw && gb && ws, VM_E_ARG, "vm_conv3d_wgrad_tc: null pointer");
-  VM_REQUIRE(B > 0 && Cin > 0 && Cout > 0 && D > 0 && H > 0 && W > 0, VM_E_SHAPE,
-             "vm_conv3d_wgrad_tc: bad shape");
+// One call of the weight-gradient kernels for Cout <= kWgradMaxCout output channels; gw rows
+// have stride ldo (>= Cout) so that a chunk of a wider layer writes its columns in place.
+static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_t gy_bstride, float* gw, float* gb,
+                        void* ws, int B, int Cin, int Cout, int D, int H, int W, int ldo, void* stream) {
   {
     WkParams pk;
     size_t wsk = 0;
@@ -1962,7 +1962,7 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
       const int nk = pk.grid / pk.ngroups;
       const int ntiles = pk.MT * 3 * (3 * pk.Nc / 8) * 4;
       k_wgrad_finalize_tiles<true><<<ntiles, 256, 0, st>>>(pk.ws, gw, gb, nk, pk.MT, pk.Nc, pk.CG, Cin, Cout,
-                                                          pk.ones_slot, 0, nullptr, 0, 0);
+                                                          pk.ones_slot, 0, nullptr, 0, 0, Cout);
       return launch_status("vm_conv3d_wgrad_tc (kd) finalize");
     }
   }
@@ -2010,6 +2010,24 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
   const int ntiles = p.MT * 3 * (p.Nc / 8) * 4;
   const int nbias = p.ones_slot < 0 ? (Cout + 255) / 256 : 0;
   k_wgrad_finalize_tiles<false><<<ntiles + nbias, 256, 0, st>>>(p.ws, gw, gb, nk, p.MT, p.Nc, p.CG, Cin, Cout,
-                                                               p.ones_slot, p.runs, wsb, nsb, (Cout + 7) / 8);
+                                                               p.ones_slot, p.runs, wsb, nsb, (Cout + 7) / 8, ldo);
   return launch_status("vm_conv3d_wgrad_tc finalize");
+}
+
+extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* gy,
+                                  int64_t gy_bstride, float* gw, float* gb, void* ws, int B, int Cin,
+                                  int Cout, int D, int H, int W, void* stream) {
+  VM_REQUIRE(x && gy && gw && gb && ws, VM_E_ARG, "vm_conv3d_wgrad_tc: null pointer");
+  VM_REQUIRE(B > 0 && Cin > 0 && Cout > 0 && D > 0 && H > 0 && W > 0, VM_E_SHAPE,
+             "vm_conv3d_wgrad_tc: bad shape");
+  const int64_t gbs = gy_bstride ? gy_bstride : default_bstride(Cout, D, H, W, 1);
+  if (Cout <= kWgradMaxCout) return wgrad_tc_one(x, x_bstride, gy, gbs, gw, gb, ws, B, Cin, Cout, D, H, W, Cout, stream);
+  const int64_t plane8 = (int64_t)(D + 2) * (H + 2) * (W + 2) * 8;
+  for (int co0 = 0; co0 < Cout; co0 += kWgradChunk) {
+    const int cc = min(kWgradChunk, Cout - co0);
+    const bf16* gyc = static_cast<const bf16*>(gy) + (int64_t)(co0 / 8) * plane8;
+    const int rc = wgrad_tc_one(x, x_bstride, gyc, gbs, gw + co0, gb + co0, ws, B, Cin, cc, D, H, W, Cout, stream);
+    if (rc) return rc;
+  }
+  return VM_OK;
 }

@@ -381,41 +381,59 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_fwd_fixed(
   float st[3 * NC + 1];
 #pragma unroll
   for (int k = 0; k < 3 * NC + 1; ++k) st[k] = 0.f;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvox;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    int b, d, h, w;
-    decompose((uint32_t)v, sy, b, d, h, w);
-    float lg[NC];
+  // U voxels per thread per iteration with every load issued first (loads in flight bound it)
+  constexpr int U = C <= 16 ? 2 : 1;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < nvox; v0 += U * stride) {
+    float yv[U][C], gk[U][NC];
+    bool ok[U];
 #pragma unroll
-    for (int k = 0; k < NC; ++k) lg[k] = sb[k];
-    const T* base = y + sy.at(b, 0, d, h, w);
+    for (int u = 0; u < U; ++u) {
+      const int64_t v = v0 + u * stride;
+      ok[u] = v < nvox;
+      int b, d, h, w;
+      decompose(ok[u] ? (uint32_t)v : 0u, sy, b, d, h, w);
+      const T* base = y + sy.at(b, 0, d, h, w);
 #pragma unroll
-    for (int cg = 0; cg < C / 8; ++cg) {
-      float yv[8];
-      V8<T>::ld(base + cg * sy.plane(), yv);
+      for (int cg = 0; cg < C / 8; ++cg) {
+        float t8[8];
+        V8<T>::ld(base + cg * sy.plane(), t8);
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < 8; ++j) yv[u][cg * 8 + j] = t8[j];
+      }
 #pragma unroll
-        for (int k = 0; k < NC; ++k) lg[k] = fmaf(yv[j], sW[(cg * 8 + j) * NC + k], lg[k]);
-    }
-    float m = lg[0];
-#pragma unroll
-    for (int k = 1; k < NC; ++k) m = fmaxf(m, lg[k]);
-    float p[NC], ssum = 0.f;
-#pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      p[k] = __expf(lg[k] - m);
-      ssum += p[k];
+      for (int k = 0; k < NC; ++k) gk[u][k] = ok[u] ? onehot[v * NC + k] : 0.f;
     }
 #pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      p[k] = __fdividef(p[k], ssum);
-      const float g = onehot[v * NC + k];
-      if (probs) probs[v * NC + k] = p[k];
-      st[k] += p[k] * g;
-      st[NC + k] += p[k];
-      st[2 * NC + k] += g;
-      st[3 * NC] += -__logf(fmaxf(p[k], clamp)) * g;
+    for (int u = 0; u < U; ++u) {
+      if (!ok[u]) continue;
+      const int64_t v = v0 + u * stride;
+      float lg[NC];
+#pragma unroll
+      for (int k = 0; k < NC; ++k) lg[k] = sb[k];
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+#pragma unroll
+        for (int k = 0; k < NC; ++k) lg[k] = fmaf(yv[u][c], sW[c * NC + k], lg[k]);
+      float m = lg[0];
+#pragma unroll
+      for (int k = 1; k < NC; ++k) m = fmaxf(m, lg[k]);
+      float p[NC], ssum = 0.f;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        p[k] = __expf(lg[k] - m);
+        ssum += p[k];
+      }
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        p[k] = __fdividef(p[k], ssum);
+        const float g = gk[u][k];
+        if (probs) probs[v * NC + k] = p[k];
+        st[k] += p[k] * g;
+        st[NC + k] += p[k];
+        st[2 * NC + k] += g;
+        st[3 * NC] += -__logf(fmaxf(p[k], clamp)) * g;
+      }
     }
   }
 #pragma unroll
@@ -552,67 +570,88 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_grp(
   }
   __syncthreads();
   const int cg = threadIdx.x % TPV;
-  float wr[8 * NC];  // this thread's 8 channels of the head weights, in registers
-#pragma unroll
-  for (int i = 0; i < 8 * NC; ++i) wr[i] = sW[cg * 8 * NC + i];
+  // this thread's 8 channels of the head weights, read from shared memory (two broadcast
+  // addresses per warp): keeping them in registers left room for only 2 items in flight
+  const float* wr = sW + cg * 8 * NC;
   const uint32_t nvox = (uint32_t)B * sy.D * sy.H * sy.W;
   const float ce_scale = -w_ce / total;
   float acc[NACC];
 #pragma unroll
   for (int i = 0; i < NACC; ++i) acc[i] = 0.f;
-  for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < nvox * TPV; gi += gridDim.x * blockDim.x) {
-    const uint32_t v = gi / TPV;
-    int b, d, h, w;
-    decompose(v, sy, b, d, h, w);
-    float yv[8];
-    V8<T>::ld(y + sy.at(b, cg, d, h, w), yv);
-    float lg[NC];
+  // U voxel items per thread per iteration, all loads issued before any math: the kernel is
+  // limited by loads in flight (2 blocks of 256 threads per SM), not by arithmetic
+  constexpr int U = 3;
+  const uint32_t total_items = nvox * TPV;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  // warp-uniform trip count (the loop body shuffles): iterate while the warp's first item is live
+  const uint32_t lane_off = threadIdx.x & 31;
+  for (uint32_t gi0 = blockIdx.x * blockDim.x + threadIdx.x; gi0 - lane_off < total_items; gi0 += U * stride) {
+    float yv[U][8], gk[U][NC];
+    int64_t go[U];
+    bool ok[U];
 #pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      float t = 0.f;
+    for (int u = 0; u < U; ++u) {
+      const uint32_t gi = gi0 + u * stride;
+      ok[u] = gi < total_items;
+      const uint32_t v = ok[u] ? gi / TPV : 0u;
+      int b, d, h, w;
+      decompose(v, sy, b, d, h, w);
+      V8<T>::ld(y + sy.at(b, cg, d, h, w), yv[u]);
+      go[u] = sg.at(b, cg, d, h, w);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) t = fmaf(yv[j], wr[j * NC + k], t);
-#pragma unroll
-      for (int o = 1; o < TPV; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-      lg[k] = t + sb[k];
+      for (int k = 0; k < NC; ++k) gk[u][k] = onehot[(size_t)v * NC + k];
     }
-    float m = lg[0];
 #pragma unroll
-    for (int k = 1; k < NC; ++k) m = fmaxf(m, lg[k]);
-    float p[NC], ssum = 0.f;
-#pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      p[k] = __expf(lg[k] - m);
-      ssum += p[k];
-    }
-    float gp[NC], dot = 0.f;
-#pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      p[k] = __fdividef(p[k], ssum);
-      const float gk = onehot[(size_t)v * NC + k];
-      float r = coef[3 * k + 2] != 0.f ? coef[3 * k] * (2.f * gk - coef[3 * k + 1]) : 0.f;
-      r += p[k] >= clamp ? ce_scale * (gk / fmaxf(p[k], clamp)) : 0.f;  // training.py:125-126
-      gp[k] = r;
-      dot += r * p[k];
-    }
-    float gl[NC];
-#pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      gl[k] = p[k] * (gp[k] - dot);  // ops.py:197-199
-      if (cg == 0) acc[8 * NC + k] += gl[k];
-    }
-    float o[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float sacc = 0.f;
+    for (int u = 0; u < U; ++u) {
+      // (inactive tail items still run the shuffles with their lanes, then skip the store)
+      float lg[NC];
 #pragma unroll
       for (int k = 0; k < NC; ++k) {
-        sacc = fmaf(wr[j * NC + k], gl[k], sacc);
-        acc[j * NC + k] = fmaf(yv[j], gl[k], acc[j * NC + k]);
+        float t = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) t = fmaf(yv[u][j], wr[j * NC + k], t);
+#pragma unroll
+        for (int o = 1; o < TPV; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        lg[k] = t + sb[k];
       }
-      o[j] = (relu_mask && !(yv[j] > 0.f)) ? 0.f : sacc;
+      float m = lg[0];
+#pragma unroll
+      for (int k = 1; k < NC; ++k) m = fmaxf(m, lg[k]);
+      float p[NC], ssum = 0.f;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        p[k] = __expf(lg[k] - m);
+        ssum += p[k];
+      }
+      float gp[NC], dot = 0.f;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        p[k] = __fdividef(p[k], ssum);
+        float r = coef[3 * k + 2] != 0.f ? coef[3 * k] * (2.f * gk[u][k] - coef[3 * k + 1]) : 0.f;
+        r += p[k] >= clamp ? ce_scale * (gk[u][k] / fmaxf(p[k], clamp)) : 0.f;  // training.py:125-126
+        gp[k] = r;
+        dot += r * p[k];
+      }
+      float gl[NC];
+#pragma unroll
+      for (int k = 0; k < NC; ++k) gl[k] = ok[u] ? p[k] * (gp[k] - dot) : 0.f;  // ops.py:197-199
+      if (cg == 0) {
+#pragma unroll
+        for (int k = 0; k < NC; ++k) acc[8 * NC + k] += gl[k];
+      }
+      float o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float sacc = 0.f;
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          sacc = fmaf(wr[j * NC + k], gl[k], sacc);
+          acc[j * NC + k] = fmaf(yv[u][j], gl[k], acc[j * NC + k]);
+        }
+        o[j] = (relu_mask && !(yv[u][j] > 0.f)) ? 0.f : sacc;
+      }
+      if (ok[u]) V8<T>::st(g + go[u], o);
     }
-    V8<T>::st(g + sg.at(b, cg, d, h, w), o);
   }
   // reduce over the lanes of this warp holding the same group, then over warps (fixed order)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;

@@ -31,6 +31,10 @@ SHAPES = [
     (1, 16, 3, 5, 6, 7),
     (3, 16, 16, 3, 30, 30),
     (1, 8, 48, 70, 4, 4),
+    # wide layers of the cfg3/cfg4 ladders: several 256-column N chunks, Cout > 1024 (the dgrad
+    # of a 1536-channel concat input), Cin 512
+    (1, 16, 1040, 2, 4, 4),
+    (1, 512, 256, 2, 4, 6),
 ]
 
 
@@ -139,6 +143,11 @@ WG_SHAPES = [
     (1, 64, 64, 6, 6, 34),
     (1, 32, 64, 4, 8, 40),
     (2, 16, 80, 3, 4, 48),
+    # Cout > 160: output-channel chunks of 128 (3 kw x Nc TMEM columns per M-tile), a ragged
+    # last chunk, no ones slot (separate bias partials)
+    (1, 32, 256, 4, 6, 8),
+    (1, 64, 200, 3, 4, 6),
+    (1, 128, 512, 2, 4, 4),
 ]
 
 

@@ -83,6 +83,18 @@ def test_tc_step_32cube_exercises_thin_kernels():
     mesh.shutdown()
 
 
+def test_tc_step_wide_ladder():
+    # cfg3/cfg4-style ladder (to 256 channels): chunked wide wgrad, multi-chunk fwd/dgrad
+    mesh, graph, params, x, oh = _setup(extent=16, filters=(32, 64, 128, 256), cpb=1, seed=5)
+    st, probs, stats, grads = _run(graph, params, x, oh, torch.bfloat16, "tc")
+    rprobs, rstats, rgrads, _ = oracle_step(graph, params, x, oh)
+    assert rel_l2(probs, rprobs) <= 1e-2
+    assert rel_l2(stats, rstats) <= 1e-2
+    worst = max(rel_l2(grads[k][0], rgrads[k][0]) for k in rgrads)
+    assert worst <= 1e-1, worst
+    mesh.shutdown()
+
+
 def test_train_step_host_prefetch_is_bitwise_the_plain_path():
     # the copy-stream prefetch of step k+1's inputs must not change any result
     extent = 32
