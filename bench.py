@@ -389,6 +389,8 @@ def run_ours(a):
                  "share_of_kernel_time": dom["ms"] / step_kernel_ms, "peak_source": peak_src,
                  "traffic_source": traffic_src})
     conv_flops = graph.conv_flops(a.batch) * (world * E ** 3) / (E ** 3) / world  # per rank
+    cfg_name = {(128, 0.125): "cfg2", (256, 0.5): "cfg3", (512, 1.0): "cfg4"}.get((E, a.scale), "custom")
+    act_gb = torch.cuda.memory_allocated() / 1e9  # activation slabs, tape, grads, workspaces
     conv_ms = sum(c["ms"] for k, c in classes.items() if k.startswith("conv"))
     if a.layer_csv and rank == 0:
         with open(a.layer_csv, "w") as f:
@@ -423,14 +425,14 @@ def run_ours(a):
         "dtype": "bf16",
         "data": "synthetic (data_io.synthesize_record distribution, SeedSequence([7, rank]))",
         "config": {
-            "workload": f"cfg2: U-Net recipe_for_resolution({E}, {a.scale}) = {cfg.encoder_filters}, "
+            "workload": f"{cfg_name}: U-Net recipe_for_resolution({E}, {a.scale:g}) = {cfg.encoder_filters}, "
                         f"{E}^3 per GPU, batch {a.batch}" + (f", depth-split x{world}" if world > 1 else ""),
             "global_batch": a.batch,
             "volume": [E * world, E, E],
             "parallelism": f"spatial depth-split x{world}" if world > 1 else "single GPU",
             "conv": a.conv,
             "cuda_graph": graph_note,
-            "l2": "working set (activation slabs, ~1.5 GB) >> 126 MB L2; no flush needed",
+            "l2": f"working set (activation slabs, {act_gb:.1f} GB) >> 126 MB L2; no flush needed",
             "conv_tflop_per_step_rank": conv_flops / 1e12,
         },
         "e2e": {"value": voxels / (ms_e2e * 1e-3), "unit": "voxels/s", "h2d_bytes_per_step": h2d,
