@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(320, 1)
     k_conv_fwd_tc(const FwdParams p) {
   auto clk = []() -> long long { return DBG ? (long long)clock64() : 0LL; };
   extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ float sbias[1024];  // Cout <= 1024; wider layers read the bias through L1
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -326,6 +327,10 @@ __global__ void __launch_bounds__(320, 1)
     // warp w drains TMEM lane quarter (w & 3) of every other tile (parity (w-2)/4)
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
+    const bool bias_smem = p.Cout <= 1024;
+    if (!(p.flags & VM_CONV_NOBIAS) && bias_smem)
+      for (int c = threadIdx.x - 64; c < p.Cout; c += 256) sbias[c] = p.bias[c];
+    asm volatile("bar.sync 1, 256;" ::: "memory");
     int ab = 0;
     uint32_t aphase = 0;
     long long t_epi_wait = 0;
@@ -397,7 +402,8 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
                 v[e] = __uint_as_float(r[jj * 8 + e]);
-                if (!(p.flags & VM_CONV_NOBIAS)) v[e] += (co0 + e < p.Cout) ? __ldg(p.bias + co0 + e) : 0.f;
+                if (!(p.flags & VM_CONV_NOBIAS))
+                  v[e] += (co0 + e < p.Cout) ? (bias_smem ? sbias[co0 + e] : __ldg(p.bias + co0 + e)) : 0.f;
               }
               if (p.flags & VM_CONV_RELU) {
 #pragma unroll
@@ -687,20 +693,20 @@ __global__ void __launch_bounds__(192, 1)
 // 4-byte scattered stores with a Cout stride.  Blocks past the tiles reduce the separate
 // bias partials wsb[nsb][CGo*8] when the ones slot does not exist.  ldo: row stride of gw
 // (the full Cout when this call covers a chunk of the output channels).
-template <bool KD>
-__global__ void __launch_bounds__(256) k_wgrad_finalize_tiles(const float* __restrict__ ws, float* __restrict__ gw,
+template <bool KD, int NW>  // NW warps per block split the K partials (32 when there are many)
+__global__ void __launch_bounds__(NW * 32) k_wgrad_finalize_tiles(const float* __restrict__ ws, float* __restrict__ gw,
                                                              float* __restrict__ gb, int nk, int MT, int Nc, int CG,
                                                              int Cin, int Cout, int ones_slot, int runs,
                                                              const float* __restrict__ wsb, int nsb, int CGo,
                                                              int ldo) {
-  __shared__ float part[8][8][33];
+  __shared__ float part[NW][8][33];
   const int N = KD ? 3 * Nc : Nc;
   const int n8 = N / 8;
   const int64_t E = (int64_t)MT * 3 * N * 128;
   const int ntiles = MT * 3 * n8 * 4;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if ((int)blockIdx.x >= ntiles) {
-    const int co = ((int)blockIdx.x - ntiles) * 256 + threadIdx.x;
+    const int co = ((int)blockIdx.x - ntiles) * (NW * 32) + threadIdx.x;
     if (co < Cout) {
       float sb = 0.f;
       for (int sp = 0; sp < nsb; ++sp) sb += wsb[(int64_t)sp * CGo * 8 + co];
@@ -719,7 +725,7 @@ __global__ void __launch_bounds__(256) k_wgrad_finalize_tiles(const float* __res
   float acc[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-  for (int k = w; k < nk; k += 8) {
+  for (int k = w; k < nk; k += NW) {
     const float* src = ws + (int64_t)k * E + e0;
     float v[8];
 #pragma unroll
@@ -731,10 +737,11 @@ __global__ void __launch_bounds__(256) k_wgrad_finalize_tiles(const float* __res
   for (int j = 0; j < 8; ++j) part[w][j][lane] = acc[j];
   __syncthreads();
   // thread -> (m = mq*32 + mm, n = nb*8 + j): 8 consecutive n per m
+  if (threadIdx.x >= 256) return;
   const int j = threadIdx.x & 7, mm = threadIdx.x >> 3;
   float s = 0.f;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) s += part[i][j][mm];
+  for (int i = 0; i < NW; ++i) s += part[i][j][mm];
   const int m = mq * 32 + mm;
   const int n = nb * 8 + j;
   const int g = mt * 16 + m / 8;
@@ -1961,7 +1968,9 @@ static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_
       if (rc) return rc;
       const int nk = pk.grid / pk.ngroups;
       const int ntiles = pk.MT * 3 * (3 * pk.Nc / 8) * 4;
-      k_wgrad_finalize_tiles<true><<<ntiles, 256, 0, st>>>(pk.ws, gw, gb, nk, pk.MT, pk.Nc, pk.CG, Cin, Cout,
+      // many partials (one per CTA of a wide K split): 32 warps per tile keep more loads in flight
+      auto fin = nk >= 64 ? k_wgrad_finalize_tiles<true, 32> : k_wgrad_finalize_tiles<true, 8>;
+      fin<<<ntiles, nk >= 64 ? 1024 : 256, 0, st>>>(pk.ws, gw, gb, nk, pk.MT, pk.Nc, pk.CG, Cin, Cout,
                                                           pk.ones_slot, 0, nullptr, 0, 0, Cout);
       return launch_status("vm_conv3d_wgrad_tc (kd) finalize");
     }
@@ -2009,7 +2018,7 @@ static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_
   }
   const int ntiles = p.MT * 3 * (p.Nc / 8) * 4;
   const int nbias = p.ones_slot < 0 ? (Cout + 255) / 256 : 0;
-  k_wgrad_finalize_tiles<false><<<ntiles + nbias, 256, 0, st>>>(p.ws, gw, gb, nk, p.MT, p.Nc, p.CG, Cin, Cout,
+  k_wgrad_finalize_tiles<false, 8><<<ntiles + nbias, 256, 0, st>>>(p.ws, gw, gb, nk, p.MT, p.Nc, p.CG, Cin, Cout,
                                                                p.ones_slot, p.runs, wsb, nsb, (Cout + 7) / 8, ldo);
   return launch_status("vm_conv3d_wgrad_tc finalize");
 }
