@@ -62,6 +62,8 @@ __device__ __forceinline__ int split_cg(int64_t i, int64_t nvox, uint32_t& v) {
 // out grid: pooled voxels (D,H,W are the POOLED extents) x channel blocks
 template <typename T>
 __global__ void k_maxpool_fwd(const T* __restrict__ x, Slab gx, T* __restrict__ y, Slab gy, int B) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t nvox = (int64_t)B * gy.D * gy.H * gy.W;
   const int64_t total = nvox * gy.CG;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -135,6 +137,8 @@ __global__ void k_maxpool_bwd(const T* __restrict__ x, Slab gx, const T* __restr
 // neighbouring threads re-read the same input vector from L1
 template <typename T>
 __global__ void k_upsample_fwd(const T* __restrict__ x, Slab gx, T* __restrict__ y, Slab gy, int B) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t nvox = (int64_t)B * gy.D * gy.H * gy.W;
   const int64_t total = nvox * gy.CG;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -373,6 +377,8 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_fwd_fixed(
     const T* __restrict__ y, Slab sy, const float* __restrict__ W, const float* __restrict__ bias,
     const float* __restrict__ onehot, float* __restrict__ probs, float* __restrict__ partials, int B,
     float clamp) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float sW[C * NC], sb[NC], red[kHeadThreads / 32];
   for (int i = threadIdx.x; i < C * NC; i += blockDim.x) sW[i] = W[i];
   if (threadIdx.x < NC) sb[threadIdx.x] = bias[threadIdx.x];
@@ -678,6 +684,8 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_grp(
 // one warp per column; lanes take strided rows, then a fixed shuffle tree (deterministic)
 __global__ void k_reduce_rows(const float* __restrict__ part, int rows, int width,
                               float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x % 32;
   for (int j = (blockIdx.x * blockDim.x + threadIdx.x) / 32; j < width; j += gridDim.x * blockDim.x / 32) {
     float s = 0.f;
@@ -743,7 +751,7 @@ extern "C" int vm_maxpool2_fwd(int dtype, const void* x, int64_t x_bstride, void
   int64_t work = (int64_t)B * (D / 2) * (H / 2) * (W / 2) * gy.CG;
   VM_REQUIRE(work < (1LL << 32), VM_E_SHAPE, "index space %lld exceeds 2^32", (long long)work);
   DISPATCH_T(dtype, "vm_maxpool2_fwd",
-             k_maxpool_fwd<T><<<grid_for(work, 256), 256, 0, as_stream(stream)>>>(
+             launch_pdl(k_maxpool_fwd<T>, grid_for(work, 256), 256, 0, as_stream(stream),
                  (const T*)x, gx, (T*)y, gy, B));
   return launch_status("vm_maxpool2_fwd");
 }
@@ -771,7 +779,7 @@ extern "C" int vm_upsample2_fwd(int dtype, const void* x, int64_t x_bstride, voi
   int64_t work = (int64_t)B * D * H * W * gx.CG * 8;  // output vectors
   VM_REQUIRE(work < (1LL << 32), VM_E_SHAPE, "index space %lld exceeds 2^32", (long long)work);
   DISPATCH_T(dtype, "vm_upsample2_fwd",
-             k_upsample_fwd<T><<<grid_for(work, 256), 256, 0, as_stream(stream)>>>(
+             launch_pdl(k_upsample_fwd<T>, grid_for(work, 256), 256, 0, as_stream(stream),
                  (const T*)x, gx, (T*)y, gy, B));
   return launch_status("vm_upsample2_fwd");
 }
@@ -824,11 +832,11 @@ extern "C" int vm_head_fwd(int dtype, const void* y, int64_t y_bstride, const fl
     using T = __nv_bfloat16;
     auto st = as_stream(stream);
     if (C == 16)
-      k_head_fwd_fixed<T, 16, 3><<<grid, kHeadThreads, 0, st>>>((const T*)y, sy, w, b, onehot, probs, partials, B, clamp);
+      launch_pdl(k_head_fwd_fixed<T, 16, 3>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, onehot, probs, partials, B, clamp);
     else if (C == 32)
-      k_head_fwd_fixed<T, 32, 3><<<grid, kHeadThreads, 0, st>>>((const T*)y, sy, w, b, onehot, probs, partials, B, clamp);
+      launch_pdl(k_head_fwd_fixed<T, 32, 3>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, onehot, probs, partials, B, clamp);
     else
-      k_head_fwd_fixed<T, 8, 3><<<grid, kHeadThreads, 0, st>>>((const T*)y, sy, w, b, onehot, probs, partials, B, clamp);
+      launch_pdl(k_head_fwd_fixed<T, 8, 3>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, onehot, probs, partials, B, clamp);
     return launch_status("vm_head_fwd");
   }
   DISPATCH_T(dtype, "vm_head_fwd",
@@ -839,7 +847,7 @@ extern "C" int vm_head_fwd(int dtype, const void* y, int64_t y_bstride, const fl
 
 extern "C" int vm_reduce_rows(const float* partials, int rows, int width, float* out, void* stream) {
   VM_REQUIRE(partials && out && rows > 0 && width > 0, VM_E_ARG, "vm_reduce_rows: bad argument");
-  k_reduce_rows<<<(width + 3) / 4, 128, 0, as_stream(stream)>>>(partials, rows, width, out);
+  launch_pdl(k_reduce_rows, (width + 3) / 4, 128, 0, as_stream(stream), partials, rows, width, out);
   return launch_status("vm_reduce_rows");
 }
 

@@ -140,6 +140,10 @@ class UNetStep:
         self._rec = None
         self.packer = None  # halo pack/unpack backend (None: the CUDA box kernels)
         self.overlap_wgrad = True  # weight gradients on a side stream, concurrent with dgrad
+        # programmatic dependent launch between the forward's kernels (the next kernel's CTAs
+        # are scheduled and set up while the previous one drains); off in the backward, where
+        # CTAs parked at the dependency wait would take SMs from the side-stream wgrad
+        self.pdl_forward = True
         self._build_buffers(params)
 
     # ------------------------------------------------------------------ setup
@@ -501,6 +505,13 @@ class UNetStep:
 
     # ------------------------------------------------------------------ passes
     def forward(self):
+        prev = _lib.load().vm_set_pdl(1 if self.pdl_forward else 0)
+        try:
+            self._forward_nodes()
+        finally:
+            _lib.load().vm_set_pdl(prev)
+
+    def _forward_nodes(self):
         for n in self.graph.nodes:
             if n.op == "conv" and n.k == 3:
                 x = self.out[n.inputs[0]]

@@ -21,14 +21,14 @@ from paper_1909_03108_b200.data import synth_record  # noqa: E402
 from paper_1909_03108_b200.step import UNetStep  # noqa: E402
 from bench import _capture  # noqa: E402
 
-pdl = int(os.environ.get("VM_PDL", "0"))
-_lib.load().vm_set_pdl(pdl)
+pdl = int(os.environ.get("PDL_FWD", "1"))
 cfg = vm.recipe_for_resolution(128, 1 / 8)
 mesh = vm.create_mesh([("one", 1)], backend="threads")
 graph = vm.build(cfg, mesh, {})
 st = UNetStep(graph, vm.init_params(graph, 1), batch=1, ctx=None, dtype=torch.bfloat16)
 im, lb = synth_record(128, 7, 0)
 st.upload(torch.from_numpy(im[None, ..., None].copy()), torch.from_numpy(lb[None].copy()))
+st.pdl_forward = bool(pdl)
 st.step()
 torch.cuda.synchronize()
 
@@ -77,4 +77,4 @@ def wg():
 
 
 res["wgrad_only"] = timed(wg)
-print(f"PDL={pdl} " + " ".join(f"{k}={v:.3f}ms" for k, v in res.items()))
+print(f"pdl_forward={pdl} " + " ".join(f"{k}={v:.3f}ms" for k, v in res.items()))
