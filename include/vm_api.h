@@ -55,7 +55,8 @@ const char* vm_last_error(void);
 int vm_num_sms(int device);
 /* number of kernels this library has launched in this process (bench bookkeeping) */
 long long vm_launch_count(void);
-/* programmatic dependent launch between this library's kernels (default from $VM_PDL);
+/* programmatic dependent launch between this library's kernels (default from $VM_PDL):
+ * 0 off, 1 on with the trigger at kernel start, 2 on with the trigger at CTA exit;
  * returns the previous setting */
 int vm_set_pdl(int on);
 

@@ -24,7 +24,7 @@ void set_error(const char* fmt, ...) {
 static std::atomic<long long> g_launches{0};
 void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
-static int g_pdl = -1;  // -1: from $VM_PDL (default on)
+static int g_pdl = -1;  // -1: from $VM_PDL (default off); 1: early trigger; 2: late (implicit) trigger
 bool pdl_enabled() {
   if (g_pdl < 0) {
     const char* e = getenv("VM_PDL");
@@ -32,6 +32,7 @@ bool pdl_enabled() {
   }
   return g_pdl != 0;
 }
+bool pdl_late() { return pdl_enabled() && g_pdl == 2; }
 
 static int g_num_sms = -1;
 static int num_sms() {
@@ -171,8 +172,8 @@ extern "C" const char* vm_last_error(void) { return g_err; }
 
 extern "C" long long vm_launch_count(void) { return g_launches.load(); }
 extern "C" int vm_set_pdl(int on) {
-  const int prev = vm::pdl_enabled() ? 1 : 0;
-  vm::g_pdl = on ? 1 : 0;
+  const int prev = vm::pdl_enabled() ? vm::g_pdl : 0;
+  vm::g_pdl = on == 2 ? 2 : on ? 1 : 0;
   return prev;
 }
 

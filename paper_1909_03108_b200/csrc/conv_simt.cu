@@ -181,6 +181,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_bias_grad_partial(const T* __restrict__ gy, Slab gg,
                                                            float* __restrict__ ws, int B, int CGout,
                                                            int64_t chunk) {
+  pdl_wait();
   __shared__ float red[8][9];
   const int cgo = blockIdx.y;
   const int64_t nvox = (int64_t)B * gg.D * gg.H * gg.W;
@@ -277,8 +278,8 @@ int bias_grad_partial_bf16(const void* gy, int64_t gy_bstride, float* ws, int B,
   int64_t nvox = (int64_t)B * D * H * W;
   int ns = (int)(bias_grad_ws_bytes(nvox, Cout) / (gg.CG * 8 * sizeof(float)));
   int64_t chunk = (nvox + ns - 1) / ns;
-  k_bias_grad_partial<__nv_bfloat16><<<dim3(ns, gg.CG), 256, 0, st>>>((const __nv_bfloat16*)gy, gg, ws, B,
-                                                                      gg.CG, chunk);
+  launch_pdl(k_bias_grad_partial<__nv_bfloat16>, dim3(ns, gg.CG), 256, 0, st, (const __nv_bfloat16*)gy, gg, ws, B,
+             gg.CG, chunk);
   *nsplit = ns;
   return launch_status("bias_grad_partial_bf16");
 }

@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(320, 1)
   tc_fence_after();
   const uint32_t tbase = tslot;
   pdl_wait();
-  pdl_trigger();
+  if (!(p.flags & kFlagPdlLate)) pdl_trigger();
   const int nstage_k = p.KC * 3;
 
   if (warp == 0) {
@@ -522,6 +522,7 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = tslot;
+  pdl_wait();  // dependents launch as this grid's CTAs exit (no early trigger)
   const int ngroups_total = 9 * p.CG;
 
   if (warp == 0) {
@@ -699,6 +700,7 @@ __global__ void __launch_bounds__(NW * 32) k_wgrad_finalize_tiles(const float* _
                                                              int Cin, int Cout, int ones_slot, int runs,
                                                              const float* __restrict__ wsb, int nsb, int CGo,
                                                              int ldo) {
+  pdl_wait();
   __shared__ float part[NW][8][33];
   const int N = KD ? 3 * Nc : Nc;
   const int n8 = N / 8;
@@ -841,7 +843,7 @@ __global__ void __launch_bounds__(352, 1)
   tc_fence_after();
   const uint32_t tbase = tslot;
   pdl_wait();
-  pdl_trigger();
+  if (!(p.flags & kFlagPdlLate)) pdl_trigger();
 
   if (warp == 0) {
     // ===================== producer: resident weights, then one stage per (plane, K chunk)
@@ -1252,6 +1254,7 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = tslot;
+  pdl_wait();  // dependents launch as this grid's CTAs exit (no early trigger)
 
   if (warp == 0) {
     if (elect_one()) {
@@ -1602,7 +1605,7 @@ extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wp
   p.Cout = Cout;
   p.Nc = pg.Nc;
   p.nchunk = pg.nchunk;
-  p.flags = flags;
+  p.flags = flags | (pdl_late() ? kFlagPdlLate : 0u);
   p.dbg = g_fwd_dbg;
   p.wp_magic = (uint32_t)(0x100000000ULL / (uint64_t)(W + 2)) + 1;
   p.hp_magic = (uint32_t)(0x100000000ULL / (uint64_t)(H + 2)) + 1;
@@ -1963,14 +1966,14 @@ static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_
       auto kern = table[pk.mt_per_unit - 1][var];
       (void)dbg;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
-      kern<<<pk.grid, 192, (size_t)pk.stages * pk.stage_bytes, st>>>(gmap, pk);
+      launch_pdl(kern, pk.grid, 192, (size_t)pk.stages * pk.stage_bytes, st, gmap, pk);
       rc = launch_status("vm_conv3d_wgrad_tc (kd)");
       if (rc) return rc;
       const int nk = pk.grid / pk.ngroups;
       const int ntiles = pk.MT * 3 * (3 * pk.Nc / 8) * 4;
       // many partials (one per CTA of a wide K split): 32 warps per tile keep more loads in flight
       auto fin = nk >= 64 ? k_wgrad_finalize_tiles<true, 32> : k_wgrad_finalize_tiles<true, 8>;
-      fin<<<ntiles, nk >= 64 ? 1024 : 256, 0, st>>>(pk.ws, gw, gb, nk, pk.MT, pk.Nc, pk.CG, Cin, Cout,
+      launch_pdl(fin, ntiles, nk >= 64 ? 1024 : 256, 0, st, pk.ws, gw, gb, nk, pk.MT, pk.Nc, pk.CG, Cin, Cout,
                                                           pk.ones_slot, 0, nullptr, 0, 0, Cout);
       return launch_status("vm_conv3d_wgrad_tc (kd) finalize");
     }
@@ -2004,7 +2007,7 @@ static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_
   };
   auto kern = table[nmt_t][nkk_t / 4];
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
-  kern<<<p.grid, 192, (size_t)p.stages * p.stage_bytes, st>>>(gmap, p);
+  launch_pdl(kern, p.grid, 192, (size_t)p.stages * p.stage_bytes, st, gmap, p);
   rc = launch_status("vm_conv3d_wgrad_tc");
   if (rc) return rc;
   const int nk = p.grid / p.n_mtgroups;
@@ -2018,7 +2021,7 @@ static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_
   }
   const int ntiles = p.MT * 3 * (p.Nc / 8) * 4;
   const int nbias = p.ones_slot < 0 ? (Cout + 255) / 256 : 0;
-  k_wgrad_finalize_tiles<false, 8><<<ntiles + nbias, 256, 0, st>>>(p.ws, gw, gb, nk, p.MT, p.Nc, p.CG, Cin, Cout,
+  launch_pdl(k_wgrad_finalize_tiles<false, 8>, ntiles + nbias, 256, 0, st, p.ws, gw, gb, nk, p.MT, p.Nc, p.CG, Cin, Cout,
                                                                p.ones_slot, p.runs, wsb, nsb, (Cout + 7) / 8, ldo);
   return launch_status("vm_conv3d_wgrad_tc finalize");
 }

@@ -88,6 +88,7 @@ template <typename T>
 __global__ void k_maxpool_bwd(const T* __restrict__ x, Slab gx, const T* __restrict__ gout, Slab go,
                               const T* __restrict__ add, Slab ga, T* __restrict__ gin, Slab gi,
                               int B, int relu_mask) {
+  pdl_wait();
   const int64_t nvox = (int64_t)B * go.D * go.H * go.W;
   const int64_t total = nvox * go.CG;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -157,6 +158,7 @@ __global__ void k_upsample_fwd(const T* __restrict__ x, Slab gx, T* __restrict__
 template <typename T>
 __global__ void k_upsample_bwd(const T* __restrict__ gy, Slab sgy, const T* __restrict__ mask,
                                Slab sm, T* __restrict__ gx, Slab sgx, int B) {
+  pdl_wait();
   const int64_t nvox = (int64_t)B * sgx.D * sgx.H * sgx.W;
   const int64_t total = nvox * sgx.CG;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -556,6 +558,7 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_grp(
     const float* __restrict__ onehot, const float* __restrict__ stats, T* __restrict__ g, Slab sg,
     float* __restrict__ wpart, int B, float w_dice, float w_ce, float total, int dice_mask, float clamp,
     int relu_mask) {
+  pdl_wait();
   constexpr int TPV = C / 8;
   constexpr int NACC = 8 * NC + NC;  // group's weight grads + bias grads (used by cg == 0)
   constexpr int NWARP = kHeadThreads / 32;
@@ -767,7 +770,7 @@ extern "C" int vm_maxpool2_bwd(int dtype, const void* x, int64_t x_bstride, cons
   int64_t work = (int64_t)B * (D / 2) * (H / 2) * (W / 2) * go.CG;
   VM_REQUIRE(work < (1LL << 32), VM_E_SHAPE, "index space %lld exceeds 2^32", (long long)work);
   DISPATCH_T(dtype, "vm_maxpool2_bwd",
-             k_maxpool_bwd<T><<<grid_for(work, 256), 256, 0, as_stream(stream)>>>(
+             launch_pdl(k_maxpool_bwd<T>, grid_for(work, 256), 256, 0, as_stream(stream),
                  (const T*)x, gx, (const T*)gout, go, (const T*)add, ga, (T*)gin, gi, B, relu_mask));
   return launch_status("vm_maxpool2_bwd");
 }
@@ -793,7 +796,7 @@ extern "C" int vm_upsample2_bwd(int dtype, const void* gy, int64_t gy_bstride, c
   int64_t work = (int64_t)B * D * H * W * sgx.CG;
   VM_REQUIRE(work < (1LL << 32), VM_E_SHAPE, "index space %lld exceeds 2^32", (long long)work);
   DISPATCH_T(dtype, "vm_upsample2_bwd",
-             k_upsample_bwd<T><<<grid_for(work, 256), 256, 0, as_stream(stream)>>>(
+             launch_pdl(k_upsample_bwd<T>, grid_for(work, 256), 256, 0, as_stream(stream),
                  (const T*)gy, sgy, (const T*)mask, sm, (T*)gx, sgx, B));
   return launch_status("vm_upsample2_bwd");
 }
@@ -866,7 +869,7 @@ extern "C" int vm_head_bwd(int dtype, const void* y, int64_t y_bstride, const fl
     using T = __nv_bfloat16;
     auto st = as_stream(stream);
 #define HEAD_BWD_FIXED(CC)                                                                          \
-  k_head_bwd_grp<T, CC, 3><<<grid, kHeadThreads, 0, st>>>((const T*)y, sy, w, b, onehot, stats, (T*)g, sg, \
+  launch_pdl(k_head_bwd_grp<T, CC, 3>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, onehot, stats, (T*)g, sg, \
                                                             wpartials, B, w_dice, w_ce, total_voxels,    \
                                                             dice_mask, clamp, relu_mask)
     if (C == 16)

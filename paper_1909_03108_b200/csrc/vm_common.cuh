@@ -44,6 +44,8 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // CTAs be scheduled (prologue: barrier init, TMEM alloc) before this one finishes.  Both are
 // no-ops when the kernel was launched without the attribute.  vm_set_pdl(0) turns it off.
 bool pdl_enabled();
+bool pdl_late();  // mode 2: kernels skip the early trigger (dependents launch as CTAs exit)
+constexpr unsigned kFlagPdlLate = 1u << 8;  // conv params flag bit set from pdl_late()
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

@@ -28,7 +28,8 @@ graph = vm.build(cfg, mesh, {})
 st = UNetStep(graph, vm.init_params(graph, 1), batch=1, ctx=None, dtype=torch.bfloat16)
 im, lb = synth_record(128, 7, 0)
 st.upload(torch.from_numpy(im[None, ..., None].copy()), torch.from_numpy(lb[None].copy()))
-st.pdl_forward = bool(pdl)
+st.pdl_forward = pdl
+st.pdl_backward = int(os.environ.get("PDL_BWD", "2"))
 st.step()
 torch.cuda.synchronize()
 
@@ -77,4 +78,4 @@ def wg():
 
 
 res["wgrad_only"] = timed(wg)
-print(f"pdl_forward={pdl} " + " ".join(f"{k}={v:.3f}ms" for k, v in res.items()))
+print(f"pdl_forward={pdl} pdl_backward={int(st.pdl_backward)} " + " ".join(f"{k}={v:.3f}ms" for k, v in res.items()))
