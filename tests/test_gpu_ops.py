@@ -96,3 +96,36 @@ def test_distributed_losses_match_oracle():
     st = O.loss_stats(probs.astype(np.float64), oh.astype(np.float64))
     rcomb, rdice, rce = O.losses_from_stats(st, 3, D * H * W)
     assert abs(dice - rdice) <= 1e-9 and abs(ce - rce) <= 1e-9 and abs(comb - rcomb) <= 1e-9
+
+
+@pytest.mark.parametrize("C,D,H,W", [(16, 4, 6, 8), (24, 3, 5, 7), (32, 8, 8, 8)])
+def test_bf16_slab_upsample_and_pool_bit_exact(C, D, H, W):
+    # the bf16 slab kernels the train step runs (upsample: one thread per input vector writing
+    # the 2x2x2 cell; pool: first max in scan order) against numpy on the same bf16 values
+    from paper_1909_03108_b200 import _lib
+    from paper_1909_03108_b200.step import Slab
+    import torch
+    rng = np.random.default_rng(C + D)
+    B = 2
+    x = O.bf16_round(rng.standard_normal((B, D, H, W, C)).astype(np.float32))
+
+    def to_slab(a):
+        b_, d_, h_, w_, c_ = a.shape
+        s = Slab(b_, c_, d_, h_, w_, torch.bfloat16, "cuda")
+        t = torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+        _lib.call("vm_dense_to_slab", _lib.ptr(t), _lib.VM_F32, s.p(), _lib.VM_BF16, s.bstride, b_, c_, d_, h_, w_, 1,
+                  _lib.stream_ptr())
+        return s
+
+    xs = to_slab(x)
+    ys = Slab(B, C, 2 * D, 2 * H, 2 * W, torch.bfloat16, "cuda")
+    _lib.call("vm_upsample2_fwd", _lib.VM_BF16, xs.p(), xs.bstride, ys.p(), ys.bstride, B, C, D, H, W,
+              _lib.stream_ptr())
+    up = ys.interior().float().cpu().numpy()
+    assert np.array_equal(up, x.repeat(2, 1).repeat(2, 2).repeat(2, 3))
+    ps = Slab(B, C, D // 2, H // 2, W // 2, torch.bfloat16, "cuda") if D % 2 == 0 and H % 2 == 0 and W % 2 == 0 else None
+    if ps is not None:
+        _lib.call("vm_maxpool2_fwd", _lib.VM_BF16, xs.p(), xs.bstride, ps.p(), ps.bstride, B, C, D, H, W,
+                  _lib.stream_ptr())
+        rp, _ = O.maxpool2_dense(x)
+        assert np.array_equal(ps.interior().float().cpu().numpy(), rp)
