@@ -132,6 +132,16 @@ int vm_pack_weights_batch(const vm_pack_job* jobs, int njobs, int64_t total_elem
 int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wpacked, const float* bias,
                      void* y, int64_t y_bstride, const void* mask, int64_t mask_bstride, int B,
                      int Cin, int Cout, int D, int H, int W, unsigned flags, void* stream);
+/* Same, with a caller scratch buffer that lets the general (non-sweep) kernel split the
+ * K = 27*Cin reduction over up to 3 CTAs per tile (deep levels with few tiles).  `ws` must be
+ * zero-filled once before first use (tile counters; every launch leaves them zero) and used
+ * by one stream at a time; ws_bytes >= vm_conv3d_fwd_tc_ws_bytes(...) allows every split,
+ * smaller (or NULL) restricts the plan.  Results are bitwise independent of arrival order. */
+int vm_conv3d_fwd_tc_ws(const void* x, int64_t x_bstride, const void* wpacked, const float* bias,
+                        void* y, int64_t y_bstride, const void* mask, int64_t mask_bstride, int B,
+                        int Cin, int Cout, int D, int H, int W, unsigned flags, void* ws,
+                        size_t ws_bytes, void* stream);
+size_t vm_conv3d_fwd_tc_ws_bytes(int B, int Cin, int Cout, int D, int H, int W);
 size_t vm_conv3d_wgrad_tc_ws(int B, int Cin, int Cout, int D, int H, int W);
 int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* gy, int64_t gy_bstride,
                        float* gw, float* gb, void* ws, int B, int Cin, int Cout, int D, int H,

@@ -26,6 +26,7 @@ _I = ctypes.c_int
 _L = ctypes.c_int64
 _F = ctypes.c_float
 _U = ctypes.c_uint
+_S = ctypes.c_size_t
 
 # name -> (restype, argtypes)
 _SIGS = {
@@ -50,6 +51,8 @@ _SIGS = {
     "vm_pack_weights": (_I, [_P, _P, _I, _I, _I, _P]),
     "vm_pack_weights_batch": (_I, [_P, _I, _L, _P]),
     "vm_conv3d_fwd_tc": (_I, [_P, _L, _P, _P, _P, _L, _P, _L, _I, _I, _I, _I, _I, _I, _U, _P]),
+    "vm_conv3d_fwd_tc_ws": (_I, [_P, _L, _P, _P, _P, _L, _P, _L, _I, _I, _I, _I, _I, _I, _U, _P, _S, _P]),
+    "vm_conv3d_fwd_tc_ws_bytes": (_S, [_I, _I, _I, _I, _I, _I]),
     "vm_conv3d_wgrad_tc_ws": (ctypes.c_size_t, [_I, _I, _I, _I, _I, _I]),
     "vm_conv3d_wgrad_tc": (_I, [_P, _L, _P, _L, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     "vm_maxpool2_fwd": (_I, [_I, _P, _L, _P, _L, _I, _I, _I, _I, _I, _P]),

@@ -37,6 +37,7 @@ using bf16 = __nv_bfloat16;
 constexpr int kBoxR = 128;  // TMA box height (rows of 8 bf16 = 16 B)
 constexpr int kMaxStages = 6;
 constexpr int kSmemBudget = 220 * 1024;
+constexpr int kFwdMaxSplit = 3;  // split-K ways of the general forward kernel
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -192,8 +193,14 @@ struct FwdParams {
   uint32_t stage_bytes;
   uint32_t idesc;
   unsigned flags;
-  long long* dbg;  // optional timing probes [gridDim][4]
+  long long* dbg;  // optional timing probes [gridDim][8]
   uint32_t wp_magic, hp_magic;  // floor(2^32 / d) + 1 for the anchor (w, h) split
+  // split-K over the 3*KC (kc, kd) stages: unit = (tile unit tu, split ks); split ks writes
+  // f32 partials ws[ks][tu][MB][Nc][128], the last split of a tile unit to finish (counter)
+  // sums all splits in split order (deterministic) and runs the epilogue
+  int ksplit, spk;
+  float* ws;
+  int* counters;  // [tile units], zero between launches (the last split resets its counter)
 };
 
 // MB (tiles per unit) is a template parameter so that the MMA issue loop is straight-line
@@ -234,13 +241,16 @@ __global__ void __launch_bounds__(320, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        const int nch = u % p.nchunk;
-        const int mb = (u / p.nchunk) % p.mblocks;
-        const int b = u / (p.nchunk * p.mblocks);
+        const int ks = u % p.ksplit, tu = u / p.ksplit;
+        const int nch = tu % p.nchunk;
+        const int mb = (tu / p.nchunk) % p.mblocks;
+        const int b = tu / (p.nchunk * p.mblocks);
         const int64_t a0 = (int64_t)mb * p.MB * 128;
-        for (int kc = 0; kc < p.KC; ++kc) {
+        const int s0 = ks * p.spk, s1 = min(nstage_k, s0 + p.spk);
+        for (int s = s0; s < s1; ++s) {
+          const int kc = s / 3, kd = s % 3;
           const int ng = (kc * 2 + 1 < p.CG) ? 2 : 1;
-          for (int kd = 0; kd < 3; ++kd) {
+          {
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* sA = smem + (size_t)stage * p.stage_bytes;
             uint8_t* sB = sA + 2 * p.a_bytes;
@@ -272,10 +282,11 @@ __global__ void __launch_bounds__(320, 1)
       mbar_wait(&tempty[ab], aphase ^ 1);
       t_wait_tmem += clk() - tw0;
       tc_fence_after();
-      for (int s = 0; s < nstage_k; ++s) {
+      const int s0 = (u % p.ksplit) * p.spk, s1 = min(nstage_k, s0 + p.spk);
+      for (int s = s0; s < s1; ++s) {
         const int kc = s / 3;
         const int ng = (kc * 2 + 1 < p.CG) ? 2 : 1;
-        const int aset = s % p.nacc;  // consecutive stages feed different accumulators
+        const int aset = (s - s0) % p.nacc;  // consecutive stages feed different accumulators
         long long tf0 = clk();
         mbar_wait(&full[stage], phase);
         t_wait_full += clk() - tf0;
@@ -291,7 +302,7 @@ __global__ void __launch_bounds__(320, 1)
           const uint32_t d0 = tbase + (uint32_t)((ab * p.MB * p.nacc + aset) * p.Nc);
           const uint32_t tstep = (uint32_t)(p.nacc * p.Nc);
           const uint32_t bstep = (uint32_t)(2 * p.Nc * 16) >> 4;
-          const uint32_t acc0 = s >= p.nacc ? 1u : 0u;
+          const uint32_t acc0 = s - s0 >= p.nacc ? 1u : 0u;
           const uint32_t wp1 = (uint32_t)p.Wp;
 #pragma unroll
           for (int j = 0; j < 9; ++j) {
@@ -318,9 +329,9 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
     if (p.dbg && lane == 0) {
-      p.dbg[blockIdx.x * 4 + 0] = clk() - t_start;
-      p.dbg[blockIdx.x * 4 + 1] = t_wait_tmem;
-      p.dbg[blockIdx.x * 4 + 2] = t_wait_full;
+      p.dbg[blockIdx.x * 8 + 0] = clk() - t_start;
+      p.dbg[blockIdx.x * 8 + 1] = t_wait_tmem;
+      p.dbg[blockIdx.x * 8 + 2] = t_wait_full;
     }
   } else {
     // ===================== epilogue (warps 2..9) =====================
@@ -335,36 +346,84 @@ __global__ void __launch_bounds__(320, 1)
     uint32_t aphase = 0;
     long long t_epi_wait = 0;
     const int ng_out = p.Nc / 8;
+    const int ng_half = (ng_out + 1) / 2;
     const bool domask = p.flags & VM_CONV_MASK;
+    const int et = threadIdx.x - 64;  // 0..255
+    __shared__ int s_last;
+    // bias, ReLU / mask, zero beyond Cout, bf16 store of 8 channels of one output row
+    auto emit = [&](bf16* ybase, int co0, float (&v)[8], const int4& mkv, int64_t orow) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (!(p.flags & VM_CONV_NOBIAS))
+          v[e] += (co0 + e < p.Cout) ? (bias_smem ? sbias[co0 + e] : __ldg(p.bias + co0 + e)) : 0.f;
+      }
+      if (p.flags & VM_CONV_RELU) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
+      }
+      if (domask) {
+        const __nv_bfloat162* mh = reinterpret_cast<const __nv_bfloat162*>(&mkv);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float2 f = __bfloat1622float2(mh[e]);
+          if (!(f.x > 0.f)) v[2 * e] = 0.f;
+          if (!(f.y > 0.f)) v[2 * e + 1] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (co0 + e >= p.Cout) v[e] = 0.f;
+      int4 out;
+      __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&out);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) oh[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+      *reinterpret_cast<int4*>(ybase + (co0 / 8) * p.plane8 + orow * 8) = out;
+    };
+    // output row of anchor a: (w, h) via multiply-high division (divisors are small)
+    auto anchor_row = [&](int a, bool& valid) -> int64_t {
+      uint32_t qa = __umulhi((uint32_t)a, p.wp_magic);
+      if (qa * (uint32_t)p.Wp > (uint32_t)a) --qa;
+      if ((qa + 1) * (uint32_t)p.Wp <= (uint32_t)a) ++qa;
+      const int wq = a - (int)qa * p.Wp;
+      uint32_t qh = __umulhi(qa, p.hp_magic);
+      if (qh * (uint32_t)p.Hp > qa) --qh;
+      if ((qh + 1) * (uint32_t)p.Hp <= qa) ++qh;
+      const int hq = (int)qa - (int)qh * p.Hp;
+      valid = a < p.anchors && wq < p.W && hq < p.H;
+      return (int64_t)a + p.P + p.Wp + 1;
+    };
+    const int ntu = p.units / p.ksplit;
+    const long long t_epi0 = clk();
+    long long t_fix = 0, t_pub = 0, t_arr = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      const int nch = u % p.nchunk;
-      const int mb = (u / p.nchunk) % p.mblocks;
-      const int b = u / (p.nchunk * p.mblocks);
+      const int ks = u % p.ksplit, tu = u / p.ksplit;
+      const int nch = tu % p.nchunk;
+      const int mb = (tu / p.nchunk) % p.mblocks;
+      const int b = tu / (p.nchunk * p.mblocks);
       const int a0 = mb * p.MB * 128;
+      const int s0 = ks * p.spk, nst = min(3 * p.KC, s0 + p.spk) - s0;
+      const int nsets = min(p.nacc, nst);  // accumulator sets this split wrote
+      const bool split = p.ksplit > 1;
       const bf16* mbase = p.mask + b * p.m_bstride;
       bf16* ybase = p.y + b * p.y_bstride;
       long long te0 = clk();
       mbar_wait(&tfull[ab], aphase);
       t_epi_wait += clk() - te0;
       tc_fence_after();
-      for (int i = half; i < p.MB; i += 2) {
-        const int a = a0 + i * 128 + q * 32 + lane;
-        // (w, h) of the anchor via multiply-high division (divisors are small)
-        uint32_t qa = __umulhi((uint32_t)a, p.wp_magic);
-        if (qa * (uint32_t)p.Wp > (uint32_t)a) --qa;
-        if ((qa + 1) * (uint32_t)p.Wp <= (uint32_t)a) ++qa;
-        const int wq = a - (int)qa * p.Wp;
-        uint32_t qh = __umulhi(qa, p.hp_magic);
-        if (qh * (uint32_t)p.Hp > qa) --qh;
-        if ((qh + 1) * (uint32_t)p.Hp <= qa) ++qh;
-        const int hq = (int)qa - (int)qh * p.Hp;
-        const bool valid = a < p.anchors && wq < p.W && hq < p.H;
-        const int64_t orow = (int64_t)a + p.P + p.Wp + 1;
+      // MB = 1: both warp halves drain the single tile, each half its own channel groups
+      const int glo = MB == 1 ? (half ? ng_half : 0) : 0, ghi = MB == 1 ? (half ? ng_out : ng_half) : ng_out;
+      for (int i = MB == 1 ? 0 : half; i < p.MB; i += MB == 1 ? 1 : 2) {
+        const int row = q * 32 + lane;
+        const int a = a0 + i * 128 + row;
+        bool valid;
+        const int64_t orow = anchor_row(a, valid);
         const uint32_t tcol = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * p.MB + i) * p.nacc * p.Nc);
-        for (int g0 = 0; g0 < ng_out; g0 += 8) {
-          const int gn = min(8, ng_out - g0);
+        // partial layout [ks][tu][tile][row][Nc]: a thread's channels are contiguous (float4 I/O)
+        float* wsp = split ? p.ws + ((((int64_t)ks * ntu + tu) * p.MB + i) * 128 + row) * p.Nc : nullptr;
+        for (int g0 = glo; g0 < ghi; g0 += 8) {
+          const int gn = min(8, ghi - g0);
           int4 mk[8];
-          if (domask) {  // issue the mask loads first (latency overlap)
+          if (domask && !split) {  // issue the mask loads first (latency overlap)
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const int co0 = nch * p.Nc + (g0 + j) * 8;
@@ -377,7 +436,7 @@ __global__ void __launch_bounds__(320, 1)
           for (int j = 0; j < 8; j += 2) {
             if (j >= gn) break;
             uint32_t r[16];
-            for (int a = 0; a < p.nacc; ++a) {  // sum the accumulator sets (fixed order)
+            for (int a = 0; a < nsets; ++a) {  // sum the accumulator sets (fixed order)
               uint32_t ra[16];
               const uint32_t ca = tcol + (uint32_t)(a * p.Nc + (g0 + j) * 8);
               if (j + 1 < gn) {
@@ -393,6 +452,15 @@ __global__ void __launch_bounds__(320, 1)
               for (int e = 0; e < 16; ++e)
                 r[e] = a == 0 ? ra[e] : __float_as_uint(__uint_as_float(r[e]) + __uint_as_float(ra[e]));
             }
+            if (split) {  // f32 partial of 8 or 16 channels of this row
+              float4* dst = reinterpret_cast<float4*>(wsp + (g0 + j) * 8);
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (e < 2 || j + 1 < gn)
+                  __stcg(dst + e, make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]),
+                                              __uint_as_float(r[4 * e + 2]), __uint_as_float(r[4 * e + 3])));
+              continue;
+            }
 #pragma unroll
             for (int jj = 0; jj < 2; ++jj) {
               if (j + jj >= gn) break;
@@ -400,32 +468,8 @@ __global__ void __launch_bounds__(320, 1)
               if (!valid || co0 >= p.Cout) continue;
               float v[8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                v[e] = __uint_as_float(r[jj * 8 + e]);
-                if (!(p.flags & VM_CONV_NOBIAS))
-                  v[e] += (co0 + e < p.Cout) ? (bias_smem ? sbias[co0 + e] : __ldg(p.bias + co0 + e)) : 0.f;
-              }
-              if (p.flags & VM_CONV_RELU) {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
-              }
-              if (domask) {
-                const __nv_bfloat162* mh = reinterpret_cast<const __nv_bfloat162*>(&mk[j + jj]);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  float2 f = __bfloat1622float2(mh[e]);
-                  if (!(f.x > 0.f)) v[2 * e] = 0.f;
-                  if (!(f.y > 0.f)) v[2 * e + 1] = 0.f;
-                }
-              }
-#pragma unroll
-              for (int e = 0; e < 8; ++e)
-                if (co0 + e >= p.Cout) v[e] = 0.f;
-              int4 out;
-              __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&out);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) oh[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
-              *reinterpret_cast<int4*>(ybase + (co0 / 8) * p.plane8 + orow * 8) = out;
+              for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[jj * 8 + e]);
+              emit(ybase, co0, v, mk[j + jj], orow);
             }
           }
         }
@@ -436,8 +480,57 @@ __global__ void __launch_bounds__(320, 1)
         ab = 0;
         aphase ^= 1;
       }
+      if (split) {
+        // publish this split's partial; the last split of the tile unit finishes it
+        const long long tpa = clk();
+        __threadfence();
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (et == 0) s_last = atomicAdd(p.counters + tu, 1) == p.ksplit - 1;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        t_pub += clk() - tpa;
+        t_arr = clk() - t_epi0;
+        if (s_last) {
+          const long long tfx = clk();
+          __threadfence();
+          for (int i = MB == 1 ? 0 : half; i < p.MB; i += MB == 1 ? 1 : 2) {
+            const int row = q * 32 + lane;
+            bool valid;
+            const int64_t orow = anchor_row(a0 + i * 128 + row, valid);
+            if (valid) {
+#pragma unroll 4
+              for (int g = glo; g < ghi; ++g) {
+                const int co0 = nch * p.Nc + g * 8;
+                if (co0 >= p.Cout) break;
+                int4 mkv = make_int4(0, 0, 0, 0);
+                if (domask) mkv = __ldg(reinterpret_cast<const int4*>(mbase + (co0 / 8) * p.plane8 + orow * 8));
+                float v[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[e] = 0.f;
+#pragma unroll
+                for (int k = 0; k < kFwdMaxSplit; ++k) {  // split order: deterministic
+                  if (k >= p.ksplit) break;
+                  const float4* src = reinterpret_cast<const float4*>(
+                      p.ws + ((((int64_t)k * ntu + tu) * p.MB + i) * 128 + row) * p.Nc + g * 8);
+                  const float4 lo = __ldcg(src), hi = __ldcg(src + 1);
+                  v[0] += lo.x, v[1] += lo.y, v[2] += lo.z, v[3] += lo.w;
+                  v[4] += hi.x, v[5] += hi.y, v[6] += hi.z, v[7] += hi.w;
+                }
+                emit(ybase, co0, v, mkv, orow);
+              }
+            }
+          }
+          if (et == 0) p.counters[tu] = 0;  // ready for the next launch
+          t_fix += clk() - tfx;
+        }
+      }
     }
-    if (p.dbg && threadIdx.x == 64) p.dbg[blockIdx.x * 4 + 3] = t_epi_wait;
+    if (p.dbg && threadIdx.x == 64) {
+      p.dbg[blockIdx.x * 8 + 3] = t_epi_wait;
+      p.dbg[blockIdx.x * 8 + 4] = clk() - t_epi0;
+      p.dbg[blockIdx.x * 8 + 5] = t_fix;
+      p.dbg[blockIdx.x * 8 + 6] = t_pub;
+      p.dbg[blockIdx.x * 8 + 7] = t_arr;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -1573,10 +1666,50 @@ static int launch_sweep(const FwdParams& f, int nsm, void* stream) {
 
 extern "C" void vm_debug_set_fwd_probe(long long* buf) { g_fwd_dbg = buf; }
 
+// Split-K workspace of the general forward kernel: [tile-unit counters (256 B aligned)]
+// [f32 partials ksplit x tile units x MB x Nc x 128].  Zeroed once by the caller.
+static size_t fwd_ws_need(int ksplit, int64_t ntu, int MB, int Nc) {
+  if (ksplit <= 1) return 0;
+  return (size_t)((ntu * 4 + 255) / 256 * 256) + (size_t)ksplit * ntu * MB * Nc * 128 * sizeof(float);
+}
+// Split-K is off by default: measured on B200 it loses at every deep-level shape of the cfg2
+// ladder (128->128 @16^3: 19.1 us unsplit, 24.9 / 26.6 us with 2 / 3 splits — the partial
+// round trip and the last split's fix-up cost more than the shorter K loop saves).
+static int g_fwd_max_split = 1;  // vm_debug_set_fwd_max_split (A/B probes, tests)
+extern "C" void vm_debug_set_fwd_max_split(int v) { g_fwd_max_split = v < 1 ? 1 : v > kFwdMaxSplit ? kFwdMaxSplit : v; }
+
+static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, const float* bias, void* y,
+                         int64_t y_bstride, const void* mask, int64_t mask_bstride, int B, int Cin, int Cout, int D,
+                         int H, int W, unsigned flags, void* ws, size_t ws_bytes, void* stream);
+
 extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wpacked,
                                 const float* bias, void* y, int64_t y_bstride, const void* mask,
                                 int64_t mask_bstride, int B, int Cin, int Cout, int D, int H, int W,
                                 unsigned flags, void* stream) {
+  return fwd_tc_launch(x, x_bstride, wpacked, bias, y, y_bstride, mask, mask_bstride, B, Cin, Cout, D, H, W, flags,
+                       nullptr, 0, stream);
+}
+
+extern "C" int vm_conv3d_fwd_tc_ws(const void* x, int64_t x_bstride, const void* wpacked, const float* bias,
+                                   void* y, int64_t y_bstride, const void* mask, int64_t mask_bstride, int B,
+                                   int Cin, int Cout, int D, int H, int W, unsigned flags, void* ws,
+                                   size_t ws_bytes, void* stream) {
+  return fwd_tc_launch(x, x_bstride, wpacked, bias, y, y_bstride, mask, mask_bstride, B, Cin, Cout, D, H, W, flags,
+                       ws, ws_bytes, stream);
+}
+
+// Upper bound of the split-K workspace any plan of this shape may use (0: never splits).
+extern "C" size_t vm_conv3d_fwd_tc_ws_bytes(int B, int Cin, int Cout, int D, int H, int W) {
+  const PackGeom pg = pack_geom(Cin, Cout);
+  if (pg.sweep) return 0;
+  const int64_t tiles = ((int64_t)D * (H + 2) * (W + 2) + 127) / 128;
+  // MB tiles per unit round the tile count up by < MB tiles: bound by MB = 1 plus 8 tiles
+  return fwd_ws_need(kFwdMaxSplit, (int64_t)B * (tiles + 8) * pg.nchunk, 1, pg.Nc) + 256;
+}
+
+static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, const float* bias, void* y,
+                         int64_t y_bstride, const void* mask, int64_t mask_bstride, int B, int Cin, int Cout, int D,
+                         int H, int W, unsigned flags, void* ws, size_t ws_bytes, void* stream) {
   VM_REQUIRE(x && wpacked && y, VM_E_ARG, "vm_conv3d_fwd_tc: null pointer");
   VM_REQUIRE((flags & VM_CONV_NOBIAS) || bias, VM_E_ARG, "vm_conv3d_fwd_tc: bias required");
   VM_REQUIRE(!(flags & VM_CONV_MASK) || mask, VM_E_ARG, "vm_conv3d_fwd_tc: mask required");
@@ -1631,7 +1764,7 @@ extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wp
     return bw > 68 ? bw * 1.5 : 68;
   };
   double best = 1e30;
-  int bMB = 1, bacc = 1, bbuf = 1, bstages = 0;
+  int bMB = 1, bacc = 1, bbuf = 1, bstages = 0, bsplit = 1;
   for (int MB = 1; MB <= 8; ++MB) {
     const int R = MB * 128 + 2 * p.Wp + 2;
     const uint32_t a_bytes = (uint32_t)((R + 7) / 8 * 8) * 16;
@@ -1639,20 +1772,31 @@ extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wp
     int stages = kSmemBudget / (int)stage_bytes;
     if (stages > kMaxStages) stages = kMaxStages;
     if (stages < 2) continue;
-    const int64_t units = (int64_t)B * ((tiles + MB - 1) / MB) * p.nchunk;
-    const int64_t waves = (units + nsm - 1) / nsm;
-    for (int nacc : {1, 3}) {
-      for (int nbuf = 2; nbuf >= 1; --nbuf) {
-        if (nbuf * MB * nacc * N > 512) continue;
-        const double mma = 9.0 * MB * mma_cycles(N, MB * nacc);
-        const double smem = (2.0 * R * 16 + p.b_bytes + 9.0 * MB * (4096 + 32.0 * N)) / 128.0;
-        const double stage = mma > smem ? mma : smem;
-        // single-buffered TMEM: the epilogue drain (~MB*N/8 x 200 cycles) is not overlapped
-        const double drain = nbuf == 1 ? MB * (N / 8.0) * 200.0 / (MB > 1 ? 2 : 1) : 0.0;
-        const double cost = (double)waves * (3.0 * p.KC * stage + drain + 2000.0);
-        if (cost < best * 0.999) {
-          best = cost;
-          bMB = MB, bacc = nacc, bbuf = nbuf, bstages = stages;
+    const int64_t ntu = (int64_t)B * ((tiles + MB - 1) / MB) * p.nchunk;
+    // split-K over the 3*KC (kc, kd) stages when a caller workspace can hold the f32
+    // partials: more CTAs for layers with few tiles (deep levels)
+    for (int ksplit = 1; ksplit <= g_fwd_max_split; ++ksplit) {
+      const int spk = (3 * p.KC + ksplit - 1) / ksplit;
+      if (ksplit > 1 &&
+          ((3 * p.KC + spk - 1) / spk != ksplit || !ws || fwd_ws_need(ksplit, ntu, MB, N) > ws_bytes))
+        continue;
+      const int64_t units = ntu * ksplit;
+      const int64_t waves = (units + nsm - 1) / nsm;
+      for (int nacc : {1, 3}) {
+        for (int nbuf = 2; nbuf >= 1; --nbuf) {
+          if (nbuf * MB * nacc * N > 512) continue;
+          const double mma = 9.0 * MB * mma_cycles(N, MB * nacc);
+          const double smem = (2.0 * R * 16 + p.b_bytes + 9.0 * MB * (4096 + 32.0 * N)) / 128.0;
+          const double stage = mma > smem ? mma : smem;
+          // single-buffered TMEM: the epilogue drain (~MB*N/8 x 200 cycles) is not overlapped
+          const double drain = nbuf == 1 ? MB * (N / 8.0) * 200.0 / (MB > 1 ? 2 : 1) : 0.0;
+          // split: partial write + the last split's read-back of every partial
+          const double fix = ksplit > 1 ? MB * (N / 8.0) * (150.0 + 100.0 * ksplit) : 0.0;
+          const double cost = (double)waves * ((double)spk * stage + drain + fix + 2000.0);
+          if (cost < best * 0.999) {
+            best = cost;
+            bMB = MB, bacc = nacc, bbuf = nbuf, bstages = stages, bsplit = ksplit;
+          }
         }
       }
     }
@@ -1667,7 +1811,14 @@ extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wp
   p.stage_bytes = 2 * p.a_bytes + p.b_bytes;
   p.stages = bstages;
   p.mblocks = (tiles + p.MB - 1) / p.MB;
-  p.units = B * p.mblocks * p.nchunk;
+  p.ksplit = bsplit;
+  p.spk = (3 * p.KC + bsplit - 1) / bsplit;
+  p.units = B * p.mblocks * p.nchunk * bsplit;
+  if (bsplit > 1) {
+    const int64_t ntu = (int64_t)B * p.mblocks * p.nchunk;
+    p.counters = static_cast<int*>(ws);
+    p.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + (ntu * 4 + 255) / 256 * 256);
+  }
   p.idesc = make_idesc_bf16(128, N, false, false);
   (void)rows;
   const size_t smem = (size_t)p.stages * p.stage_bytes;

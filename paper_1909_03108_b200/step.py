@@ -198,6 +198,16 @@ class UNetStep:
                 L.ws_bytes = int(_lib.call_size(ws_fn, self.B, L.cin, L.cout, L.D, L.H, L.W))
         self.wgrad_ws = torch.empty(max([L.ws_bytes for L in self.layers if L.k == 3] + [16]) // 4 + 4,
                                     dtype=torch.float32, device=dev)
+        # split-K scratch of the general forward/dgrad kernel (deep levels); zeroed once, its
+        # tile counters return to zero after every launch.  Main stream only.
+        conv_ws = [16]
+        if self.conv_impl == "tc":
+            for L in self.layers:
+                if L.k == 3:
+                    for ci, co in ((L.cin, L.cout), (L.cout, L.cin)):
+                        conv_ws.append(int(_lib.call_size("vm_conv3d_fwd_tc_ws_bytes", self.B, ci, co, L.D, L.H, L.W)))
+        self.conv_ws_bytes = max(conv_ws)
+        self.conv_ws = torch.zeros(self.conv_ws_bytes // 4 + 64, dtype=torch.float32, device=dev)
 
         # activation slabs -------------------------------------------------
         self.out = {}  # node id -> Slab holding that node's output (relu shares its conv's slab)
@@ -319,8 +329,9 @@ class UNetStep:
         nbytes = 2.0 * vox * (cin + cout + (cout if mask is not None else 0))
         if self.conv_impl == "tc":
             w = L.wpt if dgrad else L.wp
-            self._k(kind, L.node.id, self._conv_flops(L), nbytes, "vm_conv3d_fwd_tc", x.p(), x.bstride,
-                    _lib.ptr(w), _lib.ptr(L.b), y.p(), y.bstride, mp, mb, self.B, cin, cout, L.D, L.H, L.W, flags)
+            self._k(kind, L.node.id, self._conv_flops(L), nbytes, "vm_conv3d_fwd_tc_ws", x.p(), x.bstride,
+                    _lib.ptr(w), _lib.ptr(L.b), y.p(), y.bstride, mp, mb, self.B, cin, cout, L.D, L.H, L.W, flags,
+                    _lib.ptr(self.conv_ws), self.conv_ws_bytes)
         else:
             w = L.wt if dgrad else L.w
             self._k(kind, L.node.id, self._conv_flops(L), nbytes, "vm_conv3d_fwd_simt", self.dt, x.p(), x.bstride,

@@ -246,3 +246,44 @@ def test_survey_abi_names_are_the_kernels():
               B, cin, cout, D, H, W, _lib.stream_ptr())
     torch.cuda.synchronize()
     assert np.array_equal(gw2.cpu().numpy().reshape(gw1.shape), gw1) and np.array_equal(gb2.cpu().numpy(), gb1)
+
+
+@pytest.mark.parametrize("shape", [(1, 128, 128, 16, 16, 16), (1, 64, 128, 8, 8, 8), (2, 128, 64, 8, 8, 8),
+                                   (1, 256, 512, 4, 4, 4)])
+def test_tc_forward_split_k_workspace(shape):
+    # vm_conv3d_fwd_tc_ws: deep-level shapes split the K reduction over CTAs with f32 partials
+    # in the caller's scratch; the last split of each tile sums them in split order
+    B, cin, cout, D, H, W = shape
+    rng = np.random.default_rng(7 + sum(shape))
+    x = O.bf16_round(rng.standard_normal((B, D, H, W, cin)).astype(np.float32))
+    w = O.bf16_round(rng.uniform(-1, 1, (3, 3, 3, cin, cout)).astype(np.float32) / np.sqrt(27 * cin))
+    b = rng.standard_normal(cout).astype(np.float32) * 0.1
+    m = O.bf16_round(rng.standard_normal((B, D, H, W, cout)).astype(np.float32))
+    xs, ms = _slab_from(x), _slab_from(m)
+    wt = torch.from_numpy(np.ascontiguousarray(w, np.float32)).cuda()
+    wp = torch.empty(_lib.call_size("vm_packed_weights_bytes", cin, cout) // 2, dtype=torch.bfloat16, device="cuda")
+    _lib.call("vm_pack_weights", _lib.ptr(wt), _lib.ptr(wp), cin, cout, 0, _lib.stream_ptr())
+    bt = torch.from_numpy(b).cuda()
+    nbytes = _lib.call_size("vm_conv3d_fwd_tc_ws_bytes", B, cin, cout, D, H, W)
+    assert nbytes > 0
+    ws = torch.zeros(nbytes // 4 + 64, dtype=torch.float32, device="cuda")
+    flags = _lib.VM_CONV_RELU | _lib.VM_CONV_MASK
+    outs = []
+    _lib.load().vm_debug_set_fwd_max_split(3)  # split-K is off by default (slower on B200)
+    for use_ws in (False, True, True):
+        ys = Slab(B, cout, D, H, W, torch.bfloat16, "cuda")
+        if use_ws:
+            _lib.call("vm_conv3d_fwd_tc_ws", xs.p(), xs.bstride, _lib.ptr(wp), _lib.ptr(bt), ys.p(), ys.bstride,
+                      ms.p(), ms.bstride, B, cin, cout, D, H, W, flags, _lib.ptr(ws), nbytes, _lib.stream_ptr())
+        else:
+            _lib.call("vm_conv3d_fwd_tc", xs.p(), xs.bstride, _lib.ptr(wp), _lib.ptr(bt), ys.p(), ys.bstride,
+                      ms.p(), ms.bstride, B, cin, cout, D, H, W, flags, _lib.stream_ptr())
+        outs.append(ys.interior().cpu().numpy())
+    _lib.load().vm_debug_set_fwd_max_split(1)
+    assert np.array_equal(outs[1], outs[2])          # deterministic
+    assert rel_l2(outs[1], outs[0]) <= 5e-3          # same math, other f32 summation order
+    dense = np.maximum(O.conv3d_dense(x.astype(np.float64), w.astype(np.float64), b.astype(np.float64)), 0)
+    dense = np.where(m > 0, dense, 0)
+    assert rel_l2(outs[1], dense) <= 1e-2
+    nz = int(torch.count_nonzero(ws[:64]).item())  # tile counters (first 256 B) are back to zero
+    assert nz == 0
