@@ -210,8 +210,9 @@ template <int MB, bool DBG>  // DBG: cycle probes (tools/dbg_fwd_probe.py)
 __global__ void __launch_bounds__(320, 1)
     k_conv_fwd_tc(const FwdParams p) {
   auto clk = []() -> long long { return DBG ? (long long)clock64() : 0LL; };
+  const long long t_kstart = clk();
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ float sbias[1024];  // Cout <= 1024; wider layers read the bias through L1
+  __shared__ __align__(16) float sbias[1024];  // Cout <= 1024 (zero-padded to 8); wider: L1
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -340,7 +341,8 @@ __global__ void __launch_bounds__(320, 1)
     const int half = (warp - 2) >> 2;
     const bool bias_smem = p.Cout <= 1024;
     if (!(p.flags & VM_CONV_NOBIAS) && bias_smem)
-      for (int c = threadIdx.x - 64; c < p.Cout; c += 256) sbias[c] = p.bias[c];
+      for (int c = threadIdx.x - 64; c < min(1024, (p.Cout + 7) / 8 * 8); c += 256)
+        sbias[c] = c < p.Cout ? p.bias[c] : 0.f;
     asm volatile("bar.sync 1, 256;" ::: "memory");
     int ab = 0;
     uint32_t aphase = 0;
@@ -350,14 +352,27 @@ __global__ void __launch_bounds__(320, 1)
     const bool domask = p.flags & VM_CONV_MASK;
     const int et = threadIdx.x - 64;  // 0..255
     __shared__ int s_last;
-    // bias, ReLU / mask, zero beyond Cout, bf16 store of 8 channels of one output row
+    // bias, ReLU / mask, zero beyond Cout, bf16 store of 8 channels of one output row.  Kept
+    // free of per-element branches: the drain is instruction-bound (8 warps x 8 channels per
+    // call), and the per-element bias/bound selects made it ~500 instructions per 16 channels.
+    const bool nobias = p.flags & VM_CONV_NOBIAS;
+    const bool relu = p.flags & VM_CONV_RELU;
+    const bool cout8 = (p.Cout & 7) == 0;
     auto emit = [&](bf16* ybase, int co0, float (&v)[8], const int4& mkv, int64_t orow) {
+      if (!nobias) {
+        float bb[8];
+        if (bias_smem) {
+          const float4 b0 = *reinterpret_cast<const float4*>(&sbias[co0]);
+          const float4 b1 = *reinterpret_cast<const float4*>(&sbias[co0 + 4]);
+          bb[0] = b0.x, bb[1] = b0.y, bb[2] = b0.z, bb[3] = b0.w, bb[4] = b1.x, bb[5] = b1.y, bb[6] = b1.z, bb[7] = b1.w;
+        } else {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        if (!(p.flags & VM_CONV_NOBIAS))
-          v[e] += (co0 + e < p.Cout) ? (bias_smem ? sbias[co0 + e] : __ldg(p.bias + co0 + e)) : 0.f;
+          for (int e = 0; e < 8; ++e) bb[e] = co0 + e < p.Cout ? __ldg(p.bias + co0 + e) : 0.f;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] += bb[e];
       }
-      if (p.flags & VM_CONV_RELU) {
+      if (relu) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.f);
       }
@@ -366,18 +381,19 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           float2 f = __bfloat1622float2(mh[e]);
-          if (!(f.x > 0.f)) v[2 * e] = 0.f;
-          if (!(f.y > 0.f)) v[2 * e + 1] = 0.f;
+          v[2 * e] = f.x > 0.f ? v[2 * e] : 0.f;
+          v[2 * e + 1] = f.y > 0.f ? v[2 * e + 1] : 0.f;
         }
       }
+      if (!cout8) {
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (co0 + e >= p.Cout) v[e] = 0.f;
+        for (int e = 0; e < 8; ++e) v[e] = co0 + e < p.Cout ? v[e] : 0.f;
+      }
       int4 out;
       __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&out);
 #pragma unroll
       for (int e = 0; e < 4; ++e) oh[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
-      *reinterpret_cast<int4*>(ybase + (co0 / 8) * p.plane8 + orow * 8) = out;
+      if (!(p.flags & (1u << 9))) *reinterpret_cast<int4*>(ybase + (co0 / 8) * p.plane8 + orow * 8) = out;  // DBG bit 9: no store
     };
     // output row of anchor a: (w, h) via multiply-high division (divisors are small)
     auto anchor_row = [&](int a, bool& valid) -> int64_t {
@@ -394,7 +410,7 @@ __global__ void __launch_bounds__(320, 1)
     };
     const int ntu = p.units / p.ksplit;
     const long long t_epi0 = clk();
-    long long t_fix = 0, t_pub = 0, t_arr = 0;
+    long long t_fix = 0, t_pub = 0, t_arr = 0, t_drain = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       const int ks = u % p.ksplit, tu = u / p.ksplit;
       const int nch = tu % p.nchunk;
@@ -408,11 +424,13 @@ __global__ void __launch_bounds__(320, 1)
       bf16* ybase = p.y + b * p.y_bstride;
       long long te0 = clk();
       mbar_wait(&tfull[ab], aphase);
-      t_epi_wait += clk() - te0;
+      const long long taw = clk();
+      t_epi_wait += taw - te0;
       tc_fence_after();
       // MB = 1: both warp halves drain the single tile, each half its own channel groups
       const int glo = MB == 1 ? (half ? ng_half : 0) : 0, ghi = MB == 1 ? (half ? ng_out : ng_half) : ng_out;
       for (int i = MB == 1 ? 0 : half; i < p.MB; i += MB == 1 ? 1 : 2) {
+        if (p.flags & (1u << 11)) break;  // DBG bit 11: skip the drain
         const int row = q * 32 + lane;
         const int a = a0 + i * 128 + row;
         bool valid;
@@ -435,8 +453,12 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
           for (int j = 0; j < 8; j += 2) {
             if (j >= gn) break;
-            uint32_t r[16];
-            for (int a = 0; a < nsets; ++a) {  // sum the accumulator sets (fixed order)
+            // sum the accumulator sets in fixed order; the set loop is unrolled (a runtime
+            // bound made the compiler rotate all 16 sums through moves every iteration)
+            float r[16];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+              if (a >= nsets) break;
               uint32_t ra[16];
               const uint32_t ca = tcol + (uint32_t)(a * p.Nc + (g0 + j) * 8);
               if (j + 1 < gn) {
@@ -446,19 +468,18 @@ __global__ void __launch_bounds__(320, 1)
                 tmem_ld8(ca, r8);
 #pragma unroll
                 for (int e = 0; e < 8; ++e) ra[e] = r8[e];
+#pragma unroll
+                for (int e = 8; e < 16; ++e) ra[e] = 0u;
               }
               tmem_ld_wait();
 #pragma unroll
-              for (int e = 0; e < 16; ++e)
-                r[e] = a == 0 ? ra[e] : __float_as_uint(__uint_as_float(r[e]) + __uint_as_float(ra[e]));
+              for (int e = 0; e < 16; ++e) r[e] = a == 0 ? __uint_as_float(ra[e]) : r[e] + __uint_as_float(ra[e]);
             }
             if (split) {  // f32 partial of 8 or 16 channels of this row
               float4* dst = reinterpret_cast<float4*>(wsp + (g0 + j) * 8);
 #pragma unroll
               for (int e = 0; e < 4; ++e)
-                if (e < 2 || j + 1 < gn)
-                  __stcg(dst + e, make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]),
-                                              __uint_as_float(r[4 * e + 2]), __uint_as_float(r[4 * e + 3])));
+                if (e < 2 || j + 1 < gn) __stcg(dst + e, make_float4(r[4 * e], r[4 * e + 1], r[4 * e + 2], r[4 * e + 3]));
               continue;
             }
 #pragma unroll
@@ -468,12 +489,13 @@ __global__ void __launch_bounds__(320, 1)
               if (!valid || co0 >= p.Cout) continue;
               float v[8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[jj * 8 + e]);
+              for (int e = 0; e < 8; ++e) v[e] = r[jj * 8 + e];
               emit(ybase, co0, v, mk[j + jj], orow);
             }
           }
         }
       }
+      t_drain += clk() - taw;
       tc_fence_before();
       mbar_arrive(&tempty[ab]);
       if (++ab == p.nbuf) {
@@ -528,8 +550,8 @@ __global__ void __launch_bounds__(320, 1)
       p.dbg[blockIdx.x * 8 + 3] = t_epi_wait;
       p.dbg[blockIdx.x * 8 + 4] = clk() - t_epi0;
       p.dbg[blockIdx.x * 8 + 5] = t_fix;
-      p.dbg[blockIdx.x * 8 + 6] = t_pub;
-      p.dbg[blockIdx.x * 8 + 7] = t_arr;
+      p.dbg[blockIdx.x * 8 + 6] = p.ksplit > 1 ? t_pub : t_drain;
+      p.dbg[blockIdx.x * 8 + 7] = p.ksplit > 1 ? t_arr : t_epi0 - t_kstart;
     }
   }
   tc_fence_before();
