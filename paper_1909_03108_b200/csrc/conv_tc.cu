@@ -928,7 +928,7 @@ constexpr int kSwMaxStages = 8;
 
 // Warps: 0 producer, 1 and 10 MMA issuers (tiles t = 0, 2, .. and 1, 3, ..: a single issuing
 // thread's per-plane bookkeeping otherwise leaves the tensor core idle), 2..9 epilogue.
-template <int MB, bool DBG>  // DBG: cycle probes (tools/dbg_sweep_probe.py); off in production
+template <int MB, bool DBG, int NG>  // NG = Nc/8 channel groups; DBG: cycle probes (tools/dbg_sweep_probe.py)
 __global__ void __launch_bounds__(352, 1)
     k_conv_fwd_sweep(const SwParams p) {
   auto clk = []() -> long long { return DBG ? (long long)clock64() : 0LL; };
@@ -936,7 +936,7 @@ __global__ void __launch_bounds__(352, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t full[kSwMaxStages], empty[kSwMaxStages], tfull[kSwMaxRing], tempty[kSwMaxRing], wbar;
   __shared__ uint32_t tslot;
-  __shared__ float sbias[kSweepMaxNc];
+  __shared__ __align__(16) float sbias[kSweepMaxNc];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   uint8_t* sW = smem;
   uint8_t* sStage = smem + p.w_bytes;
@@ -1173,8 +1173,10 @@ __global__ void __launch_bounds__(352, 1)
     const int h = (warp - 2) >> 2;
     // tiles t = h, h+2, ... of every block (MB = 1: both halves share the tile, split by group)
     constexpr int TPT = MB == 1 ? 1 : (MB + 1) / 2;  // tiles per thread (max)
-    constexpr int GPT = MB == 1 ? kSweepMaxNc / 16 : kSweepMaxNc / 8;  // channel groups per thread (max)
-    const int ngrp = p.Nc / 8;
+    // channel groups per thread: compile-time, so the TMEM, mask and prefetch arrays hold
+    // exactly the groups this layer has (sized for Nc = 48 they spilled at MB = 3, 4)
+    constexpr int GPT = MB == 1 ? (NG + 1) / 2 : NG;
+    constexpr int ngrp = NG;
     const int g_lo = MB == 1 ? h : 0, g_step = MB == 1 ? 2 : 1;  // channel groups of this thread
     const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
     const bool nobias = p.flags & VM_CONV_NOBIAS;
@@ -1240,22 +1242,30 @@ __global__ void __launch_bounds__(352, 1)
             if (t >= MB) break;
             const int64_t orow = orow0[k] + (int64_t)o * p.P;
             const uint32_t tcol = lane_base + (uint32_t)((t * p.ring + (int)r) * p.Nc);
+            // every group of this tile in flight before one wait
+            uint32_t rr[GPT][8];
+#pragma unroll
+            for (int gi = 0; gi < GPT; ++gi) {
+              const int g = g_lo + gi * g_step;
+              if (g < ngrp && g * 8 < p.Cout) tmem_ld8(tcol + (uint32_t)(g * 8), rr[gi]);
+            }
+            tmem_ld_wait();
 #pragma unroll
             for (int gi = 0; gi < GPT; ++gi) {
               const int g = g_lo + gi * g_step;
               if (g >= ngrp || g * 8 >= p.Cout) break;
-              uint32_t rr[8];
-              tmem_ld8(tcol + (uint32_t)(g * 8), rr);
-              tmem_ld_wait();
+              const float4 b0 = *reinterpret_cast<const float4*>(&sbias[g * 8]);
+              const float4 b1 = *reinterpret_cast<const float4*>(&sbias[g * 8 + 4]);
+              const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
               float v[8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(rr[e]) + sbias[g * 8 + e];
+              for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(rr[gi][e]) + bb[e];
               if (p.flags & VM_CONV_MASK) {
                 const uint32_t* mw = reinterpret_cast<const uint32_t*>(&mk[k][gi]);
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                  if (!((int16_t)(mw[e] & 0xFFFFu) > 0)) v[2 * e] = 0.f;
-                  if (!((int16_t)(mw[e] >> 16) > 0)) v[2 * e + 1] = 0.f;
+                  v[2 * e] = (int16_t)(mw[e] & 0xFFFFu) > 0 ? v[2 * e] : 0.f;
+                  v[2 * e + 1] = (int16_t)(mw[e] >> 16) > 0 ? v[2 * e + 1] : 0.f;
                 }
               }
               int4 out;
@@ -1677,10 +1687,14 @@ static int launch_sweep(const FwdParams& f, int nsm, void* stream) {
   const size_t smem = (size_t)p.w_bytes + (size_t)p.stages * p.stage_bytes;
   const int grid = p.units < nsm ? p.units : nsm;
   const bool dbg = p.dbg != nullptr;
-  auto kern = p.MB == 4 ? (dbg ? k_conv_fwd_sweep<4, true> : k_conv_fwd_sweep<4, false>)
-            : p.MB == 3 ? (dbg ? k_conv_fwd_sweep<3, true> : k_conv_fwd_sweep<3, false>)
-            : p.MB == 2 ? (dbg ? k_conv_fwd_sweep<2, true> : k_conv_fwd_sweep<2, false>)
-                        : (dbg ? k_conv_fwd_sweep<1, true> : k_conv_fwd_sweep<1, false>);
+  using SwKern = void (*)(const SwParams);
+#define SW_ROW(MB_)                                                                                   \
+  {k_conv_fwd_sweep<MB_, false, 2>, k_conv_fwd_sweep<MB_, false, 4>, k_conv_fwd_sweep<MB_, false, 6>, \
+   k_conv_fwd_sweep<MB_, true, 2>, k_conv_fwd_sweep<MB_, true, 4>, k_conv_fwd_sweep<MB_, true, 6>}
+  static const SwKern table[4][6] = {SW_ROW(1), SW_ROW(2), SW_ROW(3), SW_ROW(4)};
+#undef SW_ROW
+  VM_REQUIRE(p.Nc == 16 || p.Nc == 32 || p.Nc == 48, VM_E_UNSUPPORTED, "sweep conv: Nc %d", p.Nc);
+  auto kern = table[p.MB - 1][(dbg ? 3 : 0) + p.Nc / 16 - 1];
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   launch_pdl(kern, grid, 352, smem, as_stream(stream), p);
   return launch_status("vm_conv3d_fwd_tc (sweep)");
