@@ -142,6 +142,20 @@ int vm_conv3d_fwd_tc_ws(const void* x, int64_t x_bstride, const void* wpacked, c
                         int Cin, int Cout, int D, int H, int W, unsigned flags, void* ws,
                         size_t ws_bytes, void* stream);
 size_t vm_conv3d_fwd_tc_ws_bytes(int B, int Cin, int Cout, int D, int H, int W);
+
+/* Single-input-channel conv (the first U-Net conv on the CT volume, conv3d_local ops.py:69-97
+ * and conv3d_param_grads_local ops.py:117-138 with Cin = 1): im2col tcgen05 GEMMs with the 27
+ * taps as K.  x is the compact padded input [B][(D+2)(H+2)(W+2)] bf16 with zero margins
+ * (vm_dense_to_compact1; x_bstride in elements, 0 = packed), w the fp32 reference kernel
+ * [3][3][3][1][Cout] (converted to bf16 in-kernel: no packing), Cout <= 32.  flags: RELU /
+ * NOBIAS (no MASK).  The weight gradient is deterministic (per-CTA TMEM partials summed in
+ * CTA order); gb comes from a ones column of the im2col tile. */
+int vm_conv3d_fwd_c1(const void* x, int64_t x_bstride, const float* w, const float* bias, void* y,
+                     int64_t y_bstride, int B, int Cout, int D, int H, int W, unsigned flags, void* stream);
+size_t vm_conv3d_wgrad_c1_ws(int B, int Cout, int D, int H, int W);
+int vm_dense_to_compact1(const float* src, void* dst, int B, int D, int H, int W, void* stream);
+int vm_conv3d_wgrad_c1(const void* x, int64_t x_bstride, const void* gy, int64_t gy_bstride, float* gw,
+                       float* gb, void* ws, int B, int Cout, int D, int H, int W, void* stream);
 size_t vm_conv3d_wgrad_tc_ws(int B, int Cin, int Cout, int D, int H, int W);
 int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* gy, int64_t gy_bstride,
                        float* gw, float* gb, void* ws, int B, int Cin, int Cout, int D, int H,

@@ -53,6 +53,10 @@ _SIGS = {
     "vm_conv3d_fwd_tc": (_I, [_P, _L, _P, _P, _P, _L, _P, _L, _I, _I, _I, _I, _I, _I, _U, _P]),
     "vm_conv3d_fwd_tc_ws": (_I, [_P, _L, _P, _P, _P, _L, _P, _L, _I, _I, _I, _I, _I, _I, _U, _P, _S, _P]),
     "vm_conv3d_fwd_tc_ws_bytes": (_S, [_I, _I, _I, _I, _I, _I]),
+    "vm_conv3d_fwd_c1": (_I, [_P, _L, _P, _P, _P, _L, _I, _I, _I, _I, _I, _U, _P]),
+    "vm_conv3d_wgrad_c1_ws": (_S, [_I, _I, _I, _I, _I]),
+    "vm_dense_to_compact1": (_I, [_P, _P, _I, _I, _I, _I, _P]),
+    "vm_conv3d_wgrad_c1": (_I, [_P, _L, _P, _L, _P, _P, _P, _I, _I, _I, _I, _I, _P]),
     "vm_conv3d_wgrad_tc_ws": (ctypes.c_size_t, [_I, _I, _I, _I, _I, _I]),
     "vm_conv3d_wgrad_tc": (_I, [_P, _L, _P, _L, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     "vm_maxpool2_fwd": (_I, [_I, _P, _L, _P, _L, _I, _I, _I, _I, _I, _P]),

@@ -335,6 +335,35 @@ extern "C" int vm_dense_to_slab(const void* src, int src_dtype, void* slab, int 
   return launch_status("vm_dense_to_slab");
 }
 
+// Single-channel input in the compact padded layout [B][(D+2)(H+2)(W+2)] bf16 (zero margins):
+// the operand of the Cin = 1 im2col convs (first_layer.cu), 2 bytes per voxel instead of the
+// 16 of an 8-channel slab group.  One thread per padded row.
+__global__ void k_dense_to_compact1(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, int B, int D,
+                                    int H, int W) {
+  const int Hp = H + 2, Wp = W + 2;
+  const int64_t per = (int64_t)(D + 2) * Hp * Wp;
+  const int64_t total = (int64_t)B * per;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(i / per);
+    int64_t r = i - (int64_t)b * per;
+    const int wq = (int)(r % Wp) - 1;
+    r /= Wp;
+    const int hq = (int)(r % Hp) - 1;
+    const int dq = (int)(r / Hp) - 1;
+    float v = 0.f;
+    if (dq >= 0 && dq < D && hq >= 0 && hq < H && wq >= 0 && wq < W)
+      v = src[(((int64_t)b * D + dq) * H + hq) * W + wq];
+    dst[i] = __float2bfloat16_rn(v);
+  }
+}
+
+extern "C" int vm_dense_to_compact1(const float* src, void* dst, int B, int D, int H, int W, void* stream) {
+  VM_REQUIRE(src && dst, VM_E_ARG, "vm_dense_to_compact1: null pointer");
+  const int64_t total = (int64_t)B * (D + 2) * (H + 2) * (W + 2);
+  k_dense_to_compact1<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(src, (__nv_bfloat16*)dst, B, D, H, W);
+  return launch_status("vm_dense_to_compact1");
+}
+
 extern "C" int vm_slab_to_dense(const void* slab, int slab_dtype, int64_t bstride, void* dst,
                                 int dst_dtype, int B, int C, int D, int H, int W, int m,
                                 void* stream) {

@@ -144,6 +144,7 @@ class UNetStep:
         # the previous one drains).  Forward: trigger at kernel start.  Backward: trigger at CTA
         # exit only — CTAs parked early at the dependency wait would take SMs from the
         # side-stream wgrad (measured: early 3.22 ms, late 3.12 ms, off 3.17 ms per step)
+        self.first_layer_c1 = True  # Cin = 1 convs through the im2col kernels (vm_conv3d_*_c1)
         self.pdl_forward = 1  # 0 off, 1 trigger at kernel start, 2 trigger at CTA exit
         self.pdl_backward = 2
         self._build_buffers(params)
@@ -196,6 +197,14 @@ class UNetStep:
                     L.wt = torch.empty(L.nk, dtype=torch.float32, device=dev)
                 ws_fn = "vm_conv3d_wgrad_tc_ws" if self.conv_impl == "tc" else "vm_conv3d_wgrad_simt_ws"
                 L.ws_bytes = int(_lib.call_size(ws_fn, self.B, L.cin, L.cout, L.D, L.H, L.W))
+                # single-channel first conv: im2col tcgen05 kernels (27 taps as K) on a compact
+                # copy of the input (no halo: a partitioned rank keeps the slab path, whose
+                # margins receive the neighbours' faces)
+                L.c1 = (self.conv_impl == "tc" and self.first_layer_c1 and not self.has_halo and L.cin == 1
+                        and L.cout <= 32)
+                if L.c1:
+                    L.ws_bytes = max(L.ws_bytes, int(_lib.call_size("vm_conv3d_wgrad_c1_ws", self.B, L.cout,
+                                                                    L.D, L.H, L.W)))
         self.wgrad_ws = torch.empty(max([L.ws_bytes for L in self.layers if L.k == 3] + [16]) // 4 + 4,
                                     dtype=torch.float32, device=dev)
         # split-K scratch of the general forward/dgrad kernel (deep levels); zeroed once, its
@@ -221,6 +230,11 @@ class UNetStep:
         e0 = self._ext(nodes[0].id)
         self.x_in = self._slab(cfg.in_channels, e0)
         self.out["input"] = self.x_in
+        # compact single-channel copy of the input for the Cin = 1 im2col convs
+        self.x1 = None
+        if any(getattr(L, "c1", False) for L in self.layers):
+            self.x1 = torch.zeros(self.B * (e0[0] + 2) * (e0[1] + 2) * (e0[2] + 2), dtype=torch.bfloat16,
+                                  device=dev)
         self.cat_parts = {}
         # concat slabs first, so skip producers can write into them
         for n in nodes:
@@ -327,7 +341,10 @@ class UNetStep:
         kind = "conv_dgrad" if dgrad else "conv_fwd"
         vox = self.B * L.D * L.H * L.W
         nbytes = 2.0 * vox * (cin + cout + (cout if mask is not None else 0))
-        if self.conv_impl == "tc":
+        if self.conv_impl == "tc" and L.c1 and not dgrad:
+            self._k(kind, L.node.id, self._conv_flops(L), nbytes, "vm_conv3d_fwd_c1", _lib.ptr(self.x1), 0,
+                    _lib.ptr(L.w), _lib.ptr(L.b), y.p(), y.bstride, self.B, cout, L.D, L.H, L.W, flags)
+        elif self.conv_impl == "tc":
             w = L.wpt if dgrad else L.wp
             self._k(kind, L.node.id, self._conv_flops(L), nbytes, "vm_conv3d_fwd_tc_ws", x.p(), x.bstride,
                     _lib.ptr(w), _lib.ptr(L.b), y.p(), y.bstride, mp, mb, self.B, cin, cout, L.D, L.H, L.W, flags,
@@ -340,7 +357,11 @@ class UNetStep:
     def _wgrad(self, x, L, g):
         vox = self.B * L.D * L.H * L.W
         nbytes = 2.0 * vox * (L.cin + L.cout) + 4.0 * (L.nk + L.cout)
-        if self.conv_impl == "tc":
+        if self.conv_impl == "tc" and L.c1:
+            self._k("conv_wgrad", L.node.id, self._conv_flops(L), nbytes, "vm_conv3d_wgrad_c1", _lib.ptr(self.x1),
+                    0, g.p(), g.bstride, _lib.ptr(L.gw), _lib.ptr(L.gb), _lib.ptr(self.wgrad_ws), self.B, L.cout, L.D,
+                    L.H, L.W)
+        elif self.conv_impl == "tc":
             self._k("conv_wgrad", L.node.id, self._conv_flops(L), nbytes, "vm_conv3d_wgrad_tc", x.p(), x.bstride,
                     g.p(), g.bstride, _lib.ptr(L.gw), _lib.ptr(L.gb), _lib.ptr(self.wgrad_ws), self.B, L.cin,
                     L.cout, L.D, L.H, L.W)
@@ -402,7 +423,14 @@ class UNetStep:
         x = self.x_in
         self._k("io", "image", 0, 0, "vm_dense_to_slab", _lib.ptr(image.contiguous()), _lib.VM_F32, x.p(), self.dt,
                 x.bstride, self.B, x.C, x.D, x.H, x.W, 1)
+        self._compact_input(image.contiguous())
         self.onehot.copy_(onehot.reshape(-1))
+
+    def _compact_input(self, image):
+        if self.x1 is not None:
+            x = self.x_in
+            self._k("io", "image", 0, 0, "vm_dense_to_compact1", _lib.ptr(image), _lib.ptr(self.x1), self.B, x.D,
+                    x.H, x.W)
 
     def upload(self, image_host, labels_host):
         """Public-API input path: host f32 image [B,D,H,W,Cin] + u8 labels [B,D,H,W]
@@ -452,6 +480,7 @@ class UNetStep:
         x = self.x_in
         self._k("io", "image", 0, 0, "vm_dense_to_slab", _lib.ptr(img), _lib.VM_F32, x.p(), self.dt,
                 x.bstride, self.B, x.C, x.D, x.H, x.W, 1)
+        self._compact_input(img)
         self._k("io", "onehot", 0, 0, "vm_onehot_u8", _lib.ptr(lab), _lib.ptr(self.onehot), self.nvox,
                 self.ncls)
         ev = torch.cuda.Event()

@@ -287,3 +287,52 @@ def test_tc_forward_split_k_workspace(shape):
     assert rel_l2(outs[1], dense) <= 1e-2
     nz = int(torch.count_nonzero(ws[:64]).item())  # tile counters (first 256 B) are back to zero
     assert nz == 0
+
+
+C1_SHAPES = [(1, 16, 16, 16, 16), (2, 32, 6, 10, 34), (1, 8, 5, 7, 9), (1, 16, 12, 32, 128), (1, 24, 3, 4, 5)]
+
+
+@pytest.mark.parametrize("shape", C1_SHAPES)
+def test_first_layer_c1_forward_and_wgrad(shape):
+    # Cin = 1 im2col kernels (27 taps as K) against the f64 oracle and the channel-blocked path
+    B, cout, D, H, W = shape
+    rng = np.random.default_rng(21 + sum(shape))
+    x = O.bf16_round(rng.standard_normal((B, D, H, W, 1)).astype(np.float32))
+    w = O.bf16_round(rng.uniform(-1, 1, (3, 3, 3, 1, cout)).astype(np.float32) / np.sqrt(27))
+    b = rng.standard_normal(cout).astype(np.float32) * 0.1
+    g = O.bf16_round(rng.standard_normal((B, D, H, W, cout)).astype(np.float32))
+    xs, gs = _slab_from(x), _slab_from(g)
+    xd = torch.from_numpy(np.ascontiguousarray(x[..., 0], np.float32)).cuda()
+    x1 = torch.full((B * (D + 2) * (H + 2) * (W + 2),), float("nan"), dtype=torch.bfloat16, device="cuda")
+    _lib.call("vm_dense_to_compact1", _lib.ptr(xd), _lib.ptr(x1), B, D, H, W, _lib.stream_ptr())
+    wt = torch.from_numpy(np.ascontiguousarray(w, np.float32)).cuda()
+    bt = torch.from_numpy(b).cuda()
+    ys = Slab(B, cout, D, H, W, torch.bfloat16, "cuda")
+    _lib.call("vm_conv3d_fwd_c1", _lib.ptr(x1), 0, _lib.ptr(wt), _lib.ptr(bt), ys.p(), ys.bstride, B, cout, D, H,
+              W, _lib.VM_CONV_RELU, _lib.stream_ptr())
+    got = ys.interior().cpu().numpy()
+    dense = np.maximum(O.conv3d_dense(x.astype(np.float64), w.astype(np.float64), b.astype(np.float64)), 0)
+    assert rel_l2(got, dense) <= 1e-2
+    if cout % 16 == 0:
+        ref = _conv_tc(xs, w, b, cout).interior().cpu().numpy()
+        assert rel_l2(got, ref) <= 2e-3
+    # margins stay zero (the next conv reads them as padding)
+    full = ys.storage[: B * ys.CG * ys.plane].float().reshape(B, ys.CG, D + 2, H + 2, W + 2, 8).cpu().numpy()
+    inner = np.zeros_like(full, dtype=bool)
+    inner[:, :, 1:-1, 1:-1, 1:-1] = True
+    assert not full[~inner].any()
+    # weight gradient
+    gw = torch.zeros(27 * cout, dtype=torch.float32, device="cuda")
+    gb = torch.zeros(cout, dtype=torch.float32, device="cuda")
+    nb = _lib.call_size("vm_conv3d_wgrad_c1_ws", B, cout, D, H, W)
+    ws = torch.empty(nb // 4 + 64, dtype=torch.float32, device="cuda")
+    outs = []
+    for _ in range(2):
+        _lib.call("vm_conv3d_wgrad_c1", _lib.ptr(x1), 0, gs.p(), gs.bstride, _lib.ptr(gw), _lib.ptr(gb),
+                  _lib.ptr(ws), B, cout, D, H, W, _lib.stream_ptr())
+        torch.cuda.synchronize()
+        outs.append((gw.cpu().numpy().copy(), gb.cpu().numpy().copy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    _, rgk, rgb = O.conv3d_dense_backward(g.astype(np.float64), x.astype(np.float64), np.zeros((3, 3, 3, 1, cout)))
+    assert rel_l2(outs[0][0].reshape(3, 3, 3, 1, cout), rgk) <= 1e-5
+    assert rel_l2(outs[0][1], rgb) <= 1e-5
