@@ -1521,41 +1521,63 @@ extern "C" size_t vm_packed_weights_bytes(int Cin, int Cout) {
   return (size_t)g.nchunk * g.KC * 27 * 2 * g.Nc * 8 * sizeof(bf16);
 }
 
-// Batched repack of every layer's operands in one launch (after each SGD step): grid.y = job,
-// one thread per 16-byte output vector (8 input channels of one (tap, output channel)), so
-// the decode runs once per vector and the fp32 reads are coalesced (plain: consecutive
+// Batched repack of every layer's operands in one launch (after each SGD step): one thread
+// per 16-byte output vector (8 input channels of one (tap, output channel)) over the
+// concatenation of all jobs, the job found by binary search over the job offsets — load
+// balanced across layers of very different sizes (a grid.y-per-job launch sized for the
+// average job left the deep layers' blocks looping long after the thin ones were done).
+// The decode runs once per vector and the fp32 reads are coalesced (plain: consecutive
 // threads read consecutive co; flip: each thread reads 8 consecutive floats).
+constexpr int kPackSmemJobs = 256;
 __global__ void k_pack_batch(const vm_pack_job* __restrict__ jobs, int njobs, int64_t total) {
-  const int jb_i = blockIdx.y;
-  const vm_pack_job& jb = jobs[jb_i];
-  const int64_t nvec = ((jb_i + 1 < njobs ? jobs[jb_i + 1].begin : total) - jb.begin) / 8;
-  const PackGeom g = jb.flip ? pack_geom(jb.cout, jb.cin) : pack_geom(jb.cin, jb.cout);
-  const float* __restrict__ w = jb.w;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = v;
+  // job offsets and layouts cached in shared memory (searched and decoded per vector)
+  __shared__ int64_t sbegin[kPackSmemJobs];
+  __shared__ PackGeom sgeom[kPackSmemJobs];
+  const bool cached = njobs <= kPackSmemJobs;
+  pdl_wait();
+  if (cached) {
+    for (int i = threadIdx.x; i < njobs; i += blockDim.x) {
+      sbegin[i] = jobs[i].begin;
+      sgeom[i] = jobs[i].flip ? pack_geom(jobs[i].cout, jobs[i].cin) : pack_geom(jobs[i].cin, jobs[i].cout);
+    }
+    __syncthreads();
+  }
+  for (int64_t gv = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gv < total / 8;
+       gv += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = njobs - 1;  // last job with begin <= 8*gv
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if ((cached ? sbegin[mid] : jobs[mid].begin) <= gv * 8) lo = mid; else hi = mid - 1;
+    }
+    const vm_pack_job& jb = jobs[lo];
+    const PackGeom g = cached ? sgeom[lo] : (jb.flip ? pack_geom(jb.cout, jb.cin) : pack_geom(jb.cin, jb.cout));
+    const float* __restrict__ w = jb.w;
+    const int64_t v = gv - jb.begin / 8;
+    uint32_t r = (uint32_t)v;  // < 2^31 vectors per job (VM_REQUIRE at launch)
     int kd, kh, kw, kc, co, half;
     if (g.sweep) {
-      const int n = r % (3 * g.Nc);
-      r /= 3 * g.Nc;
-      half = r % 2;
-      r /= 2;
-      const int j = r % 9;
-      kc = (int)(r / 9);
+      const uint32_t N3 = 3u * g.Nc;
+      const int n = (int)(r % N3);
+      r /= N3;
+      half = r & 1;
+      r >>= 1;
+      const int j = (int)(r % 9u);
+      kc = (int)(r / 9u);
       kh = j / 3;
       kw = j % 3;
       kd = 2 - n / g.Nc;
       co = n % g.Nc;
     } else {
-      const int n = r % g.Nc;
-      r /= g.Nc;
-      half = r % 2;
-      r /= 2;
-      const int j = r % 9;
-      r /= 9;
-      kd = r % 3;
-      r /= 3;
-      kc = r % g.KC;
-      co = (int)(r / g.KC) * g.Nc + n;
+      const int n = (int)(r % (uint32_t)g.Nc);
+      r /= (uint32_t)g.Nc;
+      half = r & 1;
+      r >>= 1;
+      const int j = (int)(r % 9u);
+      r /= 9u;
+      kd = (int)(r % 3u);
+      r /= 3u;
+      kc = (int)(r % (uint32_t)g.KC);
+      co = (int)(r / (uint32_t)g.KC) * g.Nc + n;
       kh = j / 3;
       kw = j % 3;
     }
@@ -1583,15 +1605,8 @@ __global__ void k_pack_batch(const vm_pack_job* __restrict__ jobs, int njobs, in
 extern "C" int vm_pack_weights_batch(const vm_pack_job* jobs, int njobs, int64_t total_elems, void* stream) {
   VM_REQUIRE(jobs && njobs > 0 && total_elems > 0, VM_E_ARG, "vm_pack_weights_batch: bad argument");
   VM_REQUIRE(njobs <= 65535, VM_E_ARG, "vm_pack_weights_batch: too many jobs");
-  // ~4 waves of 256-thread blocks over all jobs
-  int nsm = vm_num_sms(0);
-  if (nsm <= 0) nsm = 148;
-  const int64_t per_job = total_elems / 8 / njobs + 1;
-  int gx = (int)((per_job + 255) / 256);
-  const int cap = (4 * nsm * 8 + njobs - 1) / njobs;
-  if (gx > cap) gx = cap;
-  if (gx < 1) gx = 1;
-  k_pack_batch<<<dim3(gx, njobs), 256, 0, as_stream(stream)>>>(jobs, njobs, total_elems);
+  VM_REQUIRE(total_elems / 8 < (1LL << 31), VM_E_SHAPE, "vm_pack_weights_batch: too many elements");
+  launch_pdl(k_pack_batch, grid_for(total_elems / 8, 256), 256, 0, as_stream(stream), jobs, njobs, total_elems);
   return launch_status("vm_pack_weights_batch");
 }
 

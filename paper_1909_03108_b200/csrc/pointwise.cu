@@ -709,25 +709,46 @@ __global__ void k_reduce_rows(const float* __restrict__ part, int rows, int widt
 }
 
 // ------------------------------------------------------------------ SGD (training.py:202-219)
-__global__ void k_sgd_check(const float* __restrict__ g, const int64_t* __restrict__ off,
+// Grid-stride over the whole flat parameter buffer (balanced across layers of very different
+// sizes; a per-layer grid.y left the deep layers' blocks looping alone), the layer of an element
+// found by binary search over the offsets cached in shared memory.
+constexpr int kSgdMaxLayers = 512;
+__device__ __forceinline__ int sgd_layer(const int64_t* soff, int nl, int64_t i) {
+  int lo = 0, hi = nl - 1;  // last layer with off[l] <= i
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (soff[mid] <= i) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void k_sgd_check(const float* __restrict__ g, const int64_t* __restrict__ off, int nl,
                             int* __restrict__ flags) {
-  const int l = blockIdx.y;
-  const int64_t a = off[l], e = off[l + 1];
-  bool bad = false;
-  for (int64_t i = a + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e;
+  __shared__ int64_t soff[kSgdMaxLayers + 1];
+  pdl_wait();
+  for (int i = threadIdx.x; i <= nl; i += blockDim.x) soff[i] = off[i];
+  __syncthreads();
+  const int64_t n = soff[nl];
+  for (int64_t i = soff[0] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    bad |= !isfinite(g[i]);
-  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&flags[l], 1);
+    if (!isfinite(g[i])) atomicOr(&flags[sgd_layer(soff, nl, i)], 1);  // rare
 }
 
 __global__ void k_sgd_apply(float* __restrict__ p, float* __restrict__ v, const float* __restrict__ g,
-                            const int64_t* __restrict__ off, const int* __restrict__ flags, float lr,
+                            const int64_t* __restrict__ off, int nl, const int* __restrict__ flags, float lr,
                             float mu) {
-  const int l = blockIdx.y;
-  if (flags[l]) return;
-  const int64_t a = off[l], e = off[l + 1];
-  for (int64_t i = a + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e;
+  __shared__ int64_t soff[kSgdMaxLayers + 1];
+  __shared__ int sflag[kSgdMaxLayers];
+  pdl_wait();
+  for (int i = threadIdx.x; i <= nl; i += blockDim.x) {
+    soff[i] = off[i];
+    if (i < nl) sflag[i] = flags[i];
+  }
+  __syncthreads();
+  const int64_t n = soff[nl];
+  for (int64_t i = soff[0] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
+    if (sflag[sgd_layer(soff, nl, i)]) continue;
     // numpy fp32 order: v *= mu; v += g; p -= lr * v   (no FMA contraction)
     float vv = __fadd_rn(__fmul_rn(v[i], mu), g[i]);
     v[i] = vv;
@@ -903,12 +924,11 @@ extern "C" int vm_sgd_momentum(float* params, float* moments, const float* grads
   VM_REQUIRE(params && moments && grads && offsets && flags && nlayers > 0, VM_E_ARG,
              "vm_sgd_momentum: bad argument");
   cudaStream_t st = as_stream(stream);
+  VM_REQUIRE(nlayers <= kSgdMaxLayers, VM_E_UNSUPPORTED, "vm_sgd_momentum: %d layers > %d", nlayers, kSgdMaxLayers);
   cudaMemsetAsync(flags, 0, sizeof(int) * nlayers, st);
-  int64_t bx = (max_layer_elems + 255) / 256;
-  if (bx > 64) bx = 64;
-  if (bx < 1) bx = 1;
-  dim3 grid((unsigned)bx, (unsigned)nlayers);
-  k_sgd_check<<<grid, 256, 0, st>>>(grads, offsets, flags);
-  k_sgd_apply<<<grid, 256, 0, st>>>(params, moments, grads, offsets, flags, lr, momentum);
+  const int grid = grid_for(max_layer_elems * nlayers, 256);  // upper bound of the buffer size
+  launch_pdl(k_sgd_check, grid, 256, 0, st, grads, offsets, nlayers, flags);
+  launch_pdl(k_sgd_apply, grid, 256, 0, st, params, moments, grads, offsets, nlayers, (const int*)flags, lr,
+             momentum);
   return launch_status("vm_sgd_momentum", 2);
 }
