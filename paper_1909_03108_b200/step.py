@@ -232,6 +232,9 @@ class UNetStep:
         self.out["input"] = self.x_in
         # compact single-channel copy of the input for the Cin = 1 im2col convs
         self.x1 = None
+        # the 8-channel input slab is only written when a consumer still reads it
+        self.input_slab_needed = not all(
+            self.by_id[n.id].c1 for n in g.nodes if n.op == "conv" and n.k == 3 and n.inputs[0] == "input")
         if any(getattr(L, "c1", False) for L in self.layers):
             self.x1 = torch.zeros(self.B * (e0[0] + 2) * (e0[1] + 2) * (e0[2] + 2), dtype=torch.bfloat16,
                                   device=dev)
@@ -421,8 +424,9 @@ class UNetStep:
     def load_inputs(self, image, onehot):
         """image: device f32 [B,D,H,W,Cin] (local block); onehot: device f32 [B,D,H,W,ncls]."""
         x = self.x_in
-        self._k("io", "image", 0, 0, "vm_dense_to_slab", _lib.ptr(image.contiguous()), _lib.VM_F32, x.p(), self.dt,
-                x.bstride, self.B, x.C, x.D, x.H, x.W, 1)
+        if self.input_slab_needed:
+            self._k("io", "image", 0, 0, "vm_dense_to_slab", _lib.ptr(image.contiguous()), _lib.VM_F32, x.p(),
+                    self.dt, x.bstride, self.B, x.C, x.D, x.H, x.W, 1)
         self._compact_input(image.contiguous())
         self.onehot.copy_(onehot.reshape(-1))
 
@@ -478,8 +482,9 @@ class UNetStep:
         if self._copied[i] is not None:
             torch.cuda.current_stream().wait_event(self._copied[i])
         x = self.x_in
-        self._k("io", "image", 0, 0, "vm_dense_to_slab", _lib.ptr(img), _lib.VM_F32, x.p(), self.dt,
-                x.bstride, self.B, x.C, x.D, x.H, x.W, 1)
+        if self.input_slab_needed:
+            self._k("io", "image", 0, 0, "vm_dense_to_slab", _lib.ptr(img), _lib.VM_F32, x.p(), self.dt,
+                    x.bstride, self.B, x.C, x.D, x.H, x.W, 1)
         self._compact_input(img)
         self._k("io", "onehot", 0, 0, "vm_onehot_u8", _lib.ptr(lab), _lib.ptr(self.onehot), self.nvox,
                 self.ncls)

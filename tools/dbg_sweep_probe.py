@@ -13,7 +13,7 @@ buf = torch.zeros(148 * 8, dtype=torch.int64, device='cuda')
 lib.vm_debug_set_fwd_probe.argtypes = [ctypes.c_void_p]
 lib.vm_debug_set_sweep_mode.argtypes = [ctypes.c_int]
 MODES = [int(v) for v in sys.argv[1:]] or [0]
-for (ci, co, e, mode) in [(ci, co, e, m) for m in MODES for (ci, co, e) in [(16, 16, 128), (48, 16, 128)]] + [(16, 16, 128, 'dgrad')]:
+for (ci, co, e, mode) in [(ci, co, e, m) for m in MODES for (ci, co, e) in [(16, 16, 128), (48, 16, 128), (32, 32, 64), (16, 32, 64)]] + [(16, 16, 128, 'dgrad'), (32, 32, 64, 'dgrad')]:
     dgrad = mode == 'dgrad'
     lib.vm_debug_set_sweep_mode(0 if dgrad else mode)
     x = Slab(1, ci, e, e, e, torch.bfloat16, 'cuda')
