@@ -97,10 +97,11 @@ __global__ void k_maxpool_bwd(const T* __restrict__ x, Slab gx, const T* __restr
     int cg = split_cg(i, nvox, v32);
     int b, d, h, w;
     decompose(v32, go, b, d, h, w);
-    // pass 1: argmax per channel (first max wins); pass 2 re-reads the 2x2x2 cell (L1/L2
-    // hits) for the ReLU mask instead of holding 64 values in registers
+    // one pass over the 2x2x2 cell: argmax per channel (first max wins) and the ReLU mask
+    // bits (x > 0) per (cell, channel), so the write pass needs no second read of x
     int arg[8];
     float best[8];
+    uint32_t pos_lo = 0, pos_hi = 0;  // bit (cell*8 + j): x > 0
 #pragma unroll
     for (int cell = 0; cell < 8; ++cell) {
       float xv[8];
@@ -111,6 +112,10 @@ __global__ void k_maxpool_bwd(const T* __restrict__ x, Slab gx, const T* __restr
           best[j] = xv[j];
           arg[j] = cell;
         }
+        if (xv[j] > 0.f) {
+          if (cell < 4) pos_lo |= 1u << (cell * 8 + j);
+          else pos_hi |= 1u << ((cell - 4) * 8 + j);
+        }
       }
     }
     float g[8];
@@ -118,14 +123,14 @@ __global__ void k_maxpool_bwd(const T* __restrict__ x, Slab gx, const T* __restr
 #pragma unroll 2
     for (int cell = 0; cell < 8; ++cell) {
       int pd = 2 * d + (cell >> 2), ph = 2 * h + ((cell >> 1) & 1), pw = 2 * w + (cell & 1);
-      float o[8], xv[8];
+      float o[8];
       if (add) V8<T>::ld(add + ga.at(b, cg, pd, ph, pw), o);
-      if (relu_mask) V8<T>::ld(x + gx.at(b, cg, pd, ph, pw), xv);
+      const uint32_t pos = cell < 4 ? pos_lo >> (cell * 8) : pos_hi >> ((cell - 4) * 8);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         float r = (arg[j] == cell) ? g[j] : 0.f;
         if (add) r += o[j];
-        if (relu_mask && !(xv[j] > 0.f)) r = 0.f;
+        if (relu_mask && !((pos >> j) & 1u)) r = 0.f;
         o[j] = r;
       }
       V8<T>::st(gin + gi.at(b, cg, pd, ph, pw), o);
