@@ -154,6 +154,30 @@ int vm_conv3d_fwd_c1(const void* x, int64_t x_bstride, const float* w, const flo
                      int64_t y_bstride, int B, int Cout, int D, int H, int W, unsigned flags, void* stream);
 size_t vm_conv3d_wgrad_c1_ws(int B, int Cout, int D, int H, int W);
 int vm_dense_to_compact1(const float* src, void* dst, int B, int D, int H, int W, void* stream);
+
+/* ------------------------------------------------------------------ augmentation
+ * Tumour remove / synthesise (augment.py:53-151) on dense C-order [D][H][W] volumes (image
+ * f32, labels u8: 0 background, 1 liver, 2 tumour).  Host code draws the random numbers and
+ * the Gaussian weights with numpy exactly as the reference; these kernels do the per-voxel
+ * work.  Background voxels are never written (vm_aug_finish adds delta * 0 there). */
+size_t vm_aug_stats_ws_bytes(void);
+/* out[4] = {sum(image | 2), #2, sum(image | 1), #1} in float64 (intensity_delta, :53-64) */
+int vm_aug_stats(const float* image, const uint8_t* labels, int64_t n, double* ws, double* out, void* stream);
+/* image[label 2] -= delta (f32); label 2 -> 1 (remove_tumor, :67-78) */
+int vm_aug_remove(float* image, uint8_t* labels, int64_t n, float delta, void* stream);
+/* counts[c] = #{label == value} in voxels [c*chunk, (c+1)*chunk) (k-th liver voxel lookup) */
+int vm_aug_count_chunks(const uint8_t* labels, int64_t n, int chunk, int value, int* counts, void* stream);
+/* mask = 1 on liver voxels inside any ellipsoid (centers [n][3] int64, radii [n][3] f64; the
+ * reference's float64 accumulation order, :81-86) */
+int vm_aug_paint(const uint8_t* labels, int D, int H, int W, const int64_t* centers, const double* radii,
+                 int ntumours, float* mask, void* stream);
+/* one scipy.ndimage.correlate1d pass along `axis` (mode constant), symmetric weights w[0..r]
+ * (centre first), double accumulation in scipy's order, f32 result */
+int vm_aug_blur_axis(const float* in, float* out, int D, int H, int W, int axis, const double* w, int r,
+                     void* stream);
+/* w = clip(w,0,1) * liver; image += delta * w; label 1 -> 2 where w >= threshold (:119-133) */
+int vm_aug_finish(float* image, uint8_t* labels, const float* w, int64_t n, float delta, float threshold,
+                  void* stream);
 int vm_conv3d_wgrad_c1(const void* x, int64_t x_bstride, const void* gy, int64_t gy_bstride, float* gw,
                        float* gb, void* ws, int B, int Cout, int D, int H, int W, void* stream);
 size_t vm_conv3d_wgrad_tc_ws(int B, int Cin, int Cout, int D, int H, int W);

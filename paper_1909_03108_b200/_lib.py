@@ -56,6 +56,13 @@ _SIGS = {
     "vm_conv3d_fwd_c1": (_I, [_P, _L, _P, _P, _P, _L, _I, _I, _I, _I, _I, _U, _P]),
     "vm_conv3d_wgrad_c1_ws": (_S, [_I, _I, _I, _I, _I]),
     "vm_dense_to_compact1": (_I, [_P, _P, _I, _I, _I, _I, _P]),
+    "vm_aug_stats_ws_bytes": (_S, []),
+    "vm_aug_stats": (_I, [_P, _P, _L, _P, _P, _P]),
+    "vm_aug_remove": (_I, [_P, _P, _L, _F, _P]),
+    "vm_aug_count_chunks": (_I, [_P, _L, _I, _I, _P, _P]),
+    "vm_aug_paint": (_I, [_P, _I, _I, _I, _P, _P, _I, _P, _P]),
+    "vm_aug_blur_axis": (_I, [_P, _P, _I, _I, _I, _I, _P, _I, _P]),
+    "vm_aug_finish": (_I, [_P, _P, _P, _L, _F, _F, _P]),
     "vm_conv3d_wgrad_c1": (_I, [_P, _L, _P, _L, _P, _P, _P, _I, _I, _I, _I, _I, _P]),
     "vm_conv3d_wgrad_tc_ws": (ctypes.c_size_t, [_I, _I, _I, _I, _I, _I]),
     "vm_conv3d_wgrad_tc": (_I, [_P, _L, _P, _L, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),

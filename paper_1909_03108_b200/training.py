@@ -20,8 +20,10 @@ Mirrors ``voxmesh.training`` (training.py) for a user switching over:
   training.py:166-194) plus the mean loss.
 
 The arithmetic is the GPU step's (bf16 storage, fp32 accumulation; ``compute_dtype="f32"``
-selects the fp32 CUDA-core kernels).  Augmentation (``augment.py``) is out of scope (§8(f)
-row 4) and rejected explicitly.
+selects the fp32 CUDA-core kernels).  ``TrainConfig.augment`` (a ``SynthConfig``) runs the
+tumour remove / synthesise augmentation (``augment.py``, GPU kernels) on every sample with
+the reference's per-sample seed ``SeedSequence([seed, 104729, global index])``
+(training.py:266-273); its outputs are bitwise the reference's.
 """
 
 from __future__ import annotations
@@ -209,12 +211,13 @@ class BatchSource:
     Returns the host image ``[B, E, E, E, 1]`` (f32) and labels ``[B, E, E, E]`` (u8); the
     one-hot expansion happens on the GPU."""
 
-    def __init__(self, records, batch_size, seed):
+    def __init__(self, records, batch_size, seed, augment=None):
         if not records:
             raise VoxmeshError("empty training set")
         self.records = list(records)
         self.batch_size = int(batch_size)
         self.seed = int(seed)
+        self.augment = augment
         self._perms = {}
 
     def perm(self, epoch):
@@ -227,9 +230,20 @@ class BatchSource:
         n = len(self.records)
         return int(self.perm(global_idx // n)[global_idx % n])
 
+    def _pair(self, global_idx):
+        rec = self.records[self.record_index(global_idx)]
+        img, lab = _image_labels(rec)
+        if self.augment is not None:  # training.py:268-272
+            from . import augment as _aug
+
+            aug_seed = int(np.random.SeedSequence([self.seed, 104729, int(global_idx)]).generate_state(1)[0])
+            out = _aug.augment_pipeline(_aug.VolumeRecord(img, lab, getattr(rec, "id", "")),
+                                        _aug.with_seed(self.augment, aug_seed))
+            img, lab = out.image, out.labels
+        return img, lab
+
     def batch(self, step):
-        idx = [self.record_index(step * self.batch_size + j) for j in range(self.batch_size)]
-        pairs = [_image_labels(self.records[i]) for i in idx]
+        pairs = [self._pair(step * self.batch_size + j) for j in range(self.batch_size)]
         img = np.stack([np.asarray(p[0], dtype=np.float32) for p in pairs])[..., None]
         lab = np.stack([np.asarray(p[1], dtype=np.uint8) for p in pairs])
         return img, lab
@@ -303,8 +317,6 @@ def train_loop(graph, dataset, cfg, resume_from=None, run_echo=None):
     """Train on the graph's mesh; returns the final TrainState (training.py:442-533)."""
     from . import unet as _unet
 
-    if cfg.augment:
-        raise VoxmeshError("train_loop: augmentation is not part of the GPU path (SURVEY §8(f) row 4)")
     records = dataset.load_split("train") if hasattr(dataset, "load_split") else list(dataset)
     mesh = graph.mesh
     if resume_from is not None:
@@ -326,7 +338,7 @@ def train_loop(graph, dataset, cfg, resume_from=None, run_echo=None):
             "seed": cfg.seed, "steps": cfg.steps, "batch_size": cfg.batch_size, "lr": cfg.lr,
             "momentum": cfg.momentum, "dtype": cfg.dtype, "compute_dtype": cfg.compute_dtype,
             "dice_classes": list(cfg.dice_classes), "loss_weights": [cfg.loss_weights.dice, cfg.loss_weights.ce],
-            "augment": False, "config_kv": graph.config.to_kv(),
+            "augment": bool(cfg.augment), "config_kv": graph.config.to_kv(),
             "resume_from": str(resume_from) if resume_from else None,
         }
         echo.update(run_echo or {})
@@ -336,7 +348,7 @@ def train_loop(graph, dataset, cfg, resume_from=None, run_echo=None):
         if fresh:
             csv_f.write("step,loss,dice_loss,ce_loss,lr,wall_ms\n")
 
-    source = BatchSource(records, cfg.batch_size, cfg.seed)
+    source = BatchSource(records, cfg.batch_size, cfg.seed, cfg.augment)
     state = TrainState(start, params, moments or {})
     try:
         for step in range(start, start + cfg.steps):

@@ -243,3 +243,17 @@ def test_conv_params_validation():
         vm.ConvParams(k, np.zeros(3, np.float32))
     with pytest.raises(vm.VoxmeshError):
         vm.ConvParams(np.full((3, 3, 3, 2, 4), np.nan, np.float32), np.zeros(4, np.float32))
+
+
+def test_augment_config_and_quantize_host_side():
+    # SynthConfig validation (augment.py:40-45) and the 1/256 delta snap (:48-50)
+    from paper_1909_03108_b200 import augment as A
+    from paper_1909_03108_b200.errors import AugmentError
+    with pytest.raises(AugmentError):
+        A.SynthConfig(n_tumors=(0, 2))
+    with pytest.raises(AugmentError):
+        A.SynthConfig(n_tumors=(3, 2))
+    with pytest.raises(AugmentError):
+        A.SynthConfig(radius_range=(0.5, 2.0))
+    assert A.quantize_delta(0.3) == float(np.float32(round(0.3 * 256) / 256))
+    assert A.with_seed(A.SynthConfig(), 7).seed == 7
