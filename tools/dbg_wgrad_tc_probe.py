@@ -13,8 +13,12 @@ lib = _lib.load()
 buf = torch.zeros(148 * 8, dtype=torch.int64, device='cuda')
 lib.vm_debug_set_fwd_probe.argtypes = [ctypes.c_void_p]
 SHAPES = [(64, 64, 32), (192, 64, 32), (128, 128, 16), (64, 128, 16), (32, 64, 32)]
-MIN_SPK = [3]
+MIN_SPK = [2]
 args = sys.argv[1:]
+FORCE = None
+if args and args[0].startswith('force='):  # force=runs,ks,mpu
+    FORCE = [int(v) for v in args.pop(0)[6:].split(',')]
+    lib.vm_debug_force_wgrad_plan(*FORCE)
 if args and args[0].startswith('spk='):
     MIN_SPK = [int(v) for v in args.pop(0)[4:].split(',')]
 if args:
