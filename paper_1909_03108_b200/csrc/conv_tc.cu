@@ -1945,7 +1945,7 @@ int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
     return kSmemBudget / (int)stage >= 2;
   };
   auto forced_ok = [&](int runs, int KS, int mpu) {
-    return !((g_force_runs >= 0 && runs != g_force_runs) || (g_force_ks && KS != g_force_ks) ||
+    return !((g_force_runs >= 0 && g_force_runs <= 1 && runs != g_force_runs) || (g_force_ks && KS != g_force_ks) ||
              (g_force_mpu && mpu != g_force_mpu));
   };
   if (ks_run >= 64 && g_force_runs != 0) {
@@ -2056,7 +2056,7 @@ extern "C" int vm_debug_wgrad_plan(int B, int Cin, int Cout, int D, int H, int W
 // (3*Nc > 144 or TMEM, rows narrower than 34, or no double-buffered stage fits).
 static bool plan_wgrad_kd(int B, int Cin, int Cout, int D, int H, int W, WkParams& p, size_t& ws) {
   p = WkParams{};
-  if (g_force_runs == 0) return false;  // debug override selects the general kernel
+  if (g_force_runs == 0 || g_force_runs == 2) return false;  // debug override: the general kernel
   p.B = B;
   p.Wp = W + 2;
   p.P = (H + 2) * p.Wp;
@@ -2069,9 +2069,11 @@ static bool plan_wgrad_kd(int B, int Cin, int Cout, int D, int H, int W, WkParam
   if (3 * p.Nc > 256) return false;  // N = 3*Nc per MMA
   p.KS = min(256, ((p.Wp - 2) / 16) * 16);  // a run of KS + 2Wp + 2 rows fits 3 slots of Wp rows
   if (p.KS < 32) return false;
-  // one kw tap per CTA (Nc > 48) triples the A traffic per output: only with long K chunks
-  // (measured: 64->64 at 32^3, KS = 32, is slower than k_conv_wgrad_tc)
-  if (p.Nc > 48 && p.KS < 64) return false;
+  // Nc > 48 needs one kw tap per CTA, which triples the A traffic per output: the general
+  // kernel wins at every such shape measured (tools/dbg_wgrad_modes.py: 64->64 at 128^3
+  // 0.55 vs 0.98 ms, 192->64 1.28 vs 4.75 ms, 32->64 0.38 vs 0.84 ms, 16->80 at 64^3
+  // 0.054 vs 0.12 ms), while Cout <= 48 stays here (32->32 at 256^3: 1.19 vs 3.50 ms)
+  if (p.Nc > 48) return false;
   if ((3 * p.CG) % 16 == 0) return false;  // no spare M slot for the bias-gradient ones block
   p.MT = (3 * p.CG + 1 + 15) / 16;
   p.ones_slot = 3 * p.CG;
