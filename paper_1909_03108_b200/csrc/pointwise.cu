@@ -651,7 +651,9 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_grp(
       for (int k = 0; k < NC; ++k) {
         p[k] = __fdividef(p[k], ssum);
         float r = coef[3 * k + 2] != 0.f ? coef[3 * k] * (2.f * gk[u][k] - coef[3 * k + 1]) : 0.f;
-        r += p[k] >= clamp ? ce_scale * (gk[u][k] / fmaxf(p[k], clamp)) : 0.f;  // training.py:125-126
+        // g / max(p, clamp) with the correctly rounded reciprocal: exact for one-hot g in {0, 1}
+        // and no division slow path (FCHK + branches showed in the stall profile)
+        r += p[k] >= clamp ? ce_scale * (gk[u][k] * __frcp_rn(fmaxf(p[k], clamp))) : 0.f;  // training.py:125-126
         gp[k] = r;
         dot += r * p[k];
       }
