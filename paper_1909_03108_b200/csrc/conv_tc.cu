@@ -1902,6 +1902,7 @@ struct WgPlan {
 int g_force_runs = -1, g_force_ks = 0, g_force_mpu = 0;  // tools/tune_wgrad.py overrides
 int g_wg_min_spk = 2;  // minimum stages per K-split unit (vm_debug_set_wgrad_min_spk)
 int g_wk_runtime = 0;  // 1: force the runtime-bounded kd wgrad issue loop (A/B probe)
+int g_wk_ksub_min_stages = 2;  // two K chunks per stage when this many stages still fit (measured: 2 best)
 
 int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
   WgParams& p = pl.p;
@@ -2033,6 +2034,7 @@ int make_group_map(CUtensorMap* m, const void* base, int64_t bstride, int CG, in
 
 
 extern "C" void vm_debug_set_wgrad_kd_runtime(int v) { g_wk_runtime = v; }
+extern "C" void vm_debug_set_wgrad_ksub_stages(int v) { g_wk_ksub_min_stages = v > 0 ? v : 2; }
 
 extern "C" void vm_debug_set_wgrad_min_spk(int v) { g_wg_min_spk = v > 0 ? v : 2; }
 
@@ -2093,7 +2095,7 @@ static bool plan_wgrad_kd(int B, int Cin, int Cout, int D, int H, int W, WkParam
     p.a_bytes = ((uint32_t)slots * p.Wp * 16 + 1023) & ~1023u;
     p.sub_bytes = (p.a_bytes + 3 * p.g_bytes + 1023) & ~1023u;
     // two K chunks per stage halve the per-stage MMA-warp bookkeeping when 4 stages still fit
-    p.ksub = kSmemBudget / (int)(2 * p.sub_bytes) >= 4 ? 2 : 1;
+    p.ksub = kSmemBudget / (int)(2 * p.sub_bytes) >= g_wk_ksub_min_stages ? 2 : 1;
     p.stage_bytes = p.ksub * p.sub_bytes;
     p.stages = kSmemBudget / (int)p.stage_bytes;
     if (p.stages >= 2 || p.mt_per_unit == 1) break;

@@ -19,8 +19,12 @@ for (ci, co, e) in SHAPES:
     gb = torch.zeros(co, device='cuda')
     ws = torch.empty(_lib.call_size("vm_conv3d_wgrad_tc_ws", 1, ci, co, e, e, e) // 4 + 64, device='cuda')
     res, outs = {}, {}
-    for rt in (1, 0):
-        lib.vm_debug_set_wgrad_kd_runtime(rt)
+    mode = sys.argv[1] if len(sys.argv) > 1 else "runtime"
+    for rt in ((1, 0) if mode == "runtime" else (4, 3, 2)):
+        if mode == "runtime":
+            lib.vm_debug_set_wgrad_kd_runtime(rt)
+        else:
+            lib.vm_debug_set_wgrad_ksub_stages(rt)
 
         def run():
             _lib.call("vm_conv3d_wgrad_tc", x.p(), x.bstride, g.p(), g.bstride, _lib.ptr(gw), _lib.ptr(gb),
@@ -45,5 +49,9 @@ for (ci, co, e) in SHAPES:
         res[rt] = e0.elapsed_time(e1) * 1e3 / 50
         outs[rt] = (gw.clone(), gb.clone())
     lib.vm_debug_set_wgrad_kd_runtime(0)
-    same = torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
-    print(f"{ci}->{co} @{e}^3: runtime loop {res[1]:.1f} us, straight-line {res[0]:.1f} us, bitwise same {same}")
+    lib.vm_debug_set_wgrad_ksub_stages(2)
+    if mode == "runtime":
+        same = torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+        print(f"{ci}->{co} @{e}^3: runtime loop {res[1]:.1f} us, straight-line {res[0]:.1f} us, bitwise same {same}")
+    else:
+        print(f"{ci}->{co} @{e}^3: ksub min-stages 4/3/2: {res[4]:.1f} / {res[3]:.1f} / {res[2]:.1f} us")
