@@ -56,8 +56,8 @@ int vm_num_sms(int device);
 /* number of kernels this library has launched in this process (bench bookkeeping) */
 long long vm_launch_count(void);
 /* programmatic dependent launch between this library's kernels (default from $VM_PDL):
- * 0 off, 1 on with the trigger at kernel start, 2 on with the trigger at CTA exit;
- * returns the previous setting */
+ * 0 off, 1 on with the trigger at kernel start, 2 on with the trigger at CTA exit; the mode
+ * is per calling host thread; returns the previous setting */
 int vm_set_pdl(int on);
 
 /* ------------------------------------------------------------------ boxes / halo

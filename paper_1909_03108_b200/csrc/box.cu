@@ -24,7 +24,8 @@ void set_error(const char* fmt, ...) {
 static std::atomic<long long> g_launches{0};
 void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
-static int g_pdl = -1;  // -1: from $VM_PDL (default off); 1: early trigger; 2: late (implicit) trigger
+// per host thread: the threads mesh drives one rank per thread, each setting its own mode
+static thread_local int g_pdl = -1;  // -1: from $VM_PDL (default off); 1: early trigger; 2: late (implicit) trigger
 bool pdl_enabled() {
   if (g_pdl < 0) {
     const char* e = getenv("VM_PDL");
