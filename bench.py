@@ -445,6 +445,15 @@ def run_ours(a):
         "gpu_launches": launches_per_step * a.steps,
         "halo": halo,
         "kernel_ms_per_step": {k: round(c["ms"], 4) for k, c in classes.items()},
+        # every kernel class against its own roofline (tensor for convs, HBM for the rest),
+        # each launch replayed alone: the dominant class above is one row of this table
+        "roofline_by_kind": {
+            k: ({"bound": "tensor", "tflops": round(c["flops"] / (c["ms"] * 1e-3) / 1e12, 1),
+                 "frac": round(c["flops"] / (c["ms"] * 1e-3) / 1e12 / peaks["bf16_tflops"], 3)}
+                if c["flops"] > 0 and k.startswith("conv") else
+                {"bound": "hbm", "gbs": round(c["bytes"] / (c["ms"] * 1e-3) / 1e9, 0),
+                 "frac": round(c["bytes"] / (c["ms"] * 1e-3) / 1e9 / peaks["hbm_gbs"], 3)})
+            for k, c in classes.items() if c["ms"] > 0},
         "conv_tflops_effective": conv_flops / (conv_ms * 1e-3) / 1e12 if conv_ms else None,
     }
     print(json.dumps(line), flush=True)
