@@ -25,6 +25,8 @@ for (ci, co, e) in SHAPES:
             lib.vm_debug_set_wgrad_kd_runtime(rt)
         else:
             lib.vm_debug_set_wgrad_ksub_stages(rt)
+        # the workspace depends on the plan (cluster mode keeps one partial per 8 CTAs)
+        ws = torch.empty(_lib.call_size("vm_conv3d_wgrad_tc_ws", 1, ci, co, e, e, e) // 4 + 64, device='cuda')
 
         def run():
             _lib.call("vm_conv3d_wgrad_tc", x.p(), x.bstride, g.p(), g.bstride, _lib.ptr(gw), _lib.ptr(gb),
