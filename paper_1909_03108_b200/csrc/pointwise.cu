@@ -407,7 +407,9 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_fwd_fixed(
   constexpr int U = C <= 16 ? 2 : 1;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < nvox; v0 += U * stride) {
-    float yv[U][C], gk[U][NC];
+    // logits accumulated as the channel groups arrive (same c order as a full dot product,
+    // so bitwise the same), instead of holding all C inputs: C = 32/64 spilled otherwise
+    float lgu[U][NC], gk[U][NC];
     bool ok[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -417,11 +419,15 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_fwd_fixed(
       decompose(ok[u] ? (uint32_t)v : 0u, sy, b, d, h, w);
       const T* base = y + sy.at(b, 0, d, h, w);
 #pragma unroll
+      for (int k = 0; k < NC; ++k) lgu[u][k] = sb[k];
+#pragma unroll 2
       for (int cg = 0; cg < C / 8; ++cg) {
         float t8[8];
         V8<T>::ld(base + cg * sy.plane(), t8);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) yv[u][cg * 8 + j] = t8[j];
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+          for (int k = 0; k < NC; ++k) lgu[u][k] = fmaf(t8[j], sW[(cg * 8 + j) * NC + k], lgu[u][k]);
       }
 #pragma unroll
       for (int k = 0; k < NC; ++k) gk[u][k] = ok[u] ? onehot[v * NC + k] : 0.f;
@@ -432,11 +438,7 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_fwd_fixed(
       const int64_t v = v0 + u * stride;
       float lg[NC];
 #pragma unroll
-      for (int k = 0; k < NC; ++k) lg[k] = sb[k];
-#pragma unroll
-      for (int c = 0; c < C; ++c)
-#pragma unroll
-        for (int k = 0; k < NC; ++k) lg[k] = fmaf(yv[u][c], sW[c * NC + k], lg[k]);
+      for (int k = 0; k < NC; ++k) lg[k] = lgu[u][k];
       float m = lg[0];
 #pragma unroll
       for (int k = 1; k < NC; ++k) m = fmaxf(m, lg[k]);
@@ -873,10 +875,12 @@ extern "C" int vm_head_fwd(int dtype, const void* y, int64_t y_bstride, const fl
   Slab sy = SLAB(y_bstride, C, D, H, W);
   int grid = vm_head_partials_count(B, D, H, W);
   size_t sh = (C * ncls + ncls + 32) * sizeof(float);
-  if (dtype == VM_BF16 && ncls == 3 && (C == 16 || C == 32 || C == 8)) {
+  if (dtype == VM_BF16 && ncls == 3 && (C == 16 || C == 32 || C == 8 || C == 64)) {
     using T = __nv_bfloat16;
     auto st = as_stream(stream);
-    if (C == 16)
+    if (C == 64)
+      launch_pdl(k_head_fwd_fixed<T, 64, 3>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, onehot, probs, partials, B, clamp);
+    else if (C == 16)
       launch_pdl(k_head_fwd_fixed<T, 16, 3>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, onehot, probs, partials, B, clamp);
     else if (C == 32)
       launch_pdl(k_head_fwd_fixed<T, 32, 3>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, onehot, probs, partials, B, clamp);
@@ -907,7 +911,7 @@ extern "C" int vm_head_bwd(int dtype, const void* y, int64_t y_bstride, const fl
   Slab sy = SLAB(y_bstride, C, D, H, W), sg = SLAB(g_bstride, C, D, H, W);
   int grid = vm_head_partials_count(B, D, H, W);
   size_t sh = (C * ncls + ncls + 32 + 3 * kMaxCls) * sizeof(float);
-  if (dtype == VM_BF16 && ncls == 3 && (C == 16 || C == 32 || C == 8)) {
+  if (dtype == VM_BF16 && ncls == 3 && (C == 16 || C == 32 || C == 8 || C == 64 || C == 128)) {
     using T = __nv_bfloat16;
     auto st = as_stream(stream);
 #define HEAD_BWD_FIXED(CC)                                                                          \
@@ -918,6 +922,10 @@ extern "C" int vm_head_bwd(int dtype, const void* y, int64_t y_bstride, const fl
       HEAD_BWD_FIXED(16);
     else if (C == 32)
       HEAD_BWD_FIXED(32);
+    else if (C == 64)  // wide first levels (recipe_for_resolution(256, 1.0)): the generic
+      HEAD_BWD_FIXED(64);  // one-thread-per-voxel kernel took 38.7 ms at 256^3
+    else if (C == 128)
+      HEAD_BWD_FIXED(128);
     else
       HEAD_BWD_FIXED(8);
 #undef HEAD_BWD_FIXED

@@ -140,3 +140,20 @@ def test_train_loop_host_matches_step_by_step():
     for k in pa:
         assert np.array_equal(pa[k]["kernel"], pb[k]["kernel"])
     mesh.shutdown()
+
+
+@pytest.mark.parametrize("filters", [(64, 128), (128, 256)])
+def test_tc_step_wide_base_head(filters):
+    # 64/128-channel head input: the fixed head fwd/bwd kernels for wide first levels
+    mesh, graph, params, x, oh = _setup(extent=16, filters=filters, cpb=1, seed=7)
+    st, probs, stats, grads = _run(graph, params, x, oh, torch.bfloat16, "tc")
+    rprobs, rstats, rgrads, _ = oracle_step(graph, params, x, oh)
+    assert rel_l2(probs, rprobs) <= 1e-2
+    assert rel_l2(stats, rstats) <= 1e-2
+    head = [k for k in rgrads if k.startswith("head")]
+    for k in head:
+        assert rel_l2(grads[k][0], rgrads[k][0]) <= 2e-2, k
+        assert rel_l2(grads[k][1], rgrads[k][1]) <= 2e-2, k
+    worst = max(rel_l2(grads[k][0], rgrads[k][0]) for k in rgrads)
+    assert worst <= 1e-1, worst
+    mesh.shutdown()
