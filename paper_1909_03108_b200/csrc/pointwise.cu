@@ -875,18 +875,24 @@ extern "C" int vm_head_fwd(int dtype, const void* y, int64_t y_bstride, const fl
   Slab sy = SLAB(y_bstride, C, D, H, W);
   int grid = vm_head_partials_count(B, D, H, W);
   size_t sh = (C * ncls + ncls + 32) * sizeof(float);
-  if (dtype == VM_BF16 && ncls == 3 && (C == 16 || C == 32 || C == 8 || C == 64)) {
+  if (dtype == VM_BF16) {  // fixed-width kernels: C in {8, 16, 32, 64}, 2..4 classes
     using T = __nv_bfloat16;
     auto st = as_stream(stream);
-    if (C == 64)
-      launch_pdl(k_head_fwd_fixed<T, 64, 3>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, onehot, probs, partials, B, clamp);
-    else if (C == 16)
-      launch_pdl(k_head_fwd_fixed<T, 16, 3>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, onehot, probs, partials, B, clamp);
-    else if (C == 32)
-      launch_pdl(k_head_fwd_fixed<T, 32, 3>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, onehot, probs, partials, B, clamp);
-    else
-      launch_pdl(k_head_fwd_fixed<T, 8, 3>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, onehot, probs, partials, B, clamp);
+#define HF_CASE(CC, NN)                                                                               \
+  case NN * 1000 + CC:                                                                                \
+    launch_pdl(k_head_fwd_fixed<T, CC, NN>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, onehot, \
+               probs, partials, B, clamp);                                                            \
     return launch_status("vm_head_fwd");
+#define HF_ROW(NN) HF_CASE(8, NN) HF_CASE(16, NN) HF_CASE(32, NN) HF_CASE(64, NN)
+    switch (ncls * 1000 + C) {
+      HF_ROW(2)
+      HF_ROW(3)
+      HF_ROW(4)
+      default:
+        break;
+    }
+#undef HF_ROW
+#undef HF_CASE
   }
   DISPATCH_T(dtype, "vm_head_fwd",
              k_head_fwd<T><<<grid, kHeadThreads, sh, as_stream(stream)>>>(
@@ -911,25 +917,24 @@ extern "C" int vm_head_bwd(int dtype, const void* y, int64_t y_bstride, const fl
   Slab sy = SLAB(y_bstride, C, D, H, W), sg = SLAB(g_bstride, C, D, H, W);
   int grid = vm_head_partials_count(B, D, H, W);
   size_t sh = (C * ncls + ncls + 32 + 3 * kMaxCls) * sizeof(float);
-  if (dtype == VM_BF16 && ncls == 3 && (C == 16 || C == 32 || C == 8 || C == 64 || C == 128)) {
-    using T = __nv_bfloat16;
+  if (dtype == VM_BF16) {  // fixed-width kernels: C in {8, 16, 32, 64, 128}, 2..4 classes (the
+    using T = __nv_bfloat16;  // generic one-thread-per-voxel kernel took 38.7 ms at 256^3, C = 64)
     auto st = as_stream(stream);
-#define HEAD_BWD_FIXED(CC)                                                                          \
-  launch_pdl(k_head_bwd_grp<T, CC, 3>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, onehot, stats, (T*)g, sg, \
-                                                            wpartials, B, w_dice, w_ce, total_voxels,    \
-                                                            dice_mask, clamp, relu_mask)
-    if (C == 16)
-      HEAD_BWD_FIXED(16);
-    else if (C == 32)
-      HEAD_BWD_FIXED(32);
-    else if (C == 64)  // wide first levels (recipe_for_resolution(256, 1.0)): the generic
-      HEAD_BWD_FIXED(64);  // one-thread-per-voxel kernel took 38.7 ms at 256^3
-    else if (C == 128)
-      HEAD_BWD_FIXED(128);
-    else
-      HEAD_BWD_FIXED(8);
-#undef HEAD_BWD_FIXED
+#define HB_CASE(CC, NN)                                                                                  \
+  case NN * 1000 + CC:                                                                                   \
+    launch_pdl(k_head_bwd_grp<T, CC, NN>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, onehot, stats, \
+               (T*)g, sg, wpartials, B, w_dice, w_ce, total_voxels, dice_mask, clamp, relu_mask);          \
     return launch_status("vm_head_bwd");
+#define HB_ROW(NN) HB_CASE(8, NN) HB_CASE(16, NN) HB_CASE(32, NN) HB_CASE(64, NN) HB_CASE(128, NN)
+    switch (ncls * 1000 + C) {
+      HB_ROW(2)
+      HB_ROW(3)
+      HB_ROW(4)
+      default:
+        break;
+    }
+#undef HB_ROW
+#undef HB_CASE
   }
   DISPATCH_T(dtype, "vm_head_bwd",
              k_head_bwd<T><<<grid, kHeadThreads, sh, as_stream(stream)>>>(

@@ -7,7 +7,7 @@ import torch
 import paper_1909_03108_b200 as vm
 from oracle import voxmesh_oracle as O
 from paper_1909_03108_b200.step import UNetStep
-from tests.helpers import oracle_step, rel_l2
+from tests.helpers import node_tuples, oracle_step, rel_l2
 
 pytestmark = pytest.mark.gpu
 
@@ -154,6 +154,38 @@ def test_tc_step_wide_base_head(filters):
     for k in head:
         assert rel_l2(grads[k][0], rgrads[k][0]) <= 2e-2, k
         assert rel_l2(grads[k][1], rgrads[k][1]) <= 2e-2, k
+    worst = max(rel_l2(grads[k][0], rgrads[k][0]) for k in rgrads)
+    assert worst <= 1e-1, worst
+    mesh.shutdown()
+
+
+@pytest.mark.parametrize("ncls,dice", [(2, (1,)), (4, (1, 2))])
+def test_tc_step_other_class_counts(ncls, dice):
+    # 2 and 4 classes: the fixed head kernels' other instantiations against the oracle
+    cfg = vm.UNetConfig(16, (16, 32), convs_per_block=1, num_classes=ncls)
+    mesh = vm.create_mesh([("one", 1)])
+    graph = vm.build(cfg, mesh, {})
+    params = vm.init_params(graph, 2)
+    img, labels = O.record_for(16, 0)
+    labels = np.minimum(labels, ncls - 1).astype(labels.dtype)
+    x = img[None, ..., None]
+    oh = O.one_hot(labels[None], ncls)
+    st = UNetStep(graph, params, dtype=torch.bfloat16, conv_impl="tc", device="cuda", dice_classes=dice)
+    st.keep_probs = True
+    st.load_inputs(torch.from_numpy(x).cuda(), torch.from_numpy(oh).cuda())
+    st.forward()
+    st.backward()
+    torch.cuda.synchronize()
+    probs = st.probs.reshape(oh.shape).cpu().numpy()
+    stats, grads = st.stats.cpu().numpy(), st.grad_dict()
+    p64 = {k: {"kernel": np.asarray(v["kernel"], np.float64), "bias": np.asarray(v["bias"], np.float64)}
+           for k, v in params.items()}
+    rprobs, tape, _ = O.oracle_forward(node_tuples(graph), p64, x.astype(np.float64))
+    rstats = O.loss_stats(rprobs, oh.astype(np.float64))
+    dprobs = O.loss_grad(rprobs, oh.astype(np.float64), rstats, int(np.prod(x.shape[:4])), dice_classes=dice)
+    rgrads, _ = O.oracle_backward(node_tuples(graph), p64, tape, dprobs)
+    assert rel_l2(probs, rprobs) <= 1e-2
+    assert rel_l2(stats, rstats) <= 1e-2
     worst = max(rel_l2(grads[k][0], rgrads[k][0]) for k in rgrads)
     assert worst <= 1e-1, worst
     mesh.shutdown()
