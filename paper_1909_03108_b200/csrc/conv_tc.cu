@@ -1622,6 +1622,8 @@ extern "C" int vm_pack_weights(const float* w, void* packed, int Cin, int Cout, 
 static long long* g_fwd_dbg = nullptr;
 static int g_sweep_xmode = 0;
 extern "C" void vm_debug_set_sweep_mode(int m) { g_sweep_xmode = m; }
+static int g_sweep_force_mb = 0;  // A/B probes: restrict the sweep planner to one MB
+extern "C" void vm_debug_set_sweep_mb(int mb) { g_sweep_force_mb = mb; }
 
 // Plan + launch of the kd-stacked sweep kernel (weights packed with PackGeom::sweep).
 // Units = (sample, column of MB*128 in-plane anchors, segment of S output planes); MB and
@@ -1663,6 +1665,7 @@ static int launch_sweep(const FwdParams& f, int nsm, void* stream) {
   };
   double best = 1e30;
   for (int MB = 4; MB >= 1; --MB) {
+    if (g_sweep_force_mb && MB != g_sweep_force_mb) continue;
     int ring = 512 / (MB * p.Nc);
     if (ring > kSwMaxRing) ring = kSwMaxRing;
     if (ring < 4) continue;
