@@ -1623,6 +1623,8 @@ static long long* g_fwd_dbg = nullptr;
 static int g_sweep_xmode = 0;
 extern "C" void vm_debug_set_sweep_mode(int m) { g_sweep_xmode = m; }
 static int g_sweep_force_mb = 0;  // A/B probes: restrict the sweep planner to one MB
+static int g_fwd_force_mb = 0, g_fwd_force_acc = 0;  // A/B probes: restrict the general fwd planner
+extern "C" void vm_debug_set_fwd_plan(int mb, int nacc) { g_fwd_force_mb = mb, g_fwd_force_acc = nacc; }
 extern "C" void vm_debug_set_sweep_mb(int mb) { g_sweep_force_mb = mb; }
 
 // Plan + launch of the kd-stacked sweep kernel (weights packed with PackGeom::sweep).
@@ -1821,6 +1823,7 @@ static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, 
   double best = 1e30;
   int bMB = 1, bacc = 1, bbuf = 1, bstages = 0, bsplit = 1;
   for (int MB = 1; MB <= 8; ++MB) {
+    if (g_fwd_force_mb && MB != g_fwd_force_mb) continue;
     const int R = MB * 128 + 2 * p.Wp + 2;
     const uint32_t a_bytes = (uint32_t)((R + 7) / 8 * 8) * 16;
     const uint32_t stage_bytes = 2 * a_bytes + p.b_bytes;
@@ -1838,13 +1841,16 @@ static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, 
       const int64_t units = ntu * ksplit;
       const int64_t waves = (units + nsm - 1) / nsm;
       for (int nacc : {1, 3}) {
+        if (g_fwd_force_acc && nacc != g_fwd_force_acc) continue;
         for (int nbuf = 2; nbuf >= 1; --nbuf) {
           if (nbuf * MB * nacc * N > 512) continue;
           const double mma = 9.0 * MB * mma_cycles(N, MB * nacc);
           const double smem = (2.0 * R * 16 + p.b_bytes + 9.0 * MB * (4096 + 32.0 * N)) / 128.0;
           const double stage = mma > smem ? mma : smem;
-          // single-buffered TMEM: the epilogue drain (~MB*N/8 x 200 cycles) is not overlapped
-          const double drain = nbuf == 1 ? MB * (N / 8.0) * 200.0 / (MB > 1 ? 2 : 1) : 0.0;
+          // single-buffered TMEM: the epilogue drain is not overlapped (~600 cycles per
+          // 8-channel group and thread, measured with tools/dbg_fwd_probe.py; 200 made the
+          // planner pick MB = 5 single-buffered for 32->96 at 64^3: 64.9 us vs 48.4 at MB = 2)
+          const double drain = nbuf == 1 ? MB * (N / 8.0) * 600.0 / (MB > 1 ? 2 : 1) : 0.0;
           // split: partial write + the last split's read-back of every partial
           const double fix = ksplit > 1 ? MB * (N / 8.0) * (150.0 + 100.0 * ksplit) : 0.0;
           const double cost = (double)waves * ((double)spk * stage + drain + fix + 2000.0);
