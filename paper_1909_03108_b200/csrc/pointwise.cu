@@ -862,7 +862,7 @@ extern "C" int vm_relu_mask(int dtype, const void* g, int64_t g_bstride, const v
 extern "C" int vm_head_partials_count(int B, int D, int H, int W) {
   int64_t nvox = (int64_t)B * D * H * W;
   int64_t blocks = (nvox + kHeadThreads - 1) / kHeadThreads;
-  int cap = 148 * 4;
+  int cap = 148 * 2;  // one wave of 2 resident 256-thread blocks per SM (register-limited)
   return (int)(blocks < cap ? (blocks < 1 ? 1 : blocks) : cap);
 }
 
