@@ -300,7 +300,7 @@ int c1_setup(C1Params& p, int B, int Cout, int D, int H, int W) {
   return VM_OK;
 }
 
-constexpr int kC1WgCtasPerSm = 8;  // weight gradient: cap (partials), below the occupancy
+constexpr int kC1WgCtasPerSm = 16;  // weight gradient: cap on the partial count (occupancy binds first)
 
 // One wave: as many CTAs as are resident at once (a second partial wave cost 1.33x).  The
 // runtime occupancy query answers 1 CTA/SM for these TMEM-allocating kernels, so the limit is
