@@ -1623,6 +1623,8 @@ static long long* g_fwd_dbg = nullptr;
 static int g_sweep_xmode = 0;
 extern "C" void vm_debug_set_sweep_mode(int m) { g_sweep_xmode = m; }
 static int g_sweep_force_mb = 0;  // A/B probes: restrict the sweep planner to one MB
+static int g_sweep_force_s = 0;   // A/B probes: restrict the sweep planner to one segment length
+extern "C" void vm_debug_set_sweep_s(int sv) { g_sweep_force_s = sv; }
 static int g_fwd_force_mb = 0, g_fwd_force_acc = 0;  // A/B probes: restrict the general fwd planner
 extern "C" void vm_debug_set_fwd_plan(int mb, int nacc) { g_fwd_force_mb = mb, g_fwd_force_acc = nacc; }
 extern "C" void vm_debug_set_sweep_mb(int mb) { g_sweep_force_mb = mb; }
@@ -1682,6 +1684,7 @@ static int launch_sweep(const FwdParams& f, int nsm, void* stream) {
     // + ~900 cycles of per-plane MMA-warp bookkeeping (measured with tools/dbg_sweep_probe.py)
     const double plane = (9.0 * p.KC + 1) * MB * mma_cycles(3 * p.Nc, MB) * (ring < 6 ? 1.15 : 1.0) + 900.0;
     for (int S = 1; S <= p.D; ++S) {
+      if (g_sweep_force_s && S != g_sweep_force_s && g_sweep_force_s <= p.D) continue;
       const int nseg = (p.D + S - 1) / S;
       const int64_t units = (int64_t)f.B * ncol * nseg;
       const int64_t waves = (units + nsm - 1) / nsm;

@@ -19,8 +19,13 @@ for (ci, co, e, dg) in [(16, 16, 128, 0), (16, 16, 128, 1), (32, 32, 64, 0), (32
     wp = torch.empty(_lib.call_size("vm_packed_weights_bytes", ci, co) // 2, dtype=torch.bfloat16, device='cuda')
     _lib.call("vm_pack_weights", _lib.ptr(w), _lib.ptr(wp), ci, co, 0, _lib.stream_ptr())
     res = {}
-    for mb in (0, 1, 2, 3, 4):
-        lib.vm_debug_set_sweep_mb(mb)
+    knob = sys.argv[1] if len(sys.argv) > 1 else "mb"
+    vals = (0, 1, 2, 3, 4) if knob == "mb" else (0, 4, 8, 12, 16, 24, 32)
+    for mb in vals:
+        if knob == "mb":
+            lib.vm_debug_set_sweep_mb(mb)
+        else:
+            lib.vm_debug_set_sweep_s(mb)
         try:
             s = torch.cuda.Stream()
             with torch.cuda.stream(s):
@@ -50,4 +55,6 @@ for (ci, co, e, dg) in [(16, 16, 128, 0), (16, 16, 128, 1), (32, 32, 64, 0), (32
         except Exception:
             res[mb] = "-"
     lib.vm_debug_set_sweep_mb(0)
-    print(f"{ci}->{co} @{e}^3 {'dgrad' if dg else 'fwd'}: auto/1/2/3/4 = " + " / ".join(res[m] for m in (0, 1, 2, 3, 4)))
+    lib.vm_debug_set_sweep_s(0)
+    print(f"{ci}->{co} @{e}^3 {'dgrad' if dg else 'fwd'} {knob} auto/" + "/".join(str(v) for v in vals[1:]) + " = "
+          + " / ".join(res[m] for m in vals))
