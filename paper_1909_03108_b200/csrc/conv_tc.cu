@@ -2096,6 +2096,7 @@ static bool plan_wgrad_kd(int B, int Cin, int Cout, int D, int H, int W, WkParam
   p.nkw = 9 * p.Nc <= 512 ? 3 : 1;
   p.mt_per_unit = 512 / (p.nkw * 3 * p.Nc);
   if (p.mt_per_unit > p.MT) p.mt_per_unit = p.MT;
+  if (g_force_mpu > 0 && g_force_mpu < p.mt_per_unit) p.mt_per_unit = g_force_mpu;  // A/B probes
   while (p.mt_per_unit > 1 && p.MT % p.mt_per_unit) --p.mt_per_unit;  // equal groups (kernel template)
   if (p.mt_per_unit < 1) return false;
   p.g_bytes = (uint32_t)(p.Nc / 8) * p.KS * 16;
