@@ -1591,8 +1591,16 @@ __global__ void k_pack_batch(const vm_pack_job* __restrict__ jobs, int njobs, in
         f[e] = (ci0 + e < g.cin && co < g.cout) ? w[((int64_t)t * jb.cin + ci0 + e) * jb.cout + co] : 0.f;
     } else {  // W'[t][ci'][co'] = W[26 - t][co'][ci']: 8 consecutive floats of row co'
       const float* src = w + ((int64_t)(26 - t) * jb.cin + co) * jb.cout + ci0;
+      if (co < g.cout && ci0 + 8 <= g.cin && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        // two 16-byte loads instead of eight scalar ones (each lane reads its own row: the
+        // scalar form made the kernel L1-wavefront bound)
+        const float4 a = __ldg(reinterpret_cast<const float4*>(src));
+        const float4 c = __ldg(reinterpret_cast<const float4*>(src + 4));
+        f[0] = a.x, f[1] = a.y, f[2] = a.z, f[3] = a.w, f[4] = c.x, f[5] = c.y, f[6] = c.z, f[7] = c.w;
+      } else {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) f[e] = (ci0 + e < g.cin && co < g.cout) ? src[e] : 0.f;
+        for (int e = 0; e < 8; ++e) f[e] = (ci0 + e < g.cin && co < g.cout) ? src[e] : 0.f;
+      }
     }
     uint4 o;
     o.x = pack_bf16x2(f[0], f[1]);
