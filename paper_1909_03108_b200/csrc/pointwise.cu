@@ -742,10 +742,18 @@ __global__ void k_sgd_check(const float* __restrict__ g, const int64_t* __restri
   pdl_wait();
   for (int i = threadIdx.x; i <= nl; i += blockDim.x) soff[i] = off[i];
   __syncthreads();
-  const int64_t n = soff[nl];
-  for (int64_t i = soff[0] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    if (!isfinite(g[i])) atomicOr(&flags[sgd_layer(soff, nl, i)], 1);  // rare
+  const int64_t a = soff[0], n = soff[nl];
+  // 4 elements per thread (16-byte loads from a 16-byte aligned base); the layer lookup only
+  // for the rare non-finite element
+  for (int64_t i = (a & ~3LL) + 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); i < n;
+       i += 4 * (int64_t)gridDim.x * blockDim.x) {
+    if (i >= a && i + 4 <= n && (reinterpret_cast<uintptr_t>(g + i) & 15) == 0) {
+      const float4 v = *reinterpret_cast<const float4*>(g + i);
+      if (isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w)) continue;
+    }
+    for (int64_t j = i; j < i + 4 && j < n; ++j)
+      if (j >= a && !isfinite(g[j])) atomicOr(&flags[sgd_layer(soff, nl, j)], 1);  // rare
+  }
 }
 
 __global__ void k_sgd_apply(float* __restrict__ p, float* __restrict__ v, const float* __restrict__ g,
@@ -759,14 +767,37 @@ __global__ void k_sgd_apply(float* __restrict__ p, float* __restrict__ v, const 
     if (i < nl) sflag[i] = flags[i];
   }
   __syncthreads();
-  const int64_t n = soff[nl];
-  for (int64_t i = soff[0] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    if (sflag[sgd_layer(soff, nl, i)]) continue;
-    // numpy fp32 order: v *= mu; v += g; p -= lr * v   (no FMA contraction)
-    float vv = __fadd_rn(__fmul_rn(v[i], mu), g[i]);
-    v[i] = vv;
-    p[i] = __fsub_rn(p[i], __fmul_rn(lr, vv));
+  const int64_t a = soff[0], n = soff[nl];
+  // numpy fp32 order: v *= mu; v += g; p -= lr * v   (no FMA contraction)
+  auto upd = [&](float& pp, float& vv, float gg) {
+    vv = __fadd_rn(__fmul_rn(vv, mu), gg);
+    pp = __fsub_rn(pp, __fmul_rn(lr, vv));
+  };
+  // 4 elements per thread: one layer lookup when all four are in the same layer
+  for (int64_t i = (a & ~3LL) + 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); i < n;
+       i += 4 * (int64_t)gridDim.x * blockDim.x) {
+    const bool vec = i >= a && i + 4 <= n && ((reinterpret_cast<uintptr_t>(p + i) | reinterpret_cast<uintptr_t>(v + i) |
+                                               reinterpret_cast<uintptr_t>(g + i)) & 15) == 0;
+    const int l0 = sgd_layer(soff, nl, i >= a ? i : a);
+    if (vec && (l0 + 1 >= nl + 1 || soff[l0 + 1] >= i + 4)) {  // all four in layer l0
+      if (sflag[l0]) continue;
+      float4 pp = *reinterpret_cast<float4*>(p + i), vv = *reinterpret_cast<float4*>(v + i);
+      const float4 gg = *reinterpret_cast<const float4*>(g + i);
+      upd(pp.x, vv.x, gg.x);
+      upd(pp.y, vv.y, gg.y);
+      upd(pp.z, vv.z, gg.z);
+      upd(pp.w, vv.w, gg.w);
+      *reinterpret_cast<float4*>(v + i) = vv;
+      *reinterpret_cast<float4*>(p + i) = pp;
+      continue;
+    }
+    for (int64_t j = i; j < i + 4 && j < n; ++j) {
+      if (j < a || sflag[sgd_layer(soff, nl, j)]) continue;
+      float pp = p[j], vv = v[j];
+      upd(pp, vv, g[j]);
+      v[j] = vv;
+      p[j] = pp;
+    }
   }
 }
 

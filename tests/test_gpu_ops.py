@@ -129,3 +129,35 @@ def test_bf16_slab_upsample_and_pool_bit_exact(C, D, H, W):
                   _lib.stream_ptr())
         rp, _ = O.maxpool2_dense(x)
         assert np.array_equal(ps.interior().float().cpu().numpy(), rp)
+
+
+def test_sgd_momentum_bitwise_and_nonfinite_skip():
+    # vm_sgd_momentum (training.py:202-219): numpy fp32 op order per element, layers with
+    # non-finite gradients skipped entirely; odd layer sizes exercise the 4-wide path's edges
+    from paper_1909_03108_b200 import _lib
+    rng = np.random.default_rng(17)
+    sizes = [5, 4096 + 3, 7, 12, 1025, 64]
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    n = int(off[-1])
+    p = rng.standard_normal(n).astype(np.float32)
+    v = rng.standard_normal(n).astype(np.float32)
+    g = rng.standard_normal(n).astype(np.float32)
+    g[off[1] + 100] = np.nan  # layer 1 is skipped
+    g[off[4] + 3] = np.inf    # layer 4 is skipped
+    lr, mu = np.float32(0.01), np.float32(0.9)
+    pt, vt, gt = (torch.from_numpy(a.copy()).cuda() for a in (p, v, g))
+    ot = torch.from_numpy(off).cuda()
+    flags = torch.zeros(len(sizes), dtype=torch.int32, device="cuda")
+    _lib.call("vm_sgd_momentum", _lib.ptr(pt), _lib.ptr(vt), _lib.ptr(gt), _lib.ptr(ot), len(sizes), max(sizes),
+              _lib.ptr(flags), float(lr), float(mu), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    rp, rv = p.copy(), v.copy()
+    for li, (a, b) in enumerate(zip(off[:-1], off[1:])):
+        if not np.isfinite(g[a:b]).all():
+            continue
+        rv[a:b] = rv[a:b] * mu
+        rv[a:b] = rv[a:b] + g[a:b]
+        rp[a:b] = rp[a:b] - lr * rv[a:b]
+    assert np.array_equal(pt.cpu().numpy().view(np.uint32), rp.view(np.uint32))
+    assert np.array_equal(vt.cpu().numpy().view(np.uint32), rv.view(np.uint32))
+    assert flags.cpu().numpy().tolist() == [0, 1, 0, 0, 1, 0]
