@@ -392,10 +392,34 @@ __global__ void k_onehot(const uint8_t* __restrict__ lab, float* __restrict__ oh
   }
 }
 
+// 3 classes: 4 voxels per thread, one 4-byte label load and three 16-byte stores (the scalar
+// kernel above spends a 64-bit division per output float)
+__global__ void k_onehot3x4(const uint8_t* __restrict__ lab, float* __restrict__ oh, int64_t n4) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n4; q += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t l4 = reinterpret_cast<const uint32_t*>(lab)[q];
+    float o[12];
+#pragma unroll
+    for (int vv = 0; vv < 4; ++vv) {
+      const uint32_t l = (l4 >> (8 * vv)) & 0xFFu;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) o[vv * 3 + c] = l == (uint32_t)c ? 1.f : 0.f;
+    }
+    float4* dst = reinterpret_cast<float4*>(oh + q * 12);
+    dst[0] = make_float4(o[0], o[1], o[2], o[3]);
+    dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+    dst[2] = make_float4(o[8], o[9], o[10], o[11]);
+  }
+}
+
 extern "C" int vm_onehot_u8(const uint8_t* labels, float* onehot, int64_t nvox, int ncls,
                             void* stream) {
   VM_REQUIRE(labels && onehot && nvox >= 0 && ncls > 0, VM_E_ARG, "vm_onehot_u8: bad argument");
   if (nvox == 0) return VM_OK;
+  if (ncls == 3 && nvox % 4 == 0 && (reinterpret_cast<uintptr_t>(labels) & 3) == 0 &&
+      (reinterpret_cast<uintptr_t>(onehot) & 15) == 0) {
+    k_onehot3x4<<<grid_for(nvox / 4, 256), 256, 0, as_stream(stream)>>>(labels, onehot, nvox / 4);
+    return launch_status("vm_onehot_u8");
+  }
   k_onehot<<<grid_for(nvox * ncls, 256), 256, 0, as_stream(stream)>>>(labels, onehot, nvox, ncls);
   return launch_status("vm_onehot_u8");
 }

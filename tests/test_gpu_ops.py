@@ -161,3 +161,14 @@ def test_sgd_momentum_bitwise_and_nonfinite_skip():
     assert np.array_equal(pt.cpu().numpy().view(np.uint32), rp.view(np.uint32))
     assert np.array_equal(vt.cpu().numpy().view(np.uint32), rv.view(np.uint32))
     assert flags.cpu().numpy().tolist() == [0, 1, 0, 0, 1, 0]
+
+
+@pytest.mark.parametrize("nvox,ncls", [(4096, 3), (4095, 3), (1000, 2), (64, 4)])
+def test_onehot_u8_kernel(nvox, ncls):
+    # vm_onehot_u8 (training.py:68-69 on the GPU): the 4-voxel vector path and the scalar path
+    from paper_1909_03108_b200 import _lib
+    lab = np.random.default_rng(nvox).integers(0, ncls, nvox).astype(np.uint8)
+    lt = torch.from_numpy(lab).cuda()
+    oh = torch.full((nvox * ncls,), -1.0, dtype=torch.float32, device="cuda")
+    _lib.call("vm_onehot_u8", _lib.ptr(lt), _lib.ptr(oh), nvox, ncls, _lib.stream_ptr())
+    assert np.array_equal(oh.cpu().numpy().reshape(nvox, ncls), np.eye(ncls, dtype=np.float32)[lab])
