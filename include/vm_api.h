@@ -209,19 +209,28 @@ int vm_relu_mask(int dtype, const void* g, int64_t g_bstride, const void* mask,
 /* ------------------------------------------------------------------ head + loss
  * 1x1x1 head conv (unet.py:223) + channel softmax (ops.py:190-194) + per-block
  * loss-statistics partials (training.py:77-92): stats[3*ncls+1] over the
- * block's voxels.  probs (optional, may be NULL) is dense f32 [B][D][H][W][ncls].
+ * block's voxels.  labels are the u8 class indices [B][D][H][W] (the one-hot of
+ * training.py:68-69 is never materialised); a label >= ncls sets *label_err = 1
+ * (np.eye(ncls)[labels] raises IndexError).  probs (optional, may be NULL) is
+ * dense f32 [B][D][H][W][ncls]; pred (optional) receives the u8 argmax class of
+ * every voxel, first maximum on ties (np.argmax, training.py:355).
  * partials must hold vm_head_partials_count(...) * (3*ncls+1) floats. */
 int vm_head_partials_count(int B, int D, int H, int W);
 int vm_head_fwd(int dtype, const void* y, int64_t y_bstride, const float* w, const float* b,
-                const float* onehot, float* probs, float* partials, int B, int C, int ncls, int D,
-                int H, int W, float clamp, void* stream);
+                const uint8_t* labels, int* label_err, float* probs, uint8_t* pred, float* partials,
+                int B, int C, int ncls, int D, int H, int W, float clamp, void* stream);
+/* hard-Dice counts of an argmax prediction (training.py:166-194, :355): counts[k] =
+ * |pred==k & gt==k|, counts[ncls+k] = |pred==k|, counts[2*ncls+k] = |gt==k| (exact u64).
+ * pred and gt are 16-byte aligned u8 volumes of n voxels. */
+int vm_label_counts(const uint8_t* pred, const uint8_t* gt, int64_t n, int ncls,
+                    unsigned long long* counts, void* stream);
 /* deterministic fixed-order sum of `rows` partial vectors of length `width` */
 int vm_reduce_rows(const float* partials, int rows, int width, float* out, void* stream);
 /* loss gradient from reduced stats (training.py:110-127) -> softmax backward
  * (ops.py:197-199) -> head input grad (masked by y>0) into slab g, plus
  * head-weight-grad partials [rows][C*ncls + ncls]. */
 int vm_head_bwd(int dtype, const void* y, int64_t y_bstride, const float* w, const float* b,
-                const float* onehot, const float* stats, void* g, int64_t g_bstride,
+                const uint8_t* labels, const float* stats, void* g, int64_t g_bstride,
                 float* wpartials, int B, int C, int ncls, int D, int H, int W, float w_dice,
                 float w_ce, float total_voxels, int dice_mask, float clamp, int relu_mask,
                 void* stream);
@@ -236,38 +245,12 @@ int vm_sgd_momentum(float* params, float* moments, const float* grads, const int
                     int nlayers, int64_t max_layer_elems, int* flags, float lr, float momentum,
                     void* stream);
 
-/* ------------------------------------------------------------------ SURVEY §8(b) names
- * Thin wrappers (csrc/abi.cu) carrying the entry-point names of the SURVEY's ABI sketch.
- * Transport (vm_init / vm_comm_split / vm_allreduce_f32, the NCCL half of vm_halo_fwd/bwd)
- * is torch.distributed on the Python side (mesh.py); the halo's device half is
- * vm_box_pack / vm_box_unpack / vm_box_unpack_add above. */
-/* conv3d_local (ops.py:69-97) */
-int vm_conv3d_fwd(const void* x, int64_t x_bstride, const void* wpacked, const float* bias, void* y,
-                  int64_t y_bstride, int B, int Cin, int Cout, int D, int H, int W, unsigned flags,
-                  void* stream);
-/* conv3d_input_grad_local (ops.py:100-114) [* relu mask]; Cin/Cout of the forward conv */
+/* conv3d_input_grad_local (ops.py:100-114) fused with relu_backward_local (ops.py:186-187):
+ * gx = conv(gy_halo, flip(W)^T) [* (mask > 0)] with the flip-packed operand; Cin/Cout are the
+ * FORWARD conv's (gx has Cin channels); mask may be NULL (no ReLU before this conv). */
 int vm_conv3d_dgrad(const void* gy, int64_t gy_bstride, const void* wpacked_t, const void* mask,
                     int64_t mask_bstride, void* gx, int64_t gx_bstride, int B, int Cin, int Cout,
                     int D, int H, int W, void* stream);
-/* conv3d_param_grads_local (ops.py:117-138) */
-size_t vm_conv3d_wgrad_ws(int B, int Cin, int Cout, int D, int H, int W);
-int vm_conv3d_wgrad(const void* x, int64_t x_bstride, const void* gy, int64_t gy_bstride, float* gw,
-                    float* gb, void* ws, int B, int Cin, int Cout, int D, int H, int W, void* stream);
-/* relu_backward_local (ops.py:186-187) */
-int vm_relu_bwd(int dtype, const void* g, int64_t g_bstride, const void* mask, int64_t mask_bstride,
-                void* out, int64_t out_bstride, int B, int C, int D, int H, int W, void* stream);
-/* upsample2_local (ops.py:171-173) into the concat slab's up half (unet.py:215) */
-int vm_upsample2_concat_fwd(int dtype, const void* x, int64_t x_bstride, void* y_concat,
-                            int64_t y_bstride, int B, int C, int D, int H, int W, void* stream);
-/* head + softmax + loss statistics; loss gradient + head backward (== vm_head_fwd / _bwd) */
-int vm_head_softmax_stats(int dtype, const void* y, int64_t y_bstride, const float* w,
-                          const float* b, const float* onehot, float* probs, float* partials, int B,
-                          int C, int ncls, int D, int H, int W, float clamp, void* stream);
-int vm_loss_grad_head_bwd(int dtype, const void* y, int64_t y_bstride, const float* w,
-                          const float* b, const float* onehot, const float* stats, void* g,
-                          int64_t g_bstride, float* wpartials, int B, int C, int ncls, int D, int H,
-                          int W, float w_dice, float w_ce, float total_voxels, int dice_mask,
-                          float clamp, int relu_mask, void* stream);
 
 #ifdef __cplusplus
 }

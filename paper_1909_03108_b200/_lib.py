@@ -72,20 +72,13 @@ _SIGS = {
     "vm_upsample2_bwd": (_I, [_I, _P, _L, _P, _L, _P, _L, _I, _I, _I, _I, _I, _P]),
     "vm_relu_mask": (_I, [_I, _P, _L, _P, _L, _P, _L, _I, _I, _I, _I, _I, _P]),
     "vm_head_partials_count": (_I, [_I, _I, _I, _I]),
-    "vm_head_fwd": (_I, [_I, _P, _L, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _F, _P]),
+    "vm_head_fwd": (_I, [_I, _P, _L, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _F, _P]),
     "vm_reduce_rows": (_I, [_P, _I, _I, _P, _P]),
+    "vm_label_counts": (_I, [_P, _P, _L, _I, _P, _P]),
     "vm_head_bwd": (_I, [_I, _P, _L, _P, _P, _P, _P, _P, _L, _P, _I, _I, _I, _I, _I, _I, _F, _F, _F, _I, _F, _I, _P]),
     "vm_sgd_momentum": (_I, [_P, _P, _P, _P, _I, _L, _P, _F, _F, _P]),
-    # SURVEY §8(b) names (csrc/abi.cu)
-    "vm_conv3d_fwd": (_I, [_P, _L, _P, _P, _P, _L, _I, _I, _I, _I, _I, _I, _U, _P]),
+    # SURVEY §8(b) composites (csrc/abi.cu)
     "vm_conv3d_dgrad": (_I, [_P, _L, _P, _P, _L, _P, _L, _I, _I, _I, _I, _I, _I, _P]),
-    "vm_conv3d_wgrad_ws": (ctypes.c_size_t, [_I, _I, _I, _I, _I, _I]),
-    "vm_conv3d_wgrad": (_I, [_P, _L, _P, _L, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
-    "vm_relu_bwd": (_I, [_I, _P, _L, _P, _L, _P, _L, _I, _I, _I, _I, _I, _P]),
-    "vm_upsample2_concat_fwd": (_I, [_I, _P, _L, _P, _L, _I, _I, _I, _I, _I, _P]),
-    "vm_head_softmax_stats": (_I, [_I, _P, _L, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _F, _P]),
-    "vm_loss_grad_head_bwd": (_I, [_I, _P, _L, _P, _P, _P, _P, _P, _L, _P, _I, _I, _I, _I, _I, _I, _F, _F, _F, _I,
-                                   _F, _I, _P]),
 }
 
 # entry points declared in include/vm_api.h (the ABI test checks each is exported)

@@ -266,8 +266,10 @@ template <typename T>
 __global__ void __launch_bounds__(kHeadThreads) k_head_fwd(const T* __restrict__ y, Slab sy,
                                                            const float* __restrict__ W,
                                                            const float* __restrict__ bias,
-                                                           const float* __restrict__ onehot,
+                                                           const uint8_t* __restrict__ labels,
+                                                           int* __restrict__ label_err,
                                                            float* __restrict__ probs,
+                                                           uint8_t* __restrict__ pred,
                                                            float* __restrict__ partials, int B,
                                                            int C, int ncls, float clamp) {
   extern __shared__ float sh[];
@@ -287,8 +289,14 @@ __global__ void __launch_bounds__(kHeadThreads) k_head_fwd(const T* __restrict__
     float lg[kMaxCls], p[kMaxCls];
     head_logits(y, sy, b, d, h, w, sW, sb, C, ncls, lg);
     softmax_n(lg, ncls, p);
+    if (labels[v] >= ncls) atomicOr(label_err, 1);
+    if (pred) {  // np.argmax: the first maximal class
+      int a = 0;
+      for (int k = 1; k < ncls; ++k) a = p[k] > p[a] ? k : a;
+      pred[v] = (uint8_t)a;
+    }
     for (int k = 0; k < ncls; ++k) {
-      float g = onehot[v * ncls + k];
+      const float g = labels[v] == k ? 1.f : 0.f;
       if (probs) probs[v * ncls + k] = p[k];
       st[k] += p[k] * g;
       st[ncls + k] += p[k];
@@ -305,7 +313,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_head_fwd(const T* __restrict__
 template <typename T>
 __global__ void __launch_bounds__(kHeadThreads) k_head_bwd(
     const T* __restrict__ y, Slab sy, const float* __restrict__ W, const float* __restrict__ bias,
-    const float* __restrict__ onehot, const float* __restrict__ stats, T* __restrict__ g, Slab sg,
+    const uint8_t* __restrict__ labels, const float* __restrict__ stats, T* __restrict__ g, Slab sg,
     float* __restrict__ wpart, int B, int C, int ncls, float w_dice, float w_ce, float total,
     int dice_mask, float clamp, int relu_mask) {
   extern __shared__ float sh[];
@@ -347,7 +355,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_head_bwd(
       softmax_n(lg, ncls, p);
       float dot = 0.f;
       for (int k = 0; k < ncls; ++k) {
-        float gk = onehot[v * ncls + k];
+        const float gk = labels[v] == k ? 1.f : 0.f;
         float r = coef[3 * k + 2] != 0.f ? coef[3 * k] * (2.f * gk - coef[3 * k + 1]) : 0.f;
         float pm = fmaxf(p[k], clamp);
         r += p[k] >= clamp ? ce_scale * (gk / pm) : 0.f;  // training.py:125-126
@@ -391,8 +399,8 @@ __global__ void __launch_bounds__(kHeadThreads) k_head_bwd(
 template <typename T, int C, int NC>
 __global__ void __launch_bounds__(kHeadThreads, 2) k_head_fwd_fixed(
     const T* __restrict__ y, Slab sy, const float* __restrict__ W, const float* __restrict__ bias,
-    const float* __restrict__ onehot, float* __restrict__ probs, float* __restrict__ partials, int B,
-    float clamp) {
+    const uint8_t* __restrict__ labels, int* __restrict__ label_err, float* __restrict__ probs,
+    uint8_t* __restrict__ pred, float* __restrict__ partials, int B, float clamp) {
   pdl_wait();
   pdl_trigger();
   __shared__ float sW[C * NC], sb[NC], red[kHeadThreads / 32];
@@ -430,7 +438,10 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_fwd_fixed(
           for (int k = 0; k < NC; ++k) lgu[u][k] = fmaf(t8[j], sW[(cg * 8 + j) * NC + k], lgu[u][k]);
       }
 #pragma unroll
-      for (int k = 0; k < NC; ++k) gk[u][k] = ok[u] ? onehot[v * NC + k] : 0.f;
+      const uint32_t lab = ok[u] ? labels[v] : 0u;
+      if (lab >= (uint32_t)NC) atomicOr(label_err, 1);  // training.py:68-69 (np.eye indexing) raises
+#pragma unroll
+      for (int k = 0; k < NC; ++k) gk[u][k] = lab == (uint32_t)k ? 1.f : 0.f;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -458,6 +469,12 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_fwd_fixed(
         st[2 * NC + k] += g;
         st[3 * NC] += -__logf(fmaxf(p[k], clamp)) * g;
       }
+      if (pred) {  // np.argmax of these probabilities: the first maximal class
+        int a = 0;
+#pragma unroll
+        for (int k = 1; k < NC; ++k) a = p[k] > p[a] ? k : a;
+        pred[v] = (uint8_t)a;
+      }
     }
   }
 #pragma unroll
@@ -470,7 +487,7 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_fwd_fixed(
 template <typename T, int C, int NC>
 __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_fixed(
     const T* __restrict__ y, Slab sy, const float* __restrict__ W, const float* __restrict__ bias,
-    const float* __restrict__ onehot, const float* __restrict__ stats, T* __restrict__ g, Slab sg,
+    const uint8_t* __restrict__ labels, const float* __restrict__ stats, T* __restrict__ g, Slab sg,
     float* __restrict__ wpart, int B, float w_dice, float w_ce, float total, int dice_mask, float clamp,
     int relu_mask) {
   __shared__ float sW[C * NC], sb[NC], red[kHeadThreads / 32], coef[3 * NC];
@@ -526,7 +543,7 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_fixed(
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
       p[k] = p[k] / ssum;
-      const float gk = onehot[v * NC + k];
+      const float gk = labels[v] == k ? 1.f : 0.f;
       float r = coef[3 * k + 2] != 0.f ? coef[3 * k] * (2.f * gk - coef[3 * k + 1]) : 0.f;
       r += p[k] >= clamp ? ce_scale * (gk / fmaxf(p[k], clamp)) : 0.f;  // training.py:125-126
       gp[k] = r;
@@ -571,7 +588,7 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_fixed(
 template <typename T, int C, int NC>
 __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_grp(
     const T* __restrict__ y, Slab sy, const float* __restrict__ W, const float* __restrict__ bias,
-    const float* __restrict__ onehot, const float* __restrict__ stats, T* __restrict__ g, Slab sg,
+    const uint8_t* __restrict__ labels, const float* __restrict__ stats, T* __restrict__ g, Slab sg,
     float* __restrict__ wpart, int B, float w_dice, float w_ce, float total, int dice_mask, float clamp,
     int relu_mask) {
   pdl_wait();
@@ -624,7 +641,7 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_grp(
       V8<T>::ld(y + sy.at(b, cg, d, h, w), yv[u]);
       go[u] = sg.at(b, cg, d, h, w);
 #pragma unroll
-      for (int k = 0; k < NC; ++k) gk[u][k] = onehot[(size_t)v * NC + k];
+      for (int k = 0; k < NC; ++k) gk[u][k] = labels[v] == k ? 1.f : 0.f;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -898,9 +915,9 @@ extern "C" int vm_head_partials_count(int B, int D, int H, int W) {
 }
 
 extern "C" int vm_head_fwd(int dtype, const void* y, int64_t y_bstride, const float* w,
-                           const float* b, const float* onehot, float* probs, float* partials,
-                           int B, int C, int ncls, int D, int H, int W, float clamp, void* stream) {
-  VM_REQUIRE(y && w && b && onehot && partials, VM_E_ARG, "vm_head_fwd: null pointer");
+                           const float* b, const uint8_t* labels, int* label_err, float* probs,
+                           uint8_t* pred, float* partials, int B, int C, int ncls, int D, int H, int W, float clamp, void* stream) {
+  VM_REQUIRE(y && w && b && labels && label_err && partials, VM_E_ARG, "vm_head_fwd: null pointer");
   VM_REQUIRE(ncls > 0 && ncls <= kMaxCls, VM_E_UNSUPPORTED, "vm_head_fwd: ncls %d > %d", ncls, kMaxCls);
   VM_REQUIRE((int64_t)B * D * H * W < (1LL << 32), VM_E_SHAPE, "vm_head_fwd: voxel count exceeds 2^32");
   Slab sy = SLAB(y_bstride, C, D, H, W);
@@ -911,8 +928,8 @@ extern "C" int vm_head_fwd(int dtype, const void* y, int64_t y_bstride, const fl
     auto st = as_stream(stream);
 #define HF_CASE(CC, NN)                                                                               \
   case NN * 1000 + CC:                                                                                \
-    launch_pdl(k_head_fwd_fixed<T, CC, NN>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, onehot, \
-               probs, partials, B, clamp);                                                            \
+    launch_pdl(k_head_fwd_fixed<T, CC, NN>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, labels, \
+               label_err, probs, pred, partials, B, clamp);                                                            \
     return launch_status("vm_head_fwd");
 #define HF_ROW(NN) HF_CASE(8, NN) HF_CASE(16, NN) HF_CASE(32, NN) HF_CASE(64, NN)
     switch (ncls * 1000 + C) {
@@ -927,8 +944,60 @@ extern "C" int vm_head_fwd(int dtype, const void* y, int64_t y_bstride, const fl
   }
   DISPATCH_T(dtype, "vm_head_fwd",
              k_head_fwd<T><<<grid, kHeadThreads, sh, as_stream(stream)>>>(
-                 (const T*)y, sy, w, b, onehot, probs, partials, B, C, ncls, clamp));
+                 (const T*)y, sy, w, b, labels, label_err, probs, pred, partials, B, C, ncls, clamp));
   return launch_status("vm_head_fwd");
+}
+
+// Hard-Dice counts of a prediction (training.py:166-194): per class k, |pred==k & gt==k|,
+// |pred==k|, |gt==k| as exact 64-bit integers (integer atomics: order-independent, so the
+// result is deterministic).  16 voxels per thread per iteration (one 16-byte load of each).
+__global__ void k_label_counts(const uint8_t* __restrict__ pred, const uint8_t* __restrict__ gt, int64_t n,
+                               int ncls, unsigned long long* __restrict__ counts) {
+  __shared__ unsigned int sc[3 * kMaxCls];
+  for (int i = threadIdx.x; i < 3 * ncls; i += blockDim.x) sc[i] = 0u;
+  __syncthreads();
+  unsigned int loc[3 * kMaxCls];
+#pragma unroll
+  for (int i = 0; i < 3 * kMaxCls; ++i) loc[i] = 0u;
+  const int64_t n16 = n / 16;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  auto tally = [&](uint32_t p, uint32_t g) {
+#pragma unroll
+    for (int k = 0; k < kMaxCls; ++k) {
+      loc[k] += (p == (uint32_t)k) & (g == (uint32_t)k);
+      loc[kMaxCls + k] += p == (uint32_t)k;
+      loc[2 * kMaxCls + k] += g == (uint32_t)k;
+    }
+  };
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n16; q += stride) {
+    const uint4 pv = reinterpret_cast<const uint4*>(pred)[q];
+    const uint4 gv = reinterpret_cast<const uint4*>(gt)[q];
+    const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w}, gw[4] = {gv.x, gv.y, gv.z, gv.w};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) tally((pw[j / 4] >> (8 * (j % 4))) & 0xFFu, (gw[j / 4] >> (8 * (j % 4))) & 0xFFu);
+  }
+  for (int64_t i = n16 * 16 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) tally(pred[i], gt[i]);
+  for (int k = 0; k < ncls; ++k) {
+    atomicAdd(&sc[k], loc[k]);
+    atomicAdd(&sc[ncls + k], loc[kMaxCls + k]);
+    atomicAdd(&sc[2 * ncls + k], loc[2 * kMaxCls + k]);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 3 * ncls; i += blockDim.x) atomicAdd(&counts[i], (unsigned long long)sc[i]);
+}
+
+extern "C" int vm_label_counts(const uint8_t* pred, const uint8_t* gt, int64_t n, int ncls,
+                               unsigned long long* counts, void* stream) {
+  VM_REQUIRE(pred && gt && counts && n >= 0 && ncls > 0 && ncls <= kMaxCls, VM_E_ARG, "vm_label_counts: bad argument");
+  VM_REQUIRE(((reinterpret_cast<uintptr_t>(pred) | reinterpret_cast<uintptr_t>(gt)) & 15) == 0, VM_E_ARG,
+             "vm_label_counts: pred / gt must be 16-byte aligned");
+  cudaStream_t st = as_stream(stream);
+  cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * 3 * ncls, st);
+  if (n == 0) return launch_status("vm_label_counts");
+  const int64_t blocks = (n / 16 + 255) / 256;
+  k_label_counts<<<(int)(blocks < 1 ? 1 : (blocks > 2 * 148 ? 2 * 148 : blocks)), 256, 0, st>>>(pred, gt, n, ncls,
+                                                                                                counts);
+  return launch_status("vm_label_counts");
 }
 
 extern "C" int vm_reduce_rows(const float* partials, int rows, int width, float* out, void* stream) {
@@ -938,11 +1007,11 @@ extern "C" int vm_reduce_rows(const float* partials, int rows, int width, float*
 }
 
 extern "C" int vm_head_bwd(int dtype, const void* y, int64_t y_bstride, const float* w,
-                           const float* b, const float* onehot, const float* stats, void* g,
+                           const float* b, const uint8_t* labels, const float* stats, void* g,
                            int64_t g_bstride, float* wpartials, int B, int C, int ncls, int D,
                            int H, int W, float w_dice, float w_ce, float total_voxels,
                            int dice_mask, float clamp, int relu_mask, void* stream) {
-  VM_REQUIRE(y && w && b && onehot && stats && g && wpartials, VM_E_ARG, "vm_head_bwd: null pointer");
+  VM_REQUIRE(y && w && b && labels && stats && g && wpartials, VM_E_ARG, "vm_head_bwd: null pointer");
   VM_REQUIRE(ncls > 0 && ncls <= kMaxCls, VM_E_UNSUPPORTED, "vm_head_bwd: ncls %d", ncls);
   VM_REQUIRE((int64_t)B * D * H * W < (1LL << 32), VM_E_SHAPE, "vm_head_bwd: voxel count exceeds 2^32");
   Slab sy = SLAB(y_bstride, C, D, H, W), sg = SLAB(g_bstride, C, D, H, W);
@@ -953,7 +1022,7 @@ extern "C" int vm_head_bwd(int dtype, const void* y, int64_t y_bstride, const fl
     auto st = as_stream(stream);
 #define HB_CASE(CC, NN)                                                                                  \
   case NN * 1000 + CC:                                                                                   \
-    launch_pdl(k_head_bwd_grp<T, CC, NN>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, onehot, stats, \
+    launch_pdl(k_head_bwd_grp<T, CC, NN>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, labels, stats, \
                (T*)g, sg, wpartials, B, w_dice, w_ce, total_voxels, dice_mask, clamp, relu_mask);          \
     return launch_status("vm_head_bwd");
 #define HB_ROW(NN) HB_CASE(8, NN) HB_CASE(16, NN) HB_CASE(32, NN) HB_CASE(64, NN) HB_CASE(128, NN)
@@ -969,7 +1038,7 @@ extern "C" int vm_head_bwd(int dtype, const void* y, int64_t y_bstride, const fl
   }
   DISPATCH_T(dtype, "vm_head_bwd",
              k_head_bwd<T><<<grid, kHeadThreads, sh, as_stream(stream)>>>(
-                 (const T*)y, sy, w, b, onehot, stats, (T*)g, sg, wpartials, B, C, ncls, w_dice,
+                 (const T*)y, sy, w, b, labels, stats, (T*)g, sg, wpartials, B, C, ncls, w_dice,
                  w_ce, total_voxels, dice_mask, clamp, relu_mask));
   return launch_status("vm_head_bwd");
 }

@@ -6,7 +6,7 @@ Same distribution and random-stream consumption as the reference generator
 ellipsoid (centre E/2 +- U(E/10), radii U(0.30, 0.40) E, +1.0, label 1),
 1-3 tumour spheres (radius U(E/16, E/8), centred on liver voxels, clipped to
 the liver, +1.5, label 2).  Draw order is identical, so records are bitwise the
-reference's (checked in tests/test_data.py).
+reference's (checked in tests/test_host_logic.py::test_synthetic_record_bitwise_reference).
 """
 
 from __future__ import annotations

@@ -8,7 +8,9 @@ with two transports behind it:
 
 ``threads``  (single process, the default when torch.distributed is not
              initialised): one worker thread per mesh rank, each with its own
-             CUDA stream on device ``rank % cuda.device_count()``.  Payloads are
+             CUDA stream, all on the current CUDA device unless ``devices=``
+             spreads them (payloads that arrive from another device are copied
+             to the receiver's device on its stream).  Payloads are
              device tensors handed over FIFO queues together with a CUDA event
              recorded on the sender's stream; the receiver's stream waits on it.
              This is how the multi-rank parity tests run on ONE GPU: every rank
@@ -218,9 +220,9 @@ class DeviceMesh:
             return torch.device(self._devices[rank % len(self._devices)])
         if not torch.cuda.is_available():
             return torch.device("cpu")
-        if getattr(self, "backend", "threads") == "spmd":
-            return torch.device("cuda", torch.cuda.current_device())
-        return torch.device("cuda", rank % torch.cuda.device_count())
+        # spmd: this process's device; threads: every rank on the current device (the
+        # single-GPU parity transport) unless devices= spreads them explicitly
+        return torch.device("cuda", torch.cuda.current_device())
 
     def context(self, rank):
         return self._contexts[rank]
@@ -352,8 +354,10 @@ class DeviceMesh:
         torch = _torch()
         ev = None
         if ctx.device.type == "cuda":
+            # recorded on the stream the payload was produced on (the rank's stream, or a
+            # comm stream the caller made current)
             ev = torch.cuda.Event()
-            ev.record(ctx.stream)
+            ev.record(torch.cuda.current_stream(ctx.device))
         self._chan(ctx.rank, dst).put((tag, payload, ev))
 
     def _take(self, ctx, src, tag, timeout=None):
@@ -361,9 +365,12 @@ class DeviceMesh:
         if got != tag:
             raise ProtocolError(f"{ctx.coord} expected tag {tag!r} from {self.coords[src]}, got {got!r}")
         if ev is not None and ctx.device.type == "cuda":
-            ctx.stream.wait_event(ev)
+            cur = _torch().cuda.current_stream(ctx.device)
+            cur.wait_event(ev)
             if hasattr(payload, "record_stream") and getattr(payload, "is_cuda", False):
-                payload.record_stream(ctx.stream)
+                payload.record_stream(cur)
+                if payload.device != ctx.device:  # a rank on another GPU: copy in on our stream
+                    payload = payload.to(ctx.device, non_blocking=True)
         return payload
 
     # ---- transport ------------------------------------------------------------------

@@ -117,6 +117,11 @@ class UNetStep:
         self.clamp = clamp
         self.keep_probs = False
         self.probs = None
+        self.keep_pred = False  # evaluation: u8 argmax class per voxel (training.py:355)
+        self.pred = None
+        # mesh axes the loss statistics are summed over: None = all (training.py:337); the
+        # evaluation's per-sample statistics use the spatial axes only (training.py:353-354)
+        self.stats_axes = None
         self.ncls = cfg.num_classes
         # local extents per spatial dim (x->D, y->H, z->W)
         layout, mesh = graph.layout, graph.mesh
@@ -278,7 +283,11 @@ class UNetStep:
         self.head_in = head.node.inputs[0]
         hD, hH, hW = head.D, head.H, head.W
         self.nvox = self.B * hD * hH * hW
-        self.onehot = torch.zeros(self.nvox * self.ncls, dtype=torch.float32, device=dev)
+        # u8 class labels (the one-hot of training.py:68-69 is never materialised: the head
+        # kernels compare the label, 1 B per voxel instead of 4*ncls) + a sticky error flag set
+        # by the head forward when a label is >= ncls (np.eye(ncls)[labels] raises)
+        self.labels = torch.zeros(self.nvox, dtype=torch.uint8, device=dev)
+        self.label_err = torch.zeros(1, dtype=torch.int32, device=dev)
         self.n_part = int(_lib.load().vm_head_partials_count(self.B, hD, hH, hW))
         self.partials = torch.zeros(self.n_part * (3 * self.ncls + 1), dtype=torch.float32, device=dev)
         self.stats = torch.zeros(3 * self.ncls + 1, dtype=torch.float32, device=dev)
@@ -421,14 +430,25 @@ class UNetStep:
                             _lib.i64arr(lo5), _lib.i64arr(ext5))
 
     # ------------------------------------------------------------------ inputs
-    def load_inputs(self, image, onehot):
-        """image: device f32 [B,D,H,W,Cin] (local block); onehot: device f32 [B,D,H,W,ncls]."""
+    def load_inputs(self, image, labels):
+        """image: device f32 [B,D,H,W,Cin] (local block); labels: device u8 [B,D,H,W] class
+        indices, or a one-hot f32 [B,D,H,W,ncls] (test convenience: its argmax is taken)."""
         x = self.x_in
+        self._check_shape(image, labels)
         if self.input_slab_needed:
             self._k("io", "image", 0, 0, "vm_dense_to_slab", _lib.ptr(image.contiguous()), _lib.VM_F32, x.p(),
                     self.dt, x.bstride, self.B, x.C, x.D, x.H, x.W, 1)
         self._compact_input(image.contiguous())
-        self.onehot.copy_(onehot.reshape(-1))
+        if labels.dtype != torch.uint8:
+            labels = labels.argmax(dim=-1).to(torch.uint8)
+        self.labels.copy_(labels.reshape(-1))
+
+    def _check_shape(self, image, labels):
+        x = self.x_in
+        want = (self.B, x.D, x.H, x.W)
+        if tuple(image.shape[:4]) != want or tuple(labels.shape[:4]) != want:
+            raise VoxmeshError(f"input block {tuple(image.shape)} / labels {tuple(labels.shape)} do not match the "
+                               f"step's local block {want} (batch, D, H, W)")
 
     def _compact_input(self, image):
         if self.x1 is not None:
@@ -446,6 +466,7 @@ class UNetStep:
     # stream while step k computes (a data loader's prefetch); each step still moves its own
     # input bytes and reads its loss back.
     def _stage_bufs(self, image_host, labels_host):
+        self._check_shape(image_host, labels_host)
         if getattr(self, "_stage", None) is None:
             self._stage = [(torch.empty(tuple(image_host.shape), dtype=torch.float32, device=self.device),
                             torch.empty(tuple(labels_host.shape), dtype=torch.uint8, device=self.device))
@@ -486,8 +507,7 @@ class UNetStep:
             self._k("io", "image", 0, 0, "vm_dense_to_slab", _lib.ptr(img), _lib.VM_F32, x.p(), self.dt,
                     x.bstride, self.B, x.C, x.D, x.H, x.W, 1)
         self._compact_input(img)
-        self._k("io", "onehot", 0, 0, "vm_onehot_u8", _lib.ptr(lab), _lib.ptr(self.onehot), self.nvox,
-                self.ncls)
+        self.labels.copy_(lab.reshape(-1), non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
         self._consumed[i] = ev
@@ -523,6 +543,7 @@ class UNetStep:
         if getattr(self, "_loss_host", None) is None:
             self._loss_host = [torch.empty(self.stats.numel(), dtype=self.stats.dtype).pin_memory()
                                for _ in range(2)]
+            self._err_host = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in range(2)]
         out, prev = [], None
         self.upload(*batches[0])
         for k in range(len(batches)):
@@ -532,19 +553,86 @@ class UNetStep:
                 replay()
             else:
                 self.step()
-            buf = self._loss_host[k % 2]
+            buf, err = self._loss_host[k % 2], self._err_host[k % 2]
             buf.copy_(self.stats, non_blocking=True)
+            err.copy_(self.label_err, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record()
             if k + 1 < len(batches):
                 self._stage_h2d(*batches[k + 1], on_copy_stream=True)
             if prev is not None:
                 prev[0].synchronize()
+                self._check_labels(int(prev[2][0]))
                 out.append(self._loss_from(prev[1].numpy()))
-            prev = (ev, buf)
+            prev = (ev, buf, err)
         prev[0].synchronize()
+        self._check_labels(int(prev[2][0]))
         out.append(self._loss_from(prev[1].numpy()))
         return out
+
+    # ------------------------------------------------------------------ public training loop
+    # training.train_loop drives these: the host batch goes into persistent pinned buffers
+    # (two slots), its H2D + slab kernels run on this rank's stream, the step replays a captured
+    # CUDA graph when the transport allows it (one rank, or NCCL through the C ABI), and the
+    # loss statistics come back by an async D2H that the caller collects one step later.
+    def capture(self):
+        """Capture step() as a CUDA graph (None when the transport cannot be captured: the
+        threads mesh exchanges through host queues).  Replays run on the current stream."""
+        if self.ctx is not None and self.ctx.mesh.worker_count > 1 and not self.graph_capturable():
+            return None
+        cur = torch.cuda.current_stream(self.device)
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(cur)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                self.step()
+        cur.wait_stream(s)
+        return g
+
+    def graph_capturable(self):
+        return False
+
+    def launch_host_step(self, image_np, labels_np, replay=None):
+        """Stage numpy host blocks -> pinned -> device, run one step, start the D2H of its
+        loss statistics; returns a handle for ``collect`` (no host sync)."""
+        if getattr(self, "_loop", None) is None:
+            self._loop = {"slot": 0, "pinned": [None, None], "ev": [None, None],
+                          "stats": [torch.empty(self.stats.numel(), dtype=torch.float32).pin_memory() for _ in range(2)],
+                          "err": [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in range(2)],
+                          "skip": [torch.zeros(len(self.layers), dtype=torch.int32).pin_memory() for _ in range(2)]}
+        lp = self._loop
+        i = lp["slot"]
+        lp["slot"] = 1 - i
+        if lp["ev"][i] is not None:
+            lp["ev"][i].synchronize()  # the step that last used slot i has finished (H2D + D2H)
+        if lp["pinned"][i] is None or tuple(lp["pinned"][i][0].shape) != tuple(image_np.shape):
+            lp["pinned"][i] = (torch.empty(tuple(image_np.shape), dtype=torch.float32).pin_memory(),
+                               torch.empty(tuple(labels_np.shape), dtype=torch.uint8).pin_memory())
+        img, lab = lp["pinned"][i]
+        np.copyto(img.numpy(), image_np, casting="same_kind")
+        np.copyto(lab.numpy(), labels_np, casting="unsafe")
+        self.upload(img, lab)
+        if replay is not None:
+            replay()
+        else:
+            self.step()
+        lp["stats"][i].copy_(self.stats, non_blocking=True)
+        lp["err"][i].copy_(self.label_err, non_blocking=True)
+        lp["skip"][i].copy_(self.skip_flags, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        lp["ev"][i] = ev
+        return i, ev
+
+    def collect(self, handle):
+        """(combined, dice, ce), skipped layer ids of a launched step (waits for it)."""
+        i, ev = handle
+        lp = self._loop
+        ev.synchronize()
+        self._check_labels(int(lp["err"][i][0]))
+        flags = lp["skip"][i].numpy()
+        return self._loss_from(lp["stats"][i].numpy()), [L.node.id for L, f in zip(self.layers, flags) if f]
 
     def _has_prefetch(self, image_host):
         return (getattr(self, "_pending", None) is not None and self._copied[self._pending] is not None
@@ -585,14 +673,17 @@ class UNetStep:
             if getattr(self, "probs", None) is None:
                 self.probs = torch.empty(self.nvox * self.ncls, dtype=torch.float32, device=self.device)
             probs = _lib.ptr(self.probs)
-        nb = 2.0 * self.nvox * h.cin + 4.0 * self.nvox * self.ncls
+        if self.keep_pred and self.pred is None:
+            self.pred = torch.empty(self.nvox, dtype=torch.uint8, device=self.device)
+        nb = 2.0 * self.nvox * h.cin + 1.0 * self.nvox
         self._k("head_fwd", "head", 2.0 * self.nvox * h.cin * self.ncls, nb, "vm_head_fwd", self.dt, y.p(), y.bstride,
-                _lib.ptr(h.w), _lib.ptr(h.b), _lib.ptr(self.onehot), probs, _lib.ptr(self.partials), self.B, h.cin,
+                _lib.ptr(h.w), _lib.ptr(h.b), _lib.ptr(self.labels), _lib.ptr(self.label_err), probs,
+                _lib.ptr(self.pred) if self.keep_pred else None, _lib.ptr(self.partials), self.B, h.cin,
                 self.ncls, h.D, h.H, h.W, self.clamp)
         self._k("reduce", "stats", 0, 0, "vm_reduce_rows", _lib.ptr(self.partials), self.n_part, 3 * self.ncls + 1,
                 _lib.ptr(self.stats))
-        if self.ctx is not None and self.ctx.mesh.worker_count > 1:
-            red = self.ctx.all_reduce_sum(self.stats, tag="loss-stats")
+        if self.ctx is not None and self.ctx.mesh.worker_count > 1 and self.stats_axes != ():
+            red = self.ctx.all_reduce_sum(self.stats, axes=self.stats_axes, tag="loss-stats")
             if red is not self.stats:
                 self.stats.copy_(red)
 
@@ -609,9 +700,9 @@ class UNetStep:
         last = self.graph.node(self.head_in)
         last_conv = last.inputs[0] if last.op == "relu" else last.id
         g = self.gpre[last_conv]
-        nb = 4.0 * self.nvox * h.cin + 4.0 * self.nvox * self.ncls
+        nb = 4.0 * self.nvox * h.cin + 1.0 * self.nvox
         self._k("head_bwd", "head", 4.0 * self.nvox * h.cin * self.ncls, nb, "vm_head_bwd", self.dt, y.p(),
-                y.bstride, _lib.ptr(h.w), _lib.ptr(h.b), _lib.ptr(self.onehot), _lib.ptr(self.stats), g.p(), g.bstride,
+                y.bstride, _lib.ptr(h.w), _lib.ptr(h.b), _lib.ptr(self.labels), _lib.ptr(self.stats), g.p(), g.bstride,
                 _lib.ptr(self.hpartials), self.B, h.cin, self.ncls, h.D, h.H, h.W, self.w_dice, self.w_ce,
                 self.total_voxels, self.dice_mask, self.clamp, 1)
         self._k("reduce", "head", 0, 0, "vm_reduce_rows", _lib.ptr(self.hpartials), self.n_part, self.hw_width,
@@ -770,7 +861,13 @@ class UNetStep:
     # ------------------------------------------------------------------ readout
     def loss(self):
         """(combined, dice, ce) from the reduced statistics (training.py:95-107)."""
+        self._check_labels(int(self.label_err.item()))
         return self._loss_from(self.stats.double().cpu().numpy())
+
+    def _check_labels(self, flag):
+        if flag:
+            raise VoxmeshError(f"label volume holds a class index >= num_classes ({self.ncls}): "
+                               "one_hot (training.py:68-69) would raise IndexError")
 
     def _loss_from(self, s):
         s = np.asarray(s, dtype=np.float64)

@@ -36,7 +36,7 @@ from pathlib import Path
 
 import numpy as np
 
-from .errors import VoxmeshError
+from .errors import ShardingError, VoxmeshError
 
 DICE_EPS = 1e-6
 
@@ -250,67 +250,109 @@ class BatchSource:
 
 
 # ---------------------------------------------------------------------------- placement
+def _batch_axis(graph):
+    return graph.layout.axis_for("batch") if graph.layout is not None else None
+
+
+def _spatial_axes(graph):
+    if graph.layout is None:
+        return []
+    return [a for a in (graph.layout.axis_for(d) for d in ("x", "y", "z")) if a is not None]
+
+
 def _blocks(graph, arr, spatial_from=1):
-    """Per-rank local blocks of a host array whose spatial dims start at ``spatial_from``
-    (the layout's x/y/z → mesh axes, sharding.py:123-143); batch sharding is not used by
-    the slab step, so every rank sees the whole batch of its spatial block."""
+    """Per-rank local blocks of a host array ``[B, X, Y, Z, ...]``: dim 0 split over the
+    layout's batch axis, the spatial dims (from ``spatial_from``) over theirs — the block
+    slices of sharding.local_slices (sharding.py:123-143)."""
     mesh, layout = graph.mesh, graph.layout
     out = []
     for coord in mesh.coords:
         sl = [slice(None)] * arr.ndim
-        for i, d in enumerate(("x", "y", "z")):
+        for i, d in enumerate(("batch", "x", "y", "z")):
             ax = layout.axis_for(d) if layout is not None else None
             if ax is None:
                 continue
-            n = arr.shape[spatial_from + i] // mesh.axis_size(ax)
+            dim = 0 if d == "batch" else spatial_from + i - 1
+            size = mesh.axis_size(ax)
+            if arr.shape[dim] % size:
+                raise ShardingError(f"dim {d!r} of extent {arr.shape[dim]} is not divisible by mesh axis "
+                                    f"{ax!r} of size {size}")
+            n = arr.shape[dim] // size
             c = coord[mesh.axis_index[ax]]
-            sl[spatial_from + i] = slice(c * n, (c + 1) * n)
+            sl[dim] = slice(c * n, (c + 1) * n)
         out.append(np.ascontiguousarray(arr[tuple(sl)]))
     return out
 
 
-def _make_steps(graph, params, cfg, batch):
+def _make_steps(graph, params, cfg, batch, key="vm_step", evaluation=False):
+    """One UNetStep per rank: the local batch is ``batch`` over the layout's batch axis; the
+    loss is normalised by the global batch (training.py:396-406).  ``evaluation``: batch of one
+    sample per batch coordinate, per-sample statistics summed over the spatial axes only and
+    normalised by one volume (training.py:346-355, :557-561), argmax predictions kept."""
     import torch
 
     from .step import UNetStep
 
-    if graph.layout is not None and graph.layout.axis_for("batch") is not None:
-        raise VoxmeshError("train_loop: batch-sharded layouts are not supported by the slab step")
+    mesh = graph.mesh
+    b_axis = _batch_axis(graph)
+    bdiv = mesh.axis_size(b_axis) if b_axis else 1
+    if batch % bdiv:
+        raise ShardingError(f"batch {batch} is not divisible by mesh axis {b_axis!r} of size {bdiv}")
     dtype = torch.bfloat16 if cfg.compute_dtype == "bf16" else torch.float32
     E = graph.config.input_extent
-    multi = graph.mesh.worker_count > 1
+    multi = mesh.worker_count > 1
+    spatial = _spatial_axes(graph)
 
     def make(ctx):
-        st = UNetStep(graph, params, batch=batch, ctx=ctx if multi else None, device=ctx.device, dtype=dtype,
+        st = UNetStep(graph, params, batch=batch // bdiv, ctx=ctx if multi else None, device=ctx.device, dtype=dtype,
                       lr=cfg.lr, momentum=cfg.momentum,
                       loss_weights=(cfg.loss_weights.dice, cfg.loss_weights.ce),
-                      dice_classes=tuple(cfg.dice_classes), clamp=cfg.prob_clamp, global_shape=(E, E, E))
-        ctx.store["vm_step"] = st
+                      dice_classes=tuple(cfg.dice_classes), clamp=cfg.prob_clamp, global_shape=(E, E, E),
+                      global_batch=1 if evaluation else batch)
+        if evaluation:
+            st.keep_pred = True
+            st.stats_axes = tuple(spatial)
+        ctx.store[key] = st
         return None
 
-    graph.mesh.run(make)
+    mesh.run(make)
 
 
-def _pinned(a):
-    import torch
-
-    return torch.from_numpy(a).pin_memory()
-
-
-def _host_step(ctx, img, lab):
-    st = ctx.store["vm_step"]
-    st.train_step_host(img, lab)
-    return st.loss(), st.skipped_layers()
+def _zero_moments(params):
+    return {n: {k: np.zeros_like(np.asarray(v)) for k, v in b.items()} for n, b in params.items()}
 
 
 def install_params(graph, params, moments=None):
-    """Put an externally built parameter store on every rank's step (training.py:536-540)."""
-    graph.mesh.run(lambda ctx: ctx.store["vm_step"].load_state(params, moments))
+    """Put an externally built parameter store on every rank (training.py:536-540): builds
+    the per-rank steps when none exist yet; ``moments=None`` resets momentum to zero."""
+    have = graph.mesh.run(lambda ctx: "vm_step" in ctx.store)[0]
+    if not have:
+        b_axis = _batch_axis(graph)
+        _make_steps(graph, params, TrainConfig(), graph.mesh.axis_size(b_axis) if b_axis else 1)
+    mom = moments if moments is not None else _zero_moments(params)
+    graph.mesh.run(lambda ctx: ctx.store["vm_step"].load_state(params, mom))
+    graph.mesh.run(lambda ctx: ctx.store.pop("vm_eval_step", None) and None)
 
 
 def _export_state(graph):
     return graph.mesh.run(lambda ctx: (ctx.store["vm_step"].param_dict(), ctx.store["vm_step"].moment_dict())
                           if ctx.rank == 0 else None)[0]
+
+
+def _launch(ctx, img, lab):
+    st = ctx.store["vm_step"]
+    return st.launch_host_step(img, lab, replay=ctx.store.get("vm_graph_replay"))
+
+
+def _collect(ctx, handle):
+    return ctx.store["vm_step"].collect(handle)
+
+
+def _capture(ctx):
+    g = ctx.store["vm_step"].capture()
+    ctx.store["vm_graph"] = g
+    ctx.store["vm_graph_replay"] = g.replay if g is not None else None
+    return g is not None
 
 
 def train_loop(graph, dataset, cfg, resume_from=None, run_echo=None):
@@ -350,27 +392,45 @@ def train_loop(graph, dataset, cfg, resume_from=None, run_echo=None):
 
     source = BatchSource(records, cfg.batch_size, cfg.seed, cfg.augment)
     state = TrainState(start, params, moments or {})
+    # step k+1's host batch is built while step k runs on the GPU; step k's loss is read one
+    # step behind (async D2H into pinned memory), so the loop never waits on a loss it does
+    # not need yet.  The step is a captured CUDA graph whenever the transport allows it.
+    pending = None
+
+    def finish(item):
+        step, t0, handles = item
+        (loss, dice, ce), skipped = mesh.run(_collect, per_worker=(handles,))[0]
+        wall_ms = (time.perf_counter() - t0) * 1e3
+        if skipped:
+            warnings.warn(f"step {step}: non-finite gradients, skipped layers {skipped}")
+        state.step = step + 1
+        state.history.append((step, loss, dice, ce, wall_ms))
+        if csv_f:
+            csv_f.write(f"{step},{loss:.8f},{dice:.8f},{ce:.8f},{cfg.lr},{wall_ms:.2f}\n")
+        if cfg.log_every and step % cfg.log_every == 0:
+            print(f"step {step:5d}  loss {loss:.6f}  dice {dice:.6f}  ce {ce:.6f}  ({wall_ms:.0f} ms)")
+        if cfg.checkpoint_every and out_dir and (step + 1) % cfg.checkpoint_every == 0:
+            p, m = _export_state(graph)
+            save_checkpoint(out_dir / "checkpoints" / f"step_{step + 1:06d}", step + 1, p, m,
+                            extra={"config_kv": graph.config.to_kv(), "seed": cfg.seed})
+
     try:
         for step in range(start, start + cfg.steps):
             img, lab = source.batch(step)
             t0 = time.perf_counter()
-            bi = [_pinned(b) for b in _blocks(graph, img)]
-            bl = [_pinned(b) for b in _blocks(graph, lab)]
-            res = mesh.run(_host_step, per_worker=(bi, bl))
-            (loss, dice, ce), skipped = res[0]
-            wall_ms = (time.perf_counter() - t0) * 1e3
-            if skipped:
-                warnings.warn(f"step {step}: non-finite gradients, skipped layers {skipped}")
-            state.step = step + 1
-            state.history.append((step, loss, dice, ce, wall_ms))
-            if csv_f:
-                csv_f.write(f"{step},{loss:.8f},{dice:.8f},{ce:.8f},{cfg.lr},{wall_ms:.2f}\n")
-            if cfg.log_every and step % cfg.log_every == 0:
-                print(f"step {step:5d}  loss {loss:.6f}  dice {dice:.6f}  ce {ce:.6f}  ({wall_ms:.0f} ms)")
-            if cfg.checkpoint_every and out_dir and (step + 1) % cfg.checkpoint_every == 0:
-                p, m = _export_state(graph)
-                save_checkpoint(out_dir / "checkpoints" / f"step_{step + 1:06d}", step + 1, p, m,
-                                extra={"config_kv": graph.config.to_kv(), "seed": cfg.seed})
+            cur = (step, t0, mesh.run(_launch, per_worker=(_blocks(graph, img), _blocks(graph, lab))))
+            if pending is not None:
+                finish(pending)
+                pending = None
+            ckpt = cfg.checkpoint_every and out_dir and (step + 1) % cfg.checkpoint_every == 0
+            if step == start or ckpt:  # a checkpoint must not see the next step's update
+                finish(cur)
+                if step == start:  # the first step ran eagerly; later ones replay its graph
+                    mesh.run(_capture)
+            else:
+                pending = cur
+        if pending is not None:
+            finish(pending)
     finally:
         if csv_f:
             csv_f.close()
@@ -381,48 +441,88 @@ def train_loop(graph, dataset, cfg, resume_from=None, run_echo=None):
     return state
 
 
-def evaluate(graph, dataset, cfg, params=None):
-    """Forward-only pass over records on the GPU; hard Dice per case / pooled and the mean
-    per-sample loss (training.py:543-602).  ``params`` defaults to the weights installed by
-    the last ``train_loop``/``install_params`` on this graph."""
+def _eval_chunk(ctx, img, lab):
+    """Forward of one sample block; per-sample loss statistics and hard-Dice counts summed
+    over the spatial axes (training.py:346-355).  Predictions stay on the GPU: the argmax is
+    written by the head kernel and counted against the labels by vm_label_counts."""
     import torch
 
+    from . import _lib
+
+    st = ctx.store["vm_eval_step"]
+    st.upload(torch.from_numpy(img), torch.from_numpy(lab))
+    st.forward()
+    counts = torch.zeros(3 * st.ncls, dtype=torch.int64, device=st.device)
+    _lib.call("vm_label_counts", _lib.ptr(st.pred), _lib.ptr(st.labels), st.nvox, st.ncls, _lib.ptr(counts),
+              _lib.stream_ptr())
+    if st.stats_axes:
+        counts = ctx.all_reduce_sum(counts, axes=list(st.stats_axes), tag="eval-counts")
+    st._check_labels(int(st.label_err.item()))
+    return st.stats.double().cpu().numpy(), counts.cpu().numpy()
+
+
+def _dice_from_counts(inter, a, b):
+    """hard_dice (training.py:166-175) from |A∩B|, |A|, |B|."""
+    if a + b == 0:
+        return 1.0
+    if a == 0 or b == 0:
+        return 0.0
+    return 2.0 * inter / (a + b)
+
+
+def evaluate(graph, dataset, cfg, params=None, cls=2):
+    """Forward-only pass over records on the GPU (training.py:543-602): records go in chunks
+    of the batch axis' width, a partial last chunk is padded by repeating its last record and
+    the padding is dropped; returns hard Dice of class ``cls`` per case and pooled, and the
+    mean per-sample loss.  ``params`` defaults to the weights of the last ``train_loop`` /
+    ``install_params`` on this graph."""
     records = dataset.load_split("val") if hasattr(dataset, "load_split") else list(dataset)
     if not records:
         raise VoxmeshError("empty evaluation set")
     mesh = graph.mesh
+    b_axis = _batch_axis(graph)
+    chunk = mesh.axis_size(b_axis) if b_axis else 1
     have = mesh.run(lambda ctx: "vm_step" in ctx.store)[0]
-    if not have or params is not None:
-        if params is None:
-            raise VoxmeshError("evaluate: no parameters installed on this graph")
-        _make_steps(graph, params, cfg, 1)
-    preds, gts, losses = [], [], []
-    for rec in records:
-        img, lab = _image_labels(rec)
-        img = np.asarray(img, dtype=np.float32)[None, ..., None]
-        lab = np.asarray(lab, dtype=np.uint8)[None]
-        bi = [_pinned(b) for b in _blocks(graph, img)]
-        bl = [_pinned(b) for b in _blocks(graph, lab)]
-
-        def fwd(ctx, i, l):
-            st = ctx.store["vm_step"]
-            st.keep_probs = True
-            st.upload(i, l)
-            st.forward()
-            p = st.probs.reshape(i.shape[1], i.shape[2], i.shape[3], -1)
-            pred = torch.argmax(p, dim=-1).to(torch.uint8).cpu().numpy()
-            return pred, st.loss()[0]
-
-        res = mesh.run(fwd, per_worker=(bi, bl))
-        full = np.zeros(lab.shape[1:], dtype=np.uint8)
-        for (pred, _), blk in zip(res, _blocks(graph, np.arange(full.size).reshape(full.shape)[None])):
-            full.reshape(-1)[blk[0].reshape(-1)] = pred.reshape(-1)
-        preds.append(full)
-        gts.append(lab[0])
-        losses.append(res[0][1])
+    if params is None and not have:
+        raise VoxmeshError("evaluate: no parameters installed on this graph")
+    if mesh.run(lambda ctx: "vm_eval_step" in ctx.store)[0] is False:
+        _make_steps(graph, params if params is not None else _export_state(graph)[0], cfg, chunk,
+                    key="vm_eval_step", evaluation=True)
+    if params is not None:
+        mesh.run(lambda ctx: ctx.store["vm_eval_step"].load_state(params))
+    else:  # the training step's current weights
+        def sync(ctx):
+            ev = ctx.store["vm_eval_step"]
+            ev.params.copy_(ctx.store["vm_step"].params)
+            ev.repack()
+        mesh.run(sync)
+    ncls = graph.config.num_classes
+    E = graph.config.input_extent
+    dice_cases, losses = [], []
+    inter_t = a_t = b_t = 0
+    for i0 in range(0, len(records), chunk):
+        recs = records[i0 : i0 + chunk]
+        valid = len(recs)
+        while len(recs) < chunk:
+            recs.append(recs[-1])
+        pairs = [_image_labels(r) for r in recs]
+        img = np.stack([np.asarray(p[0], dtype=np.float32) for p in pairs])[..., None]
+        lab = np.stack([np.asarray(p[1], dtype=np.uint8) for p in pairs])
+        res = mesh.run(_eval_chunk, per_worker=(_blocks(graph, img), _blocks(graph, lab)))
+        by_sample = {}
+        for rank, coord in enumerate(mesh.coords):
+            bc = coord[mesh.axis_index[b_axis]] if b_axis else 0
+            by_sample.setdefault(bc, res[rank])
+        for j in range(valid):
+            stats, counts = by_sample[j]
+            inter, a, b = int(counts[cls]), int(counts[ncls + cls]), int(counts[2 * ncls + cls])
+            dice_cases.append(_dice_from_counts(inter, a, b))
+            inter_t, a_t, b_t = inter_t + inter, a_t + a, b_t + b
+            ds = soft_dice_from_stats(stats, ncls, tuple(cfg.dice_classes))
+            losses.append(cfg.loss_weights.dice * ds + cfg.loss_weights.ce * float(stats[3 * ncls]) / E ** 3)
     return {
-        "dice_per_case": dice_per_case(preds, gts),
-        "dice_global": dice_global(preds, gts),
+        "dice_per_case": float(np.mean(dice_cases)),
+        "dice_global": 1.0 if a_t + b_t == 0 else 2.0 * inter_t / (a_t + b_t),
         "mean_loss": float(sum(losses) / len(losses)),
-        "n_cases": len(preds),
+        "n_cases": len(dice_cases),
     }
