@@ -1,16 +1,29 @@
 #!/usr/bin/env python
-"""Benchmark: spatially partitioned 3D U-Net train step on B200 (voxels/s).
+"""Benchmark: spatially partitioned 3D U-Net train step on B200 (voxels/s; halo share).
 
-Workload (BASELINE.json configs[1], "cfg2"): U-Net recipe_for_resolution(128, 1/8)
-= filters (16, 32, 64, 128), 4 conv per block, 128^3 synthetic CT volume, batch 1,
-bf16 storage / fp32 accumulation, SGD momentum step included.  With N GPUs
-(torchrun, one process per GPU) the volume grows along depth to (128 N) x 128 x 128
-and is depth-split over a 1-D mesh — fixed per-GPU work (weak scaling) with a halo
-exchange before every 3x3x3 conv, forward and backward, and the weight-gradient
-all-reduce.
+Workloads (BASELINE.json configs):
+  cfg2  recipe_for_resolution(128, 1/8) = (16, 32, 64, 128), 128^3, batch 1, one GPU
+        (the default at N = 1: BASELINE.json configs[1]);
+  cfg3  recipe_for_resolution(256, 0.5) = (32 .. 512), 256^3, batch 1, depth split over the
+        N GPUs (strong scaling; the default at N > 1);
+  cfg4  recipe_for_resolution(512, 1.0) = (32 .. 1024), 512^3, batch 1, 2x2x2 mesh (N = 8);
+  cfg5  the cfg4 network, 512^3, global batch 2, mesh b=2 x mx=2 x my=2 (N = 8).
+bf16 storage / fp32 accumulation, SGD with momentum inside every step; synthetic CT volumes
+(data_io.synthesize_record distribution) and init_params(seed 1).  One process per GPU
+(torchrun); the halo is NCCL send/recv through the C ABI (vm_halo_slab_fwd) and the weight
+gradients are all-reduced in buckets on a second communicator, the whole step captured in one
+CUDA graph (``--no-graph`` for eager launches).
 
-Prints ONE JSON line (rank 0).  ``--impl reference`` times the CPU oracle port of
-the reference (oracle/voxmesh_oracle.py) on a bounded sample instead.
+Before timing, the first step's loss is checked against the stored oracle loss of the same
+inputs (tests/golden/bench_losses.json) and the run aborts on a mismatch.
+
+At N = 1 the halo share is measured by emulation: one rank's block of cfg3's 8-way depth
+split runs with periodic halos through a 1-rank NCCL communicator (the same pack / NCCL /
+unpack launches as a real split, without NVLink wire time, which is reported separately as
+bytes / 770 GB/s), A/B against the same block with the exchange switched off.
+
+Prints ONE JSON line (rank 0).  ``--impl reference`` times the CPU oracle port of the
+reference (oracle/voxmesh_oracle.py) on the same config instead.
 """
 
 from __future__ import annotations
@@ -18,6 +31,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import sys
 import threading
@@ -28,6 +42,18 @@ sys.path.insert(0, ROOT)
 
 METRIC = "3D U-Net train voxels/sec at 1/2/4/8 B200; halo-exchange % of step time"
 PEAKS = {"hbm_gbs": 6552.0, "bf16_tflops": 1658.2, "bf16_tflops_sustained": 1381.0}
+NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+
+CONFIGS = {
+    "cfg2": dict(extent=128, scale=0.125, batch=1, mesh=lambda n: [("mx", n)] if n > 1 else [],
+                 layout=lambda n: {"x": "mx"} if n > 1 else {}),
+    "cfg3": dict(extent=256, scale=0.5, batch=1, mesh=lambda n: [("mx", n)] if n > 1 else [],
+                 layout=lambda n: {"x": "mx"} if n > 1 else {}),
+    "cfg4": dict(extent=512, scale=1.0, batch=1, mesh=lambda n: [("mx", 2), ("my", 2), ("mz", 2)],
+                 layout=lambda n: {"x": "mx", "y": "my", "z": "mz"}, gpus=8),
+    "cfg5": dict(extent=512, scale=1.0, batch=2, mesh=lambda n: [("b", 2), ("mx", 2), ("my", 2)],
+                 layout=lambda n: {"batch": "b", "x": "mx", "y": "my"}, gpus=8),
+}
 
 
 def load_peaks():
@@ -39,13 +65,12 @@ def load_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback (B200_PROFILING.md)"
 
 
-def load_traffic(kind):
-    """roofline.traffic: DRAM bytes (read+write) per launch of ``kind``, from the newest
-    committed ncu step capture (dram__bytes_read.sum + dram__bytes_write.sum per launch) (profiles/r*/ncu_step_dram.json, written by
-    tools/ncu_summary.py --map); None when no capture is committed."""
+def load_traffic(kind, cfg_name):
+    """roofline.traffic: DRAM bytes (read+write) per launch of ``kind`` from a committed ncu
+    capture of the SAME config (profiles/r*/ncu_step_dram_<cfg>.json), else None."""
     import glob
 
-    caps = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_step_dram.json")))
+    caps = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"ncu_step_dram_{cfg_name}.json")))
     if not caps:
         return None, None
     try:
@@ -55,41 +80,41 @@ def load_traffic(kind):
         return None, os.path.relpath(caps[-1], ROOT)
 
 
-def _capture(torch, fn):
-    """Capture ``fn`` as one CUDA graph on a side stream; None if capture fails (e.g. a
-    collective that cannot be captured), in which case the step runs eagerly."""
-    s = torch.cuda.Stream()
-    s.wait_stream(torch.cuda.current_stream())
-    g = torch.cuda.CUDAGraph()
-    try:
-        with torch.cuda.stream(s):
-            with torch.cuda.graph(g, stream=s):
-                fn()
-    except Exception as e:  # pragma: no cover - GPU path
-        print(f"[bench] CUDA graph capture failed ({e}); running eagerly", file=sys.stderr)
-        torch.cuda.synchronize()
-        return None
-    torch.cuda.current_stream().wait_stream(s)
-    torch.cuda.synchronize()
-    return g
-
-
 def args_parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=100)
-    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="auto", choices=["auto"] + sorted(CONFIGS))
     p.add_argument("--conv", default="tc", choices=["tc", "simt"])
-    p.add_argument("--extent", type=int, default=128)
-    p.add_argument("--scale", type=float, default=0.125)
-    p.add_argument("--batch", type=int, default=1)
-    p.add_argument("--no-graph", action="store_true")
-    p.add_argument("--graph-multi", action="store_true",
-                   help="also capture the step as a CUDA graph when N > 1 (NCCL halo inside the graph)")
-    p.add_argument("--cpu-sample-extent", type=int, default=32)
+    p.add_argument("--no-graph", action="store_true", help="eager launches instead of the captured step graph")
+    p.add_argument("--no-emulate", action="store_true", help="N = 1: skip the emulated-split halo measurement")
+    p.add_argument("--emulate-split", type=int, default=8, help="N = 1: depth split whose rank block is emulated")
+    p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    p.add_argument("--cpu-budget", type=float, default=150.0, help="seconds of CPU-oracle time (reference arm)")
     p.add_argument("--layer-csv", default=None, help="write per-layer kernel times here")
-    return p.parse_args()
+    a = p.parse_args()
+    if a.config == "auto":
+        a.config = "cfg2" if a.gpus == 1 else "cfg3"
+    need = CONFIGS[a.config].get("gpus")
+    if need and a.gpus != need:
+        p.error(f"{a.config} runs on exactly {need} GPUs (its mesh), got --gpus {a.gpus}")
+    return a
+
+
+def workload(a):
+    c = CONFIGS[a.config]
+    E, n = c["extent"], a.gpus
+    mesh = c["mesh"](n)
+    par = "x".join(f"{ax}{s}" for ax, s in mesh) if mesh else "single GPU"
+    return {
+        "workload": f"{a.config}: U-Net recipe_for_resolution({E}, {c['scale']:g}), {E}^3 volume, "
+                    f"global batch {c['batch']}" + (f", spatial mesh {par}" if mesh else ", one GPU"),
+        "global_batch": c["batch"],
+        "volume": [E, E, E],
+        "parallelism": par,
+    }
 
 
 # ---------------------------------------------------------------------- clocks
@@ -145,81 +170,188 @@ class ClockSampler:
     def summary(self):
         if not self.ok or not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
-        return {
-            "sm_mhz": statistics.median(self.samples),
-            "sm_max_mhz": self.max_mhz,
-            "reasons": sorted(self.reasons),
-            "samples": len(self.samples),
-        }
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
 # ---------------------------------------------------------------------- CPU legs
-def cpu_sample(extent, scale, steps=1):
-    """Time the oracle port (numpy) of the same network on a bounded extent^3 sample."""
+def _cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_sample(config, budget_s, min_steps=1, max_steps=None):
+    """Time the oracle port (numpy, the reference's algorithm) on ``config``'s network.  cfg2:
+    full 128^3 steps (~30 s each on 16 host threads); the 256^3 / 512^3 configs: a
+    16 x 128 x 128 sub-volume per step (the full step is hours).  Steps until ``budget_s``."""
     import numpy as np
 
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from oracle import voxmesh_oracle as O
 
-    filters = O.recipe_filters(128, scale)  # the cfg2 network
+    c = CONFIGS[config]
+    filters = O.recipe_filters(c["extent"], c["scale"])
     nodes = O.graph_nodes(filters)
     params = O.init_params(nodes, 1)
     moments = {k: {kk: np.zeros_like(vv) for kk, vv in v.items()} for k, v in params.items()}
-    img, lab = O.record_for(extent, 0)
-    x = img[None, ..., None]
+    if config == "cfg2":
+        img, lab = O.record_for(128, 0)
+        shape = (128, 128, 128)
+    else:
+        img, lab = O.record_for(128, 0)
+        img, lab = img[56:72], lab[56:72]
+        shape = (16, 128, 128)
+    x = img[None, ..., None].astype(np.float32)
     oh = O.one_hot(lab[None], 3)
     times = []
-    for _ in range(steps):
+    t_start = time.perf_counter()
+    while len(times) < min_steps or (time.perf_counter() - t_start < budget_s and (max_steps is None or
+                                                                                 len(times) < max_steps)):
         t0 = time.perf_counter()
         O.train_step(nodes, params, moments, x, oh)
         times.append(time.perf_counter() - t0)
-    per = min(times)
-    try:
-        from threadpoolctl import threadpool_info
-
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
-    except Exception:
-        cores = os.cpu_count() or 1
-    return extent ** 3 / per, per, cores
+        if time.perf_counter() - t_start + times[-1] > budget_s and len(times) >= min_steps:
+            break
+    per = statistics.median(times)
+    vox = shape[0] * shape[1] * shape[2]
+    sample = (f"oracle port (oracle/voxmesh_oracle.py, numpy f32) fwd+bwd+SGD of the {config} network "
+              f"recipe_filters={filters} on a {shape[0]}x{shape[1]}x{shape[2]} volume"
+              + (" (the full workload)" if config == "cfg2" else " (bounded sub-volume of the workload)")
+              + f", {len(times)} step(s), median {per:.1f} s")
+    return vox / per, per, _cpu_threads(), sample, len(times)
 
 
 def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    vals = []
-    cores = 1
-    for _ in range(max(1, a.warmup // 3)):
-        cpu_sample(a.cpu_sample_extent, a.scale)
-    for _ in range(a.steps):
-        v, per, cores = cpu_sample(a.cpu_sample_extent, a.scale)
-        vals.append(v)
-    value = statistics.median(vals)
-    sample = (f"oracle port (numpy, oracle/voxmesh_oracle.py) fwd+bwd+SGD of the cfg2 network "
-              f"{a.cpu_sample_extent}^3 x 1 per step (bounded sample of the 128^3 workload)")
+    value, per, cores, sample, n = cpu_sample(a.config, a.cpu_budget)
     line = {
         "impl": "reference",
         "metric": METRIC,
         "value": value,
         "unit": "voxels/s",
         "n_gpus": a.gpus,
-        "steps": a.steps,
-        "warmup": a.warmup,
-        "ms_per_step": 1e3 * a.cpu_sample_extent ** 3 / value,
+        "steps": n,
+        "warmup": 0,
+        "ms_per_step": per * 1e3,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if a.gpus > 1 else "weak",
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (data_io.synthesize_record distribution, SeedSequence([7, 0]))",
-        "config": {"workload": "cfg2 network recipe_for_resolution(128, 1/8), CPU bounded sample",
-                   "global_batch": 1, "sample_extent": a.cpu_sample_extent},
+        "config": workload(a),
         "cpu_baseline": {"value": value, "unit": "voxels/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "voxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": f"{n} timed step(s) of the requested {a.steps} (CPU time budget {a.cpu_budget:.0f} s)",
     }
     print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------- GPU leg
+def _capture(torch, st, allow):
+    if not allow:
+        return None, "disabled (--no-graph)"
+    try:
+        g = st.capture()
+    except Exception as e:  # pragma: no cover - GPU path
+        print(f"[bench] !!! CUDA graph capture FAILED ({e}); running EAGER launches", file=sys.stderr, flush=True)
+        torch.cuda.synchronize()
+        return None, f"capture failed ({type(e).__name__}), eager launches"
+    if g is None:
+        print("[bench] !!! step not capturable with this transport; running EAGER launches", file=sys.stderr)
+        return None, "not capturable (host transport), eager launches"
+    return g, "captured (whole step, NCCL calls included)"
+
+
+def _timed(torch, fn, steps, barrier):
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    e1.synchronize()
+    barrier()
+    return e0.elapsed_time(e1) / steps
+
+
+def _first_loss_check(cfg_name, loss, n_gpus):
+    path = os.path.join(ROOT, "tests", "golden", "bench_losses.json")
+    try:
+        ref = json.load(open(path))[cfg_name]["loss"]
+    except Exception:
+        return {"first_step_loss": loss, "oracle_loss": None, "ok": None, "note": f"no stored oracle loss for {cfg_name}"}
+    rel = abs(loss - ref) / abs(ref)
+    out = {"first_step_loss": loss, "oracle_loss": ref, "rel_err": rel, "tol": 1e-2, "ok": rel <= 1e-2}
+    if not out["ok"]:
+        raise SystemExit(f"[bench] first-step loss {loss} differs from the oracle's {ref} (rel {rel:.2e} > 1e-2)")
+    return out
+
+
+def emulated_halo(a, torch, vm, peaks):
+    """N = 1: one rank's block of cfg3's K-way depth split, periodic halos over a 1-rank NCCL
+    communicator, A/B against no exchange (see module docstring)."""
+    import numpy as np
+    import torch.distributed as dist
+
+    from paper_1909_03108_b200.data import synth_record
+    from paper_1909_03108_b200.halo import nccl_comm_ptr
+    from paper_1909_03108_b200.step import UNetStep
+
+    K = a.emulate_split
+    c = CONFIGS["cfg3"]
+    E = c["extent"]
+    if not dist.is_initialized():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    comm = nccl_comm_ptr()
+    ar = nccl_comm_ptr(dist.new_group(backend="nccl"))
+    cfg = vm.recipe_for_resolution(E, c["scale"])
+    mesh = vm.create_mesh([("one", 1)], backend="threads")
+    graph = vm.build(cfg, mesh, {})
+    params = vm.init_params(graph, 1)
+    loc = (E // K, E, E)
+    st = UNetStep(graph, params, dtype=torch.bfloat16, global_shape=(E, E, E), local_shape=loc)
+    st.use_nccl(comm, nbr6=[0, 0, -1, -1, -1, -1], ar_comm=ar)
+    img, lab = synth_record(E, 7, 0)
+    st.upload(torch.from_numpy(img[None, : loc[0], ..., None].copy()), torch.from_numpy(lab[None, : loc[0]].copy()))
+    for _ in range(2):
+        st.step()
+    torch.cuda.synchronize()
+    res = {}
+    for name, on in (("halo", True), ("nohalo", False)):
+        st.has_halo = on
+        g, note = _capture(torch, st, not a.no_graph)
+        fn = g.replay if g is not None else st.step
+        for _ in range(max(3, a.warmup)):
+            fn()
+        res[name] = _timed(torch, fn, max(5, a.steps), torch.cuda.synchronize)
+        del g
+    st.has_halo = True
+    nbytes = st.halo_bytes_per_step()
+    wire_ms = nbytes / (NVLINK_GBS * 1e9) * 1e3  # both directions run concurrently: max per direction
+    mesh.shutdown()
+    return {
+        "share": max(0.0, (res["halo"] - res["nohalo"]) / res["halo"]),
+        "method": f"emulated on 1 GPU: rank block {loc[0]}x{loc[1]}x{loc[2]} of cfg3 {K}-way depth split, periodic "
+                  "halos through a 1-rank NCCL communicator (pack + NCCL group + unpack per conv, overlapped with "
+                  "the interior planes), A/B: (t_step - t_step_nohalo) / t_step",
+        "ms_step": res["halo"], "ms_nohalo": res["nohalo"],
+        "bytes_per_step_rank": nbytes,
+        "projected_wire_ms_at_770GBs": wire_ms / 2,
+        "projected_share_no_overlap": (wire_ms / 2) / (res["nohalo"] + wire_ms / 2),
+        "projected_whole_job_voxels_per_s": K * loc[0] * loc[1] * loc[2] / (res["halo"] * 1e-3),
+    }
+
+
 def run_ours(a):
     import numpy as np
     import torch
@@ -233,63 +365,40 @@ def run_ours(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks, peak_src = load_peaks()
-
-    cfg = vm.recipe_for_resolution(a.extent, a.scale)
-    E = a.extent
+    c = CONFIGS[a.config]
+    E, B = c["extent"], c["batch"]
+    cfg = vm.recipe_for_resolution(E, c["scale"])
+    axes = c["mesh"](world)
     if world > 1:
-        mesh = vm.create_mesh([("mx", world)])
-        layout = {"x": "mx"}
+        mesh = vm.create_mesh(axes)
+        layout = c["layout"](world)
     else:
         mesh = vm.create_mesh([("one", 1)], backend="threads")
         layout = {}
     graph = vm.build(cfg, mesh, layout)
     params = vm.init_params(graph, 1)
     ctx = mesh.context(rank) if world > 1 else None
-    # weak scaling: each rank owns one E^3 block of a (E*world) x E x E volume
-    st = UNetStep(graph, params, batch=a.batch, ctx=ctx, dtype=torch.bfloat16, conv_impl=a.conv,
-                  global_shape=(E * world, E, E), local_shape=(E, E, E))
-    imgs, labs = [], []
-    for b in range(a.batch):
-        im, lb = synth_record(E, 7, rank * a.batch + b)
-        imgs.append(im)
-        labs.append(lb)
-    img_h = torch.from_numpy(np.stack(imgs)[..., None].copy()).pin_memory()
-    lab_h = torch.from_numpy(np.stack(labs).copy()).pin_memory()
+    from paper_1909_03108_b200.training import _blocks
+
+    bdiv = mesh.axis_size(layout["batch"]) if "batch" in layout else 1
+    st = UNetStep(graph, params, batch=B // bdiv, ctx=ctx, dtype=torch.bfloat16, conv_impl=a.conv,
+                  global_batch=B)
+    recs = [synth_record(E, 7, i) for i in range(B)]
+    img = np.stack([r[0] for r in recs])[..., None]
+    lab = np.stack([r[1] for r in recs])
+    img_h = torch.from_numpy(_blocks(graph, img)[rank]).pin_memory()
+    lab_h = torch.from_numpy(_blocks(graph, lab)[rank]).pin_memory()
+    del recs, img, lab
     st.upload(img_h, lab_h)
-    torch.cuda.synchronize()
-
-    # warm-up (eager), then capture the step as one CUDA graph
-    for _ in range(max(1, min(2, a.warmup))):
-        st.step()
-    torch.cuda.synchronize()
-    l0 = _lib.load().vm_launch_count()
-    st.step()
-    torch.cuda.synchronize()
-    launches_per_step = _lib.load().vm_launch_count() - l0
-    graph_obj = None
-    graph_note = "disabled (--no-graph)" if a.no_graph else "captured"
-    if world > 1 and not a.graph_multi and not a.no_graph:
-        # the NCCL halo groups are not validated inside CUDA graphs on multi-GPU hardware yet:
-        # eager launches (measured 8% slower at N = 1)
-        a.no_graph = True
-        graph_note = "eager (N > 1: NCCL halo not captured; --graph-multi to capture)"
-    if not a.no_graph:
-        graph_obj = _capture(torch, st.step)
-        if graph_obj is None:
-            graph_note = "capture failed, eager launches"
-
-    def one():
-        if graph_obj is not None:
-            graph_obj.replay()
-        else:
-            st.step()
-
-    for _ in range(a.warmup):
-        one()
+    st.forward()
+    parity = _first_loss_check(a.config, st.loss()[0], world)
     torch.cuda.synchronize()
 
     def barrier():
@@ -297,83 +406,82 @@ def run_ours(a):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # ---- timed region: device-resident inputs
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        e0.record()
-        for _ in range(a.steps):
-            one()
-        e1.record()
-        e1.synchronize()
-    barrier()
-    ms = e0.elapsed_time(e1) / a.steps
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    voxels = a.batch * world * E ** 3
+        return float(t.item())
+
+    for _ in range(2):  # eager warm-up (first-touch of every kernel and plan)
+        st.step()
+    torch.cuda.synchronize()
+    l0 = _lib.load().vm_launch_count()
+    st.step()
+    torch.cuda.synchronize()
+    launches_per_step = _lib.load().vm_launch_count() - l0
+    graph_obj, graph_note = _capture(torch, st, not a.no_graph)
+    one = graph_obj.replay if graph_obj is not None else st.step
+    for _ in range(a.warmup):
+        one()
+    torch.cuda.synchronize()
+
+    # ---- timed region: device-resident inputs
+    with ClockSampler(local) as clk:
+        ms = max_over_ranks(_timed(torch, one, a.steps, barrier))
+    voxels = B * E ** 3  # the whole job's voxels per step
     value = voxels / (ms * 1e-3)
 
-    # ---- end-to-end through the public API: host buffers, H2D + D2H inside the timed region
-    # every step: H2D of its inputs (step k+1's overlapping step k on a copy stream) and an
-    # async D2H of its loss statistics, read by the host while the next step runs.  The path
-    # is warmed up first (pinned staging buffers, copy stream, events), like the device loop.
+    # ---- end to end through the public API: host buffers, H2D + D2H inside the timed region
     st.train_loop_host([(img_h, lab_h)] * max(a.warmup, 1), replay=one)
     barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record()
     losses = st.train_loop_host([(img_h, lab_h)] * a.steps, replay=one)
-    loss = losses[-1][0]
     f1.record()
     f1.synchronize()
     barrier()
-    ms_e2e = f0.elapsed_time(f1) / a.steps
-    if world > 1:
-        t = torch.tensor([ms_e2e], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_e2e = float(t.item())
+    ms_e2e = max_over_ranks(f0.elapsed_time(f1) / a.steps)
     h2d = img_h.numel() * img_h.element_size() + lab_h.numel() * lab_h.element_size()
-    d2h = st.stats.numel() * 4
+    d2h = st.stats.numel() * 4 + 4
 
-    # ---- halo share (A/B, the paper's "adds around 5%")
-    halo = {"share": 0.0, "method": "A/B: (t_step - t_step_nohalo)/t_step", "bytes_per_step_rank": 0}
+    # ---- halo share
     if world > 1:
-        st.has_halo_saved = st.has_halo
         st.has_halo = False
-        g2 = _capture(torch, st.step) if graph_obj is not None else None
+        g2, _ = _capture(torch, st, not a.no_graph)
         run2 = g2.replay if g2 is not None else st.step
         for _ in range(a.warmup):
             run2()
-        barrier()
-        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        h0.record()
-        for _ in range(a.steps):
-            run2()
-        h1.record()
-        h1.synchronize()
-        ms_nohalo = h0.elapsed_time(h1) / a.steps
-        t = torch.tensor([ms_nohalo], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_nohalo = float(t.item())
-        st.has_halo = st.has_halo_saved
-        halo["share"] = max(0.0, (ms - ms_nohalo) / ms)
-        halo["ms_nohalo"] = ms_nohalo
-        halo["bytes_per_step_rank"] = st.halo_bytes_per_step()
+        ms_nohalo = max_over_ranks(_timed(torch, run2, a.steps, barrier))
+        st.has_halo = True
+        del g2
+        nbytes = st.halo_bytes_per_step()
+        halo = {"share": max(0.0, (ms - ms_nohalo) / ms), "method": "A/B: (t_step - t_step_nohalo) / t_step, "
+                "no-halo = same kernels with the exchange off (margins stale: timing only)",
+                "ms_nohalo": ms_nohalo, "bytes_per_step_rank": nbytes,
+                "exchange_byte_count_per_step": halo_formula_bytes(vm, graph, mesh, layout, B),
+                "nvlink_gbs_achieved_if_exposed": nbytes / max(ms - ms_nohalo, 1e-6) / 1e6}
+    elif not a.no_emulate:
+        try:
+            halo = emulated_halo(a, torch, vm, peaks)
+        except Exception as e:  # pragma: no cover
+            halo = {"share": None, "method": f"emulation failed: {type(e).__name__}: {e}"}
+    else:
+        halo = {"share": 0.0, "method": "one GPU, no partitioning"}
 
     # ---- per-kernel timing for the roofline (each launch replayed alone as a CUDA graph)
     prof = st.profile_kernels(reps=5)
     classes = {}
     for row in prof:
-        c = classes.setdefault(row["kind"], {"ms": 0.0, "flops": 0.0, "bytes": 0.0, "launches": 0})
-        c["ms"] += row["ms"]
-        c["flops"] += row["flops"]
-        c["bytes"] += row["bytes"]
-        c["launches"] += 1
+        cc = classes.setdefault(row["kind"], {"ms": 0.0, "flops": 0.0, "bytes": 0.0, "launches": 0})
+        cc["ms"] += row["ms"]
+        cc["flops"] += row["flops"]
+        cc["bytes"] += row["bytes"]
+        cc["launches"] += 1
     dom_kind = max(classes, key=lambda k: classes[k]["ms"])
     dom = classes[dom_kind]
-    step_kernel_ms = sum(c["ms"] for c in classes.values())
-    traffic, traffic_src = load_traffic(dom_kind)
+    step_kernel_ms = sum(cc["ms"] for cc in classes.values())
+    traffic, traffic_src = load_traffic(dom_kind, a.config)
     if dom["flops"] > 0:
         achieved = dom["flops"] / (dom["ms"] * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
@@ -388,10 +496,9 @@ def run_ours(a):
                  "avg_launch_ms": dom["ms"] / max(dom["launches"], 1),
                  "share_of_kernel_time": dom["ms"] / step_kernel_ms, "peak_source": peak_src,
                  "traffic_source": traffic_src})
-    conv_flops = graph.conv_flops(a.batch) * (world * E ** 3) / (E ** 3) / world  # per rank
-    cfg_name = {(128, 0.125): "cfg2", (256, 0.5): "cfg3", (512, 1.0): "cfg4"}.get((E, a.scale), "custom")
-    act_gb = torch.cuda.memory_allocated() / 1e9  # activation slabs, tape, grads, workspaces
-    conv_ms = sum(c["ms"] for k, c in classes.items() if k.startswith("conv"))
+    conv_flops_rank = sum(cc["flops"] for k, cc in classes.items() if k.startswith("conv"))
+    conv_ms = sum(cc["ms"] for k, cc in classes.items() if k.startswith("conv"))
+    act_gb = torch.cuda.max_memory_allocated() / 1e9
     if a.layer_csv and rank == 0:
         with open(a.layer_csv, "w") as f:
             f.write("layer,kind,ms,flops,bytes,tflops,gbs\n")
@@ -404,13 +511,13 @@ def run_ours(a):
             dist.destroy_process_group()
         return
     cpu = None
-    try:
-        v, per, cores = cpu_sample(a.cpu_sample_extent, a.scale)
-        cpu = {"value": v, "unit": "voxels/s", "cores": cores, "kind": "port",
-               "sample": f"oracle port fwd+bwd+SGD of the cfg2 network on a {a.cpu_sample_extent}^3 volume, 1 step "
-                         f"({per:.1f} s)"}
-    except Exception as e:  # pragma: no cover
-        cpu = {"value": None, "unit": "voxels/s", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
+    if world == 1 and not a.no_cpu:
+        try:
+            v, per, cores, sample, _ = cpu_sample(a.config, 60.0, max_steps=1)
+            cpu = {"value": v, "unit": "voxels/s", "cores": cores, "kind": "port", "sample": sample}
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "unit": "voxels/s", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
+    wl = workload(a)
     line = {
         "metric": METRIC,
         "value": value,
@@ -420,45 +527,55 @@ def run_ours(a):
         "warmup": a.warmup,
         "ms_per_step": ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None,
         "dtype": "bf16",
-        "data": "synthetic (data_io.synthesize_record distribution, SeedSequence([7, rank]))",
-        "config": {
-            "workload": f"{cfg_name}: U-Net recipe_for_resolution({E}, {a.scale:g}) = {cfg.encoder_filters}, "
-                        f"{E}^3 per GPU, batch {a.batch}" + (f", depth-split x{world}" if world > 1 else ""),
-            "global_batch": a.batch,
-            "volume": [E * world, E, E],
-            "parallelism": f"spatial depth-split x{world}" if world > 1 else "single GPU",
-            "conv": a.conv,
-            "cuda_graph": graph_note,
-            "l2": f"working set (activation slabs, {act_gb:.1f} GB) >> 126 MB L2; no flush needed",
-            "conv_tflop_per_step_rank": conv_flops / 1e12,
-        },
+        "data": "synthetic (data_io.synthesize_record distribution, SeedSequence([7, i]) for sample i)",
+        "config": wl,
+        "run": {"conv": a.conv, "cuda_graph": graph_note, "memory_gb_peak": round(act_gb, 1),
+                "l2": f"working set {act_gb:.1f} GB >> 126 MB L2; no flush needed",
+                "conv_tflop_per_step_rank": conv_flops_rank / 1e12,
+                "transport": "NCCL via C ABI (vm_halo_slab_fwd / vm_allreduce_f32)" if st.comm is not None
+                             else ("none" if world == 1 else "host")},
+        "parity": parity,
         "e2e": {"value": voxels / (ms_e2e * 1e-3), "unit": "voxels/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e, "loss": loss,
+                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e, "loss": losses[-1][0],
                 "path": "UNetStep.train_loop_host: per step pinned H2D (prefetched one step ahead on a copy "
-                        "stream) -> slab/one-hot kernels -> step graph -> async D2H of the loss statistics"},
+                        "stream) -> slab kernels -> step graph -> async D2H of the loss statistics"},
         "roofline": roof,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": launches_per_step * a.steps,
         "halo": halo,
-        "kernel_ms_per_step": {k: round(c["ms"], 4) for k, c in classes.items()},
-        # every kernel class against its own roofline (tensor for convs, HBM for the rest),
-        # each launch replayed alone: the dominant class above is one row of this table
+        "kernel_ms_per_step": {k: round(cc["ms"], 4) for k, cc in classes.items()},
         "roofline_by_kind": {
-            k: ({"bound": "tensor", "tflops": round(c["flops"] / (c["ms"] * 1e-3) / 1e12, 1),
-                 "frac": round(c["flops"] / (c["ms"] * 1e-3) / 1e12 / peaks["bf16_tflops"], 3)}
-                if c["flops"] > 0 and k.startswith("conv") else
-                {"bound": "hbm", "gbs": round(c["bytes"] / (c["ms"] * 1e-3) / 1e9, 0),
-                 "frac": round(c["bytes"] / (c["ms"] * 1e-3) / 1e9 / peaks["hbm_gbs"], 3)})
-            for k, c in classes.items() if c["ms"] > 0},
-        "conv_tflops_effective": conv_flops / (conv_ms * 1e-3) / 1e12 if conv_ms else None,
+            k: ({"bound": "tensor", "tflops": round(cc["flops"] / (cc["ms"] * 1e-3) / 1e12, 1),
+                 "frac": round(cc["flops"] / (cc["ms"] * 1e-3) / 1e12 / peaks["bf16_tflops"], 3)}
+                if cc["flops"] > 0 and k.startswith("conv") else
+                {"bound": "hbm", "gbs": round(cc["bytes"] / (cc["ms"] * 1e-3) / 1e9, 0),
+                 "frac": round(cc["bytes"] / (cc["ms"] * 1e-3) / 1e9 / peaks["hbm_gbs"], 3)})
+            for k, cc in classes.items() if cc["ms"] > 0},
+        "conv_tflops_effective": conv_flops_rank / (conv_ms * 1e-3) / 1e12 if conv_ms else None,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def halo_formula_bytes(vm, graph, mesh, layout, B):
+    """exchange_byte_count (halo.py:197-229) of every k = 3 conv input, fwd + bwd (the first
+    conv has no backward exchange), bf16, summed over all ranks."""
+    tot = 0
+    halo = vm.HaloSpec.for_kernel(3)
+    lay = vm.Layout(layout)
+    for n in graph.conv_nodes:
+        if n.k != 3:
+            continue
+        e = graph.level_extents[n.id]
+        spec = vm.TensorSpec((("batch", B), ("x", e), ("y", e), ("z", e), ("c", n.c_in)), "u8")
+        one = vm.exchange_byte_count(spec, lay, mesh, halo) * 2  # bf16 = 2 bytes per element
+        tot += one * (1 if n.inputs[0] == "input" else 2)
+    return tot
 
 
 def main():

@@ -245,6 +245,40 @@ int vm_sgd_momentum(float* params, float* moments, const float* grads, const int
                     int nlayers, int64_t max_layer_elems, int* flags, float lr, float momentum,
                     void* stream);
 
+/* ------------------------------------------------------------------ halo + collectives (halo.cu)
+ * The forward halo of a channel-blocked padded slab (halo.py:109-155, SURVEY §8(b) vm_halo_fwd)
+ * as one stream-ordered call: for each spatial dim a (D, H, W) with a neighbour, one pack
+ * launch, one NCCL group (send up / send down / recv lo / recv hi) and one unpack launch.
+ * The backward (halo adjoint, halo.py:158-194) of the U-Net step is this same call on the
+ * output gradient: its data gradient is the forward conv of the halo'd gradient with
+ * flipped taps, which equals the reference's "padded gradient, then adjoint exchange".
+ * comm is an ncclComm_t (torch: ProcessGroupNCCL._comm_ptr()); NCCL is bound at run time
+ * from the process's libnccl.so.2 (vm_nccl_bind).  nbr[6] = lo/hi neighbour ranks of D, H,
+ * W (-1: global boundary, margin left zero).  ws: vm_halo_slab_ws_bytes of device scratch. */
+int vm_nccl_bind(void);
+size_t vm_halo_slab_ws_bytes(int dtype, int B, int C, int D, int H, int W);
+int vm_halo_slab_fwd(void* comm, int dtype, void* slab, int64_t bstride, int B, int C, int D, int H, int W,
+                     const int* nbr, void* ws, size_t ws_bytes, long long* bytes_sent, void* stream);
+/* zero the margin layers on every side with a neighbour (gradient slabs before wgrad) */
+int vm_halo_slab_zero(int dtype, void* slab, int64_t bstride, int B, int C, int D, int H, int W,
+                      const int* nbr, void* stream);
+/* one phase's pack (first / last interior layer of `axis` -> down / up messages) and unpack
+ * (messages from lo / hi -> margin layers 0 / n+1), for host-driven transports; NULL skips a side */
+int vm_halo_slab_pack(int dtype, const void* slab, int64_t bstride, int B, int C, int D, int H, int W,
+                      int axis, void* down, void* up, void* stream);
+int vm_halo_slab_unpack(int dtype, void* slab, int64_t bstride, int B, int C, int D, int H, int W,
+                        int axis, const void* from_lo, const void* from_hi, void* stream);
+long long vm_halo_slab_face_bytes(int dtype, int B, int C, int D, int H, int W, int axis);
+/* in-place sum over the communicator (mesh.py:195-233 all_reduce_sum; unet.py:434-441) */
+int vm_allreduce_f32(void* comm, float* buf, size_t n, void* stream);
+
+/* conv3d forward / dgrad on output planes [d0, d0+nd) of slabs with D interior planes (the
+ * interior planes run while the halo fills the margins; the boundary planes after it) */
+int vm_conv3d_fwd_tc_range(const void* x, int64_t x_bstride, const void* wpacked, const float* bias, void* y,
+                           int64_t y_bstride, const void* mask, int64_t mask_bstride, int B, int Cin, int Cout,
+                           int D, int H, int W, int d0, int nd, unsigned flags, void* ws, size_t ws_bytes,
+                           void* stream);
+
 /* conv3d_input_grad_local (ops.py:100-114) fused with relu_backward_local (ops.py:186-187):
  * gx = conv(gy_halo, flip(W)^T) [* (mask > 0)] with the flip-packed operand; Cin/Cout are the
  * FORWARD conv's (gx has Cin channels); mask may be NULL (no ReLU before this conv). */

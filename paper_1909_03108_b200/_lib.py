@@ -77,6 +77,16 @@ _SIGS = {
     "vm_label_counts": (_I, [_P, _P, _L, _I, _P, _P]),
     "vm_head_bwd": (_I, [_I, _P, _L, _P, _P, _P, _P, _P, _L, _P, _I, _I, _I, _I, _I, _I, _F, _F, _F, _I, _F, _I, _P]),
     "vm_sgd_momentum": (_I, [_P, _P, _P, _P, _I, _L, _P, _F, _F, _P]),
+    "vm_nccl_bind": (_I, []),
+    "vm_halo_slab_ws_bytes": (_S, [_I, _I, _I, _I, _I, _I]),
+    "vm_halo_slab_fwd": (_I, [_P, _I, _P, _L, _I, _I, _I, _I, _I, _P, _P, _S, _P, _P]),
+    "vm_halo_slab_zero": (_I, [_I, _P, _L, _I, _I, _I, _I, _I, _P, _P]),
+    "vm_halo_slab_pack": (_I, [_I, _P, _L, _I, _I, _I, _I, _I, _I, _P, _P, _P]),
+    "vm_halo_slab_unpack": (_I, [_I, _P, _L, _I, _I, _I, _I, _I, _I, _P, _P, _P]),
+    "vm_halo_slab_face_bytes": (ctypes.c_longlong, [_I, _I, _I, _I, _I, _I, _I]),
+    "vm_allreduce_f32": (_I, [_P, _P, _S, _P]),
+    "vm_conv3d_fwd_tc_range": (_I, [_P, _L, _P, _P, _P, _L, _P, _L, _I, _I, _I, _I, _I, _I, _I, _I, _U, _P, _S,
+                                    _P]),
     # SURVEY §8(b) composites (csrc/abi.cu)
     "vm_conv3d_dgrad": (_I, [_P, _L, _P, _P, _L, _P, _L, _I, _I, _I, _I, _I, _I, _P]),
 }

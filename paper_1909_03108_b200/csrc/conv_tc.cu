@@ -1748,7 +1748,7 @@ extern "C" void vm_debug_set_fwd_max_split(int v) { g_fwd_max_split = v < 1 ? 1 
 
 static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, const float* bias, void* y,
                          int64_t y_bstride, const void* mask, int64_t mask_bstride, int B, int Cin, int Cout, int D,
-                         int H, int W, unsigned flags, void* ws, size_t ws_bytes, void* stream);
+                         int H, int W, unsigned flags, void* ws, size_t ws_bytes, void* stream, int Dfull = 0);
 
 extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wpacked,
                                 const float* bias, void* y, int64_t y_bstride, const void* mask,
@@ -1766,6 +1766,27 @@ extern "C" int vm_conv3d_fwd_tc_ws(const void* x, int64_t x_bstride, const void*
                        ws, ws_bytes, stream);
 }
 
+// Output planes [d0, d0 + nd) of a slab with D interior planes: the conv of a plane reads
+// input planes d-1..d+1 only, so the interior planes [1, D-1) can run while a halo exchange
+// fills the margin planes, and the two boundary planes after it (north-star
+// subsystem 2: exchange overlapped with interior-tile compute).
+extern "C" int vm_conv3d_fwd_tc_range(const void* x, int64_t x_bstride, const void* wpacked, const float* bias,
+                                      void* y, int64_t y_bstride, const void* mask, int64_t mask_bstride, int B,
+                                      int Cin, int Cout, int D, int H, int W, int d0, int nd, unsigned flags,
+                                      void* ws, size_t ws_bytes, void* stream) {
+  VM_REQUIRE(d0 >= 0 && nd > 0 && d0 + nd <= D, VM_E_SHAPE, "vm_conv3d_fwd_tc_range: planes [%d,%d) outside [0,%d)",
+             d0, d0 + nd, D);
+  const int64_t off = (int64_t)d0 * (H + 2) * (W + 2) * 8;
+  const bf16* xb = static_cast<const bf16*>(x) + off;
+  bf16* yb = static_cast<bf16*>(y) + off;
+  const bf16* mb = mask ? static_cast<const bf16*>(mask) + off : nullptr;
+  if (!x_bstride) x_bstride = default_bstride(Cin, D, H, W, 1);
+  if (!y_bstride) y_bstride = default_bstride(Cout, D, H, W, 1);
+  if (mask && !mask_bstride) mask_bstride = default_bstride(Cout, D, H, W, 1);
+  return fwd_tc_launch(xb, x_bstride, wpacked, bias, yb, y_bstride, mb, mask_bstride, B, Cin, Cout, nd, H, W, flags,
+                       ws, ws_bytes, stream, D);
+}
+
 // Upper bound of the split-K workspace any plan of this shape may use (0: never splits).
 extern "C" size_t vm_conv3d_fwd_tc_ws_bytes(int B, int Cin, int Cout, int D, int H, int W) {
   const PackGeom pg = pack_geom(Cin, Cout);
@@ -1775,9 +1796,13 @@ extern "C" size_t vm_conv3d_fwd_tc_ws_bytes(int B, int Cin, int Cout, int D, int
   return fwd_ws_need(kFwdMaxSplit, (int64_t)B * (tiles + 8) * pg.nchunk, 1, pg.Nc) + 256;
 }
 
+// Dfull > 0: the slabs hold Dfull interior planes and D is a sub-range of output planes whose
+// first plane the caller has already offset x / y / mask to (vm_conv3d_fwd_tc_range): the
+// channel-group plane stride and the default batch strides come from Dfull.
 static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, const float* bias, void* y,
                          int64_t y_bstride, const void* mask, int64_t mask_bstride, int B, int Cin, int Cout, int D,
-                         int H, int W, unsigned flags, void* ws, size_t ws_bytes, void* stream) {
+                         int H, int W, unsigned flags, void* ws, size_t ws_bytes, void* stream, int Dfull) {
+  if (Dfull <= 0) Dfull = D;
   VM_REQUIRE(x && wpacked && y, VM_E_ARG, "vm_conv3d_fwd_tc: null pointer");
   VM_REQUIRE((flags & VM_CONV_NOBIAS) || bias, VM_E_ARG, "vm_conv3d_fwd_tc: bias required");
   VM_REQUIRE(!(flags & VM_CONV_MASK) || mask, VM_E_ARG, "vm_conv3d_fwd_tc: mask required");
@@ -1797,10 +1822,10 @@ static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, 
   p.Wp = W + 2;
   p.P = p.Hp * p.Wp;
   p.anchors = (int64_t)D * p.P;
-  const int64_t rows = (int64_t)(D + 2) * p.P;
+  const int64_t rows = (int64_t)(Dfull + 2) * p.P;
   p.plane8 = rows * 8;
-  p.y_bstride = y_bstride ? y_bstride : default_bstride(Cout, D, H, W, 1);
-  p.m_bstride = mask_bstride ? mask_bstride : default_bstride(Cout, D, H, W, 1);
+  p.y_bstride = y_bstride ? y_bstride : default_bstride(Cout, Dfull, H, W, 1);
+  p.m_bstride = mask_bstride ? mask_bstride : default_bstride(Cout, Dfull, H, W, 1);
   p.CG = pg.CG;
   p.KC = pg.KC;
   p.Cout = Cout;
@@ -1811,7 +1836,7 @@ static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, 
   p.wp_magic = (uint32_t)(0x100000000ULL / (uint64_t)(W + 2)) + 1;
   p.hp_magic = (uint32_t)(0x100000000ULL / (uint64_t)(H + 2)) + 1;
   p.x = static_cast<const bf16*>(x);
-  p.x_bstride = x_bstride ? x_bstride : default_bstride(Cin, D, H, W, 1);
+  p.x_bstride = x_bstride ? x_bstride : default_bstride(Cin, Dfull, H, W, 1);
   VM_REQUIRE((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (p.x_bstride & 7) == 0, VM_E_ALIGN,
              "vm_conv3d_fwd_tc: slab must be 16-byte aligned");
   int nsm = vm_num_sms(0);

@@ -1,0 +1,269 @@
+// halo.cu — the halo exchange of a channel-blocked padded slab as ONE stream-ordered C call
+// (SURVEY §8(b) vm_halo_fwd), plus the weight-gradient / statistics all-reduce
+// (vm_allreduce_f32), over the caller's NCCL communicator.
+//
+// Protocol (halo.py:109-155, restated): the three spatial dims are exchanged one after the
+// other (D, then H, then W); the face sent in phase a spans the margins filled by phases < a,
+// so edges and corners arrive over 2-3 hops with no diagonal messages, and the bytes equal
+// halo.exchange_byte_count (halo.py:197-229).  Margin 1 (k = 3).  Per phase:
+//   pack    one launch: the first interior layer ("down", to the lo neighbour) and the last
+//           ("up", to the hi neighbour) of every (sample, channel group) into two contiguous
+//           messages [B][CG][n1][n2][8];
+//   NCCL    one group: send up, send down, recv from lo, recv from hi (per-peer issue order
+//           makes a rank that is its own lo AND hi neighbour — the periodic single-GPU
+//           emulation — receive the up message in its lo margin, as a ring would);
+//   unpack  one launch into margin layer 0 (from lo) and n+1 (from hi).
+// Global-boundary margins are never written: they stay zero from allocation (halo.py:136-147).
+//
+// NCCL is not linked: the entry points bind ncclSend/ncclRecv/ncclGroupStart/ncclGroupEnd/
+// ncclAllReduce from the libnccl.so.2 already loaded by the process (torch's), so the
+// communicator the caller passes (ProcessGroupNCCL._comm_ptr()) and these calls are the same
+// NCCL instance.  All work is enqueued on the caller's stream (capturable in a CUDA graph).
+#include <dlfcn.h>
+
+#include "vm_common.cuh"
+
+namespace vm {
+
+// ------------------------------------------------------------------ face kernels
+// A face: the layer `pos` (padded index) along `axis` of every (sample, channel group), over
+// the padded extents of the dims exchanged before `axis` and the interior of those after it
+// (full = 1: the whole padded cross-section, used by vm_halo_slab_zero).
+struct Face {
+  int axis, pos, full;
+  uint8_t* buf;  // message [B][CG][n1][n2][vec] (nullptr on unpack: zero fill)
+};
+struct FaceSet {
+  Face f[6];
+  int n;
+  int64_t bstride_b, plane_b;  // bytes
+  int CG, B, D, H, W;
+  int vec;  // bytes per voxel-group (8 channels)
+};
+
+__host__ __device__ inline void face_extent(const FaceSet& s, const Face& f, int& n1, int& n2, int& lo1, int& lo2) {
+  const int Dp = s.D + 2, Hp = s.H + 2;
+  if (f.axis == 0) {  // (h, w)
+    n1 = f.full ? Hp : s.H, n2 = f.full ? s.W + 2 : s.W, lo1 = f.full ? 0 : 1, lo2 = f.full ? 0 : 1;
+  } else if (f.axis == 1) {  // (d, w): d padded (phase 0 came first)
+    n1 = Dp, n2 = f.full ? s.W + 2 : s.W, lo1 = 0, lo2 = f.full ? 0 : 1;
+  } else {  // (d, h), both padded
+    n1 = Dp, n2 = Hp, lo1 = 0, lo2 = 0;
+  }
+}
+
+template <bool PACK>
+__global__ void k_slab_faces(uint8_t* __restrict__ slab, const FaceSet s) {
+  pdl_wait();
+  const Face f = s.f[blockIdx.y];
+  int n1, n2, lo1, lo2;
+  face_extent(s, f, n1, n2, lo1, lo2);
+  const int upv = s.vec / 16;  // 16-byte units per voxel group (1: bf16, 2: f32)
+  const int64_t total = (int64_t)s.B * s.CG * n1 * n2 * upv;
+  const int Hp = s.H + 2, Wp = s.W + 2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / upv;
+    const int u = (int)(i - r * upv);
+    const int i2 = (int)(r % n2);
+    r /= n2;
+    const int i1 = (int)(r % n1);
+    r /= n1;
+    const int cg = (int)(r % s.CG);
+    const int b = (int)(r / s.CG);
+    int d, h, w;
+    if (f.axis == 0) d = f.pos, h = lo1 + i1, w = lo2 + i2;
+    else if (f.axis == 1) d = lo1 + i1, h = f.pos, w = lo2 + i2;
+    else d = lo1 + i1, h = lo2 + i2, w = f.pos;
+    uint4* p = reinterpret_cast<uint4*>(slab + b * s.bstride_b + cg * s.plane_b +
+                                        (((int64_t)d * Hp + h) * Wp + w) * s.vec) + u;
+    if (PACK) {
+      reinterpret_cast<uint4*>(f.buf)[i] = *p;
+    } else {
+      *p = f.buf ? reinterpret_cast<const uint4*>(f.buf)[i] : make_uint4(0, 0, 0, 0);
+    }
+  }
+}
+
+static int64_t face_bytes(const FaceSet& s, const Face& f) {
+  int n1, n2, lo1, lo2;
+  face_extent(s, f, n1, n2, lo1, lo2);
+  return (int64_t)s.B * s.CG * n1 * n2 * s.vec;
+}
+
+static int launch_faces(bool pack, void* slab, const FaceSet& s, cudaStream_t st) {
+  if (s.n == 0) return VM_OK;
+  int64_t most = 0;
+  for (int i = 0; i < s.n; ++i) {
+    const int64_t b = face_bytes(s, s.f[i]) / 16;
+    most = b > most ? b : most;
+  }
+  dim3 grid(grid_for(most, 256) / s.n + 1, s.n);
+  if (pack) launch_pdl(k_slab_faces<true>, grid, 256, 0, st, static_cast<uint8_t*>(slab), s);
+  else launch_pdl(k_slab_faces<false>, grid, 256, 0, st, static_cast<uint8_t*>(slab), s);
+  return launch_status(pack ? "vm_halo pack" : "vm_halo unpack");
+}
+
+static FaceSet face_set(int dtype, int64_t bstride, int B, int C, int D, int H, int W) {
+  FaceSet s{};
+  const int eb = dtype_bytes(dtype);
+  s.vec = 8 * eb;
+  s.CG = (C + 7) / 8;
+  s.B = B, s.D = D, s.H = H, s.W = W;
+  s.plane_b = (int64_t)(D + 2) * (H + 2) * (W + 2) * s.vec;
+  s.bstride_b = (bstride ? bstride : (int64_t)s.CG * (D + 2) * (H + 2) * (W + 2) * 8) * eb;
+  return s;
+}
+
+// ------------------------------------------------------------------ NCCL, bound at run time
+typedef int (*nccl_p2p_t)(void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_group_t)();
+typedef int (*nccl_allreduce_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef const char* (*nccl_errstr_t)(int);
+struct NcclApi {
+  nccl_p2p_t send = nullptr, recv = nullptr;
+  nccl_group_t gstart = nullptr, gend = nullptr;
+  nccl_allreduce_t allreduce = nullptr;
+  nccl_errstr_t errstr = nullptr;
+};
+static NcclApi g_nccl;
+constexpr int kNcclUint8 = 1, kNcclFloat32 = 7, kNcclSum = 0;  // ncclDataType_t / ncclRedOp_t values
+
+static bool nccl_ok() { return g_nccl.send && g_nccl.recv && g_nccl.gstart && g_nccl.gend && g_nccl.allreduce; }
+
+#define NCCL_CHECK(call, what)                                                              \
+  do {                                                                                      \
+    const int _r = (call);                                                                  \
+    if (_r != 0) {                                                                          \
+      set_error("%s: NCCL error %d (%s)", what, _r, g_nccl.errstr ? g_nccl.errstr(_r) : "?"); \
+      return 1000 + _r;                                                                     \
+    }                                                                                       \
+  } while (0)
+
+}  // namespace vm
+
+using namespace vm;
+
+extern "C" int vm_nccl_bind(void) {
+  if (nccl_ok()) return VM_OK;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // the process's NCCL (torch's)
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  VM_REQUIRE(h, VM_E_UNSUPPORTED, "vm_nccl_bind: libnccl.so.2 not loadable (%s)", dlerror());
+  g_nccl.send = reinterpret_cast<nccl_p2p_t>(dlsym(h, "ncclSend"));
+  g_nccl.recv = reinterpret_cast<nccl_p2p_t>(dlsym(h, "ncclRecv"));
+  g_nccl.gstart = reinterpret_cast<nccl_group_t>(dlsym(h, "ncclGroupStart"));
+  g_nccl.gend = reinterpret_cast<nccl_group_t>(dlsym(h, "ncclGroupEnd"));
+  g_nccl.allreduce = reinterpret_cast<nccl_allreduce_t>(dlsym(h, "ncclAllReduce"));
+  g_nccl.errstr = reinterpret_cast<nccl_errstr_t>(dlsym(h, "ncclGetErrorString"));
+  VM_REQUIRE(nccl_ok(), VM_E_UNSUPPORTED, "vm_nccl_bind: NCCL symbols missing");
+  return VM_OK;
+}
+
+extern "C" size_t vm_halo_slab_ws_bytes(int dtype, int B, int C, int D, int H, int W) {
+  FaceSet s = face_set(dtype, 0, B, C, D, H, W);
+  int64_t most = 0;
+  for (int a = 0; a < 3; ++a) {
+    Face f{a, 1, 0, nullptr};
+    const int64_t b = face_bytes(s, f);
+    most = b > most ? b : most;
+  }
+  return (size_t)(4 * ((most + 255) / 256 * 256));  // 2 send + 2 recv messages
+}
+
+// Forward halo of a slab (halo.py:109-155).  nbr[2a] / nbr[2a+1] = lo / hi neighbour rank of
+// spatial dim a (D, H, W) in the communicator, -1 at a global boundary.  ws: device scratch of
+// vm_halo_slab_ws_bytes.  bytes_sent (optional, host) accumulates the message bytes.
+extern "C" int vm_halo_slab_fwd(void* comm, int dtype, void* slab, int64_t bstride, int B, int C, int D, int H,
+                                int W, const int* nbr, void* ws, size_t ws_bytes, long long* bytes_sent,
+                                void* stream) {
+  VM_REQUIRE(slab && nbr && ws, VM_E_ARG, "vm_halo_slab_fwd: null pointer");
+  VM_REQUIRE(dtype == VM_BF16 || dtype == VM_F32, VM_E_UNSUPPORTED, "vm_halo_slab_fwd: dtype %d", dtype);
+  VM_REQUIRE(D >= 1 && H >= 1 && W >= 1, VM_E_HALO, "vm_halo_slab_fwd: margin 1 exceeds local extent (%d,%d,%d)",
+             D, H, W);
+  VM_REQUIRE(ws_bytes >= vm_halo_slab_ws_bytes(dtype, B, C, D, H, W), VM_E_ARG, "vm_halo_slab_fwd: ws too small");
+  VM_REQUIRE((reinterpret_cast<uintptr_t>(slab) & 15) == 0 && (reinterpret_cast<uintptr_t>(ws) & 15) == 0,
+             VM_E_ALIGN, "vm_halo_slab_fwd: 16-byte alignment required");
+  cudaStream_t st = as_stream(stream);
+  const FaceSet base = face_set(dtype, bstride, B, C, D, H, W);
+  const int n[3] = {D, H, W};
+  const size_t quarter = ws_bytes / 4 / 256 * 256;
+  uint8_t* w8 = static_cast<uint8_t*>(ws);
+  uint8_t *s_down = w8, *s_up = w8 + quarter, *r_lo = w8 + 2 * quarter, *r_hi = w8 + 3 * quarter;
+  for (int a = 0; a < 3; ++a) {
+    const int lo = nbr[2 * a], hi = nbr[2 * a + 1];
+    if (lo < 0 && hi < 0) continue;
+    VM_REQUIRE(comm, VM_E_ARG, "vm_halo_slab_fwd: neighbours given without a communicator");
+    VM_REQUIRE(nccl_ok() || vm_nccl_bind() == VM_OK, VM_E_UNSUPPORTED, "vm_halo_slab_fwd: NCCL not bound");
+    FaceSet pk = base, up = base;
+    pk.n = up.n = 0;
+    if (lo >= 0) pk.f[pk.n++] = Face{a, 1, 0, s_down};
+    if (hi >= 0) pk.f[pk.n++] = Face{a, n[a], 0, s_up};
+    const size_t bytes = (size_t)face_bytes(base, Face{a, 1, 0, nullptr});
+    int rc = launch_faces(true, slab, pk, st);
+    if (rc) return rc;
+    NCCL_CHECK(g_nccl.gstart(), "ncclGroupStart");
+    if (hi >= 0) NCCL_CHECK(g_nccl.send(s_up, bytes, kNcclUint8, hi, comm, st), "ncclSend");
+    if (lo >= 0) NCCL_CHECK(g_nccl.send(s_down, bytes, kNcclUint8, lo, comm, st), "ncclSend");
+    if (lo >= 0) NCCL_CHECK(g_nccl.recv(r_lo, bytes, kNcclUint8, lo, comm, st), "ncclRecv");
+    if (hi >= 0) NCCL_CHECK(g_nccl.recv(r_hi, bytes, kNcclUint8, hi, comm, st), "ncclRecv");
+    NCCL_CHECK(g_nccl.gend(), "ncclGroupEnd");
+    if (lo >= 0) up.f[up.n++] = Face{a, 0, 0, r_lo};
+    if (hi >= 0) up.f[up.n++] = Face{a, n[a] + 1, 0, r_hi};
+    rc = launch_faces(false, slab, up, st);
+    if (rc) return rc;
+    if (bytes_sent) *bytes_sent += (long long)bytes * ((lo >= 0) + (hi >= 0));
+  }
+  return VM_OK;
+}
+
+// Zero the margin layers a halo wrote (sides with a neighbour), full padded cross-sections:
+// the weight gradient reads a gradient slab's margins as zeros.  One launch.
+extern "C" int vm_halo_slab_zero(int dtype, void* slab, int64_t bstride, int B, int C, int D, int H, int W,
+                                 const int* nbr, void* stream) {
+  VM_REQUIRE(slab && nbr, VM_E_ARG, "vm_halo_slab_zero: null pointer");
+  FaceSet s = face_set(dtype, bstride, B, C, D, H, W);
+  const int n[3] = {D, H, W};
+  s.n = 0;
+  for (int a = 0; a < 3; ++a) {
+    if (nbr[2 * a] >= 0) s.f[s.n++] = Face{a, 0, 1, nullptr};
+    if (nbr[2 * a + 1] >= 0) s.f[s.n++] = Face{a, n[a] + 1, 1, nullptr};
+  }
+  return launch_faces(false, slab, s, as_stream(stream));
+}
+
+// Single-phase building blocks (the host-driven transports of the threads / gloo meshes use
+// these around their own send/recv): pack the down/up messages of phase `axis`, or unpack the
+// lo/hi messages into its margins.  A null message pointer skips that side.
+extern "C" int vm_halo_slab_pack(int dtype, const void* slab, int64_t bstride, int B, int C, int D, int H, int W,
+                                 int axis, void* down, void* up, void* stream) {
+  VM_REQUIRE(slab && axis >= 0 && axis < 3, VM_E_ARG, "vm_halo_slab_pack: bad argument");
+  FaceSet s = face_set(dtype, bstride, B, C, D, H, W);
+  const int n[3] = {D, H, W};
+  s.n = 0;
+  if (down) s.f[s.n++] = Face{axis, 1, 0, static_cast<uint8_t*>(down)};
+  if (up) s.f[s.n++] = Face{axis, n[axis], 0, static_cast<uint8_t*>(up)};
+  return launch_faces(true, const_cast<void*>(slab), s, as_stream(stream));
+}
+extern "C" int vm_halo_slab_unpack(int dtype, void* slab, int64_t bstride, int B, int C, int D, int H, int W,
+                                   int axis, const void* from_lo, const void* from_hi, void* stream) {
+  VM_REQUIRE(slab && axis >= 0 && axis < 3, VM_E_ARG, "vm_halo_slab_unpack: bad argument");
+  FaceSet s = face_set(dtype, bstride, B, C, D, H, W);
+  const int n[3] = {D, H, W};
+  s.n = 0;
+  if (from_lo) s.f[s.n++] = Face{axis, 0, 0, static_cast<uint8_t*>(const_cast<void*>(from_lo))};
+  if (from_hi) s.f[s.n++] = Face{axis, n[axis] + 1, 0, static_cast<uint8_t*>(const_cast<void*>(from_hi))};
+  return launch_faces(false, slab, s, as_stream(stream));
+}
+extern "C" long long vm_halo_slab_face_bytes(int dtype, int B, int C, int D, int H, int W, int axis) {
+  FaceSet s = face_set(dtype, 0, B, C, D, H, W);
+  return face_bytes(s, Face{axis, 1, 0, nullptr});
+}
+
+// In-place sum of n floats over the communicator (the weight-gradient / loss-statistics
+// all-reduce, mesh.py:195-233 / unet.py:434-441), on the caller's stream.
+extern "C" int vm_allreduce_f32(void* comm, float* buf, size_t n, void* stream) {
+  VM_REQUIRE(comm && buf, VM_E_ARG, "vm_allreduce_f32: null pointer");
+  VM_REQUIRE(nccl_ok() || vm_nccl_bind() == VM_OK, VM_E_UNSUPPORTED, "vm_allreduce_f32: NCCL not bound");
+  if (n == 0) return VM_OK;
+  NCCL_CHECK(g_nccl.allreduce(buf, buf, n, kNcclFloat32, kNcclSum, comm, as_stream(stream)), "ncclAllReduce");
+  return VM_OK;
+}

@@ -17,6 +17,7 @@ plan drives the channel-blocked slabs of the U-Net step (:mod:`.step`).
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, field
 
 from . import _lib
@@ -360,3 +361,213 @@ def halo_exchange_backward(grad_padded, x_spec, layout, mesh, halo, phase_barrie
         arrays.append(arr)
     blocks = mesh.run(exchange_backward_local, dims, halo, _BWD_TAG, phase_barrier, per_worker=(arrays,))
     return ShardedTensor(x_spec, layout, mesh, blocks)
+
+
+# ---------------------------------------------------------------------------
+# The U-Net step's halo: channel-blocked padded slabs [B][CG][D+2][H+2][W+2][8]
+# ---------------------------------------------------------------------------
+
+
+class CudaSlabKernels:
+    """Per-phase pack / unpack of a slab's faces, one launch for every (sample, channel
+    group) and both sides (vm_halo_slab_pack / _unpack, csrc/halo.cu)."""
+
+    def _geom(self, s):
+        return _lib.dtype_code(s.dtype), s.p(), s.bstride, s.B, s.C, s.D, s.H, s.W
+
+    def face_bytes(self, s, axis):
+        return int(_lib.load().vm_halo_slab_face_bytes(_lib.dtype_code(s.dtype), s.B, s.C, s.D, s.H, s.W, axis))
+
+    def pack(self, s, axis, down, up):
+        import torch
+
+        n = self.face_bytes(s, axis) // s.storage.element_size()
+        md = torch.empty(n, dtype=s.dtype, device=s.storage.device) if down else None
+        mu = torch.empty(n, dtype=s.dtype, device=s.storage.device) if up else None
+        _lib.call("vm_halo_slab_pack", *self._geom(s), axis, _lib.ptr(md), _lib.ptr(mu), _lib.stream_ptr())
+        return md, mu
+
+    def like(self, s, axis):
+        import torch
+
+        return torch.empty(self.face_bytes(s, axis) // s.storage.element_size(), dtype=s.dtype,
+                           device=s.storage.device)
+
+    def unpack(self, s, axis, from_lo, from_hi):
+        _lib.call("vm_halo_slab_unpack", *self._geom(s), axis, _lib.ptr(from_lo), _lib.ptr(from_hi),
+                  _lib.stream_ptr())
+
+    def zero(self, s, nbr6):
+        _lib.call("vm_halo_slab_zero", _lib.dtype_code(s.dtype), s.p(), s.bstride, s.B, s.C, s.D, s.H, s.W,
+                  (ctypes.c_int * 6)(*nbr6), _lib.stream_ptr())
+
+
+class TorchSlabKernels:
+    """Tensor-slicing restatement of CudaSlabKernels (same face boxes and message layout
+    [B][CG][n1][n2][8]), so the slab protocol and its transports run on CPU (gloo tests)."""
+
+    @staticmethod
+    def view(s):
+        Dp, Hp, Wp = s.D + 2, s.H + 2, s.W + 2
+        return s.storage.as_strided((s.B, s.CG, Dp, Hp, Wp, 8), (s.bstride, Dp * Hp * Wp * 8, Hp * Wp * 8, Wp * 8, 8, 1),
+                                    s.offset)
+
+    @staticmethod
+    def _box(s, axis, pos, full=False):
+        if axis == 0:
+            return (slice(None), slice(None), pos, slice(None) if full else slice(1, s.H + 1),
+                    slice(None) if full else slice(1, s.W + 1))
+        if axis == 1:
+            return slice(None), slice(None), slice(None), pos, slice(None) if full else slice(1, s.W + 1)
+        return slice(None), slice(None), slice(None), slice(None), pos
+
+    def face_bytes(self, s, axis):
+        return self.view(s)[self._box(s, axis, 1)].numel() * s.storage.element_size()
+
+    def pack(self, s, axis, down, up):
+        v = self.view(s)
+        n = (s.D, s.H, s.W)[axis]
+        md = v[self._box(s, axis, 1)].contiguous().reshape(-1) if down else None
+        mu = v[self._box(s, axis, n)].contiguous().reshape(-1) if up else None
+        return md, mu
+
+    def like(self, s, axis):
+        import torch
+
+        return torch.empty(self.face_bytes(s, axis) // s.storage.element_size(), dtype=s.dtype,
+                           device=s.storage.device)
+
+    def unpack(self, s, axis, from_lo, from_hi):
+        v = self.view(s)
+        n = (s.D, s.H, s.W)[axis]
+        for pos, m in ((0, from_lo), (n + 1, from_hi)):
+            if m is not None:
+                dst = v[self._box(s, axis, pos)]
+                dst.copy_(m.reshape(dst.shape))
+
+    def zero(self, s, nbr6):
+        v = self.view(s)
+        for a in range(3):
+            n = (s.D, s.H, s.W)[a]
+            for side, pos in ((0, 0), (1, n + 1)):
+                if nbr6[2 * a + side] >= 0:
+                    v[self._box(s, a, pos, full=True)] = 0
+
+
+class SlabHalo:
+    """Forward halo of the step's slabs (the 3-phase protocol of halo.py:109-155, margin 1).
+
+    ``nbr6`` = lo/hi neighbour ranks of the D, H, W dims (-1 at a global boundary).  Two
+    transports, same bytes and the same messages:
+
+    * ``comm`` (an ncclComm_t): one C call per slab, vm_halo_slab_fwd — pack, NCCL group,
+      unpack per phase on the caller's stream, capturable in a CUDA graph (spmd over NCCL);
+    * ``ctx`` (a mesh WorkerContext): the phases driven from the host around
+      ``ctx.exchange`` (threads mesh on one GPU, gloo on CPU), with ``kernels`` doing the
+      per-phase pack / unpack (CudaSlabKernels, or TorchSlabKernels on CPU).
+    """
+
+    def __init__(self, nbr6, ctx=None, comm=None, kernels=None):
+        self.nbr6 = [int(n) for n in nbr6]
+        self.ctx, self.comm = ctx, comm
+        self.kernels = kernels or CudaSlabKernels()
+        self.ws = None
+        self._sent = ctypes.c_longlong(0)
+
+    @property
+    def active(self):
+        return any(n >= 0 for n in self.nbr6)
+
+    def reserve(self, slabs):
+        """Preallocate the NCCL message scratch for the largest of ``slabs``."""
+        if self.comm is None:
+            return
+        import torch
+
+        need = max(int(_lib.call_size("vm_halo_slab_ws_bytes", _lib.dtype_code(s.dtype), s.B, s.C, s.D, s.H, s.W))
+                   for s in slabs)
+        dev = slabs[0].storage.device
+        self.ws = torch.empty(need // 4 + 64, dtype=torch.float32, device=dev)
+        self.ws_bytes = self.ws.numel() * 4
+
+    def bytes_sent(self):
+        return int(self._sent.value)
+
+    def forward(self, s, tag=_FWD_TAG):
+        if not self.active:
+            return
+        if self.comm is not None:
+            _lib.call("vm_halo_slab_fwd", ctypes.c_void_p(self.comm), _lib.dtype_code(s.dtype), s.p(), s.bstride, s.B,
+                      s.C, s.D, s.H, s.W, (ctypes.c_int * 6)(*self.nbr6), _lib.ptr(self.ws), self.ws_bytes,
+                      ctypes.byref(self._sent), _lib.stream_ptr())
+            if self.ctx is not None:
+                self.ctx.counters["p2p_bytes"] = self.bytes_sent()
+            return
+        k = self.kernels
+        for a in range(3):
+            lo, hi = self.nbr6[2 * a], self.nbr6[2 * a + 1]
+            if lo < 0 and hi < 0:
+                continue
+            down, up = k.pack(s, a, lo >= 0, hi >= 0)
+            sends, recvs = [], []
+            if lo >= 0:
+                sends.append((lo, down, (tag, a, "down")))
+            if hi >= 0:
+                sends.append((hi, up, (tag, a, "up")))
+            if lo >= 0:
+                recvs.append((lo, k.like(s, a), (tag, a, "up")))
+            if hi >= 0:
+                recvs.append((hi, k.like(s, a), (tag, a, "down")))
+            got = iter(self.ctx.exchange(sends, recvs))
+            k.unpack(s, a, next(got) if lo >= 0 else None, next(got) if hi >= 0 else None)
+
+    def zero(self, s):
+        """Zero the margins this halo wrote (a gradient slab before its weight gradient)."""
+        if self.active:
+            self.kernels.zero(s, self.nbr6)
+
+
+def nccl_comm_ptr(group=None):
+    """The ncclComm_t behind a torch.distributed NCCL process group (initialised eagerly by a
+    one-element all-reduce when torch created it lazily)."""
+    import torch
+    import torch.distributed as dist
+
+    g = group if group is not None else dist.group.WORLD
+    backend = g._get_backend(torch.device("cuda"))
+    try:
+        ptr = int(backend._comm_ptr())
+    except Exception:  # noqa: BLE001 - lazily created communicator
+        ptr = 0
+    if not ptr:
+        t = torch.zeros(1, device="cuda")
+        dist.all_reduce(t, group=g)
+        torch.cuda.synchronize()
+        ptr = int(backend._comm_ptr())
+    _lib.call("vm_nccl_bind")
+    return ptr
+
+
+def nccl_comm_of(ctx):
+    """The world NCCL communicator of an spmd mesh over NCCL, else None (threads / gloo)."""
+    if ctx is None or ctx.mesh.backend != "spmd" or ctx.device.type != "cuda":
+        return None
+    import torch.distributed as dist
+
+    if dist.get_backend() != "nccl":
+        return None
+    return nccl_comm_ptr()
+
+
+def nccl_second_comm(ctx):
+    """A second NCCL communicator over all ranks (the bucketed weight-gradient all-reduce runs
+    on its own stream and communicator, concurrently with the halo's), cached per mesh."""
+    if nccl_comm_of(ctx) is None:
+        return None
+    mesh = ctx.mesh
+    if getattr(mesh, "_ar_comm", None) is None:
+        import torch.distributed as dist
+
+        mesh._ar_group = dist.new_group(backend="nccl")
+        mesh._ar_comm = nccl_comm_ptr(mesh._ar_group)
+    return mesh._ar_comm

@@ -21,6 +21,7 @@ Replaces the reference's per-worker graph interpreter (``unet.run_forward_local`
 
 from __future__ import annotations
 
+import ctypes
 import math
 
 import numpy as np
@@ -28,7 +29,7 @@ import torch
 
 from . import _lib
 from .errors import GraphBuildError, VoxmeshError
-from .halo import run_exchange
+from .halo import SlabHalo, nccl_comm_of, nccl_second_comm
 
 _DT = {torch.bfloat16: _lib.VM_BF16, torch.float32: _lib.VM_F32}
 
@@ -134,6 +135,20 @@ class UNetStep:
                 if ctx is not None:
                     self.nbrs[1 + i] = (ctx.neighbor(a, -1), ctx.neighbor(a, +1))
         self.has_halo = any(lo is not None or hi is not None for lo, hi in self.nbrs.values())
+        nbr6 = [-1] * 6
+        for i in range(3):
+            lo, hi = self.nbrs.get(1 + i, (None, None))
+            nbr6[2 * i], nbr6[2 * i + 1] = (-1 if lo is None else lo), (-1 if hi is None else hi)
+        # the halo transport: NCCL through the C ABI when the mesh is spmd over NCCL (one C call
+        # per slab, graph-capturable), else host-driven phases around ctx.exchange (threads)
+        self.halo = SlabHalo(nbr6, ctx=ctx, comm=nccl_comm_of(ctx))
+        self.comm = self.halo.comm  # NCCL communicator of the step's collectives (None: ctx's)
+        self.ar_comm = nccl_second_comm(ctx)  # bucketed weight-gradient all-reduce
+        # overlap the exchange with the conv's interior planes: only the depth axis is split
+        # (cfg3); the interior output planes [1, D-1) read no margin plane
+        self.overlap_halo = True
+        self.overlap_min_planes = 8
+        self.bucket_bytes = 16 << 20
         bdiv = mesh.axis_size(layout.axis_for("batch")) if (layout is not None and layout.axis_for("batch")) else 1
         self.global_batch = global_batch or batch * bdiv
         E = cfg.input_extent
@@ -143,7 +158,6 @@ class UNetStep:
             g // d for g, d in zip(self.global_shape, self.div))
         self.total_voxels = float(self.global_batch * int(np.prod(self.global_shape)))
         self._rec = None
-        self.packer = None  # halo pack/unpack backend (None: the CUDA box kernels)
         self.overlap_wgrad = True  # weight gradients on a side stream, concurrent with dgrad
         # programmatic dependent launch (the next kernel's CTAs are scheduled and set up while
         # the previous one drains).  Forward: trigger at kernel start.  Backward: trigger at CTA
@@ -153,6 +167,7 @@ class UNetStep:
         self.pdl_forward = 1  # 0 off, 1 trigger at kernel start, 2 trigger at CTA exit
         self.pdl_backward = 2
         self._build_buffers(params)
+        self._reserve_halo()
 
     # ------------------------------------------------------------------ setup
     def _ext(self, nid):
@@ -346,14 +361,21 @@ class UNetStep:
     def _conv_flops(self, L):
         return 2.0 * self.B * L.D * L.H * L.W * 27 * L.cin * L.cout
 
-    def _conv(self, x, L, y, flags, mask=None, dgrad=False):
+    def _conv(self, x, L, y, flags, mask=None, dgrad=False, planes=None):
         cin, cout = (L.cout, L.cin) if dgrad else (L.cin, L.cout)
         mp = mask.p() if mask is not None else None
         mb = mask.bstride if mask is not None else 0
         kind = "conv_dgrad" if dgrad else "conv_fwd"
-        vox = self.B * L.D * L.H * L.W
+        nd = planes[1] if planes is not None else L.D
+        vox = self.B * nd * L.H * L.W
         nbytes = 2.0 * vox * (cin + cout + (cout if mask is not None else 0))
-        if self.conv_impl == "tc" and L.c1 and not dgrad:
+        flops = self._conv_flops(L) * nd / L.D
+        if planes is not None:  # output planes [d0, d0 + nd) (tensor-core path)
+            w = L.wpt if dgrad else L.wp
+            self._k(kind, L.node.id, flops, nbytes, "vm_conv3d_fwd_tc_range", x.p(), x.bstride, _lib.ptr(w),
+                    _lib.ptr(L.b), y.p(), y.bstride, mp, mb, self.B, cin, cout, L.D, L.H, L.W, planes[0], nd, flags,
+                    _lib.ptr(self.conv_ws), self.conv_ws_bytes)
+        elif self.conv_impl == "tc" and L.c1 and not dgrad:
             self._k(kind, L.node.id, self._conv_flops(L), nbytes, "vm_conv3d_fwd_c1", _lib.ptr(self.x1), 0,
                     _lib.ptr(L.w), _lib.ptr(L.b), y.p(), y.bstride, self.B, cout, L.D, L.H, L.W, flags)
         elif self.conv_impl == "tc":
@@ -383,12 +405,8 @@ class UNetStep:
                     L.cin, L.cout, L.D, L.H, L.W)
 
     def _halo(self, s, tag):
-        if not self.has_halo:
-            return
-        margins5 = [(0, 0), (1, 1), (1, 1), (1, 1), (0, 0)]
-        core5 = (s.CG, s.D, s.H, s.W, 8)
-        for b in range(self.B):
-            run_exchange(self.ctx, s.view5(b), core5, margins5, self.nbrs, tag=tag, packer=self.packer)
+        if self.has_halo:
+            self.halo.forward(s, tag)
 
     def halo_bytes_per_step(self):
         """Bytes this rank sends per step (3-phase protocol, fwd + bwd, slab channel padding included)."""
@@ -415,19 +433,74 @@ class UNetStep:
         return total
 
     def _zero_margins(self, s):
-        if not self.has_halo:
+        if self.has_halo:
+            self.halo.zero(s)
+
+    def use_nccl(self, comm, nbr6=None, ar_comm=None):
+        """Route the halo and the collectives through NCCL communicator ``comm`` (an
+        ncclComm_t).  ``nbr6`` overrides the neighbour ranks: a 1-rank communicator with the
+        rank as its own lo and hi neighbour gives periodic halos on one GPU (the single-GPU
+        emulation of a split: same pack / NCCL / unpack work, no NVLink wire time)."""
+        if nbr6 is not None:
+            self.halo = SlabHalo(nbr6, ctx=self.ctx, comm=comm)
+            for i in range(3):
+                lo, hi = nbr6[2 * i], nbr6[2 * i + 1]
+                if lo >= 0 or hi >= 0:
+                    self.nbrs[1 + i] = (lo if lo >= 0 else None, hi if hi >= 0 else None)
+            self.has_halo = self.halo.active
+        else:
+            self.halo.comm = comm
+        self.comm = comm
+        self.ar_comm = ar_comm
+        self._reserve_halo()
+
+    def _reserve_halo(self):
+        if self.halo.comm is None:
             return
-        for b in range(self.B):
-            v = s.view5(b)
-            dims = _lib.i64arr(v.shape)
-            for ax in (1, 2, 3):
-                n = v.shape[ax] - 2
-                for lo in (0, n + 1):
-                    lo5 = [0, 0, 0, 0, 0]
-                    ext5 = list(v.shape)
-                    lo5[ax], ext5[ax] = lo, 1
-                    self._k("halo", "zero", 0, 0, "vm_box_zero", _lib.ptr(v), dims, v.element_size(),
-                            _lib.i64arr(lo5), _lib.i64arr(ext5))
+        slabs = [self.out[n.inputs[0]] for n in self.graph.nodes if n.op == "conv" and n.k == 3]
+        slabs += list(self.gpre.values())
+        self.halo.reserve(slabs)
+
+    def _split_planes(self, D):
+        """Interior / boundary split of a conv's output planes around a depth-only halo."""
+        n = self.halo.nbr6
+        depth_only = (n[0] >= 0 or n[1] >= 0) and max(n[2:]) < 0
+        return (self.overlap_halo and self.has_halo and depth_only and self.conv_impl == "tc"
+                and D >= self.overlap_min_planes)
+
+    def graph_capturable(self):
+        return self.ctx is None or self.ctx.mesh.worker_count == 1 or self.comm is not None
+
+    def _comm_stream(self):
+        if getattr(self, "_cstream", None) is None:
+            self._cstream = torch.cuda.Stream(device=self.device)
+        return self._cstream
+
+    def _ar_stream(self):
+        if getattr(self, "_arstream", None) is None:
+            self._arstream = torch.cuda.Stream(device=self.device)
+        return self._arstream
+
+    def _halo_conv(self, x, L, y, flags, mask=None, dgrad=False, tag="halo"):
+        """Halo of ``x`` then conv(x): with a depth-only split the exchange runs on the comm
+        stream while the interior output planes compute, then the two boundary planes."""
+        if not self._split_planes(L.D):
+            self._halo(x, tag)
+            self._conv(x, L, y, flags, mask=mask, dgrad=dgrad)
+            return
+        main = torch.cuda.current_stream()
+        comm = self._comm_stream()
+        ready = torch.cuda.Event()
+        ready.record(main)
+        self._conv(x, L, y, flags, mask=mask, dgrad=dgrad, planes=(1, L.D - 2))
+        comm.wait_event(ready)
+        with torch.cuda.stream(comm):
+            self._halo(x, tag)
+            done = torch.cuda.Event()
+            done.record(comm)
+        main.wait_event(done)
+        self._conv(x, L, y, flags, mask=mask, dgrad=dgrad, planes=(0, 1))
+        self._conv(x, L, y, flags, mask=mask, dgrad=dgrad, planes=(L.D - 1, 1))
 
     # ------------------------------------------------------------------ inputs
     def load_inputs(self, image, labels):
@@ -650,8 +723,7 @@ class UNetStep:
         for n in self.graph.nodes:
             if n.op == "conv" and n.k == 3:
                 x = self.out[n.inputs[0]]
-                self._halo(x, "halo")
-                self._conv(x, self.by_id[n.id], self.out[n.id], _lib.VM_CONV_RELU)
+                self._halo_conv(x, self.by_id[n.id], self.out[n.id], _lib.VM_CONV_RELU)
             elif n.op == "pool":
                 x, y = self.out[n.inputs[0]], self.out[n.id]
                 nb = 2.0 * self.B * x.D * x.H * x.W * x.C * 9 / 8
@@ -682,7 +754,10 @@ class UNetStep:
                 self.ncls, h.D, h.H, h.W, self.clamp)
         self._k("reduce", "stats", 0, 0, "vm_reduce_rows", _lib.ptr(self.partials), self.n_part, 3 * self.ncls + 1,
                 _lib.ptr(self.stats))
-        if self.ctx is not None and self.ctx.mesh.worker_count > 1 and self.stats_axes != ():
+        if self.comm is not None and self.stats_axes is None:  # training.py:337 over NCCL
+            self._k("coll", "stats", 0, 0, "vm_allreduce_f32", ctypes.c_void_p(self.comm), _lib.ptr(self.stats),
+                    self.stats.numel())
+        elif self.ctx is not None and self.ctx.mesh.worker_count > 1 and self.stats_axes != ():
             red = self.ctx.all_reduce_sum(self.stats, axes=self.stats_axes, tag="loss-stats")
             if red is not self.stats:
                 self.stats.copy_(red)
@@ -711,35 +786,48 @@ class UNetStep:
         h.gw.copy_(self.hgrad[: h.nk])
         h.gb.copy_(self.hgrad[h.nk :])
         # wgrad(x, g) and dgrad(g) of a conv are independent: the weight gradients run on a
-        # side stream (joined before the gradient all-reduce), which fills the SMs the small
-        # deep-level kernels leave idle.  With a halo, the exchange writes g's margins, which
-        # wgrad reads as zeros, so it waits for that layer's wgrad.
+        # side stream (joined before SGD), which fills the SMs the small deep-level kernels
+        # leave idle.  Without a halo, wgrad starts with the layer's dgrad.  With a halo, the
+        # exchange writes g's margins and wgrad reads them as zeros: halo -> dgrad -> zero the
+        # margins on the main stream, then wgrad on the side stream behind a per-layer event,
+        # so the main stream never waits for a weight gradient.  Over NCCL the weight
+        # gradients are all-reduced in buckets on their own stream and communicator as soon
+        # as a bucket's last wgrad is done (unet.py:434-441), overlapping the rest of backward.
         main = torch.cuda.current_stream()
         side = self._side_stream() if self.overlap_wgrad else None
+        buckets = self._grad_buckets() if (self.ar_comm is not None and side is not None) else {}
+        if buckets:
+            ar = self._ar_stream()
         for n in reversed(self.graph.nodes):
             if n.op == "conv" and n.k == 3:
                 L = self.by_id[n.id]
                 x = self.out[n.inputs[0]]
                 gp = self.gpre[n.id]
+                src = n.inputs[0]
+                if src != "input" and self.has_halo:
+                    self._dgrad(gp, L, src)
+                    self._zero_margins(gp)
+                    if side is not None:
+                        ev = torch.cuda.Event()
+                        ev.record(main)
+                        side.wait_event(ev)
                 if side is not None:
-                    side.wait_stream(main)
+                    if not self.has_halo:
+                        side.wait_stream(main)
                     with torch.cuda.stream(side):
                         self._wgrad(x, L, gp)
-                    if self.has_halo:
-                        main.wait_stream(side)
+                        if L.index in buckets:
+                            ev = torch.cuda.Event()
+                            ev.record(side)
+                            ar.wait_event(ev)
+                            lo, hi = buckets[L.index]
+                            with torch.cuda.stream(ar):
+                                self._k("coll", "grads", 0, 0, "vm_allreduce_f32", ctypes.c_void_p(self.ar_comm),
+                                        _lib.ptr(self.grads[lo:hi]), hi - lo)
                 else:
                     self._wgrad(x, L, gp)
-                src = n.inputs[0]
-                if src == "input":
-                    continue
-                self._halo(gp, "halo-bwd")
-                sn = self.graph.node(src)
-                if sn.op == "relu":
-                    self._conv(gp, L, self.gpre[sn.inputs[0]], _lib.VM_CONV_MASK | _lib.VM_CONV_NOBIAS,
-                               mask=self.out[src], dgrad=True)
-                else:  # pool or concat output gradient, unmasked
-                    self._conv(gp, L, self.gnode[src], _lib.VM_CONV_NOBIAS, dgrad=True)
-                self._zero_margins(gp)
+                if src != "input" and not self.has_halo:
+                    self._dgrad(gp, L, src)
             elif n.op == "up":
                 cat = next(c for c in self.consumers[n.id] if c.op == "concat")
                 gcat = self.gnode[cat.id]
@@ -772,6 +860,34 @@ class UNetStep:
 
         if side is not None:
             main.wait_stream(side)
+        if buckets:
+            main.wait_stream(ar)
+        self._grads_reduced = bool(buckets)
+
+    def _dgrad(self, gp, L, src):
+        """Halo of the output gradient, then the data gradient (ops.py:100-114) with the
+        producer's ReLU mask fused (ops.py:186-187)."""
+        sn = self.graph.node(src)
+        if sn.op == "relu":
+            self._halo_conv(gp, L, self.gpre[sn.inputs[0]], _lib.VM_CONV_MASK | _lib.VM_CONV_NOBIAS,
+                            mask=self.out[src], dgrad=True, tag="halo-bwd")
+        else:  # pool or concat output gradient, unmasked
+            self._halo_conv(gp, L, self.gnode[src], _lib.VM_CONV_NOBIAS, dgrad=True, tag="halo-bwd")
+
+    def _grad_buckets(self):
+        """{layer index closing a bucket: (flat lo, flat hi)}: contiguous runs of layers in
+        backward order of >= bucket_bytes of fp32 gradients."""
+        if getattr(self, "_buckets", None) is None:
+            out, hi, size = {}, None, 0
+            for L in reversed(self.layers):
+                a, b = self.offsets_host[L.index], self.offsets_host[L.index + 1]
+                hi = b if hi is None else hi
+                size += 4 * (b - a)
+                if size >= self.bucket_bytes or L.index == 0:
+                    out[L.index] = (a, hi)
+                    hi, size = None, 0
+            self._buckets = out
+        return self._buckets
 
     def _side_stream(self):
         if getattr(self, "_wg_stream", None) is None:
@@ -779,7 +895,14 @@ class UNetStep:
         return self._wg_stream
 
     def all_reduce_grads(self):
-        if self.ctx is not None and self.ctx.mesh.worker_count > 1:
+        """Sum the weight gradients over every mesh axis (unet.py:434-441); a no-op when the
+        backward already all-reduced them in buckets."""
+        if getattr(self, "_grads_reduced", False):
+            return
+        if self.comm is not None:
+            self._k("coll", "grads", 0, 0, "vm_allreduce_f32", ctypes.c_void_p(self.comm), _lib.ptr(self.grads),
+                    self.grads.numel())
+        elif self.ctx is not None and self.ctx.mesh.worker_count > 1:
             red = self.ctx.all_reduce_sum(self.grads, tag="grads")
             if red is not self.grads:
                 self.grads.copy_(red)
@@ -812,6 +935,8 @@ class UNetStep:
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
             for kind, label, flops, nbytes, name, args in rec:
+                if kind == "coll":  # a collective replayed on one rank alone would wait for its peers
+                    continue
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=s):
                     for _ in range(reps):
