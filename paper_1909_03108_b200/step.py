@@ -448,6 +448,10 @@ class UNetStep:
                 if lo >= 0 or hi >= 0:
                     self.nbrs[1 + i] = (lo if lo >= 0 else None, hi if hi >= 0 else None)
             self.has_halo = self.halo.active
+            if self.has_halo:  # a halo'd first conv reads the 8-channel input slab (margins exchanged)
+                for L in self.layers:
+                    L.c1 = False
+                self.input_slab_needed = True
         else:
             self.halo.comm = comm
         self.comm = comm
@@ -484,7 +488,7 @@ class UNetStep:
     def _halo_conv(self, x, L, y, flags, mask=None, dgrad=False, tag="halo"):
         """Halo of ``x`` then conv(x): with a depth-only split the exchange runs on the comm
         stream while the interior output planes compute, then the two boundary planes."""
-        if not self._split_planes(L.D):
+        if not self._split_planes(L.D) or (L.c1 and not dgrad):
             self._halo(x, tag)
             self._conv(x, L, y, flags, mask=mask, dgrad=dgrad)
             return
@@ -653,12 +657,18 @@ class UNetStep:
         threads mesh exchanges through host queues).  Replays run on the current stream."""
         if self.ctx is not None and self.ctx.mesh.worker_count > 1 and not self.graph_capturable():
             return None
+        import gc
+
+        # a CUDAGraph freed by the garbage collector in the middle of the capture (another
+        # step's graph) would invalidate it: collect first; thread-local capture mode so that
+        # other threads' CUDA calls (the threads mesh captures one rank per thread) are legal
+        gc.collect()
         cur = torch.cuda.current_stream(self.device)
         s = torch.cuda.Stream(device=self.device)
         s.wait_stream(cur)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(s):
-            with torch.cuda.graph(g, stream=s):
+            with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
                 self.step()
         cur.wait_stream(s)
         return g

@@ -212,40 +212,39 @@ def test_batched_repack_equals_single_packs():
         assert torch.equal(ref.view(torch.int16), buf.view(torch.int16))
 
 
-def test_survey_abi_names_are_the_kernels():
-    # vm_conv3d_fwd / vm_conv3d_dgrad / vm_conv3d_wgrad (csrc/abi.cu) == the _tc entry points, bitwise
-    B, cin, cout, D, H, W = 1, 16, 32, 6, 8, 40
-    rng = np.random.default_rng(21)
-    x = O.bf16_round(rng.standard_normal((B, D, H, W, cin)).astype(np.float32))
-    g = O.bf16_round(rng.standard_normal((B, D, H, W, cout)).astype(np.float32))
-    w = O.bf16_round(rng.uniform(-1, 1, (3, 3, 3, cin, cout)).astype(np.float32) / 20)
-    b = rng.standard_normal(cout).astype(np.float32) * 0.1
-    xs, gs = _slab_from(x), _slab_from(g)
-    ref = _conv_tc(xs, w, b, cout)
-    wt = torch.from_numpy(np.ascontiguousarray(w)).cuda()
-    wp = torch.empty(_lib.call_size("vm_packed_weights_bytes", cin, cout) // 2, dtype=torch.bfloat16, device="cuda")
-    wpt = torch.empty(_lib.call_size("vm_packed_weights_bytes", cout, cin) // 2, dtype=torch.bfloat16, device="cuda")
-    _lib.call("vm_pack_weights", _lib.ptr(wt), _lib.ptr(wp), cin, cout, 0, _lib.stream_ptr())
-    _lib.call("vm_pack_weights", _lib.ptr(wt), _lib.ptr(wpt), cin, cout, 1, _lib.stream_ptr())
-    bt = torch.from_numpy(b).cuda()
-    y = Slab(B, cout, D, H, W, torch.bfloat16, "cuda")
-    _lib.call("vm_conv3d_fwd", xs.p(), xs.bstride, _lib.ptr(wp), _lib.ptr(bt), y.p(), y.bstride, B, cin, cout,
-              D, H, W, _lib.VM_CONV_RELU, _lib.stream_ptr())
-    assert torch.equal(y.storage, ref.storage)
-    gx = Slab(B, cin, D, H, W, torch.bfloat16, "cuda")
-    _lib.call("vm_conv3d_dgrad", gs.p(), gs.bstride, _lib.ptr(wpt), xs.p(), xs.bstride, gx.p(), gx.bstride, B, cin,
-              cout, D, H, W, _lib.stream_ptr())
-    gx_ref = _conv_tc(gs, w, np.zeros(cin, np.float32), cin, flags=_lib.VM_CONV_MASK | _lib.VM_CONV_NOBIAS,
-                      mask=xs, flip=True)
-    assert torch.equal(gx.storage, gx_ref.storage)
-    gw1, gb1 = _wgrad("vm_conv3d_wgrad_tc", xs, gs, cin, cout)
-    gw2 = torch.zeros(27 * cin * cout, dtype=torch.float32, device="cuda")
-    gb2 = torch.zeros(cout, dtype=torch.float32, device="cuda")
-    ws = torch.empty(_lib.call_size("vm_conv3d_wgrad_ws", B, cin, cout, D, H, W) // 4 + 64, device="cuda")
-    _lib.call("vm_conv3d_wgrad", xs.p(), xs.bstride, gs.p(), gs.bstride, _lib.ptr(gw2), _lib.ptr(gb2), _lib.ptr(ws),
-              B, cin, cout, D, H, W, _lib.stream_ptr())
-    torch.cuda.synchronize()
-    assert np.array_equal(gw2.cpu().numpy().reshape(gw1.shape), gw1) and np.array_equal(gb2.cpu().numpy(), gb1)
+def test_dgrad_composite_and_plane_ranges_are_the_kernels():
+    # vm_conv3d_dgrad (csrc/abi.cu) == the flipped-operand tc conv with the ReLU mask, and
+    # vm_conv3d_fwd_tc_range over [0,1) + [1,D-1) + [D-1,D) (the halo-overlap split) == one
+    # full launch, bitwise, for the sweep (thin) and the general kernels
+    for (B, cin, cout, D, H, W) in ((1, 16, 32, 10, 8, 40), (2, 64, 128, 9, 6, 12)):
+        rng = np.random.default_rng(21 + cin)
+        x = O.bf16_round(rng.standard_normal((B, D, H, W, cin)).astype(np.float32))
+        g = O.bf16_round(rng.standard_normal((B, D, H, W, cout)).astype(np.float32))
+        w = O.bf16_round(rng.uniform(-1, 1, (3, 3, 3, cin, cout)).astype(np.float32) / 20)
+        b = rng.standard_normal(cout).astype(np.float32) * 0.1
+        xs, gs = _slab_from(x), _slab_from(g)
+        ref = _conv_tc(xs, w, b, cout)
+        wt = torch.from_numpy(np.ascontiguousarray(w)).cuda()
+        wp = torch.empty(_lib.call_size("vm_packed_weights_bytes", cin, cout) // 2, dtype=torch.bfloat16,
+                         device="cuda")
+        wpt = torch.empty(_lib.call_size("vm_packed_weights_bytes", cout, cin) // 2, dtype=torch.bfloat16,
+                          device="cuda")
+        _lib.call("vm_pack_weights", _lib.ptr(wt), _lib.ptr(wp), cin, cout, 0, _lib.stream_ptr())
+        _lib.call("vm_pack_weights", _lib.ptr(wt), _lib.ptr(wpt), cin, cout, 1, _lib.stream_ptr())
+        bt = torch.from_numpy(b).cuda()
+        y = Slab(B, cout, D, H, W, torch.bfloat16, "cuda")
+        for d0, nd in ((1, D - 2), (0, 1), (D - 1, 1)):
+            _lib.call("vm_conv3d_fwd_tc_range", xs.p(), xs.bstride, _lib.ptr(wp), _lib.ptr(bt), y.p(), y.bstride,
+                      None, 0, B, cin, cout, D, H, W, d0, nd, _lib.VM_CONV_RELU, None, 0, _lib.stream_ptr())
+        torch.cuda.synchronize()
+        assert torch.equal(y.storage, ref.storage)
+        gx = Slab(B, cin, D, H, W, torch.bfloat16, "cuda")
+        _lib.call("vm_conv3d_dgrad", gs.p(), gs.bstride, _lib.ptr(wpt), xs.p(), xs.bstride, gx.p(), gx.bstride, B,
+                  cin, cout, D, H, W, _lib.stream_ptr())
+        gx_ref = _conv_tc(gs, w, np.zeros(cin, np.float32), cin, flags=_lib.VM_CONV_MASK | _lib.VM_CONV_NOBIAS,
+                          mask=xs, flip=True)
+        torch.cuda.synchronize()
+        assert torch.equal(gx.storage, gx_ref.storage)
 
 
 @pytest.mark.parametrize("shape", [(1, 128, 128, 16, 16, 16), (1, 64, 128, 8, 8, 8), (2, 128, 64, 8, 8, 8),
