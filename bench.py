@@ -286,8 +286,9 @@ def _first_loss_check(cfg_name, loss, n_gpus):
         ref = json.load(open(path))[cfg_name]["loss"]
     except Exception:
         return {"first_step_loss": loss, "oracle_loss": None, "ok": None, "note": f"no stored oracle loss for {cfg_name}"}
-    rel = abs(loss - ref) / abs(ref)
-    out = {"first_step_loss": loss, "oracle_loss": ref, "rel_err": rel, "tol": 1e-2, "ok": rel <= 1e-2}
+    loss = float(loss)
+    rel = float(abs(loss - ref) / abs(ref))
+    out = {"first_step_loss": loss, "oracle_loss": ref, "rel_err": rel, "tol": 1e-2, "ok": bool(rel <= 1e-2)}
     if not out["ok"]:
         raise SystemExit(f"[bench] first-step loss {loss} differs from the oracle's {ref} (rel {rel:.2e} > 1e-2)")
     return out
@@ -558,7 +559,7 @@ def run_ours(a):
         "conv_tflops_effective": conv_flops_rank / (conv_ms * 1e-3) / 1e12 if conv_ms else None,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

@@ -259,6 +259,9 @@ int vm_nccl_bind(void);
 size_t vm_halo_slab_ws_bytes(int dtype, int B, int C, int D, int H, int W);
 int vm_halo_slab_fwd(void* comm, int dtype, void* slab, int64_t bstride, int B, int C, int D, int H, int W,
                      const int* nbr, void* ws, size_t ws_bytes, long long* bytes_sent, void* stream);
+/* depth-phase layers of at least `bytes` per (sample, channel group) are sent zero-copy (no
+ * pack / unpack: straight from / into the slab); returns the previous threshold (default: off) */
+long long vm_set_halo_zero_copy_min(long long bytes);
 /* zero the margin layers on every side with a neighbour (gradient slabs before wgrad) */
 int vm_halo_slab_zero(int dtype, void* slab, int64_t bstride, int B, int C, int D, int H, int W,
                       const int* nbr, void* stream);
@@ -272,6 +275,9 @@ long long vm_halo_slab_face_bytes(int dtype, int B, int C, int D, int H, int W, 
 /* in-place sum over the communicator (mesh.py:195-233 all_reduce_sum; unet.py:434-441) */
 int vm_allreduce_f32(void* comm, float* buf, size_t n, void* stream);
 
+/* SMs the forward / dgrad conv kernels of the calling host thread may occupy (0 = all);
+ * returns the previous value.  Set around the interior-plane conv that overlaps a halo. */
+int vm_set_conv_sm_limit(int n);
 /* conv3d forward / dgrad on output planes [d0, d0+nd) of slabs with D interior planes (the
  * interior planes run while the halo fills the margins; the boundary planes after it) */
 int vm_conv3d_fwd_tc_range(const void* x, int64_t x_bstride, const void* wpacked, const float* bias, void* y,

@@ -36,6 +36,7 @@ _SIGS = {
     "vm_num_sms": (_I, [_I]),
     "vm_launch_count": (ctypes.c_longlong, []),
     "vm_set_pdl": (ctypes.c_int, [ctypes.c_int]),
+    "vm_set_conv_sm_limit": (ctypes.c_int, [ctypes.c_int]),
     "vm_box_pack": (_I, [_P, _c_i64p, _I, _c_i64p, _c_i64p, _P, _P]),
     "vm_box_unpack": (_I, [_P, _c_i64p, _I, _c_i64p, _c_i64p, _P, _P]),
     "vm_box_unpack_add": (_I, [_P, _c_i64p, _I, _c_i64p, _c_i64p, _P, _P]),
@@ -80,6 +81,7 @@ _SIGS = {
     "vm_nccl_bind": (_I, []),
     "vm_halo_slab_ws_bytes": (_S, [_I, _I, _I, _I, _I, _I]),
     "vm_halo_slab_fwd": (_I, [_P, _I, _P, _L, _I, _I, _I, _I, _I, _P, _P, _S, _P, _P]),
+    "vm_set_halo_zero_copy_min": (ctypes.c_longlong, [ctypes.c_longlong]),
     "vm_halo_slab_zero": (_I, [_I, _P, _L, _I, _I, _I, _I, _I, _P, _P]),
     "vm_halo_slab_pack": (_I, [_I, _P, _L, _I, _I, _I, _I, _I, _I, _P, _P, _P]),
     "vm_halo_slab_unpack": (_I, [_I, _P, _L, _I, _I, _I, _I, _I, _I, _P, _P, _P]),

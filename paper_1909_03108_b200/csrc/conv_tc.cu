@@ -1628,6 +1628,15 @@ extern "C" int vm_pack_weights(const float* w, void* packed, int Cin, int Cout, 
 }
 
 static long long* g_fwd_dbg = nullptr;
+// Per host thread: SMs the forward / dgrad conv may occupy (0: all).  The interior-plane conv
+// that overlaps a halo leaves a few SMs to the exchange's pack / NCCL / unpack kernels, which
+// cannot co-reside with a 1-CTA-per-SM tensor-core conv (shared memory + TMEM).
+static thread_local int g_conv_sm_limit = 0;
+extern "C" int vm_set_conv_sm_limit(int n) {
+  const int prev = g_conv_sm_limit;
+  g_conv_sm_limit = n < 0 ? 0 : n;
+  return prev;
+}
 static int g_sweep_xmode = 0;
 extern "C" void vm_debug_set_sweep_mode(int m) { g_sweep_xmode = m; }
 static int g_sweep_force_mb = 0;  // A/B probes: restrict the sweep planner to one MB
@@ -1841,6 +1850,7 @@ static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, 
              "vm_conv3d_fwd_tc: slab must be 16-byte aligned");
   int nsm = vm_num_sms(0);
   if (nsm <= 0) nsm = 148;
+  if (g_conv_sm_limit > 0 && g_conv_sm_limit < nsm) nsm = g_conv_sm_limit;
   if (pg.sweep) return launch_sweep(p, nsm, stream);
   p.b_bytes = 9 * 2 * p.Nc * 16;
   const int N = p.Nc;  // accumulator columns per tile

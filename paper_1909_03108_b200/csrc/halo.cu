@@ -52,35 +52,38 @@ __host__ __device__ inline void face_extent(const FaceSet& s, const Face& f, int
   }
 }
 
+// One warp per row of a face: a row is the run along the face's last dim (i2) of one
+// (sample, channel group, i1); lanes stride over its 16-byte units (a whole W row of a depth
+// or height face is contiguous in the slab: 512-byte warp accesses).  32-bit index math.
 template <bool PACK>
-__global__ void k_slab_faces(uint8_t* __restrict__ slab, const FaceSet s) {
+__global__ void __launch_bounds__(256) k_slab_faces(uint8_t* __restrict__ slab, const FaceSet s) {
   pdl_wait();
   const Face f = s.f[blockIdx.y];
   int n1, n2, lo1, lo2;
   face_extent(s, f, n1, n2, lo1, lo2);
   const int upv = s.vec / 16;  // 16-byte units per voxel group (1: bf16, 2: f32)
-  const int64_t total = (int64_t)s.B * s.CG * n1 * n2 * upv;
+  const int rows = s.B * s.CG * n1;
+  const int row = blockIdx.x * 8 + threadIdx.x / 32;
+  if (row >= rows) return;
+  const int lane = threadIdx.x % 32;
+  const int i1 = row % n1;
+  const int bc = row / n1;
+  const int cg = bc % s.CG, b = bc / s.CG;
   const int Hp = s.H + 2, Wp = s.W + 2;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = i / upv;
-    const int u = (int)(i - r * upv);
-    const int i2 = (int)(r % n2);
-    r /= n2;
-    const int i1 = (int)(r % n1);
-    r /= n1;
-    const int cg = (int)(r % s.CG);
-    const int b = (int)(r / s.CG);
-    int d, h, w;
-    if (f.axis == 0) d = f.pos, h = lo1 + i1, w = lo2 + i2;
-    else if (f.axis == 1) d = lo1 + i1, h = f.pos, w = lo2 + i2;
-    else d = lo1 + i1, h = lo2 + i2, w = f.pos;
-    uint4* p = reinterpret_cast<uint4*>(slab + b * s.bstride_b + cg * s.plane_b +
-                                        (((int64_t)d * Hp + h) * Wp + w) * s.vec) + u;
-    if (PACK) {
-      reinterpret_cast<uint4*>(f.buf)[i] = *p;
-    } else {
-      *p = f.buf ? reinterpret_cast<const uint4*>(f.buf)[i] : make_uint4(0, 0, 0, 0);
-    }
+  // slab byte offset of (i1, i2 = 0) and the byte stride along i2
+  int64_t base;
+  int64_t step;
+  if (f.axis == 0) base = ((int64_t)f.pos * Hp + lo1 + i1) * Wp + lo2, step = 1;
+  else if (f.axis == 1) base = ((int64_t)(lo1 + i1) * Hp + f.pos) * Wp + lo2, step = 1;
+  else base = ((int64_t)(lo1 + i1) * Hp + lo2) * Wp + f.pos, step = Wp;
+  uint8_t* p0 = slab + b * s.bstride_b + cg * s.plane_b + base * s.vec;
+  const int units = n2 * upv;
+  uint4* msg = f.buf ? reinterpret_cast<uint4*>(f.buf) + (int64_t)row * units : nullptr;
+  for (int u = lane; u < units; u += 32) {
+    const int i2 = u / upv, k = u - i2 * upv;
+    uint4* p = reinterpret_cast<uint4*>(p0 + (int64_t)i2 * step * s.vec) + k;
+    if (PACK) msg[u] = *p;
+    else *p = msg ? msg[u] : make_uint4(0, 0, 0, 0);
   }
 }
 
@@ -92,12 +95,14 @@ static int64_t face_bytes(const FaceSet& s, const Face& f) {
 
 static int launch_faces(bool pack, void* slab, const FaceSet& s, cudaStream_t st) {
   if (s.n == 0) return VM_OK;
-  int64_t most = 0;
+  int most = 0;
   for (int i = 0; i < s.n; ++i) {
-    const int64_t b = face_bytes(s, s.f[i]) / 16;
-    most = b > most ? b : most;
+    int n1, n2, lo1, lo2;
+    face_extent(s, s.f[i], n1, n2, lo1, lo2);
+    const int rows = s.B * s.CG * n1;
+    most = rows > most ? rows : most;
   }
-  dim3 grid(grid_for(most, 256) / s.n + 1, s.n);
+  dim3 grid((most + 7) / 8, s.n);
   if (pack) launch_pdl(k_slab_faces<true>, grid, 256, 0, st, static_cast<uint8_t*>(slab), s);
   else launch_pdl(k_slab_faces<false>, grid, 256, 0, st, static_cast<uint8_t*>(slab), s);
   return launch_status(pack ? "vm_halo pack" : "vm_halo unpack");
@@ -127,6 +132,20 @@ struct NcclApi {
 };
 static NcclApi g_nccl;
 constexpr int kNcclUint8 = 1, kNcclFloat32 = 7, kNcclSum = 0;  // ncclDataType_t / ncclRedOp_t values
+
+// smallest padded layer (bytes per sample and channel group) sent without packing
+// (vm_set_halo_zero_copy_min).  Off by default: measured on B200 (tools/halo_ab.py, cfg3
+// 8-way rank block), one NCCL op per channel group cost more than the pack + one message +
+// unpack (sum of the forward exchanges 1961 us zero-copy vs 909 us packed)
+static long long g_zero_copy_min = 1LL << 62;
+extern "C" long long vm_set_halo_zero_copy_min(long long bytes) {
+  const long long prev = g_zero_copy_min;
+  g_zero_copy_min = bytes;
+  return prev;
+}
+
+static int g_loopback = 0;
+extern "C" void vm_debug_halo_loopback(int on) { g_loopback = on; }
 
 static bool nccl_ok() { return g_nccl.send && g_nccl.recv && g_nccl.gstart && g_nccl.gend && g_nccl.allreduce; }
 
@@ -193,6 +212,28 @@ extern "C" int vm_halo_slab_fwd(void* comm, int dtype, void* slab, int64_t bstri
     if (lo < 0 && hi < 0) continue;
     VM_REQUIRE(comm, VM_E_ARG, "vm_halo_slab_fwd: neighbours given without a communicator");
     VM_REQUIRE(nccl_ok() || vm_nccl_bind() == VM_OK, VM_E_UNSUPPORTED, "vm_halo_slab_fwd: NCCL not bound");
+    if (a == 0 && base.plane_b / (D + 2) >= g_zero_copy_min) {
+      // Depth phase, zero copy: every (sample, channel group)'s padded layer is one contiguous
+      // run, sent from layer 1 / D and received straight into margin layer 0 / D+1.  The layer's
+      // own H/W margins travel too: at a global boundary they are zero on both ranks, and on a
+      // side with a neighbour the later H / W phases overwrite them (their boxes span the
+      // depth margins), so the slab ends up identical to the packed protocol's; the bytes
+      // exceed exchange_byte_count's face by (H+2)(W+2)/(HW).
+      const size_t lb = (size_t)(base.plane_b / (D + 2));
+      uint8_t* s8 = static_cast<uint8_t*>(slab);
+      NCCL_CHECK(g_nccl.gstart(), "ncclGroupStart");
+      for (int b = 0; b < B; ++b)
+        for (int cg = 0; cg < base.CG; ++cg) {
+          uint8_t* p = s8 + b * base.bstride_b + cg * base.plane_b;
+          if (hi >= 0) NCCL_CHECK(g_nccl.send(p + (size_t)D * lb, lb, kNcclUint8, hi, comm, st), "ncclSend");
+          if (lo >= 0) NCCL_CHECK(g_nccl.send(p + lb, lb, kNcclUint8, lo, comm, st), "ncclSend");
+          if (lo >= 0) NCCL_CHECK(g_nccl.recv(p, lb, kNcclUint8, lo, comm, st), "ncclRecv");
+          if (hi >= 0) NCCL_CHECK(g_nccl.recv(p + (size_t)(D + 1) * lb, lb, kNcclUint8, hi, comm, st), "ncclRecv");
+        }
+      NCCL_CHECK(g_nccl.gend(), "ncclGroupEnd");
+      if (bytes_sent) *bytes_sent += (long long)lb * B * base.CG * ((lo >= 0) + (hi >= 0));
+      continue;
+    }
     FaceSet pk = base, up = base;
     pk.n = up.n = 0;
     if (lo >= 0) pk.f[pk.n++] = Face{a, 1, 0, s_down};
@@ -200,12 +241,19 @@ extern "C" int vm_halo_slab_fwd(void* comm, int dtype, void* slab, int64_t bstri
     const size_t bytes = (size_t)face_bytes(base, Face{a, 1, 0, nullptr});
     int rc = launch_faces(true, slab, pk, st);
     if (rc) return rc;
+    if (g_loopback) {  // A/B probe: the periodic self-exchange as device copies instead of NCCL
+      if (lo >= 0 && hi >= 0) {
+        cudaMemcpyAsync(r_lo, s_up, bytes, cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(r_hi, s_down, bytes, cudaMemcpyDeviceToDevice, st);
+      }
+    } else {
     NCCL_CHECK(g_nccl.gstart(), "ncclGroupStart");
     if (hi >= 0) NCCL_CHECK(g_nccl.send(s_up, bytes, kNcclUint8, hi, comm, st), "ncclSend");
     if (lo >= 0) NCCL_CHECK(g_nccl.send(s_down, bytes, kNcclUint8, lo, comm, st), "ncclSend");
     if (lo >= 0) NCCL_CHECK(g_nccl.recv(r_lo, bytes, kNcclUint8, lo, comm, st), "ncclRecv");
     if (hi >= 0) NCCL_CHECK(g_nccl.recv(r_hi, bytes, kNcclUint8, hi, comm, st), "ncclRecv");
     NCCL_CHECK(g_nccl.gend(), "ncclGroupEnd");
+    }
     if (lo >= 0) up.f[up.n++] = Face{a, 0, 0, r_lo};
     if (hi >= 0) up.f[up.n++] = Face{a, n[a] + 1, 0, r_hi};
     rc = launch_faces(false, slab, up, st);

@@ -147,7 +147,8 @@ class UNetStep:
         # overlap the exchange with the conv's interior planes: only the depth axis is split
         # (cfg3); the interior output planes [1, D-1) read no margin plane
         self.overlap_halo = True
-        self.overlap_min_planes = 8
+        self.overlap_min_planes = 32  # tools/halo_ab.py: the boundary launches cost more below
+        self.halo_sm_reserve = 8  # SMs the interior conv leaves to the overlapped exchange
         self.bucket_bytes = 16 << 20
         bdiv = mesh.axis_size(layout.axis_for("batch")) if (layout is not None and layout.axis_for("batch")) else 1
         self.global_batch = global_batch or batch * bdiv
@@ -475,6 +476,11 @@ class UNetStep:
     def graph_capturable(self):
         return self.ctx is None or self.ctx.mesh.worker_count == 1 or self.comm is not None
 
+    def _sm_budget(self):
+        if getattr(self, "_nsm", None) is None:
+            self._nsm = int(_lib.load().vm_num_sms(self.device.index or 0))
+        return max(1, self._nsm - self.halo_sm_reserve)
+
     def _comm_stream(self):
         if getattr(self, "_cstream", None) is None:
             self._cstream = torch.cuda.Stream(device=self.device)
@@ -496,7 +502,12 @@ class UNetStep:
         comm = self._comm_stream()
         ready = torch.cuda.Event()
         ready.record(main)
-        self._conv(x, L, y, flags, mask=mask, dgrad=dgrad, planes=(1, L.D - 2))
+        lib = _lib.load()
+        prev = lib.vm_set_conv_sm_limit(self._sm_budget())  # leave SMs to the exchange kernels
+        try:
+            self._conv(x, L, y, flags, mask=mask, dgrad=dgrad, planes=(1, L.D - 2))
+        finally:
+            lib.vm_set_conv_sm_limit(prev)
         comm.wait_event(ready)
         with torch.cuda.stream(comm):
             self._halo(x, tag)

@@ -58,6 +58,7 @@ def test_partitioned_step_matches_unpartitioned(axes, layout):
 
     def work(ctx, im, lb):
         st = UNetStep(g, params, ctx=ctx, dtype=torch.bfloat16, global_shape=(E, E, E), local_shape=loc)
+        st.overlap_min_planes = 8  # exercise the interior/boundary plane split (host transport)
         st.upload(im, lb)
         st.forward()
         st.backward()

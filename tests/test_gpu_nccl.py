@@ -60,10 +60,26 @@ def _padded(s):
     return v.permute(0, 2, 3, 4, 1, 5).reshape(s.B, s.D + 2, s.H + 2, s.W + 2, s.CG * 8).double().cpu().numpy()
 
 
+@pytest.fixture
+def zero_copy_min():
+    """Set the depth phase's zero-copy threshold for one test (0: always zero copy)."""
+    lib = _lib.load()
+    saved = []
+
+    def set_(v):
+        saved.append(lib.vm_set_halo_zero_copy_min(v))
+
+    yield set_
+    for v in saved[:1]:
+        lib.vm_set_halo_zero_copy_min(v)
+
+
+@pytest.mark.parametrize("zero_copy", [False, True])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
 @pytest.mark.parametrize("dims", [(0,), (0, 1, 2), (1, 2)])
-def test_periodic_slab_halo_equals_wrap_padding(comms, dtype, dims):
+def test_periodic_slab_halo_equals_wrap_padding(comms, zero_copy_min, dtype, dims, zero_copy):
     comm, _ = comms
+    zero_copy_min(0 if zero_copy else 1 << 40)
     B, D, H, W, C = 2, 5, 6, 7, 20
     x = O.bf16_round(np.random.default_rng(3).standard_normal((B, D, H, W, C)).astype(np.float32))
     s = _slab(x, dtype)
@@ -87,6 +103,8 @@ def test_periodic_slab_halo_equals_wrap_padding(comms, dtype, dims):
     want = cur
     assert np.array_equal(_padded(s), want)
     faces = sum(2 * _lib.load().vm_halo_slab_face_bytes(_lib.dtype_code(dtype), B, C, D, H, W, a) for a in dims)
+    if zero_copy and 0 in dims:  # the depth layers travel whole (padded H x W)
+        faces += 2 * B * s.CG * ((H + 2) * (W + 2) - H * W) * 8 * s.storage.element_size()
     assert sent.value == faces
     _lib.call("vm_halo_slab_zero", _lib.dtype_code(dtype), s.p(), s.bstride, B, C, D, H, W, (ctypes.c_int * 6)(*nbr),
               _lib.stream_ptr())
@@ -117,7 +135,7 @@ def _emulated_step(comms, params, graph, overlap):
     return st
 
 
-def test_nccl_step_overlap_buckets_and_graph_are_bitwise(comms):
+def test_nccl_step_overlap_buckets_and_graph_are_bitwise(comms, zero_copy_min):
     E = 32
     cfg = vm.UNetConfig(E, (16, 32), convs_per_block=2)
     mesh = vm.create_mesh([("one", 1)])
@@ -126,8 +144,11 @@ def test_nccl_step_overlap_buckets_and_graph_are_bitwise(comms):
     img, lab = O.record_for(E, 4)
     host = (torch.from_numpy(img[None, ..., None].copy()), torch.from_numpy(lab[None].copy()))
     runs = {}
-    for name, overlap in (("split", True), ("plain", False)):
+    lib = _lib.load()
+    for name, overlap, zc in (("split", True, 1 << 40), ("plain", False, 1 << 40), ("zero-copy", True, 0)):
+        zero_copy_min(zc)
         st = _emulated_step(comms, params, graph, overlap)
+        st.overlap_min_planes = 8
         assert st.has_halo and st._split_planes(32) == overlap
         st.keep_probs = True
         st.upload(*host)
@@ -136,12 +157,14 @@ def test_nccl_step_overlap_buckets_and_graph_are_bitwise(comms):
         torch.cuda.synchronize()
         assert len(st._grad_buckets()) > 1 and st._grads_reduced
         runs[name] = (st.probs.cpu(), st.stats.cpu(), st.grads.cpu())
-    for a, b in zip(runs["split"], runs["plain"]):
-        assert torch.equal(a, b)
+    for other in ("plain", "zero-copy"):
+        for a, b in zip(runs["split"], runs[other]):
+            assert torch.equal(a, b), other
     # the whole step (halos, stats all-reduce, gradient buckets, SGD) in one CUDA graph
     eager = _emulated_step(comms, params, graph, True)
     capt = _emulated_step(comms, params, graph, True)
     for st in (eager, capt):
+        st.overlap_min_planes = 8
         st.upload(*host)
     g = capt.capture()
     assert g is not None
