@@ -235,6 +235,24 @@ int vm_head_bwd(int dtype, const void* y, int64_t y_bstride, const float* w, con
                 float w_ce, float total_voxels, int dice_mask, float clamp, int relu_mask,
                 void* stream);
 
+/* head backward from a given dL/dprobs [B][D][H][W][ncls] f32 (worker-level API:
+ * unet.run_backward_local fed by training.loss_grad_local) */
+int vm_head_bwd_dprobs(int dtype, const void* y, int64_t y_bstride, const float* w, const float* b,
+                       const float* dprobs, void* g, int64_t g_bstride, float* wpartials, int B, int C, int ncls,
+                       int D, int H, int W, int relu_mask, void* stream);
+
+/* ------------------------------------------------------------------ dense (row-major [rows, C]) ops
+ * the per-op / worker-level API's kernels (dense.cu): channel softmax (ops.py:190-194), channel
+ * concat (ops.py:313-323), loss statistics in f64 (training.py:77-92; ws = 2*148*(3C+1)
+ * doubles) and the per-voxel loss gradient (training.py:110-127). */
+int vm_softmax_rows(int dtype, const void* x, void* y, int64_t rows, int C, void* stream);
+int vm_concat_rows(const void* a, int64_t a_row_bytes, const void* b, int64_t b_row_bytes, void* out, int64_t rows,
+                   void* stream);
+int vm_loss_stats(const float* probs, const float* onehot, int64_t rows, int C, float clamp, double* ws,
+                  double* stats, void* stream);
+int vm_loss_grad(const float* probs, const float* onehot, const double* stats, int64_t rows, int C, float w_dice,
+                 float w_ce, double total, int dice_mask, float clamp, float* out, void* stream);
+
 /* ------------------------------------------------------------------ optimizer
  * Parameters, moments and gradients of all layers live in three flat fp32
  * buffers; layer l owns [offsets[l], offsets[l+1]) (kernel then bias).

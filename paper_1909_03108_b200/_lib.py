@@ -77,6 +77,11 @@ _SIGS = {
     "vm_reduce_rows": (_I, [_P, _I, _I, _P, _P]),
     "vm_label_counts": (_I, [_P, _P, _L, _I, _P, _P]),
     "vm_head_bwd": (_I, [_I, _P, _L, _P, _P, _P, _P, _P, _L, _P, _I, _I, _I, _I, _I, _I, _F, _F, _F, _I, _F, _I, _P]),
+    "vm_head_bwd_dprobs": (_I, [_I, _P, _L, _P, _P, _P, _P, _L, _P, _I, _I, _I, _I, _I, _I, _I, _P]),
+    "vm_softmax_rows": (_I, [_I, _P, _P, _L, _I, _P]),
+    "vm_concat_rows": (_I, [_P, _L, _P, _L, _P, _L, _P]),
+    "vm_loss_stats": (_I, [_P, _P, _L, _I, _F, _P, _P, _P]),
+    "vm_loss_grad": (_I, [_P, _P, _P, _L, _I, _F, _F, ctypes.c_double, _I, _F, _P, _P]),
     "vm_sgd_momentum": (_I, [_P, _P, _P, _P, _I, _L, _P, _F, _F, _P]),
     "vm_nccl_bind": (_I, []),
     "vm_halo_slab_ws_bytes": (_S, [_I, _I, _I, _I, _I, _I]),

@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_head_bwd(
     const T* __restrict__ y, Slab sy, const float* __restrict__ W, const float* __restrict__ bias,
     const uint8_t* __restrict__ labels, const float* __restrict__ stats, T* __restrict__ g, Slab sg,
     float* __restrict__ wpart, int B, int C, int ncls, float w_dice, float w_ce, float total,
-    int dice_mask, float clamp, int relu_mask) {
+    int dice_mask, float clamp, int relu_mask, const float* __restrict__ dprobs) {
   extern __shared__ float sh[];
   float* sW = sh;
   float* sb = sW + C * ncls;
@@ -327,8 +327,8 @@ __global__ void __launch_bounds__(kHeadThreads) k_head_bwd(
     int nfg = __popc(dice_mask);
     for (int k = 0; k < ncls; ++k) {
       // training.py:119-124 — grad_k += (-w_d/nfg) * (2 g_k - r_k) / d_k
-      float nk = 2.f * stats[k] + 1e-6f;
-      float dk = stats[ncls + k] + stats[2 * ncls + k] + 1e-6f;
+      float nk = stats ? 2.f * stats[k] + 1e-6f : 1.f;
+      float dk = stats ? stats[ncls + k] + stats[2 * ncls + k] + 1e-6f : 1.f;
       bool on = (dice_mask >> k) & 1;
       coef[3 * k + 0] = on ? (-w_dice / (float)nfg) / dk : 0.f;
       coef[3 * k + 1] = on ? nk / dk : 0.f;
@@ -355,10 +355,11 @@ __global__ void __launch_bounds__(kHeadThreads) k_head_bwd(
       softmax_n(lg, ncls, p);
       float dot = 0.f;
       for (int k = 0; k < ncls; ++k) {
-        const float gk = labels[v] == k ? 1.f : 0.f;
+        const float gk = labels && labels[v] == k ? 1.f : 0.f;
         float r = coef[3 * k + 2] != 0.f ? coef[3 * k] * (2.f * gk - coef[3 * k + 1]) : 0.f;
         float pm = fmaxf(p[k], clamp);
         r += p[k] >= clamp ? ce_scale * (gk / pm) : 0.f;  // training.py:125-126
+        if (dprobs) r = dprobs[v * ncls + k];  // external dL/dp (run_backward_local)
         gp[k] = r;
         dot += r * p[k];
       }
@@ -496,8 +497,8 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_fixed(
   if (threadIdx.x == 0) {
     const int nfg = __popc(dice_mask);
     for (int k = 0; k < NC; ++k) {  // training.py:119-124
-      const float nk = 2.f * stats[k] + 1e-6f;
-      const float dk = stats[NC + k] + stats[2 * NC + k] + 1e-6f;
+      const float nk = stats ? 2.f * stats[k] + 1e-6f : 1.f;
+      const float dk = stats ? stats[NC + k] + stats[2 * NC + k] + 1e-6f : 1.f;
       const bool on = (dice_mask >> k) & 1;
       coef[3 * k + 0] = on ? (-w_dice / (float)nfg) / dk : 0.f;
       coef[3 * k + 1] = on ? nk / dk : 0.f;
@@ -590,7 +591,7 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_grp(
     const T* __restrict__ y, Slab sy, const float* __restrict__ W, const float* __restrict__ bias,
     const uint8_t* __restrict__ labels, const float* __restrict__ stats, T* __restrict__ g, Slab sg,
     float* __restrict__ wpart, int B, float w_dice, float w_ce, float total, int dice_mask, float clamp,
-    int relu_mask) {
+    int relu_mask, const float* __restrict__ dprobs) {
   pdl_wait();
   constexpr int TPV = C / 8;
   constexpr int NACC = 8 * NC + NC;  // group's weight grads + bias grads (used by cg == 0)
@@ -602,8 +603,8 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_grp(
   if (threadIdx.x == 0) {
     const int nfg = __popc(dice_mask);
     for (int k = 0; k < NC; ++k) {  // training.py:119-124
-      const float nk = 2.f * stats[k] + 1e-6f;
-      const float dk = stats[NC + k] + stats[2 * NC + k] + 1e-6f;
+      const float nk = stats ? 2.f * stats[k] + 1e-6f : 1.f;
+      const float dk = stats ? stats[NC + k] + stats[2 * NC + k] + 1e-6f : 1.f;
       const bool on = (dice_mask >> k) & 1;
       coef[3 * k + 0] = on ? (-w_dice / (float)nfg) / dk : 0.f;
       coef[3 * k + 1] = on ? nk / dk : 0.f;
@@ -641,7 +642,7 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_grp(
       V8<T>::ld(y + sy.at(b, cg, d, h, w), yv[u]);
       go[u] = sg.at(b, cg, d, h, w);
 #pragma unroll
-      for (int k = 0; k < NC; ++k) gk[u][k] = labels[v] == k ? 1.f : 0.f;
+      for (int k = 0; k < NC; ++k) gk[u][k] = labels && labels[v] == k ? 1.f : 0.f;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -673,6 +674,7 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_grp(
         // g / max(p, clamp) with the correctly rounded reciprocal: exact for one-hot g in {0, 1}
         // and no division slow path (FCHK + branches showed in the stall profile)
         r += p[k] >= clamp ? ce_scale * (gk[u][k] * __frcp_rn(fmaxf(p[k], clamp))) : 0.f;  // training.py:125-126
+        if (dprobs) r = ok[u] ? dprobs[(size_t)((gi0 + u * stride) / TPV) * NC + k] : 0.f;  // external dL/dp
         gp[k] = r;
         dot += r * p[k];
       }
@@ -1006,12 +1008,37 @@ extern "C" int vm_reduce_rows(const float* partials, int rows, int width, float*
   return launch_status("vm_reduce_rows");
 }
 
+static int head_bwd(int dtype, const void* y, int64_t y_bstride, const float* w, const float* b,
+                    const uint8_t* labels, const float* stats, void* g, int64_t g_bstride, float* wpartials, int B,
+                    int C, int ncls, int D, int H, int W, float w_dice, float w_ce, float total_voxels,
+                    int dice_mask, float clamp, int relu_mask, const float* dprobs, void* stream);
+
 extern "C" int vm_head_bwd(int dtype, const void* y, int64_t y_bstride, const float* w,
                            const float* b, const uint8_t* labels, const float* stats, void* g,
                            int64_t g_bstride, float* wpartials, int B, int C, int ncls, int D,
                            int H, int W, float w_dice, float w_ce, float total_voxels,
                            int dice_mask, float clamp, int relu_mask, void* stream) {
-  VM_REQUIRE(y && w && b && labels && stats && g && wpartials, VM_E_ARG, "vm_head_bwd: null pointer");
+  VM_REQUIRE(labels && stats, VM_E_ARG, "vm_head_bwd: null pointer");
+  return head_bwd(dtype, y, y_bstride, w, b, labels, stats, g, g_bstride, wpartials, B, C, ncls, D, H, W, w_dice,
+                  w_ce, total_voxels, dice_mask, clamp, relu_mask, nullptr, stream);
+}
+
+// Head backward from a given dL/dprobs [B][D][H][W][ncls] (f32): softmax backward + head dgrad
+// (masked) + head-weight partials, for the worker-level API (unet.run_backward_local fed by
+// training.loss_grad_local, unet.py:376-442).
+extern "C" int vm_head_bwd_dprobs(int dtype, const void* y, int64_t y_bstride, const float* w, const float* b,
+                                  const float* dprobs, void* g, int64_t g_bstride, float* wpartials, int B, int C,
+                                  int ncls, int D, int H, int W, int relu_mask, void* stream) {
+  VM_REQUIRE(dprobs, VM_E_ARG, "vm_head_bwd_dprobs: null dprobs");
+  return head_bwd(dtype, y, y_bstride, w, b, nullptr, nullptr, g, g_bstride, wpartials, B, C, ncls, D, H, W, 0.f,
+                  0.f, 1.f, 0, 0.f, relu_mask, dprobs, stream);
+}
+
+static int head_bwd(int dtype, const void* y, int64_t y_bstride, const float* w, const float* b,
+                    const uint8_t* labels, const float* stats, void* g, int64_t g_bstride, float* wpartials, int B,
+                    int C, int ncls, int D, int H, int W, float w_dice, float w_ce, float total_voxels,
+                    int dice_mask, float clamp, int relu_mask, const float* dprobs, void* stream) {
+  VM_REQUIRE(y && w && b && g && wpartials, VM_E_ARG, "vm_head_bwd: null pointer");
   VM_REQUIRE(ncls > 0 && ncls <= kMaxCls, VM_E_UNSUPPORTED, "vm_head_bwd: ncls %d", ncls);
   VM_REQUIRE((int64_t)B * D * H * W < (1LL << 32), VM_E_SHAPE, "vm_head_bwd: voxel count exceeds 2^32");
   Slab sy = SLAB(y_bstride, C, D, H, W), sg = SLAB(g_bstride, C, D, H, W);
@@ -1023,7 +1050,7 @@ extern "C" int vm_head_bwd(int dtype, const void* y, int64_t y_bstride, const fl
 #define HB_CASE(CC, NN)                                                                                  \
   case NN * 1000 + CC:                                                                                   \
     launch_pdl(k_head_bwd_grp<T, CC, NN>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, labels, stats, \
-               (T*)g, sg, wpartials, B, w_dice, w_ce, total_voxels, dice_mask, clamp, relu_mask);          \
+               (T*)g, sg, wpartials, B, w_dice, w_ce, total_voxels, dice_mask, clamp, relu_mask, dprobs);          \
     return launch_status("vm_head_bwd");
 #define HB_ROW(NN) HB_CASE(8, NN) HB_CASE(16, NN) HB_CASE(32, NN) HB_CASE(64, NN) HB_CASE(128, NN)
     switch (ncls * 1000 + C) {
@@ -1039,7 +1066,7 @@ extern "C" int vm_head_bwd(int dtype, const void* y, int64_t y_bstride, const fl
   DISPATCH_T(dtype, "vm_head_bwd",
              k_head_bwd<T><<<grid, kHeadThreads, sh, as_stream(stream)>>>(
                  (const T*)y, sy, w, b, labels, stats, (T*)g, sg, wpartials, B, C, ncls, w_dice,
-                 w_ce, total_voxels, dice_mask, clamp, relu_mask));
+                 w_ce, total_voxels, dice_mask, clamp, relu_mask, dprobs));
   return launch_status("vm_head_bwd");
 }
 

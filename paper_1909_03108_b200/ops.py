@@ -14,8 +14,8 @@ channel-blocked padded slabs for the kernels and back.
   with flipped, transposed taps (`ops.py:100-114` is its adjoint form: the same sum, in
   another order), so ``conv3d_backward`` exchanges the gradient forward instead of running
   ``exchange_backward_local`` on a padded gradient.
-* ``softmax_channels`` uses torch's softmax.  The train step fuses softmax into the head
-  kernel (``vm_head_fwd``), so this op is off the hot path.
+* ``softmax_channels`` / ``concat_channels`` run the row kernels of csrc/dense.cu; the train
+  step itself fuses softmax into the head kernel and makes the concat zero-copy.
 """
 
 from __future__ import annotations
@@ -292,12 +292,23 @@ def upsample2_backward(gout: ShardedTensor):
 
 
 def concat_channels(a: ShardedTensor, b: ShardedTensor):
-    """[a, b] along channels (unet.py:215, ops.py:313-323)."""
+    """[a, b] along channels (unet.py:215, ops.py:313-323) through ``vm_concat_rows``."""
     import torch
 
     if a.spec.shape[:-1] != b.spec.shape[:-1] or a.layout.assignments != b.layout.assignments:
         raise VoxmeshError(f"concat needs matching spatial shape and layout: {a.spec.shape} vs {b.spec.shape}")
-    res = a.mesh.run(lambda ctx, x, y: torch.cat([x, y], dim=-1), per_worker=(a.blocks, b.blocks))
+    if a.spec.dtype != b.spec.dtype:
+        raise VoxmeshError(f"concat needs one dtype, got {a.spec.dtype} and {b.spec.dtype}")
+
+    def fn(ctx, x, y):
+        x, y = x.contiguous(), y.contiguous()
+        out = torch.empty(tuple(x.shape[:-1]) + (x.shape[-1] + y.shape[-1],), dtype=x.dtype, device=x.device)
+        rows = x.numel() // x.shape[-1]
+        _lib.call("vm_concat_rows", _lib.ptr(x), x.shape[-1] * x.element_size(), _lib.ptr(y),
+                  y.shape[-1] * y.element_size(), _lib.ptr(out), rows, _lib.stream_ptr())
+        return out
+
+    res = a.mesh.run(fn, per_worker=(a.blocks, b.blocks))
     c_out = a.spec.extent("c") + b.spec.extent("c")
     return ShardedTensor(_out_spec(a, c_out=c_out), a.layout, a.mesh, res)
 
@@ -329,8 +340,14 @@ def relu_backward(gout: ShardedTensor, x: ShardedTensor):
 
 
 def softmax_channels(x: ShardedTensor):
-    """Channel softmax (ops.py:190-194, :331-333), torch's implementation (off the hot path)."""
+    """Stable channel softmax (ops.py:190-194, :331-333) through ``vm_softmax_rows``."""
     import torch
 
-    res = _run_blocks(x, lambda ctx, b: torch.softmax(b.float(), dim=-1).to(b.dtype))
-    return ShardedTensor(x.spec, x.layout, x.mesh, res)
+    def fn(ctx, b):
+        b = b.contiguous()
+        out = torch.empty_like(b)
+        _lib.call("vm_softmax_rows", _vm_dtype(b), _lib.ptr(b), _lib.ptr(out), b.numel() // b.shape[-1], b.shape[-1],
+                  _lib.stream_ptr())
+        return out
+
+    return ShardedTensor(x.spec, x.layout, x.mesh, _run_blocks(x, fn))

@@ -783,24 +783,32 @@ class UNetStep:
             if red is not self.stats:
                 self.stats.copy_(red)
 
-    def backward(self):
+    def backward(self, dprobs=None):
+        """Backward of the step's loss; ``dprobs`` (device f32 [B,D,H,W,ncls]) replaces the
+        loss gradient with a given dL/dprobs (the worker-level API, unet.run_backward_local)."""
         prev = _lib.load().vm_set_pdl(int(self.pdl_backward))
         try:
-            self._backward_nodes()
+            self._backward_nodes(dprobs)
         finally:
             _lib.load().vm_set_pdl(prev)
 
-    def _backward_nodes(self):
+    def _backward_nodes(self, dprobs=None):
         h = self.head
         y = self.out[self.head_in]
         last = self.graph.node(self.head_in)
         last_conv = last.inputs[0] if last.op == "relu" else last.id
         g = self.gpre[last_conv]
         nb = 4.0 * self.nvox * h.cin + 1.0 * self.nvox
-        self._k("head_bwd", "head", 4.0 * self.nvox * h.cin * self.ncls, nb, "vm_head_bwd", self.dt, y.p(),
-                y.bstride, _lib.ptr(h.w), _lib.ptr(h.b), _lib.ptr(self.labels), _lib.ptr(self.stats), g.p(), g.bstride,
-                _lib.ptr(self.hpartials), self.B, h.cin, self.ncls, h.D, h.H, h.W, self.w_dice, self.w_ce,
-                self.total_voxels, self.dice_mask, self.clamp, 1)
+        if dprobs is not None:
+            dp = dprobs.contiguous().float()
+            self._k("head_bwd", "head", 4.0 * self.nvox * h.cin * self.ncls, nb, "vm_head_bwd_dprobs", self.dt, y.p(),
+                    y.bstride, _lib.ptr(h.w), _lib.ptr(h.b), _lib.ptr(dp), g.p(), g.bstride, _lib.ptr(self.hpartials),
+                    self.B, h.cin, self.ncls, h.D, h.H, h.W, 1)
+        else:
+            self._k("head_bwd", "head", 4.0 * self.nvox * h.cin * self.ncls, nb, "vm_head_bwd", self.dt, y.p(),
+                    y.bstride, _lib.ptr(h.w), _lib.ptr(h.b), _lib.ptr(self.labels), _lib.ptr(self.stats), g.p(),
+                    g.bstride, _lib.ptr(self.hpartials), self.B, h.cin, self.ncls, h.D, h.H, h.W, self.w_dice,
+                    self.w_ce, self.total_voxels, self.dice_mask, self.clamp, 1)
         self._k("reduce", "head", 0, 0, "vm_reduce_rows", _lib.ptr(self.hpartials), self.n_part, self.hw_width,
                 _lib.ptr(self.hgrad))
         # head grads: [C*ncls] kernel (DHWIO with k=1) then [ncls] bias — contiguous in the flat buffer

@@ -87,16 +87,115 @@ def one_hot(labels, num_classes, dtype=np.float32):
     return np.eye(num_classes, dtype=dtype)[labels]
 
 
-def _loss_stats_block(p, g, clamp):
-    """Per-class [sum p*g, sum p, sum g] plus the summed NLL of one device block, accumulated
-    in float64 on the GPU (training.py:77-92)."""
+def _dev(a):
+    """(device f32 tensor, was_numpy) of an array or tensor (the GPU loss kernels' operand)."""
     import torch
 
-    c = p.shape[-1]
-    pd = p.reshape(-1, c).double()
-    gd = g.reshape(-1, c).double()
-    nll = -(torch.log(torch.clamp_min(pd, clamp)) * gd).sum()
-    return torch.cat([(pd * gd).sum(0), pd.sum(0), gd.sum(0), nll[None]]).cpu().numpy()
+    if isinstance(a, torch.Tensor) and a.is_cuda:
+        return a.contiguous().float(), False
+    return torch.as_tensor(np.asarray(a, dtype=np.float32)).cuda(), True
+
+
+def _loss_stats_block(p, g, clamp):
+    """Per-class [sum p*g, sum p, sum g] plus the summed NLL of one device block (training.py
+    :77-92), on the GPU (vm_loss_stats: float64 block partials, fixed-order reduction)."""
+    import torch
+
+    from . import _lib
+
+    pd, _ = _dev(p)
+    gd, _ = _dev(g)
+    c = pd.shape[-1]
+    rows = pd.numel() // c
+    ws = torch.empty(2 * 148 * (3 * c + 1), dtype=torch.float64, device=pd.device)
+    out = torch.empty(3 * c + 1, dtype=torch.float64, device=pd.device)
+    _lib.call("vm_loss_stats", _lib.ptr(pd), _lib.ptr(gd), rows, c, float(clamp), _lib.ptr(ws), _lib.ptr(out),
+              _lib.stream_ptr())
+    return out.cpu().numpy()
+
+
+def loss_stats_local(probs, onehot, clamp=1e-12):
+    """Worker-level statistics of the local block (training.py:77-92) on the GPU."""
+    return _loss_stats_block(probs, onehot, clamp)
+
+
+@dataclass(frozen=True)
+class _RunCtx:
+    """The constants a step needs on the worker side (training.py:53-65)."""
+
+    num_classes: int
+    dice_classes: tuple
+    w_dice: float
+    w_ce: float
+    clamp: float
+    total_batch_voxels: int
+    lr: float = 0.003
+    momentum: float = 0.9
+    phase_barrier: bool = True
+    param_order: tuple = ()
+
+
+def losses_from_stats(stats, rc):
+    """(combined, dice, ce) from reduced statistics (training.py:103-107)."""
+    dice = soft_dice_from_stats(stats, rc.num_classes, rc.dice_classes)
+    ce = float(stats[3 * rc.num_classes]) / rc.total_batch_voxels
+    return rc.w_dice * dice + rc.w_ce * ce, dice, ce
+
+
+def loss_grad_local(probs, onehot, stats, rc):
+    """dL/dprobs of the combined loss per voxel from the globally reduced statistics
+    (training.py:110-127), on the GPU (vm_loss_grad); numpy in, numpy out."""
+    import torch
+
+    from . import _lib
+
+    pd, was_np = _dev(probs)
+    gd, _ = _dev(onehot)
+    st = torch.as_tensor(np.asarray(stats, dtype=np.float64)).to(pd.device)
+    c = pd.shape[-1]
+    out = torch.empty_like(pd)
+    mask = sum(1 << k for k in rc.dice_classes)
+    _lib.call("vm_loss_grad", _lib.ptr(pd), _lib.ptr(gd), _lib.ptr(st), pd.numel() // c, c, float(rc.w_dice),
+              float(rc.w_ce), float(rc.total_batch_voxels), mask, float(rc.clamp), _lib.ptr(out), _lib.stream_ptr())
+    if was_np:
+        return out.cpu().numpy().astype(np.asarray(probs).dtype)
+    return out
+
+
+def sgd_momentum_step(params, moments, grads, lr, momentum, order):
+    """v <- momentum*v + g; p <- p - lr*v per parameter blob, in ``order``; layers with
+    non-finite gradients are skipped and returned (training.py:202-219).  In place on the
+    reference-layout dicts, through the step's fused kernel (vm_sgd_momentum, numpy's fp32
+    operation order, so the results are bitwise numpy's)."""
+    import torch
+
+    from . import _lib
+
+    keys = [(nid, k) for nid in order for k in ("kernel", "bias")]
+    offs = [0]
+    for nid, k in keys:
+        offs.append(offs[-1] + int(np.asarray(params[nid][k]).size))
+    flat = {}
+    for name, store in (("p", params), ("v", moments)):
+        flat[name] = torch.cat([torch.as_tensor(np.asarray(store[nid][k], np.float32)).reshape(-1)
+                                for nid, k in keys]).cuda()
+    flat["g"] = torch.cat([torch.as_tensor(np.asarray(grads[nid][0 if k == "kernel" else 1], np.float32)).reshape(-1)
+                           for nid, k in keys]).cuda()
+    # layers = (kernel, bias) pairs: one skip decision per layer (training.py:210-213)
+    loffs = torch.tensor(offs[::2], dtype=torch.int64).cuda()
+    nl = len(order)
+    flags = torch.zeros(nl, dtype=torch.int32).cuda()
+    most = max(b - a for a, b in zip(offs[::2], offs[2::2])) if nl else 0
+    _lib.call("vm_sgd_momentum", _lib.ptr(flat["p"]), _lib.ptr(flat["v"]), _lib.ptr(flat["g"]), _lib.ptr(loffs), nl,
+              most, _lib.ptr(flags), float(lr), float(momentum), _lib.stream_ptr())
+    fl = flags.cpu().numpy()
+    hp, hv = flat["p"].cpu().numpy(), flat["v"].cpu().numpy()
+    for i, (nid, k) in enumerate(keys):
+        a, b = offs[i], offs[i + 1]
+        shape = np.asarray(params[nid][k]).shape
+        params[nid][k][...] = hp[a:b].reshape(shape)
+        moments[nid][k][...] = hv[a:b].reshape(shape)
+    return [nid for nid, f in zip(order, fl) if f]
 
 
 def soft_dice_from_stats(stats, num_classes, dice_classes, eps=DICE_EPS):

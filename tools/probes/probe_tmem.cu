@@ -16,12 +16,16 @@ __global__ void k_ld(int iters, int nwarps_active, long long* cyc, float* sink) 
   long long t0 = clock64();
   if (warp < nwarps_active) {
     const int q = warp & 3;
-    for (int it = 0; it < iters; ++it) {
-      uint32_t r[16];
-      vm::tmem_ld16(t + ((uint32_t)(q * 32) << 16) + (uint32_t)((it * 16) & 511), r);
+    for (int it = 0; it < iters; it += 4) {
+      uint32_t r[4][16];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        vm::tmem_ld16(t + ((uint32_t)(q * 32) << 16) + (uint32_t)(((it + j) * 16) & 511), r[j]);
       vm::tmem_ld_wait();
 #pragma unroll
-      for (int e = 0; e < 16; ++e) acc += __uint_as_float(r[e]);
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) acc += __uint_as_float(r[j][e]);
     }
   }
   __syncthreads();
