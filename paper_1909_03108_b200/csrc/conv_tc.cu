@@ -2142,9 +2142,10 @@ static bool plan_wgrad_kd(int B, int Cin, int Cout, int D, int H, int W, WkParam
   if (g_force_mpu > 0 && g_force_mpu < p.mt_per_unit) p.mt_per_unit = g_force_mpu;  // A/B probes
   while (p.mt_per_unit > 1 && p.MT % p.mt_per_unit) --p.mt_per_unit;  // equal groups (kernel template)
   if (p.mt_per_unit < 1) return false;
-  p.g_bytes = (uint32_t)(p.Nc / 8) * p.KS * 16;
-  p.g_load = (uint32_t)p.CGo * p.KS * 16;
+  if (g_force_ks >= 32 && g_force_ks % 16 == 0 && g_force_ks < p.KS) p.KS = g_force_ks;  // A/B probes
   for (;;) {
+    p.g_bytes = (uint32_t)(p.Nc / 8) * p.KS * 16;
+    p.g_load = (uint32_t)p.CGo * p.KS * 16;
     // slot positions a CTA touches: its 16*mt_per_unit M slots (+ up to 2 of run alignment),
     // never more than the 3*CG run slots + the ones slot; + 1 slot of slack for the last run
     const int slots = min(16 * p.mt_per_unit + 2, 3 * p.CG + 1) + 1;
@@ -2154,8 +2155,15 @@ static bool plan_wgrad_kd(int B, int Cin, int Cout, int D, int H, int W, WkParam
     p.ksub = kSmemBudget / (int)(2 * p.sub_bytes) >= g_wk_ksub_min_stages ? 2 : 1;
     p.stage_bytes = p.ksub * p.sub_bytes;
     p.stages = kSmemBudget / (int)p.stage_bytes;
-    if (p.stages >= 2 || p.mt_per_unit == 1) break;
-    do --p.mt_per_unit; while (p.mt_per_unit > 1 && p.MT % p.mt_per_unit);
+    if (p.stages >= 2) break;
+    if (p.mt_per_unit > 1) {
+      do --p.mt_per_unit; while (p.mt_per_unit > 1 && p.MT % p.mt_per_unit);
+      continue;
+    }
+    // one M-tile per CTA and still no double buffer (wide rows x many input channel groups,
+    // e.g. the decoder's 96 -> 32 conv at 256^3): shorter K chunks shrink the gy slices
+    if (p.KS <= 32) break;
+    p.KS = max(32, (p.KS / 2) / 16 * 16);
   }
   if (p.stages < 2) return false;
   if (p.stages > kMaxStages) p.stages = kMaxStages;
@@ -2213,19 +2221,18 @@ static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_
       cudaStream_t st = as_stream(stream);
       const bool dbg = pk.dbg != nullptr;
       using WkKern = void (*)(const CUtensorMap, const WkParams);
-      // [NMT-1][variant]: 0 runtime, then (NKK, KSUB) = (2,1) (2,2) (4,1) (4,2) (8,1) (8,2)
-      static const WkKern table[3][7] = {
-          {k_conv_wgrad_kd<1, 0, 0>, k_conv_wgrad_kd<1, 2, 1>, k_conv_wgrad_kd<1, 2, 2>, k_conv_wgrad_kd<1, 4, 1>,
-           k_conv_wgrad_kd<1, 4, 2>, k_conv_wgrad_kd<1, 8, 1>, k_conv_wgrad_kd<1, 8, 2>},
-          {k_conv_wgrad_kd<2, 0, 0>, k_conv_wgrad_kd<2, 2, 1>, k_conv_wgrad_kd<2, 2, 2>, k_conv_wgrad_kd<2, 4, 1>,
-           k_conv_wgrad_kd<2, 4, 2>, k_conv_wgrad_kd<2, 8, 1>, k_conv_wgrad_kd<2, 8, 2>},
-          {k_conv_wgrad_kd<3, 0, 0>, k_conv_wgrad_kd<3, 2, 1>, k_conv_wgrad_kd<3, 2, 2>, k_conv_wgrad_kd<3, 4, 1>,
-           k_conv_wgrad_kd<3, 4, 2>, k_conv_wgrad_kd<3, 8, 1>, k_conv_wgrad_kd<3, 8, 2>},
-      };
+      // [NMT-1][variant]: 0 runtime, then (NKK, KSUB) = (2,1) (2,2) (4,1) (4,2) (8,1) (8,2) (16,1) (16,2)
+#define WK_ROW(M)                                                                                               \
+  {k_conv_wgrad_kd<M, 0, 0>, k_conv_wgrad_kd<M, 2, 1>,  k_conv_wgrad_kd<M, 2, 2>, k_conv_wgrad_kd<M, 4, 1>,     \
+   k_conv_wgrad_kd<M, 4, 2>, k_conv_wgrad_kd<M, 8, 1>,  k_conv_wgrad_kd<M, 8, 2>, k_conv_wgrad_kd<M, 16, 1>,    \
+   k_conv_wgrad_kd<M, 16, 2>}
+      static const WkKern table[3][9] = {WK_ROW(1), WK_ROW(2), WK_ROW(3)};
+#undef WK_ROW
       const int nkk = pk.KS / 16;
       int var = 0;
-      if (pk.nkw == 3 && (pk.ksub == 1 || pk.ksub == 2) && (nkk == 2 || nkk == 4 || nkk == 8) && !g_wk_runtime)
-        var = (nkk == 2 ? 1 : nkk == 4 ? 3 : 5) + (pk.ksub - 1);
+      if (pk.nkw == 3 && (pk.ksub == 1 || pk.ksub == 2) && (nkk == 2 || nkk == 4 || nkk == 8 || nkk == 16) &&
+          !g_wk_runtime)
+        var = (nkk == 2 ? 1 : nkk == 4 ? 3 : nkk == 8 ? 5 : 7) + (pk.ksub - 1);
       auto kern = table[pk.mt_per_unit - 1][var];
       (void)dbg;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);

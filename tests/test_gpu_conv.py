@@ -139,6 +139,10 @@ WG_SHAPES = [
     (2, 24, 8, 3, 5, 34),
     (1, 96, 32, 4, 4, 64),
     (1, 8, 16, 40, 4, 32),
+    # 256-wide rows: K chunks of 256 anchors (NKK = 16), and the decoder's 96 -> 32 shape whose
+    # gy slices only double-buffer at shorter K chunks
+    (1, 32, 32, 3, 2, 256),
+    (1, 96, 32, 2, 2, 256),
     # Cout 64..80: one kw tap per CTA (three accumulators of N = 3*Nc exceed TMEM)
     (1, 64, 64, 6, 6, 34),
     (1, 32, 64, 4, 8, 40),
