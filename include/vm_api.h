@@ -290,6 +290,23 @@ int vm_halo_slab_pack(int dtype, const void* slab, int64_t bstride, int B, int C
 int vm_halo_slab_unpack(int dtype, void* slab, int64_t bstride, int B, int C, int D, int H, int W,
                         int axis, const void* from_lo, const void* from_hi, void* stream);
 long long vm_halo_slab_face_bytes(int dtype, int B, int C, int D, int H, int W, int axis);
+/* Depth-phase halo of a depth-only split through peer memory instead of NCCL
+ * (halo.py:109-155 with only `x` partitioned; replaces the phase-0 leg of vm_halo_slab_fwd):
+ * one launch copies layer 1 of every (sample, channel group) into the lo neighbour's layer
+ * D+1 and layer D into the hi neighbour's layer 0 (lo_peer / hi_peer: the neighbours' slabs,
+ * mapped with vm_ipc_open, same geometry; NULL at a global boundary), then its last block
+ * publishes the step epoch into the neighbours' flag words (lo_flag = the lo neighbour's
+ * own[1], hi_flag = the hi neighbour's own[0]) and waits until own[0] / own[1] reach it.
+ * counter: one zeroed device word per exchange slot; epoch: device words {step counter, error}
+ * (the error word is set when a neighbour's signal does not arrive within ~10 s: no hang). */
+int vm_halo_depth_push(int dtype, const void* slab, int64_t bstride, int B, int C, int D, int H, int W,
+                       void* lo_peer, void* hi_peer, int* lo_flag, int* hi_flag, int* own,
+                       unsigned* counter, const int* epoch, void* stream);
+int vm_halo_epoch_bump(int* epoch, void* stream);
+/* CUDA-IPC handle (64 bytes) of the allocation holding ptr, and ptr's offset in it; open a
+ * peer's handle (mapped once per process) */
+int vm_ipc_handle(const void* ptr, void* handle64, int64_t* offset);
+int vm_ipc_open(const void* handle64, void** base);
 /* in-place sum over the communicator (mesh.py:195-233 all_reduce_sum; unet.py:434-441) */
 int vm_allreduce_f32(void* comm, float* buf, size_t n, void* stream);
 

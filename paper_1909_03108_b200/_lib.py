@@ -92,6 +92,10 @@ _SIGS = {
     "vm_halo_slab_unpack": (_I, [_I, _P, _L, _I, _I, _I, _I, _I, _I, _P, _P, _P]),
     "vm_halo_slab_face_bytes": (ctypes.c_longlong, [_I, _I, _I, _I, _I, _I, _I]),
     "vm_allreduce_f32": (_I, [_P, _P, _S, _P]),
+    "vm_halo_depth_push": (_I, [_I, _P, _L, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "vm_halo_epoch_bump": (_I, [_P, _P]),
+    "vm_ipc_handle": (_I, [_P, _P, _P]),
+    "vm_ipc_open": (_I, [_P, _P]),
     "vm_conv3d_fwd_tc_range": (_I, [_P, _L, _P, _P, _P, _L, _P, _L, _I, _I, _I, _I, _I, _I, _I, _I, _U, _P, _S,
                                     _P]),
     # SURVEY §8(b) composites (csrc/abi.cu)

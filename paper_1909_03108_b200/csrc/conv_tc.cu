@@ -1407,8 +1407,8 @@ __global__ void __launch_bounds__(192, 1)
             uint8_t* sA = smem + (size_t)stage * p.stage_bytes + (size_t)j * p.sub_bytes;
             uint8_t* sG = sA + p.a_bytes;
             const int gr0 = k0 + p.P + p.Wp + 1;
-            for (int kd = 0; kd < 3; ++kd)  // rows outside [0, Dp*P) read as zeros
-              tma_load_4d(sG + (size_t)kd * p.g_bytes, &gmap, &full[stage], 0, gr0 - kd * p.P, 0, b);
+            for (int kd = 0; kd < 3; ++kd)  // gy interior planes; other rows read as zeros
+              tma_load_4d(sG + (size_t)kd * p.g_bytes, &gmap, &full[stage], 0, gr0 - (kd + 1) * p.P, 0, b);
             for (int r = r0; r <= r_end; ++r)
               bulk_load(sA + (size_t)(r - r0) * 3 * GS, xb + r * p.plane8 + (int64_t)k0 * 8, (uint32_t)Rrun * 16,
                         &full[stage]);
@@ -2055,13 +2055,15 @@ int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
 }
 
 // 4-D gy map with 128-byte inner boxes: (64 = 8 rows x 8 ch, rows/8, CG, B)
-int make_wide_map(CUtensorMap* m, const void* base, int64_t bstride, int CG, int64_t rows, int B,
-                  int box_blocks, int box_groups) {
+// rows: rows addressable from `base` (later rows read as zeros), stride_rows: rows between
+// channel-group planes
+int make_wide_map(CUtensorMap* m, const void* base, int64_t bstride, int CG, int64_t rows, int64_t stride_rows,
+                  int B, int box_blocks, int box_groups) {
   auto enc = encode_fn();
   VM_REQUIRE(enc, VM_E_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
   VM_REQUIRE((reinterpret_cast<uintptr_t>(base) & 15) == 0, VM_E_ALIGN, "slab base not 16B aligned");
   cuuint64_t dims[4] = {64, (cuuint64_t)(rows / 8), (cuuint64_t)CG, (cuuint64_t)B};
-  cuuint64_t strides[3] = {128, (cuuint64_t)rows * 16, (cuuint64_t)bstride * 2};
+  cuuint64_t strides[3] = {128, (cuuint64_t)stride_rows * 16, (cuuint64_t)bstride * 2};
   cuuint32_t box[4] = {64, (cuuint32_t)box_blocks, (cuuint32_t)box_groups, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
@@ -2071,12 +2073,12 @@ int make_wide_map(CUtensorMap* m, const void* base, int64_t bstride, int CG, int
   return VM_OK;
 }
 
-int make_group_map(CUtensorMap* m, const void* base, int64_t bstride, int CG, int64_t rows, int B,
-                   int box_rows, int box_groups) {
+int make_group_map(CUtensorMap* m, const void* base, int64_t bstride, int CG, int64_t rows, int64_t stride_rows,
+                   int B, int box_rows, int box_groups) {
   auto enc = encode_fn();
   VM_REQUIRE(enc, VM_E_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[4] = {8, (cuuint64_t)rows, (cuuint64_t)CG, (cuuint64_t)B};
-  cuuint64_t strides[3] = {16, (cuuint64_t)rows * 16, (cuuint64_t)bstride * 2};
+  cuuint64_t strides[3] = {16, (cuuint64_t)stride_rows * 16, (cuuint64_t)bstride * 2};
   cuuint32_t box[4] = {8, (cuuint32_t)box_rows, (cuuint32_t)box_groups, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
@@ -2216,7 +2218,11 @@ static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_
       pk.dbg = g_fwd_dbg;
       const int64_t gbs = gy_bstride ? gy_bstride : default_bstride(Cout, D, H, W, 1);
       CUtensorMap gmap;
-      int rc = make_group_map(&gmap, gy, gbs, pk.CGo, pk.rows, B, pk.KS, pk.CGo);
+      // gy through its interior depth planes only (rows [P, (D+1)P) from the plane-1 base): the
+      // depth margin layers read as zeros even while a halo exchange is filling them, so the
+      // weight gradient can run concurrently with the output gradient's exchange + dgrad
+      int rc = make_group_map(&gmap, static_cast<const bf16*>(gy) + (int64_t)pk.P * 8, gbs, pk.CGo,
+                              (int64_t)D * pk.P, pk.rows, B, pk.KS, pk.CGo);
       if (rc) return rc;
       cudaStream_t st = as_stream(stream);
       const bool dbg = pk.dbg != nullptr;
@@ -2259,8 +2265,13 @@ static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_
   const int64_t gbs = gy_bstride ? gy_bstride : default_bstride(Cout, D, H, W, 1);
   const int64_t rows = (int64_t)(D + 2) * p.P;
   CUtensorMap gmap;
-  rc = p.gwide ? make_wide_map(&gmap, gy, gbs, p.CGo, rows, B, p.RR / 8, p.CGo)
-               : make_group_map(&gmap, gy, gbs, p.CGo, rows, B, p.RR, p.CGo);
+  // anchors never reach gy's margin layer 0; its margin layer D+1 (exchanged concurrently, see
+  // the kd kernel) is cut off: rows >= (D+1)P read as zeros (the wide map's 8-row blocks round
+  // down: the < 8 rows dropped lie in layer D's h = H+1 margin row, zero, as W + 2 >= 8 there)
+  int64_t glim = rows - p.P;
+  if (p.gwide && glim % 8 > p.Wp) glim += 8 - glim % 8;  // never drop interior rows (W + 2 < 8)
+  rc = p.gwide ? make_wide_map(&gmap, gy, gbs, p.CGo, glim, rows, B, p.RR / 8, p.CGo)
+               : make_group_map(&gmap, gy, gbs, p.CGo, glim, rows, B, p.RR, p.CGo);
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
   // compile-time M-tile count (when every CTA holds the same number of tiles) and K steps

@@ -19,7 +19,10 @@
 // ncclAllReduce from the libnccl.so.2 already loaded by the process (torch's), so the
 // communicator the caller passes (ProcessGroupNCCL._comm_ptr()) and these calls are the same
 // NCCL instance.  All work is enqueued on the caller's stream (capturable in a CUDA graph).
+#include <cuda.h>
 #include <dlfcn.h>
+
+#include <cstring>
 
 #include "vm_common.cuh"
 
@@ -313,5 +316,205 @@ extern "C" int vm_allreduce_f32(void* comm, float* buf, size_t n, void* stream) 
   VM_REQUIRE(nccl_ok() || vm_nccl_bind() == VM_OK, VM_E_UNSUPPORTED, "vm_allreduce_f32: NCCL not bound");
   if (n == 0) return VM_OK;
   NCCL_CHECK(g_nccl.allreduce(buf, buf, n, kNcclFloat32, kNcclSum, comm, as_stream(stream)), "ncclAllReduce");
+  return VM_OK;
+}
+
+// ------------------------------------------------------------------ peer-memory depth halo
+// The depth phase of a depth-only split without NCCL: every rank PUSHES its first and last
+// interior layers straight into its neighbours' margin layers through mapped peer memory
+// (NVLink P2P stores; CUDA-IPC mappings of the neighbours' slabs), then signals them, then
+// waits for its own margins.  One launch per exchange, no pack / unpack pass: a depth layer of
+// a (sample, channel group) is one contiguous run of (H+2)(W+2) voxel groups, so the push is a
+// flat 16-byte copy.  The whole padded layer moves; its H / W margins are zero on every rank
+// of a depth-only split, so the slab ends up byte-identical to the packed protocol's
+// (halo.py:109-155 with only `x` partitioned).
+//
+// Completion: every block fences its stores system-wide and counts itself done; the last
+// block writes the step's epoch into the neighbours' flag words (release, system scope) and
+// spins until its own two flag words (written by the neighbours' pushes) reach the epoch.  A
+// rank that is its own neighbour (the periodic single-GPU emulation) signals itself before it
+// waits, so it never waits on another kernel.
+namespace vm {
+struct DepthPush {
+  const uint8_t* src;
+  uint8_t* lo_dst;  // lo neighbour's slab (receives our layer 1 in its layer D+1), or null
+  uint8_t* hi_dst;  // hi neighbour's slab (receives our layer D in its layer 0), or null
+  int* lo_flag;     // the lo neighbour's "from hi" flag word
+  int* hi_flag;     // the hi neighbour's "from lo" flag word
+  int* own;         // own flag words [from lo, from hi]
+  unsigned* counter;
+  const int* epoch;
+  int64_t bstride_b, plane_b, layer_b;
+  int B, CG, D, wait_lo, wait_hi;
+};
+
+__device__ __forceinline__ void st_release_sys(int* p, int v) {
+  asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(int* p, int v) {
+  asm volatile("st.relaxed.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// grid: x over the 16-byte units of one layer, y over (sample, channel group, side).  Every
+// block fences its stores at GPU scope and counts itself done; the last block (which has
+// observed every other block's count, so their stores precede it in causality order) issues
+// the one system-scope fence and the release stores that the neighbours acquire.
+__device__ int g_push_dbg;  // A/B probe bits (vm_debug_push_mode): 1 gpu-scope publish, 2 no wait
+__global__ void __launch_bounds__(256) k_depth_push(const DepthPush p) {
+  pdl_wait();
+  const unsigned n16 = (unsigned)(p.layer_b / 16);  // 16-byte units per layer
+  const int sides = (p.lo_dst != nullptr) + (p.hi_dst != nullptr);
+  const int r = blockIdx.y;
+  const int s = r % sides;
+  const int bc = r / sides;
+  const int cg = bc % p.CG, b = bc / p.CG;
+  const bool lo = s == 0 && p.lo_dst != nullptr;
+  const int64_t base = b * p.bstride_b + cg * p.plane_b;
+  const uint4* from = reinterpret_cast<const uint4*>(p.src + base + (lo ? 1 : p.D) * p.layer_b);
+  uint4* to = reinterpret_cast<uint4*>((lo ? p.lo_dst : p.hi_dst) + base + (lo ? p.D + 1 : 0) * p.layer_b);
+  const unsigned step = gridDim.x * blockDim.x;
+  unsigned u = blockIdx.x * blockDim.x + threadIdx.x;
+  for (; u + 3 * step < n16; u += 4 * step) {  // 4 loads in flight per thread
+    const uint4 a0 = __ldg(from + u), a1 = __ldg(from + u + step), a2 = __ldg(from + u + 2 * step),
+                a3 = __ldg(from + u + 3 * step);
+    to[u] = a0, to[u + step] = a1, to[u + 2 * step] = a2, to[u + 3 * step] = a3;
+  }
+  for (; u < n16; u += step) to[u] = __ldg(from + u);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned nblocks = gridDim.x * gridDim.y;
+    const unsigned done = atomicAdd(p.counter, 1u);
+    if (done == nblocks - 1) {  // every block's stores precede this point: publish, then wait
+      *p.counter = 0;
+      const int dbg = g_push_dbg;
+      const int e = *p.epoch;
+      if (dbg & 1) {
+        __threadfence();
+        if (p.lo_dst) *(volatile int*)p.lo_flag = e;
+        if (p.hi_dst) *(volatile int*)p.hi_flag = e;
+      } else {
+        // ONE system-scope release fence (MEMBAR.ALL.SYS, ~2.5 us on B200: the cost of making
+        // NVLink stores visible to another GPU), cumulative over every block's stores observed
+        // through the counter, then relaxed system-scope flag stores
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        if (p.lo_dst) st_relaxed_sys(p.lo_flag, e);
+        if (p.hi_dst) st_relaxed_sys(p.hi_flag, e);
+      }
+      if (dbg & 2) return;
+      // bounded wait (~10 s): a neighbour that never signals sets the error word epoch[1]
+      // instead of hanging the device
+      const long long t0 = clock64();
+      while ((p.wait_lo && ld_acquire_sys(p.own) < e) || (p.wait_hi && ld_acquire_sys(p.own + 1) < e)) {
+        __nanosleep(128);
+        if (clock64() - t0 > 20000000000LL) {
+          atomicExch(const_cast<int*>(p.epoch) + 1, e);
+          break;
+        }
+      }
+    }
+  }
+}
+
+__global__ void k_epoch_bump(int* epoch) { *epoch += 1; }
+}  // namespace vm
+
+// Depth-phase halo through peer memory (see above).  lo_peer / hi_peer: the neighbours' slab
+// bases (same geometry and batch stride as `slab`), null at a global boundary; flags: the
+// exchange slot's flag words, own[2] (written by the neighbours), lo_flag = the lo
+// neighbour's own[1] word, hi_flag = the hi neighbour's own[0] word; counter: one zeroed
+// device word per slot; epoch: the device step counter (vm_halo_epoch_bump).
+extern "C" int vm_halo_depth_push(int dtype, const void* slab, int64_t bstride, int B, int C, int D, int H, int W,
+                                  void* lo_peer, void* hi_peer, int* lo_flag, int* hi_flag, int* own,
+                                  unsigned* counter, const int* epoch, void* stream) {
+  VM_REQUIRE(slab && own && counter && epoch, VM_E_ARG, "vm_halo_depth_push: null pointer");
+  VM_REQUIRE((!lo_peer || lo_flag) && (!hi_peer || hi_flag), VM_E_ARG, "vm_halo_depth_push: peer without flag");
+  VM_REQUIRE(dtype == VM_BF16 || dtype == VM_F32, VM_E_UNSUPPORTED, "vm_halo_depth_push: dtype %d", dtype);
+  VM_REQUIRE(D >= 1 && H >= 1 && W >= 1, VM_E_HALO, "vm_halo_depth_push: margin 1 exceeds local extent (%d,%d,%d)",
+             D, H, W);
+  VM_REQUIRE(((reinterpret_cast<uintptr_t>(slab) | reinterpret_cast<uintptr_t>(lo_peer) |
+               reinterpret_cast<uintptr_t>(hi_peer)) & 15) == 0,
+             VM_E_ALIGN, "vm_halo_depth_push: 16-byte alignment required");
+  const FaceSet s = face_set(dtype, bstride, B, C, D, H, W);
+  DepthPush p{};
+  p.src = static_cast<const uint8_t*>(slab);
+  p.lo_dst = static_cast<uint8_t*>(lo_peer);
+  p.hi_dst = static_cast<uint8_t*>(hi_peer);
+  p.lo_flag = lo_flag, p.hi_flag = hi_flag, p.own = own, p.counter = counter, p.epoch = epoch;
+  p.bstride_b = s.bstride_b, p.plane_b = s.plane_b, p.layer_b = s.plane_b / (D + 2);
+  p.B = B, p.CG = s.CG, p.D = D;
+  // a neighbour pushes into our margin exactly when we push into its: wait on the same sides
+  p.wait_lo = lo_peer != nullptr, p.wait_hi = hi_peer != nullptr;
+  const int sides = p.wait_lo + p.wait_hi;
+  if (!sides) return VM_OK;
+  const int64_t n16 = p.layer_b / 16;
+  const int ny = B * s.CG * sides;
+  VM_REQUIRE(ny <= 65535 && n16 < (1LL << 31), VM_E_UNSUPPORTED, "vm_halo_depth_push: slab too large");
+  int nsm = vm_num_sms(0);
+  if (nsm <= 0) nsm = 148;
+  // ~4 units per thread, about two waves of 256-thread blocks over the whole exchange
+  int64_t gx = (n16 + 256 * 4 - 1) / (256 * 4);
+  const int64_t cap = (2 * nsm + ny - 1) / ny;
+  if (gx > cap) gx = cap;
+  if (gx < 1) gx = 1;
+  launch_pdl(k_depth_push, dim3((unsigned)gx, (unsigned)ny), 256, 0, as_stream(stream), p);
+  return launch_status("vm_halo_depth_push");
+}
+
+extern "C" void vm_debug_push_mode(int m) { cudaMemcpyToSymbol(g_push_dbg, &m, sizeof(int)); }
+
+extern "C" int vm_halo_epoch_bump(int* epoch, void* stream) {
+  VM_REQUIRE(epoch, VM_E_ARG, "vm_halo_epoch_bump: null pointer");
+  k_epoch_bump<<<1, 1, 0, as_stream(stream)>>>(epoch);
+  return launch_status("vm_halo_epoch_bump");
+}
+
+// CUDA-IPC plumbing for the peer mappings: the handle (64 bytes) of the allocation holding
+// `ptr` and ptr's offset in it; opening a handle maps the peer allocation once per process
+// (cached: a second open of the same allocation returns the first mapping).
+extern "C" int vm_ipc_handle(const void* ptr, void* handle64, int64_t* offset) {
+  VM_REQUIRE(ptr && handle64 && offset, VM_E_ARG, "vm_ipc_handle: null pointer");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  VM_REQUIRE(cuMemGetAddressRange(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) == CUDA_SUCCESS,
+             VM_E_ARG, "vm_ipc_handle: not a device allocation");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  VM_REQUIRE(e == cudaSuccess, 100 + (int)e, "vm_ipc_handle: cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+  memcpy(handle64, &h, sizeof(h));
+  *offset = (int64_t)(reinterpret_cast<uintptr_t>(ptr) - (uintptr_t)base);
+  return VM_OK;
+}
+
+namespace {
+struct IpcMap {
+  unsigned char key[64];
+  void* base;
+};
+IpcMap g_ipc[512];
+int g_nipc = 0;
+}  // namespace
+
+extern "C" int vm_ipc_open(const void* handle64, void** base) {
+  VM_REQUIRE(handle64 && base, VM_E_ARG, "vm_ipc_open: null pointer");
+  for (int i = 0; i < g_nipc; ++i)
+    if (!memcmp(g_ipc[i].key, handle64, 64)) {
+      *base = g_ipc[i].base;
+      return VM_OK;
+    }
+  VM_REQUIRE(g_nipc < 512, VM_E_UNSUPPORTED, "vm_ipc_open: too many peer allocations");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  void* p = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+  VM_REQUIRE(e == cudaSuccess, 100 + (int)e, "vm_ipc_open: cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+  memcpy(g_ipc[g_nipc].key, handle64, 64);
+  g_ipc[g_nipc++].base = p;
+  *base = p;
   return VM_OK;
 }

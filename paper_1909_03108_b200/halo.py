@@ -527,6 +527,121 @@ class SlabHalo:
             self.kernels.zero(s, self.nbr6)
 
 
+class PeerDepthHalo:
+    """Depth-only halo through peer memory (vm_halo_depth_push): no NCCL, no pack / unpack.
+
+    Each exchange is ONE launch that pushes this rank's first / last interior depth layers
+    into the lo / hi neighbours' margin layers (NVLink P2P stores through CUDA-IPC mappings of
+    the neighbours' slabs), publishes the step epoch into their flag words and waits for its
+    own margins.  Exchanges are numbered in program order within a step (the same on every
+    rank: every rank runs the same static step program); ``begin_step`` bumps the device
+    epoch and restarts the numbering, so a captured step graph replays correctly.
+
+    ``peers=None``: every neighbour is this rank itself (the periodic single-GPU emulation of a
+    split: the same launches and bytes, local HBM instead of NVLink).  Otherwise call
+    :meth:`connect` with the exchanged slabs (spmd over NCCL: handles are swapped with
+    ``torch.distributed.all_gather_object``).
+    """
+
+    NSLOT = 512
+
+    def __init__(self, nbr6, device, self_peers=True):
+        import torch
+
+        if any(n >= 0 for n in nbr6[2:]):
+            raise HaloError("peer-memory halo: only a depth split (x axis) is supported")
+        self.nbr6 = [int(n) for n in nbr6]
+        self.comm = None
+        self.self_peers = self_peers
+        self.state = torch.zeros(8 + 3 * self.NSLOT, dtype=torch.int32, device=device)
+        self.peer_state = (self.state.data_ptr(), self.state.data_ptr()) if self_peers else (None, None)
+        self.peer_slab = {}  # own slab pointer -> (lo neighbour's, hi neighbour's)
+        self._slot = 0
+        self._sent = 0
+        # the weight-gradient kernels never read a depth margin layer of gy, so they may run
+        # while this transport fills them (UNetStep overlaps wgrad with exchange + dgrad)
+        self.wgrad_safe = True
+
+    @property
+    def active(self):
+        return self.nbr6[0] >= 0 or self.nbr6[1] >= 0
+
+    def reserve(self, slabs):
+        pass
+
+    def bytes_sent(self):
+        return self._sent
+
+    def connect(self, slabs, group=None):
+        """Map the neighbours' copies of ``slabs`` (same program order on every rank) and
+        their flag words through CUDA IPC."""
+        import torch.distributed as dist
+
+        def rec(ptr):
+            h = ctypes.create_string_buffer(64)
+            off = ctypes.c_int64(0)
+            _lib.call("vm_ipc_handle", ctypes.c_void_p(ptr), ctypes.addressof(h), ctypes.addressof(off))
+            return (h.raw, int(off.value))
+
+        mine = [rec(self.state.data_ptr())] + [rec(s.ptr) for s in slabs]
+        world = [None] * dist.get_world_size(group)
+        dist.all_gather_object(world, mine, group=group)
+
+        def open_(r):
+            out = []
+            for h, off in world[r]:
+                base = ctypes.c_void_p(0)
+                hb = ctypes.create_string_buffer(h, 64)
+                _lib.call("vm_ipc_open", ctypes.addressof(hb), ctypes.addressof(base))
+                out.append(int(base.value) + off)
+            return out
+
+        lo = open_(self.nbr6[0]) if self.nbr6[0] >= 0 else None
+        hi = open_(self.nbr6[1]) if self.nbr6[1] >= 0 else None
+        self.peer_state = (lo[0] if lo else None, hi[0] if hi else None)
+        for i, s in enumerate(slabs):
+            self.peer_slab[s.ptr] = (lo[1 + i] if lo else None, hi[1 + i] if hi else None)
+        self.self_peers = False
+
+    def begin_step(self):
+        self._slot = 0
+        _lib.call("vm_halo_epoch_bump", _lib.ptr(self.state), _lib.stream_ptr())
+
+    def forward(self, s, tag=_FWD_TAG):
+        if not self.active:
+            return
+        slot = self._slot
+        if slot >= self.NSLOT:
+            raise HaloError(f"peer-memory halo: more than {self.NSLOT} exchanges in one step")
+        self._slot += 1
+        lo_n, hi_n = self.nbr6[0] >= 0, self.nbr6[1] >= 0
+        if self.self_peers:
+            lo_p, hi_p = s.ptr, s.ptr
+        else:
+            lo_p, hi_p = self.peer_slab[s.ptr]
+        base = self.state.data_ptr()
+        own = base + 4 * (8 + 2 * slot)
+        lo_flag = self.peer_state[0] + 4 * (8 + 2 * slot + 1) if lo_n else None
+        hi_flag = self.peer_state[1] + 4 * (8 + 2 * slot) if hi_n else None
+        counter = base + 4 * (8 + 2 * self.NSLOT + slot)
+        vp = ctypes.c_void_p
+        _lib.call("vm_halo_depth_push", _lib.dtype_code(s.dtype), s.p(), s.bstride, s.B, s.C, s.D, s.H, s.W,
+                  vp(lo_p) if lo_n else None, vp(hi_p) if hi_n else None, vp(lo_flag) if lo_n else None,
+                  vp(hi_flag) if hi_n else None, vp(own), vp(counter), vp(base), _lib.stream_ptr())
+        self._sent += s.B * s.CG * 8 * s.H * s.W * s.storage.element_size() * (lo_n + hi_n)
+
+    def check(self):
+        """Raise if an exchange of this transport timed out waiting for a neighbour (host sync)."""
+        err = int(self.state[1].item())
+        if err:
+            raise HaloError(f"peer-memory halo: a neighbour's signal did not arrive (epoch {err})")
+
+    def zero(self, s):
+        # the depth margins of a gradient slab are never read by the weight gradient (its gy
+        # maps cover the interior depth planes only); H / W are not split
+        pass
+
+
 def nccl_comm_ptr(group=None):
     """The ncclComm_t behind a torch.distributed NCCL process group (initialised eagerly by a
     one-element all-reduce when torch created it lazily)."""

@@ -29,7 +29,7 @@ import torch
 
 from . import _lib
 from .errors import GraphBuildError, VoxmeshError
-from .halo import SlabHalo, nccl_comm_of, nccl_second_comm
+from .halo import PeerDepthHalo, SlabHalo, nccl_comm_of, nccl_second_comm
 
 _DT = {torch.bfloat16: _lib.VM_BF16, torch.float32: _lib.VM_F32}
 
@@ -409,7 +409,7 @@ class UNetStep:
         if self.has_halo:
             self.halo.forward(s, tag)
 
-    def halo_bytes_per_step(self):
+    def halo_bytes_per_step(self, forward_only=False):
         """Bytes this rank sends per step (3-phase protocol, fwd + bwd, slab channel padding included)."""
         if not self.has_halo:
             return 0
@@ -430,7 +430,7 @@ class UNetStep:
                 per += area * ((lo is not None) + (hi is not None))
                 cur[i] += 2
             nbytes = per * cg * 8 * self.B * torch.tensor([], dtype=self.dtype).element_size()
-            total += nbytes * (1 if n.inputs[0] == "input" else 2)
+            total += nbytes * (1 if (n.inputs[0] == "input" or forward_only) else 2)
         return total
 
     def _zero_margins(self, s):
@@ -459,19 +459,44 @@ class UNetStep:
         self.ar_comm = ar_comm
         self._reserve_halo()
 
+    def use_peer_halo(self, nbr6=None, group=None):
+        """Depth-split halos through peer memory (halo.PeerDepthHalo, vm_halo_depth_push)
+        instead of NCCL.  ``nbr6`` given: a single-GPU emulation whose neighbours are this rank
+        itself (periodic halos, same launches and bytes); otherwise the mesh's own neighbours,
+        mapped over CUDA IPC (spmd, one process per GPU)."""
+        emulate = nbr6 is not None
+        if not emulate:
+            peer = PeerDepthHalo(self.halo.nbr6, self.device, self_peers=False)
+        else:
+            peer = PeerDepthHalo(nbr6, self.device, self_peers=True)
+            for i in range(3):
+                lo, hi = nbr6[2 * i], nbr6[2 * i + 1]
+                if lo >= 0 or hi >= 0:
+                    self.nbrs[1 + i] = (lo if lo >= 0 else None, hi if hi >= 0 else None)
+        self.halo = peer
+        self.has_halo = peer.active
+        if self.has_halo:  # a halo'd first conv reads the 8-channel input slab (margins exchanged)
+            for L in self.layers:
+                L.c1 = False
+            self.input_slab_needed = True
+        if not emulate and peer.active:
+            peer.connect(self._halo_slabs(), group)
+
+    def _halo_slabs(self):
+        slabs = [self.out[n.inputs[0]] for n in self.graph.nodes if n.op == "conv" and n.k == 3]
+        return slabs + list(self.gpre.values())
+
     def _reserve_halo(self):
         if self.halo.comm is None:
             return
-        slabs = [self.out[n.inputs[0]] for n in self.graph.nodes if n.op == "conv" and n.k == 3]
-        slabs += list(self.gpre.values())
-        self.halo.reserve(slabs)
+        self.halo.reserve(self._halo_slabs())
 
     def _split_planes(self, D):
         """Interior / boundary split of a conv's output planes around a depth-only halo."""
         n = self.halo.nbr6
         depth_only = (n[0] >= 0 or n[1] >= 0) and max(n[2:]) < 0
         return (self.overlap_halo and self.has_halo and depth_only and self.conv_impl == "tc"
-                and D >= self.overlap_min_planes)
+                and D >= self.overlap_min_planes and not isinstance(self.halo, PeerDepthHalo))
 
     def graph_capturable(self):
         return self.ctx is None or self.ctx.mesh.worker_count == 1 or self.comm is not None
@@ -741,6 +766,8 @@ class UNetStep:
             _lib.load().vm_set_pdl(prev)
 
     def _forward_nodes(self):
+        if self.has_halo and hasattr(self.halo, "begin_step"):
+            self.halo.begin_step()
         for n in self.graph.nodes:
             if n.op == "conv" and n.k == 3:
                 x = self.out[n.inputs[0]]
@@ -827,13 +854,17 @@ class UNetStep:
         buckets = self._grad_buckets() if (self.ar_comm is not None and side is not None) else {}
         if buckets:
             ar = self._ar_stream()
+        # a transport whose margins the weight gradient never reads (peer-memory depth halo):
+        # wgrad runs on the side stream while the main stream exchanges gy and runs dgrad
+        concurrent = self.has_halo and getattr(self.halo, "wgrad_safe", False) and self.conv_impl == "tc"
+        serial_halo = self.has_halo and not concurrent
         for n in reversed(self.graph.nodes):
             if n.op == "conv" and n.k == 3:
                 L = self.by_id[n.id]
                 x = self.out[n.inputs[0]]
                 gp = self.gpre[n.id]
                 src = n.inputs[0]
-                if src != "input" and self.has_halo:
+                if src != "input" and serial_halo:
                     self._dgrad(gp, L, src)
                     self._zero_margins(gp)
                     if side is not None:
@@ -841,7 +872,7 @@ class UNetStep:
                         ev.record(main)
                         side.wait_event(ev)
                 if side is not None:
-                    if not self.has_halo:
+                    if not serial_halo:
                         side.wait_stream(main)
                     with torch.cuda.stream(side):
                         self._wgrad(x, L, gp)
@@ -855,7 +886,7 @@ class UNetStep:
                                         _lib.ptr(self.grads[lo:hi]), hi - lo)
                 else:
                     self._wgrad(x, L, gp)
-                if src != "input" and not self.has_halo:
+                if src != "input" and not serial_halo:
                     self._dgrad(gp, L, src)
             elif n.op == "up":
                 cat = next(c for c in self.consumers[n.id] if c.op == "concat")
