@@ -479,9 +479,21 @@ extern "C" int vm_halo_epoch_bump(int* epoch, void* stream) {
 // (cached: a second open of the same allocation returns the first mapping).
 extern "C" int vm_ipc_handle(const void* ptr, void* handle64, int64_t* offset) {
   VM_REQUIRE(ptr && handle64 && offset, VM_E_ARG, "vm_ipc_handle: null pointer");
+  // the driver entry point through the runtime (libcuda is not a link dependency: the library
+  // must load on a host without a driver for the ABI checks)
+  typedef CUresult (*range_fn_t)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static range_fn_t range_fn = nullptr;
+  if (!range_fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      range_fn = reinterpret_cast<range_fn_t>(f);
+  }
+  VM_REQUIRE(range_fn, VM_E_UNSUPPORTED, "vm_ipc_handle: cuMemGetAddressRange unavailable");
   CUdeviceptr base = 0;
   size_t size = 0;
-  VM_REQUIRE(cuMemGetAddressRange(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) == CUDA_SUCCESS,
+  VM_REQUIRE(range_fn(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) == CUDA_SUCCESS,
              VM_E_ARG, "vm_ipc_handle: not a device allocation");
   cudaIpcMemHandle_t h;
   cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
