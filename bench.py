@@ -335,6 +335,10 @@ def emulated_halo(a, torch, vm, peaks):
     for _ in range(2):
         st.step()
     torch.cuda.synchronize()
+    # both arms run SGD with lr = 0 (same kernels and bytes): the no-exchange arm computes with
+    # wrong margins and, left to train on one sample, diverges within ~10 steps, after which
+    # the non-finite values make every later step (of both arms) ~3x slower
+    st.lr = 0.0
     fns, graphs = {}, []
     for name, on in (("halo", True), ("nohalo", False)):
         st.has_halo = on
@@ -346,11 +350,14 @@ def emulated_halo(a, torch, vm, peaks):
             fns[name] = (lambda on_: (lambda: (setattr(st, "has_halo", on_), st.step())))(on)
     # alternate the two programs (3 rounds, best of each): the A/B is not skewed by drift
     res = {"halo": float("inf"), "nohalo": float("inf")}
+    rounds = []
     for _ in range(3):
         for name in ("halo", "nohalo"):
             for _ in range(max(3, a.warmup)):
                 fns[name]()
-            res[name] = min(res[name], _timed(torch, fns[name], max(5, a.steps), torch.cuda.synchronize))
+            t = _timed(torch, fns[name], max(5, a.steps), torch.cuda.synchronize)
+            rounds.append((name, round(t, 4)))
+            res[name] = min(res[name], t)
     del graphs, fns
     st.has_halo = True
     nbytes = st.halo_bytes_per_step()
@@ -369,8 +376,10 @@ def emulated_halo(a, torch, vm, peaks):
         "share": max(0.0, (res["halo"] - res["nohalo"]) / res["halo"]),
         "method": f"emulated on 1 GPU: rank block {loc[0]}x{loc[1]}x{loc[2]} of cfg3 {K}-way depth split, periodic "
                   f"halos (every neighbour = this rank) through {transport}; "
-                  "A/B: (t_step - t_step_nohalo) / t_step",
+                  "A/B: (t_step - t_step_nohalo) / t_step, best of 3 alternating rounds, SGD at lr = 0 in both "
+                  "arms (same work; keeps the wrong-margin arm from diverging)",
         "transport": a.emulate_transport,
+        "rounds_ms": rounds,
         "ms_step": res["halo"], "ms_nohalo": res["nohalo"],
         "bytes_per_step_rank": nbytes,
         "forward_bytes_per_step_rank": fwd_bytes,

@@ -303,6 +303,28 @@ int vm_halo_depth_push(int dtype, const void* slab, int64_t bstride, int B, int 
                        void* lo_peer, void* hi_peer, int* lo_flag, int* hi_flag, int* own,
                        unsigned* counter, const int* epoch, void* stream);
 int vm_halo_epoch_bump(int* epoch, void* stream);
+/* The same depth halo FUSED into a tensor-core conv (vm_conv3d_fwd_tc_link, forward or dgrad):
+ * producer side, the epilogue stores output layers 1 and D into push_lo's layer D+1 and
+ * push_hi's layer 0 as it writes them (the neighbours' copies of y, same geometry and batch
+ * stride; NULL: no push) and the last CTA fences system-wide and writes the epoch into
+ * lo_flag / hi_flag; consumer side, the producer warp waits until wait_own[0] (wait_lo) and
+ * wait_own[1] (wait_hi) reach the epoch before it loads the input.  epoch: {step counter,
+ * error word}; counter: the zeroed slot word of the push. */
+typedef struct vm_halo_link {
+  void* push_lo;
+  void* push_hi;
+  int* lo_flag;
+  int* hi_flag;
+  unsigned* counter;
+  const int* wait_own;
+  int wait_lo, wait_hi;
+  const int* epoch;
+} vm_halo_link;
+/* vm_conv3d_fwd_tc_ws with a fused halo link (NULL link: no halo) */
+int vm_conv3d_fwd_tc_link(const void* x, int64_t x_bstride, const void* wpacked, const float* bias, void* y,
+                          int64_t y_bstride, const void* mask, int64_t mask_bstride, int B, int Cin, int Cout, int D,
+                          int H, int W, unsigned flags, void* ws, size_t ws_bytes, const vm_halo_link* link,
+                          void* stream);
 /* CUDA-IPC handle (64 bytes) of the allocation holding ptr, and ptr's offset in it; open a
  * peer's handle (mapped once per process) */
 int vm_ipc_handle(const void* ptr, void* handle64, int64_t* offset);

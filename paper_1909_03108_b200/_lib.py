@@ -96,6 +96,7 @@ _SIGS = {
     "vm_halo_epoch_bump": (_I, [_P, _P]),
     "vm_ipc_handle": (_I, [_P, _P, _P]),
     "vm_ipc_open": (_I, [_P, _P]),
+    "vm_conv3d_fwd_tc_link": (_I, [_P, _L, _P, _P, _P, _L, _P, _L, _I, _I, _I, _I, _I, _I, _U, _P, _S, _P, _P]),
     "vm_conv3d_fwd_tc_range": (_I, [_P, _L, _P, _P, _P, _L, _P, _L, _I, _I, _I, _I, _I, _I, _I, _I, _U, _P, _S,
                                     _P]),
     # SURVEY §8(b) composites (csrc/abi.cu)

@@ -195,6 +195,7 @@ struct FwdParams {
   unsigned flags;
   long long* dbg;  // optional timing probes [gridDim][8]
   uint32_t wp_magic, hp_magic;  // floor(2^32 / d) + 1 for the anchor (w, h) split
+  HaloLink hl;     // fused peer-memory depth halo (vm_conv3d_fwd_tc_link)
   // split-K over the 3*KC (kc, kd) stages: unit = (tile unit tu, split ks); split ks writes
   // f32 partials ws[ks][tu][MB][Nc][128], the last split of a tile unit to finish (counter)
   // sums all splits in split order (deterministic) and runs the epilogue
@@ -206,9 +207,11 @@ struct FwdParams {
 // MB (tiles per unit) is a template parameter so that the MMA issue loop is straight-line
 // code: measured on B200, a runtime-bounded issue loop costs 1.5x in MMA throughput for
 // N = 128 (tools/probes/probe_pipe.cu).
-template <int MB, bool DBG>  // DBG: cycle probes (tools/dbg_fwd_probe.py)
+// MODE 0: plain; 1: cycle probes (tools/dbg_fwd_probe.py); 2: fused peer-memory halo (p.hl)
+template <int MB, int MODE>
 __global__ void __launch_bounds__(320, 1)
     k_conv_fwd_tc(const FwdParams p) {
+  constexpr bool DBG = MODE == 1, HL = MODE == 2;
   auto clk = []() -> long long { return DBG ? (long long)clock64() : 0LL; };
   const long long t_kstart = clk();
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -239,6 +242,7 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (elect_one()) {
+      if (HL) halo_link_wait(p.hl);  // the input's margins, pushed by the neighbours' producers
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
@@ -358,7 +362,7 @@ __global__ void __launch_bounds__(320, 1)
     const bool nobias = p.flags & VM_CONV_NOBIAS;
     const bool relu = p.flags & VM_CONV_RELU;
     const bool cout8 = (p.Cout & 7) == 0;
-    auto emit = [&](bf16* ybase, int co0, float (&v)[8], const int4& mkv, int64_t orow) {
+    auto emit = [&](bf16* ybase, int co0, float (&v)[8], const int4& mkv, int64_t orow, int dq) {
       if (!nobias) {
         float bb[8];
         if (bias_smem) {
@@ -395,9 +399,14 @@ __global__ void __launch_bounds__(320, 1)
       for (int e = 0; e < 4; ++e) oh[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
       if (!(DBG && (p.flags & (1u << 9))))  // probe builds: flag bit 9 skips the store
         *reinterpret_cast<int4*>(ybase + (co0 / 8) * p.plane8 + orow * 8) = out;
+      // fused depth halo: layer 1 -> the lo neighbour's layer D+1, layer D -> the hi one's layer 0
+      if (HL && p.hl.lo && dq == 0)
+        *reinterpret_cast<int4*>(p.hl.lo + (ybase - p.y) + (co0 / 8) * p.plane8 + (orow + p.anchors) * 8) = out;
+      if (HL && p.hl.hi && dq == p.D - 1)
+        *reinterpret_cast<int4*>(p.hl.hi + (ybase - p.y) + (co0 / 8) * p.plane8 + (orow - p.anchors) * 8) = out;
     };
     // output row of anchor a: (w, h) via multiply-high division (divisors are small)
-    auto anchor_row = [&](int a, bool& valid) -> int64_t {
+    auto anchor_row = [&](int a, bool& valid, int& dq) -> int64_t {
       uint32_t qa = __umulhi((uint32_t)a, p.wp_magic);
       if (qa * (uint32_t)p.Wp > (uint32_t)a) --qa;
       if ((qa + 1) * (uint32_t)p.Wp <= (uint32_t)a) ++qa;
@@ -406,6 +415,7 @@ __global__ void __launch_bounds__(320, 1)
       if (qh * (uint32_t)p.Hp > qa) --qh;
       if ((qh + 1) * (uint32_t)p.Hp <= qa) ++qh;
       const int hq = (int)qa - (int)qh * p.Hp;
+      dq = (int)qh;
       valid = a < p.anchors && wq < p.W && hq < p.H;
       return (int64_t)a + p.P + p.Wp + 1;
     };
@@ -435,7 +445,8 @@ __global__ void __launch_bounds__(320, 1)
         const int row = q * 32 + lane;
         const int a = a0 + i * 128 + row;
         bool valid;
-        const int64_t orow = anchor_row(a, valid);
+        int dq;
+        const int64_t orow = anchor_row(a, valid, dq);
         const uint32_t tcol = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * p.MB + i) * p.nacc * p.Nc);
         // partial layout [ks][tu][tile][row][Nc]: a thread's channels are contiguous (float4 I/O)
         float* wsp = split ? p.ws + ((((int64_t)ks * ntu + tu) * p.MB + i) * 128 + row) * p.Nc : nullptr;
@@ -491,7 +502,7 @@ __global__ void __launch_bounds__(320, 1)
               float v[8];
 #pragma unroll
               for (int e = 0; e < 8; ++e) v[e] = r[jj * 8 + e];
-              emit(ybase, co0, v, mk[j + jj], orow);
+              emit(ybase, co0, v, mk[j + jj], orow, dq);
             }
           }
         }
@@ -518,7 +529,8 @@ __global__ void __launch_bounds__(320, 1)
           for (int i = MB == 1 ? 0 : half; i < p.MB; i += MB == 1 ? 1 : 2) {
             const int row = q * 32 + lane;
             bool valid;
-            const int64_t orow = anchor_row(a0 + i * 128 + row, valid);
+            int dq;
+            const int64_t orow = anchor_row(a0 + i * 128 + row, valid, dq);
             if (valid) {
 #pragma unroll 4
               for (int g = glo; g < ghi; ++g) {
@@ -538,7 +550,7 @@ __global__ void __launch_bounds__(320, 1)
                   v[0] += lo.x, v[1] += lo.y, v[2] += lo.z, v[3] += lo.w;
                   v[4] += hi.x, v[5] += hi.y, v[6] += hi.z, v[7] += hi.w;
                 }
-                emit(ybase, co0, v, mkv, orow);
+                emit(ybase, co0, v, mkv, orow, dq);
               }
             }
           }
@@ -556,7 +568,9 @@ __global__ void __launch_bounds__(320, 1)
     }
   }
   tc_fence_before();
+  if (HL && p.hl.counter) __threadfence();  // every thread's halo pushes, before the CTA counts itself
   __syncthreads();
+  if (HL && threadIdx.x == 0) halo_link_signal(p.hl);
   if (warp == 1) tmem_dealloc<512>(tbase);
 }
 
@@ -923,15 +937,19 @@ struct SwParams {
   unsigned flags;
   long long* dbg;  // optional cycle probes [gridDim][8] (vm_debug_set_fwd_probe)
   int xmode;       // experiment: 1 = skip the TMEM drain (wrong results)
+  HaloLink hl;     // fused peer-memory depth halo (vm_conv3d_fwd_tc_link)
 };
 constexpr int kSwMaxRing = 32;
 constexpr int kSwMaxStages = 8;
 
 // Warps: 0 producer, 1 and 10 MMA issuers (tiles t = 0, 2, .. and 1, 3, ..: a single issuing
 // thread's per-plane bookkeeping otherwise leaves the tensor core idle), 2..9 epilogue.
-template <int MB, bool DBG, int NG>  // NG = Nc/8 channel groups; DBG: cycle probes (tools/dbg_sweep_probe.py)
+// NG = Nc/8 channel groups; MODE 0: plain, 1: cycle probes (tools/dbg_sweep_probe.py),
+// 2: fused peer-memory halo (p.hl)
+template <int MB, int MODE, int NG>
 __global__ void __launch_bounds__(352, 1)
     k_conv_fwd_sweep(const SwParams p) {
+  constexpr bool DBG = MODE == 1, HL = MODE == 2;
   auto clk = []() -> long long { return DBG ? (long long)clock64() : 0LL; };
   constexpr int NW = MB >= 2 ? 2 : 1;  // MMA-issuing warps
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -966,6 +984,7 @@ __global__ void __launch_bounds__(352, 1)
     if (elect_one()) {
       mbar_arrive_expect_tx(&wbar, p.w_bytes);
       bulk_load(sW, p.wpk, p.w_bytes, &wbar);
+      if (HL) halo_link_wait(p.hl);  // the input's margins, pushed by the neighbours' producers
       int stage = 0;
       uint32_t phase = 0;
       long long t_pw = 0;
@@ -1278,7 +1297,14 @@ __global__ void __launch_bounds__(352, 1)
 #pragma unroll
                 for (int e = 0; e < 4; ++e) ow[e] = pack_bf16x2(v[2 * e], v[2 * e + 1]);
               }
-              if (valid[k]) *reinterpret_cast<int4*>(yb + g * p.plane8 + orow * 8) = out;
+              if (valid[k]) {
+                *reinterpret_cast<int4*>(yb + g * p.plane8 + orow * 8) = out;
+                // fused depth halo: layer 1 -> lo neighbour's layer D+1, layer D -> hi's layer 0
+                if (HL && p.hl.lo && o == 0)
+                  *reinterpret_cast<int4*>(p.hl.lo + (yb - p.y) + g * p.plane8 + (orow + (int64_t)p.D * p.P) * 8) = out;
+                if (HL && p.hl.hi && o == p.D - 1)
+                  *reinterpret_cast<int4*>(p.hl.hi + (yb - p.y) + g * p.plane8 + (orow - (int64_t)p.D * p.P) * 8) = out;
+              }
             }
           }
         }
@@ -1297,7 +1323,9 @@ __global__ void __launch_bounds__(352, 1)
     }
   }
   tc_fence_before();
+  if (HL && p.hl.counter) __threadfence();  // every thread's halo pushes, before the CTA counts itself
   __syncthreads();
+  if (HL && threadIdx.x == 0) halo_link_signal(p.hl);
   if (warp == 1) tmem_dealloc<512>(tbase);
 }
 
@@ -1672,6 +1700,7 @@ static int launch_sweep(const FwdParams& f, int nsm, void* stream) {
   p.Nc = f.Nc;
   p.flags = f.flags;
   p.dbg = f.dbg;
+  p.hl = f.hl;
   p.xmode = g_sweep_xmode;
   p.w_bytes = (uint32_t)p.KC * 9 * 2 * 3 * p.Nc * 16;
   const int static_smem = 2 * 1024;
@@ -1730,12 +1759,14 @@ static int launch_sweep(const FwdParams& f, int nsm, void* stream) {
   const bool dbg = p.dbg != nullptr;
   using SwKern = void (*)(const SwParams);
 #define SW_ROW(MB_)                                                                                   \
-  {k_conv_fwd_sweep<MB_, false, 2>, k_conv_fwd_sweep<MB_, false, 4>, k_conv_fwd_sweep<MB_, false, 6>, \
-   k_conv_fwd_sweep<MB_, true, 2>, k_conv_fwd_sweep<MB_, true, 4>, k_conv_fwd_sweep<MB_, true, 6>}
-  static const SwKern table[4][6] = {SW_ROW(1), SW_ROW(2), SW_ROW(3), SW_ROW(4)};
+  {k_conv_fwd_sweep<MB_, 0, 2>, k_conv_fwd_sweep<MB_, 0, 4>, k_conv_fwd_sweep<MB_, 0, 6>, \
+   k_conv_fwd_sweep<MB_, 1, 2>, k_conv_fwd_sweep<MB_, 1, 4>, k_conv_fwd_sweep<MB_, 1, 6>, \
+   k_conv_fwd_sweep<MB_, 2, 2>, k_conv_fwd_sweep<MB_, 2, 4>, k_conv_fwd_sweep<MB_, 2, 6>}
+  static const SwKern table[4][9] = {SW_ROW(1), SW_ROW(2), SW_ROW(3), SW_ROW(4)};
 #undef SW_ROW
   VM_REQUIRE(p.Nc == 16 || p.Nc == 32 || p.Nc == 48, VM_E_UNSUPPORTED, "sweep conv: Nc %d", p.Nc);
-  auto kern = table[p.MB - 1][(dbg ? 3 : 0) + p.Nc / 16 - 1];
+  const bool hl = p.hl.counter || p.hl.wait_own;
+  auto kern = table[p.MB - 1][(dbg ? 3 : hl ? 6 : 0) + p.Nc / 16 - 1];
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   launch_pdl(kern, grid, 352, smem, as_stream(stream), p);
   return launch_status("vm_conv3d_fwd_tc (sweep)");
@@ -1757,7 +1788,8 @@ extern "C" void vm_debug_set_fwd_max_split(int v) { g_fwd_max_split = v < 1 ? 1 
 
 static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, const float* bias, void* y,
                          int64_t y_bstride, const void* mask, int64_t mask_bstride, int B, int Cin, int Cout, int D,
-                         int H, int W, unsigned flags, void* ws, size_t ws_bytes, void* stream, int Dfull = 0);
+                         int H, int W, unsigned flags, void* ws, size_t ws_bytes, void* stream, int Dfull = 0,
+                         const vm_halo_link* link = nullptr);
 
 extern "C" int vm_conv3d_fwd_tc(const void* x, int64_t x_bstride, const void* wpacked,
                                 const float* bias, void* y, int64_t y_bstride, const void* mask,
@@ -1773,6 +1805,14 @@ extern "C" int vm_conv3d_fwd_tc_ws(const void* x, int64_t x_bstride, const void*
                                    size_t ws_bytes, void* stream) {
   return fwd_tc_launch(x, x_bstride, wpacked, bias, y, y_bstride, mask, mask_bstride, B, Cin, Cout, D, H, W, flags,
                        ws, ws_bytes, stream);
+}
+
+extern "C" int vm_conv3d_fwd_tc_link(const void* x, int64_t x_bstride, const void* wpacked, const float* bias,
+                                     void* y, int64_t y_bstride, const void* mask, int64_t mask_bstride, int B,
+                                     int Cin, int Cout, int D, int H, int W, unsigned flags, void* ws,
+                                     size_t ws_bytes, const vm_halo_link* link, void* stream) {
+  return fwd_tc_launch(x, x_bstride, wpacked, bias, y, y_bstride, mask, mask_bstride, B, Cin, Cout, D, H, W, flags,
+                       ws, ws_bytes, stream, 0, link);
 }
 
 // Output planes [d0, d0 + nd) of a slab with D interior planes: the conv of a plane reads
@@ -1810,8 +1850,13 @@ extern "C" size_t vm_conv3d_fwd_tc_ws_bytes(int B, int Cin, int Cout, int D, int
 // channel-group plane stride and the default batch strides come from Dfull.
 static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, const float* bias, void* y,
                          int64_t y_bstride, const void* mask, int64_t mask_bstride, int B, int Cin, int Cout, int D,
-                         int H, int W, unsigned flags, void* ws, size_t ws_bytes, void* stream, int Dfull) {
+                         int H, int W, unsigned flags, void* ws, size_t ws_bytes, void* stream, int Dfull,
+                         const vm_halo_link* link) {
   if (Dfull <= 0) Dfull = D;
+  VM_REQUIRE(!link || Dfull == D, VM_E_ARG, "vm_conv3d_fwd_tc_link: a halo link needs the full plane range");
+  VM_REQUIRE(!link || ((!link->push_lo && !link->push_hi) || (link->counter && link->epoch)) &&
+                          (!link->wait_own || link->epoch),
+             VM_E_ARG, "vm_conv3d_fwd_tc_link: incomplete halo link");
   VM_REQUIRE(x && wpacked && y, VM_E_ARG, "vm_conv3d_fwd_tc: null pointer");
   VM_REQUIRE((flags & VM_CONV_NOBIAS) || bias, VM_E_ARG, "vm_conv3d_fwd_tc: bias required");
   VM_REQUIRE(!(flags & VM_CONV_MASK) || mask, VM_E_ARG, "vm_conv3d_fwd_tc: mask required");
@@ -1819,6 +1864,7 @@ static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, 
              "vm_conv3d_fwd_tc: bad shape");
   PackGeom pg = pack_geom(Cin, Cout);
   FwdParams p{};
+  p.hl = halo_link_of(link);
   p.wpk = static_cast<const bf16*>(wpacked);
   p.bias = bias;
   p.y = static_cast<bf16*>(y);
@@ -1931,17 +1977,12 @@ static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, 
   const size_t smem = (size_t)p.stages * p.stage_bytes;
   int grid = p.units < nsm ? p.units : nsm;
   void (*kern)(const FwdParams) = nullptr;
-  const bool dbg = p.dbg != nullptr;
-  switch (p.MB) {
-    case 1: kern = dbg ? k_conv_fwd_tc<1, true> : k_conv_fwd_tc<1, false>; break;
-    case 2: kern = dbg ? k_conv_fwd_tc<2, true> : k_conv_fwd_tc<2, false>; break;
-    case 3: kern = dbg ? k_conv_fwd_tc<3, true> : k_conv_fwd_tc<3, false>; break;
-    case 4: kern = dbg ? k_conv_fwd_tc<4, true> : k_conv_fwd_tc<4, false>; break;
-    case 5: kern = dbg ? k_conv_fwd_tc<5, true> : k_conv_fwd_tc<5, false>; break;
-    case 6: kern = dbg ? k_conv_fwd_tc<6, true> : k_conv_fwd_tc<6, false>; break;
-    case 7: kern = dbg ? k_conv_fwd_tc<7, true> : k_conv_fwd_tc<7, false>; break;
-    default: kern = dbg ? k_conv_fwd_tc<8, true> : k_conv_fwd_tc<8, false>; break;
-  }
+  const int mode = p.dbg != nullptr ? 1 : (p.hl.counter || p.hl.wait_own) ? 2 : 0;
+#define FWD_ROW(M) {k_conv_fwd_tc<M, 0>, k_conv_fwd_tc<M, 1>, k_conv_fwd_tc<M, 2>}
+  static void (*const ftable[8][3])(const FwdParams) = {FWD_ROW(1), FWD_ROW(2), FWD_ROW(3), FWD_ROW(4),
+                                                        FWD_ROW(5), FWD_ROW(6), FWD_ROW(7), FWD_ROW(8)};
+#undef FWD_ROW
+  kern = ftable[(p.MB < 1 ? 1 : p.MB > 8 ? 8 : p.MB) - 1][mode];
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   launch_pdl(kern, grid, 320, smem, as_stream(stream), p);
   return launch_status("vm_conv3d_fwd_tc");

@@ -131,4 +131,65 @@ inline int64_t default_bstride(int C, int D, int H, int W, int m) {
   return (int64_t)((C + 7) / 8) * (D + 2 * m) * (H + 2 * m) * (W + 2 * m) * 8;
 }
 
+
+// ------------------------------------------------------------------ fused peer-memory halo
+// (vm_halo_link, include/vm_api.h): producer-side boundary-layer stores into the neighbours'
+// slabs + one system-scope publish per kernel; consumer-side wait for the own margins.
+struct HaloLink {
+  __nv_bfloat16* lo;  // lo neighbour's copy of the output slab (its layer D+1 receives our layer 1)
+  __nv_bfloat16* hi;  // hi neighbour's copy (its layer 0 receives our layer D)
+  int* lo_flag;
+  int* hi_flag;
+  unsigned* counter;
+  const int* wait_own;
+  int wait_lo, wait_hi;
+  const int* epoch;
+};
+
+inline HaloLink halo_link_of(const vm_halo_link* l) {
+  HaloLink h{};
+  if (l) {
+    h.lo = static_cast<__nv_bfloat16*>(l->push_lo), h.hi = static_cast<__nv_bfloat16*>(l->push_hi);
+    h.lo_flag = l->lo_flag, h.hi_flag = l->hi_flag, h.counter = l->counter;
+    h.wait_own = l->wait_own, h.wait_lo = l->wait_lo, h.wait_hi = l->wait_hi, h.epoch = l->epoch;
+  }
+  return h;
+}
+
+__device__ __forceinline__ int ld_acquire_sys_i32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// consumer: one thread spins (bounded, ~10 s; the error word epoch[1] records a timeout)
+__device__ __forceinline__ void halo_link_wait(const HaloLink& h) {
+  if (!h.wait_own || !(h.wait_lo | h.wait_hi)) return;
+  const int e = *(volatile const int*)h.epoch;
+  const long long t0 = clock64();
+  while ((h.wait_lo && ld_acquire_sys_i32(h.wait_own) < e) || (h.wait_hi && ld_acquire_sys_i32(h.wait_own + 1) < e)) {
+    __nanosleep(128);
+    if (clock64() - t0 > 20000000000LL) {
+      atomicExch(const_cast<int*>(h.epoch) + 1, e);
+      break;
+    }
+  }
+}
+
+// producer: called by thread 0 of every CTA after the CTA's last store (__syncthreads before).
+// Every CTA fences at GPU scope and counts itself; the last one publishes with ONE
+// system-scope fence (cumulative over the stores it observed through the counter).
+__device__ __forceinline__ void halo_link_signal(const HaloLink& h) {
+  if (!h.counter || !(h.lo || h.hi)) return;
+  __threadfence();
+  const unsigned nblocks = gridDim.x * gridDim.y * gridDim.z;
+  if (atomicAdd(h.counter, 1u) == nblocks - 1) {
+    *h.counter = 0;
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    const int e = *(volatile const int*)h.epoch;
+    if (h.lo) asm volatile("st.relaxed.sys.global.b32 [%0], %1;" ::"l"(h.lo_flag), "r"(e) : "memory");
+    if (h.hi) asm volatile("st.relaxed.sys.global.b32 [%0], %1;" ::"l"(h.hi_flag), "r"(e) : "memory");
+  }
+}
+
 }  // namespace vm

@@ -527,6 +527,23 @@ class SlabHalo:
             self.kernels.zero(s, self.nbr6)
 
 
+class HaloLinkC(ctypes.Structure):
+    """vm_halo_link (include/vm_api.h)."""
+
+    _fields_ = [("push_lo", ctypes.c_void_p), ("push_hi", ctypes.c_void_p), ("lo_flag", ctypes.c_void_p),
+                ("hi_flag", ctypes.c_void_p), ("counter", ctypes.c_void_p), ("wait_own", ctypes.c_void_p),
+                ("wait_lo", ctypes.c_int), ("wait_hi", ctypes.c_int), ("epoch", ctypes.c_void_p)]
+
+    @classmethod
+    def of(cls, push=None, wait=None):
+        if push is None and wait is None:
+            return None
+        f = dict(push or {})
+        for k, v in (wait or {}).items():
+            f[k] = v
+        return cls(**{k: v for k, v in f.items() if v is not None})
+
+
 class PeerDepthHalo:
     """Depth-only halo through peer memory (vm_halo_depth_push): no NCCL, no pack / unpack.
 
@@ -557,6 +574,7 @@ class PeerDepthHalo:
         self.peer_state = (self.state.data_ptr(), self.state.data_ptr()) if self_peers else (None, None)
         self.peer_slab = {}  # own slab pointer -> (lo neighbour's, hi neighbour's)
         self._slot = 0
+        self._pending = {}
         self._sent = 0
         # the weight-gradient kernels never read a depth margin layer of gy, so they may run
         # while this transport fills them (UNetStep overlaps wgrad with exchange + dgrad)
@@ -605,15 +623,13 @@ class PeerDepthHalo:
 
     def begin_step(self):
         self._slot = 0
+        self._pending = {}
         _lib.call("vm_halo_epoch_bump", _lib.ptr(self.state), _lib.stream_ptr())
 
     def forward(self, s, tag=_FWD_TAG):
         if not self.active:
             return
-        slot = self._slot
-        if slot >= self.NSLOT:
-            raise HaloError(f"peer-memory halo: more than {self.NSLOT} exchanges in one step")
-        self._slot += 1
+        slot = self._next_slot()
         lo_n, hi_n = self.nbr6[0] >= 0, self.nbr6[1] >= 0
         if self.self_peers:
             lo_p, hi_p = s.ptr, s.ptr
@@ -637,9 +653,47 @@ class PeerDepthHalo:
             raise HaloError(f"peer-memory halo: a neighbour's signal did not arrive (epoch {err})")
 
     def zero(self, s):
-        # the depth margins of a gradient slab are never read by the weight gradient (its gy
-        # maps cover the interior depth planes only); H / W are not split
-        pass
+        """Zero the exchanged depth margins (the serial path of a transport user whose weight
+        gradient reads them; the tensor-core wgrad never does)."""
+        if self.active:
+            _lib.call("vm_halo_slab_zero", _lib.dtype_code(s.dtype), s.p(), s.bstride, s.B, s.C, s.D, s.H, s.W,
+                      (ctypes.c_int * 6)(*self.nbr6), _lib.stream_ptr())
+
+    # ---- fused exchanges (the producer conv pushes, the consumer conv waits) ------------
+    def reserve_push(self, y):
+        """Producer side: the next exchange slot for slab ``y``, whose producer kernel pushes
+        its boundary layers itself; returns the vm_halo_link fields of that push."""
+        if not self.active:
+            return None
+        slot = self._next_slot()
+        self._pending[y.ptr] = slot
+        lo_n, hi_n = self.nbr6[0] >= 0, self.nbr6[1] >= 0
+        lo_p, hi_p = (y.ptr, y.ptr) if self.self_peers else self.peer_slab[y.ptr]
+        base = self.state.data_ptr()
+        self._sent += y.B * y.CG * 8 * y.H * y.W * y.storage.element_size() * (lo_n + hi_n)
+        return dict(push_lo=lo_p if lo_n else None, push_hi=hi_p if hi_n else None,
+                    lo_flag=self.peer_state[0] + 4 * (8 + 2 * slot + 1) if lo_n else None,
+                    hi_flag=self.peer_state[1] + 4 * (8 + 2 * slot) if hi_n else None,
+                    counter=base + 4 * (8 + 2 * self.NSLOT + slot), epoch=base)
+
+    def consume(self, s):
+        """Consumer side of a conv input: the slot a fused producer pushed ``s`` under (the
+        consumer kernel waits on it: vm_halo_link wait fields), or None after a standalone
+        push here (vm_halo_depth_push, which waits itself)."""
+        slot = self._pending.pop(s.ptr, None)
+        if slot is None:
+            self.forward(s)
+            return None
+        base = self.state.data_ptr()
+        return dict(wait_own=base + 4 * (8 + 2 * slot), wait_lo=int(self.nbr6[0] >= 0),
+                    wait_hi=int(self.nbr6[1] >= 0), epoch=base)
+
+    def _next_slot(self):
+        slot = self._slot
+        if slot >= self.NSLOT:
+            raise HaloError(f"peer-memory halo: more than {self.NSLOT} exchanges in one step")
+        self._slot += 1
+        return slot
 
 
 def nccl_comm_ptr(group=None):

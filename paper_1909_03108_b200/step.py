@@ -29,7 +29,7 @@ import torch
 
 from . import _lib
 from .errors import GraphBuildError, VoxmeshError
-from .halo import PeerDepthHalo, SlabHalo, nccl_comm_of, nccl_second_comm
+from .halo import HaloLinkC, PeerDepthHalo, SlabHalo, nccl_comm_of, nccl_second_comm
 
 _DT = {torch.bfloat16: _lib.VM_BF16, torch.float32: _lib.VM_F32}
 
@@ -149,6 +149,7 @@ class UNetStep:
         self.overlap_halo = True
         self.overlap_min_planes = 32  # tools/halo_ab.py: the boundary launches cost more below
         self.halo_sm_reserve = 8  # SMs the interior conv leaves to the overlapped exchange
+        self.fuse_halo = True  # peer transport: producer convs push their boundary layers themselves
         self.bucket_bytes = 16 << 20
         bdiv = mesh.axis_size(layout.axis_for("batch")) if (layout is not None and layout.axis_for("batch")) else 1
         self.global_batch = global_batch or batch * bdiv
@@ -362,7 +363,25 @@ class UNetStep:
     def _conv_flops(self, L):
         return 2.0 * self.B * L.D * L.H * L.W * 27 * L.cin * L.cout
 
-    def _conv(self, x, L, y, flags, mask=None, dgrad=False, planes=None):
+    def _fused_halo(self):
+        """Peer-memory depth halo fused into the tensor-core convs (producer epilogue pushes,
+        consumer waits): the transport and the conv path support it."""
+        return (self.has_halo and self.fuse_halo and self.conv_impl == "tc"
+                and isinstance(self.halo, PeerDepthHalo))
+
+    def _exchanged_ptrs(self):
+        """Slabs exchanged whole before a k=3 conv / dgrad reads them (fused-push candidates)."""
+        if getattr(self, "_xptrs", None) is None:
+            ptrs = set()
+            for n in self.graph.nodes:
+                if n.op == "conv" and n.k == 3:
+                    ptrs.add(self.out[n.inputs[0]].ptr)
+                    if n.inputs[0] != "input":
+                        ptrs.add(self.gpre[n.id].ptr)
+            self._xptrs = ptrs
+        return self._xptrs
+
+    def _conv(self, x, L, y, flags, mask=None, dgrad=False, planes=None, wait=None):
         cin, cout = (L.cout, L.cin) if dgrad else (L.cin, L.cout)
         mp = mask.p() if mask is not None else None
         mb = mask.bstride if mask is not None else 0
@@ -381,9 +400,21 @@ class UNetStep:
                     _lib.ptr(L.w), _lib.ptr(L.b), y.p(), y.bstride, self.B, cout, L.D, L.H, L.W, flags)
         elif self.conv_impl == "tc":
             w = L.wpt if dgrad else L.wp
-            self._k(kind, L.node.id, self._conv_flops(L), nbytes, "vm_conv3d_fwd_tc_ws", x.p(), x.bstride,
-                    _lib.ptr(w), _lib.ptr(L.b), y.p(), y.bstride, mp, mb, self.B, cin, cout, L.D, L.H, L.W, flags,
-                    _lib.ptr(self.conv_ws), self.conv_ws_bytes)
+            push = None
+            if self._fused_halo() and y.ptr in self._exchanged_ptrs():
+                push = self.halo.reserve_push(y)  # this conv pushes y's boundary layers itself
+            link = HaloLinkC.of(push, wait)
+            if link is not None:
+                if getattr(self, "_links", None) is None:
+                    self._links = {}
+                self._links[(L.index, dgrad)] = link  # alive for recorded re-launches (profile_kernels)
+                self._k(kind, L.node.id, self._conv_flops(L), nbytes, "vm_conv3d_fwd_tc_link", x.p(), x.bstride,
+                        _lib.ptr(w), _lib.ptr(L.b), y.p(), y.bstride, mp, mb, self.B, cin, cout, L.D, L.H, L.W,
+                        flags, _lib.ptr(self.conv_ws), self.conv_ws_bytes, ctypes.addressof(link))
+            else:
+                self._k(kind, L.node.id, self._conv_flops(L), nbytes, "vm_conv3d_fwd_tc_ws", x.p(), x.bstride,
+                        _lib.ptr(w), _lib.ptr(L.b), y.p(), y.bstride, mp, mb, self.B, cin, cout, L.D, L.H, L.W,
+                        flags, _lib.ptr(self.conv_ws), self.conv_ws_bytes)
         else:
             w = L.wt if dgrad else L.w
             self._k(kind, L.node.id, self._conv_flops(L), nbytes, "vm_conv3d_fwd_simt", self.dt, x.p(), x.bstride,
@@ -519,6 +550,12 @@ class UNetStep:
     def _halo_conv(self, x, L, y, flags, mask=None, dgrad=False, tag="halo"):
         """Halo of ``x`` then conv(x): with a depth-only split the exchange runs on the comm
         stream while the interior output planes compute, then the two boundary planes."""
+        if self._fused_halo() and not (L.c1 and not dgrad):
+            # the producer of x pushed its boundary layers (the conv waits for the
+            # neighbours' pushes), or a standalone push runs here
+            wait = self.halo.consume(x)
+            self._conv(x, L, y, flags, mask=mask, dgrad=dgrad, wait=wait)
+            return
         if not self._split_planes(L.D) or (L.c1 and not dgrad):
             self._halo(x, tag)
             self._conv(x, L, y, flags, mask=mask, dgrad=dgrad)

@@ -155,3 +155,44 @@ def test_peer_step_equals_nccl_step_eager_and_graph(comms):
     torch.cuda.synchronize()
     assert torch.equal(eager.params, capt.params) and torch.equal(eager.stats, capt.stats)
     assert int(capt.halo.state[0].item()) >= 3
+
+
+def test_fused_push_step_equals_standalone_push_step():
+    # the producer convs push their boundary layers from the epilogue (vm_conv3d_fwd_tc_link)
+    # == every exchange as a standalone vm_halo_depth_push; eager and graph; several levels
+    E = 32
+    cfg = vm.UNetConfig(E, (16, 32, 64), convs_per_block=2)
+    mesh = vm.create_mesh([("one", 1)])
+    graph = vm.build(cfg, mesh, {})
+    params = vm.init_params(graph, 3)
+    img, lab = O.record_for(E, 2)
+    host = (torch.from_numpy(img[None, ..., None].copy()), torch.from_numpy(lab[None].copy()))
+
+    def make(fuse):
+        st = UNetStep(graph, params, dtype=torch.bfloat16, device="cuda")
+        st.use_peer_halo(nbr6=[0, 0, -1, -1, -1, -1])
+        st.fuse_halo = fuse
+        st.keep_probs = True
+        st.upload(*host)
+        return st
+
+    runs = {}
+    for fuse in (False, True):
+        st = make(fuse)
+        st.forward()
+        st.backward()
+        torch.cuda.synchronize()
+        st.halo.check()
+        if fuse:
+            assert len(st._links) > 0  # fused links were used
+        runs[fuse] = (st.probs.cpu(), st.stats.cpu(), st.grads.cpu())
+    for a, b in zip(runs[False], runs[True]):
+        assert torch.equal(a, b)
+    eager, capt = make(True), make(True)
+    g = capt.capture()
+    for _ in range(3):
+        eager.step()
+        g.replay()
+    torch.cuda.synchronize()
+    capt.halo.check()
+    assert torch.equal(eager.params, capt.params) and torch.equal(eager.stats, capt.stats)

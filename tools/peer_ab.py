@@ -56,3 +56,19 @@ for rep in range(2):
               f"graph no-side {variant(halo, True, False):.3f} ms", flush=True)
 st.has_halo = True
 st.halo.check()
+
+# both programs captured first, then timed alternately (the bench.py pattern)
+gs = {}
+for halo in (True, False):
+    st.has_halo = halo
+    gs[halo] = st.capture()
+for rep in range(2):
+    for halo in (True, False):
+        print(f"both-captured rep {rep} halo={halo}: {timeit(gs[halo].replay):.3f} ms", flush=True)
+del gs
+gs = {}
+for halo in (False, True):
+    st.has_halo = halo
+    gs[halo] = st.capture()
+for halo in (True, False):
+    print(f"both-captured (nohalo first) halo={halo}: {timeit(gs[halo].replay):.3f} ms", flush=True)
