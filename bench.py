@@ -95,6 +95,8 @@ def args_parse():
     p.add_argument("--emulate-split", type=int, default=8, help="N = 1: depth split whose rank block is emulated")
     p.add_argument("--emulate-transport", default="peer", choices=["peer", "nccl"],
                    help="N = 1: halo transport of the emulated split")
+    p.add_argument("--halo-transport", default="peer", choices=["peer", "nccl"],
+                   help="N > 1, depth-only split: peer-memory pushes (CUDA IPC) or NCCL send/recv")
     p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     p.add_argument("--cpu-budget", type=float, default=150.0, help="seconds of CPU-oracle time (reference arm)")
     p.add_argument("--layer-csv", default=None, help="write per-layer kernel times here")
@@ -431,6 +433,14 @@ def run_ours(a):
     bdiv = mesh.axis_size(layout["batch"]) if "batch" in layout else 1
     st = UNetStep(graph, params, batch=B // bdiv, ctx=ctx, dtype=torch.bfloat16, conv_impl=a.conv,
                   global_batch=B)
+    transport = "none" if world == 1 else "nccl (pack / send-recv group / unpack per phase)"
+    if world > 1 and a.halo_transport == "peer" and st.has_halo and max(st.halo.nbr6[2:]) < 0:
+        try:  # depth-only split: boundary layers pushed from the conv epilogues over NVLink P2P
+            st.use_peer_halo()
+            transport = "peer (CUDA-IPC mapped neighbour slabs, pushes fused into the conv epilogues)"
+        except Exception as e:  # every rank falls back together (decided collectively)
+            print(f"[bench] !!! peer-memory halo unavailable ({e}); NCCL transport", file=sys.stderr, flush=True)
+            transport = f"nccl (peer-memory halo failed: {type(e).__name__})"
     recs = [synth_record(E, 7, i) for i in range(B)]
     img = np.stack([r[0] for r in recs])[..., None]
     lab = np.stack([r[1] for r in recs])
@@ -576,8 +586,7 @@ def run_ours(a):
         "run": {"conv": a.conv, "cuda_graph": graph_note, "memory_gb_peak": round(act_gb, 1),
                 "l2": f"working set {act_gb:.1f} GB >> 126 MB L2; no flush needed",
                 "conv_tflop_per_step_rank": conv_flops_rank / 1e12,
-                "transport": "NCCL via C ABI (vm_halo_slab_fwd / vm_allreduce_f32)" if st.comm is not None
-                             else ("none" if world == 1 else "host")},
+                "transport": transport + ("; collectives: NCCL via C ABI (vm_allreduce_f32)" if world > 1 else "")},
         "parity": parity,
         "e2e": {"value": voxels / (ms_e2e * 1e-3), "unit": "voxels/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e, "loss": losses[-1][0],

@@ -408,9 +408,9 @@ __global__ void __launch_bounds__(256) k_depth_push(const DepthPush p) {
       }
       if (dbg & 2) return;
       // bounded wait (~10 s): a neighbour that never signals sets the error word epoch[1]
-      // instead of hanging the device
+      // instead of hanging the device (and later waits fail fast)
       const long long t0 = clock64();
-      while ((p.wait_lo && ld_acquire_sys(p.own) < e) || (p.wait_hi && ld_acquire_sys(p.own + 1) < e)) {
+      while (!p.epoch[1] && (p.wait_lo && ld_acquire_sys(p.own) < e) || (p.wait_hi && ld_acquire_sys(p.own + 1) < e)) {
         __nanosleep(128);
         if (clock64() - t0 > 20000000000LL) {
           atomicExch(const_cast<int*>(p.epoch) + 1, e);
@@ -497,6 +497,7 @@ extern "C" int vm_ipc_handle(const void* ptr, void* handle64, int64_t* offset) {
              VM_E_ARG, "vm_ipc_handle: not a device allocation");
   cudaIpcMemHandle_t h;
   cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) cudaGetLastError();
   VM_REQUIRE(e == cudaSuccess, 100 + (int)e, "vm_ipc_handle: cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
   memcpy(handle64, &h, sizeof(h));
   *offset = (int64_t)(reinterpret_cast<uintptr_t>(ptr) - (uintptr_t)base);
@@ -524,6 +525,7 @@ extern "C" int vm_ipc_open(const void* handle64, void** base) {
   memcpy(&h, handle64, sizeof(h));
   void* p = nullptr;
   cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) cudaGetLastError();  // not sticky: clear it for later launches
   VM_REQUIRE(e == cudaSuccess, 100 + (int)e, "vm_ipc_open: cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
   memcpy(g_ipc[g_nipc].key, handle64, 64);
   g_ipc[g_nipc++].base = p;

@@ -165,6 +165,7 @@ __device__ __forceinline__ int ld_acquire_sys_i32(const int* p) {
 // consumer: one thread spins (bounded, ~10 s; the error word epoch[1] records a timeout)
 __device__ __forceinline__ void halo_link_wait(const HaloLink& h) {
   if (!h.wait_own || !(h.wait_lo | h.wait_hi)) return;
+  if (*(volatile const int*)(h.epoch + 1)) return;  // an earlier wait timed out: fail fast
   const int e = *(volatile const int*)h.epoch;
   const long long t0 = clock64();
   while ((h.wait_lo && ld_acquire_sys_i32(h.wait_own) < e) || (h.wait_hi && ld_acquire_sys_i32(h.wait_own + 1) < e)) {

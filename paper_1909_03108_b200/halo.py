@@ -614,8 +614,18 @@ class PeerDepthHalo:
                 out.append(int(base.value) + off)
             return out
 
-        lo = open_(self.nbr6[0]) if self.nbr6[0] >= 0 else None
-        hi = open_(self.nbr6[1]) if self.nbr6[1] >= 0 else None
+        err = None
+        try:
+            lo = open_(self.nbr6[0]) if self.nbr6[0] >= 0 else None
+            hi = open_(self.nbr6[1]) if self.nbr6[1] >= 0 else None
+        except Exception as e:  # noqa: BLE001 - decided collectively below
+            err = e
+        import torch
+
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=self.state.device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)  # every rank takes the same transport
+        if not int(ok.item()):
+            raise HaloError(f"peer-memory halo: CUDA-IPC mapping failed on some rank ({err or 'elsewhere'})")
         self.peer_state = (lo[0] if lo else None, hi[0] if hi else None)
         for i, s in enumerate(slabs):
             self.peer_slab[s.ptr] = (lo[1 + i] if lo else None, hi[1 + i] if hi else None)

@@ -498,6 +498,8 @@ class UNetStep:
         emulate = nbr6 is not None
         if not emulate:
             peer = PeerDepthHalo(self.halo.nbr6, self.device, self_peers=False)
+            if peer.active:
+                peer.connect(self._halo_slabs(), group)  # collective: every rank calls it
         else:
             peer = PeerDepthHalo(nbr6, self.device, self_peers=True)
             for i in range(3):
@@ -510,8 +512,6 @@ class UNetStep:
             for L in self.layers:
                 L.c1 = False
             self.input_slab_needed = True
-        if not emulate and peer.active:
-            peer.connect(self._halo_slabs(), group)
 
     def _halo_slabs(self):
         slabs = [self.out[n.inputs[0]] for n in self.graph.nodes if n.op == "conv" and n.k == 3]
@@ -745,9 +745,6 @@ class UNetStep:
                 self.step()
         cur.wait_stream(s)
         return g
-
-    def graph_capturable(self):
-        return False
 
     def launch_host_step(self, image_np, labels_np, replay=None):
         """Stage numpy host blocks -> pinned -> device, run one step, start the D2H of its

@@ -196,3 +196,15 @@ def test_fused_push_step_equals_standalone_push_step():
     torch.cuda.synchronize()
     capt.halo.check()
     assert torch.equal(eager.params, capt.params) and torch.equal(eager.stats, capt.stats)
+
+
+def test_ipc_connect_failure_is_collective_and_clean(comms):
+    # a CUDA-IPC handle cannot be opened by the process that exported it: connect() must
+    # report a HaloError on every rank (here: the only one) instead of leaving a half-mapped
+    # transport, so the caller can fall back to NCCL together
+    from paper_1909_03108_b200.errors import HaloError
+
+    s = Slab(1, 16, 4, 6, 8, torch.bfloat16, "cuda")
+    halo = PeerDepthHalo([0, 0, -1, -1, -1, -1], "cuda", self_peers=False)
+    with pytest.raises(HaloError):
+        halo.connect([s])
