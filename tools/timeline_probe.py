@@ -19,7 +19,6 @@ import paper_1909_03108_b200 as vm  # noqa: E402
 from paper_1909_03108_b200 import _lib  # noqa: E402
 from paper_1909_03108_b200.data import synth_record  # noqa: E402
 from paper_1909_03108_b200.step import UNetStep  # noqa: E402
-from bench import _capture  # noqa: E402
 
 pdl = int(os.environ.get("PDL_FWD", "1"))
 cfg = vm.recipe_for_resolution(128, 1 / 8)
@@ -34,8 +33,22 @@ st.step()
 torch.cuda.synchronize()
 
 
+def _capture(fn):
+    import gc
+
+    gc.collect()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    return g
+
+
 def timed(fn, reps=30):
-    g = _capture(torch, fn)
+    g = _capture(fn)
     for _ in range(3):
         g.replay()
     torch.cuda.synchronize()
