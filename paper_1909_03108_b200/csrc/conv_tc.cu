@@ -91,7 +91,9 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 //  * plain  (k_conv_fwd_tc):    [nchunk][kc][kd][9 taps (kh,kw)][2 K-halves][Nc][8],
 //                               co = nchunk*Nc + n;
 //  * sweep  (k_conv_fwd_sweep): [kc][9 taps (kh,kw)][2 K-halves][3*Nc][8], row n holds
-//                               kd = 2 - n / Nc, co = n % Nc (thin outputs, Nc <= 48).
+//                               kd = 2 - n / Nc, co = n % Nc (thin outputs, Nc <= 48);
+//  * sweep-kw (k_conv_fwd_sweepkw, Nc = 16): [kc][3 kh][2 K-halves][144][8], row n holds
+//                               kd = 2 - n / 48, kw = n % 48 / 16, co = n % 16.
 // flip = 1 packs the dgrad operand W'[t'][ci'][co'] = W[26 - t'][co'][ci'] (conv of the
 // output gradient).  Both layouts hold the same number of elements.
 struct PackGeom {
@@ -104,6 +106,7 @@ struct PackGeom {
 constexpr int kSweepMaxNc = 48;  // Nc = 48 (16->48 dgrad): 141 -> 91 us vs k_conv_fwd_tc
 constexpr uint32_t kSweepMaxWeightBytes = 100 * 1024;
 constexpr bool kSweepEnabled = true;
+constexpr bool kSweepKw = true;  // Nc = 16: the kd-and-kw-stacked sweep (N = 144)
 
 __host__ __device__ static PackGeom pack_geom(int cin, int cout) {
   PackGeom g;
@@ -116,6 +119,10 @@ __host__ __device__ static PackGeom pack_geom(int cin, int cout) {
   g.Nc = ((npad + g.nchunk - 1) / g.nchunk + 15) / 16 * 16;
   const uint32_t wbytes = (uint32_t)g.KC * 9 * 2 * 3 * g.Nc * 16;
   g.sweep = (kSweepEnabled && g.nchunk == 1 && g.Nc <= kSweepMaxNc && wbytes <= kSweepMaxWeightBytes) ? 1 : 0;
+  // kd and kw along N (k_conv_fwd_sweepkw) when a plane has >= 2 K chunks: with one chunk the
+  // per-plane MMA work (3 x 2 MMAs) is shorter than the kw-recombining drain of the block it
+  // frees (16->16 at 128^3: 67 us vs 52 with k_conv_fwd_sweep; 48->16: 93 vs 123 us)
+  if (g.sweep && g.Nc == 16 && g.KC >= 2 && kSweepKw) g.sweep = 2;
   return g;
 }
 
@@ -125,7 +132,17 @@ __device__ __forceinline__ float pack_value(const PackGeom& g, int64_t r, const 
   const int e = r % 8;
   r /= 8;
   int kd, kh, kw, kc, co, half;
-  if (g.sweep) {
+  if (g.sweep == 2) {  // [kc][3 kh][2 halves][144: (kd = 2 - n/48, kw = n%48/16, co = n%16)][8]
+    const int n = r % 144;
+    r /= 144;
+    half = r % 2;
+    r /= 2;
+    kh = r % 3;
+    kc = (int)(r / 3);
+    kd = 2 - n / 48;
+    kw = (n % 48) / 16;
+    co = n % 16;
+  } else if (g.sweep) {
     const int n = r % (3 * g.Nc);
     r /= 3 * g.Nc;
     half = r % 2;
@@ -288,10 +305,13 @@ __global__ void __launch_bounds__(320, 1)
       t_wait_tmem += clk() - tw0;
       tc_fence_after();
       const int s0 = (u % p.ksplit) * p.spk, s1 = min(nstage_k, s0 + p.spk);
+      // accumulator set of tap j = j % nacc (nacc in {1, 3}): consecutive MMAs of a tile go to
+      // different sets, so MB * nacc independent chains are in flight (a single chain of the 9
+      // taps of a stage ran at ~100 cycles per N = 128 MMA against a 64-cycle bound)
+      const uint32_t setcol = p.nacc == 3 ? (uint32_t)p.Nc : 0u;
       for (int s = s0; s < s1; ++s) {
         const int kc = s / 3;
         const int ng = (kc * 2 + 1 < p.CG) ? 2 : 1;
-        const int aset = (s - s0) % p.nacc;  // consecutive stages feed different accumulators
         long long tf0 = clk();
         mbar_wait(&full[stage], phase);
         t_wait_full += clk() - tf0;
@@ -304,19 +324,20 @@ __global__ void __launch_bounds__(320, 1)
           const uint64_t a0desc = make_sdesc(sA, lbo_a, 128);
           const uint64_t b0desc = make_sdesc(sB, p.Nc * 16, 128);
           // TMEM column of (buffer ab, tile i, set a) = ((ab*MB + i)*nacc + a)*Nc
-          const uint32_t d0 = tbase + (uint32_t)((ab * p.MB * p.nacc + aset) * p.Nc);
+          const uint32_t d0 = tbase + (uint32_t)(ab * p.MB * p.nacc * p.Nc);
           const uint32_t tstep = (uint32_t)(p.nacc * p.Nc);
           const uint32_t bstep = (uint32_t)(2 * p.Nc * 16) >> 4;
-          const uint32_t acc0 = s - s0 >= p.nacc ? 1u : 0u;
+          const bool first = s == s0;  // the unit's first stage overwrites each set once
           const uint32_t wp1 = (uint32_t)p.Wp;
 #pragma unroll
           for (int j = 0; j < 9; ++j) {
             const uint64_t bdesc = b0desc + (uint64_t)(j * bstep);
             const uint64_t adesc = a0desc + (uint64_t)((j / 3) * wp1 + (j % 3));
-            const uint32_t acc = j > 0 ? 1u : acc0;
+            const uint32_t acc = (first && (j == 0 || (j < 3 && setcol != 0u))) ? 0u : 1u;
+            const uint32_t dj = d0 + (uint32_t)(j % 3) * setcol;
 #pragma unroll
             for (int i = 0; i < MB; ++i)
-              mma_bf16_ss(d0 + (uint32_t)i * tstep, adesc + (uint64_t)(i * 128), bdesc, p.idesc, acc);
+              mma_bf16_ss(dj + (uint32_t)i * tstep, adesc + (uint64_t)(i * 128), bdesc, p.idesc, acc);
           }
           mma_commit(&empty[stage]);
         }
@@ -429,7 +450,7 @@ __global__ void __launch_bounds__(320, 1)
       const int b = tu / (p.nchunk * p.mblocks);
       const int a0 = mb * p.MB * 128;
       const int s0 = ks * p.spk, nst = min(3 * p.KC, s0 + p.spk) - s0;
-      const int nsets = min(p.nacc, nst);  // accumulator sets this split wrote
+      const int nsets = nst > 0 ? p.nacc : 0;  // taps rotate over the sets: all of them written
       const bool split = p.ksplit > 1;
       const bf16* mbase = p.mask + b * p.m_bstride;
       bf16* ybase = p.y + b * p.y_bstride;
@@ -1329,6 +1350,367 @@ __global__ void __launch_bounds__(352, 1)
   if (warp == 1) tmem_dealloc<512>(tbase);
 }
 
+// ------------------------------------------------------------------ forward / dgrad, Nc = 16, kd AND kw along N
+// k_conv_fwd_sweep with the kw taps moved from the A side to the B side as well: B rows =
+// (kd = 2, 1, 0) x (kw = 0..2) x 16 output channels, N = 144, so one MMA per (kh, K chunk)
+// covers 9 taps (3 per input plane and K chunk instead of 9, the A tile read once per 144
+// outputs instead of per 48: the SS-mode A-operand read no longer bounds the MMA).  The kw
+// taps are recombined in the epilogue: the D row of input anchor a holds its kw contribution
+// to output anchor a - kw, so out[j] = D0[j] + D1[j+1] + D2[j+2] (lane shuffles, and 2 rows
+// through shared memory across TMEM lane quarters).  Tiles advance by 126 anchors (the last
+// two rows of a 128-row tile only feed outputs of the next tile).  A drained ring block is
+// zeroed by the epilogue (tcgen05.st), so every MMA accumulates (no overwrite split).
+// TMEM: MB tiles x ring blocks x 48 columns (kw-block width).
+constexpr int kKwTile = 126;
+// warps: 0 TMA producer, 1-2 MMA issuers (tile 0 / 1), 3-18 epilogue: 4 per TMEM lane quarter,
+// one (tile, channel group) slot each (the drain is latency-bound: 16 warps, 4 per SMSP)
+constexpr int kKwThreads = 19 * 32;
+template <int MB, int MODE>
+__global__ void __launch_bounds__(kKwThreads, 1)
+    k_conv_fwd_sweepkw(const SwParams p) {
+  constexpr bool DBG = MODE == 1, HL = MODE == 2;
+  auto clk = []() -> long long { return DBG ? (long long)clock64() : 0LL; };
+  constexpr int NW = MB >= 2 ? 2 : 1;  // MMA-issuing warps
+  constexpr int BW = 48;               // TMEM columns per ring block: 3 kw x 16 co
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t full[kSwMaxStages], empty[kSwMaxStages], tfull[kSwMaxRing], tempty[kSwMaxRing], wbar;
+  __shared__ uint32_t tslot;
+  __shared__ __align__(16) float sbias[16];
+  // row exchange across TMEM lane quarters: [slot][parity][quarter][lane0 kw1, lane0 kw2, lane1 kw2][8]
+  __shared__ __align__(16) float xch[4][2][4][3][8];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  uint8_t* sW = smem;
+  uint8_t* sStage = smem + p.w_bytes;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    for (int r = 0; r < p.ring; ++r) {
+      mbar_init(&tfull[r], NW);
+      mbar_init(&tempty[r], 512);
+    }
+    mbar_init(&wbar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tslot;
+  pdl_wait();
+  if (!(p.flags & kFlagPdlLate)) pdl_trigger();
+
+  if (warp == 0) {
+    // ===================== producer: resident weights, then one stage per (plane, K chunk)
+    if (elect_one()) {
+      mbar_arrive_expect_tx(&wbar, p.w_bytes);
+      bulk_load(sW, p.wpk, p.w_bytes, &wbar);
+      if (HL) halo_link_wait(p.hl);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const int col = u % p.ncol;
+        const int seg = (u / p.ncol) % p.nseg;
+        const int b = u / (p.ncol * p.nseg);
+        const int o0 = seg * p.S, o1 = min(p.D, o0 + p.S);
+        const int64_t c0 = (int64_t)col * MB * kKwTile;
+        const bf16* xb = p.x + b * p.x_bstride;
+        for (int i = o0; i < o1 + 2; ++i) {
+          for (int kc = 0; kc < p.KC; ++kc) {
+            const int ng = (kc * 2 + 1 < p.CG) ? 2 : 1;
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sA = sStage + (size_t)stage * p.stage_bytes;
+            mbar_arrive_expect_tx(&full[stage], (uint32_t)ng * p.R * 16);
+            for (int g = 0; g < ng; ++g)
+              bulk_load(sA + (size_t)g * p.a_bytes, xb + (kc * 2 + g) * p.plane8 + ((int64_t)i * p.P + c0) * 8,
+                        (uint32_t)p.R * 16, &full[stage]);
+            if (++stage == p.stages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1 || warp == 2) {
+    // ===================== MMA issuers (warp 1: tile 0, warp 2: tile 1)
+    const int mw = warp - 1;
+    if (mw < NW) {
+      const long long t0 = clk();
+      long long t_te = 0, t_fu = 0, t_is = 0;
+      mbar_wait(&wbar, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t nstart = 0, acquired = 0, acq_slot = 0, acq_phase = 0, pos = 0;
+      const uint32_t wblk = (uint32_t)(2 * 144 * 16);  // bytes per (kc, kh) weight block
+      const uint32_t sWa = smem_u32(sW);
+      const uint32_t ring = (uint32_t)p.ring;
+      const uint32_t tcol0 = tbase + (uint32_t)(mw * p.ring * BW);  // this warp's tile
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const int seg = (u / p.ncol) % p.nseg;
+        const int o0 = seg * p.S, o1 = min(p.D, o0 + p.S);
+        const int nin = o1 - o0 + 2;
+        for (int k = 0; k < nin; ++k) {
+          const uint32_t n = nstart + (uint32_t)k;
+          const long long ta = clk();
+          while (acquired <= n + 2) {
+            mbar_wait(&tempty[acq_slot], acq_phase);
+            ++acquired;
+            if (++acq_slot == ring) {
+              acq_slot = 0;
+              acq_phase ^= 1u;
+            }
+          }
+          t_te += clk() - ta;
+          tc_fence_after();
+          // blocks pos, pos+1, pos+2 (output planes i-2, i-1, i) <- B rows [0,48), [48,96), [96,144)
+          const uint32_t d0 = tcol0 + pos * BW;
+          const int wrap = pos + 3 <= ring ? 0 : (pos + 2 == ring ? 2 : 1);  // blocks before the ring end
+          for (int kc = 0; kc < p.KC; ++kc) {
+            const int ng = (kc * 2 + 1 < p.CG) ? 2 : 1;
+            const long long tf = clk();
+            mbar_wait(&full[stage], phase);
+            const long long tf1 = clk();
+            t_fu += tf1 - tf;
+            tc_fence_after();
+            if (elect_one()) {
+              const uint32_t sA = smem_u32(sStage + (size_t)stage * p.stage_bytes);
+              const uint64_t a0desc = make_sdesc(sA, ng == 2 ? p.a_bytes : 0, 128) + (uint64_t)(mw * kKwTile);
+              const uint64_t b0desc = make_sdesc(sWa + (uint32_t)kc * 3 * wblk, 144 * 16, 128);
+              const uint32_t wp1 = (uint32_t)p.Wp, wstep = wblk >> 4;
+              if (wrap == 0) {
+#pragma unroll
+                for (int kh = 0; kh < 3; ++kh)
+                  mma_bf16_ss(d0, a0desc + (uint64_t)(kh * wp1), b0desc + (uint64_t)(kh * wstep), p.idesc3, 1u);
+              } else if (wrap == 2) {  // blocks pos, pos+1 | 0
+#pragma unroll
+                for (int kh = 0; kh < 3; ++kh) {
+                  const uint64_t ad = a0desc + (uint64_t)(kh * wp1), bd = b0desc + (uint64_t)(kh * wstep);
+                  mma_bf16_ss(d0, ad, bd, p.idesc2, 1u);
+                  mma_bf16_ss(tcol0, ad, bd + 96, p.idesc1, 1u);
+                }
+              } else {  // block pos | 0, 1
+#pragma unroll
+                for (int kh = 0; kh < 3; ++kh) {
+                  const uint64_t ad = a0desc + (uint64_t)(kh * wp1), bd = b0desc + (uint64_t)(kh * wstep);
+                  mma_bf16_ss(d0, ad, bd, p.idesc1, 1u);
+                  mma_bf16_ss(tcol0, ad, bd + 48, p.idesc2, 1u);
+                }
+              }
+              mma_commit(&empty[stage]);
+            }
+            __syncwarp();
+            t_is += clk() - tf1;
+            if (++stage == p.stages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          const uint32_t p1 = pos + 1 == ring ? 0u : pos + 1;
+          if (elect_one()) {
+            mma_commit(&tfull[pos]);
+            if (k == nin - 1) {
+              mma_commit(&tfull[p1]);
+              mma_commit(&tfull[p1 + 1 == ring ? 0u : p1 + 1]);
+            }
+          }
+          __syncwarp();
+          pos = p1;
+        }
+        nstart += (uint32_t)(nin + 2);
+        pos += 2;
+        if (pos >= ring) pos -= ring;
+      }
+      if (DBG && lane == 0 && mw == 0) {
+        p.dbg[blockIdx.x * 8 + 0] = clk() - t0;
+        p.dbg[blockIdx.x * 8 + 1] = t_te;
+        p.dbg[blockIdx.x * 8 + 2] = t_fu;
+        p.dbg[blockIdx.x * 8 + 3] = t_is;
+      }
+    }
+  } else {
+    // ===================== epilogue (warps 3..18): TMEM lane quarter q, slot hh = (tile, group)
+    const int q = warp & 3;
+    const int hh = (warp - 3) >> 2;
+    constexpr int GPT = 1;
+    const int t = hh >> 1;  // MB = 1: slots 2-3 have no tile (they only hand blocks back)
+    const int g_lo = hh & 1;
+    const bool has_tile = t < MB;
+    const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)((has_tile ? t : 0) * p.ring * BW);
+    const bool nobias = p.flags & VM_CONV_NOBIAS;
+    // every ring block starts at zero (MMAs only accumulate), then is handed to the MMA warps
+    {
+      const uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (has_tile) {
+        for (int r = 0; r < p.ring; ++r)
+#pragma unroll
+          for (int kw = 0; kw < 3; ++kw) tmem_st8(lane_base + (uint32_t)(r * BW + kw * 16 + g_lo * 8), z);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      for (int r = 0; r < p.ring; ++r) mbar_arrive(&tempty[r]);
+    }
+    for (int c = threadIdx.x - 96; c < 16; c += 512) sbias[c] = (!nobias && c < p.Cout) ? p.bias[c] : 0.f;
+    asm volatile("bar.sync 1, 512;" ::: "memory");
+    const int m = q * 32 + lane;  // TMEM row of this thread
+    uint32_t n = 0, r = 0, rphase = 0;
+    const long long e0 = clk();
+    long long e_w = 0, e_ld = 0, e_x = 0, e_m = 0, e_sw = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const int col = u % p.ncol;
+      const int seg = (u / p.ncol) % p.nseg;
+      const int b = u / (p.ncol * p.nseg);
+      const int o0 = seg * p.S, o1 = min(p.D, o0 + p.S);
+      const int L = o1 - o0 + 4;
+      const int ra = col * MB * kKwTile + t * kKwTile + m;  // output in-plane anchor of row m
+      const int hq = ra / p.Wp, wq = ra % p.Wp;
+      const bool valid = has_tile && m < kKwTile && ra < p.P && hq < p.H && wq < p.W;
+      const int64_t orow0 = (int64_t)ra + p.P + p.Wp + 1;
+      bf16* yb = p.y + b * p.y_bstride;
+      const bf16* mb = p.mask + b * p.m_bstride;
+      int4 mkn[GPT];
+#pragma unroll
+      for (int gi = 0; gi < GPT; ++gi) mkn[gi] = make_int4(0, 0, 0, 0);
+      for (int rel = 0; rel < L; ++rel, ++n) {
+        const int o = o0 + rel - 2;
+        const bool live = o >= o0 && o < o1;
+        int4 mk[GPT];
+        if (p.flags & VM_CONV_MASK) {
+#pragma unroll
+          for (int gi = 0; gi < GPT; ++gi) {
+            mk[gi] = mkn[gi];
+            const int g = g_lo + gi;
+            const int on = o + 1;
+            mkn[gi] = make_int4(0, 0, 0, 0);
+            if (on >= o0 && on < o1 && valid && g * 8 < p.Cout)
+              mkn[gi] = __ldg(reinterpret_cast<const int4*>(mb + g * p.plane8 + orow0 * 8 + (int64_t)on * p.P * 8));
+          }
+        }
+        const long long tw = clk();
+        mbar_wait(&tfull[r], rphase);
+        e_w += clk() - tw;
+        tc_fence_after();
+        const uint32_t tcol = lane_base + r * BW;
+        const long long tl0 = clk();
+        uint32_t a[GPT][3][8];
+        if (has_tile) {
+#pragma unroll
+          for (int kw = 0; kw < 3; ++kw) tmem_ld8(tcol + (uint32_t)(kw * 16 + g_lo * 8), a[0][kw]);
+          tmem_ld_wait();
+          const uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // zero the drained block for its next plane
+#pragma unroll
+          for (int kw = 0; kw < 3; ++kw) tmem_st8(tcol + (uint32_t)(kw * 16 + g_lo * 8), z);
+        }
+        const long long tl1 = clk();
+        e_ld += tl1 - tl0;
+        if (live && has_tile) {
+          // rows m+1 (kw 1) and m+2 (kw 2): shuffles within the quarter; lanes 30-31 take the
+          // next quarter's rows 0-1 through shared memory (branch-free: every lane reads the
+          // broadcast words, a select keeps them on lanes 30 / 31 only)
+          float4* xw = reinterpret_cast<float4*>(&xch[hh][n & 1][q][0][0]);
+          if (lane == 0) {
+#pragma unroll
+            for (int gi = 0; gi < GPT; ++gi) {
+              xw[0 * 2 + 0] = make_float4(__uint_as_float(a[gi][1][0]), __uint_as_float(a[gi][1][1]),
+                                                   __uint_as_float(a[gi][1][2]), __uint_as_float(a[gi][1][3]));
+              xw[0 * 2 + 1] = make_float4(__uint_as_float(a[gi][1][4]), __uint_as_float(a[gi][1][5]),
+                                                   __uint_as_float(a[gi][1][6]), __uint_as_float(a[gi][1][7]));
+            }
+          }
+          if (lane < 2) {
+#pragma unroll
+            for (int gi = 0; gi < GPT; ++gi) {
+              xw[(1 + lane) * 2 + 0] = make_float4(__uint_as_float(a[gi][2][0]), __uint_as_float(a[gi][2][1]),
+                                                            __uint_as_float(a[gi][2][2]), __uint_as_float(a[gi][2][3]));
+              xw[(1 + lane) * 2 + 1] = make_float4(__uint_as_float(a[gi][2][4]), __uint_as_float(a[gi][2][5]),
+                                                            __uint_as_float(a[gi][2][6]), __uint_as_float(a[gi][2][7]));
+            }
+          }
+          asm volatile("bar.sync %0, 128;" ::"r"(2 + hh) : "memory");
+          const float4* xn = reinterpret_cast<const float4*>(&xch[hh][n & 1][q < 3 ? q + 1 : q][0][0]);
+          const bool l31 = lane == 31, l30 = lane == 30;
+#pragma unroll
+          for (int gi = 0; gi < GPT; ++gi) {
+            const int g = g_lo + gi;
+            float xs[3][8];
+#pragma unroll
+            for (int sl = 0; sl < 3; ++sl) {
+              const float4 u0 = xn[sl * 2 + 0], u1 = xn[sl * 2 + 1];
+              xs[sl][0] = u0.x, xs[sl][1] = u0.y, xs[sl][2] = u0.z, xs[sl][3] = u0.w;
+              xs[sl][4] = u1.x, xs[sl][5] = u1.y, xs[sl][6] = u1.z, xs[sl][7] = u1.w;
+            }
+            float s1[8], s2[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              s1[e] = __shfl_down_sync(0xffffffffu, __uint_as_float(a[gi][1][e]), 1);
+              s2[e] = __shfl_down_sync(0xffffffffu, __uint_as_float(a[gi][2][e]), 2);
+            }
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float t1 = l31 ? xs[0][e] : s1[e];
+              const float t2 = l31 ? xs[2][e] : (l30 ? xs[1][e] : s2[e]);
+              v[e] = __uint_as_float(a[gi][0][e]) + t1 + t2 + sbias[g * 8 + e];
+            }
+            if (p.flags & VM_CONV_MASK) {
+              const uint32_t* mwv = reinterpret_cast<const uint32_t*>(&mk[gi]);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                v[2 * e] = (int16_t)(mwv[e] & 0xFFFFu) > 0 ? v[2 * e] : 0.f;
+                v[2 * e + 1] = (int16_t)(mwv[e] >> 16) > 0 ? v[2 * e + 1] : 0.f;
+              }
+            }
+            int4 out;
+            uint32_t* ow = reinterpret_cast<uint32_t*>(&out);
+            if (p.flags & VM_CONV_RELU) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) ow[e] = pack_bf16x2_relu(v[2 * e], v[2 * e + 1]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) ow[e] = pack_bf16x2(v[2 * e], v[2 * e + 1]);
+            }
+            if (valid && g * 8 < p.Cout) {
+              const int64_t orow = orow0 + (int64_t)o * p.P;
+              *reinterpret_cast<int4*>(yb + g * p.plane8 + orow * 8) = out;
+              if (HL && p.hl.lo && o == 0)
+                *reinterpret_cast<int4*>(p.hl.lo + (yb - p.y) + g * p.plane8 + (orow + (int64_t)p.D * p.P) * 8) = out;
+              if (HL && p.hl.hi && o == p.D - 1)
+                *reinterpret_cast<int4*>(p.hl.hi + (yb - p.y) + g * p.plane8 + (orow - (int64_t)p.D * p.P) * 8) = out;
+            }
+          }
+        }
+        const long long tm1 = clk();
+        tmem_st_wait();
+        e_sw += clk() - tm1;
+        if (DBG) e_m += tm1 - tl1;
+        tc_fence_before();
+        mbar_arrive(&tempty[r]);
+        if (++r == (uint32_t)p.ring) {
+          r = 0;
+          rphase ^= 1u;
+        }
+      }
+    }
+    if (DBG && threadIdx.x == 96) {
+      p.dbg[blockIdx.x * 8 + 4] = clk() - e0;
+      p.dbg[blockIdx.x * 8 + 5] = e_w;
+      p.dbg[blockIdx.x * 8 + 6] = (long long)n;
+      p.dbg[blockIdx.x * 8 + 7] = e_ld * 1000000LL * 0 + e_ld;
+    }
+    if (DBG && threadIdx.x == 97) {  // sub-phases (kw_probe): exchange, math+store(+ld), st wait
+      p.dbg[blockIdx.x * 8 + 1] = e_x;
+      p.dbg[blockIdx.x * 8 + 2] = e_m;
+      p.dbg[blockIdx.x * 8 + 3] = e_sw;
+    }
+  }
+  tc_fence_before();
+  if (HL && p.hl.counter) __threadfence();
+  __syncthreads();
+  if (HL && threadIdx.x == 0) halo_link_signal(p.hl);
+  if (warp == 1) tmem_dealloc<512>(tbase);
+}
+
 // ------------------------------------------------------------------ weight gradient, kd along N
 // Thin outputs (3*Nc <= 144): dW[kd,kh,kw][ci][co] = sum_a x[a + kd*P + kh*Wp + kw][ci] *
 // gy[a + P + Wp + 1][co] is computed with kd moved to the B side: B = three gy slices shifted
@@ -1584,7 +1966,17 @@ __global__ void k_pack_batch(const vm_pack_job* __restrict__ jobs, int njobs, in
     const int64_t v = gv - jb.begin / 8;
     uint32_t r = (uint32_t)v;  // < 2^31 vectors per job (VM_REQUIRE at launch)
     int kd, kh, kw, kc, co, half;
-    if (g.sweep) {
+    if (g.sweep == 2) {  // [kc][3 kh][2][144][8]
+      const int n = (int)(r % 144u);
+      r /= 144u;
+      half = r & 1;
+      r >>= 1;
+      kh = (int)(r % 3u);
+      kc = (int)(r / 3u);
+      kd = 2 - n / 48;
+      kw = (n % 48) / 16;
+      co = n % 16;
+    } else if (g.sweep) {
       const uint32_t N3 = 3u * g.Nc;
       const int n = (int)(r % N3);
       r /= N3;
@@ -1714,6 +2106,53 @@ static int launch_sweep(const FwdParams& f, int nsm, void* stream) {
     return bw > 68 ? bw : 68;
   };
   double best = 1e30;
+  const bool kw = p.Nc == 16 && p.KC >= 2 && kSweepKw;  // packed as PackGeom::sweep == 2
+  if (kw) {
+    // N = 144 per MMA (3 kh x KC per plane and tile); tiles of 126 outputs; MB <= 2 (TMEM:
+    // MB x ring x 48 columns, ring >= 4); 2 tiles = 2 independent accumulation chains
+    for (int MB = 2; MB >= 1; --MB) {
+      if (g_sweep_force_mb && MB != g_sweep_force_mb) continue;
+      int ring = 512 / (MB * 48);
+      if (ring > kSwMaxRing) ring = kSwMaxRing;
+      const int R = MB * kKwTile + 2 + 2 * p.Wp;
+      const uint32_t a_bytes = ((uint32_t)R * 16 + 127) & ~127u;
+      const uint32_t stage_bytes = 2 * a_bytes;
+      int stages = (int)((kSmemBudget - static_smem - (int)p.w_bytes) / (int)stage_bytes);
+      if (stages > kSwMaxStages) stages = kSwMaxStages;
+      if (stages < 3) continue;
+      const int ncol = (p.P + MB * kKwTile - 1) / (MB * kKwTile);
+      // two of every `ring` planes split at the ring end (two MMAs per kh)
+      const double wrapf = 1.0 + 2.0 * 0.39 / ring;
+      const double plane = 3.0 * p.KC * MB * mma_cycles(144, MB >= 2 ? 3 : 1) * wrapf + 900.0;
+      for (int S = 1; S <= p.D; ++S) {
+        if (g_sweep_force_s && S != g_sweep_force_s && g_sweep_force_s <= p.D) continue;
+        const int nseg = (p.D + S - 1) / S;
+        const int64_t units = (int64_t)f.B * ncol * nseg;
+        const int64_t waves = (units + nsm - 1) / nsm;
+        const double cost = (double)waves * (S + 3) * plane;
+        if (cost < best) {
+          best = cost;
+          p.MB = MB, p.ring = ring, p.R = R, p.a_bytes = a_bytes, p.stage_bytes = stage_bytes;
+          p.stages = stages, p.ncol = ncol, p.S = S, p.nseg = nseg, p.units = (int)units;
+        }
+      }
+    }
+    VM_REQUIRE(best < 1e30, VM_E_UNSUPPORTED, "vm_conv3d_fwd_tc: no sweep-kw configuration fits (W=%d)", p.W);
+    p.idesc1 = make_idesc_bf16(128, 48, false, false);
+    p.idesc2 = make_idesc_bf16(128, 96, false, false);
+    p.idesc3 = make_idesc_bf16(128, 144, false, false);
+    const size_t smem = (size_t)p.w_bytes + (size_t)p.stages * p.stage_bytes;
+    const int grid = p.units < nsm ? p.units : nsm;
+    const int mode = p.dbg != nullptr ? 1 : (p.hl.counter || p.hl.wait_own) ? 2 : 0;
+    using SwKern = void (*)(const SwParams);
+    static const SwKern ktable[2][3] = {
+        {k_conv_fwd_sweepkw<1, 0>, k_conv_fwd_sweepkw<1, 1>, k_conv_fwd_sweepkw<1, 2>},
+        {k_conv_fwd_sweepkw<2, 0>, k_conv_fwd_sweepkw<2, 1>, k_conv_fwd_sweepkw<2, 2>}};
+    auto kern = ktable[p.MB - 1][mode];
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch_pdl(kern, grid, kKwThreads, smem, as_stream(stream), p);
+    return launch_status("vm_conv3d_fwd_tc (sweep-kw)");
+  }
   for (int MB = 4; MB >= 1; --MB) {
     if (g_sweep_force_mb && MB != g_sweep_force_mb) continue;
     int ring = 512 / (MB * p.Nc);
