@@ -967,12 +967,23 @@ constexpr int kSwMaxStages = 8;
 // thread's per-plane bookkeeping otherwise leaves the tensor core idle), 2..9 epilogue.
 // NG = Nc/8 channel groups; MODE 0: plain, 1: cycle probes (tools/dbg_sweep_probe.py),
 // 2: fused peer-memory halo (p.hl)
+// MMA-issuing warps per CTA: one per tile for 16-channel outputs at MB = 4 (warps 1, 10, 11,
+// 12; the per-plane bookkeeping of each warp then covers 10 MMAs: measured one warp 61 us,
+// two 52 us at 16->16, 128^3), else two (one: MB = 1)
+template <int MB, int NG>
+constexpr int sweep_mma_warps() {
+  return (MB == 4 && NG == 2) ? 4 : (MB >= 2 ? 2 : 1);
+}
+template <int MB, int NG>
+constexpr int sweep_threads() {
+  return 32 * (9 + sweep_mma_warps<MB, NG>());
+}
 template <int MB, int MODE, int NG>
-__global__ void __launch_bounds__(352, 1)
+__global__ void __launch_bounds__(sweep_threads<MB, NG>(), 1)
     k_conv_fwd_sweep(const SwParams p) {
   constexpr bool DBG = MODE == 1, HL = MODE == 2;
   auto clk = []() -> long long { return DBG ? (long long)clock64() : 0LL; };
-  constexpr int NW = MB >= 2 ? 2 : 1;  // MMA-issuing warps
+  constexpr int NW = sweep_mma_warps<MB, NG>();  // MMA-issuing warps
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t full[kSwMaxStages], empty[kSwMaxStages], tfull[kSwMaxRing], tempty[kSwMaxRing], wbar;
   __shared__ uint32_t tslot;
@@ -1036,9 +1047,9 @@ __global__ void __launch_bounds__(352, 1)
       }
       if (p.dbg) p.dbg[blockIdx.x * 8 + 7] = t_pw;
     }
-  } else if (warp == 1 || warp == 10) {
+  } else if (warp == 1 || warp >= 10) {
     // ===================== MMA issuers
-    const int mw = warp == 1 ? 0 : 1;
+    const int mw = warp == 1 ? 0 : warp - 9;
     if (mw < NW) {  // (MB = 1: warp 10 idles)
     const long long t0 = clk();
     long long t_te = 0, t_fu = 0, t_is = 0;
@@ -2206,8 +2217,16 @@ static int launch_sweep(const FwdParams& f, int nsm, void* stream) {
   VM_REQUIRE(p.Nc == 16 || p.Nc == 32 || p.Nc == 48, VM_E_UNSUPPORTED, "sweep conv: Nc %d", p.Nc);
   const bool hl = p.hl.counter || p.hl.wait_own;
   auto kern = table[p.MB - 1][(dbg ? 3 : hl ? 6 : 0) + p.Nc / 16 - 1];
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  launch_pdl(kern, grid, 352, smem, as_stream(stream), p);
+  const cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int threads = 32 * (9 + ((p.MB == 4 && p.Nc == 16) ? 4 : (p.MB >= 2 ? 2 : 1)));  // sweep_threads<MB, NG>
+  VM_REQUIRE(ea == cudaSuccess, 100 + (int)ea, "sweep: smem attribute %zu B (MB %d, S %d, ring %d, stages %d): %s",
+             smem, p.MB, p.S, p.ring, p.stages, cudaGetErrorString(ea));
+  launch_pdl(kern, grid, threads, smem, as_stream(stream), p);
+  {
+    const cudaError_t el = cudaPeekAtLastError();
+    VM_REQUIRE(el == cudaSuccess, 100 + (int)el, "sweep launch: grid %d x %d threads, smem %zu (MB %d S %d ring %d stages %d units %d): %s",
+               grid, threads, smem, p.MB, p.S, p.ring, p.stages, p.units, cudaGetErrorString(el));
+  }
   return launch_status("vm_conv3d_fwd_tc (sweep)");
 }
 
