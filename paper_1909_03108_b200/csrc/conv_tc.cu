@@ -619,6 +619,7 @@ struct WgParams {
   int runs_alloc;   // run slots per stage buffer (runs mode)
   int spk;          // stages per unit (K-split chunk)
   int ksplit;       // K-split chunks per sample
+  int kinter;       // 1: stages interleaved over the split CTAs (L2 reuse of the gy rows)
   int stages_total; // per sample
   int units;
   int grid;         // CTAs (a multiple of n_mtgroups); one K partial per CTA
@@ -695,9 +696,13 @@ __global__ void __launch_bounds__(192, 1)
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
         const int ks = (u / p.n_mtgroups) % p.ksplit;
         const int b = u / (p.n_mtgroups * p.ksplit);
-        const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
+        // K stages interleaved over the split CTAs (stage s -> CTA s % ksplit): at any time the
+        // CTAs read one contiguous window of rows, and the kd-shifted gy slices (1-2 planes back)
+        // were read a few windows earlier by other CTAs: L2 hits instead of DRAM re-reads
+        const int s0 = p.kinter ? ks : ks * p.spk, s1 = p.kinter ? p.stages_total : min(p.stages_total, s0 + p.spk);
+        const int sstep = p.kinter ? p.ksplit : 1;
         const bf16* xb = p.x + b * p.x_bstride;
-        for (int s = s0; s < s1; ++s) {
+        for (int s = s0; s < s1; s += sstep) {
           const int64_t k0 = (int64_t)s * p.KS;
           const long long tw = dbg ? (long long)clock64() : 0;
           mbar_wait(&empty[stage], phase ^ 1);
@@ -745,8 +750,12 @@ __global__ void __launch_bounds__(192, 1)
     long long t_wf = 0, t_first = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       const int ks = (u / p.n_mtgroups) % p.ksplit;
-      const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
-      for (int s = s0; s < s1; ++s) {
+      // K stages interleaved over the split CTAs (stage s -> CTA s % ksplit): at any time the
+      // CTAs read one contiguous window of rows, and the kd-shifted gy slices (1-2 planes back)
+      // were read a few windows earlier by other CTAs: L2 hits instead of DRAM re-reads
+      const int s0 = p.kinter ? ks : ks * p.spk, s1 = p.kinter ? p.stages_total : min(p.stages_total, s0 + p.spk);
+      const int sstep = p.kinter ? p.ksplit : 1;
+      for (int s = s0; s < s1; s += sstep) {
         const long long tw = dbg ? (long long)clock64() : 0;
         mbar_wait(&full[stage], phase);
         if (dbg) {
@@ -1743,6 +1752,7 @@ struct WkParams {
   int ngroups;         // CTA groups = n_mtgroups * (3 / nkw): (M-tile group, kw group)
   int ones_slot;
   int spk, ksplit, stages_total, units, grid, stages;
+  int kinter;        // 1: stages interleaved over the split CTAs (L2 reuse of the kd slices)
   uint32_t a_bytes;
   uint32_t g_bytes;  // per kd slice: Nc/8 group slots of KS rows (CGo of them loaded)
   uint32_t g_load;   // loaded bytes per kd slice: CGo * KS * 16
@@ -1816,9 +1826,13 @@ __global__ void __launch_bounds__(192, 1)
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
         const int ks = (u / p.ngroups) % p.ksplit;
         const int b = u / (p.ngroups * p.ksplit);
-        const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
+        // K stages interleaved over the split CTAs (stage s -> CTA s % ksplit): at any time the
+        // CTAs read one contiguous window of rows, and the kd-shifted gy slices (1-2 planes back)
+        // were read a few windows earlier by other CTAs: L2 hits instead of DRAM re-reads
+        const int s0 = p.kinter ? ks : ks * p.spk, s1 = p.kinter ? p.stages_total : min(p.stages_total, s0 + p.spk);
+        const int sstep = p.kinter ? p.ksplit : 1;
         const bf16* xb = p.x + b * p.x_bstride;
-        for (int s = s0; s < s1; ++s) {
+        for (int s = s0; s < s1; s += sstep) {
           const long long tw = clk();
           mbar_wait(&empty[stage], phase ^ 1);
           t_pe += clk() - tw;
@@ -1851,8 +1865,12 @@ __global__ void __launch_bounds__(192, 1)
     long long t_fu = 0, t_is = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       const int ks = (u / p.ngroups) % p.ksplit;
-      const int s0 = ks * p.spk, s1 = min(p.stages_total, s0 + p.spk);
-      for (int s = s0; s < s1; ++s) {
+      // K stages interleaved over the split CTAs (stage s -> CTA s % ksplit): at any time the
+      // CTAs read one contiguous window of rows, and the kd-shifted gy slices (1-2 planes back)
+      // were read a few windows earlier by other CTAs: L2 hits instead of DRAM re-reads
+      const int s0 = p.kinter ? ks : ks * p.spk, s1 = p.kinter ? p.stages_total : min(p.stages_total, s0 + p.spk);
+      const int sstep = p.kinter ? p.ksplit : 1;
+      for (int s = s0; s < s1; s += sstep) {
         const long long tf = clk();
         mbar_wait(&full[stage], phase);
         const long long tf1 = clk();
@@ -2454,6 +2472,7 @@ struct WgPlan {
 };
 
 int g_force_runs = -1, g_force_ks = 0, g_force_mpu = 0;  // tools/tune_wgrad.py overrides
+int g_wg_interleave = 1;  // vm_debug_set_wgrad_interleave: 0 never, 1 planner's choice, 2 always (A/B)
 int g_wg_min_spk = 2;  // minimum stages per K-split unit (vm_debug_set_wgrad_min_spk)
 int g_wk_runtime = 0;  // 1: force the runtime-bounded kd wgrad issue loop (A/B probe)
 int g_wk_ksub_min_stages = 2;  // two K chunks per stage when this many stages still fit (measured: 2 best)
@@ -2544,6 +2563,8 @@ int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
   if (p.spk < g_wg_min_spk) p.spk = g_wg_min_spk;
   p.ksplit = (p.stages_total + p.spk - 1) / p.spk;
   p.units = p.n_mtgroups * B * p.ksplit;
+  // (interleaved: 64->64 at 128^3 547 -> 535 us, 192->64 1281 -> 1242 us, 64->64 at 32^3 +2%)
+  p.kinter = g_wg_interleave != 0;
   p.idesc = make_idesc_bf16(128, p.Nc, true, true);
   p.grid = p.units;
   if (p.grid > nsm) p.grid = (nsm / p.n_mtgroups) * p.n_mtgroups;  // CTA keeps one M-tile group
@@ -2589,7 +2610,10 @@ int make_group_map(CUtensorMap* m, const void* base, int64_t bstride, int CG, in
 }  // namespace
 
 
+static int g_skip_wg_fin = 0;
+extern "C" void vm_debug_skip_wgrad_finalize(int v) { g_skip_wg_fin = v; }
 extern "C" void vm_debug_set_wgrad_kd_runtime(int v) { g_wk_runtime = v; }
+extern "C" void vm_debug_set_wgrad_interleave(int v) { g_wg_interleave = v; }
 extern "C" void vm_debug_set_wgrad_ksub_stages(int v) { g_wk_ksub_min_stages = v > 0 ? v : 2; }
 
 extern "C" void vm_debug_set_wgrad_min_spk(int v) { g_wg_min_spk = v > 0 ? v : 2; }
@@ -2679,6 +2703,10 @@ static bool plan_wgrad_kd(int B, int Cin, int Cout, int D, int H, int W, WkParam
   if (p.spk < 2) p.spk = 2;
   p.ksplit = (p.stages_total + p.spk - 1) / p.spk;
   p.units = p.ngroups * B * p.ksplit;
+  // interleaved stages (tools/wgrad_inter_ab.py, alternating A/B, best of 3): 32->32 at 256^3
+  // 1159 -> 1096 us, 48->16 / 32->32 at 64^3 neutral to +1%; with several M-tile groups (96->32
+  // at 256^3) the groups' CTAs of one stage are no longer co-scheduled: 5388 -> 5507 us
+  p.kinter = g_wg_interleave == 2 || (g_wg_interleave == 1 && p.ngroups == 1);
   p.idesc = make_idesc_bf16(128, 3 * p.Nc, true, true);
   p.idesc64 = make_idesc_bf16(64, 3 * p.Nc, true, true);
   p.grid = p.units;
@@ -2748,6 +2776,7 @@ static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_
       const int ntiles = pk.MT * 3 * (3 * pk.Nc / 8) * 4;
       // many partials (one per CTA of a wide K split): 32 warps per tile keep more loads in flight
       auto fin = nk >= 64 ? k_wgrad_finalize_tiles<true, 32> : k_wgrad_finalize_tiles<true, 8>;
+      if (g_skip_wg_fin) return VM_OK;  // A/B probe (wrong results): the finalize's share of a step
       launch_pdl(fin, ntiles, nk >= 64 ? 1024 : 256, 0, st, pk.ws, gw, gb, nk, pk.MT, pk.Nc, pk.CG, Cin, Cout,
                                                           pk.ones_slot, 0, nullptr, 0, 0, Cout);
       return launch_status("vm_conv3d_wgrad_tc (kd) finalize");
@@ -2801,6 +2830,7 @@ static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_
   }
   const int ntiles = p.MT * 3 * (p.Nc / 8) * 4;
   const int nbias = p.ones_slot < 0 ? (Cout + 255) / 256 : 0;
+  if (g_skip_wg_fin) return VM_OK;
   launch_pdl(k_wgrad_finalize_tiles<false, 8>, ntiles + nbias, 256, 0, st, p.ws, gw, gb, nk, p.MT, p.Nc, p.CG, Cin, Cout,
                                                                p.ones_slot, p.runs, wsb, nsb, (Cout + 7) / 8, ldo);
   return launch_status("vm_conv3d_wgrad_tc finalize");

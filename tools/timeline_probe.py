@@ -91,4 +91,8 @@ def wg():
 
 
 res["wgrad_only"] = timed(wg)
+_lib.load().vm_debug_skip_wgrad_finalize(1)
+res["wgrad_only_nofin"] = timed(wg)
+res["full_nofin"] = timed(st.step)
+_lib.load().vm_debug_skip_wgrad_finalize(0)
 print(f"pdl_forward={pdl} pdl_backward={int(st.pdl_backward)} " + " ".join(f"{k}={v:.3f}ms" for k, v in res.items()))
