@@ -859,7 +859,7 @@ __global__ void __launch_bounds__(NW * 32) k_wgrad_finalize_tiles(const float* _
                                                              float* __restrict__ gb, int nk, int MT, int Nc, int CG,
                                                              int Cin, int Cout, int ones_slot, int runs,
                                                              const float* __restrict__ wsb, int nsb, int CGo,
-                                                             int ldo) {
+                                                             int ldo, int ci_stride) {
   pdl_wait();
   __shared__ float part[NW][8][33];
   const int N = KD ? 3 * Nc : Nc;
@@ -869,7 +869,7 @@ __global__ void __launch_bounds__(NW * 32) k_wgrad_finalize_tiles(const float* _
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if ((int)blockIdx.x >= ntiles) {
     const int co = ((int)blockIdx.x - ntiles) * (NW * 32) + threadIdx.x;
-    if (co < Cout) {
+    if (co < Cout && gb) {
       float sb = 0.f;
       for (int sp = 0; sp < nsb; ++sp) sb += wsb[(int64_t)sp * CGo * 8 + co];
       gb[co] = sb;
@@ -925,8 +925,8 @@ __global__ void __launch_bounds__(NW * 32) k_wgrad_finalize_tiles(const float* _
   }
   if (co >= Cout) return;
   if (is_w) {
-    gw[((int64_t)(pp * 3 + kw) * Cin + cgi * 8 + m % 8) * ldo + co] = s;
-  } else if (is_b) {
+    gw[((int64_t)(pp * 3 + kw) * ci_stride + cgi * 8 + m % 8) * ldo + co] = s;
+  } else if (is_b && gb) {
     gb[co] = s;
   }
 }
@@ -2472,6 +2472,7 @@ struct WgPlan {
 };
 
 int g_force_runs = -1, g_force_ks = 0, g_force_mpu = 0;  // tools/tune_wgrad.py overrides
+int g_wg_chunk = 1;  // vm_debug_set_wgrad_chunk (A/B of the input-channel chunks)
 int g_wg_interleave = 1;  // vm_debug_set_wgrad_interleave: 0 never, 1 planner's choice, 2 always (A/B)
 int g_wg_min_spk = 2;  // minimum stages per K-split unit (vm_debug_set_wgrad_min_spk)
 int g_wk_runtime = 0;  // 1: force the runtime-bounded kd wgrad issue loop (A/B probe)
@@ -2614,6 +2615,7 @@ static int g_skip_wg_fin = 0;
 extern "C" void vm_debug_skip_wgrad_finalize(int v) { g_skip_wg_fin = v; }
 extern "C" void vm_debug_set_wgrad_kd_runtime(int v) { g_wk_runtime = v; }
 extern "C" void vm_debug_set_wgrad_interleave(int v) { g_wg_interleave = v; }
+extern "C" void vm_debug_set_wgrad_chunk(int v) { g_wg_chunk = v; }
 extern "C" void vm_debug_set_wgrad_ksub_stages(int v) { g_wk_ksub_min_stages = v > 0 ? v : 2; }
 
 extern "C" void vm_debug_set_wgrad_min_spk(int v) { g_wg_min_spk = v > 0 ? v : 2; }
@@ -2721,11 +2723,31 @@ static bool plan_wgrad_kd(int B, int Cin, int Cout, int D, int H, int W, WkParam
 // chunks of 128 output channels; each chunk reads its own channel-group planes of gy.
 constexpr int kWgradMaxCout = 160, kWgradChunk = 128;
 
+// Input-channel chunks of the kd weight gradient: a layer whose (cg, kh) slots span several
+// M-tile groups (the decoder's concat convs, 96->32) runs as chunks of 32 input channels, one
+// M-tile each (13 of 16 slots live, 256-anchor K chunks), writing its rows of gw in place
+// (one call: 3 M-tile groups, 5 live slots in the third tile, shorter K chunks to fit)
+constexpr int kWgChunkCin = 32;
+// (tools/wgrad_chunk_ab.py, alternating A/B: 96->32 at 256^3 5.41 -> 3.30 ms, 64->32 at 256^3
+// 2.68 -> 2.22 ms; at 128^3 and below the extra launches and gy re-reads lose: 64->32 at 128^3
+// 0.90x, 96->32 at 64^3 0.71x, so only volumes of >= 4 M voxels are chunked)
+static bool wgrad_kd_chunked(int B, int Cin, int Cout, int D, int H, int W) {
+  WkParams pk;
+  size_t wsk = 0;
+  return (int64_t)B * D * H * W >= (1 << 22) && Cin > kWgChunkCin && Cin % kWgChunkCin == 0 &&
+         plan_wgrad_kd(B, Cin, Cout, D, H, W, pk, wsk) &&
+         pk.ngroups > 1 && plan_wgrad_kd(B, kWgChunkCin, Cout, D, H, W, pk, wsk);
+}
+
 extern "C" size_t vm_conv3d_wgrad_tc_ws(int B, int Cin, int Cout, int D, int H, int W) {
   if (Cout > kWgradMaxCout) Cout = kWgradChunk;  // chunked (vm_conv3d_wgrad_tc): the widest chunk
   WkParams pk;
   size_t wsk = 0;
-  if (plan_wgrad_kd(B, Cin, Cout, D, H, W, pk, wsk)) return wsk + 256;
+  if (plan_wgrad_kd(B, Cin, Cout, D, H, W, pk, wsk)) {
+    size_t wsc = 0;
+    if (wgrad_kd_chunked(B, Cin, Cout, D, H, W)) plan_wgrad_kd(B, kWgChunkCin, Cout, D, H, W, pk, wsc);
+    return (wsk > wsc ? wsk : wsc) + 256;
+  }
   WgPlan pl;
   if (plan_wgrad(B, Cin, Cout, D, H, W, pl) != VM_OK) return 0;
   return pl.ws_main + pl.ws_bias + 256;
@@ -2734,7 +2756,20 @@ extern "C" size_t vm_conv3d_wgrad_tc_ws(int B, int Cin, int Cout, int D, int H, 
 // One call of the weight-gradient kernels for Cout <= kWgradMaxCout output channels; gw rows
 // have stride ldo (>= Cout) so that a chunk of a wider layer writes its columns in place.
 static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_t gy_bstride, float* gw, float* gb,
-                        void* ws, int B, int Cin, int Cout, int D, int H, int W, int ldo, void* stream) {
+                        void* ws, int B, int Cin, int Cout, int D, int H, int W, int ldo, void* stream,
+                        int ci_stride = 0) {
+  if (ci_stride <= 0) ci_stride = Cin;
+  if (ci_stride == Cin && g_wg_chunk && wgrad_kd_chunked(B, Cin, Cout, D, H, W)) {
+    const int64_t xbs = x_bstride ? x_bstride : default_bstride(Cin, D, H, W, 1);
+    const int64_t plane8 = (int64_t)(D + 2) * (H + 2) * (W + 2) * 8;
+    for (int c0 = 0; c0 < Cin; c0 += kWgChunkCin) {
+      const int rc = wgrad_tc_one(static_cast<const bf16*>(x) + (int64_t)(c0 / 8) * plane8, xbs, gy, gy_bstride,
+                                  gw + (int64_t)c0 * ldo, c0 == 0 ? gb : nullptr, ws, B, kWgChunkCin, Cout, D, H, W,
+                                  ldo, stream, Cin);
+      if (rc) return rc;
+    }
+    return VM_OK;
+  }
   {
     WkParams pk;
     size_t wsk = 0;
@@ -2778,7 +2813,7 @@ static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_
       auto fin = nk >= 64 ? k_wgrad_finalize_tiles<true, 32> : k_wgrad_finalize_tiles<true, 8>;
       if (g_skip_wg_fin) return VM_OK;  // A/B probe (wrong results): the finalize's share of a step
       launch_pdl(fin, ntiles, nk >= 64 ? 1024 : 256, 0, st, pk.ws, gw, gb, nk, pk.MT, pk.Nc, pk.CG, Cin, Cout,
-                                                          pk.ones_slot, 0, nullptr, 0, 0, Cout);
+                                                          pk.ones_slot, 0, nullptr, 0, 0, Cout, ci_stride);
       return launch_status("vm_conv3d_wgrad_tc (kd) finalize");
     }
   }
@@ -2832,7 +2867,7 @@ static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_
   const int nbias = p.ones_slot < 0 ? (Cout + 255) / 256 : 0;
   if (g_skip_wg_fin) return VM_OK;
   launch_pdl(k_wgrad_finalize_tiles<false, 8>, ntiles + nbias, 256, 0, st, p.ws, gw, gb, nk, p.MT, p.Nc, p.CG, Cin, Cout,
-                                                               p.ones_slot, p.runs, wsb, nsb, (Cout + 7) / 8, ldo);
+                                                               p.ones_slot, p.runs, wsb, nsb, (Cout + 7) / 8, ldo, ci_stride);
   return launch_status("vm_conv3d_wgrad_tc finalize");
 }
 

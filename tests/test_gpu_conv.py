@@ -339,3 +339,32 @@ def test_first_layer_c1_forward_and_wgrad(shape):
     _, rgk, rgb = O.conv3d_dense_backward(g.astype(np.float64), x.astype(np.float64), np.zeros((3, 3, 3, 1, cout)))
     assert rel_l2(outs[0][0].reshape(3, 3, 3, 1, cout), rgk) <= 1e-5
     assert rel_l2(outs[0][1], rgb) <= 1e-5
+
+
+def test_wgrad_input_channel_chunks_match_one_call():
+    # the multi-group kd weight gradient split into 32-channel chunks (volumes >= 4 M voxels)
+    # == the one-call kernel within fp32 summation-order tolerance, bias written once
+    B, cin, cout, D, H, W = 1, 96, 32, 64, 256, 256
+    g = torch.Generator(device="cuda").manual_seed(5)
+    xs = Slab(B, cin, D, H, W, torch.bfloat16, "cuda")
+    gs = Slab(B, cout, D, H, W, torch.bfloat16, "cuda")
+    for s in (xs, gs):
+        v = s.storage[: s.bstride].view(s.CG, D + 2, H + 2, W + 2, 8)
+        v[:, 1:-1, 1:-1, 1:-1] = torch.randn(v[:, 1:-1, 1:-1, 1:-1].shape, generator=g, device="cuda").to(torch.bfloat16)
+    lib = _lib.load()
+    res = []
+    for chunk in (0, 1):
+        lib.vm_debug_set_wgrad_chunk(chunk)
+        try:
+            gw = torch.zeros(27 * cin * cout, device="cuda")
+            gb = torch.full((cout,), 7.0, device="cuda")
+            nb = _lib.call_size("vm_conv3d_wgrad_tc_ws", B, cin, cout, D, H, W)
+            ws = torch.empty(nb // 4 + 64, device="cuda")
+            _lib.call("vm_conv3d_wgrad_tc", xs.p(), xs.bstride, gs.p(), gs.bstride, _lib.ptr(gw), _lib.ptr(gb),
+                      _lib.ptr(ws), B, cin, cout, D, H, W, _lib.stream_ptr())
+            torch.cuda.synchronize()
+            res.append((gw.double(), gb.double()))
+        finally:
+            lib.vm_debug_set_wgrad_chunk(1)
+    assert float((res[0][0] - res[1][0]).norm() / res[0][0].norm()) <= 1e-3
+    assert float((res[0][1] - res[1][1]).norm() / res[0][1].norm()) <= 1e-3
