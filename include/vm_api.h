@@ -184,6 +184,14 @@ size_t vm_conv3d_wgrad_tc_ws(int B, int Cin, int Cout, int D, int H, int W);
 int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* gy, int64_t gy_bstride,
                        float* gw, float* gb, void* ws, int B, int Cin, int Cout, int D, int H,
                        int W, void* stream);
+/* the same in two stream-ordered halves (phase 1: main kernel + bias partials, phase 2: the
+ * K-split finalize of that workspace), so a caller can run the finalize on another stream while
+ * the next layer's weight gradient starts in a second workspace; layers that need several calls
+ * into one workspace (chunked) do everything in phase 1 (phase 2 is then a no-op) */
+int vm_conv3d_wgrad_tc_deferrable(int B, int Cin, int Cout, int D, int H, int W);
+int vm_conv3d_wgrad_tc_phase(const void* x, int64_t x_bstride, const void* gy, int64_t gy_bstride, float* gw,
+                             float* gb, void* ws, int B, int Cin, int Cout, int D, int H, int W, int phase,
+                             void* stream);
 
 /* ------------------------------------------------------------------ HBM-bound ops (slabs)
  * maxpool 2^3, first-in-scan-order ties (ops.py:141-156); out = pooled slab. */

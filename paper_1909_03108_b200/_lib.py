@@ -67,6 +67,8 @@ _SIGS = {
     "vm_conv3d_wgrad_c1": (_I, [_P, _L, _P, _L, _P, _P, _P, _I, _I, _I, _I, _I, _P]),
     "vm_conv3d_wgrad_tc_ws": (ctypes.c_size_t, [_I, _I, _I, _I, _I, _I]),
     "vm_conv3d_wgrad_tc": (_I, [_P, _L, _P, _L, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
+    "vm_conv3d_wgrad_tc_deferrable": (_I, [_I, _I, _I, _I, _I, _I]),
+    "vm_conv3d_wgrad_tc_phase": (_I, [_P, _L, _P, _L, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P]),
     "vm_maxpool2_fwd": (_I, [_I, _P, _L, _P, _L, _I, _I, _I, _I, _I, _P]),
     "vm_maxpool2_bwd": (_I, [_I, _P, _L, _P, _L, _P, _L, _P, _L, _I, _I, _I, _I, _I, _I, _P]),
     "vm_upsample2_fwd": (_I, [_I, _P, _L, _P, _L, _I, _I, _I, _I, _I, _P]),

@@ -2473,6 +2473,11 @@ struct WgPlan {
 
 int g_force_runs = -1, g_force_ks = 0, g_force_mpu = 0;  // tools/tune_wgrad.py overrides
 int g_wg_chunk = 1;  // vm_debug_set_wgrad_chunk (A/B of the input-channel chunks)
+thread_local int g_wg_phase = 0;  // vm_conv3d_wgrad_tc_phase: 0 all, 1 main kernel(s), 2 finalize
+// splits bias_grad_partial_bf16 uses for this shape (the finalize's phase needs the count only)
+static int bias_grad_partial_count(int B, int Cout, int D, int H, int W) {
+  return (int)(bias_grad_ws_bytes((int64_t)B * D * H * W, Cout) / (((Cout + 7) / 8) * 8 * sizeof(float)));
+}
 int g_wg_interleave = 1;  // vm_debug_set_wgrad_interleave: 0 never, 1 planner's choice, 2 always (A/B)
 int g_wg_min_spk = 2;  // minimum stages per K-split unit (vm_debug_set_wgrad_min_spk)
 int g_wk_runtime = 0;  // 1: force the runtime-bounded kd wgrad issue loop (A/B probe)
@@ -2788,6 +2793,7 @@ static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_
       if (rc) return rc;
       cudaStream_t st = as_stream(stream);
       const bool dbg = pk.dbg != nullptr;
+      const int phase = g_wg_phase;
       using WkKern = void (*)(const CUtensorMap, const WkParams);
       // [NMT-1][variant]: 0 runtime, then (NKK, KSUB) = (2,1) (2,2) (4,1) (4,2) (8,1) (8,2) (16,1) (16,2)
 #define WK_ROW(M)                                                                                               \
@@ -2803,10 +2809,13 @@ static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_
         var = (nkk == 2 ? 1 : nkk == 4 ? 3 : nkk == 8 ? 5 : 7) + (pk.ksub - 1);
       auto kern = table[pk.mt_per_unit - 1][var];
       (void)dbg;
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
-      launch_pdl(kern, pk.grid, 192, (size_t)pk.stages * pk.stage_bytes, st, gmap, pk);
-      rc = launch_status("vm_conv3d_wgrad_tc (kd)");
-      if (rc) return rc;
+      if (phase != 2) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
+        launch_pdl(kern, pk.grid, 192, (size_t)pk.stages * pk.stage_bytes, st, gmap, pk);
+        rc = launch_status("vm_conv3d_wgrad_tc (kd)");
+        if (rc) return rc;
+      }
+      if (phase == 1) return VM_OK;  // the finalize is issued separately (vm_conv3d_wgrad_tc_phase)
       const int nk = pk.grid / pk.ngroups;
       const int ntiles = pk.MT * 3 * (3 * pk.Nc / 8) * 4;
       // many partials (one per CTA of a wide K split): 32 warps per tile keep more loads in flight
@@ -2850,25 +2859,53 @@ static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_
       {k_conv_wgrad_tc<4, 0>, k_conv_wgrad_tc<4, 4>, k_conv_wgrad_tc<4, 8>, k_conv_wgrad_tc<4, 12>, k_conv_wgrad_tc<4, 16>},
   };
   auto kern = table[nmt_t][nkk_t / 4];
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
-  launch_pdl(kern, p.grid, 192, (size_t)p.stages * p.stage_bytes, st, gmap, p);
-  rc = launch_status("vm_conv3d_wgrad_tc");
-  if (rc) return rc;
+  const int phase = g_wg_phase;
+  if (phase != 2) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
+    launch_pdl(kern, p.grid, 192, (size_t)p.stages * p.stage_bytes, st, gmap, p);
+    rc = launch_status("vm_conv3d_wgrad_tc");
+    if (rc) return rc;
+  }
   const int nk = p.grid / p.n_mtgroups;
   // without a ones slot the bias gradient comes from separate partials, reduced by the
   // finalize's extra blocks
   int nsb = 0;
   float* wsb = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ((pl.ws_main + 255) / 256) * 256);
   if (p.ones_slot < 0) {
-    rc = bias_grad_partial_bf16(gy, gbs, wsb, B, Cout, D, H, W, st, &nsb);
-    if (rc) return rc;
+    if (phase != 2) {
+      rc = bias_grad_partial_bf16(gy, gbs, wsb, B, Cout, D, H, W, st, &nsb);
+      if (rc) return rc;
+    } else {
+      nsb = bias_grad_partial_count(B, Cout, D, H, W);
+    }
   }
+  if (phase == 1) return VM_OK;
   const int ntiles = p.MT * 3 * (p.Nc / 8) * 4;
   const int nbias = p.ones_slot < 0 ? (Cout + 255) / 256 : 0;
   if (g_skip_wg_fin) return VM_OK;
   launch_pdl(k_wgrad_finalize_tiles<false, 8>, ntiles + nbias, 256, 0, st, p.ws, gw, gb, nk, p.MT, p.Nc, p.CG, Cin, Cout,
                                                                p.ones_slot, p.runs, wsb, nsb, (Cout + 7) / 8, ldo, ci_stride);
   return launch_status("vm_conv3d_wgrad_tc finalize");
+}
+
+// The weight gradient in two stream-ordered halves, so that the K-split finalize of one layer
+// can run on another stream while the next layer's main kernel starts (the caller alternates
+// two workspaces): phase 1 launches the main kernel (and the bias partials), phase 2 the
+// finalize of the same call's workspace.  Layers that run as several calls into one workspace
+// (output-channel chunks, input-channel chunks) do everything in phase 1; phase 2 is a no-op.
+extern "C" int vm_conv3d_wgrad_tc_deferrable(int B, int Cin, int Cout, int D, int H, int W) {
+  return Cout <= kWgradMaxCout && !wgrad_kd_chunked(B, Cin, Cout, D, H, W);
+}
+extern "C" int vm_conv3d_wgrad_tc_phase(const void* x, int64_t x_bstride, const void* gy, int64_t gy_bstride,
+                                        float* gw, float* gb, void* ws, int B, int Cin, int Cout, int D, int H,
+                                        int W, int phase, void* stream) {
+  VM_REQUIRE(phase >= 0 && phase <= 2, VM_E_ARG, "vm_conv3d_wgrad_tc_phase: phase %d", phase);
+  const bool split = phase != 0 && vm_conv3d_wgrad_tc_deferrable(B, Cin, Cout, D, H, W);
+  if (phase == 2 && !split) return VM_OK;
+  g_wg_phase = split ? phase : 0;
+  const int rc = vm_conv3d_wgrad_tc(x, x_bstride, gy, gy_bstride, gw, gb, ws, B, Cin, Cout, D, H, W, stream);
+  g_wg_phase = 0;
+  return rc;
 }
 
 extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* gy,

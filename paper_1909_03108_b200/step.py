@@ -150,6 +150,7 @@ class UNetStep:
         self.overlap_min_planes = 32  # tools/halo_ab.py: the boundary launches cost more below
         self.halo_sm_reserve = 8  # SMs the interior conv leaves to the overlapped exchange
         self.fuse_halo = True  # peer transport: producer convs push their boundary layers themselves
+        self.defer_finalize = True  # wgrad K-split finalize on its own stream (two workspaces)
         self.bucket_bytes = 16 << 20
         bdiv = mesh.axis_size(layout.axis_for("batch")) if (layout is not None and layout.axis_for("batch")) else 1
         self.global_batch = global_batch or batch * bdiv
@@ -229,6 +230,9 @@ class UNetStep:
                                                                     L.D, L.H, L.W)))
         self.wgrad_ws = torch.empty(max([L.ws_bytes for L in self.layers if L.k == 3] + [16]) // 4 + 4,
                                     dtype=torch.float32, device=dev)
+        # second workspace: the K-split finalize of one layer runs on its own stream while the
+        # next layer's weight gradient fills the other workspace (defer_finalize)
+        self.wgrad_ws2 = torch.empty_like(self.wgrad_ws) if self.conv_impl == "tc" else None
         # split-K scratch of the general forward/dgrad kernel (deep levels); zeroed once, its
         # tile counters return to zero after every launch.  Main stream only.
         conv_ws = [16]
@@ -424,9 +428,37 @@ class UNetStep:
         vox = self.B * L.D * L.H * L.W
         nbytes = 2.0 * vox * (L.cin + L.cout) + 4.0 * (L.nk + L.cout)
         if self.conv_impl == "tc" and L.c1:
+            f = getattr(self, "_fin", None)
+            if f is not None and f["done"][0] is not None:  # a deferred finalize may still read wgrad_ws
+                torch.cuda.current_stream().wait_event(f["done"][0])
             self._k("conv_wgrad", L.node.id, self._conv_flops(L), nbytes, "vm_conv3d_wgrad_c1", _lib.ptr(self.x1),
                     0, g.p(), g.bstride, _lib.ptr(L.gw), _lib.ptr(L.gb), _lib.ptr(self.wgrad_ws), self.B, L.cout, L.D,
                     L.H, L.W)
+        elif self.conv_impl == "tc" and getattr(self, "_fin", None) is not None:
+            # main kernel on this (side) stream into workspace i % 2; its finalize on the finalize
+            # stream, so the next layer's weight gradient does not wait for it
+            f = self._fin
+            i = f["n"]
+            f["n"] += 1
+            ws = self.wgrad_ws if i % 2 == 0 else self.wgrad_ws2
+            side = torch.cuda.current_stream()
+            if f["done"][i % 2] is not None:  # the finalize that last read this workspace
+                side.wait_event(f["done"][i % 2])
+            self._k("conv_wgrad", L.node.id, self._conv_flops(L), nbytes, "vm_conv3d_wgrad_tc_phase", x.p(),
+                    x.bstride, g.p(), g.bstride, _lib.ptr(L.gw), _lib.ptr(L.gb), _lib.ptr(ws), self.B, L.cin,
+                    L.cout, L.D, L.H, L.W, 1)
+            ev = torch.cuda.Event()
+            ev.record(side)
+            fs = self._fin_stream()
+            fs.wait_event(ev)
+            with torch.cuda.stream(fs):
+                self._k("conv_wgrad", L.node.id, 0, 0, "vm_conv3d_wgrad_tc_phase", x.p(), x.bstride, g.p(),
+                        g.bstride, _lib.ptr(L.gw), _lib.ptr(L.gb), _lib.ptr(ws), self.B, L.cin, L.cout, L.D, L.H,
+                        L.W, 2)
+                done = torch.cuda.Event()
+                done.record(fs)
+            f["done"][i % 2] = done
+            f["last"] = done
         elif self.conv_impl == "tc":
             self._k("conv_wgrad", L.node.id, self._conv_flops(L), nbytes, "vm_conv3d_wgrad_tc", x.p(), x.bstride,
                     g.p(), g.bstride, _lib.ptr(L.gw), _lib.ptr(L.gb), _lib.ptr(self.wgrad_ws), self.B, L.cin,
@@ -886,6 +918,8 @@ class UNetStep:
         main = torch.cuda.current_stream()
         side = self._side_stream() if self.overlap_wgrad else None
         buckets = self._grad_buckets() if (self.ar_comm is not None and side is not None) else {}
+        self._fin = ({"n": 0, "done": [None, None], "last": None}
+                     if (side is not None and self.defer_finalize and self.conv_impl == "tc") else None)
         if buckets:
             ar = self._ar_stream()
         # a transport whose margins the weight gradient never reads (peer-memory depth halo):
@@ -914,6 +948,8 @@ class UNetStep:
                             ev = torch.cuda.Event()
                             ev.record(side)
                             ar.wait_event(ev)
+                            if self._fin is not None and self._fin["last"] is not None:
+                                ar.wait_event(self._fin["last"])  # the bucket's last finalize
                             lo, hi = buckets[L.index]
                             with torch.cuda.stream(ar):
                                 self._k("coll", "grads", 0, 0, "vm_allreduce_f32", ctypes.c_void_p(self.ar_comm),
@@ -954,6 +990,9 @@ class UNetStep:
 
         if side is not None:
             main.wait_stream(side)
+        if self._fin is not None:
+            main.wait_stream(self._fin_stream())
+            self._fin = None
         if buckets:
             main.wait_stream(ar)
         self._grads_reduced = bool(buckets)
@@ -982,6 +1021,11 @@ class UNetStep:
                     hi, size = None, 0
             self._buckets = out
         return self._buckets
+
+    def _fin_stream(self):
+        if getattr(self, "_fstream", None) is None:
+            self._fstream = torch.cuda.Stream(device=self.device)
+        return self._fstream
 
     def _side_stream(self):
         if getattr(self, "_wg_stream", None) is None:
