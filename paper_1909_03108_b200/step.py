@@ -991,7 +991,11 @@ class UNetStep:
         if side is not None:
             main.wait_stream(side)
         if self._fin is not None:
-            main.wait_stream(self._fin_stream())
+            # join through the recorded events only: an unused finalize stream is not part of a
+            # graph capture, and waiting on it would invalidate the capture
+            for ev in self._fin["done"]:
+                if ev is not None:
+                    main.wait_event(ev)
             self._fin = None
         if buckets:
             main.wait_stream(ar)
