@@ -29,6 +29,7 @@ the reference's per-sample seed ``SeedSequence([seed, 104729, global index])``
 from __future__ import annotations
 
 import json
+import os
 import time
 import warnings
 from dataclasses import dataclass, field
@@ -36,7 +37,7 @@ from pathlib import Path
 
 import numpy as np
 
-from .errors import ShardingError, VoxmeshError
+from .errors import HaloError, ShardingError, VoxmeshError
 
 DICE_EPS = 1e-6
 
@@ -411,6 +412,14 @@ def _make_steps(graph, params, cfg, batch, key="vm_step", evaluation=False):
         if evaluation:
             st.keep_pred = True
             st.stats_axes = tuple(spatial)
+        if (multi and st.comm is not None and st.has_halo and max(st.halo.nbr6[2:]) < 0
+                and os.environ.get("VOXMESH_HALO", "peer") == "peer"):
+            # depth-only split over NCCL ranks: the peer-memory halo fused into the conv kernels
+            # (every rank falls back to NCCL together if a CUDA-IPC mapping fails)
+            try:
+                st.use_peer_halo()
+            except HaloError:
+                pass
         ctx.store[key] = st
         return None
 
