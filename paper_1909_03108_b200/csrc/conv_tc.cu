@@ -1145,23 +1145,12 @@ __global__ void __launch_bounds__(sweep_threads<MB, NG>(), 1)
               for (int j = 0; j < 9; ++j) {
                 const uint64_t bdesc = b0desc + (uint64_t)(j * wstep);
                 const uint64_t adesc = a0desc + (uint64_t)((j / 3) * wp1 + (j % 3));
-                if (j == 0 && kc == 0) {  // block pos+2 (output plane i) starts here
+                // every block arrives zeroed from the epilogue: all MMAs accumulate
 #pragma unroll
-                  for (int tt = 0; tt < (MB + NW - 1) / NW; ++tt) {
-                    const int t = mw + tt * NW;
-                    if (t >= MB) break;
-                    const uint32_t dt = dpos + t * tstride;
-                    const uint64_t at = adesc + (uint64_t)(t * 128);
-                    mma_bf16_ss(dt, at, bdesc, id2, 1u);
-                    mma_bf16_ss(dt + 2 * Nc, at, bdesc + (uint64_t)(2 * Nc), id1, 0u);
-                  }
-                } else {
-#pragma unroll
-                  for (int tt = 0; tt < (MB + NW - 1) / NW; ++tt) {
-                    const int t = mw + tt * NW;
-                    if (t >= MB) break;
-                    mma_bf16_ss(dpos + t * tstride, adesc + (uint64_t)(t * 128), bdesc, id3, 1u);
-                  }
+                for (int tt = 0; tt < (MB + NW - 1) / NW; ++tt) {
+                  const int t = mw + tt * NW;
+                  if (t >= MB) break;
+                  mma_bf16_ss(dpos + t * tstride, adesc + (uint64_t)(t * 128), bdesc, id3, 1u);
                 }
               }
             } else {
@@ -1169,16 +1158,7 @@ __global__ void __launch_bounds__(sweep_threads<MB, NG>(), 1)
             for (int j = 0; j < 9; ++j) {
               const uint64_t bdesc = b0desc + (uint64_t)(j * wstep);
               const uint64_t adesc = a0desc + (uint64_t)((j / 3) * wp1 + (j % 3));
-              if (j == 0 && kc == 0) {
-#pragma unroll
-                for (int tt = 0; tt < (MB + NW - 1) / NW; ++tt) {
-                  const int t = mw + tt * NW;
-                  if (t >= MB) break;
-                  for (int e = 0; e < nf; ++e)
-                    mma_bf16_ss(tbase + t * tstride + fd[e], adesc + (uint64_t)(t * 128), bdesc + fb[e], fid[e],
-                                facc[e]);
-                }
-              } else if (nn == 1) {
+              if (nn == 1) {
 #pragma unroll
                 for (int tt = 0; tt < (MB + NW - 1) / NW; ++tt) {
                   const int t = mw + tt * NW;
@@ -1241,7 +1221,24 @@ __global__ void __launch_bounds__(sweep_threads<MB, NG>(), 1)
     const int g_lo = MB == 1 ? h : 0, g_step = MB == 1 ? 2 : 1;  // channel groups of this thread
     const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
     const bool nobias = p.flags & VM_CONV_NOBIAS;
-    // blocks start empty: the first MMA into a block overwrites it (enable_input_d = 0)
+    // every ring block starts at zero and is re-zeroed when drained (tcgen05.st), so all MMAs
+    // accumulate (no overwrite split of the first K step: one MMA fewer per tile and plane)
+    auto zero_block = [&](uint32_t r) {
+      const uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int k = 0; k < TPT; ++k) {
+        const int t = MB == 1 ? 0 : h + 2 * k;
+        if (t >= MB) break;
+#pragma unroll
+        for (int gi = 0; gi < GPT; ++gi) {
+          const int g = g_lo + gi * g_step;
+          if (g < ngrp) tmem_st8(lane_base + (uint32_t)((t * p.ring + (int)r) * p.Nc + g * 8), z);
+        }
+      }
+    };
+    for (int r = 0; r < p.ring; ++r) zero_block((uint32_t)r);
+    tmem_st_wait();
+    tc_fence_before();
     for (int r = 0; r < p.ring; ++r) mbar_arrive(&tempty[r]);
     for (int c = threadIdx.x - 64; c < p.Nc; c += 256) sbias[c] = (!nobias && c < p.Cout) ? p.bias[c] : 0.f;
     asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -1349,6 +1346,8 @@ __global__ void __launch_bounds__(sweep_threads<MB, NG>(), 1)
             }
           }
         }
+        zero_block(r);  // (after this block's loads completed: tmem_ld_wait above, or no loads)
+        tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&tempty[r]);
         if (++r == (uint32_t)p.ring) {
