@@ -983,9 +983,15 @@ template <int MB, int NG>
 constexpr int sweep_mma_warps() {
   return (MB == 4 && NG == 2) ? 4 : (MB >= 2 ? 2 : 1);
 }
+// epilogue warps (two per TMEM lane quarter; the kernel supports 16: measured no faster for
+// 16-channel outputs at MB = 4: fwd 47.4 -> 48.2 us, dgrad 53.2 -> 52.9 us at 128^3)
+template <int MB, int NG>
+constexpr int sweep_epi_warps() {
+  return 8;
+}
 template <int MB, int NG>
 constexpr int sweep_threads() {
-  return 32 * (9 + sweep_mma_warps<MB, NG>());
+  return 32 * (1 + sweep_epi_warps<MB, NG>() + sweep_mma_warps<MB, NG>());
 }
 template <int MB, int MODE, int NG>
 __global__ void __launch_bounds__(sweep_threads<MB, NG>(), 1)
@@ -993,6 +999,8 @@ __global__ void __launch_bounds__(sweep_threads<MB, NG>(), 1)
   constexpr bool DBG = MODE == 1, HL = MODE == 2;
   auto clk = []() -> long long { return DBG ? (long long)clock64() : 0LL; };
   constexpr int NW = sweep_mma_warps<MB, NG>();  // MMA-issuing warps
+  constexpr int EW = sweep_epi_warps<MB, NG>();  // epilogue warps (2 .. EW+1)
+  constexpr int NH = EW / 4;                     // epilogue warps per TMEM lane quarter
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t full[kSwMaxStages], empty[kSwMaxStages], tfull[kSwMaxRing], tempty[kSwMaxRing], wbar;
   __shared__ uint32_t tslot;
@@ -1007,7 +1015,7 @@ __global__ void __launch_bounds__(sweep_threads<MB, NG>(), 1)
     }
     for (int r = 0; r < p.ring; ++r) {
       mbar_init(&tfull[r], NW);
-      mbar_init(&tempty[r], 256);
+      mbar_init(&tempty[r], 32 * EW);
     }
     mbar_init(&wbar, 1);
     fence_barrier_init();
@@ -1056,9 +1064,9 @@ __global__ void __launch_bounds__(sweep_threads<MB, NG>(), 1)
       }
       if (p.dbg) p.dbg[blockIdx.x * 8 + 7] = t_pw;
     }
-  } else if (warp == 1 || warp >= 10) {
+  } else if (warp == 1 || warp >= 2 + EW) {
     // ===================== MMA issuers
-    const int mw = warp == 1 ? 0 : warp - 9;
+    const int mw = warp == 1 ? 0 : warp - (1 + EW);
     if (mw < NW) {  // (MB = 1: warp 10 idles)
     const long long t0 = clk();
     long long t_te = 0, t_fu = 0, t_is = 0;
@@ -1212,8 +1220,8 @@ __global__ void __launch_bounds__(sweep_threads<MB, NG>(), 1)
     // ===================== epilogue (warps 2..9): TMEM lane quarter q, half h
     const int q = warp & 3;
     const int h = (warp - 2) >> 2;
-    // tiles t = h, h+2, ... of every block (MB = 1: both halves share the tile, split by group)
-    constexpr int TPT = MB == 1 ? 1 : (MB + 1) / 2;  // tiles per thread (max)
+    // tiles t = h, h+NH, ... of every block (MB = 1: both halves share the tile, split by group)
+    constexpr int TPT = MB == 1 ? 1 : (MB + NH - 1) / NH;  // tiles per thread (max)
     // channel groups per thread: compile-time, so the TMEM, mask and prefetch arrays hold
     // exactly the groups this layer has (sized for Nc = 48 they spilled at MB = 3, 4)
     constexpr int GPT = MB == 1 ? (NG + 1) / 2 : NG;
@@ -1227,7 +1235,7 @@ __global__ void __launch_bounds__(sweep_threads<MB, NG>(), 1)
       const uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
       for (int k = 0; k < TPT; ++k) {
-        const int t = MB == 1 ? 0 : h + 2 * k;
+        const int t = MB == 1 ? 0 : h + NH * k;
         if (t >= MB) break;
 #pragma unroll
         for (int gi = 0; gi < GPT; ++gi) {
@@ -1240,8 +1248,8 @@ __global__ void __launch_bounds__(sweep_threads<MB, NG>(), 1)
     tmem_st_wait();
     tc_fence_before();
     for (int r = 0; r < p.ring; ++r) mbar_arrive(&tempty[r]);
-    for (int c = threadIdx.x - 64; c < p.Nc; c += 256) sbias[c] = (!nobias && c < p.Cout) ? p.bias[c] : 0.f;
-    asm volatile("bar.sync 1, 256;" ::: "memory");
+    for (int c = threadIdx.x - 64; c < p.Nc; c += 32 * EW) sbias[c] = (!nobias && c < p.Cout) ? p.bias[c] : 0.f;
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
     uint32_t n = 0;
     uint32_t r = 0, rphase = 0;  // n % ring, (n / ring) & 1
     const long long e0 = clk();
@@ -1256,7 +1264,7 @@ __global__ void __launch_bounds__(sweep_threads<MB, NG>(), 1)
       int64_t orow0[TPT];
 #pragma unroll
       for (int k = 0; k < TPT; ++k) {
-        const int t = MB == 1 ? 0 : h + 2 * k;
+        const int t = MB == 1 ? 0 : h + NH * k;
         const int ra = col * MB * 128 + t * 128 + q * 32 + lane;  // in-plane anchor
         const int hq = ra / p.Wp, wq = ra % p.Wp;
         valid[k] = t < MB && ra < p.P && hq < p.H && wq < p.W;
@@ -1296,7 +1304,7 @@ __global__ void __launch_bounds__(sweep_threads<MB, NG>(), 1)
         if (live) {
 #pragma unroll
           for (int k = 0; k < TPT; ++k) {
-            const int t = MB == 1 ? 0 : h + 2 * k;
+            const int t = MB == 1 ? 0 : h + NH * k;
             if (t >= MB) break;
             const int64_t orow = orow0[k] + (int64_t)o * p.P;
             const uint32_t tcol = lane_base + (uint32_t)((t * p.ring + (int)r) * p.Nc);
@@ -2235,7 +2243,7 @@ static int launch_sweep(const FwdParams& f, int nsm, void* stream) {
   const bool hl = p.hl.counter || p.hl.wait_own;
   auto kern = table[p.MB - 1][(dbg ? 3 : hl ? 6 : 0) + p.Nc / 16 - 1];
   const cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int threads = 32 * (9 + ((p.MB == 4 && p.Nc == 16) ? 4 : (p.MB >= 2 ? 2 : 1)));  // sweep_threads<MB, NG>
+  const int threads = (p.MB == 4 && p.Nc == 16) ? sweep_threads<4, 2>() : sweep_threads<1, 4>() + (p.MB >= 2 ? 32 : 0);
   VM_REQUIRE(ea == cudaSuccess, 100 + (int)ea, "sweep: smem attribute %zu B (MB %d, S %d, ring %d, stages %d): %s",
              smem, p.MB, p.S, p.ring, p.stages, cudaGetErrorString(ea));
   launch_pdl(kern, grid, threads, smem, as_stream(stream), p);
