@@ -37,7 +37,7 @@ using bf16 = __nv_bfloat16;
 constexpr int kBoxR = 128;  // TMA box height (rows of 8 bf16 = 16 B)
 constexpr int kMaxStages = 6;
 constexpr int kSmemBudget = 220 * 1024;
-constexpr int kFwdMaxSplit = 3;  // split-K ways of the general forward kernel
+constexpr int kFwdMaxSplit = 16;  // split-K ways of the general forward kernel
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -536,48 +536,73 @@ __global__ void __launch_bounds__(320, 1)
         aphase ^= 1;
       }
       if (split) {
-        // publish this split's partial; the last split of the tile unit finishes it
+        // publish this split's partial, wait for the tile's other splits (all resident: the
+        // planner keeps split plans to one wave), then every split finishes its own slice of
+        // the tile's rows: the fix-up runs on ksplit CTAs at once instead of the last arriver
+        // (one CTA reading every split's partial ran ~49 K cycles for 8 splits of a 512-channel
+        // tile: latency-bound)
         const long long tpa = clk();
         __threadfence();
         asm volatile("bar.sync 1, 256;" ::: "memory");
-        if (et == 0) s_last = atomicAdd(p.counters + tu, 1) == p.ksplit - 1;
+        if (et == 0) {
+          atomicAdd(p.counters + tu, 1);
+          const long long tw0 = clock64();
+          while (ld_acquire_gpu_i32(p.counters + tu) < p.ksplit) {
+            __nanosleep(64);
+            if (clock64() - tw0 > 20000000000LL) break;  // never hang the device
+          }
+        }
         asm volatile("bar.sync 1, 256;" ::: "memory");
+        __threadfence();
         t_pub += clk() - tpa;
         t_arr = clk() - t_epi0;
-        if (s_last) {
-          const long long tfx = clk();
-          __threadfence();
-          for (int i = MB == 1 ? 0 : half; i < p.MB; i += MB == 1 ? 1 : 2) {
-            const int row = q * 32 + lane;
+        const long long tfx = clk();
+        // one row per warp at a time, lanes across the row's channel groups: every split's
+        // partial row is one coalesced read, 4 splits' loads in flight
+        const int ew = et >> 5, ln = et & 31;
+        const int rps = (128 + p.ksplit - 1) / p.ksplit;
+        const int rlo = ks * rps, rhi = min(128, rlo + rps);
+        for (int i = 0; i < p.MB; ++i) {
+          for (int row = rlo + ew; row < rhi; row += 8) {
             bool valid;
             int dq;
             const int64_t orow = anchor_row(a0 + i * 128 + row, valid, dq);
-            if (valid) {
-#pragma unroll 4
-              for (int g = glo; g < ghi; ++g) {
-                const int co0 = nch * p.Nc + g * 8;
-                if (co0 >= p.Cout) break;
-                int4 mkv = make_int4(0, 0, 0, 0);
-                if (domask) mkv = __ldg(reinterpret_cast<const int4*>(mbase + (co0 / 8) * p.plane8 + orow * 8));
-                float v[8];
+            if (!valid) continue;  // warp-uniform (one row per warp)
+            for (int g = ln; g < ng_out; g += 32) {
+              const int co0 = nch * p.Nc + g * 8;
+              if (co0 >= p.Cout) break;
+              int4 mkv = make_int4(0, 0, 0, 0);
+              if (domask) mkv = __ldg(reinterpret_cast<const int4*>(mbase + (co0 / 8) * p.plane8 + orow * 8));
+              float v[8];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) v[e] = 0.f;
+              for (int e = 0; e < 8; ++e) v[e] = 0.f;
+              for (int k0 = 0; k0 < p.ksplit; k0 += 4) {
+                float4 lo[4], hi[4];
 #pragma unroll
-                for (int k = 0; k < kFwdMaxSplit; ++k) {  // split order: deterministic
-                  if (k >= p.ksplit) break;
+                for (int j = 0; j < 4; ++j) {
+                  if (k0 + j >= p.ksplit) break;
                   const float4* src = reinterpret_cast<const float4*>(
-                      p.ws + ((((int64_t)k * ntu + tu) * p.MB + i) * 128 + row) * p.Nc + g * 8);
-                  const float4 lo = __ldcg(src), hi = __ldcg(src + 1);
-                  v[0] += lo.x, v[1] += lo.y, v[2] += lo.z, v[3] += lo.w;
-                  v[4] += hi.x, v[5] += hi.y, v[6] += hi.z, v[7] += hi.w;
+                      p.ws + ((((int64_t)(k0 + j) * ntu + tu) * p.MB + i) * 128 + row) * p.Nc + g * 8);
+                  lo[j] = __ldcg(src), hi[j] = __ldcg(src + 1);
                 }
-                emit(ybase, co0, v, mkv, orow, dq);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {  // split order: deterministic
+                  if (k0 + j >= p.ksplit) break;
+                  v[0] += lo[j].x, v[1] += lo[j].y, v[2] += lo[j].z, v[3] += lo[j].w;
+                  v[4] += hi[j].x, v[5] += hi[j].y, v[6] += hi[j].z, v[7] += hi[j].w;
+                }
               }
+              emit(ybase, co0, v, mkv, orow, dq);
             }
           }
-          if (et == 0) p.counters[tu] = 0;  // ready for the next launch
-          t_fix += clk() - tfx;
         }
+        // the last split to leave resets both counters for the next launch
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (et == 0 && atomicAdd(p.counters + ntu + tu, 1) == p.ksplit - 1) {
+          p.counters[tu] = 0;
+          p.counters[ntu + tu] = 0;
+        }
+        t_fix += clk() - tfx;
       }
     }
     if (p.dbg && threadIdx.x == 64) {
@@ -2261,12 +2286,15 @@ extern "C" void vm_debug_set_fwd_probe(long long* buf) { g_fwd_dbg = buf; }
 // [f32 partials ksplit x tile units x MB x Nc x 128].  Zeroed once by the caller.
 static size_t fwd_ws_need(int ksplit, int64_t ntu, int MB, int Nc) {
   if (ksplit <= 1) return 0;
-  return (size_t)((ntu * 4 + 255) / 256 * 256) + (size_t)ksplit * ntu * MB * Nc * 128 * sizeof(float);
+  return (size_t)((ntu * 8 + 255) / 256 * 256) + (size_t)ksplit * ntu * MB * Nc * 128 * sizeof(float);
 }
 // Split-K is off by default: measured on B200 it loses at every deep-level shape of the cfg2
 // ladder (128->128 @16^3: 19.1 us unsplit, 24.9 / 26.6 us with 2 / 3 splits — the partial
 // round trip and the last split's fix-up cost more than the shorter K loop saves).
-static int g_fwd_max_split = 1;  // vm_debug_set_fwd_max_split (A/B probes, tests)
+// Split-K is planned only for layers with few tile units (<= SMs / 4): the deep levels of a
+// split volume (cfg3 8-way, level 4: 2x16x16 local, 512 channels: 12 units of 96 K stages);
+// at cfg2's deep levels (41 units) it lost (see below) and stays off by that rule
+static int g_fwd_max_split = kFwdMaxSplit;  // vm_debug_set_fwd_max_split (A/B probes, tests)
 extern "C" void vm_debug_set_fwd_max_split(int v) { g_fwd_max_split = v < 1 ? 1 : v > kFwdMaxSplit ? kFwdMaxSplit : v; }
 
 static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, const float* bias, void* y,
@@ -2324,6 +2352,9 @@ extern "C" size_t vm_conv3d_fwd_tc_ws_bytes(int B, int Cin, int Cout, int D, int
   const PackGeom pg = pack_geom(Cin, Cout);
   if (pg.sweep) return 0;
   const int64_t tiles = ((int64_t)D * (H + 2) * (W + 2) + 127) / 128;
+  int nsm = vm_num_sms(0);
+  if (nsm <= 0) nsm = 148;
+  if ((int64_t)B * tiles * pg.nchunk * 4 > nsm * 8) return 256;  // never split (planner rule, MB <= 8)
   // MB tiles per unit round the tile count up by < MB tiles: bound by MB = 1 plus 8 tiles
   return fwd_ws_need(kFwdMaxSplit, (int64_t)B * (tiles + 8) * pg.nchunk, 1, pg.Nc) + 256;
 }
@@ -2409,11 +2440,14 @@ static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, 
     // split-K over the 3*KC (kc, kd) stages when a caller workspace can hold the f32
     // partials: more CTAs for layers with few tiles (deep levels)
     for (int ksplit = 1; ksplit <= g_fwd_max_split; ++ksplit) {
+      if (ksplit > 1 && ntu * 4 > nsm) break;  // enough tile units already
       const int spk = (3 * p.KC + ksplit - 1) / ksplit;
       if (ksplit > 1 &&
           ((3 * p.KC + spk - 1) / spk != ksplit || !ws || fwd_ws_need(ksplit, ntu, MB, N) > ws_bytes))
         continue;
       const int64_t units = ntu * ksplit;
+      // the splits of a tile finish it together (they wait for each other): one wave only
+      if (ksplit > 1 && units > nsm) break;
       const int64_t waves = (units + nsm - 1) / nsm;
       for (int nacc : {1, 3}) {
         if (g_fwd_force_acc && nacc != g_fwd_force_acc) continue;
@@ -2452,8 +2486,8 @@ static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, 
   p.units = B * p.mblocks * p.nchunk * bsplit;
   if (bsplit > 1) {
     const int64_t ntu = (int64_t)B * p.mblocks * p.nchunk;
-    p.counters = static_cast<int*>(ws);
-    p.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + (ntu * 4 + 255) / 256 * 256);
+    p.counters = static_cast<int*>(ws);  // [ntu] arrivals, [ntu] departures
+    p.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + (ntu * 8 + 255) / 256 * 256);
   }
   p.idesc = make_idesc_bf16(128, N, false, false);
   (void)rows;

@@ -162,6 +162,12 @@ __device__ __forceinline__ int ld_acquire_sys_i32(const int* p) {
   return v;
 }
 
+__device__ __forceinline__ int ld_acquire_gpu_i32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // consumer: one thread spins (bounded, ~10 s; the error word epoch[1] records a timeout)
 __device__ __forceinline__ void halo_link_wait(const HaloLink& h) {
   if (!h.wait_own || !(h.wait_lo | h.wait_hi)) return;

@@ -251,11 +251,12 @@ def test_dgrad_composite_and_plane_ranges_are_the_kernels():
         assert torch.equal(gx.storage, gx_ref.storage)
 
 
-@pytest.mark.parametrize("shape", [(1, 128, 128, 16, 16, 16), (1, 64, 128, 8, 8, 8), (2, 128, 64, 8, 8, 8),
-                                   (1, 256, 512, 4, 4, 4)])
+@pytest.mark.parametrize("shape", [(1, 128, 256, 4, 16, 16), (1, 64, 128, 8, 8, 8), (2, 128, 64, 8, 8, 8),
+                                   (1, 256, 512, 4, 4, 4), (1, 512, 512, 2, 16, 16)])
 def test_tc_forward_split_k_workspace(shape):
-    # vm_conv3d_fwd_tc_ws: deep-level shapes split the K reduction over CTAs with f32 partials
-    # in the caller's scratch; the last split of each tile sums them in split order
+    # vm_conv3d_fwd_tc_ws: shapes with few tile units (<= SMs / 4, the deep levels of a split
+    # volume) split the K reduction over CTAs with f32 partials in the caller's scratch; the
+    # last split of each tile sums them in split order
     B, cin, cout, D, H, W = shape
     rng = np.random.default_rng(7 + sum(shape))
     x = O.bf16_round(rng.standard_normal((B, D, H, W, cin)).astype(np.float32))
@@ -272,7 +273,6 @@ def test_tc_forward_split_k_workspace(shape):
     ws = torch.zeros(nbytes // 4 + 64, dtype=torch.float32, device="cuda")
     flags = _lib.VM_CONV_RELU | _lib.VM_CONV_MASK
     outs = []
-    _lib.load().vm_debug_set_fwd_max_split(3)  # split-K is off by default (slower on B200)
     for use_ws in (False, True, True):
         ys = Slab(B, cout, D, H, W, torch.bfloat16, "cuda")
         if use_ws:
@@ -282,7 +282,6 @@ def test_tc_forward_split_k_workspace(shape):
             _lib.call("vm_conv3d_fwd_tc", xs.p(), xs.bstride, _lib.ptr(wp), _lib.ptr(bt), ys.p(), ys.bstride,
                       ms.p(), ms.bstride, B, cin, cout, D, H, W, flags, _lib.stream_ptr())
         outs.append(ys.interior().cpu().numpy())
-    _lib.load().vm_debug_set_fwd_max_split(1)
     assert np.array_equal(outs[1], outs[2])          # deterministic
     assert rel_l2(outs[1], outs[0]) <= 5e-3          # same math, other f32 summation order
     dense = np.maximum(O.conv3d_dense(x.astype(np.float64), w.astype(np.float64), b.astype(np.float64)), 0)
