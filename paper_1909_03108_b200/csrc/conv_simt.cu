@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(128) k_conv_fwd_simt(const T* __restrict__ x, 
   Vec8<T>::store(y + gy.at(b, cgo, d, h, wv), acc);
 }
 
-// Weight-gradient partials.  grid = (nsplit, 27 * CGin * CGout); each block reduces
+// Weight-gradient partials.  grid = (27 * CGin * CGout, nsplit); each block reduces
 // its voxel chunk for one (tap, ci-block, co-block) to 64 values (fixed order).
 template <typename T>
 __global__ void __launch_bounds__(256) k_conv_wgrad_simt(const T* __restrict__ x, Slab gx,
@@ -126,13 +126,13 @@ __global__ void __launch_bounds__(256) k_conv_wgrad_simt(const T* __restrict__ x
                                                          float* __restrict__ ws, int B, int CGin,
                                                          int CGout, int64_t chunk) {
   __shared__ float red[8][65];
-  const int combo = blockIdx.y;
+  const int combo = blockIdx.x;  // x: 27*CGin*CGout exceeds grid.y's 65535 for 512 -> 512
   const int t = combo / (CGin * CGout);
   const int cgi = (combo / CGout) % CGin;
   const int cgo = combo % CGout;
   const int kd = t / 9, kh = (t / 3) % 3, kw = t % 3;
   const int64_t nvox = (int64_t)B * gg.D * gg.H * gg.W;
-  const int64_t v0 = blockIdx.x * chunk;
+  const int64_t v0 = blockIdx.y * chunk;
   const int64_t v1 = min(nvox, v0 + chunk);
   float acc[64];
 #pragma unroll
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(256) k_conv_wgrad_simt(const T* __restrict__ x
     for (int wi = 0; wi < 8; ++wi) s += red[wi][threadIdx.x];
     const int ci = threadIdx.x / 8, co = threadIdx.x % 8;
     // ws layout: [split][t][CGin*8][CGout*8]
-    int64_t idx = (((int64_t)blockIdx.x * 27 + t) * (CGin * 8) + cgi * 8 + ci) * (CGout * 8) + cgo * 8 + co;
+    int64_t idx = (((int64_t)blockIdx.y * 27 + t) * (CGin * 8) + cgi * 8 + ci) * (CGout * 8) + cgo * 8 + co;
     ws[idx] = s;
   }
 }
@@ -358,7 +358,7 @@ extern "C" int vm_conv3d_wgrad_simt(int dtype, const void* x, int64_t x_bstride,
   float* wsw = static_cast<float*>(ws);
   float* wsb = wsw + (size_t)ns * 27 * CGin * 8 * CGout * 8;
   cudaStream_t st = as_stream(stream);
-  dim3 grid(ns, 27 * CGin * CGout);
+  dim3 grid(27 * CGin * CGout, ns);
   dim3 gridb(ns, CGout);
   if (dtype == VM_F32) {
     k_conv_wgrad_simt<float><<<grid, 256, 0, st>>>((const float*)x, gx, (const float*)gy, gg, wsw,

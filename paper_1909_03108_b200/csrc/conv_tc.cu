@@ -633,7 +633,8 @@ struct WgParams {
   int64_t x_bstride;
   int64_t plane8;   // elements per channel-group plane
   int B, D, H, W, Hp, Wp, P;
-  int CG, CGo, Cout, Nc;
+  int CG, CGo, Cout, Nc;  // CGo: gy channel groups staged per unit (Nc / 8 of one output chunk)
+  int nchunk, NcTot;      // output-channel chunks of Nc in this launch (NcTot = nchunk * Nc)
   int KS, RR;       // anchors per stage, staged rows per group (KS + 8)
   int gdelta;       // row misalignment of the gy box start (128B-inner mode)
   int gwide;        // 1: gy map has 128-byte inner boxes
@@ -653,7 +654,7 @@ struct WgParams {
   uint32_t g_bytes; // per stage loaded: CGo * RR * 16 (allocated: Nc/8 groups)
   uint32_t stage_bytes;
   uint32_t idesc;
-  float* ws;        // [kidx = b*ksplit + ks][MT][3][Nc][128]
+  float* ws;        // [kidx = b*ksplit + ks][MT][3][NcTot][128]
   long long* dbg;   // optional cycle probes [gridDim][8] (vm_debug_set_fwd_probe)
 };
 
@@ -668,7 +669,10 @@ __global__ void __launch_bounds__(192, 1)
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages], tfull, tempty;
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int mg_cta = blockIdx.x % p.n_mtgroups;  // every unit of this CTA has the same M-tile group
+  // every unit of this CTA has the same (output chunk, M-tile group) column
+  const int ncol = p.n_mtgroups * p.nchunk;
+  const int col = blockIdx.x % ncol;
+  const int mg_cta = col % p.n_mtgroups, chunk = col / p.n_mtgroups;
   const int mt0 = mg_cta * p.mt_per_unit;
   const int nmt = min(p.mt_per_unit, p.MT - mt0);
   // ones block for the bias gradient, written once into every stage buffer
@@ -719,8 +723,8 @@ __global__ void __launch_bounds__(192, 1)
       }
       const uint32_t tx = (uint32_t)nvalid * (p.runs ? Rrun : p.RR) * 16 + p.g_bytes;
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        const int ks = (u / p.n_mtgroups) % p.ksplit;
-        const int b = u / (p.n_mtgroups * p.ksplit);
+        const int ks = (u / ncol) % p.ksplit;
+        const int b = u / (ncol * p.ksplit);
         // K stages interleaved over the split CTAs (stage s -> CTA s % ksplit): at any time the
         // CTAs read one contiguous window of rows, and the kd-shifted gy slices (1-2 planes back)
         // were read a few windows earlier by other CTAs: L2 hits instead of DRAM re-reads
@@ -737,9 +741,9 @@ __global__ void __launch_bounds__(192, 1)
           mbar_arrive_expect_tx(&full[stage], tx);
           const int gr0 = (int)(k0 + p.P + p.Wp + 1);
           if (p.gwide)
-            tma_load_4d(sG, &gmap, &full[stage], 0, (gr0 - p.gdelta) >> 3, 0, b);
+            tma_load_4d(sG, &gmap, &full[stage], 0, (gr0 - p.gdelta) >> 3, chunk * p.CGo, b);
           else
-            tma_load_4d(sG, &gmap, &full[stage], 0, gr0, 0, b);
+            tma_load_4d(sG, &gmap, &full[stage], 0, gr0, chunk * p.CGo, b);
           if (p.runs) {
             for (int r = r0; r <= r_end; ++r) {
               const int kd = r / p.CG, cg = r % p.CG;
@@ -774,7 +778,7 @@ __global__ void __launch_bounds__(192, 1)
     const long long t_m0 = dbg ? (long long)clock64() : 0;
     long long t_wf = 0, t_first = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      const int ks = (u / p.n_mtgroups) % p.ksplit;
+      const int ks = (u / ncol) % p.ksplit;
       // K stages interleaved over the split CTAs (stage s -> CTA s % ksplit): at any time the
       // CTAs read one contiguous window of rows, and the kd-shifted gy slices (1-2 planes back)
       // were read a few windows earlier by other CTAs: L2 hits instead of DRAM re-reads
@@ -846,7 +850,7 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     const int q = warp & 3;
-    const int kidx = blockIdx.x / p.n_mtgroups;
+    const int kidx = blockIdx.x / ncol;
     mbar_wait(&tfull, 0);
     tc_fence_after();
     const int m_row = q * 32 + lane;
@@ -856,7 +860,7 @@ __global__ void __launch_bounds__(192, 1)
           uint32_t r[16];
           tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)((m * 3 + kw) * p.Nc + n0), r);
           tmem_ld_wait();
-          float* dst = p.ws + ((((int64_t)kidx * p.MT + mt0 + m) * 3 + kw) * p.Nc + n0) * 128 + m_row;
+          float* dst = p.ws + ((((int64_t)kidx * p.MT + mt0 + m) * 3 + kw) * p.NcTot + chunk * p.Nc + n0) * 128 + m_row;
 #pragma unroll
           for (int e = 0; e < 16; ++e) dst[e * 128] = __uint_as_float(r[e]);
         }
@@ -2513,7 +2517,13 @@ struct WgPlan {
 };
 
 int g_force_runs = -1, g_force_ks = 0, g_force_mpu = 0;  // tools/tune_wgrad.py overrides
-int g_wg_chunk = 1;  // vm_debug_set_wgrad_chunk (A/B of the input-channel chunks)
+int g_wg_chunk = 1;  // vm_debug_set_wgrad_chunk (A/B of the input-channel chunks; 2: any volume)
+int g_wg_merge = 1;  // vm_debug_set_wgrad_merge (A/B: output chunks as one launch vs one call each)
+constexpr int kWgradMaxCout = 160, kWgradChunk = 128;
+// Cout > 160 in whole 128-channel chunks: one launch, chunk = CTA column (else one call per chunk)
+static bool wgrad_merged_chunks(int Cout) {
+  return g_wg_merge && Cout > kWgradMaxCout && Cout % kWgradChunk == 0;
+}
 thread_local int g_wg_phase = 0;  // vm_conv3d_wgrad_tc_phase: 0 all, 1 main kernel(s), 2 finalize
 // splits bias_grad_partial_bf16 uses for this shape (the finalize's phase needs the count only)
 static int bias_grad_partial_count(int B, int Cout, int D, int H, int W) {
@@ -2537,9 +2547,13 @@ int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
   const int64_t rows = (int64_t)(D + 2) * p.P;
   p.plane8 = rows * 8;
   p.CG = (Cin + 7) / 8;
-  p.CGo = (Cout + 7) / 8;
   p.Cout = Cout;
-  p.Nc = (Cout + 15) / 16 * 16;
+  // wide layers: output chunks of 128 channels (3 kw x 128 TMEM columns per M-tile) as
+  // independent CTA columns of ONE launch
+  p.nchunk = wgrad_merged_chunks(Cout) ? Cout / kWgradChunk : 1;
+  p.Nc = p.nchunk > 1 ? kWgradChunk : (Cout + 15) / 16 * 16;
+  p.NcTot = p.nchunk * p.Nc;
+  p.CGo = p.nchunk > 1 ? p.Nc / 8 : (Cout + 7) / 8;
   VM_REQUIRE(3 * p.Nc <= 512, VM_E_UNSUPPORTED, "vm_conv3d_wgrad_tc: Cout %d > 160 not supported yet", Cout);
   p.MT = (9 * p.CG + 15) / 16;
   p.ones_slot = (9 * p.CG) % 16 ? 9 * p.CG : -1;
@@ -2604,19 +2618,20 @@ int plan_wgrad(int B, int Cin, int Cout, int D, int H, int W, WgPlan& pl) {
   if (nsm <= 0) nsm = 148;
   // one unit per CTA (a second wave of units would double the slowest CTA's time): as many
   // K splits as fit in one wave, at least g_wg_min_spk stages per unit (pipeline fill)
-  int want = nsm / (p.n_mtgroups * B);
+  const int ncol = p.n_mtgroups * p.nchunk;
+  int want = nsm / (ncol * B);
   if (want < 1) want = 1;
   p.spk = (p.stages_total + want - 1) / want;
   if (p.spk < g_wg_min_spk) p.spk = g_wg_min_spk;
   p.ksplit = (p.stages_total + p.spk - 1) / p.spk;
-  p.units = p.n_mtgroups * B * p.ksplit;
+  p.units = ncol * B * p.ksplit;
   // (interleaved: 64->64 at 128^3 547 -> 535 us, 192->64 1281 -> 1242 us, 64->64 at 32^3 +2%)
   p.kinter = g_wg_interleave != 0;
   p.idesc = make_idesc_bf16(128, p.Nc, true, true);
   p.grid = p.units;
-  if (p.grid > nsm) p.grid = (nsm / p.n_mtgroups) * p.n_mtgroups;  // CTA keeps one M-tile group
-  if (p.grid < p.n_mtgroups) p.grid = p.n_mtgroups;
-  pl.ws_main = (size_t)(p.grid / p.n_mtgroups) * p.MT * 3 * p.Nc * 128 * sizeof(float);
+  if (p.grid > nsm) p.grid = (nsm / ncol) * ncol;  // CTA keeps one (chunk, M-tile group) column
+  if (p.grid < ncol) p.grid = ncol;
+  pl.ws_main = (size_t)(p.grid / ncol) * p.MT * 3 * p.NcTot * 128 * sizeof(float);
   pl.ws_bias = p.ones_slot >= 0 ? 0 : bias_grad_ws_bytes((int64_t)B * D * H * W, Cout);
   return VM_OK;
 }
@@ -2662,6 +2677,7 @@ extern "C" void vm_debug_skip_wgrad_finalize(int v) { g_skip_wg_fin = v; }
 extern "C" void vm_debug_set_wgrad_kd_runtime(int v) { g_wk_runtime = v; }
 extern "C" void vm_debug_set_wgrad_interleave(int v) { g_wg_interleave = v; }
 extern "C" void vm_debug_set_wgrad_chunk(int v) { g_wg_chunk = v; }
+extern "C" void vm_debug_set_wgrad_merge(int v) { g_wg_merge = v; }
 extern "C" void vm_debug_set_wgrad_ksub_stages(int v) { g_wk_ksub_min_stages = v > 0 ? v : 2; }
 
 extern "C" void vm_debug_set_wgrad_min_spk(int v) { g_wg_min_spk = v > 0 ? v : 2; }
@@ -2767,7 +2783,6 @@ static bool plan_wgrad_kd(int B, int Cin, int Cout, int D, int H, int W, WkParam
 // Output channels per weight-gradient call: the accumulators of one M-tile are 3 kw x Nc
 // TMEM columns (<= 512), so wider layers (cfg3/cfg4: up to 512 -> 1024 channels) run as
 // chunks of 128 output channels; each chunk reads its own channel-group planes of gy.
-constexpr int kWgradMaxCout = 160, kWgradChunk = 128;
 
 // Input-channel chunks of the kd weight gradient: a layer whose (cg, kh) slots span several
 // M-tile groups (the decoder's concat convs, 96->32) runs as chunks of 32 input channels, one
@@ -2775,18 +2790,21 @@ constexpr int kWgradMaxCout = 160, kWgradChunk = 128;
 // (one call: 3 M-tile groups, 5 live slots in the third tile, shorter K chunks to fit)
 constexpr int kWgChunkCin = 32;
 // (tools/wgrad_chunk_ab.py, alternating A/B: 96->32 at 256^3 5.41 -> 3.30 ms, 64->32 at 256^3
-// 2.68 -> 2.22 ms; at 128^3 and below the extra launches and gy re-reads lose: 64->32 at 128^3
-// 0.90x, 96->32 at 64^3 0.71x, so only volumes of >= 4 M voxels are chunked)
+// 2.68 -> 2.22 ms; at 2 M voxels only three or more chunks win: 96->32 at 32x256x256 (a depth-
+// split rank's block of 256^3) 678 -> 467 us, 96->32 at 128^3 1.08x, 64->32 at 128^3 0.90x,
+// 96->32 at 64x128x128 0.82x)
 static bool wgrad_kd_chunked(int B, int Cin, int Cout, int D, int H, int W) {
   WkParams pk;
   size_t wsk = 0;
-  return (int64_t)B * D * H * W >= (1 << 22) && Cin > kWgChunkCin && Cin % kWgChunkCin == 0 &&
+  const int64_t vox = (int64_t)B * D * H * W;
+  return (g_wg_chunk == 2 || vox >= (1 << 22) || (vox >= (1 << 21) && Cin >= 3 * kWgChunkCin)) &&
+         Cin > kWgChunkCin && Cin % kWgChunkCin == 0 &&
          plan_wgrad_kd(B, Cin, Cout, D, H, W, pk, wsk) &&
          pk.ngroups > 1 && plan_wgrad_kd(B, kWgChunkCin, Cout, D, H, W, pk, wsk);
 }
 
 extern "C" size_t vm_conv3d_wgrad_tc_ws(int B, int Cin, int Cout, int D, int H, int W) {
-  if (Cout > kWgradMaxCout) Cout = kWgradChunk;  // chunked (vm_conv3d_wgrad_tc): the widest chunk
+  if (Cout > kWgradMaxCout && !wgrad_merged_chunks(Cout)) Cout = kWgradChunk;  // one call per chunk: the widest
   WkParams pk;
   size_t wsk = 0;
   if (plan_wgrad_kd(B, Cin, Cout, D, H, W, pk, wsk)) {
@@ -2883,8 +2901,9 @@ static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_
   // down: the < 8 rows dropped lie in layer D's h = H+1 margin row, zero, as W + 2 >= 8 there)
   int64_t glim = rows - p.P;
   if (p.gwide && glim % 8 > p.Wp) glim += 8 - glim % 8;  // never drop interior rows (W + 2 < 8)
-  rc = p.gwide ? make_wide_map(&gmap, gy, gbs, p.CGo, glim, rows, B, p.RR / 8, p.CGo)
-               : make_group_map(&gmap, gy, gbs, p.CGo, glim, rows, B, p.RR, p.CGo);
+  const int cgo_all = p.nchunk * p.CGo;
+  rc = p.gwide ? make_wide_map(&gmap, gy, gbs, cgo_all, glim, rows, B, p.RR / 8, p.CGo)
+               : make_group_map(&gmap, gy, gbs, cgo_all, glim, rows, B, p.RR, p.CGo);
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
   // compile-time M-tile count (when every CTA holds the same number of tiles) and K steps
@@ -2907,7 +2926,7 @@ static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_
     rc = launch_status("vm_conv3d_wgrad_tc");
     if (rc) return rc;
   }
-  const int nk = p.grid / p.n_mtgroups;
+  const int nk = p.grid / (p.n_mtgroups * p.nchunk);
   // without a ones slot the bias gradient comes from separate partials, reduced by the
   // finalize's extra blocks
   int nsb = 0;
@@ -2921,10 +2940,10 @@ static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_
     }
   }
   if (phase == 1) return VM_OK;
-  const int ntiles = p.MT * 3 * (p.Nc / 8) * 4;
+  const int ntiles = p.MT * 3 * (p.NcTot / 8) * 4;
   const int nbias = p.ones_slot < 0 ? (Cout + 255) / 256 : 0;
   if (g_skip_wg_fin) return VM_OK;
-  launch_pdl(k_wgrad_finalize_tiles<false, 8>, ntiles + nbias, 256, 0, st, p.ws, gw, gb, nk, p.MT, p.Nc, p.CG, Cin, Cout,
+  launch_pdl(k_wgrad_finalize_tiles<false, 8>, ntiles + nbias, 256, 0, st, p.ws, gw, gb, nk, p.MT, p.NcTot, p.CG, Cin, Cout,
                                                                p.ones_slot, p.runs, wsb, nsb, (Cout + 7) / 8, ldo, ci_stride);
   return launch_status("vm_conv3d_wgrad_tc finalize");
 }
@@ -2935,7 +2954,7 @@ static int wgrad_tc_one(const void* x, int64_t x_bstride, const void* gy, int64_
 // finalize of the same call's workspace.  Layers that run as several calls into one workspace
 // (output-channel chunks, input-channel chunks) do everything in phase 1; phase 2 is a no-op.
 extern "C" int vm_conv3d_wgrad_tc_deferrable(int B, int Cin, int Cout, int D, int H, int W) {
-  return Cout <= kWgradMaxCout && !wgrad_kd_chunked(B, Cin, Cout, D, H, W);
+  return (Cout <= kWgradMaxCout || wgrad_merged_chunks(Cout)) && !wgrad_kd_chunked(B, Cin, Cout, D, H, W);
 }
 extern "C" int vm_conv3d_wgrad_tc_phase(const void* x, int64_t x_bstride, const void* gy, int64_t gy_bstride,
                                         float* gw, float* gb, void* ws, int B, int Cin, int Cout, int D, int H,
@@ -2956,7 +2975,8 @@ extern "C" int vm_conv3d_wgrad_tc(const void* x, int64_t x_bstride, const void* 
   VM_REQUIRE(B > 0 && Cin > 0 && Cout > 0 && D > 0 && H > 0 && W > 0, VM_E_SHAPE,
              "vm_conv3d_wgrad_tc: bad shape");
   const int64_t gbs = gy_bstride ? gy_bstride : default_bstride(Cout, D, H, W, 1);
-  if (Cout <= kWgradMaxCout) return wgrad_tc_one(x, x_bstride, gy, gbs, gw, gb, ws, B, Cin, Cout, D, H, W, Cout, stream);
+  if (Cout <= kWgradMaxCout || wgrad_merged_chunks(Cout))
+    return wgrad_tc_one(x, x_bstride, gy, gbs, gw, gb, ws, B, Cin, Cout, D, H, W, Cout, stream);
   const int64_t plane8 = (int64_t)(D + 2) * (H + 2) * (W + 2) * 8;
   for (int co0 = 0; co0 < Cout; co0 += kWgradChunk) {
     const int cc = min(kWgradChunk, Cout - co0);

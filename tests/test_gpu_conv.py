@@ -152,6 +152,10 @@ WG_SHAPES = [
     (1, 32, 256, 4, 6, 8),
     (1, 64, 200, 3, 4, 6),
     (1, 128, 512, 2, 4, 4),
+    # whole 128-channel chunks run as CTA columns of one launch: a ones slot (9*CG % 16 != 0),
+    # two samples, and the depth-split block of cfg3's deepest level (one wave, no K split)
+    (2, 72, 384, 3, 4, 10),
+    (1, 512, 512, 2, 16, 16),
 ]
 
 
