@@ -2300,6 +2300,8 @@ static size_t fwd_ws_need(int ksplit, int64_t ntu, int MB, int Nc) {
 // at cfg2's deep levels (41 units) it lost (see below) and stays off by that rule
 static int g_fwd_max_split = kFwdMaxSplit;  // vm_debug_set_fwd_max_split (A/B probes, tests)
 extern "C" void vm_debug_set_fwd_max_split(int v) { g_fwd_max_split = v < 1 ? 1 : v > kFwdMaxSplit ? kFwdMaxSplit : v; }
+static int g_fwd_force_split = 0;  // vm_debug_force_fwd_split (plan sweeps): only this K split
+extern "C" void vm_debug_force_fwd_split(int v) { g_fwd_force_split = v; }
 
 static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, const float* bias, void* y,
                          int64_t y_bstride, const void* mask, int64_t mask_bstride, int B, int Cin, int Cout, int D,
@@ -2444,7 +2446,8 @@ static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, 
     // split-K over the 3*KC (kc, kd) stages when a caller workspace can hold the f32
     // partials: more CTAs for layers with few tiles (deep levels)
     for (int ksplit = 1; ksplit <= g_fwd_max_split; ++ksplit) {
-      if (ksplit > 1 && ntu * 4 > nsm) break;  // enough tile units already
+      if (g_fwd_force_split && ksplit != g_fwd_force_split) continue;
+      if (ksplit > 1 && ntu * 4 > nsm && !g_fwd_force_split) break;  // enough tile units already
       const int spk = (3 * p.KC + ksplit - 1) / ksplit;
       if (ksplit > 1 &&
           ((3 * p.KC + spk - 1) / spk != ksplit || !ws || fwd_ws_need(ksplit, ntu, MB, N) > ws_bytes))
