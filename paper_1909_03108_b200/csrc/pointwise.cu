@@ -721,6 +721,180 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_grp(
   }
 }
 
+// Head backward for C = 16 / 32 on rows whose width is a multiple of 32 (every U-Net level
+// here): a warp owns 32 consecutive voxels of one row, a team of TPV = C/8 lanes owns TPV of
+// them (voxel u*(32/TPV) + team, u < TPV), each lane one 8-channel group of all TPV.  The
+// per-voxel softmax + loss gradient runs ONCE per voxel: the logit partials are
+// reduce-scattered over the team (lane cg ends with voxel cg's logits), lane cg computes that
+// voxel's dL/dlogits, and the team all-gathers them.  k_head_bwd_grp computed the softmax on
+// every lane of the group (TPV x the per-voxel scalar work) and decomposed every voxel index:
+// 800 thread instructions per voxel, issue-bound at ~0.3 of HBM.  Same partial layout.
+template <typename T, int C, int NC>
+__global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_team(
+    const T* __restrict__ y, Slab sy, const float* __restrict__ W, const float* __restrict__ bias,
+    const uint8_t* __restrict__ labels, const float* __restrict__ stats, T* __restrict__ g, Slab sg,
+    float* __restrict__ wpart, int B, float w_dice, float w_ce, float total, int dice_mask, float clamp,
+    int relu_mask, const float* __restrict__ dprobs) {
+  static_assert(C == 16 || C == 32, "team kernel: C = 16 or 32");
+  pdl_wait();
+  constexpr int TPV = C / 8;          // lanes per team = voxels per team
+  constexpr int TW = 32 / TPV;        // teams per warp
+  constexpr int NACC = 8 * NC + NC;   // this lane's channel group's weight grads + bias grads
+  constexpr int NWARP = kHeadThreads / 32;
+  // 32-voxel chunks per warp iteration, all loads issued first: 4 x 16 B per lane in flight
+  // (2 x 16 B at C = 16 with one chunk held the kernel to ~2.2 TB/s, latency-bound)
+  constexpr int CH = TPV == 2 ? 2 : 1;
+  __shared__ float sW[C * NC], sb[NC], coef[3 * NC];
+  __shared__ float red[NWARP][TPV][NACC];
+  for (int i = threadIdx.x; i < C * NC; i += blockDim.x) sW[i] = W[i];
+  if (threadIdx.x < NC) sb[threadIdx.x] = bias[threadIdx.x];
+  if (threadIdx.x == 0) {
+    const int nfg = __popc(dice_mask);
+    for (int k = 0; k < NC; ++k) {  // training.py:119-124
+      const float nk = stats ? 2.f * stats[k] + 1e-6f : 1.f;
+      const float dk = stats ? stats[NC + k] + stats[2 * NC + k] + 1e-6f : 1.f;
+      const bool on = (dice_mask >> k) & 1;
+      coef[3 * k + 0] = on ? (-w_dice / (float)nfg) / dk : 0.f;
+      coef[3 * k + 1] = on ? nk / dk : 0.f;
+      coef[3 * k + 2] = on ? 1.f : 0.f;
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cg = lane % TPV, team = lane / TPV, base = lane - cg;
+  const float* wr = sW + cg * 8 * NC;  // shared: TPV distinct banks per warp, no conflicts
+  const float ce_scale = -w_ce / total;
+  float acc[NACC];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) acc[i] = 0.f;
+  const uint32_t nchunk = (uint32_t)B * sy.D * sy.H * (sy.W / 32);
+  const uint32_t wstride = gridDim.x * NWARP;
+  for (uint32_t ch0 = blockIdx.x * NWARP + warp; ch0 < nchunk; ch0 += CH * wstride) {
+    float yv[CH][TPV][8];
+    int64_t go[CH];
+    uint32_t vme[CH];
+    int lab[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const uint32_t ch = min(ch0 + c * wstride, nchunk - 1);  // a clamped duplicate is not stored
+      const uint32_t v0 = ch * 32;
+      int b, d, h, w0;
+      decompose(v0, sy, b, d, h, w0);
+      const int64_t yo = sy.at(b, cg, d, h, w0 + team);
+      go[c] = sg.at(b, cg, d, h, w0 + team);
+#pragma unroll
+      for (int u = 0; u < TPV; ++u) V8<T>::ld(y + yo + (int64_t)u * TW * 8, yv[c][u]);
+      vme[c] = v0 + cg * TW + team;  // this lane's voxel for the scalar work: u = cg
+      lab[c] = labels && !dprobs ? (int)labels[vme[c]] : 255;
+    }
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const bool live = ch0 + c * wstride < nchunk;  // warp-uniform
+      // logit partials of this lane's 8 channels for all TPV voxels
+      float pl[TPV][NC];
+#pragma unroll
+      for (int u = 0; u < TPV; ++u)
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          float t = 0.f;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) t = fmaf(yv[c][u][j], wr[j * NC + k], t);
+          pl[u][k] = t;
+        }
+      // reduce-scatter over the team: lane cg keeps the sum for voxel u = cg
+      float lg[NC];
+      if (TPV == 2) {
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          const float keep = cg ? pl[1][k] : pl[0][k], send = cg ? pl[0][k] : pl[1][k];
+          lg[k] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          const bool hi = cg & 2;
+          const float k0 = (hi ? pl[2][k] : pl[0][k]) + __shfl_xor_sync(0xffffffffu, hi ? pl[0][k] : pl[2][k], 2);
+          const float k1 = (hi ? pl[3][k] : pl[1][k]) + __shfl_xor_sync(0xffffffffu, hi ? pl[1][k] : pl[3][k], 2);
+          const bool odd = cg & 1;
+          lg[k] = (odd ? k1 : k0) + __shfl_xor_sync(0xffffffffu, odd ? k0 : k1, 1);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NC; ++k) lg[k] += sb[k];
+      float m = lg[0];
+#pragma unroll
+      for (int k = 1; k < NC; ++k) m = fmaxf(m, lg[k]);
+      float p[NC], ssum = 0.f;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        p[k] = __expf(lg[k] - m);
+        ssum += p[k];
+      }
+      float gp[NC], dot = 0.f;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        p[k] = __fdividef(p[k], ssum);
+        const float gk = lab[c] == k ? 1.f : 0.f;
+        float r = coef[3 * k + 2] != 0.f ? coef[3 * k] * (2.f * gk - coef[3 * k + 1]) : 0.f;
+        // one-hot g: only the label's class has a cross-entropy term (training.py:125-126)
+        r += (lab[c] == k && p[k] >= clamp) ? ce_scale * __frcp_rn(p[k]) : 0.f;
+        if (dprobs) r = dprobs[(size_t)vme[c] * NC + k];  // external dL/dp
+        gp[k] = r;
+        dot += r * p[k];
+      }
+      float gl[NC];
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        gl[k] = live ? p[k] * (gp[k] - dot) : 0.f;  // ops.py:197-199
+        acc[8 * NC + k] += gl[k];                   // bias: every voxel once (its own lane)
+      }
+      // all-gather the team's dL/dlogits and finish every voxel's 8 channels of this lane
+#pragma unroll
+      for (int u = 0; u < TPV; ++u) {
+        float gu[NC];
+#pragma unroll
+        for (int k = 0; k < NC; ++k) gu[k] = __shfl_sync(0xffffffffu, gl[k], base + u);
+        float o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float sacc = 0.f;
+#pragma unroll
+          for (int k = 0; k < NC; ++k) {
+            sacc = fmaf(wr[j * NC + k], gu[k], sacc);
+            acc[j * NC + k] = fmaf(yv[c][u][j], gu[k], acc[j * NC + k]);
+          }
+          o[j] = (relu_mask && !(yv[c][u][j] > 0.f)) ? 0.f : sacc;
+        }
+        if (live) V8<T>::st(g + go[c] + (int64_t)u * TW * 8, o);
+      }
+    }
+  }
+  // reduce over the lanes of this warp holding the same group, then over warps (fixed order);
+  // bias sums live on every lane (one voxel each) and are reduced over all 32 lanes
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) {
+    float t = acc[i];
+    if (i >= 8 * NC) {
+#pragma unroll
+      for (int o = 1; o < TPV; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    }
+#pragma unroll
+    for (int o = TPV; o < 32; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane < TPV) red[warp][lane][i] = t;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < C * NC + NC; i += blockDim.x) {
+    float t = 0.f;
+    if (i < C * NC) {
+      const int c = i / NC, k = i % NC;
+      for (int wq = 0; wq < NWARP; ++wq) t += red[wq][c / 8][(c % 8) * NC + k];
+    } else {
+      for (int wq = 0; wq < NWARP; ++wq) t += red[wq][0][8 * NC + (i - C * NC)];
+    }
+    wpart[(int64_t)blockIdx.x * (C * NC + NC) + i] = t;
+  }
+}
+
 // one block per column: thread t sums rows t, t+256, ... (a few independent loads), then a
 // fixed shared-memory tree (deterministic).  One warp per column looped ~20 dependent L2
 // round trips over the 592 partial rows (7 us per call).
@@ -1012,6 +1186,8 @@ static int head_bwd(int dtype, const void* y, int64_t y_bstride, const float* w,
                     const uint8_t* labels, const float* stats, void* g, int64_t g_bstride, float* wpartials, int B,
                     int C, int ncls, int D, int H, int W, float w_dice, float w_ce, float total_voxels,
                     int dice_mask, float clamp, int relu_mask, const float* dprobs, void* stream);
+static int g_head_team_off = 0;  // vm_debug_set_head_team (A/B against k_head_bwd_grp)
+extern "C" void vm_debug_set_head_team(int on) { g_head_team_off = !on; }
 
 extern "C" int vm_head_bwd(int dtype, const void* y, int64_t y_bstride, const float* w,
                            const float* b, const uint8_t* labels, const float* stats, void* g,
@@ -1047,6 +1223,19 @@ static int head_bwd(int dtype, const void* y, int64_t y_bstride, const float* w,
   if (dtype == VM_BF16) {  // fixed-width kernels: C in {8, 16, 32, 64, 128}, 2..4 classes (the
     using T = __nv_bfloat16;  // generic one-thread-per-voxel kernel took 38.7 ms at 256^3, C = 64)
     auto st = as_stream(stream);
+    if ((C == 16 || C == 32) && W % 32 == 0 && !g_head_team_off) {
+#define HT_CASE(CC, NN)                                                                                  \
+  case NN * 1000 + CC:                                                                                   \
+    launch_pdl(k_head_bwd_team<T, CC, NN>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, labels, stats,   \
+               (T*)g, sg, wpartials, B, w_dice, w_ce, total_voxels, dice_mask, clamp, relu_mask, dprobs);          \
+    return launch_status("vm_head_bwd");
+      switch (ncls * 1000 + C) {
+        HT_CASE(16, 2) HT_CASE(32, 2) HT_CASE(16, 3) HT_CASE(32, 3) HT_CASE(16, 4) HT_CASE(32, 4)
+        default:
+          break;
+      }
+#undef HT_CASE
+    }
 #define HB_CASE(CC, NN)                                                                                  \
   case NN * 1000 + CC:                                                                                   \
     launch_pdl(k_head_bwd_grp<T, CC, NN>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, labels, stats, \

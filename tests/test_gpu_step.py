@@ -189,3 +189,44 @@ def test_tc_step_other_class_counts(ncls, dice):
     worst = max(rel_l2(grads[k][0], rgrads[k][0]) for k in rgrads)
     assert worst <= 1e-1, worst
     mesh.shutdown()
+
+
+@pytest.mark.parametrize("C,ncls,dprobs", [(16, 3, False), (32, 3, False), (16, 2, False), (32, 4, False),
+                                           (16, 3, True), (32, 3, True)])
+def test_head_bwd_team_kernel_matches_group_kernel(C, ncls, dprobs):
+    # rows of 32+ voxels take the team kernel (softmax once per voxel, reduce-scattered logits);
+    # the per-group kernel is the reference: same gradients and head-weight partial sums
+    from paper_1909_03108_b200 import _lib
+    from paper_1909_03108_b200.step import Slab
+
+    lib = _lib.load()
+    torch.manual_seed(C + ncls)
+    B, D, H, W = 2, 3, 5, 64
+    y = Slab(B, C, D, H, W, torch.bfloat16, "cuda")
+    y.storage.normal_()
+    w = torch.randn(C * ncls, device="cuda") * 0.3
+    b = torch.randn(ncls, device="cuda") * 0.1
+    nvox = B * D * H * W
+    lab = torch.randint(0, ncls, (nvox,), dtype=torch.uint8, device="cuda")
+    stats = torch.rand(3 * ncls + 1, device="cuda") * 100 + 1
+    dp = torch.randn(nvox * ncls, device="cuda")
+    nb = int(lib.vm_head_partials_count(B, D, H, W))
+    out = {}
+    for team in (0, 1):
+        lib.vm_debug_set_head_team(team)
+        g = Slab(B, C, D, H, W, torch.bfloat16, "cuda")
+        wp = torch.zeros(nb * (C * ncls + ncls), device="cuda")
+        if dprobs:
+            _lib.call("vm_head_bwd_dprobs", _lib.VM_BF16, y.p(), y.bstride, _lib.ptr(w), _lib.ptr(b), _lib.ptr(dp),
+                      g.p(), g.bstride, _lib.ptr(wp), B, C, ncls, D, H, W, 1, _lib.stream_ptr())
+        else:
+            _lib.call("vm_head_bwd", _lib.VM_BF16, y.p(), y.bstride, _lib.ptr(w), _lib.ptr(b), _lib.ptr(lab),
+                      _lib.ptr(stats), g.p(), g.bstride, _lib.ptr(wp), B, C, ncls, D, H, W, 0.9, 0.1, float(nvox),
+                      (1 << ncls) - 2, 1e-12, 1, _lib.stream_ptr())
+        torch.cuda.synchronize()
+        out[team] = (g.interior().float().cpu().numpy(), wp.view(nb, -1).double().sum(0).cpu().numpy())
+    lib.vm_debug_set_head_team(1)
+    # bf16 outputs: the logits are summed in another order, so a few elements round the other way
+    assert rel_l2(out[1][0], out[0][0]) <= 1e-3
+    assert rel_l2(out[1][1], out[0][1]) <= 1e-5
+    assert np.abs(out[1][0]).max() > 0
