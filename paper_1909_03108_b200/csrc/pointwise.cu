@@ -402,6 +402,7 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_fwd_fixed(
     const T* __restrict__ y, Slab sy, const float* __restrict__ W, const float* __restrict__ bias,
     const uint8_t* __restrict__ labels, int* __restrict__ label_err, float* __restrict__ probs,
     uint8_t* __restrict__ pred, float* __restrict__ partials, int B, float clamp) {
+  static_assert(sizeof(T) == 2, "fixed head kernels read bf16 channel groups as 16-byte words");
   pdl_wait();
   pdl_trigger();
   __shared__ float sW[C * NC], sb[NC], red[kHeadThreads / 32];
@@ -412,34 +413,65 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_fwd_fixed(
   float st[3 * NC + 1];
 #pragma unroll
   for (int k = 0; k < 3 * NC + 1; ++k) st[k] = 0.f;
-  // U voxels per thread per iteration with every load issued first (loads in flight bound it)
+  // U voxels per thread per iteration with every load issued first (loads in flight bound
+  // it): the raw 16-byte channel groups of all U voxels are loaded before any math, then the
+  // logits are summed in channel order (bitwise the same as a full dot product).  (Loading
+  // two groups at a time at U = 1 held C = 32 to ~0.37 of HBM.)
   constexpr int U = C <= 16 ? 2 : 1;
+  constexpr int NG = C / 8;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < nvox; v0 += U * stride) {
-    // logits accumulated as the channel groups arrive (same c order as a full dot product,
-    // so bitwise the same), instead of holding all C inputs: C = 32/64 spilled otherwise
     float lgu[U][NC], gk[U][NC];
     bool ok[U];
+    int4 raw[U][C <= 32 ? NG : 1];
+    uint32_t labu[U];
+    const T* basep[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t v = v0 + u * stride;
       ok[u] = v < nvox;
       int b, d, h, w;
       decompose(ok[u] ? (uint32_t)v : 0u, sy, b, d, h, w);
-      const T* base = y + sy.at(b, 0, d, h, w);
+      basep[u] = y + sy.at(b, 0, d, h, w);
+      if (C <= 32) {
+#pragma unroll
+        for (int cg = 0; cg < (C <= 32 ? NG : 1); ++cg)
+          raw[u][cg] = *reinterpret_cast<const int4*>(basep[u] + cg * sy.plane());
+      }
+      labu[u] = ok[u] ? labels[v] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
 #pragma unroll
       for (int k = 0; k < NC; ++k) lgu[u][k] = sb[k];
+      if (C <= 32) {
+#pragma unroll
+        for (int cg = 0; cg < (C <= 32 ? NG : 1); ++cg) {
+          const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&raw[u][cg]);
+          float t8[8];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 f = __bfloat1622float2(hv[j]);
+            t8[2 * j] = f.x;
+            t8[2 * j + 1] = f.y;
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int k = 0; k < NC; ++k) lgu[u][k] = fmaf(t8[j], sW[(cg * 8 + j) * NC + k], lgu[u][k]);
+        }
+      } else {
 #pragma unroll 2
-      for (int cg = 0; cg < C / 8; ++cg) {
-        float t8[8];
-        V8<T>::ld(base + cg * sy.plane(), t8);
+        for (int cg = 0; cg < NG; ++cg) {
+          float t8[8];
+          V8<T>::ld(basep[u] + cg * sy.plane(), t8);
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+          for (int j = 0; j < 8; ++j)
 #pragma unroll
-          for (int k = 0; k < NC; ++k) lgu[u][k] = fmaf(t8[j], sW[(cg * 8 + j) * NC + k], lgu[u][k]);
+            for (int k = 0; k < NC; ++k) lgu[u][k] = fmaf(t8[j], sW[(cg * 8 + j) * NC + k], lgu[u][k]);
+        }
       }
-#pragma unroll
-      const uint32_t lab = ok[u] ? labels[v] : 0u;
+      const uint32_t lab = labu[u];
       if (lab >= (uint32_t)NC) atomicOr(label_err, 1);  // training.py:68-69 (np.eye indexing) raises
 #pragma unroll
       for (int k = 0; k < NC; ++k) gk[u][k] = lab == (uint32_t)k ? 1.f : 0.f;
@@ -721,6 +753,126 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_grp(
   }
 }
 
+// Team reduce-scatter of per-lane logit partials pl[u][k] (u < TPV voxels, this lane's 8
+// channels): lane cg of the team ends with the full logits of voxel u = cg.
+template <int TPV, int NC>
+__device__ __forceinline__ void team_reduce_scatter(const float (&pl)[TPV][NC], int cg, float (&lg)[NC]) {
+  if (TPV == 2) {
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const float keep = cg ? pl[1][k] : pl[0][k], send = cg ? pl[0][k] : pl[TPV - 1][k];
+      lg[k] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const bool hi = cg & 2;
+      const float k0 = (hi ? pl[2 % TPV][k] : pl[0][k]) + __shfl_xor_sync(0xffffffffu, hi ? pl[0][k] : pl[2 % TPV][k], 2);
+      const float k1 = (hi ? pl[3 % TPV][k] : pl[1][k]) + __shfl_xor_sync(0xffffffffu, hi ? pl[1][k] : pl[3 % TPV][k], 2);
+      const bool odd = cg & 1;
+      lg[k] = (odd ? k1 : k0) + __shfl_xor_sync(0xffffffffu, odd ? k0 : k1, 1);
+    }
+  }
+}
+
+// Head forward for C = 16 / 32 on rows whose width is a multiple of 32: the team layout of
+// k_head_bwd_team (TPV = C/8 lanes per TPV voxels, one 8-channel group per lane, 8*NC weights
+// per lane), so every lane issues TPV (x2 at C = 16) 16-byte loads before any math and the
+// softmax / statistics run once per voxel.  The one-thread-per-voxel kernel hoisted all C*NC
+// weights into registers and spilled at C = 32 (~0.45 of HBM).
+template <typename T, int C, int NC>
+__global__ void __launch_bounds__(kHeadThreads, 2) k_head_fwd_team(
+    const T* __restrict__ y, Slab sy, const float* __restrict__ W, const float* __restrict__ bias,
+    const uint8_t* __restrict__ labels, int* __restrict__ label_err, float* __restrict__ probs,
+    uint8_t* __restrict__ pred, float* __restrict__ partials, int B, float clamp) {
+  static_assert(C == 16 || C == 32, "team kernel: C = 16 or 32");
+  pdl_wait();
+  pdl_trigger();
+  constexpr int TPV = C / 8, TW = 32 / TPV, NWARP = kHeadThreads / 32;
+  constexpr int CH = TPV == 2 ? 2 : 1;
+  __shared__ float sW[C * NC], sb[NC], red[NWARP];
+  for (int i = threadIdx.x; i < C * NC; i += blockDim.x) sW[i] = W[i];
+  if (threadIdx.x < NC) sb[threadIdx.x] = bias[threadIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cg = lane % TPV, team = lane / TPV;
+  float wr[8 * NC];
+#pragma unroll
+  for (int i = 0; i < 8 * NC; ++i) wr[i] = sW[cg * 8 * NC + i];
+  float st[3 * NC + 1];
+#pragma unroll
+  for (int k = 0; k < 3 * NC + 1; ++k) st[k] = 0.f;
+  const uint32_t nchunk = (uint32_t)B * sy.D * sy.H * (sy.W / 32);
+  const uint32_t wstride = gridDim.x * NWARP;
+  for (uint32_t ch0 = blockIdx.x * NWARP + warp; ch0 < nchunk; ch0 += CH * wstride) {
+    float yv[CH][TPV][8];
+    uint32_t vme[CH];
+    uint32_t lab[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const uint32_t ch = min(ch0 + c * wstride, nchunk - 1);
+      const uint32_t v0 = ch * 32;
+      int b, d, h, w0;
+      decompose(v0, sy, b, d, h, w0);
+      const int64_t yo = sy.at(b, cg, d, h, w0 + team);
+#pragma unroll
+      for (int u = 0; u < TPV; ++u) V8<T>::ld(y + yo + (int64_t)u * TW * 8, yv[c][u]);
+      vme[c] = v0 + cg * TW + team;
+      lab[c] = labels[vme[c]];
+    }
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      if (ch0 + c * wstride >= nchunk) break;  // warp-uniform
+      float pl[TPV][NC];
+#pragma unroll
+      for (int u = 0; u < TPV; ++u)
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          float t = 0.f;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) t = fmaf(yv[c][u][j], wr[j * NC + k], t);
+          pl[u][k] = t;
+        }
+      float lg[NC];
+      team_reduce_scatter<TPV, NC>(pl, cg, lg);
+#pragma unroll
+      for (int k = 0; k < NC; ++k) lg[k] += sb[k];
+      float m = lg[0];
+#pragma unroll
+      for (int k = 1; k < NC; ++k) m = fmaxf(m, lg[k]);
+      float p[NC], ssum = 0.f;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        p[k] = __expf(lg[k] - m);
+        ssum += p[k];
+      }
+      if (lab[c] >= (uint32_t)NC) atomicOr(label_err, 1);  // training.py:68-69 (np.eye indexing) raises
+      const uint32_t v = vme[c];
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        p[k] = __fdividef(p[k], ssum);
+        const float g = lab[c] == (uint32_t)k ? 1.f : 0.f;
+        if (probs) probs[(size_t)v * NC + k] = p[k];
+        st[k] += p[k] * g;
+        st[NC + k] += p[k];
+        st[2 * NC + k] += g;
+        st[3 * NC] += -__logf(fmaxf(p[k], clamp)) * g;
+      }
+      if (pred) {  // np.argmax of these probabilities: the first maximal class
+        int a = 0;
+#pragma unroll
+        for (int k = 1; k < NC; ++k) a = p[k] > p[a] ? k : a;
+        pred[v] = (uint8_t)a;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3 * NC + 1; ++k) {
+    float s = block_sum(st[k], red);
+    if (threadIdx.x == 0) partials[(int64_t)blockIdx.x * (3 * NC + 1) + k] = s;
+  }
+}
+
 // Head backward for C = 16 / 32 on rows whose width is a multiple of 32 (every U-Net level
 // here): a warp owns 32 consecutive voxels of one row, a team of TPV = C/8 lanes owns TPV of
 // them (voxel u*(32/TPV) + team, u < TPV), each lane one 8-channel group of all TPV.  The
@@ -803,22 +955,7 @@ __global__ void __launch_bounds__(kHeadThreads, 2) k_head_bwd_team(
         }
       // reduce-scatter over the team: lane cg keeps the sum for voxel u = cg
       float lg[NC];
-      if (TPV == 2) {
-#pragma unroll
-        for (int k = 0; k < NC; ++k) {
-          const float keep = cg ? pl[1][k] : pl[0][k], send = cg ? pl[0][k] : pl[1][k];
-          lg[k] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < NC; ++k) {
-          const bool hi = cg & 2;
-          const float k0 = (hi ? pl[2][k] : pl[0][k]) + __shfl_xor_sync(0xffffffffu, hi ? pl[0][k] : pl[2][k], 2);
-          const float k1 = (hi ? pl[3][k] : pl[1][k]) + __shfl_xor_sync(0xffffffffu, hi ? pl[1][k] : pl[3][k], 2);
-          const bool odd = cg & 1;
-          lg[k] = (odd ? k1 : k0) + __shfl_xor_sync(0xffffffffu, odd ? k0 : k1, 1);
-        }
-      }
+      team_reduce_scatter<TPV, NC>(pl, cg, lg);
 #pragma unroll
       for (int k = 0; k < NC; ++k) lg[k] += sb[k];
       float m = lg[0];
@@ -1090,6 +1227,9 @@ extern "C" int vm_head_partials_count(int B, int D, int H, int W) {
   return (int)(blocks < cap ? (blocks < 1 ? 1 : blocks) : cap);
 }
 
+static int g_head_team_off = 0;  // vm_debug_set_head_team (A/B against the per-voxel / per-group kernels)
+extern "C" void vm_debug_set_head_team(int on) { g_head_team_off = !on; }
+
 extern "C" int vm_head_fwd(int dtype, const void* y, int64_t y_bstride, const float* w,
                            const float* b, const uint8_t* labels, int* label_err, float* probs,
                            uint8_t* pred, float* partials, int B, int C, int ncls, int D, int H, int W, float clamp, void* stream) {
@@ -1102,6 +1242,20 @@ extern "C" int vm_head_fwd(int dtype, const void* y, int64_t y_bstride, const fl
   if (dtype == VM_BF16) {  // fixed-width kernels: C in {8, 16, 32, 64}, 2..4 classes
     using T = __nv_bfloat16;
     auto st = as_stream(stream);
+    // (C = 16: the per-voxel kernel with two voxels in flight is faster, 22 vs 25 us at 128^3)
+    if (C == 32 && W % 32 == 0 && !g_head_team_off) {
+#define HT_CASE(CC, NN)                                                                                  \
+  case NN * 1000 + CC:                                                                                   \
+    launch_pdl(k_head_fwd_team<T, CC, NN>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, labels,         \
+               label_err, probs, pred, partials, B, clamp);                                                         \
+    return launch_status("vm_head_fwd");
+      switch (ncls * 1000 + C) {
+        HT_CASE(32, 2) HT_CASE(32, 3) HT_CASE(32, 4)
+        default:
+          break;
+      }
+#undef HT_CASE
+    }
 #define HF_CASE(CC, NN)                                                                               \
   case NN * 1000 + CC:                                                                                \
     launch_pdl(k_head_fwd_fixed<T, CC, NN>, grid, kHeadThreads, 0, st, (const T*)y, sy, w, b, labels, \
@@ -1186,8 +1340,6 @@ static int head_bwd(int dtype, const void* y, int64_t y_bstride, const float* w,
                     const uint8_t* labels, const float* stats, void* g, int64_t g_bstride, float* wpartials, int B,
                     int C, int ncls, int D, int H, int W, float w_dice, float w_ce, float total_voxels,
                     int dice_mask, float clamp, int relu_mask, const float* dprobs, void* stream);
-static int g_head_team_off = 0;  // vm_debug_set_head_team (A/B against k_head_bwd_grp)
-extern "C" void vm_debug_set_head_team(int on) { g_head_team_off = !on; }
 
 extern "C" int vm_head_bwd(int dtype, const void* y, int64_t y_bstride, const float* w,
                            const float* b, const uint8_t* labels, const float* stats, void* g,

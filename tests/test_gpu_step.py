@@ -230,3 +230,43 @@ def test_head_bwd_team_kernel_matches_group_kernel(C, ncls, dprobs):
     assert rel_l2(out[1][0], out[0][0]) <= 1e-3
     assert rel_l2(out[1][1], out[0][1]) <= 1e-5
     assert np.abs(out[1][0]).max() > 0
+
+
+@pytest.mark.parametrize("C,ncls", [(32, 3), (32, 2), (32, 4)])
+def test_head_fwd_team_kernel_matches_voxel_kernel(C, ncls):
+    # 32-channel rows of 32+ voxels take the team forward kernel: probabilities, argmax, loss-statistic
+    # partial sums and the label-range flag as the one-thread-per-voxel kernel gives them
+    from paper_1909_03108_b200 import _lib
+    from paper_1909_03108_b200.step import Slab
+
+    lib = _lib.load()
+    torch.manual_seed(C * ncls)
+    B, D, H, W = 2, 3, 4, 96
+    y = Slab(B, C, D, H, W, torch.bfloat16, "cuda")
+    y.storage.normal_()
+    w = torch.randn(C * ncls, device="cuda") * 0.3
+    b = torch.randn(ncls, device="cuda") * 0.1
+    nvox = B * D * H * W
+    nb = int(lib.vm_head_partials_count(B, D, H, W))
+    for bad in (False, True):
+        lab = torch.randint(0, ncls, (nvox,), dtype=torch.uint8, device="cuda")
+        if bad:
+            lab[nvox // 3] = ncls
+        out = {}
+        for team in (0, 1):
+            lib.vm_debug_set_head_team(team)
+            err = torch.zeros(1, dtype=torch.int32, device="cuda")
+            probs = torch.zeros(nvox * ncls, device="cuda")
+            pred = torch.zeros(nvox, dtype=torch.uint8, device="cuda")
+            part = torch.zeros(nb * (3 * ncls + 1), device="cuda")
+            _lib.call("vm_head_fwd", _lib.VM_BF16, y.p(), y.bstride, _lib.ptr(w), _lib.ptr(b), _lib.ptr(lab),
+                      _lib.ptr(err), _lib.ptr(probs), _lib.ptr(pred), _lib.ptr(part), B, C, ncls, D, H, W, 1e-12,
+                      _lib.stream_ptr())
+            torch.cuda.synchronize()
+            out[team] = (probs.cpu().numpy(), pred.cpu().numpy(), part.view(nb, -1).double().sum(0).cpu().numpy(),
+                         int(err.item()))
+        lib.vm_debug_set_head_team(1)
+        assert rel_l2(out[1][0], out[0][0]) <= 1e-6
+        assert (out[1][1] != out[0][1]).mean() <= 1e-3  # argmax ties may resolve differently at ulp level
+        assert rel_l2(out[1][2], out[0][2]) <= 1e-5
+        assert out[1][3] == out[0][3] == int(bad)

@@ -38,3 +38,6 @@ for k, v in sorted(by.items(), key=lambda kv: -kv[1][0])[:28]:
     print(f"{k[0]:6s} {k[1]:11s} n={v[2]:2d} {v[0] * 1e3:8.1f} us {v[1] / max(v[0], 1e-9) / 1e9:7.1f} TF/s")
 for r in sorted(rows, key=lambda r: -r["ms"])[:16]:
     print(f"  {r['layer']:12s} {r['kind']:11s} {r['ms'] * 1e3:7.1f} us {r['flops'] / max(r['ms'], 1e-9) / 1e9:7.1f} TF/s")
+for k, v in sorted(by.items()):
+    if k[1] in ("head_fwd", "head_bwd", "pool_fwd", "pool_bwd", "up_fwd", "up_bwd", "sgd", "pack"):
+        print(f"  {k[0]:6s} {k[1]:11s} {v[0] * 1e3:8.1f} us")
