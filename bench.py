@@ -449,8 +449,30 @@ def run_ours(a):
     del recs, img, lab
     st.upload(img_h, lab_h)
     st.forward()
-    parity = _first_loss_check(a.config, st.loss()[0], world)
     torch.cuda.synchronize()
+    if transport.startswith("peer"):
+        # the peer-memory halo has only run emulated on one GPU before a multi-GPU box: if its
+        # first step misses a neighbour's signal or gives the wrong loss on ANY rank, every
+        # rank rebuilds the step on the NCCL transport (decided collectively)
+        bad = 0
+        try:
+            st.halo.check()
+            _first_loss_check(a.config, st.loss()[0], world)
+        except (Exception, SystemExit) as e:
+            print(f"[bench] !!! rank {rank}: peer-memory halo failed its first step ({e})", file=sys.stderr, flush=True)
+            bad = 1
+        flag = torch.tensor([bad], device="cuda", dtype=torch.int32)
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+        if int(flag.item()):
+            peer_failed = st  # keep alive: peers may still hold IPC mappings of its slabs
+            st = UNetStep(graph, params, batch=B // bdiv, ctx=ctx, dtype=torch.bfloat16, conv_impl=a.conv,
+                          global_batch=B)
+            transport = "nccl (peer-memory halo failed its first step)"
+            st.upload(img_h, lab_h)
+            st.forward()
+            torch.cuda.synchronize()
+            del peer_failed
+    parity = _first_loss_check(a.config, st.loss()[0], world)
 
     def barrier():
         if world > 1:
@@ -525,6 +547,11 @@ def run_ours(a):
                 "ms_nohalo": ms_nohalo, "bytes_per_step_rank": nbytes,
                 "exchange_byte_count_per_step": halo_formula_bytes(vm, graph, mesh, layout, B),
                 "nvlink_gbs_achieved_if_exposed": nbytes / max(ms_ab - ms_nohalo, 1e-6) / 1e6}
+        if transport.startswith("peer"):
+            try:  # a neighbour signal missed during the timed steps would have left stale margins
+                st.halo.check()
+            except Exception as e:  # noqa: BLE001
+                halo["error"] = str(e)
     elif not a.no_emulate:
         try:
             halo = emulated_halo(a, torch, vm, peaks)
