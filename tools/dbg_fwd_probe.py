@@ -24,8 +24,8 @@ for (ci, co, e, dd) in SHAPES:
     _lib.call("vm_pack_weights", _lib.ptr(w), _lib.ptr(wp), ci, co, 0, _lib.stream_ptr())
     nb = _lib.call_size("vm_conv3d_fwd_tc_ws_bytes", 1, ci, co, dd, e, e)
     ws = torch.zeros(max(nb, 16) // 4 + 64, device='cuda')
-    for ms, fl in ((1, 1), (16, 1)):
-        lib.vm_debug_set_fwd_max_split(ms)
+    for ms, fl in ((1, 1), (1, 1 | (1 << 9)), (1, 1 | (1 << 11)), (2, 1)):
+        lib.vm_debug_force_fwd_split(ms)
         for it in range(3):
             buf.zero_()
             lib.vm_debug_set_fwd_probe(ctypes.c_void_p(buf.data_ptr()) if it == 2 else None)
@@ -37,8 +37,8 @@ for (ci, co, e, dd) in SHAPES:
         act = d[d[:, 0] > 0]
         m = act.mean(0).tolist()
         mx = act.max(0).values.tolist()
-        print(f"{ci}->{co} @{dd}x{e}^2 split<={ms} flags {fl:#x}: ctas={len(act)} MMA loop {m[0]:.0f} (max {mx[0]:.0f}) "
+        print(f"{ci}->{co} @{dd}x{e}^2 split={ms} flags {fl:#x}: ctas={len(act)} MMA loop {m[0]:.0f} (max {mx[0]:.0f}) "
               f"wait_tmem {m[1]:.0f} wait_full {m[2]:.0f} | epi total {m[4]:.0f} (max {mx[4]:.0f}) "
               f"epi_wait {m[3]:.0f} fixup {m[5]:.0f} (max {mx[5]:.0f}) drain|publish {m[6]:.0f} (max {mx[6]:.0f}) "
               f"epi-start|arrive {m[7]:.0f} (max {mx[7]:.0f})")
-    lib.vm_debug_set_fwd_max_split(16)
+    lib.vm_debug_force_fwd_split(0)
