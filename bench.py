@@ -93,6 +93,8 @@ def args_parse():
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of the captured step graph")
     p.add_argument("--no-emulate", action="store_true", help="N = 1: skip the emulated-split halo measurement")
     p.add_argument("--emulate-split", type=int, default=8, help="N = 1: depth split whose rank block is emulated")
+    p.add_argument("--emulate-config", default="cfg3", choices=["cfg3", "cfg4"],
+                   help="N = 1: cfg3 depth-split rank block, or one 256^3 rank block of cfg4's 2x2x2 mesh (NCCL)")
     p.add_argument("--emulate-transport", default="peer", choices=["peer", "nccl"],
                    help="N = 1: halo transport of the emulated split")
     p.add_argument("--halo-transport", default="peer", choices=["peer", "nccl"],
@@ -100,6 +102,8 @@ def args_parse():
     p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     p.add_argument("--cpu-budget", type=float, default=150.0, help="seconds of CPU-oracle time (reference arm)")
     p.add_argument("--layer-csv", default=None, help="write per-layer kernel times here")
+    p.add_argument("--scaling-base", default="auto", choices=["auto", "on", "off"],
+                   help="cfg3: also time the unpartitioned network on rank 0's GPU alone (auto: at N > 1)")
     a = p.parse_args()
     if a.config == "auto":
         a.config = "cfg2" if a.gpus == 1 else "cfg3"
@@ -310,10 +314,11 @@ def emulated_halo(a, torch, vm, peaks):
     from paper_1909_03108_b200.halo import nccl_comm_ptr
     from paper_1909_03108_b200.step import UNetStep
 
-    K = a.emulate_split
-    c = CONFIGS["cfg3"]
+    mesh3 = a.emulate_config == "cfg4"  # one rank's 256^3 block of cfg4's 2x2x2 mesh
+    K = 8 if mesh3 else a.emulate_split
+    c = CONFIGS[a.emulate_config]
     E = c["extent"]
-    peer = a.emulate_transport == "peer"
+    peer = a.emulate_transport == "peer" and not mesh3  # the peer-memory push covers depth splits
     if not peer and not dist.is_initialized():
         with socket.socket() as s:
             s.bind(("127.0.0.1", 0))
@@ -324,16 +329,18 @@ def emulated_halo(a, torch, vm, peaks):
     mesh = vm.create_mesh([("one", 1)], backend="threads")
     graph = vm.build(cfg, mesh, {})
     params = vm.init_params(graph, 1)
-    loc = (E // K, E, E)
+    loc = (E // 2, E // 2, E // 2) if mesh3 else (E // K, E, E)
+    nbr6 = [0] * 6 if mesh3 else [0, 0, -1, -1, -1, -1]
     st = UNetStep(graph, params, dtype=torch.bfloat16, global_shape=(E, E, E), local_shape=loc)
     if peer:  # vm_halo_depth_push with every neighbour = this rank (wgrad overlaps exchange + dgrad)
-        st.use_peer_halo(nbr6=[0, 0, -1, -1, -1, -1])
+        st.use_peer_halo(nbr6=nbr6)
     else:
         comm = nccl_comm_ptr()
         ar = nccl_comm_ptr(dist.new_group(backend="nccl"))
-        st.use_nccl(comm, nbr6=[0, 0, -1, -1, -1, -1], ar_comm=ar)
+        st.use_nccl(comm, nbr6=nbr6, ar_comm=ar)
     img, lab = synth_record(E, 7, 0)
-    st.upload(torch.from_numpy(img[None, : loc[0], ..., None].copy()), torch.from_numpy(lab[None, : loc[0]].copy()))
+    blk = (slice(None, 1), slice(0, loc[0]), slice(0, loc[1]), slice(0, loc[2]))
+    st.upload(torch.from_numpy(img[None][blk][..., None].copy()), torch.from_numpy(lab[None][blk].copy()))
     for _ in range(2):
         st.step()
     torch.cuda.synchronize()
@@ -376,11 +383,14 @@ def emulated_halo(a, torch, vm, peaks):
                  "a 1-rank NCCL communicator (pack + NCCL group + unpack per conv)")
     return {
         "share": max(0.0, (res["halo"] - res["nohalo"]) / res["halo"]),
-        "method": f"emulated on 1 GPU: rank block {loc[0]}x{loc[1]}x{loc[2]} of cfg3 {K}-way depth split, periodic "
+        "method": f"emulated on 1 GPU: rank block {loc[0]}x{loc[1]}x{loc[2]} of "
+                  + ("cfg4's 2x2x2 mesh (faces, edges and corners through the 3 sequential phases)" if mesh3
+                     else f"cfg3 {K}-way depth split") + ", periodic "
                   f"halos (every neighbour = this rank) through {transport}; "
                   "A/B: (t_step - t_step_nohalo) / t_step, best of 3 alternating rounds, SGD at lr = 0 in both "
                   "arms (same work; keeps the wrong-margin arm from diverging)",
-        "transport": a.emulate_transport,
+        "transport": "peer" if peer else "nccl",
+        "emulated_config": a.emulate_config,
         "rounds_ms": rounds,
         "ms_step": res["halo"], "ms_nohalo": res["nohalo"],
         "bytes_per_step_rank": nbytes,
@@ -393,6 +403,45 @@ def emulated_halo(a, torch, vm, peaks):
         / (res["halo"] + fwd_bytes / (NVLINK_GBS * 1e9) * 1e3),
         "projected_whole_job_voxels_per_s": K * loc[0] * loc[1] * loc[2] / (res["halo"] * 1e-3),
     }
+
+
+def scaling_base(a, torch, vm):
+    """The 1-GPU point of a strong-scaling series ("cfg3 256^3 b32, 1 GPU
+    (scaling base)"): the same network and global volume, unpartitioned, on this process's
+    GPU alone, timed like the main run (captured step graph, max(5, steps) steps).  The
+    driver's N = 1 run measures cfg2 (BASELINE.json configs[1]); this gives the N > 1 lines
+    of cfg3 their own single-GPU denominator."""
+    import numpy as np
+
+    from paper_1909_03108_b200.data import synth_record
+    from paper_1909_03108_b200.step import UNetStep
+
+    c = CONFIGS[a.config]
+    E, B = c["extent"], c["batch"]
+    cfg = vm.recipe_for_resolution(E, c["scale"])
+    mesh = vm.create_mesh([("one", 1)], backend="threads")
+    try:
+        graph = vm.build(cfg, mesh, {})
+        st = UNetStep(graph, vm.init_params(graph, 1), batch=B, dtype=torch.bfloat16, conv_impl=a.conv)
+        recs = [synth_record(E, 7, i) for i in range(B)]
+        st.upload(torch.from_numpy(np.stack([r[0] for r in recs])[..., None]),
+                  torch.from_numpy(np.stack([r[1] for r in recs])))
+        for _ in range(2):
+            st.step()
+        torch.cuda.synchronize()
+        g, note = _capture(torch, st, not a.no_graph)
+        fn = g.replay if g is not None else st.step
+        for _ in range(max(3, a.warmup)):
+            fn()
+        ms = _timed(torch, fn, max(5, a.steps), torch.cuda.synchronize)
+        out = {"config": f"{a.config} network, {E}^3, global batch {B}, unpartitioned on one GPU (rank 0's)",
+               "value": B * E ** 3 / (ms * 1e-3), "unit": "voxels/s", "ms_per_step": ms, "cuda_graph": note,
+               "loss": st.loss()[0]}
+        del g, fn, st
+        return out
+    finally:
+        mesh.shutdown()
+        torch.cuda.empty_cache()
 
 
 def run_ours(a):
@@ -604,6 +653,15 @@ def run_ours(a):
                 f.write(f"{r['layer']},{r['kind']},{r['ms']:.4f},{r['flops']:.0f},{r['bytes']:.0f},"
                         f"{r['flops'] / max(r['ms'], 1e-9) / 1e9:.1f},{r['bytes'] / max(r['ms'], 1e-9) / 1e6:.1f}\n")
 
+    base = None
+    if a.config == "cfg3" and (a.scaling_base == "on" or (a.scaling_base == "auto" and world > 1)):
+        if rank == 0:  # the other ranks wait at the barrier below (outside every timed region)
+            try:
+                base = scaling_base(a, torch, vm)
+            except Exception as e:  # noqa: BLE001
+                base = {"value": None, "error": f"{type(e).__name__}: {e}"}
+        if world > 1:
+            dist.barrier()
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -644,6 +702,7 @@ def run_ours(a):
         "clocks": clk.summary(),
         "gpu_launches": launches_per_step * a.steps,
         "halo": halo,
+        **({"scaling_base": base} if base is not None else {}),
         "kernel_ms_per_step": {k: round(cc["ms"], 4) for k, cc in classes.items()},
         "roofline_by_kind": {
             k: ({"bound": "tensor", "tflops": round(cc["flops"] / (cc["ms"] * 1e-3) / 1e12, 1),

@@ -285,6 +285,15 @@ int vm_nccl_bind(void);
 size_t vm_halo_slab_ws_bytes(int dtype, int B, int C, int D, int H, int W);
 int vm_halo_slab_fwd(void* comm, int dtype, void* slab, int64_t bstride, int B, int C, int D, int H, int W,
                      const int* nbr, void* ws, size_t ws_bytes, long long* bytes_sent, void* stream);
+/* The same margins in ONE round (3-D meshes: cfg4 2x2x2, cfg5 b x 2 x 2): boundary boxes go
+ * straight to up to 26 face / edge / corner neighbours (one pack launch, one NCCL group, one
+ * unpack launch per exchange instead of 3 of each); the slab is byte-identical to
+ * vm_halo_slab_fwd's (a diagonal neighbour's voxel arrives directly instead of over 2-3 hops).
+ * nbr26[k] = rank at offset s = (sd, sh, sw) in {-1,0,1}^3 \ {0}, k lexicographic (center
+ * skipped), -1 where there is none.  ws: vm_halo_slab_ws_bytes26 of device scratch. */
+size_t vm_halo_slab_ws_bytes26(int dtype, int B, int C, int D, int H, int W);
+int vm_halo_slab_fwd26(void* comm, int dtype, void* slab, int64_t bstride, int B, int C, int D, int H, int W,
+                       const int* nbr26, void* ws, size_t ws_bytes, long long* bytes_sent, void* stream);
 /* depth-phase layers of at least `bytes` per (sample, channel group) are sent zero-copy (no
  * pack / unpack: straight from / into the slab); returns the previous threshold (default: off) */
 long long vm_set_halo_zero_copy_min(long long bytes);

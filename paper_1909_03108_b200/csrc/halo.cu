@@ -309,6 +309,183 @@ extern "C" long long vm_halo_slab_face_bytes(int dtype, int B, int C, int D, int
   return face_bytes(s, Face{axis, 1, 0, nullptr});
 }
 
+// ------------------------------------------------------------------ one-phase halo (3-D meshes)
+// The same margins as the 3-phase protocol in ONE round: every rank sends its boundary boxes
+// straight to all (up to 26) face, edge and corner neighbours.  Direction k = index of the
+// offset s = (sd, sh, sw) in {-1,0,1}^3 \ {0}, lexicographic (opp(k) = 25 - k).  The message
+// for direction s is the interior box at layer 1 (s = -1) / n (s = +1) / 1..n (s = 0) per
+// axis; the message from the neighbour at offset s lands in the margin box at layer 0 / n+1 /
+// 1..n.  A corner or edge value is the diagonal neighbour's own interior voxel either way, so
+// the slab is byte-identical to the sequential protocol's (halo.py:109-155, where it travels
+// over 2-3 hops); at a global boundary nothing is sent and the margin stays zero.  Per
+// exchange: one pack launch, one NCCL group, one unpack launch (the 3-phase path: 3 of each).
+// Issue order: sends for k ascending; receives for k ascending from the neighbour at offset
+// opp(k) — so for every pair of ranks both sides walk their common directions in the same
+// order, and a rank that is every neighbour of itself (the periodic single-GPU emulation)
+// receives the message of direction k in its margin on side opp(k), as a torus would.
+struct Box {
+  int lo[3], n[3];
+  uint8_t* buf;
+};
+struct BoxSet {
+  Box b[26];
+  int start[27];  // prefix sums of the boxes' 16-byte units (one flat grid over all boxes)
+  int n;
+  int64_t bstride_b, plane_b;
+  int CG, B, D, H, W;
+  int vec;
+};
+
+__host__ __device__ inline int64_t box_units(const BoxSet& s, const Box& x) {
+  return (int64_t)s.B * s.CG * x.n[0] * x.n[1] * x.n[2] * (s.vec / 16);
+}
+
+template <bool PACK>
+__global__ void __launch_bounds__(256) k_slab_boxes(uint8_t* __restrict__ slab, const BoxSet s) {
+  pdl_wait();
+  const int upv = s.vec / 16;
+  const int Hp = s.H + 2, Wp = s.W + 2;
+  const int total = s.start[s.n];
+  // one flat grid over all boxes (26 per-box grids left ~20 us of empty blocks at 256^3);
+  // consecutive threads walk a box's last dim (a contiguous run of the slab when it is W)
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
+    int j = 0;
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1)  // largest j with start[j] <= g
+      if (j + step < s.n && s.start[j + step] <= g) j += step;
+    const Box& x = s.b[j];
+    const int u = g - s.start[j];
+    const int n2u = x.n[2] * upv;
+    const int r = u / n2u, w = u - r * n2u;  // (b, cg, i0, i1) row, unit within the row
+    const int i1 = r % x.n[1], r2 = r / x.n[1];
+    const int i0 = r2 % x.n[0], bc = r2 / x.n[0];
+    const int cg = bc % s.CG, b = bc / s.CG;
+    const int64_t row = ((int64_t)(x.lo[0] + i0) * Hp + x.lo[1] + i1) * Wp + x.lo[2];
+    uint4* p = reinterpret_cast<uint4*>(slab + b * s.bstride_b + cg * s.plane_b + row * s.vec) + w;
+    uint4* m = reinterpret_cast<uint4*>(x.buf) + u;
+    if (PACK) *m = *p;
+    else *p = *m;
+  }
+}
+
+static int launch_boxes(bool pack, void* slab, BoxSet& s, cudaStream_t st) {
+  if (s.n == 0) return VM_OK;
+  s.start[0] = 0;
+  for (int i = 0; i < s.n; ++i) s.start[i + 1] = s.start[i] + (int)box_units(s, s.b[i]);
+  int64_t gx = ((int64_t)s.start[s.n] + 255) / 256;
+  if (gx > 148 * 8) gx = 148 * 8;  // grid-stride beyond one full wave
+  if (pack) launch_pdl(k_slab_boxes<true>, dim3((unsigned)gx), 256, 0, st, static_cast<uint8_t*>(slab), s);
+  else launch_pdl(k_slab_boxes<false>, dim3((unsigned)gx), 256, 0, st, static_cast<uint8_t*>(slab), s);
+  return launch_status(pack ? "vm_halo26 pack" : "vm_halo26 unpack");
+}
+
+// box of direction k: send (interior boundary) or recv (margin on side s)
+static Box dir_box(int k, bool recv, int D, int H, int W) {
+  const int t = k < 13 ? k : k + 1;
+  const int s[3] = {t / 9 - 1, (t / 3) % 3 - 1, t % 3 - 1};
+  const int n[3] = {D, H, W};
+  Box x{};
+  for (int a = 0; a < 3; ++a) {
+    x.n[a] = s[a] == 0 ? n[a] : 1;
+    x.lo[a] = s[a] == 0 ? 1 : (s[a] < 0 ? (recv ? 0 : 1) : (recv ? n[a] + 1 : n[a]));
+  }
+  return x;
+}
+
+static int64_t box_bytes(const BoxSet& s, const Box& x) { return box_units(s, x) * 16; }
+
+extern "C" size_t vm_halo_slab_ws_bytes26(int dtype, int B, int C, int D, int H, int W) {
+  BoxSet s{};
+  const FaceSet f = face_set(dtype, 0, B, C, D, H, W);
+  s.vec = f.vec, s.CG = f.CG, s.B = B;
+  size_t tot = 0;
+  for (int k = 0; k < 26; ++k) tot += (size_t)((box_bytes(s, dir_box(k, false, D, H, W)) + 255) / 256 * 256);
+  return 2 * tot;
+}
+
+extern "C" int vm_halo_slab_fwd26(void* comm, int dtype, void* slab, int64_t bstride, int B, int C, int D, int H,
+                                  int W, const int* nbr26, void* ws, size_t ws_bytes, long long* bytes_sent,
+                                  void* stream) {
+  VM_REQUIRE(slab && nbr26 && ws, VM_E_ARG, "vm_halo_slab_fwd26: null pointer");
+  VM_REQUIRE(dtype == VM_BF16 || dtype == VM_F32, VM_E_UNSUPPORTED, "vm_halo_slab_fwd26: dtype %d", dtype);
+  VM_REQUIRE(D >= 1 && H >= 1 && W >= 1, VM_E_HALO, "vm_halo_slab_fwd26: margin 1 exceeds local extent (%d,%d,%d)",
+             D, H, W);
+  VM_REQUIRE(ws_bytes >= vm_halo_slab_ws_bytes26(dtype, B, C, D, H, W), VM_E_ARG, "vm_halo_slab_fwd26: ws too small");
+  VM_REQUIRE((reinterpret_cast<uintptr_t>(slab) & 15) == 0 && (reinterpret_cast<uintptr_t>(ws) & 15) == 0,
+             VM_E_ALIGN, "vm_halo_slab_fwd26: 16-byte alignment required");
+  int any = 0;
+  for (int k = 0; k < 26; ++k) any |= nbr26[k] >= 0;
+  if (!any) return VM_OK;
+  VM_REQUIRE(comm, VM_E_ARG, "vm_halo_slab_fwd26: neighbours given without a communicator");
+  VM_REQUIRE(nccl_ok() || vm_nccl_bind() == VM_OK, VM_E_UNSUPPORTED, "vm_halo_slab_fwd26: NCCL not bound");
+  cudaStream_t st = as_stream(stream);
+  const FaceSet f = face_set(dtype, bstride, B, C, D, H, W);
+  BoxSet snd{}, rcv{};
+  snd.bstride_b = rcv.bstride_b = f.bstride_b, snd.plane_b = rcv.plane_b = f.plane_b;
+  snd.CG = rcv.CG = f.CG, snd.B = rcv.B = B, snd.D = rcv.D = D, snd.H = rcv.H = H, snd.W = rcv.W = W;
+  snd.vec = rcv.vec = f.vec;
+  uint8_t* w8 = static_cast<uint8_t*>(ws);
+  const size_t half = vm_halo_slab_ws_bytes26(dtype, B, C, D, H, W) / 2;
+  uint8_t* sp = w8;
+  uint8_t* rp = w8 + half;
+  uint8_t* sbuf[26] = {};
+  uint8_t* rbuf[26] = {};
+  size_t nbytes[26] = {};
+  for (int k = 0; k < 26; ++k) {
+    Box x = dir_box(k, false, D, H, W);
+    nbytes[k] = (size_t)box_bytes(snd, x);
+    const size_t adv = (nbytes[k] + 255) / 256 * 256;
+    sbuf[k] = sp, rbuf[k] = rp;  // the slot of direction k in both halves
+    sp += adv, rp += adv;
+    if (nbr26[k] >= 0) {
+      x.buf = sbuf[k];
+      snd.b[snd.n++] = x;
+    }
+  }
+  int rc = launch_boxes(true, slab, snd, st);
+  if (rc) return rc;
+  long long sent = 0;
+  for (int k = 0; k < 26; ++k) sent += nbr26[k] >= 0 ? (long long)nbytes[k] : 0;
+  if (g_loopback) {  // A/B probe: the periodic self-exchange as one device copy (no NCCL)
+    cudaMemcpyAsync(rbuf[0], sbuf[0], half, cudaMemcpyDeviceToDevice, st);
+  } else {
+    // a run of consecutive directions with the same peer is one message (its slots are
+    // contiguous in ws, in k order, on both sides: the receiver's run from that rank covers
+    // the same k) — one NCCL op per neighbour on a 2x2x2 mesh, one in all for the emulation
+    NCCL_CHECK(g_nccl.gstart(), "ncclGroupStart");
+    for (int k = 0; k < 26;) {
+      int e = k + 1;
+      if (nbr26[k] >= 0) {
+        while (e < 26 && nbr26[e] == nbr26[k]) ++e;
+        NCCL_CHECK(g_nccl.send(sbuf[k], (size_t)(sbuf[e - 1] - sbuf[k]) + nbytes[e - 1], kNcclUint8, nbr26[k], comm,
+                               st), "ncclSend");
+      }
+      k = e;
+    }
+    for (int k = 0; k < 26;) {
+      const int from = nbr26[25 - k];  // the neighbour at offset opp(k) sent its direction-k box
+      int e = k + 1;
+      if (from >= 0) {
+        while (e < 26 && nbr26[25 - e] == from) ++e;
+        NCCL_CHECK(g_nccl.recv(rbuf[k], (size_t)(rbuf[e - 1] - rbuf[k]) + nbytes[e - 1], kNcclUint8, from, comm, st),
+                   "ncclRecv");
+      }
+      k = e;
+    }
+    NCCL_CHECK(g_nccl.gend(), "ncclGroupEnd");
+  }
+  for (int k = 0; k < 26; ++k)
+    if (nbr26[25 - k] >= 0) {
+      Box x = dir_box(25 - k, true, D, H, W);  // margin on the side of the sender (offset opp(k))
+      x.buf = rbuf[k];
+      rcv.b[rcv.n++] = x;
+    }
+  rc = launch_boxes(false, slab, rcv, st);
+  if (rc) return rc;
+  if (bytes_sent) *bytes_sent += sent;
+  return VM_OK;
+}
+
 // In-place sum of n floats over the communicator (the weight-gradient / loss-statistics
 // all-reduce, mesh.py:195-233 / unet.py:434-441), on the caller's stream.
 extern "C" int vm_allreduce_f32(void* comm, float* buf, size_t n, void* stream) {

@@ -18,6 +18,7 @@ plan drives the channel-blocked slabs of the U-Net step (:mod:`.step`).
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 from . import _lib
@@ -467,12 +468,20 @@ class SlabHalo:
       per-phase pack / unpack (CudaSlabKernels, or TorchSlabKernels on CPU).
     """
 
-    def __init__(self, nbr6, ctx=None, comm=None, kernels=None):
+    def __init__(self, nbr6, ctx=None, comm=None, kernels=None, nbr26=None):
         self.nbr6 = [int(n) for n in nbr6]
         self.ctx, self.comm = ctx, comm
         self.kernels = kernels or CudaSlabKernels()
         self.ws = None
         self._sent = ctypes.c_longlong(0)
+        # one-phase exchange (vm_halo_slab_fwd26) on meshes that split more than one spatial dim:
+        # one pack / NCCL group / unpack per exchange instead of one per dim (VOXMESH_HALO_PHASES
+        # = 3 forces the sequential protocol, = 1 the one-phase one on any mesh)
+        split = sum(1 for a in range(3) if self.nbr6[2 * a] >= 0 or self.nbr6[2 * a + 1] >= 0)
+        phases = os.environ.get("VOXMESH_HALO_PHASES", "")
+        self.nbr26 = None
+        if nbr26 is not None and (phases == "1" or (split > 1 and phases != "3")):
+            self.nbr26 = [int(n) for n in nbr26]
 
     @property
     def active(self):
@@ -484,8 +493,8 @@ class SlabHalo:
             return
         import torch
 
-        need = max(int(_lib.call_size("vm_halo_slab_ws_bytes", _lib.dtype_code(s.dtype), s.B, s.C, s.D, s.H, s.W))
-                   for s in slabs)
+        fn = "vm_halo_slab_ws_bytes26" if self.nbr26 is not None else "vm_halo_slab_ws_bytes"
+        need = max(int(_lib.call_size(fn, _lib.dtype_code(s.dtype), s.B, s.C, s.D, s.H, s.W)) for s in slabs)
         dev = slabs[0].storage.device
         self.ws = torch.empty(need // 4 + 64, dtype=torch.float32, device=dev)
         self.ws_bytes = self.ws.numel() * 4
@@ -495,6 +504,13 @@ class SlabHalo:
 
     def forward(self, s, tag=_FWD_TAG):
         if not self.active:
+            return
+        if self.comm is not None and self.nbr26 is not None:
+            _lib.call("vm_halo_slab_fwd26", ctypes.c_void_p(self.comm), _lib.dtype_code(s.dtype), s.p(), s.bstride,
+                      s.B, s.C, s.D, s.H, s.W, (ctypes.c_int * 26)(*self.nbr26), _lib.ptr(self.ws), self.ws_bytes,
+                      ctypes.byref(self._sent), _lib.stream_ptr())
+            if self.ctx is not None:
+                self.ctx.counters["p2p_bytes"] = self.bytes_sent()
             return
         if self.comm is not None:
             _lib.call("vm_halo_slab_fwd", ctypes.c_void_p(self.comm), _lib.dtype_code(s.dtype), s.p(), s.bstride, s.B,
@@ -525,6 +541,32 @@ class SlabHalo:
         """Zero the margins this halo wrote (a gradient slab before its weight gradient)."""
         if self.active:
             self.kernels.zero(s, self.nbr6)
+
+
+def directions26():
+    """Offsets (sd, sh, sw) in {-1,0,1}^3 without the center, in the order of vm_halo_slab_fwd26's
+    nbr26 (lexicographic; the opposite of direction k is 25 - k)."""
+    return [(t // 9 - 1, (t // 3) % 3 - 1, t % 3 - 1) for t in range(27) if t != 13]
+
+
+def nbr26_of(nbr6, rank_at=None):
+    """Face, edge and corner neighbours from the face neighbours ``nbr6``: direction s exists
+    when every nonzero component has a neighbour on that side; its rank is ``rank_at(s)``
+    (the mesh coordinate + s), or, with ``rank_at`` None, the single rank all face neighbours
+    share (the periodic single-GPU emulation, every neighbour = this rank)."""
+    out = []
+    for s in directions26():
+        ok = all(si == 0 or nbr6[2 * a + (si > 0)] >= 0 for a, si in enumerate(s))
+        if not ok:
+            out.append(-1)
+        elif rank_at is not None:
+            out.append(int(rank_at(s)))
+        else:
+            ranks = {n for n in nbr6 if n >= 0}
+            if len(ranks) != 1:
+                raise HaloError("nbr26_of: diagonal ranks need rank_at unless all neighbours are one rank")
+            out.append(ranks.pop())
+    return out
 
 
 class HaloLinkC(ctypes.Structure):

@@ -29,7 +29,7 @@ import torch
 
 from . import _lib
 from .errors import GraphBuildError, VoxmeshError
-from .halo import HaloLinkC, PeerDepthHalo, SlabHalo, nccl_comm_of, nccl_second_comm
+from .halo import HaloLinkC, PeerDepthHalo, SlabHalo, nbr26_of, nccl_comm_of, nccl_second_comm
 
 _DT = {torch.bfloat16: _lib.VM_BF16, torch.float32: _lib.VM_F32}
 
@@ -141,7 +141,9 @@ class UNetStep:
             nbr6[2 * i], nbr6[2 * i + 1] = (-1 if lo is None else lo), (-1 if hi is None else hi)
         # the halo transport: NCCL through the C ABI when the mesh is spmd over NCCL (one C call
         # per slab, graph-capturable), else host-driven phases around ctx.exchange (threads)
-        self.halo = SlabHalo(nbr6, ctx=ctx, comm=nccl_comm_of(ctx))
+        comm = nccl_comm_of(ctx)
+        self.halo = SlabHalo(nbr6, ctx=ctx, comm=comm,
+                             nbr26=self._nbr26(ctx, layout, nbr6) if comm is not None else None)
         self.comm = self.halo.comm  # NCCL communicator of the step's collectives (None: ctx's)
         self.ar_comm = nccl_second_comm(ctx)  # bucketed weight-gradient all-reduce
         # overlap the exchange with the conv's interior planes: only the depth axis is split
@@ -500,13 +502,32 @@ class UNetStep:
         if self.has_halo:
             self.halo.zero(s)
 
+    @staticmethod
+    def _nbr26(ctx, layout, nbr6):
+        """Face, edge and corner neighbour ranks (vm_halo_slab_fwd26 order) of this rank: the
+        mesh coordinate moved by s along the mesh axes of the split spatial dims."""
+        if ctx is None or layout is None:
+            return None
+        axes = [layout.axis_for(d) for d in ("x", "y", "z")]
+        mesh = ctx.mesh
+
+        def rank_at(s):
+            coord = list(ctx.coord)
+            for i, si in enumerate(s):
+                if si:
+                    j = mesh.axis_index[axes[i]]
+                    coord[j] += si
+            return mesh.rank_of[tuple(coord)]
+
+        return nbr26_of(nbr6, rank_at)
+
     def use_nccl(self, comm, nbr6=None, ar_comm=None):
         """Route the halo and the collectives through NCCL communicator ``comm`` (an
         ncclComm_t).  ``nbr6`` overrides the neighbour ranks: a 1-rank communicator with the
         rank as its own lo and hi neighbour gives periodic halos on one GPU (the single-GPU
         emulation of a split: same pack / NCCL / unpack work, no NVLink wire time)."""
         if nbr6 is not None:
-            self.halo = SlabHalo(nbr6, ctx=self.ctx, comm=comm)
+            self.halo = SlabHalo(nbr6, ctx=self.ctx, comm=comm, nbr26=nbr26_of(nbr6))
             for i in range(3):
                 lo, hi = nbr6[2 * i], nbr6[2 * i + 1]
                 if lo >= 0 or hi >= 0:

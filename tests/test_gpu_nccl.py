@@ -174,3 +174,77 @@ def test_nccl_step_overlap_buckets_and_graph_are_bitwise(comms, zero_copy_min):
     torch.cuda.synchronize()
     assert torch.equal(eager.params, capt.params) and torch.equal(eager.stats, capt.stats)
     mesh.shutdown()
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("dims", [(0,), (0, 1, 2), (1, 2), (0, 2)])
+def test_one_phase_slab_halo_equals_wrap_padding(comms, dtype, dims):
+    """vm_halo_slab_fwd26 (faces, edges and corners straight from the diagonal neighbours, one
+    NCCL group) == the 3-phase protocol's slab == wrap padding, bitwise; bytes = the boxes sent."""
+    from paper_1909_03108_b200.halo import directions26, nbr26_of
+
+    comm, _ = comms
+    B, D, H, W, C = 2, 5, 6, 7, 20
+    x = O.bf16_round(np.random.default_rng(4).standard_normal((B, D, H, W, C)).astype(np.float32))
+    nbr = [-1] * 6
+    for a in dims:
+        nbr[2 * a] = nbr[2 * a + 1] = 0
+    n26 = nbr26_of(nbr)
+    out = {}
+    for name in ("one", "three"):
+        s = _slab(x, dtype)
+        if name == "one":
+            ws_bytes = _lib.call_size("vm_halo_slab_ws_bytes26", _lib.dtype_code(dtype), B, C, D, H, W)
+            ws = torch.empty(ws_bytes // 4 + 64, device="cuda")
+            sent = ctypes.c_longlong(0)
+            _lib.call("vm_halo_slab_fwd26", ctypes.c_void_p(comm), _lib.dtype_code(dtype), s.p(), s.bstride, B, C, D,
+                      H, W, (ctypes.c_int * 26)(*n26), _lib.ptr(ws), ws.numel() * 4, ctypes.byref(sent),
+                      _lib.stream_ptr())
+            torch.cuda.synchronize()
+            vox = sum(np.prod([e if si == 0 else 1 for si, e in zip(sd, (D, H, W))])
+                      for sd, r in zip(directions26(), n26) if r >= 0)
+            assert sent.value == B * s.CG * vox * 8 * s.storage.element_size()
+        else:
+            ws_bytes = _lib.call_size("vm_halo_slab_ws_bytes", _lib.dtype_code(dtype), B, C, D, H, W)
+            ws = torch.empty(ws_bytes // 4 + 64, device="cuda")
+            _lib.call("vm_halo_slab_fwd", ctypes.c_void_p(comm), _lib.dtype_code(dtype), s.p(), s.bstride, B, C, D,
+                      H, W, (ctypes.c_int * 6)(*nbr), _lib.ptr(ws), ws.numel() * 4, None, _lib.stream_ptr())
+            torch.cuda.synchronize()
+        out[name] = _padded(s)
+    xp = np.zeros((B, D, H, W, out["one"].shape[-1]))
+    xp[..., :C] = x
+    for a in range(3):
+        pad = [(0, 0)] * 5
+        pad[1 + a] = (1, 1)
+        xp = np.pad(xp, pad, mode="wrap" if a in dims else "constant")
+    assert np.array_equal(out["one"], xp)
+    assert np.array_equal(out["one"], out["three"])
+
+
+def test_nccl_step_3d_mesh_one_phase_is_bitwise_three_phase(comms, monkeypatch):
+    """The U-Net step on a periodic 2x2x2-style emulation (every dim split, every neighbour =
+    this rank): one-phase halo (vm_halo_slab_fwd26) == 3-phase halo, bitwise, eager and graph."""
+    E = 32
+    cfg = vm.UNetConfig(E, (16, 32), convs_per_block=2)
+    mesh = vm.create_mesh([("one", 1)])
+    graph = vm.build(cfg, mesh, {})
+    params = vm.init_params(graph, 6)
+    img, lab = O.record_for(E, 4)
+    host = (torch.from_numpy(img[None, ..., None].copy()), torch.from_numpy(lab[None].copy()))
+    c1, c2 = comms
+    runs = {}
+    for phases in ("1", "3"):
+        monkeypatch.setenv("VOXMESH_HALO_PHASES", phases)
+        st = UNetStep(graph, params, dtype=torch.bfloat16, device="cuda")
+        st.use_nccl(c1, nbr6=[0] * 6, ar_comm=c2)
+        assert (st.halo.nbr26 is not None) == (phases == "1")
+        st.keep_probs = True
+        st.upload(*host)
+        g = st.capture()
+        assert g is not None
+        g.replay()
+        torch.cuda.synchronize()
+        runs[phases] = (st.probs.cpu(), st.stats.cpu(), st.grads.cpu(), st.params.cpu())
+    for a, b in zip(runs["1"], runs["3"]):
+        assert torch.equal(a, b)
+    mesh.shutdown()

@@ -257,3 +257,56 @@ def test_augment_config_and_quantize_host_side():
         A.SynthConfig(radius_range=(0.5, 2.0))
     assert A.quantize_delta(0.3) == float(np.float32(round(0.3 * 256) / 256))
     assert A.with_seed(A.SynthConfig(), 7).seed == 7
+
+
+def test_one_phase_directions_rebuild_the_global_padding_on_a_2x2x2_mesh():
+    """nbr26_of / directions26 (the neighbour table of vm_halo_slab_fwd26): boxes sent in
+    direction k and received from the neighbour at offset opp(k) = 25 - k, in the C call's
+    order, give every rank of a 2x2x2 mesh the slice of the globally zero-padded volume
+    (faces, edges and corners; halo.py:109-155's result without its 3 hops)."""
+    import itertools
+
+    from paper_1909_03108_b200.halo import directions26, nbr26_of
+
+    n = (3, 4, 5)
+    g = np.random.default_rng(0).standard_normal((2 * n[0], 2 * n[1], 2 * n[2]))
+    gp = np.pad(g, 1)
+    coords = list(itertools.product(range(2), repeat=3))
+    rank_of = {c: r for r, c in enumerate(coords)}
+    dirs = directions26()
+    assert all(tuple(-v for v in dirs[k]) == dirs[25 - k] for k in range(26))
+    blocks, n26 = [], []
+    for c in coords:
+        b = np.zeros(tuple(e + 2 for e in n))
+        b[1:-1, 1:-1, 1:-1] = g[c[0] * n[0]:(c[0] + 1) * n[0], c[1] * n[1]:(c[1] + 1) * n[1],
+                                c[2] * n[2]:(c[2] + 1) * n[2]]
+        blocks.append(b)
+        nbr6 = []
+        for a in range(3):
+            for d in (-1, 1):
+                cc = list(c)
+                cc[a] += d
+                nbr6.append(rank_of[tuple(cc)] if 0 <= cc[a] < 2 else -1)
+        n26.append(nbr26_of(nbr6, lambda s, c=c: rank_of[tuple(ci + si for ci, si in zip(c, s))]))
+
+    def box(s, recv):
+        return tuple(slice(1, e + 1) if si == 0 else
+                     (slice(0, 1) if recv else slice(1, 2)) if si < 0 else
+                     (slice(e + 1, e + 2) if recv else slice(e, e + 1)) for si, e in zip(s, n))
+
+    sent = {r: [(n26[r][k], blocks[r][box(dirs[k], False)].copy()) for k in range(26) if n26[r][k] >= 0]
+            for r in range(8)}
+    for r in range(8):
+        for k in range(26):
+            src = n26[r][25 - k]
+            if src < 0:
+                continue
+            # the sender's messages to r in its send order; r's receives from src in its order
+            mine = [m for dst, m in sent[src] if dst == r]
+            order = [kk for kk in range(26) if n26[r][25 - kk] == src]
+            blocks[r][box(dirs[25 - k], True)] = mine[order.index(k)]
+    for r, c in enumerate(coords):
+        want = gp[c[0] * n[0]:c[0] * n[0] + n[0] + 2, c[1] * n[1]:c[1] * n[1] + n[1] + 2,
+                  c[2] * n[2]:c[2] * n[2] + n[2] + 2]
+        assert np.array_equal(blocks[r], want)
+    assert sum(v >= 0 for v in n26[0]) == 7
