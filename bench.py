@@ -93,6 +93,7 @@ def args_parse():
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of the captured step graph")
     p.add_argument("--no-emulate", action="store_true", help="N = 1: skip the emulated-split halo measurement")
     p.add_argument("--emulate-split", type=int, default=8, help="N = 1: depth split whose rank block is emulated")
+    p.add_argument("--no-emulate-cfg4", action="store_true", help="N = 1: skip the cfg4 2x2x2 rank-block emulation")
     p.add_argument("--emulate-config", default="cfg3", choices=["cfg3", "cfg4"],
                    help="N = 1: cfg3 depth-split rank block, or one 256^3 rank block of cfg4's 2x2x2 mesh (NCCL)")
     p.add_argument("--emulate-transport", default="peer", choices=["peer", "nccl"],
@@ -305,8 +306,9 @@ def _first_loss_check(cfg_name, loss, n_gpus):
 
 
 def emulated_halo(a, torch, vm, peaks):
-    """N = 1: one rank's block of cfg3's K-way depth split, periodic halos over a 1-rank NCCL
-    communicator, A/B against no exchange (see module docstring)."""
+    """N = 1: one rank's block of cfg3's K-way depth split (peer-memory push, or a 1-rank NCCL
+    communicator), or of cfg4's 2x2x2 mesh (one-phase NCCL exchange of faces, edges and corners),
+    periodic halos, A/B against no exchange (see module docstring)."""
     import numpy as np
     import torch.distributed as dist
 
@@ -606,6 +608,18 @@ def run_ours(a):
             halo = emulated_halo(a, torch, vm, peaks)
         except Exception as e:  # pragma: no cover
             halo = {"share": None, "method": f"emulation failed: {type(e).__name__}: {e}"}
+        if a.emulate_config == "cfg3" and not a.no_emulate_cfg4:
+            # the 2x2x2 mesh of cfg4 too: one 256^3 rank block, faces + edges + corners through
+            # the one-phase NCCL exchange (vm_halo_slab_fwd26)
+            import copy
+
+            b = copy.copy(a)
+            b.emulate_config = "cfg4"
+            try:
+                halo["cfg4_2x2x2"] = emulated_halo(b, torch, vm, peaks)
+            except Exception as e:  # pragma: no cover
+                halo["cfg4_2x2x2"] = {"share": None, "method": f"emulation failed: {type(e).__name__}: {e}"}
+            torch.cuda.empty_cache()
     else:
         halo = {"share": 0.0, "method": "one GPU, no partitioning"}
 
