@@ -305,10 +305,11 @@ __global__ void __launch_bounds__(320, 1)
       t_wait_tmem += clk() - tw0;
       tc_fence_after();
       const int s0 = (u % p.ksplit) * p.spk, s1 = min(nstage_k, s0 + p.spk);
-      // accumulator set of tap j = j % nacc (nacc in {1, 3}): consecutive MMAs of a tile go to
-      // different sets, so MB * nacc independent chains are in flight (a single chain of the 9
-      // taps of a stage ran at ~100 cycles per N = 128 MMA against a 64-cycle bound)
-      const uint32_t setcol = p.nacc == 3 ? (uint32_t)p.Nc : 0u;
+      // accumulator set of tap j = j % nacc (nacc in {1, 2, 3}): consecutive MMAs of a tile go
+      // to different sets, so MB * nacc independent chains are in flight (a single chain of the
+      // 9 taps of a stage ran at ~100 cycles per N = 128 MMA against a 64-cycle bound)
+      const uint32_t setcol = p.nacc > 1 ? (uint32_t)p.Nc : 0u;
+      const int nacc = p.nacc;
       for (int s = s0; s < s1; ++s) {
         const int kc = s / 3;
         const int ng = (kc * 2 + 1 < p.CG) ? 2 : 1;
@@ -333,8 +334,9 @@ __global__ void __launch_bounds__(320, 1)
           for (int j = 0; j < 9; ++j) {
             const uint64_t bdesc = b0desc + (uint64_t)(j * bstep);
             const uint64_t adesc = a0desc + (uint64_t)((j / 3) * wp1 + (j % 3));
-            const uint32_t acc = (first && (j == 0 || (j < 3 && setcol != 0u))) ? 0u : 1u;
-            const uint32_t dj = d0 + (uint32_t)(j % 3) * setcol;
+            const int set = nacc == 3 ? j % 3 : (nacc == 2 ? (j & 1) : 0);
+            const uint32_t acc = (first && j < nacc) ? 0u : 1u;
+            const uint32_t dj = d0 + (uint32_t)set * setcol;
 #pragma unroll
             for (int i = 0; i < MB; ++i)
               mma_bf16_ss(dj + (uint32_t)i * tstep, adesc + (uint64_t)(i * 128), bdesc, p.idesc, acc);
@@ -2428,7 +2430,11 @@ static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, 
   // operand reads at ~128 B/clk).  Units = tiles/MB spread over the SMs in waves.
   auto mma_cycles = [](int n, int chains) -> double {
     const double bw = n / 2.0 > 32 + n / 4.0 ? n / 2.0 : 32 + n / 4.0;
-    if (chains >= 3) return bw + 1;
+    // below N = 256 the stage's shared-memory traffic hides the accumulator dependency: forced
+    // plans (tools/dbg_fwd_plan.py) ran nacc = 1 as fast as or faster than nacc = 3 at N = 32..128
+    // (the extra sets only cost TMEM drain: 128->128 @16^3 15.9 vs 16.2 us, 96->32 @64^3 68.6 vs
+    // 77.9 us); the chain model (probe_tput5, an MMA-only loop) applies at N = 256
+    if (chains >= 3 || n < 256) return bw + 1;
     if (chains == 2) return bw * 1.3 > 49 ? bw * 1.3 : 49;
     return bw > 68 ? bw * 1.5 : 68;
   };
@@ -2456,7 +2462,7 @@ static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, 
       // the splits of a tile finish it together (they wait for each other): one wave only
       if (ksplit > 1 && units > nsm) break;
       const int64_t waves = (units + nsm - 1) / nsm;
-      for (int nacc : {1, 3}) {
+      for (int nacc : {1, 2, 3}) {
         if (g_fwd_force_acc && nacc != g_fwd_force_acc) continue;
         for (int nbuf = 2; nbuf >= 1; --nbuf) {
           if (nbuf * MB * nacc * N > 512) continue;
@@ -2466,7 +2472,11 @@ static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, 
           // single-buffered TMEM: the epilogue drain is not overlapped (~600 cycles per
           // 8-channel group and thread, measured with tools/dbg_fwd_probe.py; 200 made the
           // planner pick MB = 5 single-buffered for 32->96 at 64^3: 64.9 us vs 48.4 at MB = 2)
-          const double drain = nbuf == 1 ? MB * (N / 8.0) * 600.0 / (MB > 1 ? 2 : 1) : 0.0;
+          // TMEM reads at 64 B/clk per SM (B300_MICROARCH: LDTM throughput) bound the drain of
+          // MB x nacc x N f32 columns of 128 lanes; the last unit's drain is never overlapped
+          const double drain_one = std::max(MB * (N / 8.0) * 600.0 / (MB > 1 ? 2 : 1),
+                                            MB * nacc * N * 128.0 * 4.0 / 64.0);
+          const double drain = nbuf == 1 ? drain_one : drain_one / (double)waves;
           // split: partial write + the last split's read-back of every partial
           const double fix = ksplit > 1 ? MB * (N / 8.0) * (150.0 + 100.0 * ksplit) : 0.0;
           const double cost = (double)waves * ((double)spk * stage + drain + fix + 2000.0);

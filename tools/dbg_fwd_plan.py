@@ -18,7 +18,7 @@ for (ci, co, e) in [(64, 64, 32), (32, 64, 32), (192, 64, 32), (128, 128, 16), (
     wp = torch.empty(_lib.call_size("vm_packed_weights_bytes", ci, co) // 2, dtype=torch.bfloat16, device='cuda')
     _lib.call("vm_pack_weights", _lib.ptr(w), _lib.ptr(wp), ci, co, 0, _lib.stream_ptr())
     res = {}
-    for key in [(0, 0)] + [(mb, acc) for mb in (1, 2, 3, 4, 5) for acc in (1, 3)]:
+    for key in [(0, 0)] + [(mb, acc) for mb in (1, 2, 3, 4, 5) for acc in (1, 2, 3)]:
         lib.vm_debug_set_fwd_plan(*key)
         try:
             s = torch.cuda.Stream()
