@@ -559,44 +559,45 @@ __global__ void __launch_bounds__(320, 1)
         t_pub += clk() - tpa;
         t_arr = clk() - t_epi0;
         const long long tfx = clk();
-        // one row per warp at a time, lanes across the row's channel groups: every split's
-        // partial row is one coalesced read, 4 splits' loads in flight
-        const int ew = et >> 5, ln = et & 31;
+        // every thread owns (row, channel group) items of this split's row slice: 256 items in
+        // flight per CTA, consecutive threads across a row's groups (coalesced partial rows),
+        // 4 splits' loads issued per item before the adds (one row per warp at a time was
+        // latency-bound: 13 K cycles for the 2-split fix-up of a 128-channel tile)
         const int rps = (128 + p.ksplit - 1) / p.ksplit;
         const int rlo = ks * rps, rhi = min(128, rlo + rps);
-        for (int i = 0; i < p.MB; ++i) {
-          for (int row = rlo + ew; row < rhi; row += 8) {
-            bool valid;
-            int dq;
-            const int64_t orow = anchor_row(a0 + i * 128 + row, valid, dq);
-            if (!valid) continue;  // warp-uniform (one row per warp)
-            for (int g = ln; g < ng_out; g += 32) {
-              const int co0 = nch * p.Nc + g * 8;
-              if (co0 >= p.Cout) break;
-              int4 mkv = make_int4(0, 0, 0, 0);
-              if (domask) mkv = __ldg(reinterpret_cast<const int4*>(mbase + (co0 / 8) * p.plane8 + orow * 8));
-              float v[8];
+        const int gvalid = min(ng_out, (p.Cout - nch * p.Nc + 7) / 8);
+        const int items = p.MB * (rhi > rlo ? rhi - rlo : 0) * gvalid;
+        for (int it = et; it < items; it += 256) {
+          const int g = it % gvalid, ri = it / gvalid;
+          const int i = ri / (rhi - rlo), row = rlo + ri % (rhi - rlo);
+          bool valid;
+          int dq;
+          const int64_t orow = anchor_row(a0 + i * 128 + row, valid, dq);
+          if (!valid) continue;
+          const int co0 = nch * p.Nc + g * 8;
+          int4 mkv = make_int4(0, 0, 0, 0);
+          if (domask) mkv = __ldg(reinterpret_cast<const int4*>(mbase + (co0 / 8) * p.plane8 + orow * 8));
+          float v[8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) v[e] = 0.f;
-              for (int k0 = 0; k0 < p.ksplit; k0 += 4) {
-                float4 lo[4], hi[4];
+          for (int e = 0; e < 8; ++e) v[e] = 0.f;
+          const float* src0 = p.ws + (((int64_t)tu * p.MB + i) * 128 + row) * p.Nc + g * 8;
+          const int64_t kstride = (int64_t)ntu * p.MB * 128 * p.Nc;
+          for (int k0 = 0; k0 < p.ksplit; k0 += 4) {
+            float4 lo[4], hi[4];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  if (k0 + j >= p.ksplit) break;
-                  const float4* src = reinterpret_cast<const float4*>(
-                      p.ws + ((((int64_t)(k0 + j) * ntu + tu) * p.MB + i) * 128 + row) * p.Nc + g * 8);
-                  lo[j] = __ldcg(src), hi[j] = __ldcg(src + 1);
-                }
+            for (int j = 0; j < 4; ++j) {
+              if (k0 + j >= p.ksplit) break;
+              const float4* src = reinterpret_cast<const float4*>(src0 + (k0 + j) * kstride);
+              lo[j] = __ldcg(src), hi[j] = __ldcg(src + 1);
+            }
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {  // split order: deterministic
-                  if (k0 + j >= p.ksplit) break;
-                  v[0] += lo[j].x, v[1] += lo[j].y, v[2] += lo[j].z, v[3] += lo[j].w;
-                  v[4] += hi[j].x, v[5] += hi[j].y, v[6] += hi[j].z, v[7] += hi[j].w;
-                }
-              }
-              emit(ybase, co0, v, mkv, orow, dq);
+            for (int j = 0; j < 4; ++j) {  // split order: deterministic
+              if (k0 + j >= p.ksplit) break;
+              v[0] += lo[j].x, v[1] += lo[j].y, v[2] += lo[j].z, v[3] += lo[j].w;
+              v[4] += hi[j].x, v[5] += hi[j].y, v[6] += hi[j].z, v[7] += hi[j].w;
             }
           }
+          emit(ybase, co0, v, mkv, orow, dq);
         }
         // the last split to leave resets both counters for the next launch
         asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -2454,6 +2455,9 @@ static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, 
     for (int ksplit = 1; ksplit <= g_fwd_max_split; ++ksplit) {
       if (g_fwd_force_split && ksplit != g_fwd_force_split) continue;
       if (ksplit > 1 && ntu * 4 > nsm && !g_fwd_force_split) break;  // enough tile units already
+      // split plans with MB > 1 lost to MB = 1 at every forced-plan shape (tools/fwd_plan_sweep.py:
+      // 256->256 @8^3 split 12: 28.3 vs 19.4 us; 512->512 @2x16^2: 34.7 vs 24.5 us)
+      if (ksplit > 1 && MB > 1 && !g_fwd_force_split) break;
       const int spk = (3 * p.KC + ksplit - 1) / ksplit;
       if (ksplit > 1 &&
           ((3 * p.KC + spk - 1) / spk != ksplit || !ws || fwd_ws_need(ksplit, ntu, MB, N) > ws_bytes))
@@ -2477,8 +2481,13 @@ static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, 
           const double drain_one = std::max(MB * (N / 8.0) * 600.0 / (MB > 1 ? 2 : 1),
                                             MB * nacc * N * 128.0 * 4.0 / 64.0);
           const double drain = nbuf == 1 ? drain_one : drain_one / (double)waves;
-          // split: partial write + the last split's read-back of every partial
-          const double fix = ksplit > 1 ? MB * (N / 8.0) * (150.0 + 100.0 * ksplit) : 0.0;
+          // split: partial write, the wait for the tile's other splits, then each split CTA
+          // sums its 1/ksplit of the rows: 256 (row, group) items in flight, 4 splits' loads
+          // per round trip (~800 cycles from L2)
+          const double fix_items = MB * std::ceil(128.0 / ksplit) * (N / 8.0);
+          const double fix = ksplit > 1 ? 1500.0 + MB * (N / 8.0) * 60.0 +
+                                              std::ceil(fix_items / 256.0) * std::ceil(ksplit / 4.0) * 800.0
+                                        : 0.0;
           const double cost = (double)waves * ((double)spk * stage + drain + fix + 2000.0);
           if (cost < best * 0.999) {
             best = cost;
