@@ -93,9 +93,9 @@ def args_parse():
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of the captured step graph")
     p.add_argument("--no-emulate", action="store_true", help="N = 1: skip the emulated-split halo measurement")
     p.add_argument("--emulate-split", type=int, default=8, help="N = 1: depth split whose rank block is emulated")
-    p.add_argument("--no-emulate-cfg4", action="store_true", help="N = 1: skip the cfg4 2x2x2 rank-block emulation")
-    p.add_argument("--emulate-config", default="cfg3", choices=["cfg3", "cfg4"],
-                   help="N = 1: cfg3 depth-split rank block, or one 256^3 rank block of cfg4's 2x2x2 mesh (NCCL)")
+    p.add_argument("--no-emulate-cfg4", action="store_true", help="N = 1: skip the cfg4 / cfg5 rank-block emulations")
+    p.add_argument("--emulate-config", default="cfg3", choices=["cfg3", "cfg4", "cfg5"],
+                   help="N = 1: cfg3 depth-split rank block, or one rank block of cfg4's 2x2x2 / cfg5's b x 2x2 mesh (NCCL)")
     p.add_argument("--emulate-transport", default="peer", choices=["peer", "nccl"],
                    help="N = 1: halo transport of the emulated split")
     p.add_argument("--halo-transport", default="peer", choices=["peer", "nccl"],
@@ -316,7 +316,9 @@ def emulated_halo(a, torch, vm, peaks):
     from paper_1909_03108_b200.halo import nccl_comm_ptr
     from paper_1909_03108_b200.step import UNetStep
 
-    mesh3 = a.emulate_config == "cfg4"  # one rank's 256^3 block of cfg4's 2x2x2 mesh
+    # cfg4: one rank's 256^3 block of the 2x2x2 mesh; cfg5: one rank's 256x256x512 block of
+    # b=2 x 2x2 spatial (one sample per rank, W unsplit)
+    mesh3 = a.emulate_config in ("cfg4", "cfg5")
     K = 8 if mesh3 else a.emulate_split
     c = CONFIGS[a.emulate_config]
     E = c["extent"]
@@ -331,8 +333,12 @@ def emulated_halo(a, torch, vm, peaks):
     mesh = vm.create_mesh([("one", 1)], backend="threads")
     graph = vm.build(cfg, mesh, {})
     params = vm.init_params(graph, 1)
-    loc = (E // 2, E // 2, E // 2) if mesh3 else (E // K, E, E)
-    nbr6 = [0] * 6 if mesh3 else [0, 0, -1, -1, -1, -1]
+    if a.emulate_config == "cfg5":
+        loc, nbr6 = (E // 2, E // 2, E), [0, 0, 0, 0, -1, -1]
+    elif mesh3:
+        loc, nbr6 = (E // 2, E // 2, E // 2), [0] * 6
+    else:
+        loc, nbr6 = (E // K, E, E), [0, 0, -1, -1, -1, -1]
     st = UNetStep(graph, params, dtype=torch.bfloat16, global_shape=(E, E, E), local_shape=loc)
     if peer:  # vm_halo_depth_push with every neighbour = this rank (wgrad overlaps exchange + dgrad)
         st.use_peer_halo(nbr6=nbr6)
@@ -386,8 +392,9 @@ def emulated_halo(a, torch, vm, peaks):
     return {
         "share": max(0.0, (res["halo"] - res["nohalo"]) / res["halo"]),
         "method": f"emulated on 1 GPU: rank block {loc[0]}x{loc[1]}x{loc[2]} of "
-                  + ("cfg4's 2x2x2 mesh (faces, edges and corners through the 3 sequential phases)" if mesh3
-                     else f"cfg3 {K}-way depth split") + ", periodic "
+                  + ({"cfg4": "cfg4's 2x2x2 mesh", "cfg5": "cfg5's b=2 x 2x2 spatial mesh (one sample per rank, "
+                      "W unsplit)"}[a.emulate_config] + " (faces, edges and corners in one round of NCCL send/recv, "
+                      "vm_halo_slab_fwd26)" if mesh3 else f"cfg3 {K}-way depth split") + ", periodic "
                   f"halos (every neighbour = this rank) through {transport}; "
                   "A/B: (t_step - t_step_nohalo) / t_step, best of 3 alternating rounds, SGD at lr = 0 in both "
                   "arms (same work; keeps the wrong-margin arm from diverging)",
@@ -609,17 +616,18 @@ def run_ours(a):
         except Exception as e:  # pragma: no cover
             halo = {"share": None, "method": f"emulation failed: {type(e).__name__}: {e}"}
         if a.emulate_config == "cfg3" and not a.no_emulate_cfg4:
-            # the 2x2x2 mesh of cfg4 too: one 256^3 rank block, faces + edges + corners through
-            # the one-phase NCCL exchange (vm_halo_slab_fwd26)
+            # the 3-D meshes too: one rank block of cfg4 (2x2x2) and of cfg5 (b=2 x 2x2), faces +
+            # edges + corners through the one-phase NCCL exchange (vm_halo_slab_fwd26)
             import copy
 
-            b = copy.copy(a)
-            b.emulate_config = "cfg4"
-            try:
-                halo["cfg4_2x2x2"] = emulated_halo(b, torch, vm, peaks)
-            except Exception as e:  # pragma: no cover
-                halo["cfg4_2x2x2"] = {"share": None, "method": f"emulation failed: {type(e).__name__}: {e}"}
-            torch.cuda.empty_cache()
+            for name, key in (("cfg4", "cfg4_2x2x2"), ("cfg5", "cfg5_b2x2x2")):
+                b = copy.copy(a)
+                b.emulate_config = name
+                try:
+                    halo[key] = emulated_halo(b, torch, vm, peaks)
+                except Exception as e:  # pragma: no cover
+                    halo[key] = {"share": None, "method": f"emulation failed: {type(e).__name__}: {e}"}
+                torch.cuda.empty_cache()
     else:
         halo = {"share": 0.0, "method": "one GPU, no partitioning"}
 
