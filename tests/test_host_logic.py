@@ -310,3 +310,43 @@ def test_one_phase_directions_rebuild_the_global_padding_on_a_2x2x2_mesh():
                   c[2] * n[2]:c[2] * n[2] + n[2] + 2]
         assert np.array_equal(blocks[r], want)
     assert sum(v >= 0 for v in n26[0]) == 7
+
+
+@pytest.mark.parametrize("axes,layout,ndir", [
+    ([("mx", 2), ("my", 2), ("mz", 2)], {"x": "mx", "y": "my", "z": "mz"}, 7),   # cfg4
+    ([("b", 2), ("mx", 2), ("my", 2)], {"batch": "b", "x": "mx", "y": "my"}, 3),  # cfg5
+    ([("mx", 4)], {"x": "mx"}, 1),                                                # cfg3 (ends)
+])
+def test_step_nbr26_stays_inside_the_batch_coordinate(axes, layout, ndir):
+    """UNetStep._nbr26 (the one-phase halo's neighbour table) on the cfg4 / cfg5 / cfg3 meshes:
+    every neighbour is the rank at coordinate + s along the split spatial axes only (same
+    batch coordinate), the table is symmetric (rank r at direction k of q  <=>  q at 25 - k of
+    r), and a corner rank of the mesh has ``ndir`` directions."""
+    from paper_1909_03108_b200.halo import directions26
+    from paper_1909_03108_b200.sharding import Layout
+    from paper_1909_03108_b200.step import UNetStep
+
+    lay = Layout(layout)
+    with vm.create_mesh(axes, backend="threads") as mesh:
+        tables = {}
+        for r in range(mesh.worker_count):
+            ctx = mesh.context(r)
+            nbr6 = []
+            for d in ("x", "y", "z"):
+                a = lay.axis_for(d)
+                for s in (-1, 1):
+                    n = ctx.neighbor(a, s) if a else None
+                    nbr6.append(-1 if n is None else n)
+            tables[r] = UNetStep._nbr26(ctx, lay, nbr6)
+        dirs = directions26()
+        for r, t in tables.items():
+            for k, q in enumerate(t):
+                if q < 0:
+                    continue
+                assert tables[q][25 - k] == r
+                cr, cq = mesh.coords[r], mesh.coords[q]
+                if "b" in mesh.axis_index:
+                    assert cr[mesh.axis_index["b"]] == cq[mesh.axis_index["b"]]
+                moved = {mesh.axis_index[lay.axis_for(d)]: s for d, s in zip(("x", "y", "z"), dirs[k]) if s}
+                assert all(cq[i] - cr[i] == moved.get(i, 0) for i in range(len(cr)))
+        assert sum(v >= 0 for v in tables[0]) == ndir
