@@ -34,8 +34,16 @@ struct C1Params {
   int64_t plane8;   // (D+2)*P*8 elements per channel-group plane
   int Cout, Nc, tiles_per_sample, tiles;
   unsigned flags;
-  uint32_t wp_magic, hp_magic;
+  uint32_t wp_magic, hp_magic, tps_magic;
 };
+
+// x / d for the small divisors of this file (multiply-high by floor(2^32 / d) + 1, corrected)
+__device__ __forceinline__ uint32_t c1_div(uint32_t x, uint32_t d, uint32_t magic) {
+  uint32_t q = __umulhi(x, magic);
+  if (q * d > x) --q;
+  if ((q + 1) * d <= x) ++q;
+  return q;
+}
 
 constexpr int kC1Threads = 128;
 constexpr uint32_t kC1TileBytes = 128 * 16;  // one 8-tap column group of the 128-row tile
@@ -46,16 +54,23 @@ constexpr uint32_t kC1TileBytes = 128 * 16;  // one 8-tap column group of the 12
 // tile's MMA and drain, then stored (c1_store).
 __device__ __forceinline__ void c1_gather(const C1Params& p, const bf16* xb, int64_t a, bool in, bool ones,
                                           uint32_t (&v)[16]) {
+  // 9 (kd, kh) row offsets in 32-bit element units (a sample is < 2^31 elements, c1_setup);
+  // the 3 kw taps of a row are immediate offsets of one address (the per-tap index arithmetic
+  // made the forward instruction-issue bound: ncu, issue slots 67% active)
   const uint16_t* xs = reinterpret_cast<const uint16_t*>(xb);
+  const uint32_t a32 = (uint32_t)a;
+  uint32_t h[28];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = 0u;
+  for (int r = 0; r < 9; ++r) {
+    const uint16_t* rp = xs + (a32 + (uint32_t)((r / 3) * p.P + (r % 3) * p.Wp));
 #pragma unroll
-  for (int t = 0; t < 27; ++t) {
-    const int kd = t / 9, kh = (t / 3) % 3, kw = t % 3;
-    const uint32_t h = in ? (uint32_t)__ldg(xs + a + (int64_t)kd * p.P + kh * p.Wp + kw) : 0u;
-    v[t >> 1] |= h << ((t & 1) * 16);
+    for (int kw = 0; kw < 3; ++kw) h[r * 3 + kw] = in ? (uint32_t)__ldg(rp + kw) : 0u;
   }
-  if (ones && in) v[13] |= 0x3F80u << 16;  // tap 27 = bf16 1.0
+  h[27] = (ones && in) ? 0x3F80u : 0u;  // tap 27 = bf16 1.0
+#pragma unroll
+  for (int i = 0; i < 14; ++i) v[i] = __byte_perm(h[2 * i], h[2 * i + 1], 0x5410);
+  v[14] = 0u;
+  v[15] = 0u;
 }
 __device__ __forceinline__ void c1_store(const uint32_t (&v)[16], uint8_t* sA, int row) {
 #pragma unroll
@@ -113,8 +128,8 @@ __global__ void __launch_bounds__(kC1Threads) k_c1_fwd(const C1Params p) {
   uint32_t phase = 0;
   uint32_t v[16];
   auto tile_anchor = [&](int tile, int& b) -> int64_t {
-    b = tile / p.tiles_per_sample;
-    return (int64_t)(tile % p.tiles_per_sample) * 128 + row;
+    b = (int)c1_div((uint32_t)tile, (uint32_t)p.tiles_per_sample, p.tps_magic);
+    return (int64_t)(tile - b * p.tiles_per_sample) * 128 + row;
   };
   if ((int)blockIdx.x < p.tiles) {
     int b0;
@@ -203,8 +218,8 @@ __global__ void __launch_bounds__(kC1Threads) k_c1_wgrad(const C1Params p) {
   uint32_t v[16];
   int4 gv[4];  // Nc <= 32: up to 4 channel groups of gy
   auto gather = [&](int tile) {
-    const int b = tile / p.tiles_per_sample;
-    const int64_t a = (int64_t)(tile % p.tiles_per_sample) * 128 + row;
+    const int b = (int)c1_div((uint32_t)tile, (uint32_t)p.tiles_per_sample, p.tps_magic);
+    const int64_t a = (int64_t)(tile - b * p.tiles_per_sample) * 128 + row;
     const bool in = a < p.anchors;
     c1_gather(p, p.x + b * p.x_bstride, a, in, true, v);
     const bf16* gyb = p.gy + b * p.gy_bstride + (a + p.P + p.Wp + 1) * 8;
@@ -296,6 +311,7 @@ int c1_setup(C1Params& p, int B, int Cout, int D, int H, int W) {
   p.tiles = B * p.tiles_per_sample;
   p.wp_magic = fastdiv_magic((uint32_t)p.Wp);
   p.hp_magic = fastdiv_magic((uint32_t)p.Hp);
+  p.tps_magic = fastdiv_magic((uint32_t)p.tiles_per_sample);
   VM_REQUIRE((int64_t)(D + 2) * p.P < (1LL << 31), VM_E_SHAPE, "first-layer conv: sample too large");
   return VM_OK;
 }
