@@ -915,6 +915,12 @@ __global__ void __launch_bounds__(NW * 32) k_wgrad_finalize_tiles(const float* _
   r /= n8;
   const int kw = r % 3;
   const int mt = r / 3;
+  {  // a block whose 4 slots hold neither a kernel row nor the ones (bias) slot writes nothing:
+     // skip its partial reads (M = 64 / partly filled M-tiles of the thin layers)
+    const int g_lo = mt * 16 + mq * 4;
+    const bool live = g_lo < (KD ? 3 : 9) * CG || (ones_slot >= g_lo && ones_slot < g_lo + 4);
+    if (!live) return;
+  }
   const int64_t e0 = (((int64_t)(mt * 3 + kw) * N + nb * 8) * 128) + mq * 32 + lane;
   float acc[8];
 #pragma unroll
