@@ -219,6 +219,10 @@ struct FwdParams {
   int ksplit, spk;
   float* ws;
   int* counters;  // [tile units], zero between launches (the last split resets its counter)
+  // 1: the ksplit CTAs of a tile unit are one thread-block cluster (cluster rank = split): each
+  // drains its f32 partial into its own shared memory (the free stage buffers) and the fix-up
+  // reads the other splits' partials over DSMEM — no global round trip, no arrival counters
+  int cluster;
 };
 
 // MB (tiles per unit) is a template parameter so that the MMA issue loop is straight-line
@@ -292,6 +296,10 @@ __global__ void __launch_bounds__(320, 1)
         }
       }
     }
+    if (p.cluster) {  // the epilogue's two cluster barriers (partials in smem; fix-up done)
+      cluster_sync();
+      cluster_sync();
+    }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     long long t_wait_tmem = 0, t_wait_full = 0, t_start = clk();
@@ -360,6 +368,10 @@ __global__ void __launch_bounds__(320, 1)
       p.dbg[blockIdx.x * 8 + 0] = clk() - t_start;
       p.dbg[blockIdx.x * 8 + 1] = t_wait_tmem;
       p.dbg[blockIdx.x * 8 + 2] = t_wait_full;
+    }
+    if (p.cluster) {
+      cluster_sync();
+      cluster_sync();
     }
   } else {
     // ===================== epilogue (warps 2..9) =====================
@@ -471,8 +483,11 @@ __global__ void __launch_bounds__(320, 1)
         int dq;
         const int64_t orow = anchor_row(a, valid, dq);
         const uint32_t tcol = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)((ab * p.MB + i) * p.nacc * p.Nc);
-        // partial layout [ks][tu][tile][row][Nc]: a thread's channels are contiguous (float4 I/O)
-        float* wsp = split ? p.ws + ((((int64_t)ks * ntu + tu) * p.MB + i) * 128 + row) * p.Nc : nullptr;
+        // partial layout [ks][tu][tile][row][Nc]: a thread's channels are contiguous (float4 I/O);
+        // cluster splits: [tile][row][Nc] in this CTA's shared memory (the stage buffers)
+        float* wsp = !split ? nullptr
+                     : p.cluster ? reinterpret_cast<float*>(smem) + ((int64_t)i * 128 + row) * p.Nc
+                                 : p.ws + ((((int64_t)ks * ntu + tu) * p.MB + i) * 128 + row) * p.Nc;
         for (int g0 = glo; g0 < ghi; g0 += 8) {
           const int gn = min(8, ghi - g0);
           int4 mk[8];
@@ -512,9 +527,15 @@ __global__ void __launch_bounds__(320, 1)
             }
             if (split) {  // f32 partial of 8 or 16 channels of this row
               float4* dst = reinterpret_cast<float4*>(wsp + (g0 + j) * 8);
+              if (p.cluster) {
 #pragma unroll
-              for (int e = 0; e < 4; ++e)
-                if (e < 2 || j + 1 < gn) __stcg(dst + e, make_float4(r[4 * e], r[4 * e + 1], r[4 * e + 2], r[4 * e + 3]));
+                for (int e = 0; e < 4; ++e)
+                  if (e < 2 || j + 1 < gn) dst[e] = make_float4(r[4 * e], r[4 * e + 1], r[4 * e + 2], r[4 * e + 3]);
+              } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  if (e < 2 || j + 1 < gn) __stcg(dst + e, make_float4(r[4 * e], r[4 * e + 1], r[4 * e + 2], r[4 * e + 3]));
+              }
               continue;
             }
 #pragma unroll
@@ -544,6 +565,55 @@ __global__ void __launch_bounds__(320, 1)
         // (one CTA reading every split's partial ran ~49 K cycles for 8 splits of a 512-channel
         // tile: latency-bound)
         const long long tpa = clk();
+        if (p.cluster) {
+          // every split's partial is in its CTA's shared memory once the cluster barrier
+          // completes; the fix-up sums the splits of this CTA's row slice over DSMEM, in split
+          // (cluster rank) order, and a second barrier keeps every CTA's shared memory alive
+          // until the whole cluster has read it
+          cluster_sync();
+          t_pub += clk() - tpa;
+          t_arr = clk() - t_epi0;
+          const long long tfx = clk();
+          const int rps = (128 + p.ksplit - 1) / p.ksplit;
+          const int rlo = ks * rps, rhi = min(128, rlo + rps);
+          const int gvalid = min(ng_out, (p.Cout - nch * p.Nc + 7) / 8);
+          const int items = p.MB * (rhi > rlo ? rhi - rlo : 0) * gvalid;
+          const uint32_t sbase = smem_u32(smem);
+          for (int it = et; it < items; it += 256) {
+            const int g = it % gvalid, ri = it / gvalid;
+            const int i = ri / (rhi - rlo), row = rlo + ri % (rhi - rlo);
+            bool valid;
+            int dq;
+            const int64_t orow = anchor_row(a0 + i * 128 + row, valid, dq);
+            if (!valid) continue;
+            const int co0 = nch * p.Nc + g * 8;
+            int4 mkv = make_int4(0, 0, 0, 0);
+            if (domask) mkv = __ldg(reinterpret_cast<const int4*>(mbase + (co0 / 8) * p.plane8 + orow * 8));
+            const uint32_t off = sbase + (uint32_t)((((i * 128 + row) * p.Nc) + g * 8) * 4);
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = 0.f;
+            for (int k0 = 0; k0 < p.ksplit; k0 += 4) {  // 4 splits' loads in flight, then the adds
+              float4 lo[4], hi[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                if (k0 + j >= p.ksplit) break;
+                const uint32_t ra = dsmem_map(off, (uint32_t)(k0 + j));
+                lo[j] = dsmem_ld_f4(ra), hi[j] = dsmem_ld_f4(ra + 16);
+              }
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {  // split order: deterministic
+                if (k0 + j >= p.ksplit) break;
+                v[0] += lo[j].x, v[1] += lo[j].y, v[2] += lo[j].z, v[3] += lo[j].w;
+                v[4] += hi[j].x, v[5] += hi[j].y, v[6] += hi[j].z, v[7] += hi[j].w;
+              }
+            }
+            emit(ybase, co0, v, mkv, orow, dq);
+          }
+          cluster_sync();
+          t_fix += clk() - tfx;
+          continue;
+        }
         __threadfence();
         asm volatile("bar.sync 1, 256;" ::: "memory");
         if (et == 0) {
@@ -2295,6 +2365,14 @@ static int launch_sweep(const FwdParams& f, int nsm, void* stream) {
 
 extern "C" void vm_debug_set_fwd_probe(long long* buf) { g_fwd_dbg = buf; }
 
+static void (*fwd_kernel(int MB, int mode))(const FwdParams) {
+#define FWD_ROW(M) {k_conv_fwd_tc<M, 0>, k_conv_fwd_tc<M, 1>, k_conv_fwd_tc<M, 2>}
+  static void (*const ftable[8][3])(const FwdParams) = {FWD_ROW(1), FWD_ROW(2), FWD_ROW(3), FWD_ROW(4),
+                                                        FWD_ROW(5), FWD_ROW(6), FWD_ROW(7), FWD_ROW(8)};
+#undef FWD_ROW
+  return ftable[(MB < 1 ? 1 : MB > 8 ? 8 : MB) - 1][mode];
+}
+
 // Split-K workspace of the general forward kernel: [tile-unit counters (256 B aligned)]
 // [f32 partials ksplit x tile units x MB x Nc x 128].  Zeroed once by the caller.
 static size_t fwd_ws_need(int ksplit, int64_t ntu, int MB, int Nc) {
@@ -2310,6 +2388,44 @@ static size_t fwd_ws_need(int ksplit, int64_t ntu, int MB, int Nc) {
 static int g_fwd_max_split = kFwdMaxSplit;  // vm_debug_set_fwd_max_split (A/B probes, tests)
 extern "C" void vm_debug_set_fwd_max_split(int v) { g_fwd_max_split = v < 1 ? 1 : v > kFwdMaxSplit ? kFwdMaxSplit : v; }
 static int g_fwd_force_split = 0;  // vm_debug_force_fwd_split (plan sweeps): only this K split
+// Cluster split-K is opt-in (vm_debug_set_fwd_cluster(1)): alone it beats the global fix-up at
+// 2-4 splits (128->128 @16^3 split 3: 15.2 vs 16.8 us; 256->256 @4x32^2 split 4: 28.7 vs 28.9),
+// bitwise the same result, but inside the step it lost (cfg2 2.728 vs 2.70 ms): a cluster needs
+// ksplit SMs of one GPC free at once while the weight-gradient stream's CTAs hold SMs.
+static int g_fwd_cluster = 0;
+extern "C" void vm_debug_set_fwd_cluster(int on) { g_fwd_cluster = on; }
+static void (*fwd_kernel(int MB, int mode))(const FwdParams);
+// clusters of `size` fwd CTAs (one per SM: TMEM + shared memory) that can be resident at once: a
+// GPC holds whole clusters only, so 4-CTA clusters leave SMs idle and a plan with more units
+// than this would run a second wave (768->256 @4x32^2, split 4: 85 vs 48 us)
+static int fwd_max_clusters(int MB, int size, size_t smem) {
+  static int cache[9][9] = {};
+  if (size < 2 || size > 8 || MB < 1 || MB > 8) return 0;
+  int& c = cache[MB][size];
+  if (c == 0) {
+    auto kern = fwd_kernel(MB, 0);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(size * 16);
+    cfg.blockDim = dim3(320);
+    cfg.dynamicSmemBytes = kSmemBudget;  // every plan's stages fill the budget: 1 CTA per SM
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)size;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) {
+      cudaGetLastError();
+      n = -1;  // unknown: no cluster plans
+    }
+    c = n;
+  }
+  (void)smem;
+  return c;
+}
 extern "C" void vm_debug_force_fwd_split(int v) { g_fwd_force_split = v; }
 
 static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, const float* bias, void* y,
@@ -2447,6 +2563,7 @@ static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, 
   };
   double best = 1e30;
   int bMB = 1, bacc = 1, bbuf = 1, bstages = 0, bsplit = 1;
+  bool bcluster = false;
   for (int MB = 1; MB <= 8; ++MB) {
     if (g_fwd_force_mb && MB != g_fwd_force_mb) continue;
     const int R = MB * 128 + 2 * p.Wp + 2;
@@ -2460,13 +2577,19 @@ static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, 
     // partials: more CTAs for layers with few tiles (deep levels)
     for (int ksplit = 1; ksplit <= g_fwd_max_split; ++ksplit) {
       if (g_fwd_force_split && ksplit != g_fwd_force_split) continue;
-      if (ksplit > 1 && ntu * 4 > nsm && !g_fwd_force_split) break;  // enough tile units already
+      // cluster split: the ksplit CTAs of a tile unit form one cluster (<= 8, portable size),
+      // one unit per CTA, the f32 partial tile fits the CTA's stage buffers
+      // (<= 4: at 6-8 splits the global fix-up measured faster, tools/split_check.py)
+      const bool cl = g_fwd_cluster && ksplit > 1 && ksplit <= 4 && ntu * ksplit <= nsm &&
+                      (int64_t)MB * 128 * N * 4 <= (int64_t)stages * stage_bytes &&
+                      ntu <= fwd_max_clusters(MB, ksplit, (size_t)stages * stage_bytes);
+      if (ksplit > 1 && ntu * 4 > nsm && !cl && !g_fwd_force_split) break;  // enough tile units already
       // split plans with MB > 1 lost to MB = 1 at every forced-plan shape (tools/fwd_plan_sweep.py:
       // 256->256 @8^3 split 12: 28.3 vs 19.4 us; 512->512 @2x16^2: 34.7 vs 24.5 us)
       if (ksplit > 1 && MB > 1 && !g_fwd_force_split) break;
       const int spk = (3 * p.KC + ksplit - 1) / ksplit;
-      if (ksplit > 1 &&
-          ((3 * p.KC + spk - 1) / spk != ksplit || !ws || fwd_ws_need(ksplit, ntu, MB, N) > ws_bytes))
+      if (ksplit > 1 && ((3 * p.KC + spk - 1) / spk != ksplit ||
+                         (!cl && (!ws || fwd_ws_need(ksplit, ntu, MB, N) > ws_bytes))))
         continue;
       const int64_t units = ntu * ksplit;
       // the splits of a tile finish it together (they wait for each other): one wave only
@@ -2491,13 +2614,18 @@ static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, 
           // sums its 1/ksplit of the rows: 256 (row, group) items in flight, 4 splits' loads
           // per round trip (~800 cycles from L2)
           const double fix_items = MB * std::ceil(128.0 / ksplit) * (N / 8.0);
-          const double fix = ksplit > 1 ? 1500.0 + MB * (N / 8.0) * 60.0 +
-                                              std::ceil(fix_items / 256.0) * std::ceil(ksplit / 4.0) * 800.0
-                                        : 0.0;
+          // cluster: drain into shared memory, two cluster barriers, DSMEM reads.  The constant
+          // terms are fitted to forced plans (tools/split_check.py: 128->128 and 64->128 at 16^3,
+          // unsplit vs split 3 — ~11 K cycles of split overhead, cluster, ~14 K global)
+          const double fix = ksplit <= 1 ? 0.0
+                             : cl ? 8000.0 + MB * (N / 8.0) * 60.0 +
+                                        std::ceil(fix_items / 256.0) * std::ceil(ksplit / 4.0) * 600.0
+                                  : 10000.0 + MB * (N / 8.0) * 60.0 +
+                                        std::ceil(fix_items / 256.0) * std::ceil(ksplit / 4.0) * 800.0;
           const double cost = (double)waves * ((double)spk * stage + drain + fix + 2000.0);
           if (cost < best * 0.999) {
             best = cost;
-            bMB = MB, bacc = nacc, bbuf = nbuf, bstages = stages, bsplit = ksplit;
+            bMB = MB, bacc = nacc, bbuf = nbuf, bstages = stages, bsplit = ksplit, bcluster = cl;
           }
         }
       }
@@ -2516,7 +2644,8 @@ static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, 
   p.ksplit = bsplit;
   p.spk = (3 * p.KC + bsplit - 1) / bsplit;
   p.units = B * p.mblocks * p.nchunk * bsplit;
-  if (bsplit > 1) {
+  p.cluster = bcluster ? 1 : 0;
+  if (bsplit > 1 && !bcluster) {
     const int64_t ntu = (int64_t)B * p.mblocks * p.nchunk;
     p.counters = static_cast<int*>(ws);  // [ntu] arrivals, [ntu] departures
     p.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + (ntu * 8 + 255) / 256 * 256);
@@ -2527,12 +2656,27 @@ static int fwd_tc_launch(const void* x, int64_t x_bstride, const void* wpacked, 
   int grid = p.units < nsm ? p.units : nsm;
   void (*kern)(const FwdParams) = nullptr;
   const int mode = p.dbg != nullptr ? 1 : (p.hl.counter || p.hl.wait_own) ? 2 : 0;
-#define FWD_ROW(M) {k_conv_fwd_tc<M, 0>, k_conv_fwd_tc<M, 1>, k_conv_fwd_tc<M, 2>}
-  static void (*const ftable[8][3])(const FwdParams) = {FWD_ROW(1), FWD_ROW(2), FWD_ROW(3), FWD_ROW(4),
-                                                        FWD_ROW(5), FWD_ROW(6), FWD_ROW(7), FWD_ROW(8)};
-#undef FWD_ROW
-  kern = ftable[(p.MB < 1 ? 1 : p.MB > 8 ? 8 : p.MB) - 1][mode];
+  kern = fwd_kernel(p.MB, mode);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (p.cluster) {  // one unit per CTA, clusters of the ksplit CTAs of a tile unit
+    VM_REQUIRE(p.units <= nsm && p.units % p.ksplit == 0, VM_E_UNSUPPORTED, "fwd cluster split: %d units", p.units);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p.units);
+    cfg.blockDim = dim3(320);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = as_stream(stream);
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)p.ksplit;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    cudaLaunchKernelEx(&cfg, kern, p);
+    return launch_status("vm_conv3d_fwd_tc (cluster split)");
+  }
   launch_pdl(kern, grid, 320, smem, as_stream(stream), p);
   return launch_status("vm_conv3d_fwd_tc");
 }

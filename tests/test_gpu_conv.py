@@ -295,6 +295,53 @@ def test_tc_forward_split_k_workspace(shape):
     assert nz == 0
 
 
+@pytest.mark.parametrize("shape,split", [((1, 128, 128, 16, 16, 16), 3), ((1, 64, 128, 4, 8, 8), 2),
+                                         ((1, 256, 256, 4, 8, 8), 4), ((2, 64, 64, 4, 8, 8), 2)])
+def test_tc_forward_cluster_split_k_is_bitwise_the_global_fix_up(shape, split):
+    """Opt-in cluster split-K (vm_debug_set_fwd_cluster): the K splits of a tile are one
+    thread-block cluster, partials in each CTA's shared memory, the fix-up reads them over DSMEM
+    (barrier.cluster + mapa + ld.shared::cluster) — bitwise the global-workspace fix-up (same
+    split order), masked epilogue included, and the f64 oracle within the bf16 bound."""
+    B, cin, cout, D, H, W = shape
+    rng = np.random.default_rng(11 + sum(shape))
+    x = O.bf16_round(rng.standard_normal((B, D, H, W, cin)).astype(np.float32))
+    w = O.bf16_round(rng.uniform(-1, 1, (3, 3, 3, cin, cout)).astype(np.float32) / np.sqrt(27 * cin))
+    b = rng.standard_normal(cout).astype(np.float32) * 0.1
+    m = O.bf16_round(rng.standard_normal((B, D, H, W, cout)).astype(np.float32))
+    xs, ms = _slab_from(x), _slab_from(m)
+    wt = torch.from_numpy(np.ascontiguousarray(w, np.float32)).cuda()
+    wp = torch.empty(_lib.call_size("vm_packed_weights_bytes", cin, cout) // 2, dtype=torch.bfloat16, device="cuda")
+    _lib.call("vm_pack_weights", _lib.ptr(wt), _lib.ptr(wp), cin, cout, 0, _lib.stream_ptr())
+    bt = torch.from_numpy(b).cuda()
+    nbytes = _lib.call_size("vm_conv3d_fwd_tc_ws_bytes", B, cin, cout, D, H, W)
+    ws = torch.zeros(nbytes // 4 + 64, dtype=torch.float32, device="cuda")
+    flags = _lib.VM_CONV_RELU | _lib.VM_CONV_MASK
+    lib = _lib.load()
+    outs = {}
+    try:
+        lib.vm_debug_set_fwd_plan(1, 1)
+        lib.vm_debug_set_fwd_max_split(16)
+        lib.vm_debug_force_fwd_split(split)
+        for cl in (1, 0, 1):
+            lib.vm_debug_set_fwd_cluster(cl)
+            ys = Slab(B, cout, D, H, W, torch.bfloat16, "cuda")
+            _lib.call("vm_conv3d_fwd_tc_ws", xs.p(), xs.bstride, _lib.ptr(wp), _lib.ptr(bt), ys.p(), ys.bstride,
+                      ms.p(), ms.bstride, B, cin, cout, D, H, W, flags, _lib.ptr(ws), nbytes, _lib.stream_ptr())
+            torch.cuda.synchronize()
+            outs.setdefault(cl, []).append(ys.storage.cpu())
+    finally:
+        lib.vm_debug_set_fwd_cluster(0)
+        lib.vm_debug_force_fwd_split(0)
+        lib.vm_debug_set_fwd_plan(0, 0)
+    assert torch.equal(outs[1][0], outs[1][1])       # deterministic
+    assert torch.equal(outs[1][0], outs[0][0])       # cluster == global fix-up
+    ys = Slab(B, cout, D, H, W, torch.bfloat16, "cuda")
+    ys.storage.copy_(outs[1][0].cuda())
+    dense = np.maximum(O.conv3d_dense(x.astype(np.float64), w.astype(np.float64), b.astype(np.float64)), 0)
+    dense = np.where(m > 0, dense, 0)
+    assert rel_l2(ys.interior().cpu().numpy(), dense) <= 1e-2
+
+
 C1_SHAPES = [(1, 16, 16, 16, 16), (2, 32, 6, 10, 34), (1, 8, 5, 7, 9), (1, 16, 12, 32, 128), (1, 24, 3, 4, 5)]
 
 
