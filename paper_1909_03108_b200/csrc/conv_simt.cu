@@ -188,12 +188,16 @@ __global__ void __launch_bounds__(256) k_bias_grad_partial(const T* __restrict__
   const int64_t v0 = blockIdx.x * chunk, v1 = min(nvox, v0 + chunk);
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int64_t v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
-    int wv = v % gg.W;
-    int64_t r = v / gg.W;
-    int h = r % gg.H;
-    r /= gg.H;
-    int d = r % gg.D;
-    int b = (int)(r / gg.D);
+    // 32-bit multiply-high split (nvox < 2^31, checked by the launchers; the 64-bit divisions
+    // made this 1 MB reduction take ~8 us at 16^3 x 128 channels)
+    const uint32_t v32 = (uint32_t)v;
+    const uint32_t q1 = fastdiv(v32, (uint32_t)gg.W, gg.mW);
+    const int wv = (int)(v32 - q1 * (uint32_t)gg.W);
+    const uint32_t q2 = fastdiv(q1, (uint32_t)gg.H, gg.mH);
+    const int h = (int)(q1 - q2 * (uint32_t)gg.H);
+    const uint32_t q3 = fastdiv(q2, (uint32_t)gg.D, gg.mD);
+    const int d = (int)(q2 - q3 * (uint32_t)gg.D);
+    const int b = (int)q3;
     float gv[8];
     Vec8<T>::load(gy + gg.at(b, cgo, d, h, wv), gv);
 #pragma unroll
@@ -274,8 +278,9 @@ size_t bias_grad_ws_bytes(int64_t nvox, int Cout) {
 // reduces the ns splits in order.
 int bias_grad_partial_bf16(const void* gy, int64_t gy_bstride, float* ws, int B, int Cout, int D, int H, int W,
                            cudaStream_t st, int* nsplit) {
-  Slab gg{gy_bstride ? gy_bstride : default_bstride(Cout, D, H, W, 1), (Cout + 7) / 8, D, H, W, 1};
+  const Slab gg = make_slab(gy_bstride ? gy_bstride : default_bstride(Cout, D, H, W, 1), (Cout + 7) / 8, D, H, W, 1);
   int64_t nvox = (int64_t)B * D * H * W;
+  VM_REQUIRE(nvox < (1LL << 31), VM_E_SHAPE, "bias_grad_partial_bf16: %lld voxels", (long long)nvox);
   int ns = (int)(bias_grad_ws_bytes(nvox, Cout) / (gg.CG * 8 * sizeof(float)));
   int64_t chunk = (nvox + ns - 1) / ns;
   launch_pdl(k_bias_grad_partial<__nv_bfloat16>, dim3(ns, gg.CG), 256, 0, st, (const __nv_bfloat16*)gy, gg, ws, B,
@@ -287,8 +292,9 @@ int bias_grad_partial_bf16(const void* gy, int64_t gy_bstride, float* ws, int B,
 // gb[co] = sum over interior voxels of gy[.., co], deterministic (bf16 slab)
 int bias_grad_bf16(const void* gy, int64_t gy_bstride, float* gb, float* ws, int B, int Cout, int D,
                    int H, int W, cudaStream_t st) {
-  Slab gg{gy_bstride ? gy_bstride : default_bstride(Cout, D, H, W, 1), (Cout + 7) / 8, D, H, W, 1};
+  const Slab gg = make_slab(gy_bstride ? gy_bstride : default_bstride(Cout, D, H, W, 1), (Cout + 7) / 8, D, H, W, 1);
   int64_t nvox = (int64_t)B * D * H * W;
+  VM_REQUIRE(nvox < (1LL << 31), VM_E_SHAPE, "bias_grad_bf16: %lld voxels", (long long)nvox);
   int ns = (int)(bias_grad_ws_bytes(nvox, Cout) / (gg.CG * 8 * sizeof(float)));
   int64_t chunk = (nvox + ns - 1) / ns;
   k_bias_grad_partial<__nv_bfloat16><<<dim3(ns, gg.CG), 256, 0, st>>>((const __nv_bfloat16*)gy, gg, ws, B,
@@ -350,7 +356,7 @@ extern "C" int vm_conv3d_wgrad_simt(int dtype, const void* x, int64_t x_bstride,
   VM_REQUIRE(B > 0 && Cin > 0 && Cout > 0 && D > 0 && H > 0 && W > 0, VM_E_SHAPE,
              "vm_conv3d_wgrad_simt: bad shape");
   Slab gx{x_bstride ? x_bstride : default_bstride(Cin, D, H, W, 1), (Cin + 7) / 8, D, H, W, 1};
-  Slab gg{gy_bstride ? gy_bstride : default_bstride(Cout, D, H, W, 1), (Cout + 7) / 8, D, H, W, 1};
+  const Slab gg = make_slab(gy_bstride ? gy_bstride : default_bstride(Cout, D, H, W, 1), (Cout + 7) / 8, D, H, W, 1);
   int64_t nvox = (int64_t)B * D * H * W;
   int CGin = gx.CG, CGout = gg.CG;
   int ns = wgrad_splits(nvox, (int64_t)27 * CGin * CGout);
