@@ -272,16 +272,32 @@ __global__ void k_dense_to_slab(const S* __restrict__ src, T* __restrict__ slab,
   // one thread per (voxel, channel-block): writes one 8-channel vector
   int64_t nvox = (int64_t)B * g.D * g.H * g.W;
   int64_t total = nvox * g.CG;
+  const bool fast = total < (1LL << 31) && g.mW;  // 32-bit multiply-high split (the usual case)
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t v = i % nvox;
-    int cg = (int)(i / nvox);
-    int w = v % g.W;
-    int64_t r = v / g.W;
-    int h = r % g.H;
-    r /= g.H;
-    int d = r % g.D;
-    int b = (int)(r / g.D);
+    int64_t v;
+    int cg, w, h, d, b;
+    if (fast) {
+      cg = (int)(i / nvox);  // nvox-sized runs: one 64-bit division per thread-iteration is fine here
+      v = i - (int64_t)cg * nvox;
+      const uint32_t v32 = (uint32_t)v;
+      const uint32_t q1 = fastdiv(v32, (uint32_t)g.W, g.mW);
+      w = (int)(v32 - q1 * (uint32_t)g.W);
+      const uint32_t q2 = fastdiv(q1, (uint32_t)g.H, g.mH);
+      h = (int)(q1 - q2 * (uint32_t)g.H);
+      const uint32_t q3 = fastdiv(q2, (uint32_t)g.D, g.mD);
+      d = (int)(q2 - q3 * (uint32_t)g.D);
+      b = (int)q3;
+    } else {
+      v = i % nvox;
+      cg = (int)(i / nvox);
+      w = v % g.W;
+      int64_t r = v / g.W;
+      h = r % g.H;
+      r /= g.H;
+      d = r % g.D;
+      b = (int)(r / g.D);
+    }
     T out[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -322,7 +338,7 @@ extern "C" int vm_dense_to_slab(const void* src, int src_dtype, void* slab, int 
   VM_REQUIRE(B > 0 && C > 0 && D > 0 && H > 0 && W > 0 && m >= 0, VM_E_SHAPE,
              "vm_dense_to_slab: bad shape");
   VM_REQUIRE(src_dtype == VM_F32, VM_E_DTYPE, "vm_dense_to_slab: source must be f32");
-  Slab g{bstride ? bstride : default_bstride(C, D, H, W, m), (C + 7) / 8, D, H, W, m};
+  const Slab g = make_slab(bstride ? bstride : default_bstride(C, D, H, W, m), (C + 7) / 8, D, H, W, m);
   cudaStream_t st = as_stream(stream);
   int64_t work = (int64_t)B * D * H * W * g.CG;
   int grid = grid_for(work, 256);
